@@ -1,0 +1,197 @@
+/*
+ * fm_gpu.h — C ABI of the B200-native floodmra hot path (libfm_gpu.so).
+ *
+ * This is the drop-in boundary.  Each entry point replaces one seam of the
+ * reference C++ library (`/root/reference/proj/core`, namespace floodmra);
+ * the interface it stands in for is cited beside it.  Plain pointers and
+ * sizes only: no C++ types, no torch types, no exceptions cross this line.
+ * Every call returns an `int` status (FM_OK = 0); on failure
+ * `fm_last_error()` returns a thread-local message and the status maps onto
+ * the reference exception types (errors.hpp:9-37) and CLI exit codes
+ * (tools/floodmra.cpp:171-186):
+ *
+ *   FM_ERR_CONFIG    ConfigError      (exit 2)
+ *   FM_ERR_IO        IoError/ParseError (exit 3)
+ *   FM_ERR_BLOWUP    BlowUpError      (exit 4; fm_run_result.blow_up_time = t)
+ *   FM_ERR_STRUCTURE StructureError   (exit 1)
+ *   FM_ERR_DOMAIN    DomainError      (exit 1)
+ *   FM_ERR_CUDA      CUDA runtime / no device (exit 1) — there is no CPU fallback
+ *
+ * Units, layouts and orders follow the reference:
+ *   - rasters are ESRI-style, row 0 = north (raster.hpp:8-26);
+ *   - a DEM of n x m cells is an (n+1) x (m+1) VERTEX raster (field.hpp:93-98);
+ *   - leaf arrays returned "in reference order" are sorted by (level, j, i)
+ *     exactly as make_quadgrid sorts them (quadgrid.cpp:94-98);
+ *   - flow coefficients per cell are 9 doubles
+ *       [h.c0 h.c1x h.c1y qx.c0 qx.c1x qx.c1y qy.c0 qy.c1x qy.c1y]
+ *     (FlowCoeffs, field.hpp:49-67) and topography 3 doubles [c0 c1x c1y].
+ */
+#ifndef FM_GPU_H
+#define FM_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+enum {
+  FM_OK = 0,
+  FM_ERR_OTHER = 1,
+  FM_ERR_CONFIG = 2,
+  FM_ERR_IO = 3,
+  FM_ERR_BLOWUP = 4,
+  FM_ERR_STRUCTURE = 5,
+  FM_ERR_DOMAIN = 6,
+  FM_ERR_CUDA = 7
+};
+
+/* SolverKind (config.hpp:9) */
+enum { FM_DG2 = 0, FM_FV1 = 1, FM_ACC = 2, FM_MWDG2 = 3, FM_HWFV1 = 4 };
+/* WaveletKind (wavelets.hpp:9) */
+enum { FM_MW = 0, FM_HW = 1 };
+/* BoundaryKind (config.hpp:11) */
+enum { FM_REFLECTIVE = 0, FM_OPEN = 1 };
+/* Side (config.hpp:12) */
+enum { FM_NORTH = 0, FM_EAST = 1, FM_SOUTH = 2, FM_WEST = 3 };
+/* leaf orders for fm_grid_leaves / fm_sim_download */
+enum { FM_ORDER_REFERENCE = 0, FM_ORDER_DEVICE = 1 };
+
+/* Raster (raster.hpp:10-26).  `values` is ncols*nrows doubles, row 0 north.
+ * `on_device` != 0 means `values` is a CUDA device pointer already resident
+ * in HBM (used by the bench's kernel-only leg); 0 means host memory. */
+typedef struct fm_raster {
+  const double* values;
+  int32_t ncols, nrows;
+  double xll, yll, cellsize, nodata;
+  int32_t on_device;
+} fm_raster;
+
+/* InflowSpec + Hydrograph (config.hpp:15-18, hydrograph.hpp:10-16): an
+ * inclusive fine-cell rectangle receiving a t,Q hydrograph as a depth source. */
+typedef struct fm_inflow {
+  const double* t;
+  const double* q;
+  int32_t nsamples;
+  int32_t i0, j0, i1, j1;
+} fm_inflow;
+
+/* The subset of ScenarioConfig (config.hpp:29-69) the solvers read. */
+typedef struct fm_sim_desc {
+  int32_t solver;          /* FM_DG2 .. FM_HWFV1 */
+  double g, h_dry;         /* 9.80665, 1e-6 */
+  double courant;          /* <= 0: per-solver default (config.cpp:37-47) */
+  int32_t bc[4];           /* N, E, S, W : FM_REFLECTIVE / FM_OPEN */
+  double manning;          /* uniform Manning n */
+  const fm_raster* manning_raster;      /* optional, CELL-centred n x m */
+  const fm_raster* initial_depth_raster; /* optional, same geometry as DEM */
+  int32_t has_initial_surface;
+  double initial_surface;
+  double initial_depth;
+  const fm_inflow* inflows;
+  int32_t n_inflows;
+  double epsilon;          /* adaptive solvers */
+  int32_t max_level;       /* adaptive solvers */
+  int32_t adapt_every;     /* adaptive solvers, >= 1 */
+} fm_sim_desc;
+
+/* EventClock (sim_common.hpp:31-45) state. */
+typedef struct fm_clock {
+  double end_time, output_interval, gauge_interval, now;
+  int64_t next_output, next_gauge;
+} fm_clock;
+
+/* What one call of the device-resident drive loop did (run.cpp:80-111). */
+typedef struct fm_run_result {
+  int64_t steps;
+  double dt_min, dt_max;
+  double volume_inflow;
+  int32_t blew_up;
+  double blow_up_time;
+  double bad_x, bad_y;
+  int32_t finished;       /* clock.now >= end_time */
+  int32_t event_due;      /* stopped because a gauge/output event was reached */
+} fm_run_result;
+
+typedef struct fm_grid fm_grid;
+typedef struct fm_sim fm_sim;
+
+/* ---- runtime ------------------------------------------------------------ */
+const char* fm_last_error(void);
+/* Select the CUDA device for this thread's subsequent calls (one rank per GPU). */
+int fm_init(int32_t device);
+/* Route all library work onto `stream` (a cudaStream_t; NULL = library stream). */
+int fm_set_stream(void* stream);
+int fm_synchronize(void);
+/* Number of kernels this library has launched since load (evidence counter). */
+int64_t fm_launch_count(void);
+
+/* ---- static MRA --------------------------------------------------------- */
+/* generate_static_grid(dem, eps, L, graded, kind)  — detail_tree.hpp:55-56,
+ * detail_tree.cpp:172-178.  Pipeline: project_raster (field.cpp:106-117) ->
+ * build_detail_tree (detail_tree.cpp:10-54) -> flag_significant
+ * (:66-74) -> grade_flags (:97-113) -> assemble_grid (:132-164). */
+int fm_mra_static(const fm_raster* dem, int32_t L, double eps, int32_t graded, int32_t kind,
+                  fm_grid** out);
+int fm_grid_destroy(fm_grid* g);
+int64_t fm_grid_num_leaves(const fm_grid* g);
+/* QuadGrid scalars (quadgrid.hpp:54-60) plus DetailTree::field_norm. */
+int fm_grid_info(const fm_grid* g, int32_t* L, int32_t* M, int32_t* N, double* Rfine, double* x0,
+                 double* y0, double* field_norm);
+/* Leaves + topography (NonUniformGrid, quadgrid.hpp:117-120).  Any output
+ * pointer may be NULL.  topo3 is 3 doubles per leaf. */
+int fm_grid_leaves(const fm_grid* g, int32_t order, int32_t* level, int32_t* i, int32_t* j,
+                   double* topo3);
+/* DetailTree::flags[level] (detail_tree.hpp:23), row-major j*(M<<level)+i. */
+int fm_grid_flags(const fm_grid* g, int32_t level, uint8_t* out);
+/* Per-node normalised details d_hat of DetailTree level `level`, row-major. */
+int fm_grid_dhat(const fm_grid* g, int32_t level, double* out);
+/* Count of nodes with |d_hat - eps| <= rel*eps. */
+int fm_grid_near_threshold(const fm_grid* g, double rel, int64_t* count);
+/* Device time of the last MRA pipeline's kernels (ms) and algorithmic bytes. */
+int fm_grid_timing(const fm_grid* g, double* ms, double* bytes);
+
+/* ---- simulations (drive<Sim> duck type, run.cpp:35-141) ----------------- */
+/* run_scenario's dispatch (run.cpp:145-164): adaptive solvers build an
+ * AdaptiveSim from the DEM (solver_adaptive.cpp:209-236); otherwise a
+ * non-NULL grid gives make_nonuniform_sim (solver_nonuniform.cpp:558-636) and
+ * a NULL grid gives make_uniform_sim (solver_uniform.cpp:522-601). */
+int fm_sim_create(const fm_sim_desc* desc, const fm_raster* dem, const fm_grid* grid,
+                  fm_sim** out);
+int fm_sim_destroy(fm_sim* s);
+int64_t fm_sim_num_cells(const fm_sim* s);
+int64_t fm_sim_num_segments(const fm_sim* s);
+/* Sim::compute_dt (solver_nonuniform.cpp:427-449, solver_uniform.cpp:424-442). */
+int fm_sim_compute_dt(fm_sim* s, double* dt);
+/* Sim::step (solver_nonuniform.cpp:420-425, solver_uniform.cpp:417-422). */
+int fm_sim_step(fm_sim* s, double dt);
+/* Sim::apply_inflows (solver_nonuniform.cpp:451-465). */
+int fm_sim_apply_inflows(fm_sim* s, double t, double dt, double* added);
+/* AdaptiveSim::adapt (solver_adaptive.cpp:136-171); FM_ERR_CONFIG for static sims. */
+int fm_sim_adapt(fm_sim* s, double t);
+/* Sim::volume (solver_nonuniform.cpp:467-477). */
+int fm_sim_volume(fm_sim* s, double* v);
+/* Sim::finite_state (solver_nonuniform.cpp:479-487). */
+int fm_sim_finite(fm_sim* s, int32_t* ok, double* bad_x, double* bad_y);
+/* State in reference order ((level,j,i) for leaves, j*nx+i for rasters).
+ * Any pointer may be NULL.  u9: 9 doubles per cell, z3: 3 per cell. */
+int fm_sim_download(fm_sim* s, int32_t* level, int32_t* i, int32_t* j, double* u9, double* z3);
+/* Overwrite the flow state (reference order) — lockstep re-seeding. */
+int fm_sim_upload(fm_sim* s, const double* u9);
+/* AdaptiveSim::element_log (solver_adaptive.hpp:23): number of entries, and copy. */
+int64_t fm_sim_element_log(fm_sim* s, double* t, int64_t* count, int64_t cap);
+/* The drive<Sim> loop body (run.cpp:80-111) resident on the device:
+ * dt = clip(compute_dt) ; step ; apply_inflows ; advance ; adapt ; finite.
+ * Runs until `max_steps`, the end time, a blow-up, or (stop_at_events != 0)
+ * a gauge/output event time is reached.  `clk` is updated in place. */
+int fm_sim_run(fm_sim* s, fm_clock* clk, int64_t max_steps, int32_t stop_at_events,
+               fm_run_result* out);
+/* Device time (ms) of the last fm_sim_run's kernels, measured with CUDA events. */
+int fm_sim_last_run_ms(fm_sim* s, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FM_GPU_H */

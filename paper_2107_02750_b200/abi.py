@@ -1,0 +1,381 @@
+"""ctypes description of the C ABI declared in include/fm_gpu.h.
+
+`Backend(path, prefix)` binds one shared library exposing that ABI.  The
+product binds libfm_gpu.so with prefix "fm_" (see api.py).  The same table
+lets the parity tests bind the CPU checkers that mirror the ABI (prefix
+"orc_" / "ref_"); those live under oracle/ and are loaded only by tests/,
+__graft_entry__.smoke() and bench.py's CPU legs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+FM_OK = 0
+ERRORS = {1: "other", 2: "config", 3: "io", 4: "blowup", 5: "structure", 6: "domain", 7: "cuda"}
+
+
+class FmError(RuntimeError):
+    """A non-zero status from the C ABI (maps to the reference exception types)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{ERRORS.get(code, code)}] {msg}")
+        self.code = code
+
+
+class BlowUpError(FmError):
+    def __init__(self, code: int, msg: str, t: float):
+        super().__init__(code, msg)
+        self.t = t
+
+
+class c_raster(C.Structure):
+    _fields_ = [("values", C.POINTER(C.c_double)), ("ncols", C.c_int32), ("nrows", C.c_int32),
+                ("xll", C.c_double), ("yll", C.c_double), ("cellsize", C.c_double),
+                ("nodata", C.c_double), ("on_device", C.c_int32)]
+
+
+class c_inflow(C.Structure):
+    _fields_ = [("t", C.POINTER(C.c_double)), ("q", C.POINTER(C.c_double)),
+                ("nsamples", C.c_int32), ("i0", C.c_int32), ("j0", C.c_int32),
+                ("i1", C.c_int32), ("j1", C.c_int32)]
+
+
+class c_desc(C.Structure):
+    _fields_ = [("solver", C.c_int32), ("g", C.c_double), ("h_dry", C.c_double),
+                ("courant", C.c_double), ("bc", C.c_int32 * 4), ("manning", C.c_double),
+                ("manning_raster", C.POINTER(c_raster)),
+                ("initial_depth_raster", C.POINTER(c_raster)),
+                ("has_initial_surface", C.c_int32), ("initial_surface", C.c_double),
+                ("initial_depth", C.c_double), ("inflows", C.POINTER(c_inflow)),
+                ("n_inflows", C.c_int32), ("epsilon", C.c_double), ("max_level", C.c_int32),
+                ("adapt_every", C.c_int32)]
+
+
+class c_clock(C.Structure):
+    _fields_ = [("end_time", C.c_double), ("output_interval", C.c_double),
+                ("gauge_interval", C.c_double), ("now", C.c_double),
+                ("next_output", C.c_int64), ("next_gauge", C.c_int64)]
+
+
+class c_result(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("dt_min", C.c_double), ("dt_max", C.c_double),
+                ("volume_inflow", C.c_double), ("blew_up", C.c_int32),
+                ("blow_up_time", C.c_double), ("bad_x", C.c_double), ("bad_y", C.c_double),
+                ("finished", C.c_int32), ("event_due", C.c_int32)]
+
+
+P = C.c_void_p
+PP = C.POINTER(C.c_void_p)
+I32 = C.c_int32
+I64 = C.c_int64
+D = C.c_double
+PD = C.POINTER(C.c_double)
+PI32 = C.POINTER(C.c_int32)
+PI64 = C.POINTER(C.c_int64)
+PU8 = C.POINTER(C.c_uint8)
+
+# name -> (restype, argtypes); the common ABI of fm_/orc_/ref_ libraries
+SIGS = {
+    "last_error": (C.c_char_p, []),
+    "mra_static": (C.c_int, [C.POINTER(c_raster), I32, D, I32, I32, PP]),
+    "grid_destroy": (C.c_int, [P]),
+    "grid_num_leaves": (I64, [P]),
+    "grid_info": (C.c_int, [P, PI32, PI32, PI32, PD, PD, PD, PD]),
+    "grid_leaves": (C.c_int, [P, I32, PI32, PI32, PI32, PD]),
+    "grid_flags": (C.c_int, [P, I32, PU8]),
+    "grid_dhat": (C.c_int, [P, I32, PD]),
+    "grid_near_threshold": (C.c_int, [P, D, PI64]),
+    "sim_create": (C.c_int, [C.POINTER(c_desc), C.POINTER(c_raster), P, PP]),
+    "sim_destroy": (C.c_int, [P]),
+    "sim_num_cells": (I64, [P]),
+    "sim_num_segments": (I64, [P]),
+    "sim_compute_dt": (C.c_int, [P, PD]),
+    "sim_step": (C.c_int, [P, D]),
+    "sim_apply_inflows": (C.c_int, [P, D, D, PD]),
+    "sim_adapt": (C.c_int, [P, D]),
+    "sim_volume": (C.c_int, [P, PD]),
+    "sim_finite": (C.c_int, [P, PI32, PD, PD]),
+    "sim_download": (C.c_int, [P, PI32, PI32, PI32, PD, PD]),
+    "sim_upload": (C.c_int, [P, PD]),
+    "sim_element_log": (I64, [P, PD, PI64, I64]),
+    "sim_run": (C.c_int, [P, C.POINTER(c_clock), I64, I32, C.POINTER(c_result)]),
+}
+OPTIONAL = {
+    "init": (C.c_int, [I32]),
+    "set_stream": (C.c_int, [P]),
+    "synchronize": (C.c_int, []),
+    "launch_count": (I64, []),
+    "grid_timing": (C.c_int, [P, PD, PD]),
+    "sim_last_run_ms": (C.c_int, [P, PD]),
+    "grid_details": (C.c_int, [P, I32, PD]),
+    "sim_acc_q": (C.c_int, [P, PD, PD]),
+    "set_threads": (None, [I32]),
+    "hw_threads": (I32, []),
+    "generate_static_grid": (C.c_int, [C.POINTER(c_raster), I32, D, I32, I32, PI64]),
+    "hll": (None, [D, D, D, D, D, D, D, D, PD]),
+    "friction": (None, [D, PD, PD, D, D, D, D]),
+    "encode": (None, [PD, I32, PD, PD]),
+    "decode": (None, [PD, PD, I32, PD]),
+    "bank": (None, [I32, PD]),
+}
+
+
+def dptr(a: np.ndarray):
+    return a.ctypes.data_as(PD)
+
+
+class Backend:
+    """One loaded library implementing the ABI under `prefix`."""
+
+    def __init__(self, path: str, prefix: str, mode: int = C.RTLD_LOCAL):
+        self.path = path
+        self.prefix = prefix
+        self.lib = C.CDLL(path, mode=mode)
+        self.fn = {}
+        for name, (res, args) in SIGS.items():
+            f = getattr(self.lib, prefix + name)
+            f.restype, f.argtypes = res, args
+            self.fn[name] = f
+        for name, (res, args) in OPTIONAL.items():
+            f = getattr(self.lib, prefix + name, None)
+            if f is not None:
+                f.restype, f.argtypes = res, args
+                self.fn[name] = f
+
+    def has(self, name: str) -> bool:
+        return name in self.fn
+
+    def check(self, status: int, result: c_result | None = None):
+        if status != FM_OK:
+            msg = self.fn["last_error"]().decode(errors="replace")
+            if status == 4 and result is not None:
+                raise BlowUpError(status, msg, result.blow_up_time)
+            raise FmError(status, msg)
+
+    def call(self, name, *args):
+        st = self.fn[name](*args)
+        self.check(st)
+        return st
+
+    # ---- helpers -------------------------------------------------------
+    def grid(self, dem, L: int, eps: float, graded: bool = True, kind: int = 0):
+        return Grid(self, dem, L, eps, graded, kind)
+
+    def sim(self, scenario, grid=None):
+        return Sim(self, scenario, grid)
+
+
+def make_raster(r, keep: list) -> c_raster:
+    vals = np.ascontiguousarray(r.values, dtype=np.float64)
+    keep.append(vals)
+    return c_raster(dptr(vals), r.ncols, r.nrows, r.xll, r.yll, r.cellsize, r.nodata, 0)
+
+
+class Grid:
+    """A static MRA grid (NonUniformGrid + the DetailTree flags)."""
+
+    def __init__(self, be: Backend, dem, L: int, eps: float, graded: bool, kind: int):
+        self.be = be
+        keep: list = []
+        self._r = make_raster(dem, keep)
+        self._keep = keep
+        h = P()
+        be.call("mra_static", C.byref(self._r), L, eps, 1 if graded else 0, kind, C.byref(h))
+        self.h = h
+        self.eps = eps
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.be.fn["grid_destroy"](self.h)
+            self.h = None
+
+    @property
+    def num_leaves(self) -> int:
+        return int(self.be.fn["grid_num_leaves"](self.h))
+
+    def info(self) -> dict:
+        L, M, N = I32(), I32(), I32()
+        R, x0, y0, nm = D(), D(), D(), D()
+        self.be.call("grid_info", self.h, C.byref(L), C.byref(M), C.byref(N), C.byref(R),
+                     C.byref(x0), C.byref(y0), C.byref(nm))
+        return dict(L=L.value, M=M.value, N=N.value, R=R.value, x0=x0.value, y0=y0.value,
+                    field_norm=nm.value)
+
+    def leaves(self, order: int = 0):
+        n = self.num_leaves
+        lv = np.zeros(n, np.int32)
+        i = np.zeros(n, np.int32)
+        j = np.zeros(n, np.int32)
+        z = np.zeros((n, 3), np.float64)
+        self.be.call("grid_leaves", self.h, order, lv.ctypes.data_as(PI32), i.ctypes.data_as(PI32),
+                     j.ctypes.data_as(PI32), dptr(z))
+        return lv, i, j, z
+
+    def flags(self, level: int) -> np.ndarray:
+        inf = self.info()
+        out = np.zeros((inf["N"] << level) * (inf["M"] << level), np.uint8)
+        self.be.call("grid_flags", self.h, level, out.ctypes.data_as(PU8))
+        return out
+
+    def dhat(self, level: int) -> np.ndarray:
+        inf = self.info()
+        out = np.zeros((inf["N"] << level) * (inf["M"] << level), np.float64)
+        self.be.call("grid_dhat", self.h, level, dptr(out))
+        return out
+
+    def near_threshold(self, rel: float = 1e-12) -> int:
+        c = I64()
+        self.be.call("grid_near_threshold", self.h, rel, C.byref(c))
+        return int(c.value)
+
+    def timing(self):
+        ms, b = D(), D()
+        self.be.call("grid_timing", self.h, C.byref(ms), C.byref(b))
+        return ms.value, b.value
+
+
+class Sim:
+    """A drive<Sim>-shaped simulation (run.cpp:35-141) behind the ABI."""
+
+    def __init__(self, be: Backend, sc, grid: Grid | None = None):
+        from .scenarios import SOLVERS
+
+        self.be = be
+        keep: list = []
+        d = c_desc()
+        d.solver = SOLVERS[sc.solver]
+        d.g = sc.g
+        d.h_dry = sc.h_dry
+        d.courant = sc.courant
+        for k in range(4):
+            d.bc[k] = int(sc.bc[k])
+        d.manning = sc.manning
+        if sc.manning_raster is not None:
+            mr = make_raster(sc.manning_raster, keep)
+            keep.append(mr)
+            d.manning_raster = C.pointer(mr)
+        if sc.initial_depth_raster is not None:
+            hr = make_raster(sc.initial_depth_raster, keep)
+            keep.append(hr)
+            d.initial_depth_raster = C.pointer(hr)
+        if sc.initial_surface is not None:
+            d.has_initial_surface = 1
+            d.initial_surface = sc.initial_surface
+        d.initial_depth = sc.initial_depth
+        if sc.inflows:
+            arr = (c_inflow * len(sc.inflows))()
+            for k, f in enumerate(sc.inflows):
+                t = np.ascontiguousarray(f.t, np.float64)
+                q = np.ascontiguousarray(f.q, np.float64)
+                keep += [t, q]
+                arr[k] = c_inflow(dptr(t), dptr(q), len(t), f.i0, f.j0, f.i1, f.j1)
+            keep.append(arr)
+            d.inflows = C.cast(arr, C.POINTER(c_inflow))
+            d.n_inflows = len(sc.inflows)
+        d.epsilon = sc.eps
+        d.max_level = sc.L
+        d.adapt_every = sc.adapt_every
+        dem = make_raster(sc.dem, keep)
+        h = P()
+        be.call("sim_create", C.byref(d), C.byref(dem), grid.h if grid is not None else None,
+                C.byref(h))
+        self.h = h
+        self.grid = grid
+        self.scenario = sc
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.be.fn["sim_destroy"](self.h)
+            self.h = None
+
+    @property
+    def num_cells(self) -> int:
+        return int(self.be.fn["sim_num_cells"](self.h))
+
+    @property
+    def num_segments(self) -> int:
+        return int(self.be.fn["sim_num_segments"](self.h))
+
+    def compute_dt(self) -> float:
+        v = D()
+        self.be.call("sim_compute_dt", self.h, C.byref(v))
+        return v.value
+
+    def step(self, dt: float):
+        self.be.call("sim_step", self.h, dt)
+
+    def apply_inflows(self, t: float, dt: float) -> float:
+        v = D()
+        self.be.call("sim_apply_inflows", self.h, t, dt, C.byref(v))
+        return v.value
+
+    def adapt(self, t: float):
+        self.be.call("sim_adapt", self.h, t)
+
+    def volume(self) -> float:
+        v = D()
+        self.be.call("sim_volume", self.h, C.byref(v))
+        return v.value
+
+    def finite_state(self):
+        ok, bx, by = I32(), D(), D()
+        self.be.call("sim_finite", self.h, C.byref(ok), C.byref(bx), C.byref(by))
+        return bool(ok.value), bx.value, by.value
+
+    def download(self):
+        n = self.num_cells
+        lv = np.zeros(n, np.int32)
+        i = np.zeros(n, np.int32)
+        j = np.zeros(n, np.int32)
+        u = np.zeros((n, 9), np.float64)
+        z = np.zeros((n, 3), np.float64)
+        self.be.call("sim_download", self.h, lv.ctypes.data_as(PI32), i.ctypes.data_as(PI32),
+                     j.ctypes.data_as(PI32), dptr(u), dptr(z))
+        return lv, i, j, u, z
+
+    def upload(self, u9: np.ndarray):
+        u9 = np.ascontiguousarray(u9, np.float64)
+        self.be.call("sim_upload", self.h, dptr(u9))
+
+    def element_log(self):
+        n = int(self.be.fn["sim_element_log"](self.h, None, None, 0))
+        t = np.zeros(n, np.float64)
+        c = np.zeros(n, np.int64)
+        self.be.fn["sim_element_log"](self.h, dptr(t), c.ctypes.data_as(PI64), n)
+        return t, c
+
+    def run(self, steps: int, clock: c_clock | None = None, end_time: float = 1e12,
+            gauge_interval: float = 0.0, output_interval: float = 0.0,
+            stop_at_events: bool = False):
+        """drive<Sim> loop body for `steps` steps (run.cpp:80-111)."""
+        if clock is None:
+            clock = c_clock(end_time, output_interval, gauge_interval, 0.0, 1, 1)
+        res = c_result()
+        st = self.be.fn["sim_run"](self.h, C.byref(clock), steps, 1 if stop_at_events else 0,
+                                   C.byref(res))
+        self.be.check(st, res)
+        return clock, res
+
+    def last_run_ms(self) -> float:
+        v = D()
+        self.be.call("sim_last_run_ms", self.h, C.byref(v))
+        return v.value
+
+
+def default_clock(sc) -> c_clock:
+    """The clock the parity harness and bench use: a 10 s gauge cadence so a
+    dry domain advances by 10 s steps (SURVEY §8 d2 "Dry start"), no end in reach."""
+    return c_clock(1e12, 0.0, 10.0, 0.0, 1, 1)
+
+
+def isclose_flow(a: np.ndarray, b: np.ndarray, rel: float = 1e-9, abs_: float = 1e-10):
+    """The north_star flow tolerance: |d| <= rel*|ref| or |d| <= abs (m, m^2/s)."""
+    d = np.abs(a - b)
+    return (d <= rel * np.abs(b)) | (d <= abs_)
+
+
+__all__ = ["Backend", "Grid", "Sim", "FmError", "BlowUpError", "c_clock", "c_result",
+           "default_clock", "isclose_flow", "math"]
