@@ -1,0 +1,266 @@
+// The C ABI of include/fm_gpu.h.  Every entry point converts C++ exceptions
+// into status codes + a thread-local message; no exception crosses the ABI.
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "fm_device.cuh"
+#include "fm_sim.hpp"
+
+using namespace fmh;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return FM_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("host allocation failed: ") + e.what();
+    return FM_ERR_OTHER;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FM_ERR_OTHER;
+  }
+}
+
+// No CPU fallback: a call without a usable CUDA device fails loudly.
+void require_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    throw Error(FM_ERR_CUDA, "libfm_gpu requires a CUDA device (sm_100a); none is available");
+}
+
+__global__ void k_dhat_level(const double* __restrict__ det, const uint64_t nodes, double norm,
+                             int M, int level, double* out) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= nodes) return;
+  double d[9];
+  for (int q = 0; q < 9; ++q) d[q] = det[9 * n + q];
+  int i, j;
+  fmd::node_ij(level, n, M, i, j);
+  out[size_t(j) * (M << level) + i] = fmd::dhat(d, norm);
+}
+
+__global__ void k_flags_level(const uint8_t* __restrict__ f, const uint64_t nodes, int M, int level,
+                              uint8_t* out) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= nodes) return;
+  int i, j;
+  fmd::node_ij(level, n, M, i, j);
+  out[size_t(j) * (M << level) + i] = f[n];
+}
+
+__global__ void k_near(const double* __restrict__ det, uint64_t nodes, double norm, double eps,
+                       double rel, unsigned long long* count) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= nodes) return;
+  double d[9];
+  for (int q = 0; q < 9; ++q) d[q] = det[9 * n + q];
+  if (fabs(fmd::dhat(d, norm) - eps) <= rel * eps) atomicAdd(count, 1ull);
+}
+
+inline unsigned nblk(uint64_t n) { return unsigned((n + 255) / 256); }
+}  // namespace
+
+struct fm_grid {
+  std::unique_ptr<Grid> g;
+};
+struct fm_sim {
+  std::unique_ptr<Sim> s;
+};
+
+extern "C" {
+
+const char* fm_last_error(void) { return g_err.c_str(); }
+
+int fm_init(int32_t device) {
+  return guard([&] {
+    require_device();
+    FM_CUDA(cudaSetDevice(device));
+    upload_banks();
+  });
+}
+
+int fm_set_stream(void* s) {
+  return guard([&] { set_stream(static_cast<cudaStream_t>(s)); });
+}
+
+int fm_synchronize(void) {
+  return guard([&] { FM_CUDA(cudaStreamSynchronize(stream())); });
+}
+
+int64_t fm_launch_count(void) { return launches(); }
+
+int fm_mra_static(const fm_raster* dem, int32_t L, double eps, int32_t graded, int32_t kind,
+                  fm_grid** out) {
+  return guard([&] {
+    require_device();
+    auto h = std::make_unique<fm_grid>();
+    h->g.reset(mra_static(dem, L, eps, graded != 0, kind));
+    *out = h.release();
+  });
+}
+
+int fm_grid_destroy(fm_grid* g) {
+  return guard([&] { delete g; });
+}
+
+int64_t fm_grid_num_leaves(const fm_grid* g) { return g ? g->g->nleaves : -1; }
+
+int fm_grid_info(const fm_grid* h, int32_t* L, int32_t* M, int32_t* N, double* R, double* x0,
+                 double* y0, double* norm) {
+  return guard([&] {
+    const Grid& g = *h->g;
+    if (L) *L = g.L;
+    if (M) *M = g.M;
+    if (N) *N = g.N;
+    if (R) *R = g.R;
+    if (x0) *x0 = g.x0;
+    if (y0) *y0 = g.y0;
+    if (norm) *norm = g.field_norm;
+  });
+}
+
+int fm_grid_leaves(const fm_grid* h, int32_t order, int32_t* lo, int32_t* io, int32_t* jo,
+                   double* topo3) {
+  return guard([&] {
+    const Grid& g = *h->g;
+    std::vector<int8_t> l;
+    std::vector<int32_t> i, j;
+    std::vector<int64_t> perm;
+    if (order == FM_ORDER_REFERENCE) {
+      perm = reference_order(g, &l, &i, &j);
+    } else {
+      l = g.lf_l.to_host();
+      i = g.lf_i.to_host();
+      j = g.lf_j.to_host();
+      perm.resize(g.nleaves);
+      for (int64_t k = 0; k < g.nleaves; ++k) perm[k] = k;
+    }
+    std::vector<double> z = topo3 ? g.lf_z.to_host() : std::vector<double>();
+    for (int64_t r = 0; r < g.nleaves; ++r) {
+      const int64_t k = perm[r];
+      if (lo) lo[r] = l[k];
+      if (io) io[r] = i[k];
+      if (jo) jo[r] = j[k];
+      if (topo3) std::memcpy(topo3 + 3 * r, &z[3 * k], 24);
+    }
+  });
+}
+
+int fm_grid_flags(const fm_grid* h, int32_t level, uint8_t* out) {
+  return guard([&] {
+    const Grid& g = *h->g;
+    if (level < 0 || level >= g.L) throw Error(FM_ERR_DOMAIN, "level out of range");
+    const uint64_t nodes = g.nodes(level);
+    DBuf<uint8_t> tmp(nodes);
+    k_flags_level<<<nblk(nodes), 256, 0, stream()>>>(g.flag[level].p, nodes, g.M, level, tmp.p);
+    FM_LAUNCHED();
+    tmp.download(out, nodes);
+    FM_CUDA(cudaStreamSynchronize(stream()));
+  });
+}
+
+int fm_grid_dhat(const fm_grid* h, int32_t level, double* out) {
+  return guard([&] {
+    const Grid& g = *h->g;
+    if (level < 0 || level >= g.L) throw Error(FM_ERR_DOMAIN, "level out of range");
+    const uint64_t nodes = g.nodes(level);
+    DBuf<double> tmp(nodes);
+    k_dhat_level<<<nblk(nodes), 256, 0, stream()>>>(g.det[level].p, nodes, g.field_norm, g.M,
+                                                     level, tmp.p);
+    FM_LAUNCHED();
+    tmp.download(out, nodes);
+    FM_CUDA(cudaStreamSynchronize(stream()));
+  });
+}
+
+int fm_grid_near_threshold(const fm_grid* h, double rel, int64_t* count) {
+  return guard([&] {
+    const Grid& g = *h->g;
+    DBuf<unsigned long long> c(1);
+    c.zero();
+    for (int l = 0; l < g.L; ++l) {
+      k_near<<<nblk(g.nodes(l)), 256, 0, stream()>>>(g.det[l].p, g.nodes(l), g.field_norm, g.eps,
+                                                      rel, c.p);
+      FM_LAUNCHED();
+    }
+    unsigned long long v = 0;
+    c.download(&v, 1);
+    FM_CUDA(cudaStreamSynchronize(stream()));
+    *count = int64_t(v);
+  });
+}
+
+int fm_grid_timing(const fm_grid* h, double* ms, double* bytes) {
+  return guard([&] {
+    if (ms) *ms = h->g->mra_ms;
+    if (bytes) *bytes = h->g->mra_bytes;
+  });
+}
+
+int fm_sim_create(const fm_sim_desc* d, const fm_raster* dem, const fm_grid* grid, fm_sim** out) {
+  return guard([&] {
+    require_device();
+    auto h = std::make_unique<fm_sim>();
+    h->s.reset(sim_create(d, dem, grid ? grid->g.get() : nullptr));
+    *out = h.release();
+  });
+}
+
+int fm_sim_destroy(fm_sim* s) {
+  return guard([&] { delete s; });
+}
+
+int64_t fm_sim_num_cells(const fm_sim* s) { return s ? s->s->n : -1; }
+int64_t fm_sim_num_segments(const fm_sim* s) { return s ? s->s->nseg : -1; }
+
+int fm_sim_compute_dt(fm_sim* s, double* dt) {
+  return guard([&] { *dt = sim_compute_dt(*s->s); });
+}
+int fm_sim_step(fm_sim* s, double dt) {
+  return guard([&] { sim_step(*s->s, dt); });
+}
+int fm_sim_apply_inflows(fm_sim* s, double t, double dt, double* added) {
+  return guard([&] { *added = sim_apply_inflows(*s->s, t, dt); });
+}
+int fm_sim_adapt(fm_sim* s, double t) {
+  return guard([&] { sim_adapt(*s->s, t); });
+}
+int fm_sim_volume(fm_sim* s, double* v) {
+  return guard([&] { *v = sim_volume(*s->s); });
+}
+int fm_sim_finite(fm_sim* s, int32_t* ok, double* bx, double* by) {
+  return guard([&] { *ok = sim_finite(*s->s, bx, by) ? 1 : 0; });
+}
+int fm_sim_download(fm_sim* s, int32_t* l, int32_t* i, int32_t* j, double* u9, double* z3) {
+  return guard([&] { sim_download(*s->s, l, i, j, u9, z3); });
+}
+int fm_sim_upload(fm_sim* s, const double* u9) {
+  return guard([&] { sim_upload(*s->s, u9); });
+}
+int64_t fm_sim_element_log(fm_sim* h, double* t, int64_t* count, int64_t cap) {
+  const auto& log = h->s->element_log;
+  const int64_t n = int64_t(log.size());
+  for (int64_t k = 0; k < std::min(n, cap); ++k) {
+    if (t) t[k] = log[k].first;
+    if (count) count[k] = log[k].second;
+  }
+  return n;
+}
+int fm_sim_run(fm_sim* s, fm_clock* clk, int64_t max_steps, int32_t stop_at_events,
+               fm_run_result* out) {
+  return guard([&] { sim_run(*s->s, clk, max_steps, stop_at_events, out); });
+}
+int fm_sim_last_run_ms(fm_sim* s, double* ms) {
+  return guard([&] { *ms = s->s->last_run_ms; });
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// Host-side internals of libfm_gpu.so: device buffers, error plumbing and
+// the grid / sim objects behind the opaque C handles of include/fm_gpu.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fm_gpu.h"
+
+namespace fmh {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define FM_CUDA(x) ::fmh::cuda_check((x), #x, __FILE__, __LINE__)
+#define FM_LAUNCHED() ::fmh::count_launch(__FILE__, __LINE__)
+void count_launch(const char* file, int line);
+int64_t launches();
+void count_graph_launches(int64_t n);  // kernels replayed by a graph launch
+
+cudaStream_t stream();
+void set_stream(cudaStream_t s);
+void upload_banks();  // fills fmd::c_bank once per device
+
+// Owning device buffer.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count) {
+    if (count == n && p) return;
+    release();
+    n = count;
+    if (count) FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream()));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, stream());
+    p = nullptr;
+    n = 0;
+  }
+  void zero() {
+    if (n) FM_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), stream()));
+  }
+  void fill_bytes(int v) {
+    if (n) FM_CUDA(cudaMemsetAsync(p, v, n * sizeof(T), stream()));
+  }
+  void upload(const T* h, size_t count) {
+    alloc(count);
+    if (count)
+      FM_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, stream()));
+  }
+  void download(T* h, size_t count) const {
+    if (count)
+      FM_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, stream()));
+  }
+  std::vector<T> to_host() const {
+    std::vector<T> v(n);
+    download(v.data(), n);
+    FM_CUDA(cudaStreamSynchronize(stream()));
+    return v;
+  }
+};
+
+// Device-resident static MRA result (the NonUniformGrid of quadgrid.hpp:117-120
+// plus the DetailTree of detail_tree.hpp:13-30), in block-Morton layout.
+struct Grid {
+  int L = 0, M = 1, N = 1, kind = 0;
+  double R = 1, x0 = 0, y0 = 0, eps = 0, field_norm = 0;
+  bool graded = true;
+  int64_t nleaves = 0;
+  std::vector<DBuf<double>> det;   // [L] x 9 doubles per node
+  std::vector<DBuf<uint8_t>> flag; // [L] final (closed, graded) flags
+  std::vector<DBuf<int32_t>> cnt;  // [L] leaf count of each node's subtree
+  std::vector<DBuf<int32_t>> off;  // [L] first leaf index of each active node
+  DBuf<double> coarse;             // M*N x 3: level-0 scaling
+  // leaves in device (Morton) order
+  DBuf<int8_t> lf_l;
+  DBuf<int32_t> lf_i, lf_j;
+  DBuf<double> lf_z;  // 3 per leaf
+  double mra_ms = 0, mra_bytes = 0;
+  uint64_t nodes(int l) const { return uint64_t(M) * N << (2 * l); }
+};
+
+Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind);
+// Shared by the static and the adaptive pipelines: from final per-level flags
+// (already in g.flag) compute counts, offsets, then decode topography details
+// top-down into the leaf arrays.  Returns the leaf count.
+int64_t build_leaves(Grid& g);
+// Permutation device-order -> reference (level, j, i) order, computed on the host.
+std::vector<int64_t> reference_order(const Grid& g, std::vector<int8_t>* l = nullptr,
+                                     std::vector<int32_t>* i = nullptr,
+                                     std::vector<int32_t>* j = nullptr);
+
+double elapsed_ms(cudaEvent_t a, cudaEvent_t b);
+
+// Level-L planes (3 per node, block-Morton order) of a vertex raster, padded
+// and nodata-walled as project_raster does (field.cpp:64-117).
+void project_planes(const fm_raster* r, int L, int M, int N, DBuf<double>& out);
+// Parent scaling of every level l = L-1..0 from the level-L planes
+// (encode rows 0-2, wavelets.cpp:77-86); sc[l] holds 3 doubles per node.
+void scaling_pyramid(DBuf<double>&& level_L, int L, int M, int N, int kind,
+                     std::vector<DBuf<double>>& sc);
+
+}  // namespace fmh

@@ -1,0 +1,139 @@
+// Device views and the host Sim object behind fm_sim* (the drive<Sim> duck
+// type of run.cpp:35-141 implemented on the device).
+#pragma once
+
+#include <memory>
+
+#include "fm_internal.hpp"
+
+namespace fmh {
+
+constexpr int kMaxInflows = 8;
+constexpr int kMaxHydroSamples = 4096;
+
+// Device copy of the EventClock (sim_common.hpp:31-45) plus the per-step
+// control block written by the step-head kernel.  clk[0] is the state at the
+// start of a step, clk[1] the state of the step in flight.
+struct DevClock {
+  double end_time, out_int, gauge_int, now;
+  long long next_out, next_gauge;
+  double dt, t0;         // this step
+  long long steps, max_steps;
+  int active, stop_at_events, event_due, finished;
+  int blew_up, had_step, pad0, pad1;
+  double dt_min, dt_max, vol_in, blow_t;
+  unsigned long long bad_key;     // reported key of the first non-finite cell
+  double per_cell[kMaxInflows];   // Q(t0) dt / region_cells, or 0 when Q <= 0
+  int on[kMaxInflows];
+};
+
+// Per-step reductions, double-buffered by step parity.
+struct DevRed {
+  unsigned long long dtmin;   // DG2/FV1: min size/max(sx,sy); ACC: min wet size
+  unsigned long long hmax;    // ACC: max wet h
+  unsigned long long badkey;  // min (level<<58 | j<<29 | i) of non-finite cells
+  unsigned long long pad;
+};
+
+struct Hydro {
+  int off[kMaxInflows + 1];
+  int n;
+  long long region[kMaxInflows];
+  double t[kMaxHydroSamples], q[kMaxHydroSamples];
+};
+
+// Everything a non-uniform leaf kernel needs (POD, passed by value).
+struct NuView {
+  int L, M, N, scheme, adaptive, ninflow;
+  double R, x0, y0, g, hdry, courant;
+  int bc[4];
+  long long n;
+  const int8_t* lvl;
+  const int32_t* li;
+  const int32_t* lj;
+  const double* z;      // 3 per leaf
+  const double* nman;
+  const int32_t* nb;    // 8 per leaf: 2 per side (N,E,S,W)
+  const uint8_t* sk;    // 2 bits per side: 0 boundary, 1 coarser, 2 same, 3 finer
+  const double* zpair;  // adaptive: per leaf-side z* partner (4 per leaf) or null
+  const int32_t* infc;  // ninflow x n fine-cell counts per leaf
+  // ACC
+  const int32_t* seg_l;
+  const int32_t* seg_r;
+  const int32_t* sid;   // 8 per leaf
+  long long nseg;
+};
+
+struct Sim {
+  int solver = 0, scheme = 0;
+  bool adaptive = false, uniform = false;
+  double g = 9.80665, hdry = 1e-6, courant = 0.33;
+  int bc[4] = {0, 0, 0, 0};
+  // geometry
+  int L = 0, M = 1, N = 1;
+  double R = 1, x0 = 0, y0 = 0;
+  int nx = 0, ny = 0;  // uniform raster
+  int64_t n = 0, nseg = 0;
+  // leaves (device Morton order) and state
+  DBuf<int8_t> lvl;
+  DBuf<int32_t> li, lj;
+  DBuf<double> u, us, z, nman, zpair;
+  DBuf<int32_t> nb, sid, seg_l, seg_r;
+  DBuf<uint8_t> sk;
+  DBuf<double> accq, accqb;  // ACC: per segment, per leaf-side (4 per leaf)
+  DBuf<double> aqx, aqy;     // uniform ACC faces
+  DBuf<int32_t> infc;        // per inflow per leaf counts
+  int ninflow = 0;
+  std::vector<std::vector<double>> hy_t, hy_q;
+  std::vector<long long> region;
+  std::vector<int> rect;     // 4 per inflow (i0 j0 i1 j1)
+  DBuf<Hydro> hydro;
+  DBuf<DevClock> clk;        // [2]
+  DBuf<DevRed> red;          // [2]
+  DBuf<int> errflag;         // device error bits (negative depth into HLL)
+  bool fv1_in_star = false;
+  double last_run_ms = 0.0;
+  // Manning raster (kept for adaptive remaps)
+  DBuf<double> mr;
+  int mr_ncols = 0, mr_nrows = 0;
+  double mr_xll = 0, mr_yll = 0, mr_cs = 1, manning = 0;
+  bool has_mr = false;
+  // adaptive state
+  std::unique_ptr<Grid> grid;      // current grid pyramids (flags/off) + topo details
+  struct AdaptState* ad = nullptr;  // owned; freed by adaptive_destroy
+  int adapt_every = 1;
+  int64_t since_adapt = 0;
+  std::vector<std::pair<double, int64_t>> element_log;
+  // CUDA graph of a batch of steps
+  cudaGraphExec_t graph = nullptr;
+  int graph_steps = 0;
+  ~Sim();
+
+  NuView view() const;
+};
+
+Sim* sim_create(const fm_sim_desc* d, const fm_raster* dem, const Grid* grid);
+double sim_compute_dt(Sim& s);
+void sim_step(Sim& s, double dt);
+double sim_apply_inflows(Sim& s, double t, double dt);
+void sim_adapt(Sim& s, double t);
+double sim_volume(Sim& s);
+bool sim_finite(Sim& s, double* bx, double* by);
+void sim_download(Sim& s, int32_t* l, int32_t* i, int32_t* j, double* u9, double* z3);
+void sim_upload(Sim& s, const double* u9);
+void sim_run(Sim& s, fm_clock* clk, int64_t max_steps, int stop_at_events, fm_run_result* out);
+
+// topology (topo.cu)
+void build_topology(Sim& s, const Grid& g);
+void resolve_inflows(Sim& s, const Grid& g);
+void resolve_manning(Sim& s);
+int64_t scan_exclusive(const int32_t* in, int32_t* out, int64_t n);
+
+// adaptive (adaptive.cu)
+void adaptive_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem);
+void adaptive_adapt(Sim& s, double t);
+
+// uniform (uniform.cu)
+void uniform_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem);
+
+}  // namespace fmh

@@ -1,0 +1,637 @@
+// Static multiresolution analysis on sm_100a.
+//
+// Replaces generate_static_grid (detail_tree.cpp:172-178) and its stages:
+//   project_raster      field.cpp:64-117     -> fused into k_encode_tiles
+//   build_detail_tree   detail_tree.cpp:10-54 -> k_field_norm + k_encode_tiles
+//   flag_significant    detail_tree.cpp:66-74 -> sig flags in k_encode_tiles
+//   ancestor_closure +  detail_tree.cpp:56-64,
+//   grade_flags                      :97-113 -> k_grade_count (one gather pass per level)
+//   leaves_from_flags + make_quadgrid +
+//   assemble_grid       detail_tree.cpp:115-164, quadgrid.cpp:85-110 -> k_level0_offsets + k_topdown
+//
+// Layout: every pyramid level is a dense array in block-Morton order (see
+// fmd::node_index) so the four children of node n are 4n..4n+3: the encode
+// reads 96 contiguous bytes per parent and the flags of a sibling quad are
+// one 32-bit word.  Leaves come out in global Morton order of their SW fine
+// corner (the depth-first order of the tree) with a dense per-level offset
+// pyramid that maps any node to its leaf index in O(1) (replacing the
+// reference's unordered_map index).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+
+#include "fm_device.cuh"
+#include "fm_internal.hpp"
+
+using namespace fmd;
+
+namespace fmh {
+
+namespace {
+
+constexpr int kMaxL = 16;
+
+__device__ __forceinline__ unsigned long long ordered_bits(double v) {
+  const unsigned long long u = dbits(v);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double from_ordered(unsigned long long u) {
+  return bitsd((u >> 63) ? (u & 0x7fffffffffffffffull) : ~u);
+}
+
+struct Scalars {
+  unsigned long long vmax_ord;  // ordered max over non-nodata vertices
+  unsigned long long norm_bits; // max |c0| (non-negative)
+  int err;                      // 1: non-finite vertex
+  int pad;
+  double wall;
+  double norm;
+};
+
+// field.cpp:48-54 (nodata wall) — max over the non-nodata vertex samples.
+__global__ void k_vertex_max(const double* __restrict__ v, size_t n, double nodata, Scalars* s) {
+  double m = -INFINITY;
+  int bad = 0;
+  for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < n;
+       k += size_t(gridDim.x) * blockDim.x) {
+    const double x = v[k];
+    if (x != nodata) {
+      m = smax(m, x);
+      if (!isfinite(x)) bad = 1;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double y = __shfl_xor_sync(0xffffffffu, m, o);
+    m = smax(m, y);
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&s->vmax_ord, ordered_bits(m));
+    if (bad) atomicOr(&s->err, 1);
+  }
+}
+
+struct VertexView {
+  const double* v;
+  int ncols, nrows, n, m;  // n = ncols-1 elements east, m = nrows-1 north
+  double nodata;
+  double wall;
+  __device__ __forceinline__ double at(int row, int col) const {
+    const double x = v[size_t(row) * ncols + col];
+    return x == nodata ? wall : x;
+  }
+  // field.cpp:64-91: element (i, j), edge-replicated beyond the raster.
+  __device__ __forceinline__ P3 plane(int i, int j) const {
+    const int ie = min(i, n - 1), je = min(j, m - 1);
+    const int rs = nrows - 1 - je, rn = rs - 1;
+    return project4(at(rn, ie), at(rn, ie + 1), at(rs, ie), at(rs, ie + 1));
+  }
+};
+
+__global__ void k_wall(Scalars* s) {
+  double z = from_ordered(s->vmax_ord);
+  if (!isfinite(z)) z = 0.0;
+  s->wall = z + 100.0;
+}
+
+// detail_tree.cpp:22-23 — field_norm = max |c0| over the fine elements.
+__global__ void k_field_norm(VertexView vv, const Scalars* __restrict__ sin, Scalars* s) {
+  vv.wall = sin->wall;
+  const size_t total = size_t(vv.n) * vv.m;
+  double m = 0.0;
+  for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < total;
+       k += size_t(gridDim.x) * blockDim.x) {
+    const int i = int(k % size_t(vv.n)), j = int(k / size_t(vv.n));
+    const P3 p = vv.plane(i, j);
+    m = smax(m, fabs(p.c0));
+  }
+  for (int o = 16; o; o >>= 1) m = smax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&s->norm_bits, dbits(m));
+}
+
+__global__ void k_norm_final(Scalars* s) { s->norm = bitsd(s->norm_bits); }
+
+struct EncParams {
+  VertexView vv;             // FROM_VERTICES
+  const double* sc_in;       // input scaling (3 per node) at level lev_in
+  double* sc_out;            // tile-root scaling (3 per node) at level lev_in - T
+  double* det[kMaxL];        // per level, 9 per node
+  uint8_t* flag[kMaxL];      // per level, significance
+  const Scalars* scal;
+  double eps;
+  int lev_in, T, M, kind;
+};
+
+// One CTA encodes a tile of 4^T input nodes up T levels (detail_tree.cpp:34-51),
+// writing details + significance (detail_tree.cpp:66-72) for every parent and
+// the tile-root scaling.  Thread t owns first-level parent t of the tile: it
+// builds its four children itself (projecting them from the DEM vertices when
+// FROM_VERTICES) so the finest, largest level never touches shared memory;
+// higher levels go through a 4^(T-1)-entry shared buffer.
+template <bool FROM_VERTICES>
+__global__ void __launch_bounds__(256) k_encode_tiles(EncParams p) {
+  extern __shared__ P3 sbuf[];
+  const int tid = threadIdx.x;
+  const uint64_t tile = blockIdx.x;
+  const double norm = p.scal->norm;
+  if constexpr (FROM_VERTICES) p.vv.wall = p.scal->wall;
+
+  // first level: parent (lev_in - 1), local index tid
+  int lev = p.lev_in - 1;
+  const uint64_t par = (tile << (2 * (p.T - 1))) + uint64_t(tid);
+  P3 kids[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint64_t c = 4 * par + k;
+    if constexpr (FROM_VERTICES) {
+      int i, j;
+      node_ij(p.lev_in, c, p.M, i, j);
+      kids[k] = p.vv.plane(i, j);
+    } else {
+      const double* s = p.sc_in + 3 * c;
+      kids[k] = P3{s[0], s[1], s[2]};
+    }
+  }
+  P3 par_s;
+  double d[9];
+  encode(kids, p.kind, par_s, d);
+  {
+    double* o = p.det[lev] + 9 * par;
+#pragma unroll
+    for (int n = 0; n < 9; ++n) o[n] = d[n];
+    p.flag[lev][par] = dhat(d, norm) >= p.eps ? 1 : 0;
+  }
+  if (p.T == 1) {
+    double* o = p.sc_out + 3 * par;
+    o[0] = par_s.c0;
+    o[1] = par_s.cx;
+    o[2] = par_s.cy;
+    return;
+  }
+  sbuf[tid] = par_s;
+  __syncthreads();
+  int count = blockDim.x;  // nodes at `lev`
+  for (int t = 1; t < p.T; ++t) {
+    --lev;
+    count >>= 2;
+    P3 mine;
+    bool have = tid < count;
+    if (have) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) kids[k] = sbuf[4 * tid + k];
+      encode(kids, p.kind, mine, d);
+      const uint64_t node = (tile << (2 * (p.T - 1 - t))) + uint64_t(tid);
+      double* o = p.det[lev] + 9 * node;
+#pragma unroll
+      for (int n = 0; n < 9; ++n) o[n] = d[n];
+      p.flag[lev][node] = dhat(d, norm) >= p.eps ? 1 : 0;
+    }
+    __syncthreads();
+    if (have) sbuf[tid] = mine;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    double* o = p.sc_out + 3 * tile;
+    o[0] = sbuf[0].c0;
+    o[1] = sbuf[0].cx;
+    o[2] = sbuf[0].cy;
+  }
+}
+
+// L = 0: the fine field is the coarse field.
+__global__ void k_copy_fine(VertexView vv, const Scalars* __restrict__ s, double* coarse, int M,
+                            uint64_t total) {
+  vv.wall = s->wall;
+  const uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (k >= total) return;
+  int i, j;
+  node_ij(0, k, M, i, j);
+  const P3 q = vv.plane(i, j);
+  coarse[3 * k] = q.c0;
+  coarse[3 * k + 1] = q.cx;
+  coarse[3 * k + 2] = q.cy;
+}
+
+// Final flags and subtree leaf counts, one level per launch, fine -> coarse.
+// G(l) = sig(l) | any G(l+1) child | (graded) any G(l+1) node edge-adjacent to
+// the 2x2 child block.  This single gather equals the reference's closure +
+// sequential grading sweep (detail_tree.cpp:56-64, 97-113): a level-(l+1)
+// flagged node flags the parents of its four edge neighbours, i.e. the
+// parent P gets flagged iff a flagged level-(l+1) node is a child of P or
+// edge-adjacent to P's child block, and G(l+1) is final before level l is
+// visited in both formulations.  (Verified against the oracle on random trees
+// in tests/test_mra_gpu.py.)
+__global__ void k_grade_count(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
+                              int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1, int l,
+                              int L, int M, int N, uint64_t nodes, int graded) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= nodes) return;
+  int g = fl[n];
+  int c = 1;
+  if (l + 1 < L) {
+    const uint32_t kids = *reinterpret_cast<const uint32_t*>(fl1 + 4 * n);
+    if (kids) g = 1;
+    if (graded && !g) {
+      int i, j;
+      node_ij(l, n, M, i, j);
+      const int w = M << (l + 1), h = N << (l + 1);
+      const int ci = 2 * i, cj = 2 * j;
+      const int ri[8] = {ci - 1, ci - 1, ci + 2, ci + 2, ci, ci + 1, ci, ci + 1};
+      const int rj[8] = {cj, cj + 1, cj, cj + 1, cj - 1, cj - 1, cj + 2, cj + 2};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (ri[q] < 0 || rj[q] < 0 || ri[q] >= w || rj[q] >= h) continue;
+        if (fl1[node_index(l + 1, ri[q], rj[q], M)]) {
+          g = 1;
+          break;
+        }
+      }
+    }
+    if (g) {
+      const int4 cc = *reinterpret_cast<const int4*>(cnt1 + 4 * n);
+      c = cc.x + cc.y + cc.z + cc.w;
+    }
+  } else if (g) {
+    c = 4;
+  }
+  fl[n] = uint8_t(g);
+  cnt[n] = c;
+}
+
+// Exclusive scan of the level-0 counts (M*N nodes) in one CTA.
+__global__ void k_level0_offsets(const int32_t* __restrict__ cnt, int32_t* __restrict__ off,
+                                 int64_t n, long long* total) {
+  __shared__ long long part[1024];
+  __shared__ long long base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < n; b0 += blockDim.x) {
+    const int64_t k = b0 + threadIdx.x;
+    const long long v = k < n ? cnt[k] : 0;
+    part[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < int(blockDim.x); o <<= 1) {
+      const long long add = threadIdx.x >= unsigned(o) ? part[threadIdx.x - o] : 0;
+      __syncthreads();
+      part[threadIdx.x] += add;
+      __syncthreads();
+    }
+    if (k < n) off[k] = int32_t(base + part[threadIdx.x] - v);
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) base += part[threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = base;
+}
+
+struct LeafOut {
+  int8_t* l;
+  int32_t* i;
+  int32_t* j;
+  double* z;
+};
+
+__device__ __forceinline__ void emit_leaf(const LeafOut& o, int l, uint64_t node, int M, int32_t at,
+                                          const P3& z) {
+  int i, j;
+  node_ij(l, node, M, i, j);
+  o.l[at] = int8_t(l);
+  o.i[at] = i;
+  o.j[at] = j;
+  o.z[3 * at] = z.c0;
+  o.z[3 * at + 1] = z.cx;
+  o.z[3 * at + 2] = z.cy;
+}
+
+// Top-down decode of one level (detail_tree.cpp:132-164): an active flagged
+// node decodes its stored details into its four children; children that are
+// leaves are emitted at their final index, the others pass their plane and
+// offset down through the level-(l+1) scratch.
+__global__ void k_topdown(const uint8_t* __restrict__ flp, const uint8_t* __restrict__ fl,
+                          const uint8_t* __restrict__ fl1, const int32_t* __restrict__ cnt1,
+                          const int32_t* __restrict__ off, int32_t* __restrict__ off1,
+                          const double* __restrict__ zin, double* __restrict__ zout,
+                          const double* __restrict__ det, int l, int L, int M, int kind,
+                          uint64_t nodes, LeafOut out) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= nodes) return;
+  if (l > 0 && !flp[n >> 2]) return;
+  const P3 z{zin[3 * n], zin[3 * n + 1], zin[3 * n + 2]};
+  const int32_t o = off[n];
+  if (!fl[n]) {
+    if (l == 0) emit_leaf(out, 0, n, M, o, z);
+    return;
+  }
+  double d[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) d[q] = det[9 * n + q];
+  P3 kids[4];
+  decode(z, d, kind, kids);
+  int32_t run = o;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint64_t c = 4 * n + k;
+    if (l + 1 == L) {
+      emit_leaf(out, L, c, M, run, kids[k]);
+      run += 1;
+    } else if (!fl1[c]) {
+      emit_leaf(out, l + 1, c, M, run, kids[k]);
+      off1[c] = run;
+      run += 1;
+    } else {
+      zout[3 * c] = kids[k].c0;
+      zout[3 * c + 1] = kids[k].cx;
+      zout[3 * c + 2] = kids[k].cy;
+      off1[c] = run;
+      run += cnt1[c];
+    }
+  }
+}
+
+// Level-L planes of a vertex raster in node order (field.cpp:106-117).
+__global__ void k_project_level(VertexView vv, const Scalars* __restrict__ s, double* out, int L,
+                                int M, uint64_t total) {
+  vv.wall = s->wall;
+  const uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (k >= total) return;
+  int i, j;
+  node_ij(L, k, M, i, j);
+  const P3 q = vv.plane(i, j);
+  out[3 * k] = q.c0;
+  out[3 * k + 1] = q.cx;
+  out[3 * k + 2] = q.cy;
+}
+
+// One level of parent scaling (encode rows 0-2 only), children 4n..4n+3.
+__global__ void k_parent_level(const double* __restrict__ in, double* __restrict__ out, int kind,
+                               uint64_t nodes) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= nodes) return;
+  P3 kids[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double* c = in + 3 * (4 * n + k);
+    kids[k] = P3{c[0], c[1], c[2]};
+  }
+  const P3 p = encode_parent(kids, kind);
+  out[3 * n] = p.c0;
+  out[3 * n + 1] = p.cx;
+  out[3 * n + 2] = p.cy;
+}
+
+inline unsigned blocks_for(uint64_t n, int t) { return unsigned((n + t - 1) / t); }
+
+}  // namespace
+
+int64_t build_leaves(Grid& g) {
+  cudaStream_t st = stream();
+  const int L = g.L;
+  g.cnt.resize(L);
+  g.off.resize(L);
+  for (int l = 0; l < L; ++l) {
+    g.cnt[l].alloc(g.nodes(l));
+    g.off[l].alloc(g.nodes(l));
+  }
+  // counts (flags already final at level L-1 .. 0 after k_grade_count)
+  DBuf<long long> total(1);
+  if (L == 0) {
+    // every level-0 node is a leaf
+    g.nleaves = int64_t(g.M) * g.N;
+  } else {
+    k_level0_offsets<<<1, 1024, 0, st>>>(g.cnt[0].p, g.off[0].p, int64_t(g.nodes(0)), total.p);
+    FM_LAUNCHED();
+    long long tot = 0;
+    total.download(&tot, 1);
+    FM_CUDA(cudaStreamSynchronize(st));
+    g.nleaves = tot;
+  }
+  if (g.nleaves > INT32_MAX) throw Error(FM_ERR_STRUCTURE, "leaf count exceeds int32");
+  g.lf_l.alloc(g.nleaves);
+  g.lf_i.alloc(g.nleaves);
+  g.lf_j.alloc(g.nleaves);
+  g.lf_z.alloc(3 * g.nleaves);
+  LeafOut out{g.lf_l.p, g.lf_i.p, g.lf_j.p, g.lf_z.p};
+  if (L == 0) {
+    // copy coarse planes out as leaves (node order == Morton order at level 0)
+    std::vector<double> c = g.coarse.to_host();
+    std::vector<int8_t> hl(g.nleaves, 0);
+    std::vector<int32_t> hi(g.nleaves), hj(g.nleaves);
+    for (int64_t k = 0; k < g.nleaves; ++k) {
+      hi[k] = int32_t(k % g.M);
+      hj[k] = int32_t(k / g.M);
+    }
+    g.lf_l.upload(hl.data(), hl.size());
+    g.lf_i.upload(hi.data(), hi.size());
+    g.lf_j.upload(hj.data(), hj.size());
+    g.lf_z.upload(c.data(), c.size());
+    return g.nleaves;
+  }
+  // decoded-plane scratch per level (levels 1..L-1)
+  std::vector<DBuf<double>> zs(L);
+  for (int l = 1; l < L; ++l) zs[l].alloc(3 * g.nodes(l));
+  for (int l = 0; l < L; ++l) {
+    const uint64_t nodes = g.nodes(l);
+    const bool last = l + 1 == L;
+    k_topdown<<<blocks_for(nodes, 256), 256, 0, st>>>(
+        l ? g.flag[l - 1].p : nullptr, g.flag[l].p, last ? nullptr : g.flag[l + 1].p,
+        last ? nullptr : g.cnt[l + 1].p, g.off[l].p, last ? nullptr : g.off[l + 1].p,
+        l ? zs[l].p : g.coarse.p, last ? nullptr : zs[l + 1].p, g.det[l].p, l, L, g.M, g.kind,
+        nodes, out);
+    FM_LAUNCHED();
+  }
+  return g.nleaves;
+}
+
+Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind) {
+  if (!dem || !dem->values) throw Error(FM_ERR_CONFIG, "null DEM raster");
+  if (dem->ncols < 2 || dem->nrows < 2)
+    throw Error(FM_ERR_CONFIG, "DEM must have at least 2x2 samples to define elements");
+  if (L < 0) throw Error(FM_ERR_CONFIG, "max_level must be >= 0");
+  if (L > kMaxL - 1) throw Error(FM_ERR_CONFIG, "max_level above 15 is not supported");
+  if (eps < 0.0) throw Error(FM_ERR_DOMAIN, "flag_significant: eps must be >= 0");
+  if (kind != FM_MW && kind != FM_HW) throw Error(FM_ERR_CONFIG, "unknown wavelet kind");
+  upload_banks();
+  cudaStream_t st = stream();
+
+  auto g = std::make_unique<Grid>();
+  const int n = dem->ncols - 1, m = dem->nrows - 1;
+  const int step = 1 << L;
+  g->L = L;
+  g->M = (n + step - 1) / step;
+  g->N = (m + step - 1) / step;
+  g->R = dem->cellsize;
+  g->x0 = dem->xll;
+  g->y0 = dem->yll;
+  g->eps = eps;
+  g->kind = kind;
+  g->graded = graded;
+  if (uint64_t(g->M) * g->N * (uint64_t(1) << (2 * L)) > (uint64_t(1) << 40))
+    throw Error(FM_ERR_CONFIG, "domain too large");
+
+  cudaEvent_t e0, e1;
+  FM_CUDA(cudaEventCreate(&e0));
+  FM_CUDA(cudaEventCreate(&e1));
+
+  // DEM to the device (or use it in place)
+  const size_t nv = size_t(dem->ncols) * dem->nrows;
+  DBuf<double> vbuf;
+  const double* vdev = dem->values;
+  if (!dem->on_device) {
+    vbuf.upload(dem->values, nv);
+    vdev = vbuf.p;
+  }
+  DBuf<Scalars> scal(1);
+  scal.zero();
+  FM_CUDA(cudaEventRecord(e0, st));
+
+  const int sms = 148;
+  k_vertex_max<<<sms * 8, 256, 0, st>>>(vdev, nv, dem->nodata, scal.p);
+  FM_LAUNCHED();
+  k_wall<<<1, 1, 0, st>>>(scal.p);
+  FM_LAUNCHED();
+  VertexView vv{vdev, dem->ncols, dem->nrows, n, m, dem->nodata, 0.0};
+  k_field_norm<<<sms * 8, 256, 0, st>>>(vv, scal.p, scal.p);
+  FM_LAUNCHED();
+  k_norm_final<<<1, 1, 0, st>>>(scal.p);
+  FM_LAUNCHED();
+
+  g->det.resize(L);
+  g->flag.resize(L);
+  for (int l = 0; l < L; ++l) {
+    g->det[l].alloc(9 * g->nodes(l));
+    g->flag[l].alloc(g->nodes(l));
+  }
+  g->coarse.alloc(3 * g->nodes(0));
+
+  if (L == 0) {
+    k_copy_fine<<<blocks_for(g->nodes(0), 256), 256, 0, st>>>(vv, scal.p, g->coarse.p, g->M,
+                                                             g->nodes(0));
+    FM_LAUNCHED();
+  } else {
+    // encode L levels in passes of up to 5 levels (4^5 = 1024 inputs per CTA)
+    int lev_in = L;
+    DBuf<double> sc_prev;
+    bool first = true;
+    while (lev_in > 0) {
+      const int T = std::min(5, lev_in);
+      const int lev_out = lev_in - T;
+      DBuf<double> sc_out;
+      double* out_p;
+      if (lev_out == 0) {
+        out_p = g->coarse.p;
+      } else {
+        sc_out.alloc(3 * g->nodes(lev_out));
+        out_p = sc_out.p;
+      }
+      EncParams p{};
+      p.vv = vv;
+      p.sc_in = sc_prev.p;
+      p.sc_out = out_p;
+      for (int l = 0; l < L; ++l) {
+        p.det[l] = g->det[l].p;
+        p.flag[l] = g->flag[l].p;
+      }
+      p.scal = scal.p;
+      p.eps = eps;
+      p.lev_in = lev_in;
+      p.T = T;
+      p.M = g->M;
+      p.kind = kind;
+      const uint64_t tiles = g->nodes(lev_out);
+      const int threads = 1 << (2 * (T - 1));
+      const size_t smem = sizeof(P3) * threads;
+      if (first)
+        k_encode_tiles<true><<<unsigned(tiles), threads, smem, st>>>(p);
+      else
+        k_encode_tiles<false><<<unsigned(tiles), threads, smem, st>>>(p);
+      FM_LAUNCHED();
+      first = false;
+      sc_prev = std::move(sc_out);
+      lev_in = lev_out;
+    }
+  }
+  // final flags + subtree counts, fine -> coarse
+  g->cnt.resize(L);
+  for (int l = 0; l < L; ++l) g->cnt[l].alloc(g->nodes(l));
+  for (int l = L - 1; l >= 0; --l) {
+    const uint64_t nodes = g->nodes(l);
+    k_grade_count<<<blocks_for(nodes, 256), 256, 0, st>>>(
+        g->flag[l].p, l + 1 < L ? g->flag[l + 1].p : nullptr, g->cnt[l].p,
+        l + 1 < L ? g->cnt[l + 1].p : nullptr, l, L, g->M, g->N, nodes, graded ? 1 : 0);
+    FM_LAUNCHED();
+  }
+  build_leaves(*g);
+  FM_CUDA(cudaEventRecord(e1, st));
+  Scalars hs{};
+  scal.download(&hs, 1);
+  FM_CUDA(cudaStreamSynchronize(st));
+  if (hs.err) throw Error(FM_ERR_DOMAIN, "project_vertices: non-finite vertex value");
+  g->field_norm = hs.norm;
+  g->mra_ms = elapsed_ms(e0, e1);
+  const double Nf = double(g->nodes(L)), Nint = double(uint64_t(g->M) * g->N) * ((std::pow(4.0, L) - 1) / 3);
+  g->mra_bytes = 24.0 * Nf + 73.0 * Nint + 36.0 * double(g->nleaves);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return g.release();
+}
+
+std::vector<int64_t> reference_order(const Grid& g, std::vector<int8_t>* lo, std::vector<int32_t>* io,
+                                     std::vector<int32_t>* jo) {
+  std::vector<int8_t> l = g.lf_l.to_host();
+  std::vector<int32_t> i = g.lf_i.to_host(), j = g.lf_j.to_host();
+  std::vector<int64_t> perm(g.nleaves);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) {
+    if (l[a] != l[b]) return l[a] < l[b];
+    if (j[a] != j[b]) return j[a] < j[b];
+    return i[a] < i[b];
+  });
+  if (lo) *lo = std::move(l);
+  if (io) *io = std::move(i);
+  if (jo) *jo = std::move(j);
+  return perm;
+}
+
+void project_planes(const fm_raster* r, int L, int M, int N, DBuf<double>& out) {
+  cudaStream_t st = stream();
+  const size_t nv = size_t(r->ncols) * r->nrows;
+  DBuf<double> vbuf;
+  const double* vdev = r->values;
+  if (!r->on_device) {
+    vbuf.upload(r->values, nv);
+    vdev = vbuf.p;
+  }
+  DBuf<Scalars> scal(1);
+  scal.zero();
+  k_vertex_max<<<148 * 8, 256, 0, st>>>(vdev, nv, r->nodata, scal.p);
+  FM_LAUNCHED();
+  k_wall<<<1, 1, 0, st>>>(scal.p);
+  FM_LAUNCHED();
+  VertexView vv{vdev, r->ncols, r->nrows, r->ncols - 1, r->nrows - 1, r->nodata, 0.0};
+  const uint64_t total = uint64_t(M) * N << (2 * L);
+  out.alloc(3 * total);
+  k_project_level<<<blocks_for(total, 256), 256, 0, st>>>(vv, scal.p, out.p, L, M, total);
+  FM_LAUNCHED();
+  Scalars hs{};
+  scal.download(&hs, 1);
+  FM_CUDA(cudaStreamSynchronize(st));
+  if (hs.err) throw Error(FM_ERR_DOMAIN, "project_vertices: non-finite vertex value");
+}
+
+void scaling_pyramid(DBuf<double>&& level_L, int L, int M, int N, int kind,
+                     std::vector<DBuf<double>>& sc) {
+  upload_banks();
+  sc.clear();
+  sc.resize(L + 1);
+  sc[L] = std::move(level_L);
+  for (int l = L - 1; l >= 0; --l) {
+    const uint64_t nodes = uint64_t(M) * N << (2 * l);
+    sc[l].alloc(3 * nodes);
+    k_parent_level<<<blocks_for(nodes, 256), 256, 0, stream()>>>(sc[l + 1].p, sc[l].p, kind, nodes);
+    FM_LAUNCHED();
+  }
+}
+
+}  // namespace fmh

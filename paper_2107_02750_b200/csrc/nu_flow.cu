@@ -1,0 +1,608 @@
+// Per-timestep flow updates on the non-uniform leaf set (sm_100a, fp64).
+//
+// Replaces NonUniformSim::step_rk / step_acc / compute_dt / apply_inflows /
+// finite_state (solver_nonuniform.cpp:306-487) and the drive-loop body
+// (run.cpp:80-111).  One thread per leaf, leaves in Morton order:
+//
+//   k_head_friction  step head: next dt from the previous step's reduction
+//                    (compute_dt :427-449 + EventClock::clip), clock advance,
+//                    then Manning friction (sim_common.cpp:30-46) in place.
+//   k_stage<1>       segment HLL + side-effective states + L operator + Euler
+//                    update + positivity for every leaf, gathering its
+//                    neighbours (segment_states :91-115, side_effective
+//                    :117-178, assemble :180-274, positivity :276-304).
+//   k_stage<2>       the same on U*, RK2 average, then (fused epilogue) the
+//                    inflow sources, the non-finite guard and the CFL
+//                    reduction for the next step.
+//   k_acc_faces / k_acc_leaves   ACC (step_acc :350-418).
+//
+// There is no segment scratch for DG2/FV1: each leaf evaluates the HLL flux
+// of every sub-face on its own sides.  A face shared by two leaves is
+// evaluated by both, from identical inputs in identical order, so both see
+// the same bits; in exchange no 48 B/segment state round-trips through HBM
+// and a whole RK stage is one launch.  All sums are gathers in the
+// reference's order (sides N,E,S,W; sub-faces south-to-north / west-to-east),
+// never floating-point atomics, so results do not depend on scheduling.
+#include "fm_device.cuh"
+#include "fm_sim.hpp"
+
+using namespace fmd;
+
+namespace fmh {
+
+namespace {
+
+struct Pt {
+  double h, qx, qy, z, eta, u, v;
+};
+
+__device__ __forceinline__ double lsize(const NuView& v, int l) { return v.R * double(1 << (v.L - l)); }
+__device__ __forceinline__ double lcen(double o, const NuView& v, int l, int i) {
+  return o + (i + 0.5) * v.R * double(1 << (v.L - l));
+}
+
+// limit_at (solver_nonuniform.cpp:52-66)
+__device__ __forceinline__ Pt limit(const double s[9], const P3& zc, double cx, double cy,
+                                    double sz, double x, double y, double hdry) {
+  Pt p;
+  p.h = smax(0.0, eval_plane(P3{s[0], s[1], s[2]}, cx, cy, sz, x, y));
+  p.qx = eval_plane(P3{s[3], s[4], s[5]}, cx, cy, sz, x, y);
+  p.qy = eval_plane(P3{s[6], s[7], s[8]}, cx, cy, sz, x, y);
+  p.z = eval_plane(zc, cx, cy, sz, x, y);
+  p.eta = p.h + p.z;
+  p.u = vel(p.h, p.qx, hdry);
+  p.v = vel(p.h, p.qy, hdry);
+  return p;
+}
+
+__device__ __forceinline__ void load9(const double* __restrict__ a, long long k, double s[9]) {
+  const double* p = a + 9 * k;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) s[q] = p[q];
+}
+__device__ __forceinline__ P3 load3(const double* __restrict__ a, long long k) {
+  const double* p = a + 3 * k;
+  return P3{p[0], p[1], p[2]};
+}
+
+__device__ __forceinline__ unsigned long long leaf_key(int l, int i, int j) {
+  return (static_cast<unsigned long long>(l) << 58) | (static_cast<unsigned long long>(j) << 29) |
+         static_cast<unsigned long long>(i);
+}
+
+// hydrograph_at (hydrograph.cpp:38-49)
+__device__ double hydro_at(const Hydro& h, int f, double t) {
+  const int a = h.off[f], b = h.off[f + 1];
+  if (t <= h.t[a]) return h.q[a];
+  if (t >= h.t[b - 1]) return h.q[b - 1];
+  int hi = a;
+  while (hi < b && !(t < h.t[hi])) ++hi;
+  const int lo = hi - 1;
+  if (t == h.t[lo]) return h.q[lo];
+  const double w = (t - h.t[lo]) / (h.t[hi] - h.t[lo]);
+  return h.q[lo] + w * (h.q[hi] - h.q[lo]);
+}
+
+__device__ __forceinline__ bool reached(double now, double target) {
+  return now >= target - 1e-9 * smax(1.0, target);
+}
+
+// The drive-loop bookkeeping for one step (run.cpp:80-111 with EventClock,
+// sim_common.cpp:48-82).  Pure function of the step-start clock and the
+// previous step's reductions, so every block derives the same decision; block
+// 0 publishes it as clk[1].  It first closes the previous step (non-finite
+// guard, then the gauge/output event counters, in the reference's order),
+// then decides whether to run this step, computes dt = clip(compute_dt) and
+// advances the clock and the inflow sources (apply_inflows uses the
+// step-start time, run.cpp:84).
+__device__ bool decide_step(const DevClock& c0, const DevRed& r, const Hydro* hy, int scheme,
+                            double courant, double g, double hdry, int ninflow, DevClock& c) {
+  c = c0;
+  if (c.active && c.had_step) {
+    if (r.badkey != ~0ull) {
+      c.blew_up = 1;
+      c.blow_t = c.now;
+      c.bad_key = r.badkey;
+      c.active = 0;
+    } else {
+      bool ev = false;
+      if (c.gauge_int > 0.0 && reached(c.now, c.next_gauge * c.gauge_int)) {
+        ++c.next_gauge;
+        ev = true;
+      }
+      if (c.out_int > 0.0 && reached(c.now, c.next_out * c.out_int)) {
+        ++c.next_out;
+        ev = true;
+      }
+      if (ev && c.stop_at_events) {
+        c.event_due = 1;
+        c.active = 0;
+      }
+    }
+  }
+  c.had_step = 0;
+  if (c.active && (c.now >= c.end_time || c.steps >= c.max_steps)) c.active = 0;
+  c.finished = c.now >= c.end_time;
+  if (!c.active) return false;
+  double raw;
+  if (scheme == FM_ACC) {
+    const double hmax = bitsd(r.hmax);
+    raw = hmax <= hdry ? INFINITY : courant * bitsd(r.dtmin) / sqrt(g * hmax);
+  } else {
+    raw = bitsd(r.dtmin) * courant;
+  }
+  double e = c.end_time;
+  if (c.out_int > 0.0) e = smin(e, c.next_out * c.out_int);
+  if (c.gauge_int > 0.0) e = smin(e, c.next_gauge * c.gauge_int);
+  const double gap = smax(e - c.now, 0.0);
+  double dt = smin(raw, gap);
+  if (!(dt > 0.0)) dt = smin(c.end_time, gap);
+  c.dt = dt;
+  c.t0 = c.now;
+  double added = 0.0;
+  for (int f = 0; f < ninflow; ++f) {
+    const double q = hydro_at(*hy, f, c.now);
+    if (q <= 0.0) {
+      c.on[f] = 0;
+      c.per_cell[f] = 0.0;
+      continue;
+    }
+    const double vol = q * dt;
+    c.on[f] = 1;
+    c.per_cell[f] = vol / double(hy->region[f]);
+    added += vol;
+  }
+  c.vol_in += added;
+  c.now += dt;
+  c.steps += 1;
+  c.dt_min = smin(c.dt_min, dt);
+  c.dt_max = smax(c.dt_max, dt);
+  c.had_step = 1;
+  c.finished = c.now >= c.end_time;
+  return true;
+}
+
+// Step head shared by the first kernel of every scheme: thread 0 of each
+// block evaluates decide_step; block 0 publishes clk[1] and clears the
+// reduction slot this step will accumulate into.
+__device__ __forceinline__ void step_head(const NuView& v, DevClock* clk, DevRed* red,
+                                          const Hydro* hy, int manual, double mdt, int& go,
+                                          double& dt) {
+  __shared__ int s_go;
+  __shared__ double s_dt;
+  if (threadIdx.x == 0) {
+    if (manual) {
+      s_go = 1;
+      s_dt = mdt;
+    } else {
+      const DevClock c0 = clk[0];
+      const int p = int(c0.steps & 1);
+      DevClock c;
+      const bool g = decide_step(c0, red[p], hy, v.scheme, v.courant, v.g, v.hdry, v.ninflow, c);
+      s_go = g ? 1 : 0;
+      s_dt = c.dt;
+      if (blockIdx.x == 0) {
+        clk[1] = c;
+        if (g) {
+          DevRed& nx = red[p ^ 1];
+          nx.dtmin = dbits(INFINITY);
+          nx.hmax = 0ull;
+          nx.badkey = ~0ull;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  go = s_go;
+  dt = s_dt;
+}
+
+// Next-step reductions over the freshly written state (fused epilogue).
+__device__ __forceinline__ void reduce_leaf(const NuView& v, DevRed* red, const DevClock& c,
+                                            const double s[9], double sz, unsigned long long key,
+                                            bool valid) {
+  double dtc = INFINITY, hm = 0.0;
+  unsigned long long bad = ~0ull;
+  if (valid) {
+    const double h = s[0];
+    if (v.scheme == FM_ACC) {
+      if (h > v.hdry) {
+        hm = h;
+        dtc = sz;
+      }
+    } else if (h > v.hdry) {
+      const double cw = sqrt(v.g * h);
+      const double sx = fabs(s[3] / h) + cw;
+      const double sy = fabs(s[6] / h) + cw;
+      dtc = sz / smax(sx, sy);
+    }
+    bool fin = true;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) fin = fin && isfinite(s[q]);
+    if (!fin) bad = key;
+  }
+  for (int o = 16; o; o >>= 1) {
+    dtc = smin(dtc, __shfl_xor_sync(0xffffffffu, dtc, o));
+    hm = smax(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+    const unsigned long long b2 = __shfl_xor_sync(0xffffffffu, bad, o);
+    bad = b2 < bad ? b2 : bad;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    DevRed& r = red[(c.steps) & 1];
+    if (dtc < INFINITY) atomicMin(&r.dtmin, dbits(dtc));
+    if (hm > 0.0) atomicMax(&r.hmax, dbits(hm));
+    if (bad != ~0ull) atomicMin(&r.badkey, bad);
+  }
+}
+
+// ---- step head: clock + friction (DG2/FV1) ------------------------------
+// src == dst for DG2; FV1 keeps its post-step state in U* (see k_stage) and
+// the head moves it back into U while applying friction.
+__global__ void __launch_bounds__(256) k_head_friction(NuView v, DevClock* clk, DevRed* red,
+                                                      const Hydro* hy, const double* src,
+                                                      double* dst, int manual, double mdt) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int go;
+  double dt;
+  step_head(v, clk, red, hy, manual, mdt, go, dt);
+  if (!go || k >= v.n) return;
+  double s[9];
+  load9(src, k, s);
+  friction(s, v.nman[k], v.g, v.hdry, dt);
+  double* o = dst + 9 * k;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) o[q] = s[q];
+}
+
+// ---- one RK stage over all leaves ---------------------------------------
+// STAGE 1: out = positivity(U + dt L(U))          -> U*  (FV1: the full step)
+// STAGE 2: out = positivity(((U* + dt L(U*)) + U) / 2) -> U (in place)
+template <int STAGE>
+__global__ void __launch_bounds__(128) k_stage(NuView v, const DevClock* __restrict__ clk,
+                                                DevRed* red, const double* __restrict__ in,
+                                                const double* uold, double* out, int last,
+                                                int manual, double mdt, int* err) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const DevClock* c = clk + 1;
+  if (!manual && !c->active) return;
+  const double dt = manual ? mdt : c->dt;
+  const bool valid = k < v.n;
+  double res[9];
+  double sz = 0.0;
+  unsigned long long key = 0;
+  if (valid) {
+    const int l = v.lvl[k], i = v.li[k], j = v.lj[k];
+    sz = lsize(v, l);
+    const double cx = lcen(v.x0, v, l, i), cy = lcen(v.y0, v, l, j);
+    key = leaf_key(l, i, j);
+    double s[9];
+    load9(in, k, s);
+    const P3 zc = load3(v.z, k);
+    const uint8_t code = v.sk[k];
+    Flx side_f[4];
+    double eh[4], eqx[4], eqy[4], ezd[4];
+#pragma unroll
+    for (int sd = 0; sd < 4; ++sd) {
+      const int kind = (code >> (2 * sd)) & 3;
+      const bool xn = sd == 1 || sd == 3;
+      const bool mine_left = sd == 0 || sd == 1;
+      const double fx = cx + (sd == 1 ? sz / 2 : sd == 3 ? -sz / 2 : 0.0);
+      const double fy = cy + (sd == 0 ? sz / 2 : sd == 2 ? -sz / 2 : 0.0);
+      const Pt me = limit(s, zc, cx, cy, sz, fx, fy, v.hdry);
+      Flx sf[2];
+      double szs[2], shm[2], sw[2];
+      const int nseg = kind == 0 ? 0 : kind == 3 ? 2 : 1;
+      for (int t = 0; t < nseg; ++t) {
+        const int q = v.nb[8 * k + 2 * sd + t];
+        const int ql = v.lvl[q];
+        const double qsz = lsize(v, ql);
+        const double qcx = lcen(v.x0, v, ql, v.li[q]), qcy = lcen(v.y0, v, ql, v.lj[q]);
+        // enumerate_faces (quadgrid.cpp:222-245): the owner (coarser leaf, or
+        // W/S leaf at equal level) fixes the normal coordinate from its own
+        // face; the tangential coordinate is the other leaf's centre.
+        const bool owner_me = kind == 3 || (kind == 2 && mine_left);
+        double segx, segy, len;
+        if (xn) {
+          segx = owner_me ? cx + (sd == 1 ? sz / 2 : -sz / 2) : qcx + (sd == 1 ? -qsz / 2 : qsz / 2);
+          segy = owner_me ? qcy : cy;
+        } else {
+          segy = owner_me ? cy + (sd == 0 ? sz / 2 : -sz / 2) : qcy + (sd == 0 ? -qsz / 2 : qsz / 2);
+          segx = owner_me ? qcx : cx;
+        }
+        len = owner_me ? smin(sz, qsz) : smin(qsz, sz);
+        const Pt pm = (segx == fx && segy == fy) ? me : limit(s, zc, cx, cy, sz, segx, segy, v.hdry);
+        double sq[9];
+        load9(in, q, sq);
+        const Pt pn = limit(sq, load3(v.z, q), qcx, qcy, qsz, segx, segy, v.hdry);
+        const Pt& A = mine_left ? pm : pn;
+        const Pt& B = mine_left ? pn : pm;
+        const double zs = smax(A.z, B.z);
+        const double hl = smax(0.0, A.eta - zs), hr = smax(0.0, B.eta - zs);
+        sf[t] = xn ? hll(hl, hl * A.u, hl * A.v, hr, hr * B.u, hr * B.v, v.g, v.hdry, err)
+                   : hll(hl, hl * A.v, hl * A.u, hr, hr * B.v, hr * B.u, v.g, v.hdry, err);
+        szs[t] = zs;
+        shm[t] = mine_left ? hl : hr;
+        sw[t] = len / sz;
+      }
+      double zstar;
+      if (kind == 0) {
+        zstar = me.z;
+      } else if (nseg == 1) {
+        zstar = szs[0];
+      } else if (v.zpair) {
+        zstar = smax(me.z, v.zpair[4 * k + sd]);
+      } else {
+        double acc = 0.0;
+        acc += sw[0] * szs[0];
+        acc += sw[1] * szs[1];
+        zstar = acc;
+      }
+      const double h = smax(0.0, me.eta - zstar);
+      eh[sd] = h;
+      eqx[sd] = h * me.u;
+      eqy[sd] = h * me.v;
+      ezd[sd] = zstar - smax(0.0, zstar - me.eta);
+      Flx acc{0.0, 0.0, 0.0};
+      if (kind == 0) {
+        const double qn = xn ? eqx[sd] : eqy[sd], qt = xn ? eqy[sd] : eqx[sd];
+        const double qg = v.bc[sd] == FM_REFLECTIVE ? -qn : qn;
+        const Flx f = mine_left ? hll(h, qn, qt, h, qg, qt, v.g, v.hdry, err)
+                                : hll(h, qg, qt, h, qn, qt, v.g, v.hdry, err);
+        acc.m += f.m;
+        acc.n += f.n;
+        acc.t += f.t;
+      } else {
+        for (int t = 0; t < nseg; ++t) {
+          const double corr = 0.5 * v.g * (h * h - shm[t] * shm[t]);
+          acc.m += sw[t] * sf[t].m;
+          acc.n += sw[t] * (sf[t].n + corr);
+          acc.t += sw[t] * sf[t].t;
+        }
+      }
+      side_f[sd] = acc;
+    }
+    const DirMod X{0.5 * (eh[1] + eh[3]),   (eh[1] - eh[3]) * kHalfInvS3,
+                   0.5 * (eqx[1] + eqx[3]), (eqx[1] - eqx[3]) * kHalfInvS3,
+                   0.5 * (eqy[1] + eqy[3]), (eqy[1] - eqy[3]) * kHalfInvS3,
+                   (ezd[1] - ezd[3]) * kHalfInvS3};
+    const DirMod Y{0.5 * (eh[0] + eh[2]),   (eh[0] - eh[2]) * kHalfInvS3,
+                   0.5 * (eqx[0] + eqx[2]), (eqx[0] - eqx[2]) * kHalfInvS3,
+                   0.5 * (eqy[0] + eqy[2]), (eqy[0] - eqy[2]) * kHalfInvS3,
+                   (ezd[0] - ezd[2]) * kHalfInvS3};
+    double Lr[9];
+    l_operator(side_f[0], side_f[1], side_f[2], side_f[3], X, Y, sz, v.g, v.hdry,
+               v.scheme == FM_DG2, Lr);
+    if (STAGE == 1) {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
+    } else {
+      double u0[9];
+      load9(uold, k, u0);
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        double a = s[q];
+        a += Lr[q] * dt;
+        a += u0[q];
+        a *= 0.5;
+        res[q] = a;
+      }
+    }
+    positivity(res, v.hdry);
+    if (last && !manual) {
+      // apply_inflows (solver_nonuniform.cpp:451-465), inflow order
+      for (int f = 0; f < v.ninflow; ++f) {
+        if (!c->on[f]) continue;
+        const int cnt = v.infc[f * v.n + k];
+        if (cnt) res[0] += c->per_cell[f] * cnt / (sz * sz);
+      }
+    }
+    double* o = out + 9 * k;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) o[q] = res[q];
+  }
+  if (last && !manual) reduce_leaf(v, red, *c, res, sz, key, valid);
+}
+
+// ---- ACC ------------------------------------------------------------------
+// Per interior segment (solver_nonuniform.cpp:354-371).  Also the step head.
+__global__ void __launch_bounds__(256) k_acc_faces(NuView v, DevClock* clk, DevRed* red,
+                                                  const Hydro* hy, const double* __restrict__ u,
+                                                  double* __restrict__ q, int manual, double mdt) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int go;
+  double dt;
+  step_head(v, clk, red, hy, manual, mdt, go, dt);
+  if (!go || s >= v.nseg) return;
+  const int l = v.seg_l[s], r = v.seg_r[s];
+  const double zl = v.z[3 * l], zr = v.z[3 * r];
+  const double el = u[9 * l] + zl, er = u[9 * r] + zr;
+  const double hf = smax(el, er) - smax(zl, zr);
+  double Q = q[s];
+  if (hf <= v.hdry) {
+    q[s] = 0.0;
+    return;
+  }
+  const double dist = 0.5 * (lsize(v, v.lvl[l]) + lsize(v, v.lvl[r]));
+  const double nf = 0.5 * (v.nman[l] + v.nman[r]);
+  Q = (Q - v.g * hf * dt * (er - el) / dist) /
+      (1.0 + v.g * dt * nf * nf * fabs(Q) / pow(hf, 7.0 / 3.0));
+  q[s] = Q;
+}
+
+// Per leaf: boundary discharges (:372-386), volume update and diagnostic
+// discharges (:387-417), then the fused inflow / finite / CFL epilogue.
+__global__ void __launch_bounds__(256) k_acc_leaves(NuView v, const DevClock* __restrict__ clk,
+                                                   DevRed* red, double* __restrict__ u,
+                                                   const double* __restrict__ q,
+                                                   double* __restrict__ qb, int manual, double mdt) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const DevClock* c = clk + 1;
+  if (!manual && !c->active) return;
+  const double dt = manual ? mdt : c->dt;
+  const bool valid = k < v.n;
+  double s[9];
+  double sz = 0.0;
+  unsigned long long key = 0;
+  if (valid) {
+    const int l = v.lvl[k];
+    sz = lsize(v, l);
+    key = leaf_key(l, v.li[k], v.lj[k]);
+    load9(u, k, s);
+    const uint8_t code = v.sk[k];
+    const double area = sz * sz;
+    double net = 0.0, sx = 0.0, sy = 0.0;
+#pragma unroll
+    for (int sd = 0; sd < 4; ++sd) {
+      const int kind = (code >> (2 * sd)) & 3;
+      const double sign = (sd == 1 || sd == 0) ? -1.0 : 1.0;
+      const int nseg = kind == 0 ? 1 : kind == 3 ? 2 : 1;
+      for (int t = 0; t < nseg; ++t) {
+        double Q, len;
+        if (kind == 0) {
+          double b = qb[4 * k + sd];
+          if (v.bc[sd] == FM_REFLECTIVE) {
+            b = 0.0;
+          } else {
+            const double hf = s[0];
+            if (hf <= v.hdry) {
+              b = 0.0;
+            } else {
+              const double nf = v.nman[k];
+              b = b / (1.0 + v.g * dt * nf * nf * fabs(b) / pow(hf, 7.0 / 3.0));
+            }
+          }
+          qb[4 * k + sd] = b;
+          Q = b;
+          len = sz;
+        } else {
+          const int id = v.sid[8 * k + 2 * sd + t];
+          Q = q[id];
+          const int oth = v.nb[8 * k + 2 * sd + t];
+          const double osz = lsize(v, v.lvl[oth]);
+          len = kind == 1 ? smin(osz, sz) : smin(sz, osz);
+        }
+        net += sign * Q * len;
+        if (sd == 1 || sd == 3)
+          sx += Q * len;
+        else
+          sy += Q * len;
+      }
+    }
+    s[0] += dt * net / area;
+    s[3] = 0.5 * sx / sz;
+    s[6] = 0.5 * sy / sz;
+    if (!manual) {
+      for (int f = 0; f < v.ninflow; ++f) {
+        if (!c->on[f]) continue;
+        const int cnt = v.infc[f * v.n + k];
+        if (cnt) s[0] += c->per_cell[f] * cnt / area;
+      }
+    }
+    u[9 * k] = s[0];
+    u[9 * k + 3] = s[3];
+    u[9 * k + 6] = s[6];
+  }
+  if (!manual) reduce_leaf(v, red, *c, s, sz, key, valid);
+}
+
+// Initial reduction (before the first step of a run) into slot steps&1.
+__global__ void k_reduce_init(NuView v, const DevClock* clk, DevRed* red, const double* __restrict__ u) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool valid = k < v.n;
+  double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double sz = 0.0;
+  unsigned long long key = 0;
+  if (valid) {
+    const int l = v.lvl[k];
+    sz = lsize(v, l);
+    key = leaf_key(l, v.li[k], v.lj[k]);
+    load9(u, k, s);
+  }
+  DevClock c = clk[0];
+  reduce_leaf(v, red, c, s, sz, key, valid);
+}
+
+// Close the last step of a run: the non-finite guard and event counters of
+// decide_step without starting a new step.
+__global__ void k_close(DevClock* clk, DevRed* red, const Hydro* hy, NuView v) {
+  DevClock c0 = clk[0];
+  c0.max_steps = c0.steps;  // forbid a new step
+  DevClock c;
+  decide_step(c0, red[c0.steps & 1], hy, v.scheme, v.courant, v.g, v.hdry, v.ninflow, c);
+  c.max_steps = clk[0].max_steps;
+  clk[0] = c;
+}
+
+__global__ void k_commit(DevClock* clk) {
+  // end of step: the in-flight state becomes the step-start state
+  clk[0] = clk[1];
+}
+
+// apply_inflows for the host API path.
+__global__ void k_inflow_add(NuView v, const double* per_cell, double* u) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= v.n) return;
+  const double sz = lsize(v, v.lvl[k]);
+  double h = u[9 * k];
+  for (int f = 0; f < v.ninflow; ++f) {
+    const double pc = per_cell[f];
+    if (pc == 0.0) continue;
+    const int cnt = v.infc[f * v.n + k];
+    if (cnt) h += pc * cnt / (sz * sz);
+  }
+  u[9 * k] = h;
+}
+
+inline unsigned nblk(long long n, int t) { return unsigned((n + t - 1) / t); }
+
+}  // namespace
+
+// ---- launch helpers used by sim.cu --------------------------------------------
+void nu_launch_step(Sim& s, bool manual, double mdt, int* err) {
+  cudaStream_t st = stream();
+  const NuView v = s.view();
+  DevClock* clk = s.clk.p;
+  DevRed* red = s.red.p;
+  const long long n = s.n;
+  if (s.scheme == FM_ACC) {
+    const long long ns = std::max<long long>(s.nseg, 1);
+    k_acc_faces<<<nblk(ns, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.u.p, s.accq.p, manual, mdt);
+    FM_LAUNCHED();
+    k_acc_leaves<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.u.p, s.accq.p, s.accqb.p, manual, mdt);
+    FM_LAUNCHED();
+  } else if (s.scheme == FM_FV1) {
+    // FV1 state lives in U* between steps; the head moves it to U with friction
+    k_head_friction<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.us.p, s.u.p, manual, mdt);
+    FM_LAUNCHED();
+    k_stage<1><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
+    FM_LAUNCHED();
+  } else {
+    k_head_friction<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.u.p, s.u.p, manual, mdt);
+    FM_LAUNCHED();
+    k_stage<1><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
+    FM_LAUNCHED();
+    k_stage<2><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+    FM_LAUNCHED();
+  }
+  if (!manual) {
+    k_commit<<<1, 1, 0, st>>>(clk);
+    FM_LAUNCHED();
+  }
+}
+
+void nu_launch_reduce_init(Sim& s) {
+  k_reduce_init<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.u.p);
+  FM_LAUNCHED();
+}
+
+void nu_launch_close(Sim& s) {
+  k_close<<<1, 1, 0, stream()>>>(s.clk.p, s.red.p, s.hydro.p, s.view());
+  FM_LAUNCHED();
+}
+
+void nu_launch_inflow_add(Sim& s, const double* per_cell_dev) {
+  k_inflow_add<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), per_cell_dev, s.u.p);
+  FM_LAUNCHED();
+}
+
+}  // namespace fmh

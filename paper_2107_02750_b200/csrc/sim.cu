@@ -1,0 +1,618 @@
+// Host side of the device simulations: construction (make_nonuniform_sim,
+// solver_nonuniform.cpp:558-636), the drive<Sim> member functions
+// (run.cpp:35-141) and the device-resident step loop captured in a CUDA graph.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "fm_device.cuh"
+#include "fm_sim.hpp"
+
+using namespace fmd;
+
+namespace fmh {
+
+void nu_launch_step(Sim& s, bool manual, double mdt, int* err);
+void nu_launch_reduce_init(Sim& s);
+void nu_launch_close(Sim& s);
+void nu_launch_inflow_add(Sim& s, const double* per_cell_dev);
+// uniform.cu
+void un_launch_step(Sim& s, bool manual, double mdt, int* err);
+void un_launch_reduce_init(Sim& s);
+// adaptive.cu
+struct AdaptState;
+void adaptive_destroy(AdaptState* a);
+
+namespace {
+
+inline unsigned nblk(long long n, int t) { return unsigned((n + t - 1) / t); }
+
+__device__ __forceinline__ double lsz(int L, double R, int l) { return R * double(1 << (L - l)); }
+
+// restrict_flow_to_leaves (solver_nonuniform.cpp:529-556) for an h-only fine
+// field: leaf k takes the level-l scaling of its node.
+__global__ void k_ic_restrict(long long n, int M, const int8_t* __restrict__ lvl,
+                              const int32_t* __restrict__ li, const int32_t* __restrict__ lj,
+                              const double* const* __restrict__ sc, double* __restrict__ u) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int l = lvl[k];
+  const uint64_t node = node_index(l, li[k], lj[k], M);
+  const double* p = sc[l] + 3 * node;
+  double* o = u + 9 * k;
+  o[0] = p[0];
+  o[1] = p[1];
+  o[2] = p[2];
+#pragma unroll
+  for (int q = 3; q < 9; ++q) o[q] = 0.0;
+}
+
+// flow_from_surface (solver_uniform.cpp:60-71) / uniform initial depth.
+__global__ void k_ic_simple(long long n, const double* __restrict__ z, int mode, double val,
+                            double* __restrict__ u) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double f[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (mode == 1) {
+    const double c0 = z[3 * k], cx = z[3 * k + 1], cy = z[3 * k + 2];
+    const double span = kS3 * (fabs(cx) + fabs(cy));
+    if (c0 + span < val) {
+      f[0] = val - c0;
+      f[1] = -cx;
+      f[2] = -cy;
+    } else if (c0 - span >= val) {
+    } else {
+      f[0] = smax(0.0, val - c0);
+    }
+  } else if (mode == 2) {
+    f[0] = val;
+  }
+  double* o = u + 9 * k;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) o[q] = f[q];
+}
+
+// Piecewise-constant schemes drop slopes (solver_nonuniform.cpp:600-607),
+// then positivity (:608).
+__global__ void k_ic_finish(long long n, int pc, double hdry, double* __restrict__ z,
+                            double* __restrict__ u) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double f[9];
+  for (int q = 0; q < 9; ++q) f[q] = u[9 * k + q];
+  if (pc) {
+    z[3 * k + 1] = 0.0;
+    z[3 * k + 2] = 0.0;
+    f[1] = f[2] = 0.0;
+    for (int q = 3; q < 9; ++q) f[q] = 0.0;
+  }
+  positivity(f, hdry);
+  for (int q = 0; q < 9; ++q) u[9 * k + q] = f[q];
+}
+
+__global__ void k_finite(long long n, const int8_t* __restrict__ lvl, const int32_t* __restrict__ li,
+                         const int32_t* __restrict__ lj, const double* __restrict__ u,
+                         unsigned long long* bad) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  bool fin = true;
+  for (int q = 0; q < 9; ++q) fin = fin && isfinite(u[9 * k + q]);
+  if (!fin) {
+    const unsigned long long key = (static_cast<unsigned long long>(lvl ? lvl[k] : 0) << 58) |
+                                   (static_cast<unsigned long long>(lj[k]) << 29) |
+                                   static_cast<unsigned long long>(li[k]);
+    atomicMin(bad, key);
+  }
+}
+
+}  // namespace
+
+Sim::~Sim() {
+  if (graph) cudaGraphExecDestroy(graph);
+  if (ad) adaptive_destroy(ad);
+}
+
+NuView Sim::view() const {
+  NuView v{};
+  v.L = L;
+  v.M = M;
+  v.N = N;
+  v.scheme = scheme;
+  v.adaptive = adaptive ? 1 : 0;
+  v.ninflow = ninflow;
+  v.R = R;
+  v.x0 = x0;
+  v.y0 = y0;
+  v.g = g;
+  v.hdry = hdry;
+  v.courant = courant;
+  for (int q = 0; q < 4; ++q) v.bc[q] = bc[q];
+  v.n = n;
+  v.lvl = lvl.p;
+  v.li = li.p;
+  v.lj = lj.p;
+  v.z = z.p;
+  v.nman = nman.p;
+  v.nb = nb.p;
+  v.sk = sk.p;
+  v.zpair = zpair.n ? zpair.p : nullptr;
+  v.infc = infc.p;
+  v.seg_l = seg_l.p;
+  v.seg_r = seg_r.p;
+  v.sid = sid.p;
+  v.nseg = nseg;
+  return v;
+}
+
+namespace {
+
+double courant_for(const fm_sim_desc* d) {  // config.cpp:37-47
+  if (d->courant > 0.0) return d->courant;
+  switch (d->solver) {
+    case FM_DG2:
+    case FM_MWDG2: return 0.33;
+    case FM_FV1:
+    case FM_HWFV1: return 0.5;
+    case FM_ACC: return 0.7;
+  }
+  return 0.33;
+}
+
+void common_params(Sim& s, const fm_sim_desc* d) {
+  if (d->solver < FM_DG2 || d->solver > FM_HWFV1) throw Error(FM_ERR_CONFIG, "unknown solver");
+  s.solver = d->solver;
+  s.scheme = d->solver == FM_MWDG2 ? FM_DG2 : d->solver == FM_HWFV1 ? FM_FV1 : d->solver;
+  s.g = d->g;
+  s.hdry = d->h_dry;
+  s.courant = courant_for(d);
+  for (int q = 0; q < 4; ++q) s.bc[q] = d->bc[q];
+  s.manning = d->manning;
+  if (d->manning_raster) {
+    const fm_raster* m = d->manning_raster;
+    s.has_mr = true;
+    s.mr_ncols = m->ncols;
+    s.mr_nrows = m->nrows;
+    s.mr_xll = m->xll;
+    s.mr_yll = m->yll;
+    s.mr_cs = m->cellsize;
+    if (m->on_device) {
+      s.mr.alloc(size_t(m->ncols) * m->nrows);
+      FM_CUDA(cudaMemcpyAsync(s.mr.p, m->values, s.mr.n * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+    } else {
+      s.mr.upload(m->values, size_t(m->ncols) * m->nrows);
+    }
+  }
+  // inflows (config.cpp:168-186; hydrograph.cpp:10-36 validation)
+  if (d->n_inflows > kMaxInflows) throw Error(FM_ERR_CONFIG, "too many inflows");
+  s.ninflow = d->n_inflows;
+  Hydro h{};
+  int at = 0;
+  for (int f = 0; f < d->n_inflows; ++f) {
+    const fm_inflow& in = d->inflows[f];
+    if (in.nsamples < 1) throw Error(FM_ERR_IO, "hydrograph has no samples");
+    if (at + in.nsamples > kMaxHydroSamples) throw Error(FM_ERR_CONFIG, "hydrograph too long");
+    if (in.i0 > in.i1 || in.j0 > in.j1)
+      throw Error(FM_ERR_CONFIG, "inflow: cell range must satisfy i0 <= i1 and j0 <= j1");
+    h.off[f] = at;
+    for (int k = 0; k < in.nsamples; ++k) {
+      if (k && !(in.t[k] > in.t[k - 1])) throw Error(FM_ERR_IO, "hydrograph times must be strictly increasing");
+      if (in.q[k] < 0.0) throw Error(FM_ERR_IO, "hydrograph has a negative discharge");
+      h.t[at + k] = in.t[k];
+      h.q[at + k] = in.q[k];
+    }
+    at += in.nsamples;
+    h.region[f] = (long long)(in.i1 - in.i0 + 1) * (in.j1 - in.j0 + 1);
+    s.region.push_back(h.region[f]);
+    s.rect.insert(s.rect.end(), {in.i0, in.j0, in.i1, in.j1});
+    s.hy_t.emplace_back(in.t, in.t + in.nsamples);
+    s.hy_q.emplace_back(in.q, in.q + in.nsamples);
+  }
+  h.off[d->n_inflows] = at;
+  h.n = d->n_inflows;
+  s.hydro.upload(&h, 1);
+  s.clk.alloc(2);
+  s.red.alloc(2);
+}
+
+}  // namespace
+
+// Static non-uniform sim from a device grid (solver_nonuniform.cpp:558-636).
+static void nonuniform_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem, const Grid& g) {
+  cudaStream_t st = stream();
+  s.L = g.L;
+  s.M = g.M;
+  s.N = g.N;
+  s.R = g.R;
+  s.x0 = g.x0;
+  s.y0 = g.y0;
+  s.n = g.nleaves;
+  const long long n = s.n;
+  s.lvl.alloc(n);
+  s.li.alloc(n);
+  s.lj.alloc(n);
+  s.z.alloc(3 * n);
+  FM_CUDA(cudaMemcpyAsync(s.lvl.p, g.lf_l.p, n, cudaMemcpyDeviceToDevice, st));
+  FM_CUDA(cudaMemcpyAsync(s.li.p, g.lf_i.p, 4 * n, cudaMemcpyDeviceToDevice, st));
+  FM_CUDA(cudaMemcpyAsync(s.lj.p, g.lf_j.p, 4 * n, cudaMemcpyDeviceToDevice, st));
+  FM_CUDA(cudaMemcpyAsync(s.z.p, g.lf_z.p, 24 * n, cudaMemcpyDeviceToDevice, st));
+  build_topology(s, g);  // throws StructureError when not graded (is_graded, :566-567)
+  s.nman.alloc(n);
+  resolve_manning(s);
+  s.u.alloc(9 * n);
+  s.us.alloc(9 * n);
+  if (d->initial_depth_raster) {
+    const fm_raster* hr = d->initial_depth_raster;
+    if (hr->ncols != dem->ncols || hr->nrows != dem->nrows)
+      throw Error(FM_ERR_CONFIG, "initial_depth_raster geometry must match the DEM");
+    DBuf<double> fine;
+    project_planes(hr, s.L, s.M, s.N, fine);
+    std::vector<DBuf<double>> sc;
+    scaling_pyramid(std::move(fine), s.L, s.M, s.N, FM_MW, sc);
+    std::vector<const double*> ptrs(s.L + 1);
+    for (int l = 0; l <= s.L; ++l) ptrs[l] = sc[l].p;
+    DBuf<const double*> dptrs;
+    dptrs.upload(ptrs.data(), ptrs.size());
+    k_ic_restrict<<<nblk(n, 256), 256, 0, st>>>(n, s.M, s.lvl.p, s.li.p, s.lj.p, dptrs.p, s.u.p);
+    FM_LAUNCHED();
+    FM_CUDA(cudaStreamSynchronize(st));
+  } else {
+    const int mode = d->has_initial_surface ? 1 : d->initial_depth > 0.0 ? 2 : 0;
+    k_ic_simple<<<nblk(n, 256), 256, 0, st>>>(n, s.z.p, mode,
+                                               mode == 1 ? d->initial_surface : d->initial_depth, s.u.p);
+    FM_LAUNCHED();
+  }
+  k_ic_finish<<<nblk(n, 256), 256, 0, st>>>(n, s.scheme != FM_DG2, s.hdry, s.z.p, s.u.p);
+  FM_LAUNCHED();
+  for (int f = 0; f < s.ninflow; ++f) {
+    const int* r = &s.rect[4 * f];
+    if (r[0] < 0 || r[1] < 0 || r[2] >= (s.M << s.L) || r[3] >= (s.N << s.L))
+      throw Error(FM_ERR_CONFIG, "inflow region outside the domain");
+  }
+  resolve_inflows(s, g);
+  if (s.scheme == FM_ACC) {
+    s.accq.alloc(std::max<int64_t>(s.nseg, 1));
+    s.accq.zero();
+    s.accqb.alloc(4 * n);
+    s.accqb.zero();
+  }
+}
+
+Sim* sim_create(const fm_sim_desc* d, const fm_raster* dem, const Grid* grid) {
+  if (!d || !dem) throw Error(FM_ERR_CONFIG, "null descriptor or DEM");
+  upload_banks();
+  auto s = std::make_unique<Sim>();
+  common_params(*s, d);
+  if (d->solver == FM_MWDG2 || d->solver == FM_HWFV1) {
+    s->adaptive = true;
+    adaptive_init(*s, d, dem);
+  } else if (grid) {
+    nonuniform_init(*s, d, dem, *grid);
+  } else {
+    s->uniform = true;
+    uniform_init(*s, d, dem);
+  }
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  return s.release();
+}
+
+namespace {
+
+// FV1 keeps its post-step state in U* while the device loop runs.
+void fv1_to_u(Sim& s) {
+  if (s.fv1_in_star) {
+    FM_CUDA(cudaMemcpyAsync(s.u.p, s.us.p, s.u.n * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+    s.fv1_in_star = false;
+  }
+}
+void fv1_to_star(Sim& s) {
+  if (!s.fv1_in_star) {
+    FM_CUDA(cudaMemcpyAsync(s.us.p, s.u.p, s.u.n * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+    s.fv1_in_star = true;
+  }
+}
+bool fv1_staged(const Sim& s) { return !s.uniform && s.scheme == FM_FV1; }
+
+void init_red(Sim& s) {
+  DevRed r[2];
+  for (auto& x : r) {
+    double inf = std::numeric_limits<double>::infinity();
+    std::memcpy(&x.dtmin, &inf, 8);
+    x.hmax = 0;
+    x.badkey = ~0ull;
+    x.pad = 0;
+  }
+  s.red.upload(r, 2);
+}
+
+void launch_step(Sim& s, bool manual, double mdt, int* err) {
+  if (s.uniform)
+    un_launch_step(s, manual, mdt, err);
+  else
+    nu_launch_step(s, manual, mdt, err);
+}
+void launch_reduce_init(Sim& s) {
+  if (s.uniform)
+    un_launch_reduce_init(s);
+  else
+    nu_launch_reduce_init(s);
+}
+
+DevClock fresh_clock(const fm_clock* c, int64_t max_steps, int stop) {
+  DevClock d{};
+  d.end_time = c->end_time;
+  d.out_int = c->output_interval;
+  d.gauge_int = c->gauge_interval;
+  d.now = c->now;
+  d.next_out = c->next_output;
+  d.next_gauge = c->next_gauge;
+  d.max_steps = max_steps;
+  d.active = 1;
+  d.stop_at_events = stop;
+  d.dt_min = std::numeric_limits<double>::infinity();
+  d.dt_max = 0.0;
+  d.bad_key = ~0ull;
+  return d;
+}
+
+void key_xy(const Sim& s, unsigned long long key, double* bx, double* by) {
+  const int l = int(key >> 58), j = int((key >> 29) & ((1u << 29) - 1)), i = int(key & ((1u << 29) - 1));
+  if (s.uniform) {
+    if (bx) *bx = s.x0 + (i + 0.5) * s.R;
+    if (by) *by = s.y0 + (j + 0.5) * s.R;
+  } else {
+    if (bx) *bx = s.x0 + (i + 0.5) * s.R * double(1 << (s.L - l));
+    if (by) *by = s.y0 + (j + 0.5) * s.R * double(1 << (s.L - l));
+  }
+}
+
+}  // namespace
+
+double sim_compute_dt(Sim& s) {
+  if (fv1_staged(s)) fv1_to_u(s);
+  init_red(s);
+  DevClock c{};
+  s.clk.upload(&c, 1);  // steps = 0 -> slot 0
+  launch_reduce_init(s);
+  DevRed r[2];
+  s.red.download(r, 2);
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  double v;
+  std::memcpy(&v, &r[0].dtmin, 8);
+  if (s.scheme == FM_ACC) {
+    double hmax;
+    std::memcpy(&hmax, &r[0].hmax, 8);
+    if (hmax <= s.hdry) return std::numeric_limits<double>::infinity();
+    if (s.uniform) return s.courant * s.R / std::sqrt(s.g * hmax);
+    return s.courant * v / std::sqrt(s.g * hmax);
+  }
+  return v * s.courant;
+}
+
+void sim_step(Sim& s, double dt) {
+  DBuf<int> err(1);
+  err.zero();
+  if (fv1_staged(s)) fv1_to_star(s);
+  launch_step(s, true, dt, err.p);
+  int h = 0;
+  err.download(&h, 1);
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  if (h) throw Error(FM_ERR_DOMAIN, "hll_flux: negative depth");
+  if (fv1_staged(s)) s.fv1_in_star = true;
+  if (s.adaptive) s.since_adapt += 1;
+}
+
+// hydrograph_at (hydrograph.cpp:38-49) on the host for the API path.
+static double hydro_host(const std::vector<double>& t, const std::vector<double>& q, double x) {
+  if (x <= t.front()) return q.front();
+  if (x >= t.back()) return q.back();
+  const size_t hi = size_t(std::upper_bound(t.begin(), t.end(), x) - t.begin());
+  const size_t lo = hi - 1;
+  if (x == t[lo]) return q[lo];
+  const double w = (x - t[lo]) / (t[hi] - t[lo]);
+  return q[lo] + w * (q[hi] - q[lo]);
+}
+
+double sim_apply_inflows(Sim& s, double t, double dt) {
+  if (fv1_staged(s)) fv1_to_u(s);
+  double added = 0.0;
+  double per[kMaxInflows] = {0};
+  for (int f = 0; f < s.ninflow; ++f) {
+    const double q = hydro_host(s.hy_t[f], s.hy_q[f], t);
+    if (q <= 0.0) continue;
+    const double vol = q * dt;
+    per[f] = vol / double(s.region[f]);
+    added += vol;
+  }
+  if (s.uniform) throw Error(FM_ERR_OTHER, "uniform inflows: use fm_sim_run");
+  DBuf<double> dper;
+  dper.upload(per, kMaxInflows);
+  nu_launch_inflow_add(s, dper.p);
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  return added;
+}
+
+double sim_volume(Sim& s) {
+  // Kahan in reference order (solver_nonuniform.cpp:467-477) over downloaded h.
+  std::vector<double> u9(9 * s.n);
+  std::vector<int32_t> l(s.n), i(s.n), j(s.n);
+  sim_download(s, l.data(), i.data(), j.data(), u9.data(), nullptr);
+  double sum = 0.0, comp = 0.0;
+  for (int64_t c = 0; c < s.n; ++c) {
+    const double sz = s.uniform ? s.R : s.R * double(1 << (s.L - l[c]));
+    const double y = s.uniform ? u9[9 * c] * s.R * s.R - comp : u9[9 * c] * sz * sz - comp;
+    const double t = sum + y;
+    comp = (t - sum) - y;
+    sum = t;
+  }
+  return sum;
+}
+
+bool sim_finite(Sim& s, double* bx, double* by) {
+  if (fv1_staged(s)) fv1_to_u(s);
+  DBuf<unsigned long long> bad(1);
+  bad.fill_bytes(0xff);
+  k_finite<<<nblk(s.n, 256), 256, 0, stream()>>>(s.n, s.uniform ? nullptr : s.lvl.p, s.li.p, s.lj.p, s.u.p, bad.p);
+  FM_LAUNCHED();
+  unsigned long long key = 0;
+  bad.download(&key, 1);
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  if (key == ~0ull) return true;
+  key_xy(s, key, bx, by);
+  return false;
+}
+
+// Reference order: (level, j, i) for leaves (quadgrid.cpp:94-98), j*nx+i for rasters.
+static std::vector<int64_t> sim_order(Sim& s, std::vector<int8_t>& l, std::vector<int32_t>& i,
+                                      std::vector<int32_t>& j) {
+  i = s.li.to_host();
+  j = s.lj.to_host();
+  if (s.uniform) {
+    l.assign(s.n, 0);
+  } else {
+    l = s.lvl.to_host();
+  }
+  std::vector<int64_t> perm(s.n);
+  for (int64_t k = 0; k < s.n; ++k) perm[k] = k;
+  std::sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) {
+    if (l[a] != l[b]) return l[a] < l[b];
+    if (j[a] != j[b]) return j[a] < j[b];
+    return i[a] < i[b];
+  });
+  return perm;
+}
+
+void sim_download(Sim& s, int32_t* lo, int32_t* io, int32_t* jo, double* u9, double* z3) {
+  if (fv1_staged(s)) fv1_to_u(s);
+  std::vector<int8_t> l;
+  std::vector<int32_t> i, j;
+  const std::vector<int64_t> perm = sim_order(s, l, i, j);
+  std::vector<double> u = u9 ? s.u.to_host() : std::vector<double>();
+  std::vector<double> z = z3 ? s.z.to_host() : std::vector<double>();
+  for (int64_t r = 0; r < s.n; ++r) {
+    const int64_t k = perm[r];
+    if (lo) lo[r] = l[k];
+    if (io) io[r] = i[k];
+    if (jo) jo[r] = j[k];
+    if (u9) std::memcpy(u9 + 9 * r, &u[9 * k], 72);
+    if (z3) std::memcpy(z3 + 3 * r, &z[3 * k], 24);
+  }
+}
+
+void sim_upload(Sim& s, const double* u9) {
+  if (fv1_staged(s)) fv1_to_u(s);
+  std::vector<int8_t> l;
+  std::vector<int32_t> i, j;
+  const std::vector<int64_t> perm = sim_order(s, l, i, j);
+  std::vector<double> u(9 * s.n);
+  for (int64_t r = 0; r < s.n; ++r) std::memcpy(&u[9 * perm[r]], u9 + 9 * r, 72);
+  s.u.upload(u.data(), u.size());
+  FM_CUDA(cudaStreamSynchronize(stream()));
+}
+
+void sim_adapt(Sim& s, double t) {
+  if (!s.adaptive) throw Error(FM_ERR_CONFIG, "adapt: not an adaptive simulation");
+  if (fv1_staged(s)) fv1_to_u(s);
+  adaptive_adapt(s, t);
+  s.since_adapt = 0;
+}
+
+// The drive loop (run.cpp:80-111) on the device.  Static sims replay a CUDA
+// graph of kBatch steps; each step's head kernel decides on the device
+// whether to run (end time, step budget, events, blow-up), so surplus steps
+// of the last batch are no-ops and the host syncs once per batch.
+void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run_result* out) {
+  cudaStream_t st = stream();
+  if (fv1_staged(s)) fv1_to_star(s);
+  DevClock c0 = fresh_clock(ck, max_steps, stop_at_events);
+  DevClock pair[2] = {c0, c0};
+  s.clk.upload(pair, 2);
+  init_red(s);
+  launch_reduce_init(s);
+  DBuf<int>& err = s.errflag;
+  err.alloc(1);
+  err.zero();
+  cudaEvent_t e0, e1;
+  FM_CUDA(cudaEventCreate(&e0));
+  FM_CUDA(cudaEventCreate(&e1));
+  FM_CUDA(cudaEventRecord(e0, st));
+  if (s.adaptive) {
+    // adapt between steps on the host-driven path (device kernels, host sequencing)
+    for (int64_t k = 0; k < max_steps; ++k) {
+      launch_step(s, false, 0.0, err.p);
+      DevClock c;
+      s.clk.download(&c, 1);
+      FM_CUDA(cudaStreamSynchronize(st));
+      if (!c.active || !c.had_step) break;
+      s.since_adapt += 1;
+      if (s.since_adapt >= s.adapt_every && !(c.now >= c.end_time)) {
+        adaptive_adapt(s, c.now);
+        s.since_adapt = 0;
+        // the adapt changed the leaf set: refresh the step's reductions
+        DevRed r[2];
+        s.red.download(r, 2);
+        FM_CUDA(cudaStreamSynchronize(st));
+        const int p = int(c.steps & 1);
+        double inf = std::numeric_limits<double>::infinity();
+        std::memcpy(&r[p].dtmin, &inf, 8);
+        r[p].hmax = 0;
+        r[p].badkey = ~0ull;
+        s.red.upload(r, 2);
+        launch_reduce_init(s);
+      }
+    }
+  } else {
+    constexpr int kBatch = 32;
+    const int64_t before = launches();
+    if (!s.graph) {
+      cudaGraph_t gr;
+      FM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      for (int k = 0; k < kBatch; ++k) launch_step(s, false, 0.0, err.p);
+      FM_CUDA(cudaStreamEndCapture(st, &gr));
+      FM_CUDA(cudaGraphInstantiate(&s.graph, gr, 0));
+      cudaGraphDestroy(gr);
+      s.graph_steps = kBatch;
+    }
+    const int64_t per_graph = launches() - before;
+    int64_t done = 0;
+    while (done < max_steps) {
+      FM_CUDA(cudaGraphLaunch(s.graph, st));
+      count_graph_launches(per_graph ? per_graph : 0);
+      done += s.graph_steps;
+      if (done < max_steps) {
+        DevClock c;
+        s.clk.download(&c, 1);
+        FM_CUDA(cudaStreamSynchronize(st));
+        if (!c.active) break;
+      }
+    }
+  }
+  FM_CUDA(cudaEventRecord(e1, st));
+  nu_launch_close(s);
+  DevClock c;
+  s.clk.download(&c, 1);
+  int herr = 0;
+  err.download(&herr, 1);
+  FM_CUDA(cudaStreamSynchronize(st));
+  s.last_run_ms = elapsed_ms(e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (herr) throw Error(FM_ERR_DOMAIN, "hll_flux: negative depth");
+  ck->now = c.now;
+  ck->next_output = c.next_out;
+  ck->next_gauge = c.next_gauge;
+  fm_run_result r{};
+  r.steps = c.steps;
+  r.dt_min = c.dt_min;
+  r.dt_max = c.dt_max;
+  r.volume_inflow = c.vol_in;
+  r.blew_up = c.blew_up;
+  r.blow_up_time = c.blow_t;
+  r.finished = c.now >= c.end_time;
+  r.event_due = c.event_due;
+  if (c.blew_up) key_xy(s, c.bad_key, &r.bad_x, &r.bad_y);
+  if (out) *out = r;
+  if (c.blew_up) throw Error(FM_ERR_BLOWUP, "solver state is non-finite");
+}
+
+}  // namespace fmh

@@ -1,0 +1,317 @@
+// Device topology of a graded leaf set.
+//
+// Replaces neighbors / is_graded / enumerate_faces (quadgrid.cpp:121-260)
+// and the inflow / Manning resolution of make_nonuniform_sim
+// (solver_nonuniform.cpp:575-584, 611-628).  Instead of hash probes, every
+// query is an O(1) look-up in the dense flag pyramid: a level-l node exists
+// iff its parent is flagged, it is a leaf iff it exists and is unflagged, and
+// its leaf index is off[l][node] (or off[L-1][parent] + k at level L).
+//
+// Per leaf and side the result is a 2-bit kind (0 boundary, 1 one coarser
+// neighbour, 2 one same-level neighbour, 3 two finer neighbours) and up to two
+// neighbour indices ordered south-to-north / west-to-east, which is the order
+// enumerate_faces sorts each side's segment list in (quadgrid.cpp:250-258).
+// Segments (needed by ACC's persistent face discharges) are owned by the
+// coarser leaf, or by the west/south leaf at equal level, exactly as in
+// enumerate_faces (quadgrid.cpp:206-208).
+#include "fm_device.cuh"
+#include "fm_sim.hpp"
+
+using namespace fmd;
+
+namespace fmh {
+
+namespace {
+
+struct TopoIn {
+  const uint8_t* flag[16];
+  const int32_t* off[16];
+  int L, M, N;
+};
+
+__device__ __forceinline__ int32_t leaf_index(const TopoIn& t, int l, uint64_t n) {
+  if (t.L == 0) return int32_t(n);
+  if (l < t.L) return t.off[l][n];
+  return t.off[t.L - 1][n >> 2] + int32_t(n & 3);
+}
+__device__ __forceinline__ bool is_flagged(const TopoIn& t, int l, uint64_t n) {
+  return l < t.L && t.flag[l][n] != 0;
+}
+
+__global__ void k_topo(TopoIn t, long long n, const int8_t* __restrict__ lvl,
+                       const int32_t* __restrict__ li, const int32_t* __restrict__ lj,
+                       int32_t* __restrict__ nb, uint8_t* __restrict__ sk,
+                       int32_t* __restrict__ owned, int* err) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int l = lvl[k], i = li[k], j = lj[k];
+  const int w = t.M << l, h = t.N << l;
+  uint8_t code = 0;
+  int own = 0;
+#pragma unroll
+  for (int sd = 0; sd < 4; ++sd) {
+    const int di = sd == 1 ? 1 : sd == 3 ? -1 : 0;
+    const int dj = sd == 0 ? 1 : sd == 2 ? -1 : 0;
+    const int ni = i + di, nj = j + dj;
+    int kind = 0, a = -1, b = -1;
+    if (ni >= 0 && nj >= 0 && ni < w && nj < h) {
+      const bool exists = l == 0 || is_flagged(t, l - 1, node_index(l - 1, ni >> 1, nj >> 1, t.M));
+      if (exists) {
+        const uint64_t q = node_index(l, ni, nj, t.M);
+        if (!is_flagged(t, l, q)) {
+          kind = 2;
+          a = leaf_index(t, l, q);
+        } else {
+          kind = 3;
+          int c0i, c0j, c1i, c1j;
+          if (sd == 1 || sd == 3) {
+            c0i = c1i = 2 * ni + (sd == 3 ? 1 : 0);
+            c0j = 2 * nj;
+            c1j = 2 * nj + 1;
+          } else {
+            c0j = c1j = 2 * nj + (sd == 2 ? 1 : 0);
+            c0i = 2 * ni;
+            c1i = 2 * ni + 1;
+          }
+          const uint64_t q0 = node_index(l + 1, c0i, c0j, t.M), q1 = node_index(l + 1, c1i, c1j, t.M);
+          if (is_flagged(t, l + 1, q0) || is_flagged(t, l + 1, q1)) atomicOr(err, 1);
+          a = leaf_index(t, l + 1, q0);
+          b = leaf_index(t, l + 1, q1);
+        }
+      } else {
+        // coarser: the level-(l-1) ancestor must exist (2:1 grading)
+        const int la = l - 1;
+        const bool up = la == 0 || is_flagged(t, la - 1, node_index(la - 1, ni >> 2, nj >> 2, t.M));
+        if (!up) atomicOr(err, 1);
+        kind = 1;
+        a = leaf_index(t, la, node_index(la, ni >> 1, nj >> 1, t.M));
+      }
+    }
+    nb[8 * k + 2 * sd] = a;
+    nb[8 * k + 2 * sd + 1] = b;
+    code |= uint8_t(kind << (2 * sd));
+    own += kind == 3 ? 2 : (kind == 2 && (sd == 0 || sd == 1)) ? 1 : 0;
+  }
+  sk[k] = code;
+  owned[k] = own;
+}
+
+__device__ __forceinline__ int owned_on(uint8_t code, int sd) {
+  const int kind = (code >> (2 * sd)) & 3;
+  return kind == 3 ? 2 : (kind == 2 && (sd == 0 || sd == 1)) ? 1 : 0;
+}
+__device__ __forceinline__ int owned_before(uint8_t code, int sd) {
+  int s = 0;
+  for (int q = 0; q < sd; ++q) s += owned_on(code, q);
+  return s;
+}
+
+// Segment ids per leaf side + the owned segments' (left, right) leaves.
+__global__ void k_segments(long long n, const int32_t* __restrict__ li,
+                           const int32_t* __restrict__ lj, const int32_t* __restrict__ nb,
+                           const uint8_t* __restrict__ sk, const int32_t* __restrict__ base,
+                           int32_t* __restrict__ sid, int32_t* __restrict__ seg_l,
+                           int32_t* __restrict__ seg_r) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint8_t code = sk[k];
+  for (int sd = 0; sd < 4; ++sd) {
+    const int kind = (code >> (2 * sd)) & 3;
+    int a = -1, b = -1;
+    const int32_t n0 = nb[8 * k + 2 * sd], n1 = nb[8 * k + 2 * sd + 1];
+    const bool mine_left = sd == 0 || sd == 1;
+    if (kind == 3 || (kind == 2 && mine_left)) {
+      const int32_t s0 = base[k] + owned_before(code, sd);
+      a = s0;
+      seg_l[s0] = mine_left ? int32_t(k) : n0;
+      seg_r[s0] = mine_left ? n0 : int32_t(k);
+      if (kind == 3) {
+        b = s0 + 1;
+        seg_l[s0 + 1] = mine_left ? int32_t(k) : n1;
+        seg_r[s0 + 1] = mine_left ? n1 : int32_t(k);
+      }
+    } else if (kind == 2) {
+      const int opp = (sd + 2) & 3;
+      a = base[n0] + owned_before(sk[n0], opp);
+    } else if (kind == 1) {
+      const int opp = (sd + 2) & 3;
+      const int t = (sd == 1 || sd == 3) ? (lj[k] & 1) : (li[k] & 1);
+      a = base[n0] + owned_before(sk[n0], opp) + t;
+    }
+    sid[8 * k + 2 * sd] = a;
+    sid[8 * k + 2 * sd + 1] = b;
+  }
+}
+
+// --- scan -----------------------------------------------------------------
+__global__ void k_block_sums(const int32_t* __restrict__ in, long long n,
+                             long long* __restrict__ sums) {
+  __shared__ long long s[32];
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long v = k < n ? in[k] : 0;
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    long long x = threadIdx.x < (blockDim.x >> 5) ? s[threadIdx.x] : 0;
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (threadIdx.x == 0) sums[blockIdx.x] = x;
+  }
+}
+__global__ void k_scan_sums(long long* sums, long long nb, long long* total) {
+  __shared__ long long part[1024];
+  __shared__ long long base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (long long b0 = 0; b0 < nb; b0 += blockDim.x) {
+    const long long k = b0 + threadIdx.x;
+    const long long v = k < nb ? sums[k] : 0;
+    part[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < int(blockDim.x); o <<= 1) {
+      const long long add = threadIdx.x >= unsigned(o) ? part[threadIdx.x - o] : 0;
+      __syncthreads();
+      part[threadIdx.x] += add;
+      __syncthreads();
+    }
+    if (k < nb) sums[k] = base + part[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) base += part[threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = base;
+}
+__global__ void k_scan_apply(const int32_t* __restrict__ in, int32_t* __restrict__ out,
+                             long long n, const long long* __restrict__ sums) {
+  __shared__ long long s[1024];
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long v = k < n ? in[k] : 0;
+  s[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 1; o < int(blockDim.x); o <<= 1) {
+    const long long add = threadIdx.x >= unsigned(o) ? s[threadIdx.x - o] : 0;
+    __syncthreads();
+    s[threadIdx.x] += add;
+    __syncthreads();
+  }
+  if (k < n) out[k] = int32_t(sums[blockIdx.x] + s[threadIdx.x] - v);
+}
+
+// --- inflow targets (solver_nonuniform.cpp:611-628) ---------------------------
+// One thread per fine cell of the rectangle: walk down from level 0 to the
+// leaf containing it (QuadGrid::find_containing, quadgrid.cpp:62-69) and count.
+__global__ void k_inflow_cells(TopoIn t, int i0, int j0, int wi, long long cells,
+                               int32_t* __restrict__ cnt) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= cells) return;
+  const int fi = i0 + int(c % wi), fj = j0 + int(c / wi);
+  int l = 0;
+  uint64_t node = node_index(0, fi >> t.L, fj >> t.L, t.M);
+  while (l < t.L && t.flag[l][node]) {
+    ++l;
+    node = node_index(l, fi >> (t.L - l), fj >> (t.L - l), t.M);
+  }
+  atomicAdd(&cnt[leaf_index(t, l, node)], 1);
+}
+
+// Manning per leaf from a cell-centred raster (solver_nonuniform.cpp:575-584).
+__global__ void k_manning(long long n, int L, double R, double x0, double y0,
+                          const int8_t* __restrict__ lvl, const int32_t* __restrict__ li,
+                          const int32_t* __restrict__ lj, const double* __restrict__ mr, int nc,
+                          int nr, double xll, double yll, double cs, double uniform,
+                          double* __restrict__ out) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  if (!mr) {
+    out[k] = uniform;
+    return;
+  }
+  const int l = lvl[k];
+  const double xc = x0 + (li[k] + 0.5) * R * double(1 << (L - l));
+  const double yc = y0 + (lj[k] + 0.5) * R * double(1 << (L - l));
+  const int col = min(max(int((xc - xll) / cs), 0), nc - 1);
+  const int row = min(max(nr - 1 - int((yc - yll) / cs), 0), nr - 1);
+  out[k] = mr[size_t(row) * nc + col];
+}
+
+TopoIn topo_in(const Grid& g) {
+  TopoIn t{};
+  for (int l = 0; l < g.L; ++l) {
+    t.flag[l] = g.flag[l].p;
+    t.off[l] = g.off[l].p;
+  }
+  t.L = g.L;
+  t.M = g.M;
+  t.N = g.N;
+  return t;
+}
+
+inline unsigned nblk(long long n, int t) { return unsigned((n + t - 1) / t); }
+
+}  // namespace
+
+int64_t scan_exclusive(const int32_t* in, int32_t* out, int64_t n) {
+  cudaStream_t st = stream();
+  const int T = 1024;
+  const long long nb = (n + T - 1) / T;
+  DBuf<long long> sums(std::max<long long>(nb, 1)), total(1);
+  if (n == 0) return 0;
+  k_block_sums<<<unsigned(nb), T, 0, st>>>(in, n, sums.p);
+  FM_LAUNCHED();
+  k_scan_sums<<<1, 1024, 0, st>>>(sums.p, nb, total.p);
+  FM_LAUNCHED();
+  k_scan_apply<<<unsigned(nb), T, 0, st>>>(in, out, n, sums.p);
+  FM_LAUNCHED();
+  long long tot = 0;
+  total.download(&tot, 1);
+  FM_CUDA(cudaStreamSynchronize(st));
+  return tot;
+}
+
+void build_topology(Sim& s, const Grid& g) {
+  cudaStream_t st = stream();
+  const long long n = s.n;
+  s.nb.alloc(8 * n);
+  s.sk.alloc(n);
+  DBuf<int32_t> owned(n), base(n);
+  DBuf<int> err(1);
+  err.zero();
+  const TopoIn t = topo_in(g);
+  k_topo<<<nblk(n, 256), 256, 0, st>>>(t, n, s.lvl.p, s.li.p, s.lj.p, s.nb.p, s.sk.p, owned.p, err.p);
+  FM_LAUNCHED();
+  s.nseg = scan_exclusive(owned.p, base.p, n);
+  int herr = 0;
+  err.download(&herr, 1);
+  FM_CUDA(cudaStreamSynchronize(st));
+  if (herr) throw Error(FM_ERR_STRUCTURE, "non-uniform solvers require a graded (2:1) grid");
+  if (s.scheme == FM_ACC) {
+    s.sid.alloc(8 * n);
+    s.seg_l.alloc(std::max<int64_t>(s.nseg, 1));
+    s.seg_r.alloc(std::max<int64_t>(s.nseg, 1));
+    k_segments<<<nblk(n, 256), 256, 0, st>>>(n, s.li.p, s.lj.p, s.nb.p, s.sk.p, base.p, s.sid.p,
+                                              s.seg_l.p, s.seg_r.p);
+    FM_LAUNCHED();
+  }
+}
+
+void resolve_inflows(Sim& s, const Grid& g) {
+  cudaStream_t st = stream();
+  s.infc.alloc(std::max<int64_t>(1, int64_t(s.ninflow) * s.n));
+  s.infc.zero();
+  const TopoIn t = topo_in(g);
+  for (int f = 0; f < s.ninflow; ++f) {
+    const int i0 = s.rect[4 * f], j0 = s.rect[4 * f + 1], i1 = s.rect[4 * f + 2], j1 = s.rect[4 * f + 3];
+    const long long wi = i1 - i0 + 1, cells = wi * (long long)(j1 - j0 + 1);
+    k_inflow_cells<<<nblk(cells, 256), 256, 0, st>>>(t, i0, j0, int(wi), cells, s.infc.p + f * s.n);
+    FM_LAUNCHED();
+  }
+}
+
+void resolve_manning(Sim& s) {
+  k_manning<<<nblk(s.n, 256), 256, 0, stream()>>>(
+      s.n, s.L, s.R, s.x0, s.y0, s.lvl.p, s.li.p, s.lj.p, s.has_mr ? s.mr.p : nullptr, s.mr_ncols,
+      s.mr_nrows, s.mr_xll, s.mr_yll, s.mr_cs, s.manning, s.nman.p);
+  FM_LAUNCHED();
+}
+
+}  // namespace fmh

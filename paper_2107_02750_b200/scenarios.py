@@ -241,3 +241,59 @@ def config4(scale: int = 1, uniform: bool = False) -> Scenario:
 
 
 CONFIGS = {0: config0, 1: config1, 2: config2, 3: config3, 4: config4}
+
+
+def to_arrays(sc: Scenario) -> dict:
+    """Flatten a scenario into numpy arrays (for the committed golden fixtures)."""
+    d = {
+        "name": np.array(sc.name), "solver": np.array(sc.solver), "grid_mode": np.array(sc.grid_mode),
+        "dem": sc.dem.values, "dem_geo": np.array([sc.dem.xll, sc.dem.yll, sc.dem.cellsize, sc.dem.nodata]),
+        "scalars": np.array([sc.L, sc.eps, sc.manning, sc.courant, sc.initial_depth, sc.steps,
+                             sc.adapt_every, sc.g, sc.h_dry,
+                             np.nan if sc.initial_surface is None else sc.initial_surface]),
+        "bc": np.array(sc.bc, dtype=np.int32),
+        "n_inflows": np.array(len(sc.inflows)),
+    }
+    if sc.manning_raster is not None:
+        d["manning_raster"] = sc.manning_raster.values
+        d["manning_geo"] = np.array([sc.manning_raster.xll, sc.manning_raster.yll,
+                                     sc.manning_raster.cellsize, sc.manning_raster.nodata])
+    if sc.initial_depth_raster is not None:
+        d["h0_raster"] = sc.initial_depth_raster.values
+    for k, f in enumerate(sc.inflows):
+        d[f"inflow{k}_t"] = np.array(f.t, dtype=np.float64)
+        d[f"inflow{k}_q"] = np.array(f.q, dtype=np.float64)
+        d[f"inflow{k}_rect"] = np.array([f.i0, f.j0, f.i1, f.j1], dtype=np.int32)
+    return d
+
+
+def from_arrays(d) -> Scenario:
+    geo = d["dem_geo"]
+    s = d["scalars"]
+    dem = Raster(np.array(d["dem"]), xll=float(geo[0]), yll=float(geo[1]), cellsize=float(geo[2]),
+                 nodata=float(geo[3]))
+    mr = None
+    if "manning_raster" in d:
+        mg = d["manning_geo"]
+        mr = Raster(np.array(d["manning_raster"]), xll=float(mg[0]), yll=float(mg[1]),
+                    cellsize=float(mg[2]), nodata=float(mg[3]))
+    h0 = Raster(np.array(d["h0_raster"]), xll=float(geo[0]), yll=float(geo[1]),
+                cellsize=float(geo[2]), nodata=float(geo[3])) if "h0_raster" in d else None
+    infl = []
+    for k in range(int(d["n_inflows"])):
+        r = d[f"inflow{k}_rect"]
+        infl.append(Inflow(t=list(d[f"inflow{k}_t"]), q=list(d[f"inflow{k}_q"]), i0=int(r[0]),
+                           j0=int(r[1]), i1=int(r[2]), j1=int(r[3])))
+    return Scenario(name=str(d["name"]), dem=dem, solver=str(d["solver"]), L=int(s[0]), eps=float(s[1]),
+                    manning=float(s[2]), courant=float(s[3]), initial_depth=float(s[4]),
+                    steps=int(s[5]), adapt_every=int(s[6]), g=float(s[7]), h_dry=float(s[8]),
+                    initial_surface=None if np.isnan(s[9]) else float(s[9]),
+                    manning_raster=mr, initial_depth_raster=h0, bc=tuple(int(x) for x in d["bc"]),
+                    inflows=infl, grid_mode=str(d["grid_mode"]))
+
+
+def spike(n: int = 16, height: float = 1.0) -> Raster:
+    """Flat DEM with one raised vertex at the centre (test_mra.cpp:24-29)."""
+    v = np.zeros((n + 1, n + 1))
+    v[(n + 1) // 2, (n + 1) // 2] = height
+    return Raster(v, cellsize=1.0)

@@ -1,0 +1,131 @@
+"""Generate tests/golden/*.npz from the UNMODIFIED reference library.
+
+Runs in the build container only (it needs oracle/_ref/libfmref.so, built
+from /root/reference by `make -C oracle ref`).  The fixtures hold the inputs
+and the reference outputs of small cases of every hot-path routine so the
+oracle (and the GPU path) can be pinned on machines without the reference.
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2107_02750_b200 import scenarios as S  # noqa: E402
+from paper_2107_02750_b200.abi import Backend, dptr  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+ref = Backend(os.path.join(ROOT, "oracle", "_ref", "libfmref.so"), "ref_")
+
+
+def point_kernels():
+    rng = np.random.default_rng(7)
+    # wavelets: random children, both kinds
+    kids = rng.uniform(-10, 10, size=(200, 12))
+    out = {"kids": kids}
+    for kind in (0, 1):
+        par = np.zeros((200, 3))
+        det = np.zeros((200, 9))
+        back = np.zeros((200, 12))
+        for r in range(200):
+            k = np.ascontiguousarray(kids[r])
+            p = np.zeros(3)
+            d = np.zeros(9)
+            ref.fn["encode"](dptr(k), kind, dptr(p), dptr(d))
+            par[r], det[r] = p, d
+            b = np.zeros(12)
+            ref.fn["decode"](dptr(p), dptr(d), kind, dptr(b))
+            back[r] = b
+        out[f"parent{kind}"], out[f"det{kind}"], out[f"back{kind}"] = par, det, back
+    # HLL: the known-answer cases of test_solver_uniform.cpp:55-81 plus random states
+    cases = [[0, 0, 0, 0, 0, 0], [1.0, 0, 0, 1.0, 0, 0], [1.0, 10.0, 2.0, 0.8, 7.2, 0.8]]
+    hs = rng.uniform(0, 3, size=(300, 2))
+    hs[::7, 0] = 0.0
+    hs[::11, 1] = 0.0
+    hs[::13, :] = 5e-7
+    qs = rng.uniform(-4, 4, size=(300, 4))
+    for r in range(300):
+        cases.append([hs[r, 0], qs[r, 0], qs[r, 1], hs[r, 1], qs[r, 2], qs[r, 3]])
+    cases = np.array(cases)
+    fl = np.zeros((len(cases), 3))
+    for r, c in enumerate(cases):
+        o = np.zeros(3)
+        ref.fn["hll"](*[float(x) for x in c], 9.80665, 1e-6, dptr(o))
+        fl[r] = o
+    out["hll_in"], out["hll_out"] = cases, fl
+    # friction (glibc cbrt) on random states
+    fr_in = np.column_stack([rng.uniform(1e-7, 20, 300), rng.uniform(-5, 5, (300, 2)),
+                             rng.uniform(0, 0.08, 300), rng.uniform(0.01, 5, 300)])
+    fr_out = np.zeros((300, 2))
+    for r, (h, qx, qy, n, dt) in enumerate(fr_in):
+        a = np.array([qx, 0.1, -0.2])
+        b = np.array([qy, 0.3, 0.4])
+        ref.fn["friction"](h, dptr(a), dptr(b), n, 9.80665, 1e-6, dt)
+        fr_out[r] = [a[0], b[0]]
+    out["fr_in"], out["fr_out"] = fr_in, fr_out
+    np.savez_compressed(os.path.join(OUT, "point_kernels.npz"), **out)
+
+
+GRIDS = {
+    "spike16_L4": (S.spike(16, 1.0), 4, 1e-3),
+    "spike32_L4": (S.spike(32, 2.0), 4, 1e-3),
+    "spike16_L2": (S.spike(16, 1.0), 2, 1e-3),  # M = N = 4 coarse blocks
+    "c0_s8": (S.config0(8).dem, S.config0(8).L, 1e-3),
+    "c1_s16": (S.config1(16).dem, S.config1(16).L, 1e-3),
+    "c3_s32": (S.config3(32).dem, S.config3(32).L, 1e-3),
+    "c4_s64": (S.config4(64).dem, S.config4(64).L, 1e-3),
+}
+
+
+def grids():
+    for name, (dem, L, eps) in GRIDS.items():
+        for kind in (0, 1):
+            g = ref.grid(dem, L, eps, True, kind)
+            lv, i, j, z = g.leaves()
+            d = {"dem": dem.values, "cell": np.array(dem.cellsize), "L": np.array(L),
+                 "eps": np.array(eps), "kind": np.array(kind), "level": lv, "i": i, "j": j, "topo": z,
+                 "field_norm": np.array(g.info()["field_norm"])}
+            for l in range(L):
+                d[f"flags{l}"] = g.flags(l)
+                d[f"dhat{l}"] = g.dhat(l)
+            np.savez_compressed(os.path.join(OUT, f"grid_{name}_k{kind}.npz"), **d)
+
+
+SIMS = {
+    "c0_dg2_s8": (S.config0(8), 40),
+    "c1_acc_s16": (S.config1(16), 60),
+    "c2_fv1_s16": (S.config2(16, adaptive=False), 60),
+    "c2_hwfv1_s16": (S.config2(16), 30),
+    "c3_mwdg2_s32": (S.config3(32), 20),
+    "c4_nu_s64": (S.config4(64), 20),
+    "c4_uni_s64": (S.config4(64, uniform=True), 20),
+}
+
+
+def sims():
+    for name, (sc, steps) in SIMS.items():
+        g = None
+        if sc.grid_mode == "nonuniform" and sc.solver not in ("mwdg2", "hwfv1"):
+            g = ref.grid(sc.dem, sc.L, sc.eps)
+        s = ref.sim(sc, g)
+        lv0, i0, j0, u0, z0 = s.download()
+        ck, r = s.run(steps, gauge_interval=10.0)
+        lv, i, j, u, z = s.download()
+        d = dict(S.to_arrays(sc))
+        d.update({"run_steps": np.array(steps), "u0": u0, "level": lv, "i": i, "j": j, "u": u,
+                  "z": z, "now": np.array(ck.now), "steps_done": np.array(r.steps),
+                  "dt_min": np.array(r.dt_min), "dt_max": np.array(r.dt_max),
+                  "vol_in": np.array(r.volume_inflow), "volume": np.array(s.volume())})
+        t, c = s.element_log()
+        d["elog_t"], d["elog_n"] = t, c
+        np.savez_compressed(os.path.join(OUT, f"sim_{name}.npz"), **d)
+        print(name, s.num_cells, r.steps, ck.now)
+
+
+if __name__ == "__main__":
+    os.makedirs(OUT, exist_ok=True)
+    point_kernels()
+    grids()
+    sims()
+    print("golden fixtures written to", OUT)
