@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path on BASELINE.json's headline configuration.
+
+Workload (config 4, the 8192^2 urban case the north_star's roofline and
+scaling targets are quoted on): multiwavelet MRA (L = 13, eps = 1e-3) of the
+seeded synthetic DEM, then static non-uniform DG2 RK2 steps under the 50 mm/h
+rain on the resulting ~2.3 M leaves.  A "step" is one RK2 step of every leaf
+(cell-updates/s = leaves x steps / time).  Synthetic inputs (DESIGN.md
+§"Synthetic inputs"); state ~0.6 GB per GPU > the 126 MB L2, so no flush is
+needed between steps.
+
+Legs:
+  value    device loop (CUDA graph) with the DEM resident in HBM, CUDA-event time
+           of exactly K steps, max over ranks;
+  e2e      the public API from host buffers: DEM upload, fm_mra_static,
+           fm_sim_create, K steps, final-state download, wall-clock;
+  roofline the dominant kernel (k_stage<2>) from a per-launch CUDA-event profile;
+  cpu_baseline  the reference library (oracle/_ref, built from the reference's own
+           sources) on the host cores, on a bounded sample of the workload.
+`--impl reference` runs only the reference arm and prints its line.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2107_02750_b200 import scenarios as S  # noqa: E402
+from paper_2107_02750_b200.abi import Backend, c_clock  # noqa: E402
+
+METRIC = "DG2/ACC cell-updates/s and MRA coeffs/s; % of B200 HBM roofline"
+UNIT = "cell-updates/s"
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "libfmref.so")
+ORC_SO = os.path.join(ROOT, "oracle", "liboracle.so")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 9 and f[1].isdigit():
+                    rows.append(f)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [int(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": int(rows[0][2]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def allreduce_max(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(ws: int):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def reference_backend():
+    if os.path.exists(REF_SO):
+        return Backend(REF_SO, "ref_"), "reference"
+    return Backend(ORC_SO, "orc_"), "port"
+
+
+def cpu_rate(steps: int, warmup: int, scale: int = 4):
+    """The reference CPU path on a bounded sample: config 4's generator at
+    (8192/scale)^2 cells, L = 13 - log2(scale), warm-up then `steps` timed DG2
+    steps with all host threads (run.cpp:79-113 times the step loop only)."""
+    be, kind = reference_backend()
+    cores = os.cpu_count() or 1
+    if be.has("set_threads"):
+        be.fn["set_threads"](cores)
+    else:
+        cores = 1
+    sc = S.config4(scale)
+    g = be.grid(sc.dem, sc.L, sc.eps)
+    s = be.sim(sc, g)
+    ck, _ = s.run(warmup, gauge_interval=10.0)
+    t0 = time.perf_counter()
+    ck, r = s.run(steps, clock=ck)
+    dt = time.perf_counter() - t0
+    n = s.num_cells
+    return {"value": n * r.steps / dt, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"config-4 generator at {8192 // scale}^2 cells (L={sc.L}, {n} leaves), "
+                      f"{r.steps} timed DG2 steps after {warmup} warm-up, {cores} threads, "
+                      f"{dt:.2f} s"}, r.steps, dt
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    steps = max(1, min(args.steps, args.cpu_steps_cap))
+    cb, n_done, secs = cpu_rate(steps, max(1, min(args.warmup, 3)))
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": n_done, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * secs / max(n_done, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c4_static_nonuniform_dg2 (bounded CPU sample)",
+                       "sample": cb["sample"]},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+
+    from paper_2107_02750_b200 import api
+
+    lib = api.lib()
+    sc = S.config4(args.scale)
+    hbm, peak_kind = peaks()
+
+    # ---- value leg: DEM resident in HBM, device loop, CUDA-event timing ----
+    dem_d = torch.from_numpy(np.ascontiguousarray(sc.dem.values)).to(f"cuda:{local}")
+    torch.cuda.synchronize()
+    grid = lib.grid(sc.dem, sc.L, sc.eps, device_ptr=dem_d.data_ptr())
+    mra_ms, mra_bytes = grid.timing()
+    n_int = (4 ** sc.L - 1) // 3
+    sim = lib.sim(sc, grid)
+    n_leaves, n_seg = sim.num_cells, sim.num_segments
+    ck, r = sim.run(args.warmup, gauge_interval=10.0)
+    # The reference DG2 scheme diverges under this forcing after ~130 steps (thin
+    # rain films on 10 m building walls; DESIGN.md §"Config 4 dynamics"), so the
+    # K timed steps run in chunks that each restart from the post-warm-up state
+    # (device-side snapshot, restored outside the timed region).
+    sim.snapshot()
+    ck0 = (ck.end_time, ck.output_interval, ck.gauge_interval, ck.now, ck.next_output,
+           ck.next_gauge)
+    ms = 0.0
+    done = 0
+    launches = 0
+    with Clocks(local) as clocks:
+        while done < args.steps:
+            n = min(args.chunk, args.steps - done)
+            sim.restore()
+            ckc = c_clock(*ck0)
+            barrier(ws)
+            torch.cuda.synchronize()
+            launches0 = api.launch_count()
+            ckc, r = sim.run(n, clock=ckc)
+            torch.cuda.synchronize()
+            launches += api.launch_count() - launches0
+            barrier(ws)
+            if r.steps != n:
+                raise SystemExit(f"only {r.steps} of {n} steps ran (blew_up={r.blew_up})")
+            ms += sim.last_run_ms()
+            done += n
+    ms_max = allreduce_max(ms, ws)
+    cells_total = allreduce_sum(float(n_leaves) * args.steps, ws)
+    value = cells_total / (ms_max / 1000.0)
+
+    # ---- roofline of the dominant kernel (per-launch CUDA events) ----
+    sim.restore()
+    prof = sim.profile(args.profile_steps)
+    stage2_ms, stage2_n = prof.get("k_stage<2>", (0.0, 1))
+    avg_ms = stage2_ms / max(stage2_n, 1)
+    # DG2 stage 2 reads U^n 72 + U* 72 + z 24 + n 8, writes 72 B per
+    # leaf, + 8 B of segment indices per segment
+    bytes_launch = 248.0 * n_leaves + 8.0 * n_seg
+    achieved = bytes_launch / (avg_ms / 1000.0) / 1e9
+    step_ms = sum(v[0] for v in prof.values()) / max(args.profile_steps, 1)
+    step_bytes = 424.0 * n_leaves + 16.0 * n_seg
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("k_stage<2>")
+        except Exception:
+            traffic = None
+    del sim, grid, dem_d
+
+    # ---- e2e leg: public API from host buffers, wall clock ----
+    barrier(ws)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g2 = lib.grid(sc.dem, sc.L, sc.eps)
+    s2 = lib.sim(sc, g2)
+    ck2, r2 = s2.run(args.warmup, gauge_interval=10.0)
+    s2.snapshot()
+    ck0 = (ck2.end_time, ck2.output_interval, ck2.gauge_interval, ck2.now, ck2.next_output,
+           ck2.next_gauge)
+    done = 0
+    while done < args.steps:
+        n = min(args.chunk, args.steps - done)
+        s2.restore()
+        _, r2 = s2.run(n, clock=c_clock(*ck0))
+        done += r2.steps
+    out = s2.download()
+    e2e_s = time.perf_counter() - t0
+    e2e_s = allreduce_max(e2e_s, ws)
+    h2d = sc.dem.values.nbytes + sc.manning_raster.values.nbytes
+    d2h = sum(a.nbytes for a in out)
+    e2e_steps = args.warmup + args.steps
+    e2e_value = allreduce_sum(float(n_leaves) * e2e_steps, ws) / e2e_s
+    del s2, g2
+
+    if rank != 0:
+        return
+    cpu = None
+    if ws == 1 and not args.no_cpu:
+        cpu, _, _ = cpu_rate(args.cpu_steps, 2)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c4_static_nonuniform_dg2", "cells": f"{8192 // args.scale}^2",
+                   "L": sc.L, "eps": sc.eps, "leaves": n_leaves, "segments": n_seg,
+                   "parallelism": "replicas" if ws > 1 else "single",
+                   "l2": "state > 126 MB L2 (no flush needed)",
+                   "solver": "static non-uniform DG2 RK2, rain 50 mm/h, Manning street raster"},
+        "roofline": {"bound": "hbm", "kernel": "k_stage<2>", "achieved": achieved, "peak": hbm,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic, "bytes_per_launch": bytes_launch,
+                     "avg_launch_ms": avg_ms,
+                     "step": {"bytes": step_bytes, "ms": step_ms,
+                              "achieved": step_bytes / (step_ms / 1000.0) / 1e9,
+                              "frac": step_bytes / (step_ms / 1000.0) / 1e9 / hbm},
+                     "kernels_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in prof.items()}},
+        "mra": {"coeffs_per_s": 12.0 * n_int / (mra_ms / 1000.0), "ms": mra_ms,
+                "bytes": mra_bytes, "achieved_gbs": mra_bytes / (mra_ms / 1000.0) / 1e9,
+                "frac": mra_bytes / (mra_ms / 1000.0) / 1e9 / hbm},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
+                "d2h_bytes_per_step": d2h / e2e_steps, "seconds": e2e_s,
+                "what": "host DEM -> fm_mra_static -> fm_sim_create -> W+K steps -> host state"},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--scale", type=int, default=1, help="shrink config 4 (tests only)")
+    p.add_argument("--profile-steps", type=int, default=10)
+    p.add_argument("--chunk", type=int, default=64, help="timed steps between state restores")
+    p.add_argument("--cpu-steps", type=int, default=40)
+    p.add_argument("--cpu-steps-cap", type=int, default=20)
+    p.add_argument("--no-cpu", action="store_true")
+    args = p.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    ws, rank, local = dist_setup() if args.impl == "ours" else (
+        int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -57,6 +57,8 @@ enum { FM_REFLECTIVE = 0, FM_OPEN = 1 };
 enum { FM_NORTH = 0, FM_EAST = 1, FM_SOUTH = 2, FM_WEST = 3 };
 /* leaf orders for fm_grid_leaves / fm_sim_download */
 enum { FM_ORDER_REFERENCE = 0, FM_ORDER_DEVICE = 1 };
+/* fm_sim_desc.libm */
+enum { FM_LIBM_NATIVE = 0, FM_LIBM_PORTABLE = 1 };
 
 /* Raster (raster.hpp:10-26).  `values` is ncols*nrows doubles, row 0 north.
  * `on_device` != 0 means `values` is a CUDA device pointer already resident
@@ -94,6 +96,11 @@ typedef struct fm_sim_desc {
   double epsilon;          /* adaptive solvers */
   int32_t max_level;       /* adaptive solvers */
   int32_t adapt_every;     /* adaptive solvers, >= 1 */
+  /* libm used by friction (cbrt) and ACC (pow(h, 7/3)):
+   *   FM_LIBM_NATIVE   the platform's (CUDA on the GPU, glibc in the reference);
+   *   FM_LIBM_PORTABLE a deterministic +,-,*,/ implementation that the CPU
+   *                    oracle reproduces bit-for-bit (parity harness only). */
+  int32_t libm;
 } fm_sim_desc;
 
 /* EventClock (sim_common.hpp:31-45) state. */
@@ -151,6 +158,10 @@ int fm_grid_dhat(const fm_grid* g, int32_t level, double* out);
 int fm_grid_near_threshold(const fm_grid* g, double rel, int64_t* count);
 /* Device time of the last MRA pipeline's kernels (ms) and algorithmic bytes. */
 int fm_grid_timing(const fm_grid* g, double* ms, double* bytes);
+/* ancestor_closure (detail_tree.cpp:56-64) followed, when `graded`, by
+ * grade_flags (detail_tree.cpp:97-113) on caller-supplied flags: `flags` holds
+ * levels 0..L-1 back to back, each row-major j*(M<<l)+i; updated in place. */
+int fm_grade_flags(int32_t L, int32_t M, int32_t N, int32_t graded, uint8_t* flags);
 
 /* ---- simulations (drive<Sim> duck type, run.cpp:35-141) ----------------- */
 /* run_scenario's dispatch (run.cpp:145-164): adaptive solvers build an
@@ -179,6 +190,11 @@ int fm_sim_finite(fm_sim* s, int32_t* ok, double* bad_x, double* bad_y);
 int fm_sim_download(fm_sim* s, int32_t* level, int32_t* i, int32_t* j, double* u9, double* z3);
 /* Overwrite the flow state (reference order) — lockstep re-seeding. */
 int fm_sim_upload(fm_sim* s, const double* u9);
+/* Device-side checkpoint of the flow state (U, U*, ACC discharges) and
+ * its restore, without host traffic; restore fails if the leaf set changed
+ * since the snapshot (adaptive re-gridding). */
+int fm_sim_snapshot(fm_sim* s);
+int fm_sim_restore(fm_sim* s);
 /* AdaptiveSim::element_log (solver_adaptive.hpp:23): number of entries, and copy. */
 int64_t fm_sim_element_log(fm_sim* s, double* t, int64_t* count, int64_t cap);
 /* The drive<Sim> loop body (run.cpp:80-111) resident on the device:
@@ -189,6 +205,13 @@ int fm_sim_run(fm_sim* s, fm_clock* clk, int64_t max_steps, int32_t stop_at_even
                fm_run_result* out);
 /* Device time (ms) of the last fm_sim_run's kernels, measured with CUDA events. */
 int fm_sim_last_run_ms(fm_sim* s, double* ms);
+/* Per-kernel timing: runs `steps` device-loop steps launching each kernel
+ * individually between CUDA events on the library stream; writes per kernel
+ * family the summed milliseconds and launch counts (family names via
+ * fm_sim_kernel_name).  Returns the number of families in *n. */
+int fm_sim_profile(fm_sim* s, int64_t steps, double* ms, int64_t* launches, int32_t cap,
+                   int32_t* n);
+const char* fm_sim_kernel_name(fm_sim* s, int32_t family);
 
 #ifdef __cplusplus
 }

@@ -88,6 +88,7 @@ Cfg to_cfg(const fm_sim_desc* d) {
   c.eps = d->epsilon;
   c.L = d->max_level;
   c.adapt_every = d->adapt_every;
+  c.libm = d->libm;
   return c;
 }
 }  // namespace
@@ -398,6 +399,31 @@ void orc_friction(double h0, double* qx3, double* qy3, double n, double g, doubl
   qx3[2] = a.cy;
   qy3[1] = b.cx;
   qy3[2] = b.cy;
+}
+double orc_pcbrt(double x) { return pcbrt(x); }
+
+// detail_tree.cpp:56-64 then :97-113 on caller flags (levels back to back).
+int orc_grade_flags(int32_t L, int32_t M, int32_t N, int32_t graded, uint8_t* flags) {
+  return guard([&] {
+    Tree t;
+    t.L = L;
+    t.M = M;
+    t.N = N;
+    t.flag.resize(L);
+    size_t at = 0;
+    for (int l = 0; l < L; ++l) {
+      const size_t n = size_t(t.w(l)) * t.h(l);
+      t.flag[l].assign(flags + at, flags + at + n);
+      at += n;
+    }
+    closure(t);
+    if (graded) grade(t);
+    at = 0;
+    for (int l = 0; l < L; ++l) {
+      std::memcpy(flags + at, t.flag[l].data(), t.flag[l].size());
+      at += t.flag[l].size();
+    }
+  });
 }
 void orc_encode(const double* kids12, int32_t kind, double* parent3, double* det9) {
   Pl k[4];

@@ -482,7 +482,38 @@ Flux hll(double hl, double qnl, double qtl, double hr, double qnr, double qtr, d
 }
 
 // sim_common.cpp:30-46
-void friction(double h0, Pl& qx, Pl& qy, double n, double g, double hdry, double dt) {
+// Portable cube root for positive finite x: split x = f 2^E (f in [1,2)),
+// E = 3k + r, solve y^3 = f 2^r in [1,8) with six Newton steps from a linear
+// guess, rescale by 2^k.  Only IEEE +,-,*,/ and exact power-of-two scalings.
+double pcbrt(double x) {
+  if (!(x > 0.0) || !std::isfinite(x)) return x;  // callers pass h > h_dry > 0
+  uint64_t b;
+  std::memcpy(&b, &x, 8);
+  int e = int((b >> 52) & 0x7ff), shift = 0;
+  if (e == 0) {
+    const double y = x * 18014398509481984.0;  // 2^54
+    std::memcpy(&b, &y, 8);
+    e = int((b >> 52) & 0x7ff);
+    shift = 54;
+  }
+  const int E = e - 1023 - shift;
+  const int k = E >= 0 ? E / 3 : -((2 - E) / 3);
+  const int r = E - 3 * k;
+  uint64_t fb = (b & 0x000fffffffffffffull) | (uint64_t(1023 + r) << 52);
+  double m;
+  std::memcpy(&m, &fb, 8);
+  double y = 0.8 + 0.15 * m;
+  for (int it = 0; it < 6; ++it) y = (2.0 * y + m / (y * y)) / 3.0;
+  const uint64_t sb = uint64_t(1023 + k) << 52;
+  double sc;
+  std::memcpy(&sc, &sb, 8);
+  return y * sc;
+}
+
+double cbrt_m(double x, int libm) { return libm ? pcbrt(x) : std::cbrt(x); }
+double pow73_m(double x, int libm) { return libm ? x * x * pcbrt(x) : std::pow(x, 7.0 / 3.0); }
+
+void friction(double h0, Pl& qx, Pl& qy, double n, double g, double hdry, double dt, int libm) {
   if (h0 <= hdry) {
     qx = {};
     qy = {};
@@ -492,7 +523,7 @@ void friction(double h0, Pl& qx, Pl& qy, double n, double g, double hdry, double
   const double u = qx.c0 / h0, v = qy.c0 / h0;
   const double sp = std::sqrt(u * u + v * v);
   if (sp == 0.0) return;
-  const double cf = g * n * n / std::cbrt(h0);
+  const double cf = g * n * n / cbrt_m(h0, libm);
   const double den = 1.0 + dt * cf * sp / h0;
   qx.c0 /= den;
   qy.c0 /= den;

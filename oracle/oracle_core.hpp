@@ -133,7 +133,13 @@ Faces faces_of(const Grid& g, bool need_graded);                         // quad
 // ---- point kernels ----------------------------------------------------------
 Flux hll(double hl, double qnl, double qtl, double hr, double qnr, double qtr, double g,
          double hdry);                                                   // hll.cpp:10-58
-void friction(double h0, Pl& qx, Pl& qy, double n, double g, double hdry, double dt);  // sim_common.cpp:30-46
+void friction(double h0, Pl& qx, Pl& qy, double n, double g, double hdry, double dt,
+              int libm = 0);  // sim_common.cpp:30-46
+// Deterministic cube root / h^(7/3) from +,-,*,/ only (parity harness,
+// FM_LIBM_PORTABLE); the CUDA path implements the same operation sequence.
+double pcbrt(double x);
+double cbrt_m(double x, int libm);
+double pow73_m(double x, int libm);
 void positivity(Fl& f, double hdry);                                     // solver_nonuniform.cpp:276-304
 
 struct Hydro {

@@ -278,7 +278,7 @@ void NU::rate_pass() {
 // solver_nonuniform.cpp:306-348
 void NU::step_rk(double dt) {
   const size_t n = u.size();
-  for (size_t c = 0; c < n; ++c) friction(u[c].h.c0, u[c].qx, u[c].qy, nman[c], g, hdry, dt);
+  for (size_t c = 0; c < n; ++c) friction(u[c].h.c0, u[c].qx, u[c].qy, nman[c], g, hdry, dt, libm);
   seg_pass(u);
   side_pass(u);
   rate_pass();
@@ -302,7 +302,6 @@ void NU::step_rk(double dt) {
 
 // solver_nonuniform.cpp:350-418
 void NU::step_acc(double dt) {
-  const double e73 = 7.0 / 3.0;
   for (size_t q = 0; q < F.in.size(); ++q) {
     const Seg& e = F.in[q];
     const int l = e.l, r = e.r;
@@ -316,7 +315,7 @@ void NU::step_acc(double dt) {
     const double dist = 0.5 * (grid.size(l) + grid.size(r));
     const double nf = 0.5 * (nman[l] + nman[r]);
     Q = (Q - g * hf * dt * (er - el) / dist) /
-        (1.0 + g * dt * nf * nf * std::abs(Q) / std::pow(hf, e73));
+        (1.0 + g * dt * nf * nf * std::abs(Q) / pow73_m(hf, libm));
   }
   for (size_t q = 0; q < F.bd.size(); ++q) {
     const BSeg& b = F.bd[q];
@@ -331,7 +330,7 @@ void NU::step_acc(double dt) {
       continue;
     }
     const double nf = nman[b.leaf];
-    Q = Q / (1.0 + g * dt * nf * nf * std::abs(Q) / std::pow(hf, e73));
+    Q = Q / (1.0 + g * dt * nf * nf * std::abs(Q) / pow73_m(hf, libm));
   }
   for (int k = 0; k < int(grid.lv.size()); ++k) {
     const double sz = grid.size(k), area = sz * sz;
@@ -485,6 +484,7 @@ Fl from_surface(const Pl& z, double eta0) {
 NU make_nu(const Cfg& c, const Raster& dem, const Grid& grid, const std::vector<Pl>& topo) {
   NU s;
   s.scheme = c.solver == S_MWDG2 ? S_DG2 : c.solver == S_HWFV1 ? S_FV1 : c.solver;
+  s.libm = c.libm;
   s.grid = grid;
   s.z = topo;
   if (!graded(s.grid)) throw Fail(E_STRUCT, "non-uniform solvers require a graded (2:1) grid");
@@ -833,7 +833,7 @@ void UN::assemble(bool dg2) {
 // solver_uniform.cpp:283-328
 void UN::step_rk(double dt) {
   const size_t n = u.size();
-  for (size_t c = 0; c < n; ++c) friction(u[c].h.c0, u[c].qx, u[c].qy, nman[c], g, hdry, dt);
+  for (size_t c = 0; c < n; ++c) friction(u[c].h.c0, u[c].qx, u[c].qy, nman[c], g, hdry, dt, libm);
   revise(u);
   fluxes();
   assemble(kind == S_DG2);
@@ -857,7 +857,6 @@ void UN::step_rk(double dt) {
 
 // solver_uniform.cpp:330-415
 void UN::step_acc(double dt) {
-  const double e73 = 7.0 / 3.0;
   auto face = [&](double& q, size_t l, size_t r) {
     const double el = u[l].h.c0 + z[l].c0, er = u[r].h.c0 + z[r].c0;
     const double hf = mx(el, er) - mx(z[l].c0, z[r].c0);
@@ -866,7 +865,7 @@ void UN::step_acc(double dt) {
       return;
     }
     const double nf = 0.5 * (nman[l] + nman[r]);
-    q = (q - g * hf * dt * (er - el) / R) / (1.0 + g * dt * nf * nf * std::abs(q) / std::pow(hf, e73));
+    q = (q - g * hf * dt * (er - el) / R) / (1.0 + g * dt * nf * nf * std::abs(q) / pow73_m(hf, libm));
   };
   auto edge = [&](double& q, int side, size_t c) {
     if (bc[side] == 0) {
@@ -878,7 +877,7 @@ void UN::step_acc(double dt) {
       q = 0.0;
       return;
     }
-    q = q / (1.0 + g * dt * nman[c] * nman[c] * std::abs(q) / std::pow(hf, e73));
+    q = q / (1.0 + g * dt * nman[c] * nman[c] * std::abs(q) / pow73_m(hf, libm));
   };
   for (int j = 0; j < ny; ++j)
     for (int i = 0; i <= nx; ++i) {
@@ -975,6 +974,7 @@ bool UN::finite(double* bx, double* by) const {
 UN make_un(const Cfg& c, const Raster& dem) {
   UN s;
   s.kind = c.solver;
+  s.libm = c.libm;
   if (c.solver == S_MWDG2 || c.solver == S_HWFV1)
     throw Fail(E_CONFIG, "uniform solver cannot run adaptive kinds");
   const Field f = project_plain(dem);

@@ -24,6 +24,7 @@ struct Cfg {
   std::vector<Inflow> inflows;  // hydrograph + rectangle (targets unresolved)
   double eps = 1e-3;
   int L = -1, adapt_every = 1;
+  int libm = 0;  // FM_LIBM_NATIVE / FM_LIBM_PORTABLE
   double courant_for() const;  // config.cpp:37-47
 };
 
@@ -39,6 +40,7 @@ struct NU {
   std::vector<double> nman;
   std::vector<Inflow> inflows;
   int pairing = -1;  // encode_pairing bank (adaptive) or -1
+  int libm = 0;
   std::vector<double> accq, accqb;
 
   // scratch
@@ -109,6 +111,7 @@ struct UN {
   int nx = 0, ny = 0;
   double R = 1, x0 = 0, y0 = 0, g = 9.80665, hdry = 1e-6, cour = 0.33;
   int bc[4] = {0, 0, 0, 0};
+  int libm = 0;
   std::vector<Pl> z;
   std::vector<Fl> u;
   std::vector<double> nman;

@@ -409,6 +409,29 @@ int ref_sim_run(ref_sim* s, fm_clock* ck, int64_t max_steps, int32_t stop_at_eve
   });
 }
 
+int ref_grade_flags(int32_t L, int32_t M, int32_t N, int32_t graded, uint8_t* flags) {
+  return guard([&] {
+    fm::DetailTree t;
+    t.L = L;
+    t.M = M;
+    t.N = N;
+    t.flags.resize(L);
+    size_t at = 0;
+    for (int l = 0; l < L; ++l) {
+      const size_t n = size_t(t.width(l)) * t.height(l);
+      t.flags[l].assign(flags + at, flags + at + n);
+      at += n;
+    }
+    fm::ancestor_closure(t);
+    if (graded) fm::grade_flags(t);
+    at = 0;
+    for (int l = 0; l < L; ++l) {
+      std::memcpy(flags + at, t.flags[l].data(), t.flags[l].size());
+      at += t.flags[l].size();
+    }
+  });
+}
+
 void ref_hll(double hl, double qnl, double qtl, double hr, double qnr, double qtr, double g,
              double hdry, double* out3) {
   const fm::Flux3 f = fm::hll_flux(hl, qnl, qtl, hr, qnr, qtr, g, hdry);

@@ -51,7 +51,7 @@ class c_desc(C.Structure):
                 ("has_initial_surface", C.c_int32), ("initial_surface", C.c_double),
                 ("initial_depth", C.c_double), ("inflows", C.POINTER(c_inflow)),
                 ("n_inflows", C.c_int32), ("epsilon", C.c_double), ("max_level", C.c_int32),
-                ("adapt_every", C.c_int32)]
+                ("adapt_every", C.c_int32), ("libm", C.c_int32)]
 
 
 class c_clock(C.Structure):
@@ -111,10 +111,16 @@ OPTIONAL = {
     "grid_timing": (C.c_int, [P, PD, PD]),
     "sim_last_run_ms": (C.c_int, [P, PD]),
     "grid_details": (C.c_int, [P, I32, PD]),
+    "sim_profile": (C.c_int, [P, I64, PD, PI64, I32, PI32]),
+    "sim_snapshot": (C.c_int, [P]),
+    "sim_restore": (C.c_int, [P]),
+    "sim_kernel_name": (C.c_char_p, [P, I32]),
     "sim_acc_q": (C.c_int, [P, PD, PD]),
     "set_threads": (None, [I32]),
     "hw_threads": (I32, []),
     "generate_static_grid": (C.c_int, [C.POINTER(c_raster), I32, D, I32, I32, PI64]),
+    "grade_flags": (C.c_int, [I32, I32, I32, I32, PU8]),
+    "pcbrt": (D, [D]),
     "hll": (None, [D, D, D, D, D, D, D, D, PD]),
     "friction": (None, [D, PD, PD, D, D, D, D]),
     "encode": (None, [PD, I32, PD, PD]),
@@ -161,11 +167,13 @@ class Backend:
         return st
 
     # ---- helpers -------------------------------------------------------
-    def grid(self, dem, L: int, eps: float, graded: bool = True, kind: int = 0):
-        return Grid(self, dem, L, eps, graded, kind)
+    def grid(self, dem, L: int, eps: float, graded: bool = True, kind: int = 0,
+             device_ptr: int | None = None):
+        """fm_mra_static; `device_ptr` passes a DEM already resident in HBM."""
+        return Grid(self, dem, L, eps, graded, kind, device_ptr)
 
-    def sim(self, scenario, grid=None):
-        return Sim(self, scenario, grid)
+    def sim(self, scenario, grid=None, libm: int = 0):
+        return Sim(self, scenario, grid, libm)
 
 
 def make_raster(r, keep: list) -> c_raster:
@@ -177,10 +185,15 @@ def make_raster(r, keep: list) -> c_raster:
 class Grid:
     """A static MRA grid (NonUniformGrid + the DetailTree flags)."""
 
-    def __init__(self, be: Backend, dem, L: int, eps: float, graded: bool, kind: int):
+    def __init__(self, be: Backend, dem, L: int, eps: float, graded: bool, kind: int,
+                 device_ptr: int | None = None):
         self.be = be
         keep: list = []
-        self._r = make_raster(dem, keep)
+        if device_ptr is not None:
+            self._r = c_raster(C.cast(C.c_void_p(device_ptr), PD), dem.ncols, dem.nrows, dem.xll,
+                               dem.yll, dem.cellsize, dem.nodata, 1)
+        else:
+            self._r = make_raster(dem, keep)
         self._keep = keep
         h = P()
         be.call("mra_static", C.byref(self._r), L, eps, 1 if graded else 0, kind, C.byref(h))
@@ -240,7 +253,7 @@ class Grid:
 class Sim:
     """A drive<Sim>-shaped simulation (run.cpp:35-141) behind the ABI."""
 
-    def __init__(self, be: Backend, sc, grid: Grid | None = None):
+    def __init__(self, be: Backend, sc, grid: Grid | None = None, libm: int = 0):
         from .scenarios import SOLVERS
 
         self.be = be
@@ -278,6 +291,7 @@ class Sim:
         d.epsilon = sc.eps
         d.max_level = sc.L
         d.adapt_every = sc.adapt_every
+        d.libm = libm
         dem = make_raster(sc.dem, keep)
         h = P()
         be.call("sim_create", C.byref(d), C.byref(dem), grid.h if grid is not None else None,
@@ -363,6 +377,26 @@ class Sim:
         v = D()
         self.be.call("sim_last_run_ms", self.h, C.byref(v))
         return v.value
+
+    def snapshot(self):
+        self.be.call("sim_snapshot", self.h)
+
+    def restore(self):
+        self.be.call("sim_restore", self.h)
+
+    def profile(self, steps: int) -> dict:
+        """Per-kernel device time over `steps` steps: {name: (ms_total, launches)}."""
+        ms = np.zeros(16)
+        cnt = np.zeros(16, np.int64)
+        nf = I32()
+        self.be.call("sim_profile", self.h, steps, dptr(ms), cnt.ctypes.data_as(PI64), 16,
+                     C.byref(nf))
+        out = {}
+        for f in range(nf.value):
+            if cnt[f]:
+                name = self.be.fn["sim_kernel_name"](self.h, f).decode()
+                out[name] = (float(ms[f]), int(cnt[f]))
+        return out
 
 
 def default_clock(sc) -> c_clock:

@@ -206,6 +206,14 @@ int fm_grid_timing(const fm_grid* h, double* ms, double* bytes) {
   });
 }
 
+int fm_grade_flags(int32_t L, int32_t M, int32_t N, int32_t graded, uint8_t* flags) {
+  return guard([&] {
+    require_device();
+    if (L < 1) return;
+    grade_flags_host(L, M, N, graded != 0, flags);
+  });
+}
+
 int fm_sim_create(const fm_sim_desc* d, const fm_raster* dem, const fm_grid* grid, fm_sim** out) {
   return guard([&] {
     require_device();
@@ -246,6 +254,12 @@ int fm_sim_download(fm_sim* s, int32_t* l, int32_t* i, int32_t* j, double* u9, d
 int fm_sim_upload(fm_sim* s, const double* u9) {
   return guard([&] { sim_upload(*s->s, u9); });
 }
+int fm_sim_snapshot(fm_sim* s) {
+  return guard([&] { sim_snapshot(*s->s); });
+}
+int fm_sim_restore(fm_sim* s) {
+  return guard([&] { sim_restore(*s->s); });
+}
 int64_t fm_sim_element_log(fm_sim* h, double* t, int64_t* count, int64_t cap) {
   const auto& log = h->s->element_log;
   const int64_t n = int64_t(log.size());
@@ -262,5 +276,14 @@ int fm_sim_run(fm_sim* s, fm_clock* clk, int64_t max_steps, int32_t stop_at_even
 int fm_sim_last_run_ms(fm_sim* s, double* ms) {
   return guard([&] { *ms = s->s->last_run_ms; });
 }
+int fm_sim_profile(fm_sim* s, int64_t steps, double* ms, int64_t* launches, int32_t cap,
+                   int32_t* n) {
+  return guard([&] {
+    int nf = 0;
+    sim_profile(*s->s, steps, ms, launches, cap, &nf);
+    *n = nf;
+  });
+}
+const char* fm_sim_kernel_name(fm_sim*, int32_t family) { return kernel_family_name(family); }
 
 }  // extern "C"

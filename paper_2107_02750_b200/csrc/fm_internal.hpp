@@ -119,6 +119,33 @@ std::vector<int64_t> reference_order(const Grid& g, std::vector<int8_t>* l = nul
 
 double elapsed_ms(cudaEvent_t a, cudaEvent_t b);
 
+// Optional per-launch timing for fm_sim_profile: when on, every kernel launch
+// of a step is bracketed by CUDA events on the library stream.
+enum KernelFamily {
+  KF_HEAD = 0,    // step head + friction (DG2/FV1)
+  KF_STAGE1,      // RK stage 1 (FV1: the whole update)
+  KF_STAGE2,      // RK stage 2 + fused epilogue
+  KF_COMMIT,      // clock commit
+  KF_ACC_FACES,   // ACC face discharges + step head
+  KF_ACC_LEAVES,  // ACC leaf update + fused epilogue
+  KF_UNI_HEAD,    // uniform raster: head + friction
+  KF_UNI_STAGE1,  // uniform raster: stage 1
+  KF_UNI_STAGE2,  // uniform raster: stage 2
+  KF_COUNT
+};
+const char* kernel_family_name(int f);
+struct KTimer {
+  bool on = false;
+  std::vector<int> fam;
+  std::vector<cudaEvent_t> a, b;
+};
+KTimer& ktimer();
+void kt_begin(int fam);
+void kt_end();
+
+// ancestor_closure + grade_flags on host flags (levels back to back, row-major).
+void grade_flags_host(int L, int M, int N, bool graded, uint8_t* flags);
+
 // Level-L planes (3 per node, block-Morton order) of a vertex raster, padded
 // and nodata-walled as project_raster does (field.cpp:64-117).
 void project_planes(const fm_raster* r, int L, int M, int N, DBuf<double>& out);

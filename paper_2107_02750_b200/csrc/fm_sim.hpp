@@ -44,7 +44,7 @@ struct Hydro {
 
 // Everything a non-uniform leaf kernel needs (POD, passed by value).
 struct NuView {
-  int L, M, N, scheme, adaptive, ninflow;
+  int L, M, N, scheme, adaptive, ninflow, libm;
   double R, x0, y0, g, hdry, courant;
   int bc[4];
   long long n;
@@ -65,7 +65,7 @@ struct NuView {
 };
 
 struct Sim {
-  int solver = 0, scheme = 0;
+  int solver = 0, scheme = 0, libm = 0;
   bool adaptive = false, uniform = false;
   double g = 9.80665, hdry = 1e-6, courant = 0.33;
   int bc[4] = {0, 0, 0, 0};
@@ -73,6 +73,10 @@ struct Sim {
   int L = 0, M = 1, N = 1;
   double R = 1, x0 = 0, y0 = 0;
   int nx = 0, ny = 0;  // uniform raster
+  // Power-of-two element sizes with exactly representable coordinates: the
+  // stage kernels evaluate planes at exact offsets and replace divisions by
+  // the element size with exact reciprocal multiplies (bit-identical).
+  bool p2 = false;
   int64_t n = 0, nseg = 0;
   // leaves (device Morton order) and state
   DBuf<int8_t> lvl;
@@ -92,6 +96,10 @@ struct Sim {
   DBuf<DevRed> red;          // [2]
   DBuf<int> errflag;         // device error bits (negative depth into HLL)
   bool fv1_in_star = false;
+  // device-side checkpoint (fm_sim_snapshot / fm_sim_restore)
+  DBuf<double> snap_u, snap_us, snap_q, snap_qb, snap_aqx, snap_aqy;
+  int64_t snap_n = -1;
+  bool snap_fv1 = false;
   double last_run_ms = 0.0;
   // Manning raster (kept for adaptive remaps)
   DBuf<double> mr;
@@ -122,6 +130,9 @@ bool sim_finite(Sim& s, double* bx, double* by);
 void sim_download(Sim& s, int32_t* l, int32_t* i, int32_t* j, double* u9, double* z3);
 void sim_upload(Sim& s, const double* u9);
 void sim_run(Sim& s, fm_clock* clk, int64_t max_steps, int stop_at_events, fm_run_result* out);
+void sim_profile(Sim& s, int64_t steps, double* ms, int64_t* counts, int cap, int* nfam);
+void sim_snapshot(Sim& s);
+void sim_restore(Sim& s);
 
 // topology (topo.cu)
 void build_topology(Sim& s, const Grid& g);

@@ -594,6 +594,56 @@ std::vector<int64_t> reference_order(const Grid& g, std::vector<int8_t>* lo, std
   return perm;
 }
 
+namespace {
+__global__ void k_rowmajor_to_node(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                   int l, int M, uint64_t nodes, int back) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= nodes) return;
+  int i, j;
+  node_ij(l, n, M, i, j);
+  const size_t r = size_t(j) * (M << l) + i;
+  if (back)
+    out[r] = in[n];
+  else
+    out[n] = in[r];
+}
+}  // namespace
+
+void grade_flags_host(int L, int M, int N, bool graded, uint8_t* flags) {
+  cudaStream_t st = stream();
+  std::vector<DBuf<uint8_t>> f(L);
+  std::vector<DBuf<int32_t>> cnt(L);
+  size_t at = 0;
+  for (int l = 0; l < L; ++l) {
+    const uint64_t nodes = uint64_t(M) * N << (2 * l);
+    DBuf<uint8_t> rm;
+    rm.upload(flags + at, nodes);
+    f[l].alloc(nodes);
+    cnt[l].alloc(nodes);
+    k_rowmajor_to_node<<<blocks_for(nodes, 256), 256, 0, st>>>(rm.p, f[l].p, l, M, nodes, 0);
+    FM_LAUNCHED();
+    FM_CUDA(cudaStreamSynchronize(st));
+    at += nodes;
+  }
+  for (int l = L - 1; l >= 0; --l) {
+    const uint64_t nodes = uint64_t(M) * N << (2 * l);
+    k_grade_count<<<blocks_for(nodes, 256), 256, 0, st>>>(
+        f[l].p, l + 1 < L ? f[l + 1].p : nullptr, cnt[l].p, l + 1 < L ? cnt[l + 1].p : nullptr, l,
+        L, M, N, nodes, graded ? 1 : 0);
+    FM_LAUNCHED();
+  }
+  at = 0;
+  for (int l = 0; l < L; ++l) {
+    const uint64_t nodes = uint64_t(M) * N << (2 * l);
+    DBuf<uint8_t> rm(nodes);
+    k_rowmajor_to_node<<<blocks_for(nodes, 256), 256, 0, st>>>(f[l].p, rm.p, l, M, nodes, 1);
+    FM_LAUNCHED();
+    rm.download(flags + at, nodes);
+    FM_CUDA(cudaStreamSynchronize(st));
+    at += nodes;
+  }
+}
+
 void project_planes(const fm_raster* r, int L, int M, int N, DBuf<double>& out) {
   cudaStream_t st = stream();
   const size_t nv = size_t(r->ncols) * r->nrows;

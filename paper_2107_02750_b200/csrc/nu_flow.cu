@@ -55,6 +55,27 @@ __device__ __forceinline__ Pt limit(const double s[9], const P3& zc, double cx, 
   return p;
 }
 
+// P2 geometry (power-of-two element sizes, every coordinate exactly
+// representable; checked on the host, Sim::p2): a point at offset (rx, ry)
+// from the element centre in units of its size, rx, ry in {0, +-1/4, +-1/2}.
+// There (x - xc) = rx R exactly and ((A (rx R)) / R) == A rx bit-for-bit, so
+// evaluate (field.cpp:21-24) needs no division.
+__device__ __forceinline__ double eval_rel(double c0, double cx, double cy, double rx, double ry) {
+  return c0 + cx * 2.0 * kS3 * rx + cy * 2.0 * kS3 * ry;
+}
+__device__ __forceinline__ Pt limit_rel(const double s[9], const P3& zc, double rx, double ry,
+                                        double hdry) {
+  Pt p;
+  p.h = smax(0.0, eval_rel(s[0], s[1], s[2], rx, ry));
+  p.qx = eval_rel(s[3], s[4], s[5], rx, ry);
+  p.qy = eval_rel(s[6], s[7], s[8], rx, ry);
+  p.z = eval_rel(zc.c0, zc.cx, zc.cy, rx, ry);
+  p.eta = p.h + p.z;
+  p.u = vel(p.h, p.qx, hdry);
+  p.v = vel(p.h, p.qy, hdry);
+  return p;
+}
+
 __device__ __forceinline__ void load9(const double* __restrict__ a, long long k, double s[9]) {
   const double* p = a + 9 * k;
 #pragma unroll
@@ -248,7 +269,7 @@ __global__ void __launch_bounds__(256) k_head_friction(NuView v, DevClock* clk, 
   if (!go || k >= v.n) return;
   double s[9];
   load9(src, k, s);
-  friction(s, v.nman[k], v.g, v.hdry, dt);
+  friction(s, v.nman[k], v.g, v.hdry, dt, v.libm);
   double* o = dst + 9 * k;
 #pragma unroll
   for (int q = 0; q < 9; ++q) o[q] = s[q];
@@ -257,7 +278,7 @@ __global__ void __launch_bounds__(256) k_head_friction(NuView v, DevClock* clk, 
 // ---- one RK stage over all leaves ---------------------------------------
 // STAGE 1: out = positivity(U + dt L(U))          -> U*  (FV1: the full step)
 // STAGE 2: out = positivity(((U* + dt L(U*)) + U) / 2) -> U (in place)
-template <int STAGE>
+template <int STAGE, bool P2>
 __global__ void __launch_bounds__(128) k_stage(NuView v, const DevClock* __restrict__ clk,
                                                 DevRed* red, const double* __restrict__ in,
                                                 const double* uold, double* out, int last,
@@ -273,7 +294,8 @@ __global__ void __launch_bounds__(128) k_stage(NuView v, const DevClock* __restr
   if (valid) {
     const int l = v.lvl[k], i = v.li[k], j = v.lj[k];
     sz = lsize(v, l);
-    const double cx = lcen(v.x0, v, l, i), cy = lcen(v.y0, v, l, j);
+    const double inv = 1.0 / sz;
+    const double cx = P2 ? 0.0 : lcen(v.x0, v, l, i), cy = P2 ? 0.0 : lcen(v.y0, v, l, j);
     key = leaf_key(l, i, j);
     double s[9];
     load9(in, k, s);
@@ -286,34 +308,62 @@ __global__ void __launch_bounds__(128) k_stage(NuView v, const DevClock* __restr
       const int kind = (code >> (2 * sd)) & 3;
       const bool xn = sd == 1 || sd == 3;
       const bool mine_left = sd == 0 || sd == 1;
-      const double fx = cx + (sd == 1 ? sz / 2 : sd == 3 ? -sz / 2 : 0.0);
-      const double fy = cy + (sd == 0 ? sz / 2 : sd == 2 ? -sz / 2 : 0.0);
-      const Pt me = limit(s, zc, cx, cy, sz, fx, fy, v.hdry);
+      // side-centre offsets in units of the element size
+      const double ox = sd == 1 ? 0.5 : sd == 3 ? -0.5 : 0.0;
+      const double oy = sd == 0 ? 0.5 : sd == 2 ? -0.5 : 0.0;
+      const double fx = P2 ? 0.0 : cx + (sd == 1 ? sz / 2 : sd == 3 ? -sz / 2 : 0.0);
+      const double fy = P2 ? 0.0 : cy + (sd == 0 ? sz / 2 : sd == 2 ? -sz / 2 : 0.0);
+      const Pt me = P2 ? limit_rel(s, zc, ox, oy, v.hdry) : limit(s, zc, cx, cy, sz, fx, fy, v.hdry);
       Flx sf[2];
       double szs[2], shm[2], sw[2];
       const int nseg = kind == 0 ? 0 : kind == 3 ? 2 : 1;
       for (int t = 0; t < nseg; ++t) {
         const int q = v.nb[8 * k + 2 * sd + t];
-        const int ql = v.lvl[q];
-        const double qsz = lsize(v, ql);
-        const double qcx = lcen(v.x0, v, ql, v.li[q]), qcy = lcen(v.y0, v, ql, v.lj[q]);
-        // enumerate_faces (quadgrid.cpp:222-245): the owner (coarser leaf, or
-        // W/S leaf at equal level) fixes the normal coordinate from its own
-        // face; the tangential coordinate is the other leaf's centre.
-        const bool owner_me = kind == 3 || (kind == 2 && mine_left);
-        double segx, segy, len;
-        if (xn) {
-          segx = owner_me ? cx + (sd == 1 ? sz / 2 : -sz / 2) : qcx + (sd == 1 ? -qsz / 2 : qsz / 2);
-          segy = owner_me ? qcy : cy;
-        } else {
-          segy = owner_me ? cy + (sd == 0 ? sz / 2 : -sz / 2) : qcy + (sd == 0 ? -qsz / 2 : qsz / 2);
-          segx = owner_me ? qcx : cx;
-        }
-        len = owner_me ? smin(sz, qsz) : smin(qsz, sz);
-        const Pt pm = (segx == fx && segy == fy) ? me : limit(s, zc, cx, cy, sz, segx, segy, v.hdry);
         double sq[9];
         load9(in, q, sq);
-        const Pt pn = limit(sq, load3(v.z, q), qcx, qcy, qsz, segx, segy, v.hdry);
+        const P3 zq = load3(v.z, q);
+        Pt pm, pn;
+        if (P2) {
+          // enumerate_faces geometry (quadgrid.cpp:222-245) as offsets: the
+          // segment centre sits on the owner's face, at the non-owner's centre
+          // along the face.
+          if (kind == 3) {  // two finer neighbours, S->N / W->E
+            const double tan = t == 0 ? -0.25 : 0.25;
+            pm = limit_rel(s, zc, xn ? ox : tan, xn ? tan : oy, v.hdry);
+          } else {
+            pm = me;
+          }
+          double nx = -ox, ny = -oy;
+          if (kind == 1) {  // coarser neighbour: I sit in one half of its face
+            const double tan = ((xn ? j : i) & 1) ? 0.25 : -0.25;
+            if (xn)
+              ny = tan;
+            else
+              nx = tan;
+          }
+          pn = limit_rel(sq, zq, nx, ny, v.hdry);
+          sw[t] = kind == 3 ? 0.5 : 1.0;
+        } else {
+          const int ql = v.lvl[q];
+          const double qsz = lsize(v, ql);
+          const double qcx = lcen(v.x0, v, ql, v.li[q]), qcy = lcen(v.y0, v, ql, v.lj[q]);
+          // enumerate_faces (quadgrid.cpp:222-245): the owner (coarser leaf, or
+          // W/S leaf at equal level) fixes the normal coordinate from its own
+          // face; the tangential coordinate is the other leaf's centre.
+          const bool owner_me = kind == 3 || (kind == 2 && mine_left);
+          double segx, segy;
+          if (xn) {
+            segx = owner_me ? cx + (sd == 1 ? sz / 2 : -sz / 2) : qcx + (sd == 1 ? -qsz / 2 : qsz / 2);
+            segy = owner_me ? qcy : cy;
+          } else {
+            segy = owner_me ? cy + (sd == 0 ? sz / 2 : -sz / 2) : qcy + (sd == 0 ? -qsz / 2 : qsz / 2);
+            segx = owner_me ? qcx : cx;
+          }
+          const double len = owner_me ? smin(sz, qsz) : smin(qsz, sz);
+          pm = (segx == fx && segy == fy) ? me : limit(s, zc, cx, cy, sz, segx, segy, v.hdry);
+          pn = limit(sq, zq, qcx, qcy, qsz, segx, segy, v.hdry);
+          sw[t] = len / sz;
+        }
         const Pt& A = mine_left ? pm : pn;
         const Pt& B = mine_left ? pn : pm;
         const double zs = smax(A.z, B.z);
@@ -322,7 +372,6 @@ __global__ void __launch_bounds__(128) k_stage(NuView v, const DevClock* __restr
                    : hll(hl, hl * A.v, hl * A.u, hr, hr * B.v, hr * B.u, v.g, v.hdry, err);
         szs[t] = zs;
         shm[t] = mine_left ? hl : hr;
-        sw[t] = len / sz;
       }
       double zstar;
       if (kind == 0) {
@@ -370,8 +419,8 @@ __global__ void __launch_bounds__(128) k_stage(NuView v, const DevClock* __restr
                    0.5 * (eqy[0] + eqy[2]), (eqy[0] - eqy[2]) * kHalfInvS3,
                    (ezd[0] - ezd[2]) * kHalfInvS3};
     double Lr[9];
-    l_operator(side_f[0], side_f[1], side_f[2], side_f[3], X, Y, sz, v.g, v.hdry,
-               v.scheme == FM_DG2, Lr);
+    l_operator<P2>(side_f[0], side_f[1], side_f[2], side_f[3], X, Y, sz, inv, v.g, v.hdry,
+                   v.scheme == FM_DG2, Lr);
     if (STAGE == 1) {
 #pragma unroll
       for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
@@ -425,7 +474,7 @@ __global__ void __launch_bounds__(256) k_acc_faces(NuView v, DevClock* clk, DevR
   const double dist = 0.5 * (lsize(v, v.lvl[l]) + lsize(v, v.lvl[r]));
   const double nf = 0.5 * (v.nman[l] + v.nman[r]);
   Q = (Q - v.g * hf * dt * (er - el) / dist) /
-      (1.0 + v.g * dt * nf * nf * fabs(Q) / pow(hf, 7.0 / 3.0));
+      (1.0 + v.g * dt * nf * nf * fabs(Q) / pow73_m(hf, v.libm));
   q[s] = Q;
 }
 
@@ -468,7 +517,7 @@ __global__ void __launch_bounds__(256) k_acc_leaves(NuView v, const DevClock* __
               b = 0.0;
             } else {
               const double nf = v.nman[k];
-              b = b / (1.0 + v.g * dt * nf * nf * fabs(b) / pow(hf, 7.0 / 3.0));
+              b = b / (1.0 + v.g * dt * nf * nf * fabs(b) / pow73_m(hf, v.libm));
             }
           }
           qb[4 * k + sd] = b;
@@ -566,27 +615,52 @@ void nu_launch_step(Sim& s, bool manual, double mdt, int* err) {
   const long long n = s.n;
   if (s.scheme == FM_ACC) {
     const long long ns = std::max<long long>(s.nseg, 1);
+    kt_begin(KF_ACC_FACES);
     k_acc_faces<<<nblk(ns, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.u.p, s.accq.p, manual, mdt);
     FM_LAUNCHED();
+    kt_end();
+    kt_begin(KF_ACC_LEAVES);
     k_acc_leaves<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.u.p, s.accq.p, s.accqb.p, manual, mdt);
     FM_LAUNCHED();
+    kt_end();
   } else if (s.scheme == FM_FV1) {
     // FV1 state lives in U* between steps; the head moves it to U with friction
+    kt_begin(KF_HEAD);
     k_head_friction<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.us.p, s.u.p, manual, mdt);
     FM_LAUNCHED();
-    k_stage<1><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
+    kt_end();
+    kt_begin(KF_STAGE1);
+    if (s.p2)
+      k_stage<1, true><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
+    else
+      k_stage<1, false><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
     FM_LAUNCHED();
+    kt_end();
   } else {
+    kt_begin(KF_HEAD);
     k_head_friction<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.u.p, s.u.p, manual, mdt);
     FM_LAUNCHED();
-    k_stage<1><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
+    kt_end();
+    kt_begin(KF_STAGE1);
+    if (s.p2)
+      k_stage<1, true><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
+    else
+      k_stage<1, false><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
     FM_LAUNCHED();
-    k_stage<2><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+    kt_end();
+    kt_begin(KF_STAGE2);
+    if (s.p2)
+      k_stage<2, true><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+    else
+      k_stage<2, false><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
     FM_LAUNCHED();
+    kt_end();
   }
   if (!manual) {
+    kt_begin(KF_COMMIT);
     k_commit<<<1, 1, 0, st>>>(clk);
     FM_LAUNCHED();
+    kt_end();
   }
 }
 

@@ -51,6 +51,35 @@ double elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
   return double(ms);
 }
 
+const char* kernel_family_name(int f) {
+  static const char* names[KF_COUNT] = {"k_head_friction", "k_stage<1>",     "k_stage<2>",
+                                        "k_commit",        "k_acc_faces",    "k_acc_leaves",
+                                        "k_uni_head",      "k_uni_stage<1>", "k_uni_stage<2>"};
+  return f >= 0 && f < KF_COUNT ? names[f] : "?";
+}
+
+KTimer& ktimer() {
+  static thread_local KTimer t;
+  return t;
+}
+void kt_begin(int fam) {
+  KTimer& t = ktimer();
+  if (!t.on) return;
+  cudaEvent_t e;
+  FM_CUDA(cudaEventCreate(&e));
+  FM_CUDA(cudaEventRecord(e, stream()));
+  t.fam.push_back(fam);
+  t.a.push_back(e);
+}
+void kt_end() {
+  KTimer& t = ktimer();
+  if (!t.on) return;
+  cudaEvent_t e;
+  FM_CUDA(cudaEventCreate(&e));
+  FM_CUDA(cudaEventRecord(e, stream()));
+  t.b.push_back(e);
+}
+
 // The filter banks are compile-time constants (fmd::tap); nothing to upload.
 void upload_banks() {}
 

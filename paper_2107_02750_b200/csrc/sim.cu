@@ -121,6 +121,7 @@ NuView Sim::view() const {
   v.scheme = scheme;
   v.adaptive = adaptive ? 1 : 0;
   v.ninflow = ninflow;
+  v.libm = libm;
   v.R = R;
   v.x0 = x0;
   v.y0 = y0;
@@ -162,6 +163,7 @@ double courant_for(const fm_sim_desc* d) {  // config.cpp:37-47
 void common_params(Sim& s, const fm_sim_desc* d) {
   if (d->solver < FM_DG2 || d->solver > FM_HWFV1) throw Error(FM_ERR_CONFIG, "unknown solver");
   s.solver = d->solver;
+  s.libm = d->libm;
   s.scheme = d->solver == FM_MWDG2 ? FM_DG2 : d->solver == FM_HWFV1 ? FM_FV1 : d->solver;
   s.g = d->g;
   s.hdry = d->h_dry;
@@ -217,6 +219,23 @@ void common_params(Sim& s, const fm_sim_desc* d) {
 
 }  // namespace
 
+// The P2 fast path (Sim::p2) is exact when the fine cell size R is a power of
+// two, the origin is a multiple of R/4 and every coordinate (and the R/4
+// offsets of sub-face centres) is an exact double: then x - xc is exactly
+// rx * size for rx in {0, +-1/4, +-1/2}, as the reference computes it.
+bool geometry_is_p2(double R, double x0, double y0, int L, int M, int N) {
+  if (!(R > 0.0) || !std::isfinite(R)) return false;
+  int e = 0;
+  if (std::frexp(R, &e) != 0.5) return false;
+  const double q = R / 4.0;
+  for (double o : {x0, y0}) {
+    const double k = o / q;
+    if (k != std::floor(k) || std::fabs(k) > 1e15) return false;
+  }
+  const double ext = double(std::max(M, N)) * std::ldexp(1.0, L) * R;
+  return std::fabs(x0) / q + ext / q < 9.0e15 && std::fabs(y0) / q + ext / q < 9.0e15;
+}
+
 // Static non-uniform sim from a device grid (solver_nonuniform.cpp:558-636).
 static void nonuniform_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem, const Grid& g) {
   cudaStream_t st = stream();
@@ -226,6 +245,7 @@ static void nonuniform_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem, 
   s.R = g.R;
   s.x0 = g.x0;
   s.y0 = g.y0;
+  s.p2 = geometry_is_p2(s.R, s.x0, s.y0, s.L, s.M, s.N);
   s.n = g.nleaves;
   const long long n = s.n;
   s.lvl.alloc(n);
@@ -613,6 +633,88 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
   if (c.blew_up) key_xy(s, c.bad_key, &r.bad_x, &r.bad_y);
   if (out) *out = r;
   if (c.blew_up) throw Error(FM_ERR_BLOWUP, "solver state is non-finite");
+}
+
+}  // namespace fmh
+
+namespace fmh {
+
+// Per-kernel timing of `steps` device-loop steps launched without a graph.
+void sim_profile(Sim& s, int64_t steps, double* ms, int64_t* counts, int cap, int* nfam) {
+  cudaStream_t st = stream();
+  if (fv1_staged(s)) fv1_to_star(s);
+  fm_clock ck{1e12, 0.0, 10.0, 0.0, 1, 1};
+  DevClock c0 = fresh_clock(&ck, steps, 0);
+  DevClock pair[2] = {c0, c0};
+  s.clk.upload(pair, 2);
+  init_red(s);
+  launch_reduce_init(s);
+  s.errflag.alloc(1);
+  s.errflag.zero();
+  KTimer& t = ktimer();
+  t = KTimer{};
+  t.on = true;
+  try {
+    for (int64_t k = 0; k < steps; ++k) launch_step(s, false, 0.0, s.errflag.p);
+  } catch (...) {
+    t.on = false;
+    throw;
+  }
+  t.on = false;
+  FM_CUDA(cudaStreamSynchronize(st));
+  std::vector<double> acc(KF_COUNT, 0.0);
+  std::vector<int64_t> cnt(KF_COUNT, 0);
+  for (size_t q = 0; q < t.fam.size(); ++q) {
+    acc[t.fam[q]] += elapsed_ms(t.a[q], t.b[q]);
+    cnt[t.fam[q]] += 1;
+    cudaEventDestroy(t.a[q]);
+    cudaEventDestroy(t.b[q]);
+  }
+  t = KTimer{};
+  for (int f = 0; f < std::min(cap, int(KF_COUNT)); ++f) {
+    if (ms) ms[f] = acc[f];
+    if (counts) counts[f] = cnt[f];
+  }
+  *nfam = KF_COUNT;
+  nu_launch_close(s);
+  FM_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace fmh
+
+namespace fmh {
+
+void sim_snapshot(Sim& s) {
+  auto copy = [](DBuf<double>& dst, const DBuf<double>& src) {
+    dst.alloc(src.n);
+    if (src.n)
+      FM_CUDA(cudaMemcpyAsync(dst.p, src.p, src.n * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+  };
+  copy(s.snap_u, s.u);
+  copy(s.snap_us, s.us);
+  copy(s.snap_q, s.accq);
+  copy(s.snap_qb, s.accqb);
+  copy(s.snap_aqx, s.aqx);
+  copy(s.snap_aqy, s.aqy);
+  s.snap_n = s.n;
+  s.snap_fv1 = s.fv1_in_star;
+  FM_CUDA(cudaStreamSynchronize(stream()));
+}
+
+void sim_restore(Sim& s) {
+  if (s.snap_n != s.n || s.snap_u.n != s.u.n) throw Error(FM_ERR_CONFIG, "restore: no matching snapshot");
+  auto copy = [](DBuf<double>& dst, const DBuf<double>& src) {
+    if (src.n)
+      FM_CUDA(cudaMemcpyAsync(dst.p, src.p, src.n * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+  };
+  copy(s.u, s.snap_u);
+  copy(s.us, s.snap_us);
+  copy(s.accq, s.snap_q);
+  copy(s.accqb, s.snap_qb);
+  copy(s.aqx, s.snap_aqx);
+  copy(s.aqy, s.snap_aqy);
+  s.fv1_in_star = s.snap_fv1;
+  FM_CUDA(cudaStreamSynchronize(stream()));
 }
 
 }  // namespace fmh
