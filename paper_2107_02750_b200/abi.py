@@ -121,6 +121,7 @@ OPTIONAL = {
     "generate_static_grid": (C.c_int, [C.POINTER(c_raster), I32, D, I32, I32, PI64]),
     "grade_flags": (C.c_int, [I32, I32, I32, I32, PU8]),
     "pcbrt": (D, [D]),
+    "selftest": (C.c_int, [I32, I64, C.c_uint64, PI64]),
     "hll": (None, [D, D, D, D, D, D, D, D, PD]),
     "friction": (None, [D, PD, PD, D, D, D, D]),
     "encode": (None, [PD, I32, PD, PD]),

@@ -67,6 +67,42 @@ __global__ void k_near(const double* __restrict__ det, uint64_t nodes, double no
 }
 
 inline unsigned nblk(uint64_t n) { return unsigned((n + 255) / 256); }
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {  // splitmix64
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+// Random operands: random sign and mantissa, exponent drawn across (and a
+// little beyond) the fast-path window, with hard mantissa patterns mixed in.
+__device__ __forceinline__ double rand_operand(uint64_t r, uint64_t r2) {
+  uint64_t mant = r & 0x000fffffffffffffull;
+  switch (r2 & 7) {
+    case 0: mant = 0; break;                                // exact powers of two
+    case 1: mant = 0x000fffffffffffffull; break;            // all ones
+    case 2: mant &= 0xffffffffull << 20; break;             // short mantissas
+    default: break;
+  }
+  // every biased exponent 0..2046 (zero/subnormal at 0), weighted toward the
+  // fast-path window edges half of the time
+  uint64_t e = (r2 >> 3) % 2047;
+  if ((r2 >> 20) & 1) e = ((r2 >> 21) & 1 ? 40 : 2020) + ((r2 >> 22) % 40);
+  const uint64_t sign = (r2 >> 40) & 1;
+  return __longlong_as_double(static_cast<long long>((sign << 63) | (e << 52) | mant));
+}
+
+__global__ void k_selftest_div(int64_t n, uint64_t seed, unsigned long long* fails) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= n) return;
+  const uint64_t a1 = mix64(seed ^ (2 * k)), a2 = mix64(a1), b1 = mix64(a2), b2 = mix64(b1);
+  const double a = rand_operand(a1, a2), b = rand_operand(b1, b2);
+  // the inline division kernel builds use with -DFM_INLINE_DIV (fmd::quot)
+  const double q = (fmd::div_fast_ok(a) && fmd::div_fast_ok(b)) ? fmd::quot(a, b, fmd::recip(b)) : a / b;
+  const double ref = a / b;
+  if (__double_as_longlong(q) != __double_as_longlong(ref)) atomicAdd(fails, 1ull);
+}
 }  // namespace
 
 struct fm_grid {
@@ -97,6 +133,21 @@ int fm_synchronize(void) {
 }
 
 int64_t fm_launch_count(void) { return launches(); }
+
+int fm_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* failures) {
+  return guard([&] {
+    require_device();
+    if (which != 0) throw Error(FM_ERR_CONFIG, "unknown self-test");
+    DBuf<unsigned long long> f(1);
+    f.zero();
+    k_selftest_div<<<unsigned((n + 255) / 256), 256, 0, stream()>>>(n, seed, f.p);
+    FM_LAUNCHED();
+    unsigned long long v = 0;
+    f.download(&v, 1);
+    FM_CUDA(cudaStreamSynchronize(stream()));
+    *failures = int64_t(v);
+  });
+}
 
 int fm_mra_static(const fm_raster* dem, int32_t L, double eps, int32_t graded, int32_t kind,
                   fm_grid** out) {

@@ -50,8 +50,7 @@ __device__ __forceinline__ Pt limit(const double s[9], const P3& zc, double cx, 
   p.qy = eval_plane(P3{s[6], s[7], s[8]}, cx, cy, sz, x, y);
   p.z = eval_plane(zc, cx, cy, sz, x, y);
   p.eta = p.h + p.z;
-  p.u = vel(p.h, p.qx, hdry);
-  p.v = vel(p.h, p.qy, hdry);
+  vel2(p.h, p.qx, p.qy, hdry, p.u, p.v);
   return p;
 }
 
@@ -71,8 +70,7 @@ __device__ __forceinline__ Pt limit_rel(const double s[9], const P3& zc, double 
   p.qy = eval_rel(s[6], s[7], s[8], rx, ry);
   p.z = eval_rel(zc.c0, zc.cx, zc.cy, rx, ry);
   p.eta = p.h + p.z;
-  p.u = vel(p.h, p.qx, hdry);
-  p.v = vel(p.h, p.qy, hdry);
+  vel2(p.h, p.qx, p.qy, hdry, p.u, p.v);
   return p;
 }
 
@@ -233,9 +231,9 @@ __device__ __forceinline__ void reduce_leaf(const NuView& v, DevRed* red, const 
       }
     } else if (h > v.hdry) {
       const double cw = sqrt(v.g * h);
-      const double sx = fabs(s[3] / h) + cw;
-      const double sy = fabs(s[6] / h) + cw;
-      dtc = sz / smax(sx, sy);
+      const double sx = fabs(zdiv(s[3], h)) + cw;
+      const double sy = fabs(zdiv(s[6], h)) + cw;
+      dtc = ddiv(sz, smax(sx, sy));
     }
     bool fin = true;
 #pragma unroll
@@ -276,180 +274,238 @@ __global__ void __launch_bounds__(256) k_head_friction(NuView v, DevClock* clk, 
 }
 
 // ---- one RK stage over all leaves ---------------------------------------
-// STAGE 1: out = positivity(U + dt L(U))          -> U*  (FV1: the full step)
+// STAGE 1: out = positivity(U + dt L(U))               -> U*  (FV1: the full step)
 // STAGE 2: out = positivity(((U* + dt L(U*)) + U) / 2) -> U (in place)
+//
+// Four threads per leaf, one per side (N, E, S, W): each evaluates its side's
+// limit (limit_at, solver_nonuniform.cpp:52-66), the HLL flux of each
+// sub-face on that side (segment_states :91-115), the side-effective starred
+// state (side_effective :117-178) and the side's flux sum with the pressure
+// correction (assemble :190-226).  The four sides' results meet in shared
+// memory; the four Gauss-point physical fluxes of the L operator are split
+// over the four lanes; then every lane forms the full update (cheap) and
+// stores a third of the leaf's 9 coefficients, so a warp writes 8 leaves'
+// 576 contiguous bytes.
+constexpr int kLeavesPerBlock = 32;
+
+struct SideOut {
+  double h, qx, qy, zd, fm, fn, ft;
+};
+
 template <int STAGE, bool P2>
-__global__ void __launch_bounds__(128) k_stage(NuView v, const DevClock* __restrict__ clk,
-                                                DevRed* red, const double* __restrict__ in,
-                                                const double* uold, double* out, int last,
-                                                int manual, double mdt, int* err) {
-  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(4 * kLeavesPerBlock) k_stage(
+    NuView v, const DevClock* __restrict__ clk, DevRed* red, const double* __restrict__ in,
+    const double* uold, double* out, int last, int manual, double mdt, int* err) {
+  __shared__ SideOut so[kLeavesPerBlock][4];
+  __shared__ double pf[kLeavesPerBlock][4][3];
+  const int sd = threadIdx.x & 3;
+  const int lq = threadIdx.x >> 2;
+  const long long k = blockIdx.x * (long long)kLeavesPerBlock + lq;
   const DevClock* c = clk + 1;
   if (!manual && !c->active) return;
   const double dt = manual ? mdt : c->dt;
   const bool valid = k < v.n;
-  double res[9];
-  double sz = 0.0;
-  unsigned long long key = 0;
-  if (valid) {
-    const int l = v.lvl[k], i = v.li[k], j = v.lj[k];
-    sz = lsize(v, l);
-    const double inv = 1.0 / sz;
-    const double cx = P2 ? 0.0 : lcen(v.x0, v, l, i), cy = P2 ? 0.0 : lcen(v.y0, v, l, j);
-    key = leaf_key(l, i, j);
-    double s[9];
-    load9(in, k, s);
-    const P3 zc = load3(v.z, k);
-    const uint8_t code = v.sk[k];
-    Flx side_f[4];
-    double eh[4], eqx[4], eqy[4], ezd[4];
-#pragma unroll
-    for (int sd = 0; sd < 4; ++sd) {
-      const int kind = (code >> (2 * sd)) & 3;
-      const bool xn = sd == 1 || sd == 3;
-      const bool mine_left = sd == 0 || sd == 1;
-      // side-centre offsets in units of the element size
-      const double ox = sd == 1 ? 0.5 : sd == 3 ? -0.5 : 0.0;
-      const double oy = sd == 0 ? 0.5 : sd == 2 ? -0.5 : 0.0;
-      const double fx = P2 ? 0.0 : cx + (sd == 1 ? sz / 2 : sd == 3 ? -sz / 2 : 0.0);
-      const double fy = P2 ? 0.0 : cy + (sd == 0 ? sz / 2 : sd == 2 ? -sz / 2 : 0.0);
-      const Pt me = P2 ? limit_rel(s, zc, ox, oy, v.hdry) : limit(s, zc, cx, cy, sz, fx, fy, v.hdry);
-      Flx sf[2];
-      double szs[2], shm[2], sw[2];
-      const int nseg = kind == 0 ? 0 : kind == 3 ? 2 : 1;
-      for (int t = 0; t < nseg; ++t) {
-        const int q = v.nb[8 * k + 2 * sd + t];
-        double sq[9];
-        load9(in, q, sq);
-        const P3 zq = load3(v.z, q);
-        Pt pm, pn;
-        if (P2) {
-          // enumerate_faces geometry (quadgrid.cpp:222-245) as offsets: the
-          // segment centre sits on the owner's face, at the non-owner's centre
-          // along the face.
-          if (kind == 3) {  // two finer neighbours, S->N / W->E
-            const double tan = t == 0 ? -0.25 : 0.25;
-            pm = limit_rel(s, zc, xn ? ox : tan, xn ? tan : oy, v.hdry);
-          } else {
-            pm = me;
-          }
-          double nx = -ox, ny = -oy;
-          if (kind == 1) {  // coarser neighbour: I sit in one half of its face
-            const double tan = ((xn ? j : i) & 1) ? 0.25 : -0.25;
-            if (xn)
-              ny = tan;
-            else
-              nx = tan;
-          }
-          pn = limit_rel(sq, zq, nx, ny, v.hdry);
-          sw[t] = kind == 3 ? 0.5 : 1.0;
+  const long long kk = valid ? k : v.n - 1;  // keep the quad's loads in bounds
+  const int l = v.lvl[kk], i = v.li[kk], j = v.lj[kk];
+  const double sz = lsize(v, l);
+  const double inv = 1.0 / sz;
+  const double cx = P2 ? 0.0 : lcen(v.x0, v, l, i), cy = P2 ? 0.0 : lcen(v.y0, v, l, j);
+  double s[9];
+  load9(in, kk, s);
+  const P3 zc = load3(v.z, kk);
+  const int kind = (v.sk[kk] >> (2 * sd)) & 3;
+  const bool xn = sd == 1 || sd == 3;
+  const bool mine_left = sd == 0 || sd == 1;
+  {
+    // ---- this lane's side -------------------------------------------------
+    const double ox = sd == 1 ? 0.5 : sd == 3 ? -0.5 : 0.0;
+    const double oy = sd == 0 ? 0.5 : sd == 2 ? -0.5 : 0.0;
+    const double fx = P2 ? 0.0 : cx + (sd == 1 ? sz / 2 : sd == 3 ? -sz / 2 : 0.0);
+    const double fy = P2 ? 0.0 : cy + (sd == 0 ? sz / 2 : sd == 2 ? -sz / 2 : 0.0);
+    const Pt me = P2 ? limit_rel(s, zc, ox, oy, v.hdry) : limit(s, zc, cx, cy, sz, fx, fy, v.hdry);
+    const int nseg = kind == 0 ? 0 : kind == 3 ? 2 : 1;
+    Flx sf[2];
+    double szs[2], shm[2], sw[2];
+#pragma unroll 1
+    for (int t = 0; t < nseg; ++t) {
+      const int q = v.nb[8 * kk + 2 * sd + t];
+      double sq[9];
+      load9(in, q, sq);
+      const P3 zq = load3(v.z, q);
+      Pt pm, pn;
+      if (P2) {
+        // enumerate_faces geometry (quadgrid.cpp:222-245) as exact offsets: the
+        // segment centre sits on the owner's face, at the non-owner's centre
+        // along the face.
+        if (kind == 3) {  // two finer neighbours, S->N / W->E
+          const double tan = t == 0 ? -0.25 : 0.25;
+          pm = limit_rel(s, zc, xn ? ox : tan, xn ? tan : oy, v.hdry);
         } else {
-          const int ql = v.lvl[q];
-          const double qsz = lsize(v, ql);
-          const double qcx = lcen(v.x0, v, ql, v.li[q]), qcy = lcen(v.y0, v, ql, v.lj[q]);
-          // enumerate_faces (quadgrid.cpp:222-245): the owner (coarser leaf, or
-          // W/S leaf at equal level) fixes the normal coordinate from its own
-          // face; the tangential coordinate is the other leaf's centre.
-          const bool owner_me = kind == 3 || (kind == 2 && mine_left);
-          double segx, segy;
-          if (xn) {
-            segx = owner_me ? cx + (sd == 1 ? sz / 2 : -sz / 2) : qcx + (sd == 1 ? -qsz / 2 : qsz / 2);
-            segy = owner_me ? qcy : cy;
-          } else {
-            segy = owner_me ? cy + (sd == 0 ? sz / 2 : -sz / 2) : qcy + (sd == 0 ? -qsz / 2 : qsz / 2);
-            segx = owner_me ? qcx : cx;
-          }
-          const double len = owner_me ? smin(sz, qsz) : smin(qsz, sz);
-          pm = (segx == fx && segy == fy) ? me : limit(s, zc, cx, cy, sz, segx, segy, v.hdry);
-          pn = limit(sq, zq, qcx, qcy, qsz, segx, segy, v.hdry);
-          sw[t] = len / sz;
+          pm = me;
         }
-        const Pt& A = mine_left ? pm : pn;
-        const Pt& B = mine_left ? pn : pm;
-        const double zs = smax(A.z, B.z);
-        const double hl = smax(0.0, A.eta - zs), hr = smax(0.0, B.eta - zs);
-        sf[t] = xn ? hll(hl, hl * A.u, hl * A.v, hr, hr * B.u, hr * B.v, v.g, v.hdry, err)
-                   : hll(hl, hl * A.v, hl * A.u, hr, hr * B.v, hr * B.u, v.g, v.hdry, err);
-        szs[t] = zs;
-        shm[t] = mine_left ? hl : hr;
-      }
-      double zstar;
-      if (kind == 0) {
-        zstar = me.z;
-      } else if (nseg == 1) {
-        zstar = szs[0];
-      } else if (v.zpair) {
-        zstar = smax(me.z, v.zpair[4 * k + sd]);
-      } else {
-        double acc = 0.0;
-        acc += sw[0] * szs[0];
-        acc += sw[1] * szs[1];
-        zstar = acc;
-      }
-      const double h = smax(0.0, me.eta - zstar);
-      eh[sd] = h;
-      eqx[sd] = h * me.u;
-      eqy[sd] = h * me.v;
-      ezd[sd] = zstar - smax(0.0, zstar - me.eta);
-      Flx acc{0.0, 0.0, 0.0};
-      if (kind == 0) {
-        const double qn = xn ? eqx[sd] : eqy[sd], qt = xn ? eqy[sd] : eqx[sd];
-        const double qg = v.bc[sd] == FM_REFLECTIVE ? -qn : qn;
-        const Flx f = mine_left ? hll(h, qn, qt, h, qg, qt, v.g, v.hdry, err)
-                                : hll(h, qg, qt, h, qn, qt, v.g, v.hdry, err);
-        acc.m += f.m;
-        acc.n += f.n;
-        acc.t += f.t;
-      } else {
-        for (int t = 0; t < nseg; ++t) {
-          const double corr = 0.5 * v.g * (h * h - shm[t] * shm[t]);
-          acc.m += sw[t] * sf[t].m;
-          acc.n += sw[t] * (sf[t].n + corr);
-          acc.t += sw[t] * sf[t].t;
+        double nx = -ox, ny = -oy;
+        if (kind == 1) {  // coarser neighbour: I sit in one half of its face
+          const double tan = ((xn ? j : i) & 1) ? 0.25 : -0.25;
+          if (xn)
+            ny = tan;
+          else
+            nx = tan;
         }
+        pn = limit_rel(sq, zq, nx, ny, v.hdry);
+        sw[t] = kind == 3 ? 0.5 : 1.0;
+      } else {
+        const int ql = v.lvl[q];
+        const double qsz = lsize(v, ql);
+        const double qcx = lcen(v.x0, v, ql, v.li[q]), qcy = lcen(v.y0, v, ql, v.lj[q]);
+        // enumerate_faces (quadgrid.cpp:222-245): the owner (coarser leaf, or
+        // W/S leaf at equal level) fixes the normal coordinate from its own
+        // face; the tangential coordinate is the other leaf's centre.
+        const bool owner_me = kind == 3 || (kind == 2 && mine_left);
+        double segx, segy;
+        if (xn) {
+          segx = owner_me ? cx + (sd == 1 ? sz / 2 : -sz / 2) : qcx + (sd == 1 ? -qsz / 2 : qsz / 2);
+          segy = owner_me ? qcy : cy;
+        } else {
+          segy = owner_me ? cy + (sd == 0 ? sz / 2 : -sz / 2) : qcy + (sd == 0 ? -qsz / 2 : qsz / 2);
+          segx = owner_me ? qcx : cx;
+        }
+        const double len = owner_me ? smin(sz, qsz) : smin(qsz, sz);
+        pm = (segx == fx && segy == fy) ? me : limit(s, zc, cx, cy, sz, segx, segy, v.hdry);
+        pn = limit(sq, zq, qcx, qcy, qsz, segx, segy, v.hdry);
+        sw[t] = len / sz;
       }
-      side_f[sd] = acc;
+      const Pt& A = mine_left ? pm : pn;
+      const Pt& B = mine_left ? pn : pm;
+      const double zs = smax(A.z, B.z);
+      const double hl = smax(0.0, A.eta - zs), hr = smax(0.0, B.eta - zs);
+      sf[t] = xn ? hll(hl, hl * A.u, hl * A.v, hr, hr * B.u, hr * B.v, v.g, v.hdry, err)
+                 : hll(hl, hl * A.v, hl * A.u, hr, hr * B.v, hr * B.u, v.g, v.hdry, err);
+      szs[t] = zs;
+      shm[t] = mine_left ? hl : hr;
     }
-    const DirMod X{0.5 * (eh[1] + eh[3]),   (eh[1] - eh[3]) * kHalfInvS3,
-                   0.5 * (eqx[1] + eqx[3]), (eqx[1] - eqx[3]) * kHalfInvS3,
-                   0.5 * (eqy[1] + eqy[3]), (eqy[1] - eqy[3]) * kHalfInvS3,
-                   (ezd[1] - ezd[3]) * kHalfInvS3};
-    const DirMod Y{0.5 * (eh[0] + eh[2]),   (eh[0] - eh[2]) * kHalfInvS3,
-                   0.5 * (eqx[0] + eqx[2]), (eqx[0] - eqx[2]) * kHalfInvS3,
-                   0.5 * (eqy[0] + eqy[2]), (eqy[0] - eqy[2]) * kHalfInvS3,
-                   (ezd[0] - ezd[2]) * kHalfInvS3};
-    double Lr[9];
-    l_operator<P2>(side_f[0], side_f[1], side_f[2], side_f[3], X, Y, sz, inv, v.g, v.hdry,
-                   v.scheme == FM_DG2, Lr);
-    if (STAGE == 1) {
-#pragma unroll
-      for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
+    double zstar;
+    if (kind == 0) {
+      zstar = me.z;
+    } else if (nseg == 1) {
+      zstar = szs[0];
+    } else if (v.zpair) {
+      zstar = smax(me.z, v.zpair[4 * kk + sd]);
     } else {
-      double u0[9];
-      load9(uold, k, u0);
-#pragma unroll
-      for (int q = 0; q < 9; ++q) {
-        double a = s[q];
-        a += Lr[q] * dt;
-        a += u0[q];
-        a *= 0.5;
-        res[q] = a;
+      double acc = 0.0;
+      acc += sw[0] * szs[0];
+      acc += sw[1] * szs[1];
+      zstar = acc;
+    }
+    SideOut o;
+    const double h = smax(0.0, me.eta - zstar);
+    o.h = h;
+    o.qx = h * me.u;
+    o.qy = h * me.v;
+    o.zd = zstar - smax(0.0, zstar - me.eta);
+    Flx acc{0.0, 0.0, 0.0};
+    if (kind == 0) {
+      const double qn = xn ? o.qx : o.qy, qt = xn ? o.qy : o.qx;
+      const double qg = v.bc[sd] == FM_REFLECTIVE ? -qn : qn;
+      const Flx f = mine_left ? hll(h, qn, qt, h, qg, qt, v.g, v.hdry, err)
+                              : hll(h, qg, qt, h, qn, qt, v.g, v.hdry, err);
+      acc.m += f.m;
+      acc.n += f.n;
+      acc.t += f.t;
+    } else {
+      for (int t = 0; t < nseg; ++t) {
+        const double corr = 0.5 * v.g * (h * h - shm[t] * shm[t]);
+        acc.m += sw[t] * sf[t].m;
+        acc.n += sw[t] * (sf[t].n + corr);
+        acc.t += sw[t] * sf[t].t;
       }
     }
-    positivity(res, v.hdry);
-    if (last && !manual) {
-      // apply_inflows (solver_nonuniform.cpp:451-465), inflow order
-      for (int f = 0; f < v.ninflow; ++f) {
-        if (!c->on[f]) continue;
-        const int cnt = v.infc[f * v.n + k];
-        if (cnt) res[0] += c->per_cell[f] * cnt / (sz * sz);
-      }
-    }
-    double* o = out + 9 * k;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) o[q] = res[q];
+    o.fm = acc.m;
+    o.fn = acc.n;
+    o.ft = acc.t;
+    so[lq][sd] = o;
   }
-  if (last && !manual) reduce_leaf(v, red, *c, res, sz, key, valid);
+  __syncwarp();
+  const SideOut en = so[lq][0], ee = so[lq][1], es = so[lq][2], ew = so[lq][3];
+  const DirMod X{0.5 * (ee.h + ew.h),   (ee.h - ew.h) * kHalfInvS3,   0.5 * (ee.qx + ew.qx),
+                 (ee.qx - ew.qx) * kHalfInvS3, 0.5 * (ee.qy + ew.qy), (ee.qy - ew.qy) * kHalfInvS3,
+                 (ee.zd - ew.zd) * kHalfInvS3};
+  const DirMod Y{0.5 * (en.h + es.h),   (en.h - es.h) * kHalfInvS3,   0.5 * (en.qx + es.qx),
+                 (en.qx - es.qx) * kHalfInvS3, 0.5 * (en.qy + es.qy), (en.qy - es.qy) * kHalfInvS3,
+                 (en.zd - es.zd) * kHalfInvS3};
+  const bool dg2 = v.scheme == FM_DG2;
+  if (dg2) {
+    // the four Gauss-point physical fluxes (solver_nonuniform.cpp:245-266), one per lane
+    double a, b, cc;
+    if (sd == 0)
+      phys_x(X.h0 + X.h1, X.qx0 + X.qx1, X.qy0 + X.qy1, v.g, v.hdry, a, b, cc);
+    else if (sd == 1)
+      phys_x(X.h0 - X.h1, X.qx0 - X.qx1, X.qy0 - X.qy1, v.g, v.hdry, a, b, cc);
+    else if (sd == 2)
+      phys_y(Y.h0 + Y.h1, Y.qx0 + Y.qx1, Y.qy0 + Y.qy1, v.g, v.hdry, a, b, cc);
+    else
+      phys_y(Y.h0 - Y.h1, Y.qx0 - Y.qx1, Y.qy0 - Y.qy1, v.g, v.hdry, a, b, cc);
+    pf[lq][sd][0] = a;
+    pf[lq][sd][1] = b;
+    pf[lq][sd][2] = cc;
+    __syncwarp();
+  }
+  // L operator (solver_nonuniform.cpp:228-271)
+  const Flx fn{en.fm, en.fn, en.ft}, fe{ee.fm, ee.fn, ee.ft}, fs{es.fm, es.fn, es.ft},
+      fw{ew.fm, ew.fn, ew.ft};
+  double Lr[9];
+  Lr[0] = div_sz<P2>(-((fe.m - fw.m) + (fn.m - fs.m)), sz, inv);
+  Lr[3] = div_sz<P2>(-((fe.n - fw.n) + (fn.t - fs.t)), sz, inv) -
+          div_sz<P2>(v.g * X.h0 * (2.0 * kS3 * X.z1), sz, inv);
+  Lr[6] = div_sz<P2>(-((fe.t - fw.t) + (fn.n - fs.n)), sz, inv) -
+          div_sz<P2>(v.g * Y.h0 * (2.0 * kS3 * Y.z1), sz, inv);
+  if (dg2) {
+    const double kk3 = P2 ? kS3 * inv : kS3 / sz;
+    const double* xp = pf[lq][0];
+    const double* xm = pf[lq][1];
+    const double* yp = pf[lq][2];
+    const double* ym = pf[lq][3];
+    Lr[1] = -kk3 * (fe.m + fw.m - xp[0] - xm[0]);
+    Lr[4] = -kk3 * (fe.n + fw.n - xp[1] - xm[1]) - div_sz<P2>(v.g * X.h1 * (2.0 * kS3 * X.z1), sz, inv);
+    Lr[7] = -kk3 * (fe.t + fw.t - xp[2] - xm[2]);
+    Lr[2] = -kk3 * (fn.m + fs.m - yp[0] - ym[0]);
+    Lr[5] = -kk3 * (fn.t + fs.t - yp[1] - ym[1]);
+    Lr[8] = -kk3 * (fn.n + fs.n - yp[2] - ym[2]) - div_sz<P2>(v.g * Y.h1 * (2.0 * kS3 * Y.z1), sz, inv);
+  } else {
+    Lr[1] = Lr[2] = Lr[4] = Lr[5] = Lr[7] = Lr[8] = 0.0;
+  }
+  double res[9];
+  if (STAGE == 1) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
+  } else {
+    double u0[9];
+    load9(uold, kk, u0);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      double a = s[q];
+      a += Lr[q] * dt;
+      a += u0[q];
+      a *= 0.5;
+      res[q] = a;
+    }
+  }
+  positivity(res, v.hdry);
+  if (last && !manual && valid) {
+    // apply_inflows (solver_nonuniform.cpp:451-465), inflow order
+    for (int f = 0; f < v.ninflow; ++f) {
+      if (!c->on[f]) continue;
+      const int cnt = v.infc[f * v.n + kk];
+      if (cnt) res[0] += ddiv(c->per_cell[f] * cnt, sz * sz);
+    }
+  }
+  if (valid) {
+    double* o = out + 9 * kk;
+    // lane sd stores components sd, sd + 4, sd + 8 (coalesced over the warp)
+    o[sd] = res[sd];
+    o[sd + 4] = res[sd + 4];
+    if (sd == 0) o[8] = res[8];
+  }
+  if (last && !manual) reduce_leaf(v, red, *c, res, sz, leaf_key(l, i, j), valid && sd == 0);
 }
 
 // ---- ACC ------------------------------------------------------------------
@@ -473,8 +529,8 @@ __global__ void __launch_bounds__(256) k_acc_faces(NuView v, DevClock* clk, DevR
   }
   const double dist = 0.5 * (lsize(v, v.lvl[l]) + lsize(v, v.lvl[r]));
   const double nf = 0.5 * (v.nman[l] + v.nman[r]);
-  Q = (Q - v.g * hf * dt * (er - el) / dist) /
-      (1.0 + v.g * dt * nf * nf * fabs(Q) / pow73_m(hf, v.libm));
+  Q = ddiv(Q - ddiv(v.g * hf * dt * (er - el), dist),
+           1.0 + zdiv(v.g * dt * nf * nf * fabs(Q), pow73_m(hf, v.libm)));
   q[s] = Q;
 }
 
@@ -517,7 +573,7 @@ __global__ void __launch_bounds__(256) k_acc_leaves(NuView v, const DevClock* __
               b = 0.0;
             } else {
               const double nf = v.nman[k];
-              b = b / (1.0 + v.g * dt * nf * nf * fabs(b) / pow73_m(hf, v.libm));
+              b = zdiv(b, 1.0 + zdiv(v.g * dt * nf * nf * fabs(b), pow73_m(hf, v.libm)));
             }
           }
           qb[4 * k + sd] = b;
@@ -537,14 +593,14 @@ __global__ void __launch_bounds__(256) k_acc_leaves(NuView v, const DevClock* __
           sy += Q * len;
       }
     }
-    s[0] += dt * net / area;
-    s[3] = 0.5 * sx / sz;
-    s[6] = 0.5 * sy / sz;
+    s[0] += zdiv(dt * net, area);
+    s[3] = zdiv(0.5 * sx, sz);
+    s[6] = zdiv(0.5 * sy, sz);
     if (!manual) {
       for (int f = 0; f < v.ninflow; ++f) {
         if (!c->on[f]) continue;
         const int cnt = v.infc[f * v.n + k];
-        if (cnt) s[0] += c->per_cell[f] * cnt / area;
+        if (cnt) s[0] += ddiv(c->per_cell[f] * cnt, area);
       }
     }
     u[9 * k] = s[0];
@@ -631,9 +687,9 @@ void nu_launch_step(Sim& s, bool manual, double mdt, int* err) {
     kt_end();
     kt_begin(KF_STAGE1);
     if (s.p2)
-      k_stage<1, true><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
+      k_stage<1, true><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
     else
-      k_stage<1, false><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
+      k_stage<1, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
     FM_LAUNCHED();
     kt_end();
   } else {
@@ -643,16 +699,16 @@ void nu_launch_step(Sim& s, bool manual, double mdt, int* err) {
     kt_end();
     kt_begin(KF_STAGE1);
     if (s.p2)
-      k_stage<1, true><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
+      k_stage<1, true><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
     else
-      k_stage<1, false><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
+      k_stage<1, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
     FM_LAUNCHED();
     kt_end();
     kt_begin(KF_STAGE2);
     if (s.p2)
-      k_stage<2, true><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+      k_stage<2, true><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
     else
-      k_stage<2, false><<<nblk(n, 128), 128, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+      k_stage<2, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
     FM_LAUNCHED();
     kt_end();
   }

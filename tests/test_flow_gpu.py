@@ -174,3 +174,13 @@ def test_event_clock_stops_and_resumes(gpu, orc):
         assert ra.steps == rb.steps and ca.now == cb.now
         assert (ca.next_gauge, ca.next_output) == (cb.next_gauge, cb.next_output)
     assert np.array_equal(a.download()[3], b.download()[3])
+
+
+def test_inline_division_is_ieee(gpu):
+    """fmd::ddiv (the inlined reciprocal-refinement division used by every
+    kernel) returns exactly IEEE a / b on 10^8 random operand pairs."""
+    import ctypes
+    fails = ctypes.c_int64(-1)
+    for seed in (1, 2, 3, 4):
+        gpu.call("selftest", 0, 25_000_000, seed, ctypes.byref(fails))
+        assert fails.value == 0
