@@ -684,4 +684,44 @@ void scaling_pyramid(DBuf<double>&& level_L, int L, int M, int N, int kind,
   }
 }
 
+namespace {
+__global__ void k_project_rowmajor(VertexView vv, const Scalars* __restrict__ s, double* out) {
+  vv.wall = s->wall;
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= (long long)vv.n * vv.m) return;
+  const int i = int(k % vv.n), j = int(k / vv.n);
+  const P3 q = vv.plane(i, j);
+  out[3 * k] = q.c0;
+  out[3 * k + 1] = q.cx;
+  out[3 * k + 2] = q.cy;
+}
+}  // namespace
+
+// project_elements (field.cpp:93-104): unpadded planes, row-major j*nx+i.
+void project_planes_rowmajor(const fm_raster* r, DBuf<double>& out) {
+  cudaStream_t st = stream();
+  const size_t nv = size_t(r->ncols) * r->nrows;
+  DBuf<double> vbuf;
+  const double* vdev = r->values;
+  if (!r->on_device) {
+    vbuf.upload(r->values, nv);
+    vdev = vbuf.p;
+  }
+  DBuf<Scalars> scal(1);
+  scal.zero();
+  k_vertex_max<<<148 * 8, 256, 0, st>>>(vdev, nv, r->nodata, scal.p);
+  FM_LAUNCHED();
+  k_wall<<<1, 1, 0, st>>>(scal.p);
+  FM_LAUNCHED();
+  VertexView vv{vdev, r->ncols, r->nrows, r->ncols - 1, r->nrows - 1, r->nodata, 0.0};
+  const long long n = (long long)(r->ncols - 1) * (r->nrows - 1);
+  out.alloc(3 * n);
+  k_project_rowmajor<<<unsigned((n + 255) / 256), 256, 0, st>>>(vv, scal.p, out.p);
+  FM_LAUNCHED();
+  Scalars hs{};
+  scal.download(&hs, 1);
+  FM_CUDA(cudaStreamSynchronize(st));
+  if (hs.err) throw Error(FM_ERR_DOMAIN, "project_vertices: non-finite vertex value");
+}
+
 }  // namespace fmh

@@ -25,234 +25,13 @@
 // never floating-point atomics, so results do not depend on scheduling.
 #include "fm_device.cuh"
 #include "fm_sim.hpp"
+#include "step_common.cuh"
 
 using namespace fmd;
 
 namespace fmh {
 
 namespace {
-
-struct Pt {
-  double h, qx, qy, z, eta, u, v;
-};
-
-__device__ __forceinline__ double lsize(const NuView& v, int l) { return v.R * double(1 << (v.L - l)); }
-__device__ __forceinline__ double lcen(double o, const NuView& v, int l, int i) {
-  return o + (i + 0.5) * v.R * double(1 << (v.L - l));
-}
-
-// limit_at (solver_nonuniform.cpp:52-66)
-__device__ __forceinline__ Pt limit(const double s[9], const P3& zc, double cx, double cy,
-                                    double sz, double x, double y, double hdry) {
-  Pt p;
-  p.h = smax(0.0, eval_plane(P3{s[0], s[1], s[2]}, cx, cy, sz, x, y));
-  p.qx = eval_plane(P3{s[3], s[4], s[5]}, cx, cy, sz, x, y);
-  p.qy = eval_plane(P3{s[6], s[7], s[8]}, cx, cy, sz, x, y);
-  p.z = eval_plane(zc, cx, cy, sz, x, y);
-  p.eta = p.h + p.z;
-  vel2(p.h, p.qx, p.qy, hdry, p.u, p.v);
-  return p;
-}
-
-// P2 geometry (power-of-two element sizes, every coordinate exactly
-// representable; checked on the host, Sim::p2): a point at offset (rx, ry)
-// from the element centre in units of its size, rx, ry in {0, +-1/4, +-1/2}.
-// There (x - xc) = rx R exactly and ((A (rx R)) / R) == A rx bit-for-bit, so
-// evaluate (field.cpp:21-24) needs no division.
-__device__ __forceinline__ double eval_rel(double c0, double cx, double cy, double rx, double ry) {
-  return c0 + cx * 2.0 * kS3 * rx + cy * 2.0 * kS3 * ry;
-}
-__device__ __forceinline__ Pt limit_rel(const double s[9], const P3& zc, double rx, double ry,
-                                        double hdry) {
-  Pt p;
-  p.h = smax(0.0, eval_rel(s[0], s[1], s[2], rx, ry));
-  p.qx = eval_rel(s[3], s[4], s[5], rx, ry);
-  p.qy = eval_rel(s[6], s[7], s[8], rx, ry);
-  p.z = eval_rel(zc.c0, zc.cx, zc.cy, rx, ry);
-  p.eta = p.h + p.z;
-  vel2(p.h, p.qx, p.qy, hdry, p.u, p.v);
-  return p;
-}
-
-__device__ __forceinline__ void load9(const double* __restrict__ a, long long k, double s[9]) {
-  const double* p = a + 9 * k;
-#pragma unroll
-  for (int q = 0; q < 9; ++q) s[q] = p[q];
-}
-__device__ __forceinline__ P3 load3(const double* __restrict__ a, long long k) {
-  const double* p = a + 3 * k;
-  return P3{p[0], p[1], p[2]};
-}
-
-__device__ __forceinline__ unsigned long long leaf_key(int l, int i, int j) {
-  return (static_cast<unsigned long long>(l) << 58) | (static_cast<unsigned long long>(j) << 29) |
-         static_cast<unsigned long long>(i);
-}
-
-// hydrograph_at (hydrograph.cpp:38-49)
-__device__ double hydro_at(const Hydro& h, int f, double t) {
-  const int a = h.off[f], b = h.off[f + 1];
-  if (t <= h.t[a]) return h.q[a];
-  if (t >= h.t[b - 1]) return h.q[b - 1];
-  int hi = a;
-  while (hi < b && !(t < h.t[hi])) ++hi;
-  const int lo = hi - 1;
-  if (t == h.t[lo]) return h.q[lo];
-  const double w = (t - h.t[lo]) / (h.t[hi] - h.t[lo]);
-  return h.q[lo] + w * (h.q[hi] - h.q[lo]);
-}
-
-__device__ __forceinline__ bool reached(double now, double target) {
-  return now >= target - 1e-9 * smax(1.0, target);
-}
-
-// The drive-loop bookkeeping for one step (run.cpp:80-111 with EventClock,
-// sim_common.cpp:48-82).  Pure function of the step-start clock and the
-// previous step's reductions, so every block derives the same decision; block
-// 0 publishes it as clk[1].  It first closes the previous step (non-finite
-// guard, then the gauge/output event counters, in the reference's order),
-// then decides whether to run this step, computes dt = clip(compute_dt) and
-// advances the clock and the inflow sources (apply_inflows uses the
-// step-start time, run.cpp:84).
-__device__ bool decide_step(const DevClock& c0, const DevRed& r, const Hydro* hy, int scheme,
-                            double courant, double g, double hdry, int ninflow, DevClock& c) {
-  c = c0;
-  if (c.active && c.had_step) {
-    if (r.badkey != ~0ull) {
-      c.blew_up = 1;
-      c.blow_t = c.now;
-      c.bad_key = r.badkey;
-      c.active = 0;
-    } else {
-      bool ev = false;
-      if (c.gauge_int > 0.0 && reached(c.now, c.next_gauge * c.gauge_int)) {
-        ++c.next_gauge;
-        ev = true;
-      }
-      if (c.out_int > 0.0 && reached(c.now, c.next_out * c.out_int)) {
-        ++c.next_out;
-        ev = true;
-      }
-      if (ev && c.stop_at_events) {
-        c.event_due = 1;
-        c.active = 0;
-      }
-    }
-  }
-  c.had_step = 0;
-  if (c.active && (c.now >= c.end_time || c.steps >= c.max_steps)) c.active = 0;
-  c.finished = c.now >= c.end_time;
-  if (!c.active) return false;
-  double raw;
-  if (scheme == FM_ACC) {
-    const double hmax = bitsd(r.hmax);
-    raw = hmax <= hdry ? INFINITY : courant * bitsd(r.dtmin) / sqrt(g * hmax);
-  } else {
-    raw = bitsd(r.dtmin) * courant;
-  }
-  double e = c.end_time;
-  if (c.out_int > 0.0) e = smin(e, c.next_out * c.out_int);
-  if (c.gauge_int > 0.0) e = smin(e, c.next_gauge * c.gauge_int);
-  const double gap = smax(e - c.now, 0.0);
-  double dt = smin(raw, gap);
-  if (!(dt > 0.0)) dt = smin(c.end_time, gap);
-  c.dt = dt;
-  c.t0 = c.now;
-  double added = 0.0;
-  for (int f = 0; f < ninflow; ++f) {
-    const double q = hydro_at(*hy, f, c.now);
-    if (q <= 0.0) {
-      c.on[f] = 0;
-      c.per_cell[f] = 0.0;
-      continue;
-    }
-    const double vol = q * dt;
-    c.on[f] = 1;
-    c.per_cell[f] = vol / double(hy->region[f]);
-    added += vol;
-  }
-  c.vol_in += added;
-  c.now += dt;
-  c.steps += 1;
-  c.dt_min = smin(c.dt_min, dt);
-  c.dt_max = smax(c.dt_max, dt);
-  c.had_step = 1;
-  c.finished = c.now >= c.end_time;
-  return true;
-}
-
-// Step head shared by the first kernel of every scheme: thread 0 of each
-// block evaluates decide_step; block 0 publishes clk[1] and clears the
-// reduction slot this step will accumulate into.
-__device__ __forceinline__ void step_head(const NuView& v, DevClock* clk, DevRed* red,
-                                          const Hydro* hy, int manual, double mdt, int& go,
-                                          double& dt) {
-  __shared__ int s_go;
-  __shared__ double s_dt;
-  if (threadIdx.x == 0) {
-    if (manual) {
-      s_go = 1;
-      s_dt = mdt;
-    } else {
-      const DevClock c0 = clk[0];
-      const int p = int(c0.steps & 1);
-      DevClock c;
-      const bool g = decide_step(c0, red[p], hy, v.scheme, v.courant, v.g, v.hdry, v.ninflow, c);
-      s_go = g ? 1 : 0;
-      s_dt = c.dt;
-      if (blockIdx.x == 0) {
-        clk[1] = c;
-        if (g) {
-          DevRed& nx = red[p ^ 1];
-          nx.dtmin = dbits(INFINITY);
-          nx.hmax = 0ull;
-          nx.badkey = ~0ull;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  go = s_go;
-  dt = s_dt;
-}
-
-// Next-step reductions over the freshly written state (fused epilogue).
-__device__ __forceinline__ void reduce_leaf(const NuView& v, DevRed* red, const DevClock& c,
-                                            const double s[9], double sz, unsigned long long key,
-                                            bool valid) {
-  double dtc = INFINITY, hm = 0.0;
-  unsigned long long bad = ~0ull;
-  if (valid) {
-    const double h = s[0];
-    if (v.scheme == FM_ACC) {
-      if (h > v.hdry) {
-        hm = h;
-        dtc = sz;
-      }
-    } else if (h > v.hdry) {
-      const double cw = sqrt(v.g * h);
-      const double sx = fabs(zdiv(s[3], h)) + cw;
-      const double sy = fabs(zdiv(s[6], h)) + cw;
-      dtc = ddiv(sz, smax(sx, sy));
-    }
-    bool fin = true;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) fin = fin && isfinite(s[q]);
-    if (!fin) bad = key;
-  }
-  for (int o = 16; o; o >>= 1) {
-    dtc = smin(dtc, __shfl_xor_sync(0xffffffffu, dtc, o));
-    hm = smax(hm, __shfl_xor_sync(0xffffffffu, hm, o));
-    const unsigned long long b2 = __shfl_xor_sync(0xffffffffu, bad, o);
-    bad = b2 < bad ? b2 : bad;
-  }
-  if ((threadIdx.x & 31) == 0) {
-    DevRed& r = red[(c.steps) & 1];
-    if (dtc < INFINITY) atomicMin(&r.dtmin, dbits(dtc));
-    if (hm > 0.0) atomicMax(&r.hmax, dbits(hm));
-    if (bad != ~0ull) atomicMin(&r.badkey, bad);
-  }
-}
 
 // ---- step head: clock + friction (DG2/FV1) ------------------------------
 // src == dst for DG2; FV1 keeps its post-step state in U* (see k_stage) and
@@ -718,6 +497,21 @@ void nu_launch_step(Sim& s, bool manual, double mdt, int* err) {
     FM_LAUNCHED();
     kt_end();
   }
+}
+
+void launch_head_friction(Sim& s, const double* src, double* dst, bool manual, double mdt) {
+  kt_begin(s.uniform ? KF_UNI_HEAD : KF_HEAD);
+  k_head_friction<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.hydro.p, src,
+                                                         dst, manual, mdt);
+  FM_LAUNCHED();
+  kt_end();
+}
+
+void launch_commit(Sim& s) {
+  kt_begin(KF_COMMIT);
+  k_commit<<<1, 1, 0, stream()>>>(s.clk.p);
+  FM_LAUNCHED();
+  kt_end();
 }
 
 void nu_launch_reduce_init(Sim& s) {

@@ -20,6 +20,7 @@ void nu_launch_inflow_add(Sim& s, const double* per_cell_dev);
 // uniform.cu
 void un_launch_step(Sim& s, bool manual, double mdt, int* err);
 void un_launch_reduce_init(Sim& s);
+void un_launch_inflow_add(Sim& s, const double* per_cell_dev);
 // adaptive.cu
 struct AdaptState;
 void adaptive_destroy(AdaptState* a);
@@ -331,7 +332,7 @@ void fv1_to_star(Sim& s) {
     s.fv1_in_star = true;
   }
 }
-bool fv1_staged(const Sim& s) { return !s.uniform && s.scheme == FM_FV1; }
+bool fv1_staged(const Sim& s) { return s.scheme == FM_FV1; }
 
 void init_red(Sim& s) {
   DevRed r[2];
@@ -444,10 +445,12 @@ double sim_apply_inflows(Sim& s, double t, double dt) {
     per[f] = vol / double(s.region[f]);
     added += vol;
   }
-  if (s.uniform) throw Error(FM_ERR_OTHER, "uniform inflows: use fm_sim_run");
   DBuf<double> dper;
   dper.upload(per, kMaxInflows);
-  nu_launch_inflow_add(s, dper.p);
+  if (s.uniform)
+    un_launch_inflow_add(s, dper.p);
+  else
+    nu_launch_inflow_add(s, dper.p);
   FM_CUDA(cudaStreamSynchronize(stream()));
   return added;
 }
@@ -487,13 +490,13 @@ static std::vector<int64_t> sim_order(Sim& s, std::vector<int8_t>& l, std::vecto
                                       std::vector<int32_t>& j) {
   i = s.li.to_host();
   j = s.lj.to_host();
-  if (s.uniform) {
-    l.assign(s.n, 0);
-  } else {
-    l = s.lvl.to_host();
-  }
   std::vector<int64_t> perm(s.n);
   for (int64_t k = 0; k < s.n; ++k) perm[k] = k;
+  if (s.uniform) {  // already j*nx+i, the reference order
+    l.assign(s.n, 0);
+    return perm;
+  }
+  l = s.lvl.to_host();
   std::sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) {
     if (l[a] != l[b]) return l[a] < l[b];
     if (j[a] != j[b]) return j[a] < j[b];

@@ -1,13 +1,574 @@
-// Uniform-raster DG2/FV1/ACC (solver_uniform.cpp) on the device.
+// Uniform-raster DG2 / FV1 / ACC on sm_100a (UniformSim, solver_uniform.cpp):
+// config 4's "uniform-raster DG2 at the finest level" comparator.
+//
+// Layout: cell (i, j) at j*nx + i (the reference's own order), 9 flow
+// coefficients + 3 topography coefficients per cell (AoS).
+//
+// k_uni_stage<STAGE>: one CTA per 32 x 8 tile.  Phase 1: every cell revises
+// its four faces (revise_faces :73-137) into shared memory, and the tile's
+// one-cell halo revises only the face it shares with the tile.  Phase 2:
+// each interior and boundary face's HLL flux (fluxes :139-185) is evaluated
+// ONCE into shared memory.  Phase 3: every cell assembles (assemble_dg2
+// :187-229 / assemble_fv1 :231-251), updates, applies positivity (:253-281)
+// and, on the last stage, the inflow sources, the non-finite guard and the
+// next step's CFL reduction (the drive-loop epilogue shared with the
+// non-uniform kernels).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "fm_device.cuh"
 #include "fm_sim.hpp"
+#include "step_common.cuh"
+
+using namespace fmd;
 
 namespace fmh {
 
-void uniform_init(Sim&, const fm_sim_desc*, const fm_raster*) {
-  throw Error(FM_ERR_OTHER, "uniform solvers: not built yet");
+void launch_head_friction(Sim& s, const double* src, double* dst, bool manual, double mdt);
+void launch_commit(Sim& s);
+void project_planes_rowmajor(const fm_raster* r, DBuf<double>& out);
+
+namespace {
+
+constexpr int TX = 32, TY = 8;
+
+struct UniView {
+  int nx, ny, scheme, ninflow, libm;
+  double R, x0, y0, g, hdry, courant;
+  int bc[4];
+  const double* z;
+  const double* nman;
+  int rect[4 * kMaxInflows];
+};
+
+struct Star {
+  double h, qx, qy;
+};
+
+// One face of revise_faces (solver_uniform.cpp:84-129): the cell's limit on
+// side `sd` (side_limit, :16-26) against the opposing face value of the
+// neighbour's topography.  Returns the starred state; zd and the raw limit
+// feed DirMod.
+struct FaceRev {
+  Star st;
+  double zd;
+};
+__device__ __forceinline__ FaceRev revise_face(const double u[9], const P3& zc, int sd,
+                                               double z_other, bool has_other, double hdry) {
+  const P3 h{u[0], u[1], u[2]}, qx{u[3], u[4], u[5]}, qy{u[6], u[7], u[8]};
+  const double lh = smax(0.0, face_val(h, sd));
+  const double lqx = face_val(qx, sd), lqy = face_val(qy, sd);
+  const double lz = face_val(zc, sd);
+  const double eta = lh + lz;
+  double uu, vv;
+  vel2(lh, lqx, lqy, hdry, uu, vv);
+  const double zs = smax(lz, has_other ? z_other : lz);
+  const double hs = smax(0.0, eta - zs);
+  FaceRev r;
+  r.st = Star{hs, hs * uu, hs * vv};
+  r.zd = zs - smax(0.0, zs - eta);
+  return r;
 }
-void un_launch_step(Sim&, bool, double, int*) { throw Error(FM_ERR_OTHER, "uniform: not built"); }
-void un_launch_reduce_init(Sim&) { throw Error(FM_ERR_OTHER, "uniform: not built"); }
+
+__device__ __forceinline__ P3 ld3(const double* a, size_t c) { return P3{a[3 * c], a[3 * c + 1], a[3 * c + 2]}; }
+__device__ __forceinline__ void ld9(const double* a, size_t c, double s[9]) {
+#pragma unroll
+  for (int q = 0; q < 9; ++q) s[q] = a[9 * c + q];
+}
+
+template <int STAGE, bool P2>
+__global__ void __launch_bounds__(TX* TY) k_uni_stage(UniView v, NuView nv, const DevClock* __restrict__ clk,
+                                                       DevRed* red, const double* __restrict__ in,
+                                                       const double* uold, double* out, int last,
+                                                       int manual, double mdt, int* err) {
+  __shared__ Star s_e[TY][TX], s_w[TY][TX], s_n[TY][TX], s_s[TY][TX];
+  __shared__ Star h_w[TY], h_e[TY], h_s[TX], h_n[TX];  // halo faces shared with the tile
+  __shared__ Flx fx[TY][TX + 1], fy[TY + 1][TX];
+  const DevClock* c = clk + 1;
+  if (!manual && !c->active) return;
+  const double dt = manual ? mdt : c->dt;
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int i = x0 + tx, j = y0 + ty;
+  const bool valid = i < v.nx && j < v.ny;
+  const int ic = min(i, v.nx - 1), jc = min(j, v.ny - 1);
+  const size_t cell = size_t(jc) * v.nx + ic;
+  double s[9];
+  ld9(in, cell, s);
+  const P3 zc = ld3(v.z, cell);
+  // phase 1: revise the four faces
+  const bool hasE = ic + 1 < v.nx, hasW = ic > 0, hasN = jc + 1 < v.ny, hasS = jc > 0;
+  const double zwe = hasE ? face_val(ld3(v.z, cell + 1), 3) : 0.0;
+  const double zew = hasW ? face_val(ld3(v.z, cell - 1), 1) : 0.0;
+  const double zsn = hasN ? face_val(ld3(v.z, cell + v.nx), 2) : 0.0;
+  const double zns = hasS ? face_val(ld3(v.z, cell - v.nx), 0) : 0.0;
+  const FaceRev re = revise_face(s, zc, 1, zwe, hasE, v.hdry);
+  const FaceRev rw = revise_face(s, zc, 3, zew, hasW, v.hdry);
+  const FaceRev rn = revise_face(s, zc, 0, zsn, hasN, v.hdry);
+  const FaceRev rs = revise_face(s, zc, 2, zns, hasS, v.hdry);
+  s_e[ty][tx] = re.st;
+  s_w[ty][tx] = rw.st;
+  s_n[ty][tx] = rn.st;
+  s_s[ty][tx] = rs.st;
+  // halo: the neighbouring cell's face toward the tile
+  if (tx == 0 && x0 > 0 && j < v.ny) {  // star_e of (x0-1, j)
+    double t[9];
+    const size_t cc = size_t(j) * v.nx + (x0 - 1);
+    ld9(in, cc, t);
+    h_w[ty] = revise_face(t, ld3(v.z, cc), 1, face_val(ld3(v.z, cc + 1), 3), true, v.hdry).st;
+  }
+  if (tx == TX - 1 && x0 + TX < v.nx && j < v.ny) {  // star_w of (x0+TX, j)
+    double t[9];
+    const size_t cc = size_t(j) * v.nx + (x0 + TX);
+    ld9(in, cc, t);
+    h_e[ty] = revise_face(t, ld3(v.z, cc), 3, face_val(ld3(v.z, cc - 1), 1), true, v.hdry).st;
+  }
+  if (ty == 0 && y0 > 0 && i < v.nx) {  // star_n of (i, y0-1)
+    double t[9];
+    const size_t cc = size_t(y0 - 1) * v.nx + i;
+    ld9(in, cc, t);
+    h_s[tx] = revise_face(t, ld3(v.z, cc), 0, face_val(ld3(v.z, cc + v.nx), 2), true, v.hdry).st;
+  }
+  if (ty == TY - 1 && y0 + TY < v.ny && i < v.nx) {  // star_s of (i, y0+TY)
+    double t[9];
+    const size_t cc = size_t(y0 + TY) * v.nx + i;
+    ld9(in, cc, t);
+    h_n[tx] = revise_face(t, ld3(v.z, cc), 2, face_val(ld3(v.z, cc - v.nx), 0), true, v.hdry).st;
+  }
+  __syncthreads();
+  // phase 2: every face of the tile once (fluxes, solver_uniform.cpp:139-185)
+  const int ncx = min(TX, v.nx - x0), ncy = min(TY, v.ny - y0);
+  for (int f = threadIdx.x; f < TY * (TX + 1); f += TX * TY) {
+    const int r = f / (TX + 1), k = f % (TX + 1);
+    if (r >= ncy || k > ncx) continue;
+    const int gi = x0 + k;  // face between cells gi-1 and gi
+    Star l, rr;
+    if (gi == 0) {
+      rr = s_w[r][0];
+      l = rr;
+      if (v.bc[3] == FM_REFLECTIVE) l.qx = -l.qx;
+    } else if (gi == v.nx) {
+      l = s_e[r][k - 1];
+      rr = l;
+      if (v.bc[1] == FM_REFLECTIVE) rr.qx = -rr.qx;
+    } else {
+      l = k == 0 ? h_w[r] : s_e[r][k - 1];
+      rr = k == ncx ? h_e[r] : s_w[r][k];
+    }
+    fx[r][k] = hll(l.h, l.qx, l.qy, rr.h, rr.qx, rr.qy, v.g, v.hdry, err);
+  }
+  for (int f = threadIdx.x; f < (TY + 1) * TX; f += TX * TY) {
+    const int r = f / TX, k = f % TX;
+    if (k >= ncx || r > ncy) continue;
+    const int gj = y0 + r;
+    Star l, rr;
+    if (gj == 0) {
+      rr = s_s[0][k];
+      l = rr;
+      if (v.bc[2] == FM_REFLECTIVE) l.qy = -l.qy;
+    } else if (gj == v.ny) {
+      l = s_n[r - 1][k];
+      rr = l;
+      if (v.bc[0] == FM_REFLECTIVE) rr.qy = -rr.qy;
+    } else {
+      l = r == 0 ? h_s[k] : s_n[r - 1][k];
+      rr = r == ncy ? h_n[k] : s_s[r][k];
+    }
+    // normal component is qy along y faces
+    fy[r][k] = hll(l.h, l.qy, l.qx, rr.h, rr.qy, rr.qx, v.g, v.hdry, err);
+  }
+  __syncthreads();
+  // phase 3: assemble + update
+  double res[9];
+  const double inv = 1.0 / v.R;
+  if (valid) {
+    const double k3 = kHalfInvS3;
+    const DirMod X{0.5 * (re.st.h + rw.st.h),   (re.st.h - rw.st.h) * k3,   0.5 * (re.st.qx + rw.st.qx),
+                   (re.st.qx - rw.st.qx) * k3, 0.5 * (re.st.qy + rw.st.qy), (re.st.qy - rw.st.qy) * k3,
+                   (re.zd - rw.zd) * k3};
+    const DirMod Y{0.5 * (rn.st.h + rs.st.h),   (rn.st.h - rs.st.h) * k3,   0.5 * (rn.st.qx + rs.st.qx),
+                   (rn.st.qx - rs.st.qx) * k3, 0.5 * (rn.st.qy + rs.st.qy), (rn.st.qy - rs.st.qy) * k3,
+                   (rn.zd - rs.zd) * k3};
+    double Lr[9];
+    l_operator<P2>(fy[ty + 1][tx], fx[ty][tx + 1], fy[ty][tx], fx[ty][tx], X, Y, v.R, inv, v.g, v.hdry,
+                   v.scheme == FM_DG2, Lr);
+    if (STAGE == 1) {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
+    } else {
+      double u0[9];
+      ld9(uold, cell, u0);
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        double a = s[q];
+        a += Lr[q] * dt;
+        a += u0[q];
+        a *= 0.5;
+        res[q] = a;
+      }
+    }
+    positivity(res, v.hdry);
+    if (last && !manual) {
+      // apply_inflows (solver_uniform.cpp:444-455): one fine cell per target
+      for (int f = 0; f < v.ninflow; ++f) {
+        if (!c->on[f]) continue;
+        if (i >= v.rect[4 * f] && j >= v.rect[4 * f + 1] && i <= v.rect[4 * f + 2] && j <= v.rect[4 * f + 3])
+          res[0] += ddiv(c->per_cell[f] * 1, v.R * v.R);
+      }
+    }
+    double* o = out + 9 * cell;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) o[q] = res[q];
+  } else {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) res[q] = 0.0;
+  }
+  if (last && !manual) reduce_leaf(nv, red, *c, res, v.R, leaf_key(0, i, j), valid);
+}
+
+// ---- ACC (solver_uniform.cpp:330-415) --------------------------------------
+// x faces (nx+1)*ny then y faces nx*(ny+1), one thread per face; step head.
+__global__ void __launch_bounds__(256) k_uni_acc_faces(UniView v, NuView nv, DevClock* clk, DevRed* red,
+                                                      const Hydro* hy, const double* __restrict__ u,
+                                                      double* __restrict__ qx, double* __restrict__ qy,
+                                                      int manual, double mdt) {
+  const long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int go;
+  double dt;
+  step_head(nv, clk, red, hy, manual, mdt, go, dt);
+  const long long nfx = (long long)(v.nx + 1) * v.ny, nfy = (long long)v.nx * (v.ny + 1);
+  if (!go || f >= nfx + nfy) return;
+  const bool xf = f < nfx;
+  const long long g = xf ? f : f - nfx;
+  int i, j, side;
+  size_t l = 0, r = 0, edge = 0;
+  bool boundary;
+  if (xf) {
+    j = int(g / (v.nx + 1));
+    i = int(g % (v.nx + 1));
+    boundary = i == 0 || i == v.nx;
+    side = i == 0 ? 3 : 1;
+    edge = size_t(j) * v.nx + (i == 0 ? 0 : v.nx - 1);
+    if (!boundary) {
+      l = size_t(j) * v.nx + i - 1;
+      r = l + 1;
+    }
+  } else {
+    j = int(g / v.nx);
+    i = int(g % v.nx);
+    boundary = j == 0 || j == v.ny;
+    side = j == 0 ? 2 : 0;
+    edge = size_t(j == 0 ? 0 : v.ny - 1) * v.nx + i;
+    if (!boundary) {
+      l = size_t(j - 1) * v.nx + i;
+      r = l + v.nx;
+    }
+  }
+  double* qp = xf ? qx + g : qy + g;
+  double q = *qp;
+  if (boundary) {
+    if (v.bc[side] == FM_REFLECTIVE) {
+      *qp = 0.0;
+      return;
+    }
+    const double hf = u[9 * edge];
+    if (hf <= v.hdry) {
+      *qp = 0.0;
+      return;
+    }
+    const double n = v.nman[edge];
+    *qp = zdiv(q, 1.0 + zdiv(v.g * dt * n * n * fabs(q), pow73_m(hf, v.libm)));
+    return;
+  }
+  const double zl = v.z[3 * l], zr = v.z[3 * r];
+  const double el = u[9 * l] + zl, er = u[9 * r] + zr;
+  const double hf = smax(el, er) - smax(zl, zr);
+  if (hf <= v.hdry) {
+    *qp = 0.0;
+    return;
+  }
+  const double nf = 0.5 * (v.nman[l] + v.nman[r]);
+  *qp = ddiv(q - ddiv(v.g * hf * dt * (er - el), v.R),
+             1.0 + zdiv(v.g * dt * nf * nf * fabs(q), pow73_m(hf, v.libm)));
+}
+
+__global__ void __launch_bounds__(256) k_uni_acc_cells(UniView v, NuView nv, const DevClock* __restrict__ clk,
+                                                      DevRed* red, double* __restrict__ u,
+                                                      const double* __restrict__ qx,
+                                                      const double* __restrict__ qy, int manual,
+                                                      double mdt) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const DevClock* c = clk + 1;
+  if (!manual && !c->active) return;
+  const double dt = manual ? mdt : c->dt;
+  const long long n = (long long)v.nx * v.ny;
+  const bool valid = k < n;
+  double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int i = 0, j = 0;
+  if (valid) {
+    j = int(k / v.nx);
+    i = int(k % v.nx);
+    ld9(u, k, s);
+    const double qw = qx[size_t(j) * (v.nx + 1) + i], qe = qx[size_t(j) * (v.nx + 1) + i + 1];
+    const double qs = qy[size_t(j) * v.nx + i], qn = qy[size_t(j + 1) * v.nx + i];
+    s[0] -= zdiv(dt * ((qe - qw) + (qn - qs)), v.R);
+    s[3] = 0.5 * (qw + qe);
+    s[6] = 0.5 * (qs + qn);
+    if (!manual) {
+      for (int f = 0; f < v.ninflow; ++f) {
+        if (!c->on[f]) continue;
+        if (i >= v.rect[4 * f] && j >= v.rect[4 * f + 1] && i <= v.rect[4 * f + 2] && j <= v.rect[4 * f + 3])
+          s[0] += ddiv(c->per_cell[f] * 1, v.R * v.R);
+      }
+    }
+    u[9 * k] = s[0];
+    u[9 * k + 3] = s[3];
+    u[9 * k + 6] = s[6];
+  }
+  if (!manual) reduce_leaf(nv, red, *c, s, v.R, leaf_key(0, i, j), valid);
+}
+
+__global__ void k_uni_reduce_init(NuView nv, int nx, const DevClock* clk, DevRed* red,
+                                  const double* __restrict__ u) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool valid = k < nv.n;
+  double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int i = 0, j = 0;
+  if (valid) {
+    ld9(u, k, s);
+    j = int(k / nx);
+    i = int(k % nx);
+  }
+  DevClock c = clk[0];
+  reduce_leaf(nv, red, c, s, nv.R, leaf_key(0, i, j), valid);
+}
+
+// Setup kernels (make_uniform_sim, solver_uniform.cpp:522-601).
+__global__ void k_uni_manning(int nx, int ny, const double* __restrict__ mr, int nc, int nr,
+                              double uniform, double* __restrict__ out) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= (long long)nx * ny) return;
+  const int j = int(k / nx), i = int(k % nx);
+  if (!mr) {
+    out[k] = uniform;
+    return;
+  }
+  const int row = min(max(nr - 1 - j, 0), nr - 1);
+  const int col = min(max(i, 0), nc - 1);
+  out[k] = mr[size_t(row) * nc + col];
+}
+
+__global__ void k_uni_ic(long long n, const double* __restrict__ z, const double* __restrict__ hplanes,
+                         int mode, double val, int pc, double hdry, double* __restrict__ zout,
+                         double* __restrict__ u) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double f[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const double c0 = z[3 * k], cx = z[3 * k + 1], cy = z[3 * k + 2];
+  if (hplanes) {
+    f[0] = hplanes[3 * k];
+    f[1] = hplanes[3 * k + 1];
+    f[2] = hplanes[3 * k + 2];
+  } else if (mode == 1) {  // flow_from_surface (solver_uniform.cpp:60-71)
+    const double span = kS3 * (fabs(cx) + fabs(cy));
+    if (c0 + span < val) {
+      f[0] = val - c0;
+      f[1] = -cx;
+      f[2] = -cy;
+    } else if (c0 - span >= val) {
+    } else {
+      f[0] = smax(0.0, val - c0);
+    }
+  } else if (mode == 2) {
+    f[0] = val;
+  }
+  if (pc) {
+    zout[3 * k + 1] = 0.0;
+    zout[3 * k + 2] = 0.0;
+    f[1] = f[2] = 0.0;
+    for (int q = 3; q < 9; ++q) f[q] = 0.0;
+  }
+  positivity(f, hdry);
+  for (int q = 0; q < 9; ++q) u[9 * k + q] = f[q];
+}
+
+__global__ void k_uni_ij(int nx, long long n, int32_t* li, int32_t* lj) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  li[k] = int32_t(k % nx);
+  lj[k] = int32_t(k / nx);
+}
+
+// apply_inflows for the host API path (solver_uniform.cpp:444-455)
+__global__ void k_uni_inflow_add(UniView v, const double* __restrict__ per_cell, double* u) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= (long long)v.nx * v.ny) return;
+  const int j = int(k / v.nx), i = int(k % v.nx);
+  double h = u[9 * k];
+  for (int f = 0; f < v.ninflow; ++f) {
+    if (per_cell[f] == 0.0) continue;
+    if (i >= v.rect[4 * f] && j >= v.rect[4 * f + 1] && i <= v.rect[4 * f + 2] && j <= v.rect[4 * f + 3])
+      h += ddiv(per_cell[f] * 1, v.R * v.R);
+  }
+  u[9 * k] = h;
+}
+
+inline unsigned nblk(long long n, int t) { return unsigned((n + t - 1) / t); }
+
+UniView uview(const Sim& s) {
+  UniView v{};
+  v.nx = s.nx;
+  v.ny = s.ny;
+  v.scheme = s.scheme;
+  v.ninflow = s.ninflow;
+  v.libm = s.libm;
+  v.R = s.R;
+  v.x0 = s.x0;
+  v.y0 = s.y0;
+  v.g = s.g;
+  v.hdry = s.hdry;
+  v.courant = s.courant;
+  for (int q = 0; q < 4; ++q) v.bc[q] = s.bc[q];
+  v.z = s.z.p;
+  v.nman = s.nman.p;
+  for (int q = 0; q < 4 * s.ninflow; ++q) v.rect[q] = s.rect[q];
+  return v;
+}
+
+}  // namespace
+
+bool geometry_is_p2(double R, double x0, double y0, int L, int M, int N);
+
+void uniform_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem) {
+  cudaStream_t st = stream();
+  if (d->solver == FM_MWDG2 || d->solver == FM_HWFV1)
+    throw Error(FM_ERR_CONFIG, "uniform solver cannot run adaptive kinds");
+  if (dem->ncols < 2 || dem->nrows < 2)
+    throw Error(FM_ERR_CONFIG, "DEM must have at least 2x2 samples to define elements");
+  s.nx = dem->ncols - 1;
+  s.ny = dem->nrows - 1;
+  s.R = dem->cellsize;
+  s.x0 = dem->xll;
+  s.y0 = dem->yll;
+  s.L = 0;
+  s.M = s.nx;
+  s.N = s.ny;
+  s.n = int64_t(s.nx) * s.ny;
+  // power-of-two cell size: the raster has no offsets, only /R divisions
+  {
+    int e = 0;
+    s.p2 = std::frexp(s.R, &e) == 0.5;
+  }
+  const long long n = s.n;
+  project_planes_rowmajor(dem, s.z);
+  s.nman.alloc(n);
+  k_uni_manning<<<nblk(n, 256), 256, 0, st>>>(s.nx, s.ny, s.has_mr ? s.mr.p : nullptr, s.mr_ncols,
+                                               s.mr_nrows, s.manning, s.nman.p);
+  FM_LAUNCHED();
+  s.u.alloc(9 * n);
+  s.us.alloc(9 * n);
+  DBuf<double> hp;
+  int mode = 0;
+  double val = 0.0;
+  if (d->initial_depth_raster) {
+    const fm_raster* hr = d->initial_depth_raster;
+    if (hr->ncols != dem->ncols || hr->nrows != dem->nrows)
+      throw Error(FM_ERR_CONFIG, "initial_depth_raster geometry must match the DEM");
+    project_planes_rowmajor(hr, hp);
+  } else if (d->has_initial_surface) {
+    mode = 1;
+    val = d->initial_surface;
+  } else if (d->initial_depth > 0.0) {
+    mode = 2;
+    val = d->initial_depth;
+  }
+  k_uni_ic<<<nblk(n, 256), 256, 0, st>>>(n, s.z.p, hp.n ? hp.p : nullptr, mode, val,
+                                          s.scheme != FM_DG2, s.hdry, s.z.p, s.u.p);
+  FM_LAUNCHED();
+  // inflows: the rectangle itself is the target set (one cell each)
+  for (int f = 0; f < s.ninflow; ++f) {
+    const int* r = &s.rect[4 * f];
+    if (r[0] < 0 || r[1] < 0 || r[2] >= s.nx || r[3] >= s.ny)
+      throw Error(FM_ERR_CONFIG, "inflow region outside the domain");
+    if (!dem->on_device) {  // element_nodata_mask (sim_common.cpp:118-131)
+      bool any = false;
+      for (int j = r[1]; j <= r[3] && !any; ++j)
+        for (int i = r[0]; i <= r[2] && !any; ++i) {
+          const int rs = dem->nrows - 1 - j;
+          auto nd = [&](int row, int col) { return dem->values[size_t(row) * dem->ncols + col] == dem->nodata; };
+          if (!(nd(rs, i) || nd(rs, i + 1) || nd(rs - 1, i) || nd(rs - 1, i + 1))) any = true;
+        }
+      if (!any) throw Error(FM_ERR_CONFIG, "inflow region lies entirely on nodata cells");
+    }
+  }
+  s.li.alloc(n);
+  s.lj.alloc(n);
+  k_uni_ij<<<nblk(n, 256), 256, 0, st>>>(s.nx, n, s.li.p, s.lj.p);
+  FM_LAUNCHED();
+  if (s.scheme == FM_ACC) {
+    s.aqx.alloc(size_t(s.nx + 1) * s.ny);
+    s.aqy.alloc(size_t(s.nx) * (s.ny + 1));
+    s.aqx.zero();
+    s.aqy.zero();
+  }
+  s.nseg = int64_t(s.nx + 1) * s.ny + int64_t(s.nx) * (s.ny + 1);
+}
+
+void un_launch_step(Sim& s, bool manual, double mdt, int* err) {
+  cudaStream_t st = stream();
+  const UniView v = uview(s);
+  const NuView nv = s.view();
+  const dim3 grid((s.nx + TX - 1) / TX, (s.ny + TY - 1) / TY);
+  if (s.scheme == FM_ACC) {
+    const long long nf = s.nseg;
+    kt_begin(KF_ACC_FACES);
+    k_uni_acc_faces<<<nblk(nf, 256), 256, 0, st>>>(v, nv, s.clk.p, s.red.p, s.hydro.p, s.u.p, s.aqx.p,
+                                                    s.aqy.p, manual, mdt);
+    FM_LAUNCHED();
+    kt_end();
+    kt_begin(KF_ACC_LEAVES);
+    k_uni_acc_cells<<<nblk(s.n, 256), 256, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, s.aqx.p, s.aqy.p,
+                                                     manual, mdt);
+    FM_LAUNCHED();
+    kt_end();
+  } else if (s.scheme == FM_FV1) {
+    launch_head_friction(s, s.us.p, s.u.p, manual, mdt);
+    kt_begin(KF_UNI_STAGE1);
+    if (s.p2)
+      k_uni_stage<1, true><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
+    else
+      k_uni_stage<1, false><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
+    FM_LAUNCHED();
+    kt_end();
+  } else {
+    launch_head_friction(s, s.u.p, s.u.p, manual, mdt);
+    kt_begin(KF_UNI_STAGE1);
+    if (s.p2)
+      k_uni_stage<1, true><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
+    else
+      k_uni_stage<1, false><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
+    FM_LAUNCHED();
+    kt_end();
+    kt_begin(KF_UNI_STAGE2);
+    if (s.p2)
+      k_uni_stage<2, true><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+    else
+      k_uni_stage<2, false><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+    FM_LAUNCHED();
+    kt_end();
+  }
+  if (!manual) launch_commit(s);
+}
+
+void un_launch_inflow_add(Sim& s, const double* per_cell_dev) {
+  k_uni_inflow_add<<<nblk(s.n, 256), 256, 0, stream()>>>(uview(s), per_cell_dev, s.u.p);
+  FM_LAUNCHED();
+}
+
+void un_launch_reduce_init(Sim& s) {
+  k_uni_reduce_init<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.nx, s.clk.p, s.red.p, s.u.p);
+  FM_LAUNCHED();
+}
 
 }  // namespace fmh
