@@ -108,6 +108,9 @@ struct Grid {
 };
 
 Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind);
+// The stages of mra_static, reused by the adaptive solver.
+void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, double* ms);
+void grade_count_levels(Grid& g, bool graded);
 // Shared by the static and the adaptive pipelines: from final per-level flags
 // (already in g.flag) compute counts, offsets, then decode topography details
 // top-down into the leaf arrays.  Returns the leaf count.

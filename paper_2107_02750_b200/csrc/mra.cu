@@ -444,7 +444,11 @@ int64_t build_leaves(Grid& g) {
   return g.nleaves;
 }
 
-Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind) {
+// Projection + multi-level encode (detail_tree.cpp:10-54 with the fused
+// field.cpp:64-117): fills g.det, g.flag (= significance, detail_tree.cpp:66-72,
+// before closure), g.coarse and g.field_norm.  All buffers are allocated
+// before the first kernel so `ms` (CUDA events) times kernels only.
+void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, double* ms) {
   if (!dem || !dem->values) throw Error(FM_ERR_CONFIG, "null DEM raster");
   if (dem->ncols < 2 || dem->nrows < 2)
     throw Error(FM_ERR_CONFIG, "DEM must have at least 2x2 samples to define elements");
@@ -454,25 +458,18 @@ Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind)
   if (kind != FM_MW && kind != FM_HW) throw Error(FM_ERR_CONFIG, "unknown wavelet kind");
   upload_banks();
   cudaStream_t st = stream();
-
-  auto g = std::make_unique<Grid>();
   const int n = dem->ncols - 1, m = dem->nrows - 1;
   const int step = 1 << L;
-  g->L = L;
-  g->M = (n + step - 1) / step;
-  g->N = (m + step - 1) / step;
-  g->R = dem->cellsize;
-  g->x0 = dem->xll;
-  g->y0 = dem->yll;
-  g->eps = eps;
-  g->kind = kind;
-  g->graded = graded;
-  if (uint64_t(g->M) * g->N * (uint64_t(1) << (2 * L)) > (uint64_t(1) << 40))
+  g.L = L;
+  g.M = (n + step - 1) / step;
+  g.N = (m + step - 1) / step;
+  g.R = dem->cellsize;
+  g.x0 = dem->xll;
+  g.y0 = dem->yll;
+  g.eps = eps;
+  g.kind = kind;
+  if (uint64_t(g.M) * g.N * (uint64_t(1) << (2 * L)) > (uint64_t(1) << 40))
     throw Error(FM_ERR_CONFIG, "domain too large");
-
-  cudaEvent_t e0, e1;
-  FM_CUDA(cudaEventCreate(&e0));
-  FM_CUDA(cudaEventCreate(&e1));
 
   // DEM to the device (or use it in place)
   const size_t nv = size_t(dem->ncols) * dem->nrows;
@@ -484,92 +481,125 @@ Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind)
   }
   DBuf<Scalars> scal(1);
   scal.zero();
+  g.det.resize(L);
+  g.flag.resize(L);
+  for (int l = 0; l < L; ++l) {
+    g.det[l].alloc(9 * g.nodes(l));
+    g.flag[l].alloc(g.nodes(l));
+  }
+  g.coarse.alloc(3 * g.nodes(0));
+  // tile-root scaling buffers of the multi-pass encode
+  std::vector<int> passes;
+  for (int lev_in = L; lev_in > 0;) {
+    const int T = std::min(5, lev_in);
+    passes.push_back(T);
+    lev_in -= T;
+  }
+  std::vector<DBuf<double>> roots(passes.size());
+  {
+    int lev_in = L;
+    for (size_t k = 0; k < passes.size(); ++k) {
+      lev_in -= passes[k];
+      if (lev_in > 0) roots[k].alloc(3 * g.nodes(lev_in));
+    }
+  }
+  cudaEvent_t e0, e1;
+  FM_CUDA(cudaEventCreate(&e0));
+  FM_CUDA(cudaEventCreate(&e1));
   FM_CUDA(cudaEventRecord(e0, st));
 
-  const int sms = 148;
-  k_vertex_max<<<sms * 8, 256, 0, st>>>(vdev, nv, dem->nodata, scal.p);
+  k_vertex_max<<<148 * 8, 256, 0, st>>>(vdev, nv, dem->nodata, scal.p);
   FM_LAUNCHED();
   k_wall<<<1, 1, 0, st>>>(scal.p);
   FM_LAUNCHED();
   VertexView vv{vdev, dem->ncols, dem->nrows, n, m, dem->nodata, 0.0};
-  k_field_norm<<<sms * 8, 256, 0, st>>>(vv, scal.p, scal.p);
+  k_field_norm<<<148 * 8, 256, 0, st>>>(vv, scal.p, scal.p);
   FM_LAUNCHED();
   k_norm_final<<<1, 1, 0, st>>>(scal.p);
   FM_LAUNCHED();
-
-  g->det.resize(L);
-  g->flag.resize(L);
-  for (int l = 0; l < L; ++l) {
-    g->det[l].alloc(9 * g->nodes(l));
-    g->flag[l].alloc(g->nodes(l));
-  }
-  g->coarse.alloc(3 * g->nodes(0));
-
   if (L == 0) {
-    k_copy_fine<<<blocks_for(g->nodes(0), 256), 256, 0, st>>>(vv, scal.p, g->coarse.p, g->M,
-                                                             g->nodes(0));
+    k_copy_fine<<<blocks_for(g.nodes(0), 256), 256, 0, st>>>(vv, scal.p, g.coarse.p, g.M, g.nodes(0));
     FM_LAUNCHED();
   } else {
     // encode L levels in passes of up to 5 levels (4^5 = 1024 inputs per CTA)
     int lev_in = L;
-    DBuf<double> sc_prev;
-    bool first = true;
-    while (lev_in > 0) {
-      const int T = std::min(5, lev_in);
+    for (size_t k = 0; k < passes.size(); ++k) {
+      const int T = passes[k];
       const int lev_out = lev_in - T;
-      DBuf<double> sc_out;
-      double* out_p;
-      if (lev_out == 0) {
-        out_p = g->coarse.p;
-      } else {
-        sc_out.alloc(3 * g->nodes(lev_out));
-        out_p = sc_out.p;
-      }
       EncParams p{};
       p.vv = vv;
-      p.sc_in = sc_prev.p;
-      p.sc_out = out_p;
+      p.sc_in = k ? roots[k - 1].p : nullptr;
+      p.sc_out = lev_out == 0 ? g.coarse.p : roots[k].p;
       for (int l = 0; l < L; ++l) {
-        p.det[l] = g->det[l].p;
-        p.flag[l] = g->flag[l].p;
+        p.det[l] = g.det[l].p;
+        p.flag[l] = g.flag[l].p;
       }
       p.scal = scal.p;
       p.eps = eps;
       p.lev_in = lev_in;
       p.T = T;
-      p.M = g->M;
+      p.M = g.M;
       p.kind = kind;
-      const uint64_t tiles = g->nodes(lev_out);
+      const uint64_t tiles = g.nodes(lev_out);
       const int threads = 1 << (2 * (T - 1));
       const size_t smem = sizeof(P3) * threads;
-      if (first)
+      if (k == 0)
         k_encode_tiles<true><<<unsigned(tiles), threads, smem, st>>>(p);
       else
         k_encode_tiles<false><<<unsigned(tiles), threads, smem, st>>>(p);
       FM_LAUNCHED();
-      first = false;
-      sc_prev = std::move(sc_out);
       lev_in = lev_out;
     }
   }
-  // final flags + subtree counts, fine -> coarse
-  g->cnt.resize(L);
-  for (int l = 0; l < L; ++l) g->cnt[l].alloc(g->nodes(l));
-  for (int l = L - 1; l >= 0; --l) {
-    const uint64_t nodes = g->nodes(l);
-    k_grade_count<<<blocks_for(nodes, 256), 256, 0, st>>>(
-        g->flag[l].p, l + 1 < L ? g->flag[l + 1].p : nullptr, g->cnt[l].p,
-        l + 1 < L ? g->cnt[l + 1].p : nullptr, l, L, g->M, g->N, nodes, graded ? 1 : 0);
-    FM_LAUNCHED();
-  }
-  build_leaves(*g);
   FM_CUDA(cudaEventRecord(e1, st));
   Scalars hs{};
   scal.download(&hs, 1);
   FM_CUDA(cudaStreamSynchronize(st));
   if (hs.err) throw Error(FM_ERR_DOMAIN, "project_vertices: non-finite vertex value");
-  g->field_norm = hs.norm;
-  g->mra_ms = elapsed_ms(e0, e1);
+  g.field_norm = hs.norm;
+  if (ms) *ms = elapsed_ms(e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+// Final flags (closure + optional 2:1 grading) and subtree leaf counts, one
+// gather pass per level fine -> coarse (k_grade_count).
+void grade_count_levels(Grid& g, bool graded) {
+  cudaStream_t st = stream();
+  const int L = g.L;
+  g.cnt.resize(L);
+  for (int l = 0; l < L; ++l) g.cnt[l].alloc(g.nodes(l));
+  for (int l = L - 1; l >= 0; --l) {
+    const uint64_t nodes = g.nodes(l);
+    k_grade_count<<<blocks_for(nodes, 256), 256, 0, st>>>(
+        g.flag[l].p, l + 1 < L ? g.flag[l + 1].p : nullptr, g.cnt[l].p,
+        l + 1 < L ? g.cnt[l + 1].p : nullptr, l, L, g.M, g.N, nodes, graded ? 1 : 0);
+    FM_LAUNCHED();
+  }
+}
+
+Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind) {
+  auto g = std::make_unique<Grid>();
+  g->graded = graded;
+  double enc_ms = 0.0;
+  mra_encode(dem, L, eps, kind, *g, &enc_ms);
+  // pre-size the count/offset pyramids so the timed region holds kernels only
+  g->cnt.resize(L);
+  g->off.resize(L);
+  for (int l = 0; l < L; ++l) {
+    g->cnt[l].alloc(g->nodes(l));
+    g->off[l].alloc(g->nodes(l));
+  }
+  cudaStream_t st = stream();
+  cudaEvent_t e0, e1;
+  FM_CUDA(cudaEventCreate(&e0));
+  FM_CUDA(cudaEventCreate(&e1));
+  FM_CUDA(cudaEventRecord(e0, st));
+  grade_count_levels(*g, graded);
+  build_leaves(*g);
+  FM_CUDA(cudaEventRecord(e1, st));
+  FM_CUDA(cudaStreamSynchronize(st));
+  g->mra_ms = enc_ms + elapsed_ms(e0, e1);
   const double Nf = double(g->nodes(L)), Nint = double(uint64_t(g->M) * g->N) * ((std::pow(4.0, L) - 1) / 3);
   g->mra_bytes = 24.0 * Nf + 73.0 * Nint + 36.0 * double(g->nleaves);
   cudaEventDestroy(e0);

@@ -40,7 +40,15 @@ cudaStream_t stream() {
   if (g_stream) return g_stream;
   int dev = 0;
   FM_CUDA(cudaGetDevice(&dev));
-  if (!own[dev]) FM_CUDA(cudaStreamCreateWithFlags(&own[dev], cudaStreamNonBlocking));
+  if (!own[dev]) {
+    FM_CUDA(cudaStreamCreateWithFlags(&own[dev], cudaStreamNonBlocking));
+    // keep freed blocks in the stream-ordered pool: the pyramids of repeated
+    // MRA / adapt passes are re-allocated without new page mappings
+    cudaMemPool_t pool;
+    FM_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = UINT64_MAX;
+    FM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   return own[dev];
 }
 void set_stream(cudaStream_t s) { g_stream = s; }

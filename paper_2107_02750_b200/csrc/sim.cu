@@ -299,6 +299,18 @@ static void nonuniform_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem, 
   }
 }
 
+// Initial conditions shared with the adaptive set-up.
+void ic_surface_or_depth(Sim& s, const fm_sim_desc* d) {
+  const int mode = d->has_initial_surface ? 1 : d->initial_depth > 0.0 ? 2 : 0;
+  k_ic_simple<<<nblk(s.n, 256), 256, 0, stream()>>>(s.n, s.z.p, mode,
+                                                     mode == 1 ? d->initial_surface : d->initial_depth, s.u.p);
+  FM_LAUNCHED();
+}
+void ic_finish(Sim& s) {
+  k_ic_finish<<<nblk(s.n, 256), 256, 0, stream()>>>(s.n, s.scheme != FM_DG2, s.hdry, s.z.p, s.u.p);
+  FM_LAUNCHED();
+}
+
 Sim* sim_create(const fm_sim_desc* d, const fm_raster* dem, const Grid* grid) {
   if (!d || !dem) throw Error(FM_ERR_CONFIG, "null descriptor or DEM");
   upload_banks();
@@ -569,7 +581,9 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
       if (!c.active || !c.had_step) break;
       s.since_adapt += 1;
       if (s.since_adapt >= s.adapt_every && !(c.now >= c.end_time)) {
+        if (fv1_staged(s)) fv1_to_u(s);
         adaptive_adapt(s, c.now);
+        if (fv1_staged(s)) fv1_to_star(s);
         s.since_adapt = 0;
         // the adapt changed the leaf set: refresh the step's reductions
         DevRed r[2];
