@@ -319,7 +319,7 @@ def main():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--scale", type=int, default=1, help="shrink config 4 (tests only)")
     p.add_argument("--profile-steps", type=int, default=10)
-    p.add_argument("--chunk", type=int, default=64, help="timed steps between state restores")
+    p.add_argument("--chunk", type=int, default=16, help="timed steps between state restores")
     p.add_argument("--cpu-steps", type=int, default=40)
     p.add_argument("--cpu-steps-cap", type=int, default=20)
     p.add_argument("--no-cpu", action="store_true")

@@ -115,6 +115,7 @@ struct Sim {
   // CUDA graph of a batch of steps
   cudaGraphExec_t graph = nullptr;
   int graph_steps = 0;
+  int64_t graph_kernels = 0;
   ~Sim();
 
   NuView view() const;

@@ -609,12 +609,12 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
       FM_CUDA(cudaGraphInstantiate(&s.graph, gr, 0));
       cudaGraphDestroy(gr);
       s.graph_steps = kBatch;
+      s.graph_kernels = launches() - before;  // kernels per replay
     }
-    const int64_t per_graph = launches() - before;
     int64_t done = 0;
     while (done < max_steps) {
       FM_CUDA(cudaGraphLaunch(s.graph, st));
-      count_graph_launches(per_graph ? per_graph : 0);
+      count_graph_launches(s.graph_kernels);
       done += s.graph_steps;
       if (done < max_steps) {
         DevClock c;
