@@ -195,6 +195,21 @@ int fm_sim_finite(fm_sim* s, int32_t* ok, double* bad_x, double* bad_y);
 int fm_sim_download(fm_sim* s, int32_t* level, int32_t* i, int32_t* j, double* u9, double* z3);
 /* Overwrite the flow state (reference order) — lockstep re-seeding. */
 int fm_sim_upload(fm_sim* s, const double* u9);
+/* Geometry of the rasters below: depth_raster()/qx_raster()/qy_raster() of
+ * NonUniformSim (fine grid, (N<<L) x (M<<L), quadgrid.cpp:266-272) and
+ * UniformSim (ny x nx, solver_uniform.cpp:503-509). */
+int fm_sim_raster_shape(fm_sim* s, int32_t* ncols, int32_t* nrows, double* xll, double* yll,
+                        double* cellsize, double* nodata);
+/* Sim::depth_raster / qx_raster / qy_raster (which = 0 / 1 / 2): non-uniform
+ * sims sample every leaf plane at the fine-cell centres (sample_to_raster,
+ * quadgrid.cpp:262-285, via solver_nonuniform.cpp:508-519), uniform sims copy
+ * c0 (solver_uniform.cpp:501-520).  Row 0 north, ncols*nrows doubles into
+ * `out` (a CUDA device pointer when out_on_device != 0).  The caller applies
+ * crop_and_mask (sim_common.cpp:133-151) as drive<Sim> does. */
+int fm_sim_raster(fm_sim* s, int32_t which, double* out, int32_t out_on_device);
+/* Sim::sample_gauge (solver_nonuniform.cpp:489-506, solver_uniform.cpp:480-498)
+ * at n points: out4 = n x GaugeValue {h, eta, u, v} (sim_common.hpp:47-49). */
+int fm_sim_sample_gauges(fm_sim* s, int32_t n, const double* x, const double* y, double* out4);
 /* Device-side checkpoint of the flow state (U, U*, ACC discharges) and
  * its restore, without host traffic; restore fails if the leaf set changed
  * since the snapshot (adaptive re-gridding). */

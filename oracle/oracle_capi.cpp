@@ -293,6 +293,42 @@ int orc_sim_download(orc_sim* s, int32_t* lv, int32_t* ii, int32_t* jj, double* 
   });
 }
 
+// Raster geometry of depth_raster()/qx_raster()/qy_raster() (quadgrid.cpp:266-272,
+// solver_uniform.cpp:503-509).
+int orc_sim_raster_shape(orc_sim* s, int32_t* nc, int32_t* nr, double* xll, double* yll,
+                         double* cs, double* nodata) {
+  return guard([&] {
+    if (UN* u = s->un()) {
+      *nc = u->nx, *nr = u->ny, *xll = u->x0, *yll = u->y0, *cs = u->R, *nodata = -9999.0;
+      return;
+    }
+    const Grid& g = s->nu()->grid;
+    *nc = g.M << g.L, *nr = g.N << g.L, *xll = g.x0, *yll = g.y0, *cs = g.R, *nodata = -9999.0;
+  });
+}
+
+int orc_sim_raster(orc_sim* s, int32_t which, double* out, int32_t on_device) {
+  return guard([&] {
+    if (on_device) throw Fail(E_CONFIG, "oracle rasters are host-only");
+    if (which < 0 || which > 2) throw Fail(E_CONFIG, "raster: which must be 0 (h), 1 (qx) or 2 (qy)");
+    if (UN* u = s->un())
+      raster(*u, which, out);
+    else
+      raster(*s->nu(), which, out);
+  });
+}
+
+int orc_sim_sample_gauges(orc_sim* s, int32_t n, const double* x, const double* y, double* out4) {
+  return guard([&] {
+    for (int32_t k = 0; k < n; ++k) {
+      if (UN* u = s->un())
+        gauge(*u, x[k], y[k], out4 + 4 * k);
+      else
+        gauge(*s->nu(), x[k], y[k], out4 + 4 * k);
+    }
+  });
+}
+
 int orc_sim_upload(orc_sim* s, const double* u9) {
   return guard([&] {
     auto& u = s->un() ? s->un()->u : s->nu()->u;

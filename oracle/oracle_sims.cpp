@@ -1043,4 +1043,85 @@ UN make_un(const Cfg& c, const Raster& dem) {
   return s;
 }
 
+
+// ---- output sampling --------------------------------------------------------
+
+// NonUniformSim::sample_gauge (solver_nonuniform.cpp:489-506) via
+// QuadGrid::find_point (quadgrid.cpp:70-74).
+void gauge(const NU& s, double x, double y, double out[4]) {
+  const Grid& g = s.grid;
+  const int fi = int(std::floor((x - g.x0) / g.R));
+  const int fj = int(std::floor((y - g.y0) / g.R));
+  const int k = g.containing(std::clamp(fi, 0, (g.M << g.L) - 1), std::clamp(fj, 0, (g.N << g.L) - 1));
+  out[0] = out[1] = out[2] = out[3] = 0.0;
+  if (k < 0) return;
+  const Fl& u = s.u[k];
+  if (s.scheme == S_DG2) {
+    const double cx = g.xc(k), cy = g.yc(k), sz = g.size(k);
+    const double h = std::max(0.0, eval_plane(u.h, cx, cy, sz, x, y));
+    const double zv = eval_plane(s.z[k], cx, cy, sz, x, y);
+    const double qx = eval_plane(u.qx, cx, cy, sz, x, y);
+    const double qy = eval_plane(u.qy, cx, cy, sz, x, y);
+    out[0] = h;
+    out[1] = h + zv;
+    out[2] = vel(h, qx, s.hdry);
+    out[3] = vel(h, qy, s.hdry);
+  } else {
+    const double h = u.h.c0;
+    out[0] = h;
+    out[1] = h + s.z[k].c0;
+    out[2] = vel(h, u.qx.c0, s.hdry);
+    out[3] = vel(h, u.qy.c0, s.hdry);
+  }
+}
+
+// UniformSim::sample_gauge (solver_uniform.cpp:480-498)
+void gauge(const UN& s, double x, double y, double out[4]) {
+  const int i = std::clamp(int(std::floor((x - s.x0) / s.R)), 0, s.nx - 1);
+  const int j = std::clamp(int(std::floor((y - s.y0) / s.R)), 0, s.ny - 1);
+  const size_t c = s.cell(i, j);
+  const Fl& u = s.u[c];
+  if (s.kind == S_DG2) {
+    const double xc = s.x0 + (i + 0.5) * s.R, yc = s.y0 + (j + 0.5) * s.R;
+    const double h = std::max(0.0, eval_plane(u.h, xc, yc, s.R, x, y));
+    const double zv = eval_plane(s.z[c], xc, yc, s.R, x, y);
+    const double qx = eval_plane(u.qx, xc, yc, s.R, x, y);
+    const double qy = eval_plane(u.qy, xc, yc, s.R, x, y);
+    out[0] = h;
+    out[1] = h + zv;
+    out[2] = vel(h, qx, s.hdry);
+    out[3] = vel(h, qy, s.hdry);
+  } else {
+    const double h = u.h.c0;
+    out[0] = h;
+    out[1] = h + s.z[c].c0;
+    out[2] = vel(h, u.qx.c0, s.hdry);
+    out[3] = vel(h, u.qy.c0, s.hdry);
+  }
+}
+
+static const Pl& field_of(const Fl& f, int which) { return which == 0 ? f.h : which == 1 ? f.qx : f.qy; }
+
+// sample_to_raster (quadgrid.cpp:262-285) of leaf_raster (solver_nonuniform.cpp:508-514)
+void raster(const NU& s, int which, double* out) {
+  const Grid& g = s.grid;
+  const int nc = g.M << g.L, nr = g.N << g.L;
+  for (int fj = 0; fj < nr; ++fj)
+    for (int fi = 0; fi < nc; ++fi) {
+      const int k = g.containing(fi, fj);
+      if (k < 0) throw Fail(E_STRUCT, "sample_to_raster: hole in grid");
+      const double x = g.x0 + (fi + 0.5) * g.R;
+      const double y = g.y0 + (fj + 0.5) * g.R;
+      out[size_t(nr - 1 - fj) * nc + fi] =
+          eval_plane(field_of(s.u[k], which), g.xc(k), g.yc(k), g.size(k), x, y);
+    }
+}
+
+// field_raster (solver_uniform.cpp:501-516)
+void raster(const UN& s, int which, double* out) {
+  for (int j = 0; j < s.ny; ++j)
+    for (int i = 0; i < s.nx; ++i)
+      out[size_t(s.ny - 1 - j) * s.nx + i] = field_of(s.u[s.cell(i, j)], which).c0;
+}
+
 }  // namespace orc

@@ -141,4 +141,14 @@ struct UN {
 };
 UN make_un(const Cfg& c, const Raster& dem);  // solver_uniform.cpp:522-601
 
+// ---- output sampling --------------------------------------------------------
+// GaugeValue {h, eta, u, v} (sim_common.hpp:47-49)
+void gauge(const NU& s, double x, double y, double out[4]);  // solver_nonuniform.cpp:489-506
+void gauge(const UN& s, double x, double y, double out[4]);  // solver_uniform.cpp:480-498
+// Fine-grid rasters, row 0 north.  NU: leaf_raster -> sample_to_raster
+// (solver_nonuniform.cpp:508-519, quadgrid.cpp:262-285), (N<<L) x (M<<L);
+// UN: field_raster (solver_uniform.cpp:501-516), ny x nx.  which: 0 h, 1 qx, 2 qy.
+void raster(const NU& s, int which, double* out);
+void raster(const UN& s, int which, double* out);
+
 }  // namespace orc

@@ -323,6 +323,39 @@ int ref_sim_download(ref_sim* s, int32_t* lv, int32_t* ii, int32_t* jj, double* 
   });
 }
 
+// depth_raster()/qx_raster()/qy_raster() and sample_gauge() of the reference
+// sims (solver_nonuniform.cpp:489-519, solver_uniform.cpp:480-520).
+static fm::Raster ref_raster(ref_sim* s, int which) {
+  return s->visit([&](auto& sim) {
+    return which == 0 ? sim.depth_raster() : which == 1 ? sim.qx_raster() : sim.qy_raster();
+  });
+}
+
+int ref_sim_raster_shape(ref_sim* s, int32_t* nc, int32_t* nr, double* xll, double* yll,
+                         double* cs, double* nodata) {
+  return guard([&] {
+    const fm::Raster r = ref_raster(s, 0);
+    *nc = r.ncols, *nr = r.nrows, *xll = r.xll, *yll = r.yll, *cs = r.cellsize, *nodata = r.nodata;
+  });
+}
+
+int ref_sim_raster(ref_sim* s, int32_t which, double* out, int32_t on_device) {
+  return guard([&] {
+    if (on_device) throw fm::ConfigError("reference rasters are host-only");
+    const fm::Raster r = ref_raster(s, which);
+    std::memcpy(out, r.values.data(), r.values.size() * sizeof(double));
+  });
+}
+
+int ref_sim_sample_gauges(ref_sim* s, int32_t n, const double* x, const double* y, double* out4) {
+  return guard([&] {
+    for (int32_t k = 0; k < n; ++k) {
+      const fm::GaugeValue v = s->visit([&](auto& sim) { return sim.sample_gauge(x[k], y[k]); });
+      out4[4 * k] = v.h, out4[4 * k + 1] = v.eta, out4[4 * k + 2] = v.u, out4[4 * k + 3] = v.v;
+    }
+  });
+}
+
 int ref_sim_upload(ref_sim* s, const double* u9) {
   return guard([&] {
     auto& u = std::get_if<fm::UniformSim>(&s->s) ? std::get_if<fm::UniformSim>(&s->s)->u : s->nu()->u;

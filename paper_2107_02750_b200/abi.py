@@ -100,6 +100,9 @@ SIGS = {
     "sim_finite": (C.c_int, [P, PI32, PD, PD]),
     "sim_download": (C.c_int, [P, PI32, PI32, PI32, PD, PD]),
     "sim_upload": (C.c_int, [P, PD]),
+    "sim_raster_shape": (C.c_int, [P, PI32, PI32, PD, PD, PD, PD]),
+    "sim_raster": (C.c_int, [P, I32, PD, I32]),
+    "sim_sample_gauges": (C.c_int, [P, I32, PD, PD, PD]),
     "sim_element_log": (I64, [P, PD, PI64, I64]),
     "sim_run": (C.c_int, [P, C.POINTER(c_clock), I64, I32, C.POINTER(c_result)]),
 }
@@ -354,6 +357,29 @@ class Sim:
     def upload(self, u9: np.ndarray):
         u9 = np.ascontiguousarray(u9, np.float64)
         self.be.call("sim_upload", self.h, dptr(u9))
+
+    def raster_shape(self) -> dict:
+        nc, nr = I32(), I32()
+        xll, yll, cs, nd = D(), D(), D(), D()
+        self.be.call("sim_raster_shape", self.h, C.byref(nc), C.byref(nr), C.byref(xll),
+                     C.byref(yll), C.byref(cs), C.byref(nd))
+        return dict(ncols=nc.value, nrows=nr.value, xll=xll.value, yll=yll.value,
+                    cellsize=cs.value, nodata=nd.value)
+
+    def raster(self, which: int) -> np.ndarray:
+        """depth_raster / qx_raster / qy_raster (which 0/1/2), row 0 north."""
+        sh = self.raster_shape()
+        out = np.empty((sh["nrows"], sh["ncols"]), np.float64)
+        self.be.call("sim_raster", self.h, int(which), dptr(out), 0)
+        return out
+
+    def sample_gauges(self, x, y) -> np.ndarray:
+        """sample_gauge at each (x, y): rows of GaugeValue {h, eta, u, v}."""
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.ascontiguousarray(y, np.float64)
+        out = np.zeros((len(x), 4), np.float64)
+        self.be.call("sim_sample_gauges", self.h, len(x), dptr(x), dptr(y), dptr(out))
+        return out
 
     def element_log(self):
         n = int(self.be.fn["sim_element_log"](self.h, None, None, 0))

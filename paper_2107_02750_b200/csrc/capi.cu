@@ -305,6 +305,16 @@ int fm_sim_download(fm_sim* s, int32_t* l, int32_t* i, int32_t* j, double* u9, d
 int fm_sim_upload(fm_sim* s, const double* u9) {
   return guard([&] { sim_upload(*s->s, u9); });
 }
+int fm_sim_raster_shape(fm_sim* s, int32_t* nc, int32_t* nr, double* xll, double* yll, double* cs,
+                        double* nodata) {
+  return guard([&] { sim_raster_shape(*s->s, nc, nr, xll, yll, cs, nodata); });
+}
+int fm_sim_raster(fm_sim* s, int32_t which, double* out, int32_t on_device) {
+  return guard([&] { sim_raster(*s->s, which, out, on_device != 0); });
+}
+int fm_sim_sample_gauges(fm_sim* s, int32_t n, const double* x, const double* y, double* out4) {
+  return guard([&] { sim_sample_gauges(*s->s, n, x, y, out4); });
+}
 int fm_sim_snapshot(fm_sim* s) {
   return guard([&] { sim_snapshot(*s->s); });
 }

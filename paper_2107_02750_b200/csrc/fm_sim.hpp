@@ -133,6 +133,12 @@ void sim_upload(Sim& s, const double* u9);
 void sim_run(Sim& s, fm_clock* clk, int64_t max_steps, int stop_at_events, fm_run_result* out);
 void sim_profile(Sim& s, int64_t steps, double* ms, int64_t* counts, int cap, int* nfam);
 void sim_snapshot(Sim& s);
+void sim_sync_u(Sim& s);  // FV1: move the staged post-step state back into u
+// output sampling (output.cu)
+void sim_raster_shape(const Sim& s, int32_t* nc, int32_t* nr, double* xll, double* yll, double* cs,
+                      double* nodata);
+void sim_raster(Sim& s, int which, double* out, bool on_device);
+void sim_sample_gauges(Sim& s, int n, const double* x, const double* y, double* out4);
 void sim_restore(Sim& s);
 
 // topology (topo.cu)

@@ -517,6 +517,10 @@ static std::vector<int64_t> sim_order(Sim& s, std::vector<int8_t>& l, std::vecto
   return perm;
 }
 
+void sim_sync_u(Sim& s) {
+  if (fv1_staged(s)) fv1_to_u(s);
+}
+
 void sim_download(Sim& s, int32_t* lo, int32_t* io, int32_t* jo, double* u9, double* z3) {
   if (fv1_staged(s)) fv1_to_u(s);
   std::vector<int8_t> l;
