@@ -134,6 +134,8 @@ enum KernelFamily {
   KF_UNI_HEAD,    // uniform raster: head + friction
   KF_UNI_STAGE1,  // uniform raster: stage 1
   KF_UNI_STAGE2,  // uniform raster: stage 2
+  KF_SEG1,        // segment states, stage 1
+  KF_SEG2,        // segment states, stage 2
   KF_COUNT
 };
 const char* kernel_family_name(int f);

@@ -60,7 +60,8 @@ struct NuView {
   // ACC
   const int32_t* seg_l;
   const int32_t* seg_r;
-  const int32_t* sid;   // 8 per leaf
+  const int32_t* sid;   // 8 per leaf: segment ids of the sub-faces per side
+  const double* segst;  // 6 per segment: HLL flux (m n t), z*, h*L, h*R
   long long nseg;
 };
 
@@ -84,6 +85,7 @@ struct Sim {
   DBuf<double> u, us, z, nman, zpair;
   DBuf<int32_t> nb, sid, seg_l, seg_r;
   DBuf<uint8_t> sk;
+  DBuf<double> segst;       // DG2/FV1 segment states (6 per segment)
   DBuf<double> accq, accqb;  // ACC: per segment, per leaf-side (4 per leaf)
   DBuf<double> aqx, aqy;     // uniform ACC faces
   DBuf<int32_t> infc;        // per inflow per leaf counts

@@ -130,9 +130,28 @@ struct EncParams {
 // builds its four children itself (projecting them from the DEM vertices when
 // FROM_VERTICES) so the finest, largest level never touches shared memory;
 // higher levels go through a 4^(T-1)-entry shared buffer.
+// Details are staged in shared memory and leave the CTA as contiguous 16 B
+// vectors: a level's parents of one tile are contiguous in the block-Morton
+// layout, so the tile's 9 x count doubles are one contiguous range (direct
+// 72 B-strided per-thread stores cost ~3x the bytes in DRAM writes).
+__device__ __forceinline__ void store_details(const double* __restrict__ sdet, double* __restrict__ o,
+                                              int count, int tid, int nthr) {
+  const int total = 9 * count;
+  if ((reinterpret_cast<uintptr_t>(o) & 15) || (total & 1)) {  // a single odd-placed node
+    for (int e = tid; e < total; e += nthr) o[e] = sdet[e];
+    return;
+  }
+  const double2* src = reinterpret_cast<const double2*>(sdet);
+  double2* dst = reinterpret_cast<double2*>(o);
+  for (int e = tid; e < total / 2; e += nthr) dst[e] = src[e];
+}
+
 template <bool FROM_VERTICES>
 __global__ void __launch_bounds__(256) k_encode_tiles(EncParams p) {
-  extern __shared__ P3 sbuf[];
+  extern __shared__ double smem[];
+  const int nthr = blockDim.x;
+  P3* sbuf = reinterpret_cast<P3*>(smem);
+  double* sdet = smem + 3 * nthr;  // 9 per first-level parent
   const int tid = threadIdx.x;
   const uint64_t tile = blockIdx.x;
   const double norm = p.scal->norm;
@@ -140,7 +159,8 @@ __global__ void __launch_bounds__(256) k_encode_tiles(EncParams p) {
 
   // first level: parent (lev_in - 1), local index tid
   int lev = p.lev_in - 1;
-  const uint64_t par = (tile << (2 * (p.T - 1))) + uint64_t(tid);
+  const uint64_t par0 = tile << (2 * (p.T - 1));
+  const uint64_t par = par0 + uint64_t(tid);
   P3 kids[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -157,40 +177,41 @@ __global__ void __launch_bounds__(256) k_encode_tiles(EncParams p) {
   P3 par_s;
   double d[9];
   encode(kids, p.kind, par_s, d);
-  {
-    double* o = p.det[lev] + 9 * par;
 #pragma unroll
-    for (int n = 0; n < 9; ++n) o[n] = d[n];
-    p.flag[lev][par] = dhat(d, norm) >= p.eps ? 1 : 0;
-  }
+  for (int n = 0; n < 9; ++n) sdet[9 * tid + n] = d[n];
+  p.flag[lev][par] = dhat(d, norm) >= p.eps ? 1 : 0;
   if (p.T == 1) {
     double* o = p.sc_out + 3 * par;
     o[0] = par_s.c0;
     o[1] = par_s.cx;
     o[2] = par_s.cy;
-    return;
+  } else {
+    sbuf[tid] = par_s;
   }
-  sbuf[tid] = par_s;
   __syncthreads();
-  int count = blockDim.x;  // nodes at `lev`
+  store_details(sdet, p.det[lev] + 9 * par0, nthr, tid, nthr);
+  if (p.T == 1) return;
+  int count = nthr;  // nodes at `lev`
   for (int t = 1; t < p.T; ++t) {
     --lev;
     count >>= 2;
     P3 mine;
-    bool have = tid < count;
+    const bool have = tid < count;
+    const uint64_t node0 = tile << (2 * (p.T - 1 - t));
     if (have) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) kids[k] = sbuf[4 * tid + k];
       encode(kids, p.kind, mine, d);
-      const uint64_t node = (tile << (2 * (p.T - 1 - t))) + uint64_t(tid);
-      double* o = p.det[lev] + 9 * node;
+      p.flag[lev][node0 + tid] = dhat(d, norm) >= p.eps ? 1 : 0;
+    }
+    __syncthreads();  // sbuf reads and the previous sdet stores are done
+    if (have) {
+      sbuf[tid] = mine;
 #pragma unroll
-      for (int n = 0; n < 9; ++n) o[n] = d[n];
-      p.flag[lev][node] = dhat(d, norm) >= p.eps ? 1 : 0;
+      for (int n = 0; n < 9; ++n) sdet[9 * tid + n] = d[n];
     }
     __syncthreads();
-    if (have) sbuf[tid] = mine;
-    __syncthreads();
+    store_details(sdet, p.det[lev] + 9 * node0, count, tid, nthr);
   }
   if (tid == 0) {
     double* o = p.sc_out + 3 * tile;
@@ -542,7 +563,7 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
       p.kind = kind;
       const uint64_t tiles = g.nodes(lev_out);
       const int threads = 1 << (2 * (T - 1));
-      const size_t smem = sizeof(P3) * threads;
+      const size_t smem = (sizeof(P3) + 9 * sizeof(double)) * threads;
       if (k == 0)
         k_encode_tiles<true><<<unsigned(tiles), threads, smem, st>>>(p);
       else

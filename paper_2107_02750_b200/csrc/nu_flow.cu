@@ -52,6 +52,67 @@ __global__ void __launch_bounds__(256) k_head_friction(NuView v, DevClock* clk, 
   for (int q = 0; q < 9; ++q) o[q] = s[q];
 }
 
+// ---- segment states ------------------------------------------------------
+// One thread per interior segment (segment_states, solver_nonuniform.cpp:91-115):
+// both leaves' limits at the segment centre, z* = max(zL, zR), the starred
+// depths and the HLL flux, stored as {m, n, t, z*, h*L, h*R}.  Every segment
+// runs the same code path (one HLL), unlike a per-leaf-side formulation where
+// lanes of a warp face 0, 1 or 2 sub-faces and every face is solved twice.
+template <bool P2>
+__global__ void __launch_bounds__(256) k_seg(NuView v, const DevClock* __restrict__ clk,
+                                             const double* __restrict__ in, double* __restrict__ out,
+                                             int manual, int* err) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (!manual && !clk[1].active) return;
+  if (q >= v.nseg) return;
+  const int a = v.seg_l[q], b = v.seg_r[q];  // W/S and E/N leaf
+  const int la = v.lvl[a], lb = v.lvl[b];
+  const int ia = v.li[a], ja = v.lj[a], ib = v.li[b], jb = v.lj[b];
+  // x-normal iff b starts where a ends along x (fine-cell units)
+  const bool xn = (ib << (v.L - lb)) == ((ia + 1) << (v.L - la));
+  double sa[9], sb[9];
+  load9(in, a, sa);
+  load9(in, b, sb);
+  const P3 za = load3(v.z, a), zb = load3(v.z, b);
+  Pt A, B;
+  if (P2) {
+    // enumerate_faces geometry (quadgrid.cpp:222-245) as exact offsets: the
+    // centre lies on the face, at the finer (or either) leaf's centre along it
+    const double ta = la < lb ? (((xn ? jb : ib) & 1) ? 0.25 : -0.25) : 0.0;
+    const double tb = lb < la ? (((xn ? ja : ia) & 1) ? 0.25 : -0.25) : 0.0;
+    A = xn ? limit_rel(sa, za, 0.5, ta, v.hdry) : limit_rel(sa, za, ta, 0.5, v.hdry);
+    B = xn ? limit_rel(sb, zb, -0.5, tb, v.hdry) : limit_rel(sb, zb, tb, -0.5, v.hdry);
+  } else {
+    const double sza = lsize(v, la), szb = lsize(v, lb);
+    const double cxa = lcen(v.x0, v, la, ia), cya = lcen(v.y0, v, la, ja);
+    const double cxb = lcen(v.x0, v, lb, ib), cyb = lcen(v.y0, v, lb, jb);
+    // owner: the coarser leaf, or the W/S leaf at equal level; it fixes the
+    // normal coordinate from its face, the other leaf the tangential one
+    const bool own_a = la <= lb;
+    double x, y;
+    if (xn) {
+      x = own_a ? cxa + sza / 2 : cxb - szb / 2;
+      y = own_a ? cyb : cya;
+    } else {
+      y = own_a ? cya + sza / 2 : cyb - szb / 2;
+      x = own_a ? cxb : cxa;
+    }
+    A = limit(sa, za, cxa, cya, sza, x, y, v.hdry);
+    B = limit(sb, zb, cxb, cyb, szb, x, y, v.hdry);
+  }
+  const double zs = smax(A.z, B.z);
+  const double hl = smax(0.0, A.eta - zs), hr = smax(0.0, B.eta - zs);
+  const Flx f = xn ? hll(hl, hl * A.u, hl * A.v, hr, hr * B.u, hr * B.v, v.g, v.hdry, err)
+                   : hll(hl, hl * A.v, hl * A.u, hr, hr * B.v, hr * B.u, v.g, v.hdry, err);
+  double* o = out + 6 * q;
+  o[0] = f.m;
+  o[1] = f.n;
+  o[2] = f.t;
+  o[3] = zs;
+  o[4] = hl;
+  o[5] = hr;
+}
+
 // ---- one RK stage over all leaves ---------------------------------------
 // STAGE 1: out = positivity(U + dt L(U))               -> U*  (FV1: the full step)
 // STAGE 2: out = positivity(((U* + dt L(U*)) + U) / 2) -> U (in place)
@@ -102,77 +163,31 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock) k_stage(
     const double fx = P2 ? 0.0 : cx + (sd == 1 ? sz / 2 : sd == 3 ? -sz / 2 : 0.0);
     const double fy = P2 ? 0.0 : cy + (sd == 0 ? sz / 2 : sd == 2 ? -sz / 2 : 0.0);
     const Pt me = P2 ? limit_rel(s, zc, ox, oy, v.hdry) : limit(s, zc, cx, cy, sz, fx, fy, v.hdry);
+    // the side's segments (segment_states, solver_nonuniform.cpp:91-115,
+    // computed once per segment by k_seg); the weight len/sz is exactly 1/2
+    // for two finer neighbours and 1 otherwise (sizes are R * 2^k).
     const int nseg = kind == 0 ? 0 : kind == 3 ? 2 : 1;
-    Flx sf[2];
-    double szs[2], shm[2], sw[2];
-#pragma unroll 1
-    for (int t = 0; t < nseg; ++t) {
-      const int q = v.nb[8 * kk + 2 * sd + t];
-      double sq[9];
-      load9(in, q, sq);
-      const P3 zq = load3(v.z, q);
-      Pt pm, pn;
-      if (P2) {
-        // enumerate_faces geometry (quadgrid.cpp:222-245) as exact offsets: the
-        // segment centre sits on the owner's face, at the non-owner's centre
-        // along the face.
-        if (kind == 3) {  // two finer neighbours, S->N / W->E
-          const double tan = t == 0 ? -0.25 : 0.25;
-          pm = limit_rel(s, zc, xn ? ox : tan, xn ? tan : oy, v.hdry);
-        } else {
-          pm = me;
-        }
-        double nx = -ox, ny = -oy;
-        if (kind == 1) {  // coarser neighbour: I sit in one half of its face
-          const double tan = ((xn ? j : i) & 1) ? 0.25 : -0.25;
-          if (xn)
-            ny = tan;
-          else
-            nx = tan;
-        }
-        pn = limit_rel(sq, zq, nx, ny, v.hdry);
-        sw[t] = kind == 3 ? 0.5 : 1.0;
-      } else {
-        const int ql = v.lvl[q];
-        const double qsz = lsize(v, ql);
-        const double qcx = lcen(v.x0, v, ql, v.li[q]), qcy = lcen(v.y0, v, ql, v.lj[q]);
-        // enumerate_faces (quadgrid.cpp:222-245): the owner (coarser leaf, or
-        // W/S leaf at equal level) fixes the normal coordinate from its own
-        // face; the tangential coordinate is the other leaf's centre.
-        const bool owner_me = kind == 3 || (kind == 2 && mine_left);
-        double segx, segy;
-        if (xn) {
-          segx = owner_me ? cx + (sd == 1 ? sz / 2 : -sz / 2) : qcx + (sd == 1 ? -qsz / 2 : qsz / 2);
-          segy = owner_me ? qcy : cy;
-        } else {
-          segy = owner_me ? cy + (sd == 0 ? sz / 2 : -sz / 2) : qcy + (sd == 0 ? -qsz / 2 : qsz / 2);
-          segx = owner_me ? qcx : cx;
-        }
-        const double len = owner_me ? smin(sz, qsz) : smin(qsz, sz);
-        pm = (segx == fx && segy == fy) ? me : limit(s, zc, cx, cy, sz, segx, segy, v.hdry);
-        pn = limit(sq, zq, qcx, qcy, qsz, segx, segy, v.hdry);
-        sw[t] = len / sz;
+    const double w = kind == 3 ? 0.5 : 1.0;
+    double sg[2][6];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (t < nseg) {
+        const double* q = v.segst + 6 * (long long)v.sid[8 * kk + 2 * sd + t];
+#pragma unroll
+        for (int e = 0; e < 6; ++e) sg[t][e] = q[e];
       }
-      const Pt& A = mine_left ? pm : pn;
-      const Pt& B = mine_left ? pn : pm;
-      const double zs = smax(A.z, B.z);
-      const double hl = smax(0.0, A.eta - zs), hr = smax(0.0, B.eta - zs);
-      sf[t] = xn ? hll(hl, hl * A.u, hl * A.v, hr, hr * B.u, hr * B.v, v.g, v.hdry, err)
-                 : hll(hl, hl * A.v, hl * A.u, hr, hr * B.v, hr * B.u, v.g, v.hdry, err);
-      szs[t] = zs;
-      shm[t] = mine_left ? hl : hr;
     }
     double zstar;
     if (kind == 0) {
       zstar = me.z;
     } else if (nseg == 1) {
-      zstar = szs[0];
+      zstar = sg[0][3];
     } else if (v.zpair) {
       zstar = smax(me.z, v.zpair[4 * kk + sd]);
     } else {
       double acc = 0.0;
-      acc += sw[0] * szs[0];
-      acc += sw[1] * szs[1];
+      acc += w * sg[0][3];
+      acc += w * sg[1][3];
       zstar = acc;
     }
     SideOut o;
@@ -191,11 +206,15 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock) k_stage(
       acc.n += f.n;
       acc.t += f.t;
     } else {
-      for (int t = 0; t < nseg; ++t) {
-        const double corr = 0.5 * v.g * (h * h - shm[t] * shm[t]);
-        acc.m += sw[t] * sf[t].m;
-        acc.n += sw[t] * (sf[t].n + corr);
-        acc.t += sw[t] * sf[t].t;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (t < nseg) {
+          const double hme = mine_left ? sg[t][4] : sg[t][5];
+          const double corr = 0.5 * v.g * (h * h - hme * hme);
+          acc.m += w * sg[t][0];
+          acc.n += w * (sg[t][1] + corr);
+          acc.t += w * sg[t][2];
+        }
       }
     }
     o.fm = acc.m;
@@ -458,38 +477,44 @@ void nu_launch_step(Sim& s, bool manual, double mdt, int* err) {
     k_acc_leaves<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.u.p, s.accq.p, s.accqb.p, manual, mdt);
     FM_LAUNCHED();
     kt_end();
-  } else if (s.scheme == FM_FV1) {
-    // FV1 state lives in U* between steps; the head moves it to U with friction
-    kt_begin(KF_HEAD);
-    k_head_friction<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.us.p, s.u.p, manual, mdt);
-    FM_LAUNCHED();
-    kt_end();
-    kt_begin(KF_STAGE1);
-    if (s.p2)
-      k_stage<1, true><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
-    else
-      k_stage<1, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
-    FM_LAUNCHED();
-    kt_end();
   } else {
+    // DG2: head, (segments, leaves) x 2.  FV1 keeps its state in U* between
+    // steps; its head moves it to U with friction and stage 1 is the update.
+    const bool fv1 = s.scheme == FM_FV1;
+    const long long ns = std::max<long long>(s.nseg, 1);
+    auto seg = [&](int fam, const double* in) {
+      kt_begin(fam);
+      if (s.p2)
+        k_seg<true><<<nblk(ns, 256), 256, 0, st>>>(v, clk, in, s.segst.p, manual, err);
+      else
+        k_seg<false><<<nblk(ns, 256), 256, 0, st>>>(v, clk, in, s.segst.p, manual, err);
+      FM_LAUNCHED();
+      kt_end();
+    };
     kt_begin(KF_HEAD);
-    k_head_friction<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.u.p, s.u.p, manual, mdt);
+    k_head_friction<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, fv1 ? s.us.p : s.u.p, s.u.p,
+                                                  manual, mdt);
     FM_LAUNCHED();
     kt_end();
+    seg(KF_SEG1, s.u.p);
     kt_begin(KF_STAGE1);
+    const int last1 = fv1 ? 1 : 0;
     if (s.p2)
-      k_stage<1, true><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
+      k_stage<1, true><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, last1, manual, mdt, err);
     else
-      k_stage<1, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
+      k_stage<1, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, last1, manual, mdt, err);
     FM_LAUNCHED();
     kt_end();
-    kt_begin(KF_STAGE2);
-    if (s.p2)
-      k_stage<2, true><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
-    else
-      k_stage<2, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
-    FM_LAUNCHED();
-    kt_end();
+    if (!fv1) {
+      seg(KF_SEG2, s.us.p);
+      kt_begin(KF_STAGE2);
+      if (s.p2)
+        k_stage<2, true><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+      else
+        k_stage<2, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+      FM_LAUNCHED();
+      kt_end();
+    }
   }
   if (!manual) {
     kt_begin(KF_COMMIT);

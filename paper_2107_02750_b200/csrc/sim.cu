@@ -143,6 +143,7 @@ NuView Sim::view() const {
   v.seg_l = seg_l.p;
   v.seg_r = seg_r.p;
   v.sid = sid.p;
+  v.segst = segst.p;
   v.nseg = nseg;
   return v;
 }

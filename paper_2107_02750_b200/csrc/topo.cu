@@ -284,13 +284,14 @@ void build_topology(Sim& s, const Grid& g) {
   err.download(&herr, 1);
   FM_CUDA(cudaStreamSynchronize(st));
   if (herr) throw Error(FM_ERR_STRUCTURE, "non-uniform solvers require a graded (2:1) grid");
-  if (s.scheme == FM_ACC) {
+  {
     s.sid.alloc(8 * n);
     s.seg_l.alloc(std::max<int64_t>(s.nseg, 1));
     s.seg_r.alloc(std::max<int64_t>(s.nseg, 1));
     k_segments<<<nblk(n, 256), 256, 0, st>>>(n, s.li.p, s.lj.p, s.nb.p, s.sk.p, base.p, s.sid.p,
                                               s.seg_l.p, s.seg_r.p);
     FM_LAUNCHED();
+    if (s.scheme != FM_ACC) s.segst.alloc(6 * size_t(std::max<int64_t>(s.nseg, 1)));
   }
 }
 
