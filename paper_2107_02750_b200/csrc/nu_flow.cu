@@ -102,8 +102,10 @@ __global__ void __launch_bounds__(256) k_seg(NuView v, const DevClock* __restric
   }
   const double zs = smax(A.z, B.z);
   const double hl = smax(0.0, A.eta - zs), hr = smax(0.0, B.eta - zs);
-  const Flx f = xn ? hll(hl, hl * A.u, hl * A.v, hr, hr * B.u, hr * B.v, v.g, v.hdry, err)
-                   : hll(hl, hl * A.v, hl * A.u, hr, hr * B.v, hr * B.u, v.g, v.hdry, err);
+  // rotate to the face normal (x-normal: n = x; y-normal: n = y)
+  const double unA = xn ? A.u : A.v, utA = xn ? A.v : A.u;
+  const double unB = xn ? B.u : B.v, utB = xn ? B.v : B.u;
+  const Flx f = hll_inl(hl, hl * unA, hl * utA, hr, hr * unB, hr * utB, v.g, v.hdry, err);
   double* o = out + 6 * q;
   o[0] = f.m;
   o[1] = f.n;
@@ -154,6 +156,20 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock) k_stage(
   load9(in, kk, s);
   const P3 zc = load3(v.z, kk);
   const int kind = (v.sk[kk] >> (2 * sd)) & 3;
+  // issue the dependent gathers early: segment ids -> segment states, and
+  // (stage 2) the step-start state
+  const int nseg = kind == 0 ? 0 : kind == 3 ? 2 : 1;
+  double sg[2][6];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    if (t < nseg) {
+      const double* q = v.segst + 6 * (long long)v.sid[8 * kk + 2 * sd + t];
+#pragma unroll
+      for (int e = 0; e < 6; ++e) sg[t][e] = q[e];
+    }
+  }
+  double u0[9];
+  if (STAGE == 2) load9(uold, kk, u0);
   const bool xn = sd == 1 || sd == 3;
   const bool mine_left = sd == 0 || sd == 1;
   {
@@ -166,17 +182,7 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock) k_stage(
     // the side's segments (segment_states, solver_nonuniform.cpp:91-115,
     // computed once per segment by k_seg); the weight len/sz is exactly 1/2
     // for two finer neighbours and 1 otherwise (sizes are R * 2^k).
-    const int nseg = kind == 0 ? 0 : kind == 3 ? 2 : 1;
     const double w = kind == 3 ? 0.5 : 1.0;
-    double sg[2][6];
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      if (t < nseg) {
-        const double* q = v.segst + 6 * (long long)v.sid[8 * kk + 2 * sd + t];
-#pragma unroll
-        for (int e = 0; e < 6; ++e) sg[t][e] = q[e];
-      }
-    }
     double zstar;
     if (kind == 0) {
       zstar = me.z;
@@ -276,8 +282,6 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock) k_stage(
 #pragma unroll
     for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
   } else {
-    double u0[9];
-    load9(uold, kk, u0);
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
       double a = s[q];
@@ -288,22 +292,63 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock) k_stage(
     }
   }
   positivity(res, v.hdry);
-  if (last && !manual && valid) {
+  const bool epi = last && !manual;
+  if (!epi) {
+    if (valid) {
+      double* o = out + 9 * kk;
+      // lane sd stores components sd, sd + 4, sd + 8 (coalesced over the warp)
+      o[sd] = res[sd];
+      o[sd + 4] = res[sd + 4];
+      if (sd == 0) o[8] = res[8];
+    }
+    return;
+  }
+  // ---- fused epilogue: inflows, finite guard, next-step CFL ------------------
+  // Lanes store and check their own components; h.c0 (which the inflows
+  // modify) and the CFL of all 32 leaves are then handled by warp 0 alone, so
+  // the divisions and the reduction run once per leaf instead of on 4 lanes.
+  __shared__ double ep[kLeavesPerBlock][4];
+  if (valid) {
+    double* o = out + 9 * kk;
+    if (sd) o[sd] = res[sd];
+    o[sd + 4] = res[sd + 4];
+    if (sd == 0) o[8] = res[8];
+    const bool fin = (sd == 0 || isfinite(res[sd])) && isfinite(res[sd + 4]) &&
+                     (sd != 0 || isfinite(res[8]));
+    if (!fin) atomicMin(&red[c->steps & 1].badkey, leaf_key(l, i, j));
+  }
+  if (sd == 0) {
+    ep[lq][0] = res[0];
+    ep[lq][1] = res[3];
+    ep[lq][2] = res[6];
+    ep[lq][3] = sz;
+  }
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int e = threadIdx.x;
+  const long long ke = blockIdx.x * (long long)kLeavesPerBlock + e;
+  double dtc = INFINITY;
+  if (ke < v.n) {
+    double h = ep[e][0];
+    const double sze = ep[e][3];
     // apply_inflows (solver_nonuniform.cpp:451-465), inflow order
     for (int f = 0; f < v.ninflow; ++f) {
       if (!c->on[f]) continue;
-      const int cnt = v.infc[f * v.n + kk];
-      if (cnt) res[0] += ddiv(c->per_cell[f] * cnt, sz * sz);
+      const int cnt = v.infc[f * v.n + ke];
+      if (cnt) h += ddiv(c->per_cell[f] * cnt, sze * sze);
+    }
+    out[9 * ke] = h;
+    if (!isfinite(h)) atomicMin(&red[c->steps & 1].badkey, leaf_key(v.lvl[ke], v.li[ke], v.lj[ke]));
+    // compute_dt (solver_nonuniform.cpp:427-449) candidate of this leaf
+    if (h > v.hdry) {
+      const double cw = sqrt(v.g * h);
+      const double sx = fabs(zdiv(ep[e][1], h)) + cw;
+      const double sy = fabs(zdiv(ep[e][2], h)) + cw;
+      dtc = ddiv(sze, smax(sx, sy));
     }
   }
-  if (valid) {
-    double* o = out + 9 * kk;
-    // lane sd stores components sd, sd + 4, sd + 8 (coalesced over the warp)
-    o[sd] = res[sd];
-    o[sd + 4] = res[sd + 4];
-    if (sd == 0) o[8] = res[8];
-  }
-  if (last && !manual) reduce_leaf(v, red, *c, res, sz, leaf_key(l, i, j), valid && sd == 0);
+  for (int o = 16; o; o >>= 1) dtc = smin(dtc, __shfl_xor_sync(0xffffffffu, dtc, o));
+  if (e == 0 && dtc < INFINITY) atomicMin(&red[c->steps & 1].dtmin, dbits(dtc));
 }
 
 // ---- ACC ------------------------------------------------------------------
