@@ -48,6 +48,9 @@ struct NuView {
   double R, x0, y0, g, hdry, courant;
   int bc[4];
   long long n;
+  // per level: element size R * 2^(L-l) and its reciprocal (host-computed,
+  // the same IEEE values as the device expressions they replace)
+  double lsz[16], linv[16];
   const int8_t* lvl;
   const int32_t* li;
   const int32_t* lj;

@@ -27,6 +27,18 @@
 #include "fm_sim.hpp"
 #include "step_common.cuh"
 
+// minimum resident CTAs per SM (register caps; tuned on B200 with
+// scripts/ab_profile.py)
+#ifndef FM_STAGE1_MINB
+#define FM_STAGE1_MINB 8
+#endif
+#ifndef FM_STAGE2_MINB
+#define FM_STAGE2_MINB 8
+#endif
+#ifndef FM_SEG_MINB
+#define FM_SEG_MINB 1
+#endif
+
 using namespace fmd;
 
 namespace fmh {
@@ -59,7 +71,7 @@ __global__ void __launch_bounds__(256) k_head_friction(NuView v, DevClock* clk, 
 // runs the same code path (one HLL), unlike a per-leaf-side formulation where
 // lanes of a warp face 0, 1 or 2 sub-faces and every face is solved twice.
 template <bool P2>
-__global__ void __launch_bounds__(256) k_seg(NuView v, const DevClock* __restrict__ clk,
+__global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClock* __restrict__ clk,
                                              const double* __restrict__ in, double* __restrict__ out,
                                              int manual, int* err) {
   const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -135,7 +147,7 @@ struct SideOut {
 };
 
 template <int STAGE, bool P2>
-__global__ void __launch_bounds__(4 * kLeavesPerBlock) k_stage(
+__global__ void __launch_bounds__(4 * kLeavesPerBlock, STAGE == 2 ? FM_STAGE2_MINB : FM_STAGE1_MINB) k_stage(
     NuView v, const DevClock* __restrict__ clk, DevRed* red, const double* __restrict__ in,
     const double* uold, double* out, int last, int manual, double mdt, int* err) {
   __shared__ SideOut so[kLeavesPerBlock][4];
@@ -150,7 +162,7 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock) k_stage(
   const long long kk = valid ? k : v.n - 1;  // keep the quad's loads in bounds
   const int l = v.lvl[kk], i = v.li[kk], j = v.lj[kk];
   const double sz = lsize(v, l);
-  const double inv = 1.0 / sz;
+  const double inv = v.linv[l];
   const double cx = P2 ? 0.0 : lcen(v.x0, v, l, i), cy = P2 ? 0.0 : lcen(v.y0, v, l, j);
   double s[9];
   load9(in, kk, s);

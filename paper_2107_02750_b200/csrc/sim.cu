@@ -130,6 +130,10 @@ NuView Sim::view() const {
   v.hdry = hdry;
   v.courant = courant;
   for (int q = 0; q < 4; ++q) v.bc[q] = bc[q];
+  for (int l = 0; l <= L && l < 16; ++l) {
+    v.lsz[l] = R * double(1 << (L - l));
+    v.linv[l] = 1.0 / v.lsz[l];
+  }
   v.n = n;
   v.lvl = lvl.p;
   v.li = li.p;

@@ -16,7 +16,7 @@ struct Pt {
   double h, qx, qy, z, eta, u, v;
 };
 
-__device__ __forceinline__ double lsize(const NuView& v, int l) { return v.R * double(1 << (v.L - l)); }
+__device__ __forceinline__ double lsize(const NuView& v, int l) { return v.lsz[l]; }
 __device__ __forceinline__ double lcen(double o, const NuView& v, int l, int i) {
   return o + (i + 0.5) * v.R * double(1 << (v.L - l));
 }
