@@ -6,8 +6,9 @@ scaling targets are quoted on): multiwavelet MRA (L = 13, eps = 1e-3) of the
 seeded synthetic DEM, then static non-uniform DG2 RK2 steps under the 50 mm/h
 rain on the resulting ~2.3 M leaves.  A "step" is one RK2 step of every leaf
 (cell-updates/s = leaves x steps / time).  Synthetic inputs (DESIGN.md
-§"Synthetic inputs"); state ~0.6 GB per GPU > the 126 MB L2, so no flush is
-needed between steps.
+§6); state ~0.7 GB > the 126 MB L2, so no flush is needed between steps.
+With N GPUs (torchrun) the same domain is split into N Morton-range shards
+with NCCL halo exchanges (strong scaling: total work fixed).
 
 Legs:
   value    device loop (CUDA graph) with the DEM resident in HBM, CUDA-event time
@@ -174,7 +175,7 @@ def run_reference(args, ws, rank):
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": n_done, "warmup": args.warmup,
             "ms_per_step": 1000.0 * secs / max(n_done, 1), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "c4_static_nonuniform_dg2 (bounded CPU sample)",
                        "sample": cb["sample"]},
             "cpu_baseline": cb,
@@ -198,8 +199,23 @@ def run_ours(args, ws, rank, local):
     grid = lib.grid(sc.dem, sc.L, sc.eps, device_ptr=dem_d.data_ptr())
     mra_ms, mra_bytes = grid.timing()
     n_int = (4 ** sc.L - 1) // 3
-    sim = lib.sim(sc, grid)
+    # N > 1: the same domain split into N Morton-range shards,
+    # halo exchanges and the dt reduction over NCCL inside each step's graph
+    comm = None
+    if ws > 1:
+        import torch.distributed as dist
+        uid = [lib.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = lib.comm_nccl(ws, rank, uid[0])
+    elif args.force_shard:  # the sharded path on one GPU (a 1-rank NCCL communicator)
+        comm = lib.comm_nccl(1, 0, lib.comm_unique_id())
+
+    def make_sim(g):
+        return lib.shard_sim(sc, g, comm, rank) if comm is not None else lib.sim(sc, g)
+
+    sim = make_sim(grid)
     n_leaves, n_seg = sim.num_cells, sim.num_segments
+    n_global = sim.shard_info()["n_global"] if comm is not None else n_leaves
     ck, r = sim.run(args.warmup, gauge_interval=10.0)
     # The reference DG2 scheme diverges under this forcing after ~130 steps (thin
     # rain films on 10 m building walls; DESIGN.md §"Config 4 dynamics"), so the
@@ -256,7 +272,7 @@ def run_ours(args, ws, rank, local):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     g2 = lib.grid(sc.dem, sc.L, sc.eps)
-    s2 = lib.sim(sc, g2)
+    s2 = make_sim(g2)
     ck2, r2 = s2.run(args.warmup, gauge_interval=10.0)
     s2.snapshot()
     ck0 = (ck2.end_time, ck2.output_interval, ck2.gauge_interval, ck2.now, ck2.next_output,
@@ -275,6 +291,7 @@ def run_ours(args, ws, rank, local):
     e2e_steps = args.warmup + args.steps
     e2e_value = allreduce_sum(float(n_leaves) * e2e_steps, ws) / e2e_s
     del s2, g2
+    comm = None
 
     if rank != 0:
         return
@@ -284,10 +301,12 @@ def run_ours(args, ws, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "c4_static_nonuniform_dg2", "cells": f"{8192 // args.scale}^2",
-                   "L": sc.L, "eps": sc.eps, "leaves": n_leaves, "segments": n_seg,
-                   "parallelism": "replicas" if ws > 1 else "single",
+                   "L": sc.L, "eps": sc.eps, "leaves": n_global, "segments_rank0": n_seg,
+                   "leaves_rank0": n_leaves,
+                   "parallelism": f"morton-shards x{ws} (NCCL halo + min-allreduce)" if ws > 1
+                   else "single",
                    "l2": "state > 126 MB L2 (no flush needed)",
                    "solver": "static non-uniform DG2 RK2, rain 50 mm/h, Manning street raster"},
         "roofline": {"bound": "hbm", "kernel": "k_stage<2>", "achieved": achieved, "peak": hbm,
@@ -303,7 +322,7 @@ def run_ours(args, ws, rank, local):
                 "frac": mra_bytes / (mra_ms / 1000.0) / 1e9 / hbm},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
                 "d2h_bytes_per_step": d2h / e2e_steps, "seconds": e2e_s,
-                "what": "host DEM -> fm_mra_static -> fm_sim_create -> W+K steps -> host state"},
+                "what": "host DEM -> fm_mra_static -> fm_sim_create(_shard) -> W+K steps -> host state"},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
@@ -323,6 +342,8 @@ def main():
     p.add_argument("--cpu-steps", type=int, default=40)
     p.add_argument("--cpu-steps-cap", type=int, default=20)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--force-shard", action="store_true",
+                   help="N=1: run the sharded (NCCL) code path with a single rank")
     args = p.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_setup() if args.impl == "ours" else (

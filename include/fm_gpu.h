@@ -233,6 +233,45 @@ int fm_sim_profile(fm_sim* s, int64_t steps, double* ms, int64_t* launches, int3
                    int32_t* n);
 const char* fm_sim_kernel_name(fm_sim* s, int32_t family);
 
+/* ---- multi-GPU: Morton-range shards of a static non-uniform sim ----------
+ * (the reference is single-process.)  Rank r of R owns the
+ * contiguous range [floor(n r / R), floor(n (r+1) / R)) of the Morton-ordered
+ * leaves plus a halo of remote neighbours; per DG2 step two halo exchanges
+ * and one min-allreduce, so every shard's state equals the unsharded sim's
+ * bit for bit.  Adaptive and uniform sims do not shard (replicas). */
+typedef struct fm_comm fm_comm;
+/* NCCL transport, one process per GPU: rank 0 makes the id, the host
+ * broadcasts it, every rank creates its communicator. */
+int fm_comm_unique_id(uint8_t id[128]);
+int fm_comm_create_nccl(int32_t nranks, int32_t rank, const uint8_t id[128], fm_comm** out);
+/* Local group: all ranks as shards in this process on this device, stepped
+ * together by fm_group_run (single-GPU check of the partition logic). */
+int fm_comm_create_local(int32_t nranks, fm_comm** out);
+int fm_comm_destroy(fm_comm* c);
+/* make_nonuniform_sim (solver_nonuniform.cpp:558-636) restricted to this
+ * rank's shard.  fm_sim_run / step / compute_dt / finite / volume on an NCCL
+ * shard are collective over the ranks; download / rasters return the shard's
+ * own leaves. */
+int fm_sim_create_shard(const fm_sim_desc* desc, const fm_raster* dem, const fm_grid* grid,
+                        fm_comm* comm, int32_t rank, fm_sim** out);
+int fm_sim_shard_info(const fm_sim* s, int32_t* rank, int32_t* nranks, int64_t* first,
+                      int64_t* owned, int64_t* halo, int64_t* n_global);
+/* The drive loop (run.cpp:80-111) over all shards of a local group. */
+int fm_group_run(fm_sim* const* sims, int32_t n, fm_clock* clk, int64_t max_steps,
+                 int32_t stop_at_events, fm_run_result* out);
+/* The partition plan on the host (no device needed): owned range, local
+ * segment count, halo (ascending global ids, their owner ranks) and the
+ * owned leaves each rank needs (send_counts[nranks], concatenated ascending
+ * lists in `send`).  Call with halo = send = NULL for the sizes. */
+int fm_shard_plan(int64_t n_leaves, int64_t n_segments, const int32_t* seg_l,
+                  const int32_t* seg_r, int32_t nranks, int32_t rank, int64_t* first,
+                  int64_t* count, int64_t* n_local_segments, int64_t* n_halo, int64_t* halo,
+                  int32_t* halo_owner, int64_t* send_counts, int64_t* send);
+/* A sim's leaves and interior segments in device (Morton) order:
+ * level/i/j per leaf (n), seg_l/seg_r per segment (W/S leaf, E/N leaf). */
+int fm_sim_topology(fm_sim* s, int32_t* level, int32_t* i, int32_t* j, int32_t* seg_l,
+                    int32_t* seg_r);
+
 #ifdef __cplusplus
 }
 #endif

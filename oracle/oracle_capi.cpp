@@ -329,6 +329,24 @@ int orc_sim_sample_gauges(orc_sim* s, int32_t n, const double* x, const double* 
   });
 }
 
+// Leaves (reference order) and interior segments (enumerate_faces order,
+// quadgrid.cpp:184-260) of a non-uniform sim: the topology the shard plan of
+// the GPU library partitions.
+int orc_sim_topology(orc_sim* s, int32_t* lv, int32_t* ii, int32_t* jj, int32_t* sl, int32_t* sr) {
+  return guard([&] {
+    NU* n = s->nu();
+    if (!n) throw Fail(E_CONFIG, "topology: uniform sims have no leaf list");
+    for (size_t k = 0; k < n->grid.lv.size(); ++k) {
+      if (lv) lv[k] = n->grid.lv[k].l;
+      if (ii) ii[k] = n->grid.lv[k].i;
+      if (jj) jj[k] = n->grid.lv[k].j;
+    }
+    for (size_t q = 0; q < n->F.in.size(); ++q) {
+      if (sl) sl[q] = n->F.in[q].l;
+      if (sr) sr[q] = n->F.in[q].r;
+    }
+  });
+}
 int orc_sim_upload(orc_sim* s, const double* u9) {
   return guard([&] {
     auto& u = s->un() ? s->un()->u : s->nu()->u;

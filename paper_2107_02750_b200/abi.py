@@ -130,6 +130,17 @@ OPTIONAL = {
     "encode": (None, [PD, I32, PD, PD]),
     "decode": (None, [PD, PD, I32, PD]),
     "bank": (None, [I32, PD]),
+    # sharding (libfm_gpu.so) and topology (both)
+    "comm_unique_id": (C.c_int, [C.c_char_p]),
+    "comm_create_nccl": (C.c_int, [I32, I32, C.c_char_p, PP]),
+    "comm_create_local": (C.c_int, [I32, PP]),
+    "comm_destroy": (C.c_int, [P]),
+    "sim_create_shard": (C.c_int, [C.POINTER(c_desc), C.POINTER(c_raster), P, P, I32, PP]),
+    "sim_shard_info": (C.c_int, [P, PI32, PI32, PI64, PI64, PI64, PI64]),
+    "group_run": (C.c_int, [C.POINTER(P), I32, C.POINTER(c_clock), I64, I32, C.POINTER(c_result)]),
+    "shard_plan": (C.c_int, [I64, I64, PI32, PI32, I32, I32, PI64, PI64, PI64, PI64, PI64, PI32,
+                             PI64, PI64]),
+    "sim_topology": (C.c_int, [P, PI32, PI32, PI32, PI32, PI32]),
 }
 
 
@@ -178,6 +189,70 @@ class Backend:
 
     def sim(self, scenario, grid=None, libm: int = 0):
         return Sim(self, scenario, grid, libm)
+
+    # ---- sharding ----
+    def comm_local(self, nranks: int) -> "Comm":
+        h = P()
+        self.call("comm_create_local", int(nranks), C.byref(h))
+        return Comm(self, h, nranks, None)
+
+    def comm_unique_id(self) -> bytes:
+        buf = C.create_string_buffer(128)
+        self.call("comm_unique_id", buf)
+        return buf.raw
+
+    def comm_nccl(self, nranks: int, rank: int, uid: bytes) -> "Comm":
+        h = P()
+        self.call("comm_create_nccl", int(nranks), int(rank), C.c_char_p(bytes(uid)), C.byref(h))
+        return Comm(self, h, nranks, rank)
+
+    def shard_sim(self, scenario, grid, comm: "Comm", rank: int, libm: int = 0):
+        return Sim(self, scenario, grid, libm, comm=comm, rank=rank)
+
+    def group_run(self, sims, steps: int, end_time: float = 1e12, gauge_interval: float = 0.0,
+                  output_interval: float = 0.0, stop_at_events: bool = False):
+        """fm_group_run: the drive loop over every shard of a local group."""
+        arr = (P * len(sims))(*[s.h for s in sims])
+        clock = c_clock(end_time, output_interval, gauge_interval, 0.0, 1, 1)
+        res = c_result()
+        st = self.fn["group_run"](arr, len(sims), C.byref(clock), steps, 1 if stop_at_events else 0,
+                                  C.byref(res))
+        self.check(st, res)
+        return clock, res
+
+    def shard_plan(self, n: int, seg_l: np.ndarray, seg_r: np.ndarray, nranks: int, rank: int):
+        """fm_shard_plan (host only): dict with first, count, nseg_local, halo,
+        halo_owner and send (list per rank of ascending global leaf ids)."""
+        sl = np.ascontiguousarray(seg_l, np.int32)
+        sr = np.ascontiguousarray(seg_r, np.int32)
+        first, count, nsl, nh = I64(), I64(), I64(), I64()
+        cnt = np.zeros(nranks, np.int64)
+        P64 = C.POINTER(C.c_int64)
+        self.call("shard_plan", n, len(sl), sl.ctypes.data_as(PI32), sr.ctypes.data_as(PI32), nranks,
+                  rank, C.byref(first), C.byref(count), C.byref(nsl), C.byref(nh), None, None,
+                  cnt.ctypes.data_as(P64), None)
+        halo = np.zeros(nh.value, np.int64)
+        owner = np.zeros(nh.value, np.int32)
+        send = np.zeros(int(cnt.sum()), np.int64)
+        self.call("shard_plan", n, len(sl), sl.ctypes.data_as(PI32), sr.ctypes.data_as(PI32), nranks,
+                  rank, C.byref(first), C.byref(count), C.byref(nsl), C.byref(nh),
+                  halo.ctypes.data_as(P64), owner.ctypes.data_as(PI32), cnt.ctypes.data_as(P64),
+                  send.ctypes.data_as(P64))
+        off = np.concatenate([[0], np.cumsum(cnt)])
+        return dict(first=first.value, count=count.value, nseg_local=nsl.value, halo=halo,
+                    halo_owner=owner, send=[send[off[r]:off[r + 1]] for r in range(nranks)])
+
+
+class Comm:
+    """fm_comm: the transport between the shards of one partition."""
+
+    def __init__(self, be: Backend, h, nranks: int, rank):
+        self.be, self.h, self.nranks, self.rank = be, h, nranks, rank
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.be.fn["comm_destroy"](self.h)
+            self.h = None
 
 
 def make_raster(r, keep: list) -> c_raster:
@@ -257,7 +332,8 @@ class Grid:
 class Sim:
     """A drive<Sim>-shaped simulation (run.cpp:35-141) behind the ABI."""
 
-    def __init__(self, be: Backend, sc, grid: Grid | None = None, libm: int = 0):
+    def __init__(self, be: Backend, sc, grid: Grid | None = None, libm: int = 0,
+                 comm: "Comm | None" = None, rank: int = 0):
         from .scenarios import SOLVERS
 
         self.be = be
@@ -298,8 +374,13 @@ class Sim:
         d.libm = libm
         dem = make_raster(sc.dem, keep)
         h = P()
-        be.call("sim_create", C.byref(d), C.byref(dem), grid.h if grid is not None else None,
-                C.byref(h))
+        if comm is not None:
+            be.call("sim_create_shard", C.byref(d), C.byref(dem),
+                    grid.h if grid is not None else None, comm.h, int(rank), C.byref(h))
+        else:
+            be.call("sim_create", C.byref(d), C.byref(dem), grid.h if grid is not None else None,
+                    C.byref(h))
+        self.comm = comm
         self.h = h
         self.grid = grid
         self.scenario = sc
@@ -357,6 +438,24 @@ class Sim:
     def upload(self, u9: np.ndarray):
         u9 = np.ascontiguousarray(u9, np.float64)
         self.be.call("sim_upload", self.h, dptr(u9))
+
+    def shard_info(self) -> dict:
+        r, nr = I32(), I32()
+        first, owned, halo, ng = I64(), I64(), I64(), I64()
+        self.be.call("sim_shard_info", self.h, C.byref(r), C.byref(nr), C.byref(first),
+                     C.byref(owned), C.byref(halo), C.byref(ng))
+        return dict(rank=r.value, nranks=nr.value, first=first.value, owned=owned.value,
+                    halo=halo.value, n_global=ng.value)
+
+    def topology(self):
+        """(level, i, j) per leaf and (seg_l, seg_r) per interior segment; device
+        order for the GPU library, reference order for the oracle."""
+        n, ns = self.num_cells, self.num_segments
+        lv, i, j = (np.zeros(n, np.int32) for _ in range(3))
+        sl, sr = np.zeros(ns, np.int32), np.zeros(ns, np.int32)
+        self.be.call("sim_topology", self.h, lv.ctypes.data_as(PI32), i.ctypes.data_as(PI32),
+                     j.ctypes.data_as(PI32), sl.ctypes.data_as(PI32), sr.ctypes.data_as(PI32))
+        return lv, i, j, sl, sr
 
     def raster_shape(self) -> dict:
         nc, nr = I32(), I32()

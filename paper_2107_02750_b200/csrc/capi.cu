@@ -111,6 +111,10 @@ struct fm_grid {
 struct fm_sim {
   std::unique_ptr<Sim> s;
 };
+struct fm_comm {
+  Comm* c = nullptr;
+  ~fm_comm() { comm_destroy(c); }
+};
 
 extern "C" {
 
@@ -314,6 +318,99 @@ int fm_sim_raster(fm_sim* s, int32_t which, double* out, int32_t on_device) {
 }
 int fm_sim_sample_gauges(fm_sim* s, int32_t n, const double* x, const double* y, double* out4) {
   return guard([&] { sim_sample_gauges(*s->s, n, x, y, out4); });
+}
+int fm_comm_unique_id(uint8_t id[128]) {
+  return guard([&] { comm_unique_id(id); });
+}
+int fm_comm_create_nccl(int32_t nranks, int32_t rank, const uint8_t id[128], fm_comm** out) {
+  return guard([&] {
+    require_device();
+    auto h = std::make_unique<fm_comm>();
+    h->c = comm_create_nccl(nranks, rank, id);
+    *out = h.release();
+  });
+}
+int fm_comm_create_local(int32_t nranks, fm_comm** out) {
+  return guard([&] {
+    auto h = std::make_unique<fm_comm>();
+    h->c = comm_create_local(nranks);
+    *out = h.release();
+  });
+}
+int fm_comm_destroy(fm_comm* c) {
+  return guard([&] { delete c; });
+}
+int fm_sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const fm_grid* grid, fm_comm* comm,
+                        int32_t rank, fm_sim** out) {
+  return guard([&] {
+    require_device();
+    if (!comm) throw Error(FM_ERR_CONFIG, "shard: null communicator");
+    auto h = std::make_unique<fm_sim>();
+    h->s.reset(sim_create_shard(d, dem, grid ? grid->g.get() : nullptr, comm->c, rank));
+    *out = h.release();
+  });
+}
+int fm_sim_shard_info(const fm_sim* s, int32_t* rank, int32_t* nranks, int64_t* first, int64_t* owned,
+                      int64_t* halo, int64_t* n_global) {
+  return guard([&] {
+    const Sim& m = *s->s;
+    const Shard* sh = m.shard.get();
+    if (rank) *rank = sh ? sh->rank : 0;
+    if (nranks) *nranks = sh ? sh->nranks : 1;
+    if (first) *first = sh ? sh->first : 0;
+    if (owned) *owned = m.n;
+    if (halo) *halo = sh ? sh->n_halo : 0;
+    if (n_global) *n_global = sh ? sh->n_global : m.n;
+  });
+}
+int fm_group_run(fm_sim* const* sims, int32_t n, fm_clock* clk, int64_t max_steps, int32_t stop_at_events,
+                 fm_run_result* out) {
+  fm_run_result r{};
+  const int st = guard([&] {
+    std::vector<Sim*> v;
+    for (int32_t k = 0; k < n; ++k) v.push_back(sims[k]->s.get());
+    group_run(v, clk, max_steps, stop_at_events, &r);
+  });
+  if (out) *out = r;
+  return st;
+}
+int fm_shard_plan(int64_t n_leaves, int64_t n_segments, const int32_t* seg_l, const int32_t* seg_r,
+                  int32_t nranks, int32_t rank, int64_t* first, int64_t* count, int64_t* n_local_segments,
+                  int64_t* n_halo, int64_t* halo, int32_t* halo_owner, int64_t* send_counts,
+                  int64_t* send) {
+  return guard([&] {
+    const ShardPlan p = shard_plan(n_leaves, n_segments, seg_l, seg_r, nranks, rank);
+    if (first) *first = p.first;
+    if (count) *count = p.count;
+    if (n_local_segments) *n_local_segments = int64_t(p.segs.size());
+    if (n_halo) *n_halo = int64_t(p.halo.size());
+    if (halo) std::copy(p.halo.begin(), p.halo.end(), halo);
+    if (halo_owner) std::copy(p.halo_owner.begin(), p.halo_owner.end(), halo_owner);
+    int64_t at = 0;
+    for (int r = 0; r < nranks; ++r) {
+      if (send_counts) send_counts[r] = int64_t(p.send[r].size());
+      if (send) std::copy(p.send[r].begin(), p.send[r].end(), send + at);
+      at += int64_t(p.send[r].size());
+    }
+  });
+}
+int fm_sim_topology(fm_sim* s, int32_t* level, int32_t* i, int32_t* j, int32_t* seg_l, int32_t* seg_r) {
+  return guard([&] {
+    Sim& m = *s->s;
+    if (m.uniform) throw Error(FM_ERR_CONFIG, "topology: uniform sims have no leaf list");
+    if (level) {
+      const std::vector<int8_t> l = m.lvl.to_host();
+      for (int64_t k = 0; k < m.n; ++k) level[k] = l[k];
+    }
+    if (i) m.li.download(i, m.n);
+    if (j) m.lj.download(j, m.n);
+    if (seg_l || seg_r) {
+      if (m.seg_l.n < size_t(m.nseg)) throw Error(FM_ERR_CONFIG, "topology: no segment list");
+      if (seg_l) m.seg_l.download(seg_l, m.nseg);
+      if (seg_r) m.seg_r.download(seg_r, m.nseg);
+    }
+    FM_CUDA(cudaStreamSynchronize(stream()));
+  });
 }
 int fm_sim_snapshot(fm_sim* s) {
   return guard([&] { sim_snapshot(*s->s); });

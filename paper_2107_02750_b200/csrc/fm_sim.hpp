@@ -30,7 +30,8 @@ struct DevClock {
 // Per-step reductions, double-buffered by step parity.
 struct DevRed {
   unsigned long long dtmin;   // DG2/FV1: min size/max(sx,sy); ACC: min wet size
-  unsigned long long hmax;    // ACC: max wet h
+  unsigned long long hmaxc;   // ACC: ~bits of the max wet h (min-reduced like the
+                              // other fields, so a slot reduces across ranks with one min)
   unsigned long long badkey;  // min (level<<58 | j<<29 | i) of non-finite cells
   unsigned long long pad;
 };
@@ -66,6 +67,26 @@ struct NuView {
   const int32_t* sid;   // 8 per leaf: segment ids of the sub-faces per side
   const double* segst;  // 6 per segment: HLL flux (m n t), z*, h*L, h*R
   long long nseg;
+};
+
+// Operations of one step (nu_step_ops in nu_flow.cu).
+enum StepOp { OP_HEAD, OP_EXCH_U, OP_STAGE1, OP_EXCH_US, OP_STAGE2, OP_ACC, OP_REDUCE, OP_COMMIT };
+
+struct Comm;  // shard.cu: the transport between the ranks of a sharded sim
+
+// A sim restricted to a contiguous Morton range of the global leaves plus a
+// halo of remote neighbours (shard.cu).  Local leaf arrays hold the `n` owned
+// leaves first, then the halo grouped by owner rank; segments are the global
+// segments with at least one owned leaf, in global order.
+struct Shard {
+  Comm* comm = nullptr;
+  int rank = 0, nranks = 1;
+  int64_t first = 0, n_global = 0, n_halo = 0;
+  std::vector<int> peers;                 // ranks exchanged with, ascending
+  std::vector<int64_t> soff, scnt;        // per peer: slice of send_idx / send_buf
+  std::vector<int64_t> hoff, hcnt;        // per peer: slice of the halo (local n + hoff)
+  DBuf<int32_t> send_idx;                 // local indices of the owned leaves sent
+  DBuf<double> send_buf;                  // 9 doubles per sent leaf
 };
 
 struct Sim {
@@ -121,6 +142,7 @@ struct Sim {
   cudaGraphExec_t graph = nullptr;
   int graph_steps = 0;
   int64_t graph_kernels = 0;
+  std::unique_ptr<Shard> shard;  // set for a sharded (multi-rank) static sim
   ~Sim();
 
   NuView view() const;
@@ -146,6 +168,33 @@ void sim_raster(Sim& s, int which, double* out, bool on_device);
 void sim_sample_gauges(Sim& s, int n, const double* x, const double* y, double* out4);
 void sim_restore(Sim& s);
 
+// step operations (nu_flow.cu) and the shard layer (shard.cu)
+std::vector<int> nu_step_ops(const Sim& s, bool manual);
+void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err);
+void shard_op(Sim& s, int op);  // exchange / reduce for a sharded sim (NCCL)
+struct ShardPlan {
+  int64_t first = 0, count = 0;
+  std::vector<int64_t> segs;              // global ids of the local segments, ascending
+  std::vector<int64_t> halo;              // global ids of the halo leaves, ascending
+  std::vector<int> halo_owner;            // owner rank of each halo leaf (ascending)
+  std::vector<std::vector<int64_t>> send; // per rank: owned global ids it needs, ascending
+};
+int64_t shard_first(int64_t n, int nranks, int r);
+ShardPlan shard_plan(int64_t n, int64_t nseg, const int32_t* seg_l, const int32_t* seg_r, int nranks,
+                     int rank);
+Comm* comm_create_local(int nranks);
+Comm* comm_create_nccl(int nranks, int rank, const uint8_t* id);
+void comm_unique_id(uint8_t* out);
+void comm_destroy(Comm* c);
+void comm_forget(Comm* c, Sim* s);
+Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* grid, Comm* comm, int rank);
+void shard_pack(Sim& s, const double* arr);
+void shard_local_recv(Sim& s, double* arr);
+void shard_local_reduce(const std::vector<Sim*>& sims);
+void shard_allreduce_u64_min(Sim& s, unsigned long long* dev, int count);
+double shard_allreduce_sum(Sim& s, double v);
+void group_run(const std::vector<Sim*>& sims, fm_clock* clk, int64_t max_steps, int stop_at_events,
+               fm_run_result* out);
 // topology (topo.cu)
 void build_topology(Sim& s, const Grid& g);
 void resolve_inflows(Sim& s, const Grid& g);

@@ -518,51 +518,79 @@ inline unsigned nblk(long long n, int t) { return unsigned((n + t - 1) / t); }
 }  // namespace
 
 // ---- launch helpers used by sim.cu --------------------------------------------
-void nu_launch_step(Sim& s, bool manual, double mdt, int* err) {
+// A step is a fixed sequence of operations (StepOp): device phases plus, for a
+// sharded sim, the halo exchanges of the state a phase is about to gather and
+// the cross-rank reduction of the next-step CFL / non-finite slot.
+//   DG2: HEAD  X(U)  STAGE1  X(U*)  STAGE2  REDUCE  COMMIT
+//   FV1: HEAD  X(U)  STAGE1  REDUCE  COMMIT
+//   ACC: X(U)  ACC  REDUCE  COMMIT
+// (manual host-API steps have no REDUCE / COMMIT).
+std::vector<int> nu_step_ops(const Sim& s, bool manual) {
+  std::vector<int> ops;
+  if (s.scheme == FM_ACC) {
+    ops = {OP_EXCH_U, OP_ACC};
+  } else if (s.scheme == FM_FV1) {
+    ops = {OP_HEAD, OP_EXCH_U, OP_STAGE1};
+  } else {
+    ops = {OP_HEAD, OP_EXCH_U, OP_STAGE1, OP_EXCH_US, OP_STAGE2};
+  }
+  if (!manual) {
+    ops.push_back(OP_REDUCE);
+    ops.push_back(OP_COMMIT);
+  }
+  return ops;
+}
+
+// The device phases of a step (exchange / reduce ops are the shard layer's).
+void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
   cudaStream_t st = stream();
   const NuView v = s.view();
   DevClock* clk = s.clk.p;
   DevRed* red = s.red.p;
   const long long n = s.n;
-  if (s.scheme == FM_ACC) {
-    const long long ns = std::max<long long>(s.nseg, 1);
-    kt_begin(KF_ACC_FACES);
-    k_acc_faces<<<nblk(ns, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.u.p, s.accq.p, manual, mdt);
+  const long long ns = std::max<long long>(s.nseg, 1);
+  const bool fv1 = s.scheme == FM_FV1;
+  auto seg = [&](int fam, const double* in) {
+    kt_begin(fam);
+    if (s.p2)
+      k_seg<true><<<nblk(ns, 256), 256, 0, st>>>(v, clk, in, s.segst.p, manual, err);
+    else
+      k_seg<false><<<nblk(ns, 256), 256, 0, st>>>(v, clk, in, s.segst.p, manual, err);
     FM_LAUNCHED();
     kt_end();
-    kt_begin(KF_ACC_LEAVES);
-    k_acc_leaves<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.u.p, s.accq.p, s.accqb.p, manual, mdt);
-    FM_LAUNCHED();
-    kt_end();
-  } else {
-    // DG2: head, (segments, leaves) x 2.  FV1 keeps its state in U* between
-    // steps; its head moves it to U with friction and stage 1 is the update.
-    const bool fv1 = s.scheme == FM_FV1;
-    const long long ns = std::max<long long>(s.nseg, 1);
-    auto seg = [&](int fam, const double* in) {
-      kt_begin(fam);
-      if (s.p2)
-        k_seg<true><<<nblk(ns, 256), 256, 0, st>>>(v, clk, in, s.segst.p, manual, err);
-      else
-        k_seg<false><<<nblk(ns, 256), 256, 0, st>>>(v, clk, in, s.segst.p, manual, err);
+  };
+  switch (op) {
+    case OP_ACC:
+      kt_begin(KF_ACC_FACES);
+      k_acc_faces<<<nblk(ns, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.u.p, s.accq.p, manual, mdt);
       FM_LAUNCHED();
       kt_end();
-    };
-    kt_begin(KF_HEAD);
-    k_head_friction<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, fv1 ? s.us.p : s.u.p, s.u.p,
-                                                  manual, mdt);
-    FM_LAUNCHED();
-    kt_end();
-    seg(KF_SEG1, s.u.p);
-    kt_begin(KF_STAGE1);
-    const int last1 = fv1 ? 1 : 0;
-    if (s.p2)
-      k_stage<1, true><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, last1, manual, mdt, err);
-    else
-      k_stage<1, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, last1, manual, mdt, err);
-    FM_LAUNCHED();
-    kt_end();
-    if (!fv1) {
+      kt_begin(KF_ACC_LEAVES);
+      k_acc_leaves<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.u.p, s.accq.p, s.accqb.p, manual, mdt);
+      FM_LAUNCHED();
+      kt_end();
+      break;
+    case OP_HEAD:
+      // FV1 keeps its state in U* between steps; the head moves it to U with friction
+      kt_begin(KF_HEAD);
+      k_head_friction<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, fv1 ? s.us.p : s.u.p, s.u.p,
+                                                    manual, mdt);
+      FM_LAUNCHED();
+      kt_end();
+      break;
+    case OP_STAGE1: {
+      seg(KF_SEG1, s.u.p);
+      kt_begin(KF_STAGE1);
+      const int last1 = fv1 ? 1 : 0;
+      if (s.p2)
+        k_stage<1, true><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, last1, manual, mdt, err);
+      else
+        k_stage<1, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, last1, manual, mdt, err);
+      FM_LAUNCHED();
+      kt_end();
+      break;
+    }
+    case OP_STAGE2:
       seg(KF_SEG2, s.us.p);
       kt_begin(KF_STAGE2);
       if (s.p2)
@@ -571,13 +599,25 @@ void nu_launch_step(Sim& s, bool manual, double mdt, int* err) {
         k_stage<2, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
       FM_LAUNCHED();
       kt_end();
-    }
+      break;
+    case OP_COMMIT:
+      kt_begin(KF_COMMIT);
+      k_commit<<<1, 1, 0, st>>>(clk);
+      FM_LAUNCHED();
+      kt_end();
+      break;
+    default:
+      break;
   }
-  if (!manual) {
-    kt_begin(KF_COMMIT);
-    k_commit<<<1, 1, 0, st>>>(clk);
-    FM_LAUNCHED();
-    kt_end();
+}
+
+void nu_launch_step(Sim& s, bool manual, double mdt, int* err) {
+  for (int op : nu_step_ops(s, manual)) {
+    if (op == OP_EXCH_U || op == OP_EXCH_US || op == OP_REDUCE) {
+      if (s.shard) shard_op(s, op);
+    } else {
+      nu_step_op(s, op, manual, mdt, err);
+    }
   }
 }
 

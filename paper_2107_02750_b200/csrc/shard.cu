@@ -1,0 +1,453 @@
+// Multi-rank sharding of static non-uniform sims.
+//
+// Partition: the leaves are stored in Morton order of their SW fine corner, so
+// rank r owns the contiguous range [floor(n r / R), floor(n (r+1) / R)) — a
+// space-filling-curve partition with compact pieces.  A rank keeps every
+// global segment with at least one owned leaf; the remote leaves of those
+// segments are its halo.  A cut segment is evaluated by both ranks from
+// identical inputs (its two leaves' states), so both see the same bits and no
+// flux is communicated.
+//
+// Per DG2 step: two halo exchanges (the state each RK stage gathers: U after
+// the friction head, U* after stage 1), 72 B per halo leaf, as one grouped
+// ncclSend / ncclRecv per peer that lands directly in the halo slots; then one
+// ncclAllReduce(min) over the 64 B reduction slots (the CFL minimum, the
+// complemented ACC depth maximum and the first non-finite key are all mins,
+// and min is exact, so dt is bit-identical for any rank count).  FV1 needs one
+// exchange, ACC one (h at the step start).  Everything is enqueued on the
+// library stream, so a whole step — NCCL calls included — is captured in the
+// sim's CUDA graph.
+//
+// Transports: NCCL (one process per GPU; libnccl is loaded at run time, the
+// copy already in the process when there is one, e.g. torch's), or a local
+// group (all ranks as shards of one process on one device, driven phase by
+// phase by fm_group_run) — the single-GPU harness that checks the partition,
+// halo and reduction logic bit-for-bit against the unsharded sim.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "fm_device.cuh"
+#include "fm_sim.hpp"
+
+namespace fmh {
+
+// ---- the transport ------------------------------------------------------------
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*ErrorString)(ncclResult_t) = nullptr;
+};
+
+static const NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) {
+    if (!api.h) throw Error(FM_ERR_CONFIG, "NCCL is not available (libnccl.so.2 not found)");
+    return api;
+  }
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // already in the process
+  if (!h) {
+    if (const char* p = std::getenv("FM_NCCL_LIB")) h = dlopen(p, RTLD_NOW | RTLD_LOCAL);
+  }
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+  if (!h) throw Error(FM_ERR_CONFIG, "NCCL is not available (libnccl.so.2 not found)");
+  auto sym = [&](const char* n) {
+    void* f = dlsym(h, n);
+    if (!f) throw Error(FM_ERR_CONFIG, std::string("NCCL symbol missing: ") + n);
+    return f;
+  };
+  api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+  api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+  api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+  api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+  api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+  api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+  api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+  api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+  api.ErrorString = reinterpret_cast<decltype(api.ErrorString)>(sym("ncclGetErrorString"));
+  api.h = h;
+  return api;
+}
+
+static void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw Error(FM_ERR_CUDA, std::string("[nccl] ") + what + ": " + nccl().ErrorString(r));
+}
+
+enum CommKind { COMM_LOCAL = 0, COMM_NCCL = 1 };
+
+struct Comm {
+  int kind = COMM_LOCAL;
+  int nranks = 1, rank = 0;
+  ncclComm_t nc = nullptr;
+  std::vector<Sim*> members;  // local group: the shard sim of each rank (or null)
+};
+
+Comm* comm_create_local(int nranks) {
+  if (nranks < 1) throw Error(FM_ERR_CONFIG, "comm: nranks must be >= 1");
+  auto c = std::make_unique<Comm>();
+  c->kind = COMM_LOCAL;
+  c->nranks = nranks;
+  c->members.assign(nranks, nullptr);
+  return c.release();
+}
+
+void comm_unique_id(uint8_t* out) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(out, &id, sizeof(id));
+}
+
+Comm* comm_create_nccl(int nranks, int rank, const uint8_t* id) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(FM_ERR_CONFIG, "comm: bad rank / size");
+  auto c = std::make_unique<Comm>();
+  c->kind = COMM_NCCL;
+  c->nranks = nranks;
+  c->rank = rank;
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  nccl_check(nccl().CommInitRank(&c->nc, nranks, u, rank), "ncclCommInitRank");
+  return c.release();
+}
+
+void comm_destroy(Comm* c) {
+  if (!c) return;
+  if (c->kind == COMM_NCCL && c->nc) nccl().CommDestroy(c->nc);
+  for (Sim* s : c->members)
+    if (s && s->shard) s->shard->comm = nullptr;
+  delete c;
+}
+
+void comm_forget(Comm* c, Sim* s) {
+  if (!c) return;
+  for (auto& m : c->members)
+    if (m == s) m = nullptr;
+}
+
+// ---- the partition plan (host) --------------------------------------------------
+
+int64_t shard_first(int64_t n, int nranks, int r) {
+  return int64_t((static_cast<__int128>(n) * r) / nranks);
+}
+
+static int owner_of(const std::vector<int64_t>& firsts, int64_t g) {
+  // firsts has nranks + 1 entries, firsts[nranks] = n
+  return int(std::upper_bound(firsts.begin(), firsts.end(), g) - firsts.begin()) - 1;
+}
+
+ShardPlan shard_plan(int64_t n, int64_t nseg, const int32_t* seg_l, const int32_t* seg_r, int nranks,
+                     int rank) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(FM_ERR_CONFIG, "shard plan: bad rank / size");
+  if (n < nranks) throw Error(FM_ERR_CONFIG, "shard plan: fewer leaves than ranks");
+  std::vector<int64_t> firsts(nranks + 1);
+  for (int r = 0; r <= nranks; ++r) firsts[r] = shard_first(n, nranks, r);
+  ShardPlan p;
+  p.first = firsts[rank];
+  p.count = firsts[rank + 1] - firsts[rank];
+  p.send.assign(nranks, {});
+  for (int64_t q = 0; q < nseg; ++q) {
+    const int64_t a = seg_l[q], b = seg_r[q];
+    if (a < 0 || b < 0 || a >= n || b >= n) throw Error(FM_ERR_STRUCTURE, "shard plan: bad segment");
+    const int oa = owner_of(firsts, a), ob = owner_of(firsts, b);
+    if (oa != rank && ob != rank) continue;
+    p.segs.push_back(q);
+    if (oa == rank && ob != rank) {
+      p.halo.push_back(b);
+      p.send[ob].push_back(a);
+    } else if (ob == rank && oa != rank) {
+      p.halo.push_back(a);
+      p.send[oa].push_back(b);
+    }
+  }
+  auto uniq = [](std::vector<int64_t>& v) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  };
+  uniq(p.halo);
+  for (auto& v : p.send) uniq(v);
+  // halo grouped by owner: ascending global ids are already grouped
+  p.halo_owner.resize(p.halo.size());
+  for (size_t k = 0; k < p.halo.size(); ++k) p.halo_owner[k] = owner_of(firsts, p.halo[k]);
+  return p;
+}
+
+// ---- sharded sim construction -------------------------------------------------
+
+namespace {
+
+inline unsigned nblk(uint64_t n, int t) { return unsigned((n + t - 1) / t); }
+
+__global__ void k_pack(const double* __restrict__ u, const int32_t* __restrict__ idx, long long m,
+                       double* __restrict__ buf) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= 9 * m) return;
+  const long long k = t / 9, q = t % 9;
+  buf[t] = u[9 * (long long)idx[k] + q];
+}
+
+// Local group: min-combine the reduction slots of every shard into all of them.
+__global__ void k_red_combine(DevRed* const* reds, int n) {
+  const int f = threadIdx.x;  // 0..7: 2 slots x 4 fields
+  if (f >= 8) return;
+  unsigned long long m = ~0ull;
+  for (int r = 0; r < n; ++r) m = min(m, reinterpret_cast<const unsigned long long*>(reds[r])[f]);
+  for (int r = 0; r < n; ++r) reinterpret_cast<unsigned long long*>(reds[r])[f] = m;
+}
+
+template <typename T>
+std::vector<T> gather(const std::vector<T>& src, const std::vector<int64_t>& ids, int width) {
+  std::vector<T> out(ids.size() * size_t(width));
+  for (size_t k = 0; k < ids.size(); ++k)
+    std::memcpy(&out[k * width], &src[size_t(ids[k]) * width], sizeof(T) * width);
+  return out;
+}
+
+}  // namespace
+
+Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* grid, Comm* comm, int rank) {
+  if (!comm) throw Error(FM_ERR_CONFIG, "shard: null communicator");
+  if (rank < 0 || rank >= comm->nranks) throw Error(FM_ERR_CONFIG, "shard: rank out of range");
+  if (comm->kind == COMM_NCCL && rank != comm->rank)
+    throw Error(FM_ERR_CONFIG, "shard: rank differs from the NCCL communicator's");
+  if (!grid || d->solver == FM_MWDG2 || d->solver == FM_HWFV1)
+    throw Error(FM_ERR_CONFIG, "shard: only static non-uniform sims shard (adaptive and uniform "
+                               "sims run as replicas)");
+  cudaStream_t st = stream();
+  std::unique_ptr<Sim> G(sim_create(d, dem, grid));
+  const int64_t n = G->n, nseg = G->nseg;
+  // global state and topology on the host
+  const std::vector<int8_t> lvl = G->lvl.to_host();
+  const std::vector<int32_t> li = G->li.to_host(), lj = G->lj.to_host();
+  const std::vector<double> z = G->z.to_host(), nman = G->nman.to_host(), u = G->u.to_host();
+  const std::vector<int32_t> nb = G->nb.to_host(), sid = G->sid.to_host();
+  const std::vector<uint8_t> sk = G->sk.to_host();
+  const std::vector<int32_t> seg_l = G->seg_l.to_host(), seg_r = G->seg_r.to_host();
+  const std::vector<int32_t> infc = G->infc.to_host();
+  ShardPlan p = shard_plan(n, nseg, seg_l.data(), seg_r.data(), comm->nranks, rank);
+
+  auto S = std::make_unique<Sim>();
+  Sim& s = *S;
+  // scalar parameters
+  s.solver = G->solver;
+  s.scheme = G->scheme;
+  s.libm = G->libm;
+  s.g = G->g;
+  s.hdry = G->hdry;
+  s.courant = G->courant;
+  std::copy(G->bc, G->bc + 4, s.bc);
+  s.L = G->L;
+  s.M = G->M;
+  s.N = G->N;
+  s.R = G->R;
+  s.x0 = G->x0;
+  s.y0 = G->y0;
+  s.p2 = G->p2;
+  s.ninflow = G->ninflow;
+  s.hy_t = G->hy_t;
+  s.hy_q = G->hy_q;
+  s.region = G->region;
+  s.rect = G->rect;
+  s.manning = G->manning;
+  {
+    Hydro h;
+    G->hydro.download(&h, 1);
+    FM_CUDA(cudaStreamSynchronize(st));
+    s.hydro.upload(&h, 1);
+  }
+  s.clk.alloc(2);
+  s.red.alloc(2);
+
+  // local leaves: owned, then the halo
+  std::vector<int64_t> loc(size_t(p.count) + p.halo.size());
+  std::iota(loc.begin(), loc.begin() + p.count, p.first);
+  std::copy(p.halo.begin(), p.halo.end(), loc.begin() + p.count);
+  auto g2l = [&](int64_t g) -> int32_t {
+    if (g >= p.first && g < p.first + p.count) return int32_t(g - p.first);
+    const auto it = std::lower_bound(p.halo.begin(), p.halo.end(), g);
+    if (it == p.halo.end() || *it != g) return -1;
+    return int32_t(p.count + (it - p.halo.begin()));
+  };
+  auto seg2l = [&](int64_t q) -> int32_t {
+    const auto it = std::lower_bound(p.segs.begin(), p.segs.end(), q);
+    if (it == p.segs.end() || *it != q) throw Error(FM_ERR_STRUCTURE, "shard: segment outside the shard");
+    return int32_t(it - p.segs.begin());
+  };
+  s.n = p.count;
+  s.nseg = int64_t(p.segs.size());
+  const size_t nt = loc.size();
+  std::vector<int64_t> owned(loc.begin(), loc.begin() + p.count);
+  s.lvl.upload(gather(lvl, loc, 1).data(), nt);
+  s.li.upload(gather(li, loc, 1).data(), nt);
+  s.lj.upload(gather(lj, loc, 1).data(), nt);
+  s.z.upload(gather(z, loc, 3).data(), 3 * nt);
+  s.nman.upload(gather(nman, loc, 1).data(), nt);
+  s.u.upload(gather(u, loc, 9).data(), 9 * nt);
+  s.us.alloc(9 * nt);
+  FM_CUDA(cudaMemcpyAsync(s.us.p, s.u.p, 9 * nt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  s.sk.upload(gather(sk, owned, 1).data(), owned.size());
+  {
+    std::vector<int32_t> nbl(8 * owned.size()), sidl(8 * owned.size());
+    for (size_t k = 0; k < owned.size(); ++k)
+      for (int e = 0; e < 8; ++e) {
+        const int32_t gn = nb[8 * owned[k] + e], gs = sid[8 * owned[k] + e];
+        nbl[8 * k + e] = gn < 0 ? -1 : g2l(gn);
+        sidl[8 * k + e] = gs < 0 ? -1 : seg2l(gs);
+      }
+    s.nb.upload(nbl.data(), nbl.size());
+    s.sid.upload(sidl.data(), sidl.size());
+  }
+  {
+    std::vector<int32_t> sl(p.segs.size()), sr(p.segs.size());
+    for (size_t k = 0; k < p.segs.size(); ++k) {
+      sl[k] = g2l(seg_l[p.segs[k]]);
+      sr[k] = g2l(seg_r[p.segs[k]]);
+      if (sl[k] < 0 || sr[k] < 0) throw Error(FM_ERR_STRUCTURE, "shard: segment leaf outside the shard");
+    }
+    if (sl.empty()) sl.push_back(0), sr.push_back(0);  // no segments: a dummy entry
+    s.seg_l.upload(sl.data(), sl.size());
+    s.seg_r.upload(sr.data(), sr.size());
+  }
+  {
+    std::vector<int32_t> ic(std::max<int64_t>(1, int64_t(s.ninflow) * s.n), 0);
+    for (int f = 0; f < s.ninflow; ++f)
+      for (int64_t k = 0; k < s.n; ++k) ic[size_t(f) * s.n + k] = infc[size_t(f) * n + owned[k]];
+    s.infc.upload(ic.data(), ic.size());
+  }
+  if (s.scheme == FM_ACC) {
+    s.accq.alloc(std::max<int64_t>(s.nseg, 1));
+    s.accq.zero();
+    s.accqb.alloc(4 * s.n);
+    s.accqb.zero();
+  } else {
+    s.segst.alloc(6 * size_t(std::max<int64_t>(s.nseg, 1)));
+  }
+
+  // exchange plan
+  auto sh = std::make_unique<Shard>();
+  sh->comm = comm;
+  sh->rank = rank;
+  sh->nranks = comm->nranks;
+  sh->first = p.first;
+  sh->n_global = n;
+  sh->n_halo = int64_t(p.halo.size());
+  std::vector<int32_t> sidx;
+  for (int r = 0; r < comm->nranks; ++r) {
+    const int64_t h0 = std::lower_bound(p.halo_owner.begin(), p.halo_owner.end(), r) - p.halo_owner.begin();
+    const int64_t h1 = std::upper_bound(p.halo_owner.begin(), p.halo_owner.end(), r) - p.halo_owner.begin();
+    if (r == rank || (p.send[r].empty() && h1 == h0)) continue;
+    sh->peers.push_back(r);
+    sh->soff.push_back(int64_t(sidx.size()));
+    sh->scnt.push_back(int64_t(p.send[r].size()));
+    for (int64_t g : p.send[r]) sidx.push_back(int32_t(g - p.first));
+    sh->hoff.push_back(h0);
+    sh->hcnt.push_back(h1 - h0);
+  }
+  if (sidx.empty()) sidx.push_back(0);  // keep the buffers non-empty (no peers)
+  sh->send_idx.upload(sidx.data(), sidx.size());
+  sh->send_buf.alloc(9 * std::max<size_t>(sidx.size(), 1));
+  s.shard = std::move(sh);
+  if (comm->kind == COMM_LOCAL) comm->members[rank] = &s;
+  G.reset();
+  FM_CUDA(cudaStreamSynchronize(st));
+  return S.release();
+}
+
+// ---- step operations ---------------------------------------------------------
+
+void shard_pack(Sim& s, const double* arr) {
+  Shard& sh = *s.shard;
+  const long long m = (long long)(sh.soff.empty() ? 0 : sh.soff.back() + sh.scnt.back());
+  if (m == 0) return;
+  k_pack<<<nblk(9 * m, 256), 256, 0, stream()>>>(arr, sh.send_idx.p, m, sh.send_buf.p);
+  FM_LAUNCHED();
+}
+
+// Local group: copy every peer's packed slice for this shard into its halo.
+void shard_local_recv(Sim& s, double* arr) {
+  Shard& sh = *s.shard;
+  Comm& c = *sh.comm;
+  for (size_t k = 0; k < sh.peers.size(); ++k) {
+    const Sim* peer = c.members[sh.peers[k]];
+    if (!peer) throw Error(FM_ERR_CONFIG, "local group: a peer shard is missing");
+    const Shard& ps = *peer->shard;
+    const auto it = std::find(ps.peers.begin(), ps.peers.end(), sh.rank);
+    if (it == ps.peers.end()) throw Error(FM_ERR_STRUCTURE, "local group: asymmetric exchange plan");
+    const size_t j = size_t(it - ps.peers.begin());
+    if (ps.scnt[j] != sh.hcnt[k]) throw Error(FM_ERR_STRUCTURE, "local group: halo size mismatch");
+    if (sh.hcnt[k])
+      FM_CUDA(cudaMemcpyAsync(arr + 9 * (s.n + sh.hoff[k]), ps.send_buf.p + 9 * ps.soff[j],
+                              9 * sh.hcnt[k] * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+  }
+}
+
+void shard_local_reduce(const std::vector<Sim*>& sims) {
+  std::vector<DevRed*> reds;
+  for (Sim* s : sims) reds.push_back(s->red.p);
+  DBuf<DevRed*> d;
+  d.upload(reds.data(), reds.size());
+  k_red_combine<<<1, 32, 0, stream()>>>(d.p, int(reds.size()));
+  FM_LAUNCHED();
+  FM_CUDA(cudaStreamSynchronize(stream()));
+}
+
+void shard_op(Sim& s, int op) {
+  Shard& sh = *s.shard;
+  if (!sh.comm) throw Error(FM_ERR_CONFIG, "shard: the communicator was destroyed");
+  if (sh.comm->kind != COMM_NCCL)
+    throw Error(FM_ERR_CONFIG, "shard: a local-group shard steps only through fm_group_run");
+  const NcclApi& api = nccl();
+  cudaStream_t st = stream();
+  if (op == OP_REDUCE) {
+    // both parity slots: the other slot is already identical on every rank
+    nccl_check(api.AllReduce(s.red.p, s.red.p, 2 * sizeof(DevRed) / 8, ncclUint64, ncclMin,
+                             sh.comm->nc, st), "ncclAllReduce");
+    return;
+  }
+  double* arr = op == OP_EXCH_U ? s.u.p : s.us.p;
+  shard_pack(s, arr);
+  nccl_check(api.GroupStart(), "ncclGroupStart");
+  for (size_t k = 0; k < sh.peers.size(); ++k) {
+    if (sh.scnt[k])
+      nccl_check(api.Send(sh.send_buf.p + 9 * sh.soff[k], size_t(9 * sh.scnt[k]), ncclFloat64,
+                          sh.peers[k], sh.comm->nc, st), "ncclSend");
+    if (sh.hcnt[k])
+      nccl_check(api.Recv(arr + 9 * (s.n + sh.hoff[k]), size_t(9 * sh.hcnt[k]), ncclFloat64,
+                          sh.peers[k], sh.comm->nc, st), "ncclRecv");
+  }
+  nccl_check(api.GroupEnd(), "ncclGroupEnd");
+}
+
+// Host-API reductions of a sharded sim across its NCCL ranks (a local-group
+// shard answers for itself).
+void shard_allreduce_u64_min(Sim& s, unsigned long long* dev, int count) {
+  if (!s.shard || !s.shard->comm || s.shard->comm->kind != COMM_NCCL) return;
+  nccl_check(nccl().AllReduce(dev, dev, size_t(count), ncclUint64, ncclMin, s.shard->comm->nc, stream()),
+             "ncclAllReduce");
+}
+double shard_allreduce_sum(Sim& s, double v) {
+  if (!s.shard || !s.shard->comm || s.shard->comm->kind != COMM_NCCL) return v;
+  DBuf<double> d;
+  d.upload(&v, 1);
+  nccl_check(nccl().AllReduce(d.p, d.p, 1, ncclFloat64, ncclSum, s.shard->comm->nc, stream()),
+             "ncclAllReduce");
+  d.download(&v, 1);
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  return v;
+}
+
+}  // namespace fmh

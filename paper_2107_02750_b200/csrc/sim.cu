@@ -110,6 +110,7 @@ __global__ void k_finite(long long n, const int8_t* __restrict__ lvl, const int3
 }  // namespace
 
 Sim::~Sim() {
+  if (shard && shard->comm) comm_forget(shard->comm, this);
   if (graph) cudaGraphExecDestroy(graph);
   if (ad) adaptive_destroy(ad);
 }
@@ -356,7 +357,7 @@ void init_red(Sim& s) {
   for (auto& x : r) {
     double inf = std::numeric_limits<double>::infinity();
     std::memcpy(&x.dtmin, &inf, 8);
-    x.hmax = 0;
+    x.hmaxc = ~0ull;
     x.badkey = ~0ull;
     x.pad = 0;
   }
@@ -374,6 +375,8 @@ void launch_reduce_init(Sim& s) {
     un_launch_reduce_init(s);
   else
     nu_launch_reduce_init(s);
+  // a sharded sim's slots become global (NCCL; a local group combines in group_run)
+  if (s.shard) shard_allreduce_u64_min(s, reinterpret_cast<unsigned long long*>(s.red.p), 8);
 }
 
 DevClock fresh_clock(const fm_clock* c, int64_t max_steps, int stop) {
@@ -419,7 +422,8 @@ double sim_compute_dt(Sim& s) {
   std::memcpy(&v, &r[0].dtmin, 8);
   if (s.scheme == FM_ACC) {
     double hmax;
-    std::memcpy(&hmax, &r[0].hmax, 8);
+    const unsigned long long hb = ~r[0].hmaxc;
+    std::memcpy(&hmax, &hb, 8);
     if (hmax <= s.hdry) return std::numeric_limits<double>::infinity();
     if (s.uniform) return s.courant * s.R / std::sqrt(s.g * hmax);
     return s.courant * v / std::sqrt(s.g * hmax);
@@ -485,7 +489,9 @@ double sim_volume(Sim& s) {
     comp = (t - sum) - y;
     sum = t;
   }
-  return sum;
+  // a shard sums its own leaves; across NCCL ranks the partial sums add up
+  // (an audit figure: not bit-identical to the unsharded Kahan order)
+  return s.shard ? shard_allreduce_sum(s, sum) : sum;
 }
 
 bool sim_finite(Sim& s, double* bx, double* by) {
@@ -494,6 +500,7 @@ bool sim_finite(Sim& s, double* bx, double* by) {
   bad.fill_bytes(0xff);
   k_finite<<<nblk(s.n, 256), 256, 0, stream()>>>(s.n, s.uniform ? nullptr : s.lvl.p, s.li.p, s.lj.p, s.u.p, bad.p);
   FM_LAUNCHED();
+  if (s.shard) shard_allreduce_u64_min(s, bad.p, 1);
   unsigned long long key = 0;
   bad.download(&key, 1);
   FM_CUDA(cudaStreamSynchronize(stream()));
@@ -601,7 +608,7 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
         const int p = int(c.steps & 1);
         double inf = std::numeric_limits<double>::infinity();
         std::memcpy(&r[p].dtmin, &inf, 8);
-        r[p].hmax = 0;
+        r[p].hmaxc = ~0ull;
         r[p].badkey = ~0ull;
         s.red.upload(r, 2);
         launch_reduce_init(s);
@@ -657,6 +664,86 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
   r.finished = c.now >= c.end_time;
   r.event_due = c.event_due;
   if (c.blew_up) key_xy(s, c.bad_key, &r.bad_x, &r.bad_y);
+  if (out) *out = r;
+  if (c.blew_up) throw Error(FM_ERR_BLOWUP, "solver state is non-finite");
+}
+
+// The drive loop over a local group of shards (all ranks of a partition in
+// this process, on this device): the same step operations as the NCCL path,
+// interleaved across the shards phase by phase, with the halo exchanges done
+// as device copies between the shards' buffers and the reduction slots
+// min-combined.  No graph: this is the single-GPU check of the sharding logic.
+void group_run(const std::vector<Sim*>& sims, fm_clock* ck, int64_t max_steps, int stop_at_events,
+               fm_run_result* out) {
+  cudaStream_t st = stream();
+  if (sims.empty()) throw Error(FM_ERR_CONFIG, "group: no shards");
+  for (Sim* s : sims)
+    if (!s || !s->shard || int(sims.size()) != s->shard->nranks)
+      throw Error(FM_ERR_CONFIG, "group: every rank of one local communicator is needed, in rank order");
+  for (size_t r = 0; r < sims.size(); ++r)
+    if (sims[r]->shard->rank != int(r) || sims[r]->shard->comm != sims[0]->shard->comm)
+      throw Error(FM_ERR_CONFIG, "group: shards must be given in rank order and share a communicator");
+  const DevClock c0 = fresh_clock(ck, max_steps, stop_at_events);
+  for (Sim* s : sims) {
+    if (fv1_staged(*s)) fv1_to_star(*s);
+    DevClock pair[2] = {c0, c0};
+    s->clk.upload(pair, 2);
+    init_red(*s);
+    nu_launch_reduce_init(*s);
+    s->errflag.alloc(1);
+    s->errflag.zero();
+  }
+  shard_local_reduce(sims);
+  cudaEvent_t e0, e1;
+  FM_CUDA(cudaEventCreate(&e0));
+  FM_CUDA(cudaEventCreate(&e1));
+  FM_CUDA(cudaEventRecord(e0, st));
+  const std::vector<int> ops = nu_step_ops(*sims[0], false);
+  for (int64_t k = 0; k < max_steps; ++k) {
+    for (int op : ops) {
+      if (op == OP_EXCH_U || op == OP_EXCH_US) {
+        for (Sim* s : sims) shard_pack(*s, op == OP_EXCH_U ? s->u.p : s->us.p);
+        for (Sim* s : sims) shard_local_recv(*s, op == OP_EXCH_U ? s->u.p : s->us.p);
+      } else if (op == OP_REDUCE) {
+        shard_local_reduce(sims);
+      } else {
+        for (Sim* s : sims) nu_step_op(*s, op, false, 0.0, s->errflag.p);
+      }
+    }
+    DevClock c;
+    sims[0]->clk.download(&c, 1);
+    FM_CUDA(cudaStreamSynchronize(st));
+    if (!c.active) break;
+  }
+  FM_CUDA(cudaEventRecord(e1, st));
+  int herr = 0;
+  for (Sim* s : sims) {
+    nu_launch_close(*s);
+    int h = 0;
+    s->errflag.download(&h, 1);
+    FM_CUDA(cudaStreamSynchronize(st));
+    herr |= h;
+  }
+  DevClock c;
+  sims[0]->clk.download(&c, 1);
+  FM_CUDA(cudaStreamSynchronize(st));
+  for (Sim* s : sims) s->last_run_ms = elapsed_ms(e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (herr) throw Error(FM_ERR_DOMAIN, "hll_flux: negative depth");
+  ck->now = c.now;
+  ck->next_output = c.next_out;
+  ck->next_gauge = c.next_gauge;
+  fm_run_result r{};
+  r.steps = c.steps;
+  r.dt_min = c.dt_min;
+  r.dt_max = c.dt_max;
+  r.volume_inflow = c.vol_in;
+  r.blew_up = c.blew_up;
+  r.blow_up_time = c.blow_t;
+  r.finished = c.now >= c.end_time;
+  r.event_due = c.event_due;
+  if (c.blew_up) key_xy(*sims[0], c.bad_key, &r.bad_x, &r.bad_y);
   if (out) *out = r;
   if (c.blew_up) throw Error(FM_ERR_BLOWUP, "solver state is non-finite");
 }

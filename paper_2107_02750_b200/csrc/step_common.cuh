@@ -125,7 +125,7 @@ __device__ bool decide_step(const DevClock& c0, const DevRed& r, const Hydro* hy
   if (!c.active) return false;
   double raw;
   if (scheme == FM_ACC) {
-    const double hmax = bitsd(r.hmax);
+    const double hmax = bitsd(~r.hmaxc);
     raw = hmax <= hdry ? INFINITY : courant * bitsd(r.dtmin) / sqrt(g * hmax);
   } else {
     raw = bitsd(r.dtmin) * courant;
@@ -185,7 +185,7 @@ __device__ __forceinline__ void step_head(const NuView& v, DevClock* clk, DevRed
         if (g) {
           DevRed& nx = red[p ^ 1];
           nx.dtmin = dbits(INFINITY);
-          nx.hmax = 0ull;
+          nx.hmaxc = ~0ull;
           nx.badkey = ~0ull;
         }
       }
@@ -229,7 +229,7 @@ __device__ __forceinline__ void reduce_leaf(const NuView& v, DevRed* red, const 
   if ((threadIdx.x & 31) == 0) {
     DevRed& r = red[(c.steps) & 1];
     if (dtc < INFINITY) atomicMin(&r.dtmin, dbits(dtc));
-    if (hm > 0.0) atomicMax(&r.hmax, dbits(hm));
+    if (hm > 0.0) atomicMin(&r.hmaxc, ~dbits(hm));
     if (bad != ~0ull) atomicMin(&r.badkey, bad);
   }
 }
