@@ -45,6 +45,11 @@ namespace fmh {
 
 namespace {
 
+// ---- the step decision (one thread) -------------------------------------
+__global__ void k_decide(NuView v, DevClock* clk, DevRed* red, const Hydro* hy) {
+  decide_publish(v, clk, red, hy);
+}
+
 // ---- step head: clock + friction (DG2/FV1) ------------------------------
 // src == dst for DG2; FV1 keeps its post-step state in U* (see k_stage) and
 // the head moves it back into U while applying friction.
@@ -168,8 +173,7 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock, STAGE == 2 ? FM_STAGE2_MI
   load9(in, kk, s);
   const P3 zc = load3(v.z, kk);
   const int kind = (v.sk[kk] >> (2 * sd)) & 3;
-  // issue the dependent gathers early: segment ids -> segment states, and
-  // (stage 2) the step-start state
+  // issue the dependent gathers early: segment ids -> segment states
   const int nseg = kind == 0 ? 0 : kind == 3 ? 2 : 1;
   double sg[2][6];
 #pragma unroll
@@ -180,8 +184,10 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock, STAGE == 2 ? FM_STAGE2_MI
       for (int e = 0; e < 6; ++e) sg[t][e] = q[e];
     }
   }
-  double u0[9];
+  double u0[9];  // stage 2: the step-start state, loaded late (fewer live registers)
+#ifdef FM_U0_EARLY
   if (STAGE == 2) load9(uold, kk, u0);
+#endif
   const bool xn = sd == 1 || sd == 3;
   const bool mine_left = sd == 0 || sd == 1;
   {
@@ -294,6 +300,9 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock, STAGE == 2 ? FM_STAGE2_MI
 #pragma unroll
     for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
   } else {
+#ifndef FM_U0_EARLY
+    load9(uold, kk, u0);
+#endif
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
       double a = s[q];
@@ -561,6 +570,10 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
   };
   switch (op) {
     case OP_ACC:
+      if (!manual) {
+        k_decide<<<1, 1, 0, st>>>(v, clk, red, s.hydro.p);
+        FM_LAUNCHED();
+      }
       kt_begin(KF_ACC_FACES);
       k_acc_faces<<<nblk(ns, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.u.p, s.accq.p, manual, mdt);
       FM_LAUNCHED();
@@ -571,6 +584,10 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       kt_end();
       break;
     case OP_HEAD:
+      if (!manual) {
+        k_decide<<<1, 1, 0, st>>>(v, clk, red, s.hydro.p);
+        FM_LAUNCHED();
+      }
       // FV1 keeps its state in U* between steps; the head moves it to U with friction
       kt_begin(KF_HEAD);
       k_head_friction<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, fv1 ? s.us.p : s.u.p, s.u.p,
@@ -619,6 +636,11 @@ void nu_launch_step(Sim& s, bool manual, double mdt, int* err) {
       nu_step_op(s, op, manual, mdt, err);
     }
   }
+}
+
+void launch_decide(Sim& s) {
+  k_decide<<<1, 1, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.hydro.p);
+  FM_LAUNCHED();
 }
 
 void launch_head_friction(Sim& s, const double* src, double* dst, bool manual, double mdt) {

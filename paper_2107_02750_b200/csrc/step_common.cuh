@@ -161,39 +161,37 @@ __device__ bool decide_step(const DevClock& c0, const DevRed& r, const Hydro* hy
   return true;
 }
 
-// Step head shared by the first kernel of every scheme: thread 0 of each
-// block evaluates decide_step; block 0 publishes clk[1] and clears the
-// reduction slot this step will accumulate into.
+// The step decision, once per step by a single thread (k_decide): evaluate
+// decide_step on the step-start clock and the previous step's reductions,
+// publish the in-flight clock clk[1] and clear the reduction slot this step
+// accumulates into.  The step's kernels then only read clk[1].
+__device__ __forceinline__ void decide_publish(const NuView& v, DevClock* clk, DevRed* red,
+                                               const Hydro* hy) {
+  const DevClock c0 = clk[0];
+  const int p = int(c0.steps & 1);
+  DevClock c;
+  const bool g = decide_step(c0, red[p], hy, v.scheme, v.courant, v.g, v.hdry, v.ninflow, c);
+  clk[1] = c;
+  if (g) {
+    DevRed& nx = red[p ^ 1];
+    nx.dtmin = dbits(INFINITY);
+    nx.hmaxc = ~0ull;
+    nx.badkey = ~0ull;
+  }
+}
+
+// Step head of the first kernel of every scheme: whether this step runs, and dt.
 __device__ __forceinline__ void step_head(const NuView& v, DevClock* clk, DevRed* red,
                                           const Hydro* hy, int manual, double mdt, int& go,
                                           double& dt) {
-  __shared__ int s_go;
-  __shared__ double s_dt;
-  if (threadIdx.x == 0) {
-    if (manual) {
-      s_go = 1;
-      s_dt = mdt;
-    } else {
-      const DevClock c0 = clk[0];
-      const int p = int(c0.steps & 1);
-      DevClock c;
-      const bool g = decide_step(c0, red[p], hy, v.scheme, v.courant, v.g, v.hdry, v.ninflow, c);
-      s_go = g ? 1 : 0;
-      s_dt = c.dt;
-      if (blockIdx.x == 0) {
-        clk[1] = c;
-        if (g) {
-          DevRed& nx = red[p ^ 1];
-          nx.dtmin = dbits(INFINITY);
-          nx.hmaxc = ~0ull;
-          nx.badkey = ~0ull;
-        }
-      }
-    }
+  if (manual) {
+    go = 1;
+    dt = mdt;
+    return;
   }
-  __syncthreads();
-  go = s_go;
-  dt = s_dt;
+  const DevClock* c = clk + 1;
+  go = c->active;
+  dt = c->dt;
 }
 
 // Next-step reductions over the freshly written state (fused epilogue).

@@ -26,6 +26,7 @@ using namespace fmd;
 namespace fmh {
 
 void launch_head_friction(Sim& s, const double* src, double* dst, bool manual, double mdt);
+void launch_decide(Sim& s);
 void launch_commit(Sim& s);
 void project_planes_rowmajor(const fm_raster* r, DBuf<double>& out);
 
@@ -520,6 +521,7 @@ void un_launch_step(Sim& s, bool manual, double mdt, int* err) {
   const UniView v = uview(s);
   const NuView nv = s.view();
   const dim3 grid((s.nx + TX - 1) / TX, (s.ny + TY - 1) / TY);
+  if (!manual) launch_decide(s);  // the step decision, once (step_common.cuh)
   if (s.scheme == FM_ACC) {
     const long long nf = s.nseg;
     kt_begin(KF_ACC_FACES);
