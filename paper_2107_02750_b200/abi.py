@@ -424,13 +424,19 @@ class Sim:
         self.be.call("sim_finite", self.h, C.byref(ok), C.byref(bx), C.byref(by))
         return bool(ok.value), bx.value, by.value
 
-    def download(self):
+    def download(self, out=None):
+        """(level, i, j, u[n,9], z[n,3]) in the reference order; `out` may hold
+        preallocated (e.g. pinned) arrays of those shapes to fill."""
         n = self.num_cells
-        lv = np.zeros(n, np.int32)
-        i = np.zeros(n, np.int32)
-        j = np.zeros(n, np.int32)
-        u = np.zeros((n, 9), np.float64)
-        z = np.zeros((n, 3), np.float64)
+        if out is None:
+            lv = np.zeros(n, np.int32)
+            i = np.zeros(n, np.int32)
+            j = np.zeros(n, np.int32)
+            u = np.zeros((n, 9), np.float64)
+            z = np.zeros((n, 3), np.float64)
+        else:
+            lv, i, j, u, z = out
+            assert len(lv) == n and u.shape == (n, 9) and z.shape == (n, 3)
         self.be.call("sim_download", self.h, lv.ctypes.data_as(PI32), i.ctypes.data_as(PI32),
                      j.ctypes.data_as(PI32), dptr(u), dptr(z))
         return lv, i, j, u, z

@@ -446,6 +446,7 @@ void adaptive_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem) {
 }
 
 void adaptive_adapt(Sim& s, double t) {
+  s.ref_perm_ok = false;  // the leaf set changes
   cudaStream_t st = stream();
   Grid& g = *s.grid;
   AdaptState& a = *s.ad;

@@ -143,6 +143,9 @@ struct Sim {
   int graph_steps = 0;
   int64_t graph_kernels = 0;
   std::unique_ptr<Shard> shard;  // set for a sharded (multi-rank) static sim
+  // device order -> reference (level, j, i) order, cached per leaf set (order.cu)
+  DBuf<int32_t> ref_perm;
+  bool ref_perm_ok = false;
   ~Sim();
 
   NuView view() const;
@@ -161,6 +164,13 @@ void sim_run(Sim& s, fm_clock* clk, int64_t max_steps, int stop_at_events, fm_ru
 void sim_profile(Sim& s, int64_t steps, double* ms, int64_t* counts, int cap, int* nfam);
 void sim_snapshot(Sim& s);
 void sim_sync_u(Sim& s);  // FV1: move the staged post-step state back into u
+// reference-order transfers (order.cu); perm == nullptr means identity
+const int32_t* sim_ref_perm(Sim& s);
+void gather_rows(const int32_t* perm, int64_t n, int width, const double* src, double* host_dst);
+void gather_i32(const int32_t* perm, int64_t n, const int32_t* src, int32_t* host_dst);
+void gather_levels(const int32_t* perm, int64_t n, const int8_t* lvl, int32_t* host_dst);
+void gather_col(const int32_t* perm, int64_t n, int stride, int col, const double* src, double* host_dst);
+void scatter_rows(const int32_t* perm, int64_t n, int width, const double* host_src, double* dst);
 // output sampling (output.cu)
 void sim_raster_shape(const Sim& s, int32_t* nc, int32_t* nr, double* xll, double* yll, double* cs,
                       double* nodata);

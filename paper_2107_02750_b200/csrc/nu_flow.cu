@@ -61,6 +61,28 @@ __global__ void __launch_bounds__(256) k_head_friction(NuView v, DevClock* clk, 
   double dt;
   step_head(v, clk, red, hy, manual, mdt, go, dt);
   if (!go || k >= v.n) return;
+  if (src == dst) {
+    // in place (DG2): friction reads h.c0, qx.c0, qy.c0 and writes q.c0 (wet)
+    // or zeroes both discharges (dry); the other coefficients stay in HBM
+    double* o = dst + 9 * k;
+    const double h0 = o[0];
+    if (h0 <= v.hdry) {
+#pragma unroll
+      for (int q = 3; q < 9; ++q) o[q] = 0.0;
+      return;
+    }
+    double s[9];
+    s[0] = h0;
+    s[3] = o[3];
+    s[6] = o[6];
+    const double q3 = s[3], q6 = s[6];
+    friction(s, v.nman[k], v.g, v.hdry, dt, v.libm);
+    if (s[3] != q3 || s[6] != q6) {  // bit-level: friction changed them
+      o[3] = s[3];
+      o[6] = s[6];
+    }
+    return;
+  }
   double s[9];
   load9(src, k, s);
   friction(s, v.nman[k], v.g, v.hdry, dt, v.libm);

@@ -1,0 +1,149 @@
+// The reference leaf order on the device.
+//
+// The reference stores leaves sorted by (level, j, i) (make_quadgrid,
+// quadgrid.cpp:94-98); the device keeps them in Morton order.  Host-facing
+// downloads/uploads permute between the two.  Sorting 2.3 M leaves and
+// scattering 200 MB of state on the host cost ~0.4 s per download for
+// config 4; here the leaf keys (level << 58 | j << 29 | i, the reference's
+// own leaf_key layout) are radix-sorted on the device once per leaf set, and
+// every transfer is a device gather/scatter plus one contiguous copy.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "fm_device.cuh"
+#include "fm_sim.hpp"
+
+namespace fmh {
+
+namespace {
+
+inline unsigned nblk(uint64_t n, int t) { return unsigned((n + t - 1) / t); }
+
+__global__ void k_keys(int64_t n, const int8_t* __restrict__ lvl, const int32_t* __restrict__ li,
+                       const int32_t* __restrict__ lj, unsigned long long* __restrict__ key,
+                       int32_t* __restrict__ idx) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= n) return;
+  key[k] = (static_cast<unsigned long long>(lvl[k]) << 58) |
+           (static_cast<unsigned long long>(lj[k]) << 29) | static_cast<unsigned long long>(li[k]);
+  idx[k] = int32_t(k);
+}
+
+// dst[r] = src[perm[r]] for rows of `width` elements
+template <typename T>
+__global__ void k_gather(int64_t n, int width, const int32_t* __restrict__ perm, const T* __restrict__ src,
+                         T* __restrict__ dst) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t >= n * width) return;
+  const int64_t r = t / width, q = t % width;
+  dst[t] = src[int64_t(perm[r]) * width + q];
+}
+
+// dst[perm[r]] = src[r]
+template <typename T>
+__global__ void k_scatter(int64_t n, int width, const int32_t* __restrict__ perm, const T* __restrict__ src,
+                          T* __restrict__ dst) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t >= n * width) return;
+  const int64_t r = t / width, q = t % width;
+  dst[int64_t(perm[r]) * width + q] = src[t];
+}
+
+// dst[r] = src[perm[r] * stride + col]
+__global__ void k_gather_col(int64_t n, int stride, int col, const int32_t* __restrict__ perm,
+                             const double* __restrict__ src, double* __restrict__ dst) {
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (r < n) dst[r] = src[int64_t(perm ? perm[r] : r) * stride + col];
+}
+
+__global__ void k_widen(int64_t n, const int32_t* __restrict__ perm, const int8_t* __restrict__ lvl,
+                        int32_t* __restrict__ out) {
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (r < n) out[r] = lvl[perm[r]];
+}
+
+}  // namespace
+
+const int32_t* sim_ref_perm(Sim& s) {
+  if (s.uniform) return nullptr;  // j * nx + i is already the reference order
+  if (s.ref_perm_ok && s.ref_perm.n == size_t(s.n)) return s.ref_perm.p;
+  cudaStream_t st = stream();
+  const int64_t n = s.n;
+  DBuf<unsigned long long> k0(std::max<int64_t>(n, 1)), k1(std::max<int64_t>(n, 1));
+  DBuf<int32_t> i0(std::max<int64_t>(n, 1));
+  s.ref_perm.alloc(std::max<int64_t>(n, 1));
+  k_keys<<<nblk(n, 256), 256, 0, st>>>(n, s.lvl.p, s.li.p, s.lj.p, k0.p, i0.p);
+  FM_LAUNCHED();
+  size_t tmp_bytes = 0;
+  FM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0.p, k1.p, i0.p, s.ref_perm.p, int(n), 0,
+                                          62, st));
+  DBuf<unsigned char> tmp(std::max<size_t>(tmp_bytes, 1));
+  FM_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, k0.p, k1.p, i0.p, s.ref_perm.p, int(n), 0,
+                                          62, st));
+  FM_LAUNCHED();
+  s.ref_perm_ok = true;
+  return s.ref_perm.p;
+}
+
+void gather_rows(const int32_t* perm, int64_t n, int width, const double* src, double* host_dst) {
+  cudaStream_t st = stream();
+  if (!perm) {
+    FM_CUDA(cudaMemcpyAsync(host_dst, src, size_t(n) * width * sizeof(double), cudaMemcpyDeviceToHost, st));
+    return;
+  }
+  DBuf<double> tmp(std::max<int64_t>(n * width, 1));
+  k_gather<double><<<nblk(n * width, 256), 256, 0, st>>>(n, width, perm, src, tmp.p);
+  FM_LAUNCHED();
+  FM_CUDA(cudaMemcpyAsync(host_dst, tmp.p, size_t(n) * width * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FM_CUDA(cudaStreamSynchronize(st));
+}
+
+void gather_i32(const int32_t* perm, int64_t n, const int32_t* src, int32_t* host_dst) {
+  cudaStream_t st = stream();
+  if (!perm) {
+    FM_CUDA(cudaMemcpyAsync(host_dst, src, size_t(n) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    return;
+  }
+  DBuf<int32_t> tmp(std::max<int64_t>(n, 1));
+  k_gather<int32_t><<<nblk(n, 256), 256, 0, st>>>(n, 1, perm, src, tmp.p);
+  FM_LAUNCHED();
+  FM_CUDA(cudaMemcpyAsync(host_dst, tmp.p, size_t(n) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  FM_CUDA(cudaStreamSynchronize(st));
+}
+
+void gather_levels(const int32_t* perm, int64_t n, const int8_t* lvl, int32_t* host_dst) {
+  cudaStream_t st = stream();
+  DBuf<int32_t> tmp(std::max<int64_t>(n, 1));
+  if (perm) {
+    k_widen<<<nblk(n, 256), 256, 0, st>>>(n, perm, lvl, tmp.p);
+    FM_LAUNCHED();
+  } else {
+    tmp.zero();
+  }
+  FM_CUDA(cudaMemcpyAsync(host_dst, tmp.p, size_t(n) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  FM_CUDA(cudaStreamSynchronize(st));
+}
+
+void gather_col(const int32_t* perm, int64_t n, int stride, int col, const double* src, double* host_dst) {
+  cudaStream_t st = stream();
+  DBuf<double> tmp(std::max<int64_t>(n, 1));
+  k_gather_col<<<nblk(n, 256), 256, 0, st>>>(n, stride, col, perm, src, tmp.p);
+  FM_LAUNCHED();
+  FM_CUDA(cudaMemcpyAsync(host_dst, tmp.p, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FM_CUDA(cudaStreamSynchronize(st));
+}
+
+void scatter_rows(const int32_t* perm, int64_t n, int width, const double* host_src, double* dst) {
+  cudaStream_t st = stream();
+  if (!perm) {
+    FM_CUDA(cudaMemcpyAsync(dst, host_src, size_t(n) * width * sizeof(double), cudaMemcpyHostToDevice, st));
+    FM_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  DBuf<double> tmp;
+  tmp.upload(host_src, size_t(n) * width);
+  k_scatter<double><<<nblk(n * width, 256), 256, 0, st>>>(n, width, perm, tmp.p, dst);
+  FM_LAUNCHED();
+  FM_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace fmh

@@ -477,14 +477,18 @@ double sim_apply_inflows(Sim& s, double t, double dt) {
 }
 
 double sim_volume(Sim& s) {
-  // Kahan in reference order (solver_nonuniform.cpp:467-477) over downloaded h.
-  std::vector<double> u9(9 * s.n);
-  std::vector<int32_t> l(s.n), i(s.n), j(s.n);
-  sim_download(s, l.data(), i.data(), j.data(), u9.data(), nullptr);
+  // Kahan in reference order (solver_nonuniform.cpp:467-477) over h.c0 and
+  // the leaf levels, gathered into reference order on the device
+  if (fv1_staged(s)) fv1_to_u(s);
+  const int32_t* perm = sim_ref_perm(s);
+  std::vector<double> h(s.n);
+  std::vector<int32_t> l(s.n, 0);
+  gather_col(perm, s.n, 9, 0, s.u.p, h.data());
+  if (!s.uniform) gather_levels(perm, s.n, s.lvl.p, l.data());
   double sum = 0.0, comp = 0.0;
   for (int64_t c = 0; c < s.n; ++c) {
     const double sz = s.uniform ? s.R : s.R * double(1 << (s.L - l[c]));
-    const double y = s.uniform ? u9[9 * c] * s.R * s.R - comp : u9[9 * c] * sz * sz - comp;
+    const double y = s.uniform ? h[c] * s.R * s.R - comp : h[c] * sz * sz - comp;
     const double t = sum + y;
     comp = (t - sum) - y;
     sum = t;
@@ -509,56 +513,26 @@ bool sim_finite(Sim& s, double* bx, double* by) {
   return false;
 }
 
-// Reference order: (level, j, i) for leaves (quadgrid.cpp:94-98), j*nx+i for rasters.
-static std::vector<int64_t> sim_order(Sim& s, std::vector<int8_t>& l, std::vector<int32_t>& i,
-                                      std::vector<int32_t>& j) {
-  i = s.li.to_host();
-  j = s.lj.to_host();
-  std::vector<int64_t> perm(s.n);
-  for (int64_t k = 0; k < s.n; ++k) perm[k] = k;
-  if (s.uniform) {  // already j*nx+i, the reference order
-    l.assign(s.n, 0);
-    return perm;
-  }
-  l = s.lvl.to_host();
-  std::sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) {
-    if (l[a] != l[b]) return l[a] < l[b];
-    if (j[a] != j[b]) return j[a] < j[b];
-    return i[a] < i[b];
-  });
-  return perm;
-}
-
 void sim_sync_u(Sim& s) {
   if (fv1_staged(s)) fv1_to_u(s);
 }
 
+// Reference order: (level, j, i) for leaves (quadgrid.cpp:94-98), j*nx+i for
+// rasters; permuted on the device (order.cu).
 void sim_download(Sim& s, int32_t* lo, int32_t* io, int32_t* jo, double* u9, double* z3) {
   if (fv1_staged(s)) fv1_to_u(s);
-  std::vector<int8_t> l;
-  std::vector<int32_t> i, j;
-  const std::vector<int64_t> perm = sim_order(s, l, i, j);
-  std::vector<double> u = u9 ? s.u.to_host() : std::vector<double>();
-  std::vector<double> z = z3 ? s.z.to_host() : std::vector<double>();
-  for (int64_t r = 0; r < s.n; ++r) {
-    const int64_t k = perm[r];
-    if (lo) lo[r] = l[k];
-    if (io) io[r] = i[k];
-    if (jo) jo[r] = j[k];
-    if (u9) std::memcpy(u9 + 9 * r, &u[9 * k], 72);
-    if (z3) std::memcpy(z3 + 3 * r, &z[3 * k], 24);
-  }
+  const int32_t* perm = sim_ref_perm(s);
+  if (lo) gather_levels(perm, s.n, s.lvl.p, lo);
+  if (io) gather_i32(perm, s.n, s.li.p, io);
+  if (jo) gather_i32(perm, s.n, s.lj.p, jo);
+  if (u9) gather_rows(perm, s.n, 9, s.u.p, u9);
+  if (z3) gather_rows(perm, s.n, 3, s.z.p, z3);
+  FM_CUDA(cudaStreamSynchronize(stream()));
 }
 
 void sim_upload(Sim& s, const double* u9) {
   if (fv1_staged(s)) fv1_to_u(s);
-  std::vector<int8_t> l;
-  std::vector<int32_t> i, j;
-  const std::vector<int64_t> perm = sim_order(s, l, i, j);
-  std::vector<double> u(9 * s.n);
-  for (int64_t r = 0; r < s.n; ++r) std::memcpy(&u[9 * perm[r]], u9 + 9 * r, 72);
-  s.u.upload(u.data(), u.size());
-  FM_CUDA(cudaStreamSynchronize(stream()));
+  scatter_rows(sim_ref_perm(s), s.n, 9, u9, s.u.p);
 }
 
 void sim_adapt(Sim& s, double t) {

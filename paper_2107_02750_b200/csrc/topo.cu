@@ -198,20 +198,21 @@ __global__ void k_scan_apply(const int32_t* __restrict__ in, int32_t* __restrict
 }
 
 // --- inflow targets (solver_nonuniform.cpp:611-628) ---------------------------
-// One thread per fine cell of the rectangle: walk down from level 0 to the
-// leaf containing it (QuadGrid::find_containing, quadgrid.cpp:62-69) and count.
-__global__ void k_inflow_cells(TopoIn t, int i0, int j0, int wi, long long cells,
-                               int32_t* __restrict__ cnt) {
-  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (c >= cells) return;
-  const int fi = i0 + int(c % wi), fj = j0 + int(c / wi);
-  int l = 0;
-  uint64_t node = node_index(0, fi >> t.L, fj >> t.L, t.M);
-  while (l < t.L && t.flag[l][node]) {
-    ++l;
-    node = node_index(l, fi >> (t.L - l), fj >> (t.L - l), t.M);
-  }
-  atomicAdd(&cnt[leaf_index(t, l, node)], 1);
+// The reference walks every fine cell of the rectangle to its containing leaf
+// (QuadGrid::find_containing, quadgrid.cpp:62-69) and counts cells per leaf.
+// A leaf's count is the area of the intersection of its fine-cell square with
+// the rectangle, computed directly per leaf (integer, so identical).
+__global__ void k_inflow_overlap(long long n, int L, const int8_t* __restrict__ lvl,
+                                 const int32_t* __restrict__ li, const int32_t* __restrict__ lj, int i0,
+                                 int j0, int i1, int j1, int32_t* __restrict__ cnt) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int sh = L - lvl[k];
+  const long long x0 = (long long)li[k] << sh, x1 = x0 + (1ll << sh);
+  const long long y0 = (long long)lj[k] << sh, y1 = y0 + (1ll << sh);
+  const long long wx = max(0ll, min(x1, (long long)i1 + 1) - max(x0, (long long)i0));
+  const long long wy = max(0ll, min(y1, (long long)j1 + 1) - max(y0, (long long)j0));
+  cnt[k] = int32_t(wx * wy);
 }
 
 // Manning per leaf from a cell-centred raster (solver_nonuniform.cpp:575-584).
@@ -296,14 +297,14 @@ void build_topology(Sim& s, const Grid& g) {
 }
 
 void resolve_inflows(Sim& s, const Grid& g) {
+  (void)g;
   cudaStream_t st = stream();
   s.infc.alloc(std::max<int64_t>(1, int64_t(s.ninflow) * s.n));
-  s.infc.zero();
-  const TopoIn t = topo_in(g);
+  if (s.ninflow == 0) s.infc.zero();
   for (int f = 0; f < s.ninflow; ++f) {
-    const int i0 = s.rect[4 * f], j0 = s.rect[4 * f + 1], i1 = s.rect[4 * f + 2], j1 = s.rect[4 * f + 3];
-    const long long wi = i1 - i0 + 1, cells = wi * (long long)(j1 - j0 + 1);
-    k_inflow_cells<<<nblk(cells, 256), 256, 0, st>>>(t, i0, j0, int(wi), cells, s.infc.p + f * s.n);
+    const int* r = &s.rect[4 * f];
+    k_inflow_overlap<<<nblk(s.n, 256), 256, 0, st>>>(s.n, s.L, s.lvl.p, s.li.p, s.lj.p, r[0], r[1], r[2],
+                                                     r[3], s.infc.p + f * s.n);
     FM_LAUNCHED();
   }
 }
