@@ -93,11 +93,16 @@ __device__ __forceinline__ double rand_operand(uint64_t r, uint64_t r2) {
   return __longlong_as_double(static_cast<long long>((sign << 63) | (e << 52) | mant));
 }
 
-__global__ void k_selftest_div(int64_t n, uint64_t seed, unsigned long long* fails) {
+__global__ void k_selftest_div(int which, int64_t n, uint64_t seed, unsigned long long* fails) {
   const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (k >= n) return;
   const uint64_t a1 = mix64(seed ^ (2 * k)), a2 = mix64(a1), b1 = mix64(a2), b2 = mix64(b1);
   const double a = rand_operand(a1, a2), b = rand_operand(b1, b2);
+  if (which == 1) {  // the constant-divisor path of project4
+    const double q1 = fmd::div_4s3(a), r1 = a / (4.0 * fmd::kS3);
+    if (__double_as_longlong(q1) != __double_as_longlong(r1)) atomicAdd(fails, 1ull);
+    return;
+  }
   // the inline division kernel builds use with -DFM_INLINE_DIV (fmd::quot)
   const double q = (fmd::div_fast_ok(a) && fmd::div_fast_ok(b)) ? fmd::quot(a, b, fmd::recip(b)) : a / b;
   const double ref = a / b;
@@ -141,10 +146,10 @@ int64_t fm_launch_count(void) { return launches(); }
 int fm_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* failures) {
   return guard([&] {
     require_device();
-    if (which != 0) throw Error(FM_ERR_CONFIG, "unknown self-test");
+    if (which != 0 && which != 1) throw Error(FM_ERR_CONFIG, "unknown self-test");
     DBuf<unsigned long long> f(1);
     f.zero();
-    k_selftest_div<<<unsigned((n + 255) / 256), 256, 0, stream()>>>(n, seed, f.p);
+    k_selftest_div<<<unsigned((n + 255) / 256), 256, 0, stream()>>>(which, n, seed, f.p);
     FM_LAUNCHED();
     unsigned long long v = 0;
     f.download(&v, 1);

@@ -57,10 +57,24 @@ struct DBuf {
     if (count == n && p) return;
     release();
     n = count;
+#ifdef FM_PLAIN_MALLOC
+    if (count) {
+      FM_CUDA(cudaStreamSynchronize(stream()));
+      FM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+    }
+#else
     if (count) FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream()));
+#endif
   }
   void release() {
+#ifdef FM_PLAIN_MALLOC
+    if (p) {
+      cudaStreamSynchronize(stream());
+      cudaFree(p);
+    }
+#else
     if (p) cudaFreeAsync(p, stream());
+#endif
     p = nullptr;
     n = 0;
   }

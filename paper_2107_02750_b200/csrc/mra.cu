@@ -155,7 +155,10 @@ __global__ void __launch_bounds__(256) k_encode_tiles(EncParams p) {
   const int tid = threadIdx.x;
   const uint64_t tile = blockIdx.x;
   const double norm = p.scal->norm;
-  if constexpr (FROM_VERTICES) p.vv.wall = p.scal->wall;
+  // a register copy: writing into the by-value parameter struct would make
+  // every thread spill the whole 344-byte EncParams to local memory
+  VertexView vv = p.vv;
+  if constexpr (FROM_VERTICES) vv.wall = p.scal->wall;
 
   // first level: parent (lev_in - 1), local index tid
   int lev = p.lev_in - 1;
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(256) k_encode_tiles(EncParams p) {
     if constexpr (FROM_VERTICES) {
       int i, j;
       node_ij(p.lev_in, c, p.M, i, j);
-      kids[k] = p.vv.plane(i, j);
+      kids[k] = vv.plane(i, j);
     } else {
       const double* s = p.sc_in + 3 * c;
       kids[k] = P3{s[0], s[1], s[2]};
