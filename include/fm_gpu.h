@@ -147,6 +147,14 @@ int fm_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* failures);
  * (:66-74) -> grade_flags (:97-113) -> assemble_grid (:132-164). */
 int fm_mra_static(const fm_raster* dem, int32_t L, double eps, int32_t graded, int32_t kind,
                   fm_grid** out);
+/* A grid from a leaf list and its topography: read_nug's construction
+ * (quadgrid.cpp:310-327) via make_quadgrid (quadgrid.cpp:85-110), e.g. for
+ * run_scenario's grid_file path (run.cpp:150-153).  Leaves in any order;
+ * StructureError when they leave the domain, do not tile it or overlap.
+ * Flags / details of an imported grid: flags = internal nodes, details 0. */
+int fm_grid_import(int32_t L, int32_t M, int32_t N, double Rfine, double x0, double y0, int64_t n,
+                   const int32_t* level, const int32_t* i, const int32_t* j, const double* topo3,
+                   fm_grid** out);
 int fm_grid_destroy(fm_grid* g);
 int64_t fm_grid_num_leaves(const fm_grid* g);
 /* QuadGrid scalars (quadgrid.hpp:54-60) plus DetailTree::field_norm. */

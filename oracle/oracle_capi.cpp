@@ -143,6 +143,26 @@ int orc_mra_static(const fm_raster* dem, int32_t L, double eps, int32_t graded, 
   });
 }
 
+// read_nug (quadgrid.cpp:310-327): make_quadgrid over a leaf list plus the
+// per-leaf topography, re-aligned to the sorted leaf order.
+int orc_grid_import(int32_t L, int32_t M, int32_t N, double R, double x0, double y0, int64_t n,
+                    const int32_t* lv, const int32_t* ii, const int32_t* jj, const double* topo3,
+                    orc_grid** out) {
+  return guard([&] {
+    auto g = std::make_unique<orc_grid>();
+    std::vector<Leaf> leaves(n);
+    for (int64_t k = 0; k < n; ++k) leaves[k] = Leaf{lv[k], ii[k], jj[k]};
+    g->grid = make_grid(L, M, N, R, x0, y0, leaves);
+    g->topo.assign(n, Pl{});
+    for (int64_t k = 0; k < n; ++k) {
+      const int idx = g->grid.find(lv[k], ii[k], jj[k]);
+      if (idx < 0) throw Fail(E_STRUCT, "grid import: duplicate leaf");
+      g->topo[idx] = Pl{topo3[3 * k], topo3[3 * k + 1], topo3[3 * k + 2]};
+    }
+    *out = g.release();
+  });
+}
+
 int orc_grid_destroy(orc_grid* g) {
   delete g;
   return FM_OK;

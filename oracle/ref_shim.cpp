@@ -176,6 +176,25 @@ int ref_generate_static_grid(const fm_raster* dem, int32_t L, double eps, int32_
   });
 }
 
+// read_nug's construction (quadgrid.cpp:310-327) from arrays: make_quadgrid +
+// topography re-aligned to the sorted leaves.
+int ref_grid_import(int32_t L, int32_t M, int32_t N, double R, double x0, double y0, int64_t n,
+                    const int32_t* lv, const int32_t* ii, const int32_t* jj, const double* topo3,
+                    ref_grid** out) {
+  return guard([&] {
+    auto g = std::make_unique<ref_grid>();
+    std::vector<fm::LeafId> leaves(n);
+    for (int64_t k = 0; k < n; ++k) leaves[k] = fm::LeafId{lv[k], ii[k], jj[k]};
+    g->nug.grid = fm::make_quadgrid(L, M, N, R, x0, y0, leaves);
+    g->nug.topo.resize(n);
+    for (int64_t k = 0; k < n; ++k) {
+      const int idx = g->nug.grid.find(lv[k], ii[k], jj[k]);
+      g->nug.topo[idx] = fm::PlanarCoeffs{topo3[3 * k], topo3[3 * k + 1], topo3[3 * k + 2]};
+    }
+    *out = g.release();
+  });
+}
+
 int ref_grid_destroy(ref_grid* g) {
   delete g;
   return FM_OK;

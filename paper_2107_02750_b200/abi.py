@@ -141,6 +141,7 @@ OPTIONAL = {
     "shard_plan": (C.c_int, [I64, I64, PI32, PI32, I32, I32, PI64, PI64, PI64, PI64, PI64, PI32,
                              PI64, PI64]),
     "sim_topology": (C.c_int, [P, PI32, PI32, PI32, PI32, PI32]),
+    "grid_import": (C.c_int, [I32, I32, I32, D, D, D, I64, PI32, PI32, PI32, PD, PP]),
 }
 
 
@@ -189,6 +190,20 @@ class Backend:
 
     def sim(self, scenario, grid=None, libm: int = 0):
         return Sim(self, scenario, grid, libm)
+
+    def grid_import(self, L: int, M: int, N: int, R: float, x0: float, y0: float, level, i, j,
+                    topo3) -> "Grid":
+        """fm_grid_import: read_nug's NonUniformGrid from a leaf list + topography."""
+        lv = np.ascontiguousarray(level, np.int32)
+        ii = np.ascontiguousarray(i, np.int32)
+        jj = np.ascontiguousarray(j, np.int32)
+        z = np.ascontiguousarray(topo3, np.float64)
+        h = P()
+        self.call("grid_import", L, M, N, R, x0, y0, len(lv), lv.ctypes.data_as(PI32),
+                  ii.ctypes.data_as(PI32), jj.ctypes.data_as(PI32), dptr(z), C.byref(h))
+        g = Grid.__new__(Grid)
+        g.be, g.h, g.eps, g._keep = self, h, 0.0, []
+        return g
 
     # ---- sharding (SURVEY §8e) ----
     def comm_local(self, nranks: int) -> "Comm":

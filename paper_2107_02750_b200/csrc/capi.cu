@@ -168,6 +168,16 @@ int fm_mra_static(const fm_raster* dem, int32_t L, double eps, int32_t graded, i
   });
 }
 
+int fm_grid_import(int32_t L, int32_t M, int32_t N, double Rfine, double x0, double y0, int64_t n,
+                   const int32_t* level, const int32_t* i, const int32_t* j, const double* topo3,
+                   fm_grid** out) {
+  return guard([&] {
+    require_device();
+    auto h = std::make_unique<fm_grid>();
+    h->g.reset(grid_from_leaves(L, M, N, Rfine, x0, y0, n, level, i, j, topo3));
+    *out = h.release();
+  });
+}
 int fm_grid_destroy(fm_grid* g) {
   return guard([&] { delete g; });
 }

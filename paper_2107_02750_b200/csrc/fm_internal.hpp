@@ -122,6 +122,9 @@ struct Grid {
 };
 
 Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind);
+// A grid from a leaf list + topography (read_nug / make_quadgrid), static sims only.
+Grid* grid_from_leaves(int L, int M, int N, double R, double x0, double y0, int64_t n, const int32_t* lv,
+                       const int32_t* li, const int32_t* lj, const double* topo3);
 // The stages of mra_static, reused by the adaptive solver.
 void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, double* ms);
 void grade_count_levels(Grid& g, bool graded);

@@ -602,6 +602,99 @@ void grade_count_levels(Grid& g, bool graded) {
   }
 }
 
+// ---- a grid from a leaf list (read_nug + make_quadgrid, quadgrid.cpp:85-110, 310-327)
+namespace {
+__global__ void k_mark_ancestors(int64_t n, const int8_t* __restrict__ lvl, const int32_t* __restrict__ li,
+                                 const int32_t* __restrict__ lj, uint8_t* const* __restrict__ flag, int M) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= n) return;
+  const int l = lvl[k];
+  for (int a = 0; a < l; ++a) flag[a][node_index(a, li[k] >> (l - a), lj[k] >> (l - a), M)] = 1;
+}
+}  // namespace
+
+Grid* grid_from_leaves(int L, int M, int N, double R, double x0, double y0, int64_t n, const int32_t* lv,
+                       const int32_t* li, const int32_t* lj, const double* topo3) {
+  if (L < 0 || L > kMaxL - 1) throw Error(FM_ERR_CONFIG, "grid import: level out of range");
+  if (M < 1 || N < 1 || n < 1) throw Error(FM_ERR_CONFIG, "grid import: empty grid");
+  // make_quadgrid's checks (quadgrid.cpp:100-108)
+  int64_t weight = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    const int l = lv[k];
+    if (l < 0 || l > L || li[k] < 0 || lj[k] < 0 || li[k] >= (M << l) || lj[k] >= (N << l))
+      throw Error(FM_ERR_STRUCTURE, "make_quadgrid: leaf outside domain");
+    weight += int64_t(1) << (2 * (L - l));
+  }
+  if (weight != int64_t(M) * N * (int64_t(1) << (2 * L)))
+    throw Error(FM_ERR_STRUCTURE, "make_quadgrid: leaves do not tile the domain");
+  cudaStream_t st = stream();
+  auto g = std::make_unique<Grid>();
+  g->L = L;
+  g->M = M;
+  g->N = N;
+  g->R = R;
+  g->x0 = x0;
+  g->y0 = y0;
+  g->kind = FM_MW;
+  g->graded = false;
+  // internal nodes = strict ancestors of the leaves
+  std::vector<int8_t> l8(lv, lv + n);
+  DBuf<int8_t> dl;
+  DBuf<int32_t> di, dj;
+  dl.upload(l8.data(), n);
+  di.upload(li, n);
+  dj.upload(lj, n);
+  g->flag.resize(L);
+  std::vector<uint8_t*> fptr(std::max(L, 1), nullptr);
+  for (int l = 0; l < L; ++l) {
+    g->flag[l].alloc(g->nodes(l));
+    g->flag[l].zero();
+    fptr[l] = g->flag[l].p;
+  }
+  if (L > 0) {
+    DBuf<uint8_t*> dfp;
+    dfp.upload(fptr.data(), fptr.size());
+    k_mark_ancestors<<<blocks_for(n, 256), 256, 0, st>>>(n, dl.p, di.p, dj.p, dfp.p, M);
+    FM_LAUNCHED();
+    FM_CUDA(cudaStreamSynchronize(st));
+  }
+  // counts, offsets and the Morton-ordered leaf list from the flags; the
+  // decode runs on zero details (the imported topography replaces it below)
+  g->det.resize(L);
+  for (int l = 0; l < L; ++l) {
+    g->det[l].alloc(9 * g->nodes(l));
+    g->det[l].zero();
+  }
+  g->coarse.alloc(3 * size_t(M) * N);
+  g->coarse.zero();
+  grade_count_levels(*g, false);
+  build_leaves(*g);
+  g->det.clear();
+  if (g->nleaves != n) throw Error(FM_ERR_STRUCTURE, "make_quadgrid: overlapping or duplicate leaves");
+  // check the derived leaves against the input and place the topography
+  const std::vector<int8_t> gl = g->lf_l.to_host();
+  const std::vector<int32_t> gi = g->lf_i.to_host(), gj = g->lf_j.to_host();
+  std::vector<int64_t> order(n);
+  std::vector<uint64_t> key(n);
+  for (int64_t k = 0; k < n; ++k) {
+    key[k] = node_index(lv[k], li[k], lj[k], M) << (2 * (L - lv[k]));
+    order[k] = k;
+  }
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
+  std::vector<double> z(3 * size_t(n));
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t k = order[r];
+    if (gl[r] != lv[k] || gi[r] != li[k] || gj[r] != lj[k])
+      throw Error(FM_ERR_STRUCTURE, "make_quadgrid: overlapping or duplicate leaves");
+    z[3 * r] = topo3[3 * k];
+    z[3 * r + 1] = topo3[3 * k + 1];
+    z[3 * r + 2] = topo3[3 * k + 2];
+  }
+  g->lf_z.upload(z.data(), z.size());
+  FM_CUDA(cudaStreamSynchronize(st));
+  return g.release();
+}
+
 Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind) {
   auto g = std::make_unique<Grid>();
   g->graded = graded;
