@@ -319,7 +319,12 @@ def run_ours(args, ws, rank, local):
     d2h = sum(a.nbytes for a in out)
     e2e_steps = args.warmup + args.steps
     e2e_value = allreduce_sum(float(n_leaves) * e2e_steps, ws) / e2e_s
-    del s2, g2
+    del s2, g2, outs, keep
+
+    # ---- config 4's comparator: the uniform raster at the finest level ----
+    uni = None
+    if args.uniform_steps > 0:
+        uni = uniform_leg(lib, args, ws, rank, comm, hbm)
     comm = None
 
     if rank != 0:
@@ -352,11 +357,54 @@ def run_ours(args, ws, rank, local):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
                 "d2h_bytes_per_step": d2h / e2e_steps, "seconds": e2e_s,
                 "what": "host DEM -> fm_mra_static -> fm_sim_create(_shard) -> W+K steps -> host state"},
+        "uniform": uni,
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
+
+
+def uniform_leg(lib, args, ws, rank, comm, hbm):
+    """Config 4's "uniform-raster DG2 at the finest level": 8192^2 cells, the
+    same forcing; N > 1: row bands with one ghost row each side (NCCL)."""
+    import torch
+    sc = S.config4(args.scale, uniform=True)
+    sim = lib.shard_sim(sc, None, comm, rank) if comm is not None else lib.sim(sc, None)
+    n = sim.num_cells
+    ck, _ = sim.run(3, gauge_interval=10.0)
+    sim.snapshot()
+    ck0 = (ck.end_time, ck.output_interval, ck.gauge_interval, ck.now, ck.next_output, ck.next_gauge)
+    ms = 0.0
+    done = 0
+    while done < args.uniform_steps:
+        k = min(args.chunk, args.uniform_steps - done)
+        sim.restore()
+        barrier(ws)
+        torch.cuda.synchronize()
+        _, r = sim.run(k, clock=c_clock(*ck0))
+        torch.cuda.synchronize()
+        barrier(ws)
+        if r.steps != k:
+            raise SystemExit(f"uniform: only {r.steps} of {k} steps ran")
+        ms += sim.last_run_ms()
+        done += k
+    ms_max = allreduce_max(ms, ws)
+    total = allreduce_sum(float(n) * args.uniform_steps, ws)
+    sim.restore()
+    prof = sim.profile(3)
+    st2_ms, st2_n = prof.get("k_uni_stage<2>", (0.0, 1))
+    avg = st2_ms / max(st2_n, 1)
+    bytes_launch = 248.0 * n  # U^n 72 + U* 72 + z 24 + n 8 read, 72 written per cell
+    del sim
+    return {"workload": "c4_uniform_dg2", "cells": int(allreduce_sum(float(n), ws)),
+            "value": total / (ms_max / 1000.0), "unit": UNIT, "steps": args.uniform_steps,
+            "ms_per_step": ms_max / args.uniform_steps,
+            "parallelism": f"row-bands x{ws}" if ws > 1 else "single",
+            "roofline": {"bound": "hbm", "kernel": "k_uni_stage<2>",
+                         "achieved": bytes_launch / (avg / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": bytes_launch / (avg / 1000.0) / 1e9 / hbm, "avg_launch_ms": avg},
+            "kernels_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in prof.items()}}
 
 
 def main():
@@ -371,6 +419,8 @@ def main():
     p.add_argument("--cpu-steps", type=int, default=40)
     p.add_argument("--cpu-steps-cap", type=int, default=20)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--uniform-steps", type=int, default=32,
+                   help="timed steps of the uniform-raster comparator (0: skip)")
     p.add_argument("--force-shard", action="store_true",
                    help="N=1: run the sharded (NCCL) code path with a single rank")
     args = p.parse_args()

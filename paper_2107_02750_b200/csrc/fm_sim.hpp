@@ -97,7 +97,9 @@ struct Sim {
   // geometry
   int L = 0, M = 1, N = 1;
   double R = 1, x0 = 0, y0 = 0;
-  int nx = 0, ny = 0;  // uniform raster
+  int nx = 0, ny = 0;  // uniform raster (ny: owned rows of a band)
+  int gy0 = 0, nyg = 0;        // band: first global row, global row count (0: unsharded)
+  int ghost_s = 0, ghost_n = 0;  // band: ghost rows stored after the owned ones
   // Power-of-two element sizes with exactly representable coordinates: the
   // stage kernels evaluate planes at exact offsets and replace divisions by
   // the element size with exact reciprocal multiplies (bit-identical).
@@ -181,6 +183,13 @@ void sim_restore(Sim& s);
 // step operations (nu_flow.cu) and the shard layer (shard.cu)
 std::vector<int> nu_step_ops(const Sim& s, bool manual);
 void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err);
+void un_step_op(Sim& s, int op, bool manual, double mdt, int* err);
+inline void step_op(Sim& s, int op, bool manual, double mdt, int* err) {
+  if (s.uniform)
+    un_step_op(s, op, manual, mdt, err);
+  else
+    nu_step_op(s, op, manual, mdt, err);
+}
 void shard_op(Sim& s, int op);  // exchange / reduce for a sharded sim (NCCL)
 struct ShardPlan {
   int64_t first = 0, count = 0;

@@ -78,6 +78,7 @@ __global__ void k_raster_uni(int nx, int ny, const double* __restrict__ u, int w
 struct GaugeGeom {
   bool uniform, dg2;
   int nx, ny;
+  int gy0, nyg;  // a raster band: its first global row, the global row count
 };
 
 __global__ void k_gauges(NuView v, GaugeGeom gg, const unsigned long long* __restrict__ start,
@@ -91,8 +92,12 @@ __global__ void k_gauges(NuView v, GaugeGeom gg, const unsigned long long* __res
   if (gg.uniform) {
     // UniformSim::sample_gauge (solver_uniform.cpp:480-483)
     const int i = min(max(int(floor((x - v.x0) / v.R)), 0), gg.nx - 1);
-    const int j = min(max(int(floor((y - v.y0) / v.R)), 0), gg.ny - 1);
-    k = (long long)j * gg.nx + i;
+    const int j = min(max(int(floor((y - v.y0) / v.R)), 0), gg.nyg - 1);
+    if (j < gg.gy0 || j >= gg.gy0 + gg.ny) {  // another band's cell
+      for (int q = 0; q < 4; ++q) out4[4 * g + q] = nan("");
+      return;
+    }
+    k = (long long)(j - gg.gy0) * gg.nx + i;
     cx = v.x0 + (i + 0.5) * v.R;
     cy = v.y0 + (j + 0.5) * v.R;
     sz = v.R;
@@ -138,11 +143,11 @@ void leaf_starts(Sim& s, DBuf<unsigned long long>& start) {
 void sim_raster_shape(const Sim& s, int32_t* nc, int32_t* nr, double* xll, double* yll, double* cs,
                       double* nodata) {
   if (s.uniform) {
-    *nc = s.nx, *nr = s.ny;
+    *nc = s.nx, *nr = s.ny;  // a band's own rows when sharded
   } else {
     *nc = s.M << s.L, *nr = s.N << s.L;
   }
-  *xll = s.x0, *yll = s.y0, *cs = s.R, *nodata = -9999.0;
+  *xll = s.x0, *yll = s.y0 + s.gy0 * s.R, *cs = s.R, *nodata = -9999.0;
 }
 
 void sim_raster(Sim& s, int which, double* out, bool on_device) {
@@ -182,7 +187,7 @@ void sim_sample_gauges(Sim& s, int n, const double* x, const double* y, double* 
   dxy.upload(xy.data(), xy.size());
   DBuf<unsigned long long> start;
   if (!s.uniform) leaf_starts(s, start);
-  GaugeGeom gg{s.uniform, s.scheme == FM_DG2, s.nx, s.ny};
+  GaugeGeom gg{s.uniform, s.scheme == FM_DG2, s.nx, s.ny, s.gy0, s.nyg ? s.nyg : s.ny};
   k_gauges<<<nblk(n, 64), 64, 0, stream()>>>(s.view(), gg, start.p, s.u.p, n, dxy.p, dout.p);
   FM_LAUNCHED();
   dout.download(out4, 4 * size_t(n));

@@ -219,14 +219,126 @@ std::vector<T> gather(const std::vector<T>& src, const std::vector<int64_t>& ids
 
 }  // namespace
 
+// The uniform raster shards into row bands: rank r owns the global rows
+// [floor(ny r / R), floor(ny (r+1) / R)) (a contiguous range of the raster's
+// own j-major cell order), stored first, then one ghost row south and one
+// north where a neighbour band exists.  The exchange per stage is one row of
+// 72 B cells each way; faces on a band edge are solved by both bands from the
+// same inputs.
+static Sim* uniform_shard(const fm_sim_desc* d, const fm_raster* dem, Comm* comm, int rank) {
+  cudaStream_t st = stream();
+  std::unique_ptr<Sim> G(sim_create(d, dem, nullptr));
+  const int R = comm->nranks, nx = G->nx, nyg = G->ny;
+  if (nyg < R) throw Error(FM_ERR_CONFIG, "shard: fewer raster rows than ranks");
+  const int g0 = int(shard_first(nyg, R, rank)), g1 = int(shard_first(nyg, R, rank + 1));
+  const int nyo = g1 - g0, hs = g0 > 0 ? 1 : 0, hn = g1 < nyg ? 1 : 0;
+  std::vector<int64_t> rows;  // storage row -> global row
+  for (int j = g0; j < g1; ++j) rows.push_back(j);
+  if (hs) rows.push_back(g0 - 1);
+  if (hn) rows.push_back(g1);
+  std::vector<int64_t> cells;
+  cells.reserve(rows.size() * size_t(nx));
+  for (int64_t j : rows)
+    for (int i = 0; i < nx; ++i) cells.push_back(j * nx + i);
+  const std::vector<double> u = G->u.to_host(), z = G->z.to_host(), nman = G->nman.to_host();
+  const std::vector<int32_t> li = G->li.to_host(), lj = G->lj.to_host();
+
+  auto S = std::make_unique<Sim>();
+  Sim& s = *S;
+  s.solver = G->solver;
+  s.scheme = G->scheme;
+  s.libm = G->libm;
+  s.g = G->g;
+  s.hdry = G->hdry;
+  s.courant = G->courant;
+  std::copy(G->bc, G->bc + 4, s.bc);
+  s.uniform = true;
+  s.L = 0;
+  s.M = nx;
+  s.N = nyo;
+  s.R = G->R;
+  s.x0 = G->x0;
+  s.y0 = G->y0;
+  s.p2 = G->p2;
+  s.nx = nx;
+  s.ny = nyo;
+  s.gy0 = g0;
+  s.nyg = nyg;
+  s.ghost_s = hs;
+  s.ghost_n = hn;
+  s.ninflow = G->ninflow;
+  s.hy_t = G->hy_t;
+  s.hy_q = G->hy_q;
+  s.region = G->region;
+  s.rect = G->rect;
+  s.manning = G->manning;
+  {
+    Hydro h;
+    G->hydro.download(&h, 1);
+    FM_CUDA(cudaStreamSynchronize(st));
+    s.hydro.upload(&h, 1);
+  }
+  s.clk.alloc(2);
+  s.red.alloc(2);
+  s.n = int64_t(nx) * nyo;
+  s.nseg = int64_t(nx + 1) * nyo + int64_t(nx) * (nyo + 1);
+  const size_t nt = cells.size();
+  std::vector<int64_t> owned(cells.begin(), cells.begin() + s.n);
+  s.u.upload(gather(u, cells, 9).data(), 9 * nt);
+  s.us.alloc(9 * nt);
+  FM_CUDA(cudaMemcpyAsync(s.us.p, s.u.p, 9 * nt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  s.z.upload(gather(z, cells, 3).data(), 3 * nt);
+  s.nman.upload(gather(nman, cells, 1).data(), nt);
+  s.li.upload(gather(li, owned, 1).data(), owned.size());
+  s.lj.upload(gather(lj, owned, 1).data(), owned.size());
+  if (s.scheme == FM_ACC) {
+    s.aqx.alloc(size_t(nx + 1) * nyo);
+    s.aqy.alloc(size_t(nx) * (nyo + 1));
+    s.aqx.zero();
+    s.aqy.zero();
+  }
+  auto sh = std::make_unique<Shard>();
+  sh->comm = comm;
+  sh->rank = rank;
+  sh->nranks = R;
+  sh->first = int64_t(g0) * nx;
+  sh->n_global = int64_t(nyg) * nx;
+  sh->n_halo = int64_t(hs + hn) * nx;
+  std::vector<int32_t> sidx;
+  if (hs) {  // row g0 to rank - 1, its row g0 - 1 into the south ghost
+    sh->peers.push_back(rank - 1);
+    sh->soff.push_back(int64_t(sidx.size()));
+    sh->scnt.push_back(nx);
+    for (int i = 0; i < nx; ++i) sidx.push_back(i);
+    sh->hoff.push_back(0);
+    sh->hcnt.push_back(nx);
+  }
+  if (hn) {  // row g1 - 1 to rank + 1, its row g1 into the north ghost
+    sh->peers.push_back(rank + 1);
+    sh->soff.push_back(int64_t(sidx.size()));
+    sh->scnt.push_back(nx);
+    for (int i = 0; i < nx; ++i) sidx.push_back(int32_t(int64_t(nyo - 1) * nx + i));
+    sh->hoff.push_back(int64_t(hs) * nx);
+    sh->hcnt.push_back(nx);
+  }
+  if (sidx.empty()) sidx.push_back(0);
+  sh->send_idx.upload(sidx.data(), sidx.size());
+  sh->send_buf.alloc(9 * sidx.size());
+  s.shard = std::move(sh);
+  if (comm->kind == COMM_LOCAL) comm->members[rank] = &s;
+  G.reset();
+  FM_CUDA(cudaStreamSynchronize(st));
+  return S.release();
+}
+
 Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* grid, Comm* comm, int rank) {
   if (!comm) throw Error(FM_ERR_CONFIG, "shard: null communicator");
   if (rank < 0 || rank >= comm->nranks) throw Error(FM_ERR_CONFIG, "shard: rank out of range");
   if (comm->kind == COMM_NCCL && rank != comm->rank)
     throw Error(FM_ERR_CONFIG, "shard: rank differs from the NCCL communicator's");
-  if (!grid || d->solver == FM_MWDG2 || d->solver == FM_HWFV1)
-    throw Error(FM_ERR_CONFIG, "shard: only static non-uniform sims shard (adaptive and uniform "
-                               "sims run as replicas)");
+  if (d->solver == FM_MWDG2 || d->solver == FM_HWFV1)
+    throw Error(FM_ERR_CONFIG, "shard: adaptive sims re-grid every step and run as replicas");
+  if (!grid) return uniform_shard(d, dem, comm, rank);
   cudaStream_t st = stream();
   std::unique_ptr<Sim> G(sim_create(d, dem, grid));
   const int64_t n = G->n, nseg = G->nseg;

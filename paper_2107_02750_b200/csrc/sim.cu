@@ -663,7 +663,10 @@ void group_run(const std::vector<Sim*>& sims, fm_clock* ck, int64_t max_steps, i
     DevClock pair[2] = {c0, c0};
     s->clk.upload(pair, 2);
     init_red(*s);
-    nu_launch_reduce_init(*s);
+    if (s->uniform)
+      un_launch_reduce_init(*s);
+    else
+      nu_launch_reduce_init(*s);
     s->errflag.alloc(1);
     s->errflag.zero();
   }
@@ -681,7 +684,7 @@ void group_run(const std::vector<Sim*>& sims, fm_clock* ck, int64_t max_steps, i
       } else if (op == OP_REDUCE) {
         shard_local_reduce(sims);
       } else {
-        for (Sim* s : sims) nu_step_op(*s, op, false, 0.0, s->errflag.p);
+        for (Sim* s : sims) step_op(*s, op, false, 0.0, s->errflag.p);
       }
     }
     DevClock c;

@@ -34,8 +34,12 @@ namespace {
 
 constexpr int TX = 32, TY = 8;
 
+// A raster band: rows [gy0, gy0 + ny) of the global ny_g rows are owned and
+// stored first (row-major); the ghost rows of a sharded band (the rows just
+// south / north of it, hs / hn) follow them.  Unsharded: gy0 = 0, ny_g = ny.
 struct UniView {
   int nx, ny, scheme, ninflow, libm;
+  int gy0, nyg, hs, hn;
   double R, x0, y0, g, hdry, courant;
   int bc[4];
   const double* z;
@@ -46,6 +50,13 @@ struct UniView {
 struct Star {
   double h, qx, qy;
 };
+
+// storage index of cell (i, local row jl), jl in [-1, ny]: owned rows first,
+// then the south and north ghost rows
+__device__ __forceinline__ size_t cidx(const UniView& v, int i, int jl) {
+  const int r = jl < 0 ? v.ny : jl >= v.ny ? v.ny + v.hs : jl;
+  return size_t(r) * v.nx + i;
+}
 
 // One face of revise_faces (solver_uniform.cpp:84-129): the cell's limit on
 // side `sd` (side_limit, :16-26) against the opposing face value of the
@@ -90,20 +101,21 @@ __global__ void __launch_bounds__(TX* TY) k_uni_stage(UniView v, NuView nv, cons
   if (!manual && !c->active) return;
   const double dt = manual ? mdt : c->dt;
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;  // y: local owned rows
   const int i = x0 + tx, j = y0 + ty;
   const bool valid = i < v.nx && j < v.ny;
   const int ic = min(i, v.nx - 1), jc = min(j, v.ny - 1);
+  const int gj = v.gy0 + j;  // global row
   const size_t cell = size_t(jc) * v.nx + ic;
   double s[9];
   ld9(in, cell, s);
   const P3 zc = ld3(v.z, cell);
   // phase 1: revise the four faces
-  const bool hasE = ic + 1 < v.nx, hasW = ic > 0, hasN = jc + 1 < v.ny, hasS = jc > 0;
+  const bool hasE = ic + 1 < v.nx, hasW = ic > 0, hasN = v.gy0 + jc + 1 < v.nyg, hasS = v.gy0 + jc > 0;
   const double zwe = hasE ? face_val(ld3(v.z, cell + 1), 3) : 0.0;
   const double zew = hasW ? face_val(ld3(v.z, cell - 1), 1) : 0.0;
-  const double zsn = hasN ? face_val(ld3(v.z, cell + v.nx), 2) : 0.0;
-  const double zns = hasS ? face_val(ld3(v.z, cell - v.nx), 0) : 0.0;
+  const double zsn = hasN ? face_val(ld3(v.z, cidx(v, ic, jc + 1)), 2) : 0.0;
+  const double zns = hasS ? face_val(ld3(v.z, cidx(v, ic, jc - 1)), 0) : 0.0;
   const FaceRev re = revise_face(s, zc, 1, zwe, hasE, v.hdry);
   const FaceRev rw = revise_face(s, zc, 3, zew, hasW, v.hdry);
   const FaceRev rn = revise_face(s, zc, 0, zsn, hasN, v.hdry);
@@ -125,17 +137,20 @@ __global__ void __launch_bounds__(TX* TY) k_uni_stage(UniView v, NuView nv, cons
     ld9(in, cc, t);
     h_e[ty] = revise_face(t, ld3(v.z, cc), 3, face_val(ld3(v.z, cc - 1), 1), true, v.hdry).st;
   }
-  if (ty == 0 && y0 > 0 && i < v.nx) {  // star_n of (i, y0-1)
+  if (ty == 0 && v.gy0 + y0 > 0 && i < v.nx) {  // star_n of (i, y0-1)
     double t[9];
-    const size_t cc = size_t(y0 - 1) * v.nx + i;
+    const size_t cc = cidx(v, i, y0 - 1);
     ld9(in, cc, t);
-    h_s[tx] = revise_face(t, ld3(v.z, cc), 0, face_val(ld3(v.z, cc + v.nx), 2), true, v.hdry).st;
+    h_s[tx] = revise_face(t, ld3(v.z, cc), 0, face_val(ld3(v.z, cidx(v, i, y0)), 2), true, v.hdry).st;
   }
-  if (ty == TY - 1 && y0 + TY < v.ny && i < v.nx) {  // star_s of (i, y0+TY)
+  // star_s of (i, yN), the row just north of the tile's last row (a ghost row
+  // when the tile ends the band)
+  const int yN = min(y0 + TY, v.ny);
+  if (ty == TY - 1 && v.gy0 + yN < v.nyg && i < v.nx) {
     double t[9];
-    const size_t cc = size_t(y0 + TY) * v.nx + i;
+    const size_t cc = cidx(v, i, yN);
     ld9(in, cc, t);
-    h_n[tx] = revise_face(t, ld3(v.z, cc), 2, face_val(ld3(v.z, cc - v.nx), 0), true, v.hdry).st;
+    h_n[tx] = revise_face(t, ld3(v.z, cc), 2, face_val(ld3(v.z, cidx(v, i, yN - 1)), 0), true, v.hdry).st;
   }
   __syncthreads();
   // phase 2: every face of the tile once (fluxes, solver_uniform.cpp:139-185)
@@ -162,13 +177,13 @@ __global__ void __launch_bounds__(TX* TY) k_uni_stage(UniView v, NuView nv, cons
   for (int f = threadIdx.x; f < (TY + 1) * TX; f += TX * TY) {
     const int r = f / TX, k = f % TX;
     if (k >= ncx || r > ncy) continue;
-    const int gj = y0 + r;
+    const int gf = v.gy0 + y0 + r;  // global face row
     Star l, rr;
-    if (gj == 0) {
+    if (gf == 0) {
       rr = s_s[0][k];
       l = rr;
       if (v.bc[2] == FM_REFLECTIVE) l.qy = -l.qy;
-    } else if (gj == v.ny) {
+    } else if (gf == v.nyg) {
       l = s_n[r - 1][k];
       rr = l;
       if (v.bc[0] == FM_REFLECTIVE) rr.qy = -rr.qy;
@@ -214,7 +229,7 @@ __global__ void __launch_bounds__(TX* TY) k_uni_stage(UniView v, NuView nv, cons
       // apply_inflows (solver_uniform.cpp:444-455): one fine cell per target
       for (int f = 0; f < v.ninflow; ++f) {
         if (!c->on[f]) continue;
-        if (i >= v.rect[4 * f] && j >= v.rect[4 * f + 1] && i <= v.rect[4 * f + 2] && j <= v.rect[4 * f + 3])
+        if (i >= v.rect[4 * f] && gj >= v.rect[4 * f + 1] && i <= v.rect[4 * f + 2] && gj <= v.rect[4 * f + 3])
           res[0] += ddiv(c->per_cell[f] * 1, v.R * v.R);
       }
     }
@@ -225,7 +240,7 @@ __global__ void __launch_bounds__(TX* TY) k_uni_stage(UniView v, NuView nv, cons
 #pragma unroll
     for (int q = 0; q < 9; ++q) res[q] = 0.0;
   }
-  if (last && !manual) reduce_leaf(nv, red, *c, res, v.R, leaf_key(0, i, j), valid);
+  if (last && !manual) reduce_leaf(nv, red, *c, res, v.R, leaf_key(0, i, gj), valid);
 }
 
 // ---- ACC (solver_uniform.cpp:330-415) --------------------------------------
@@ -256,14 +271,15 @@ __global__ void __launch_bounds__(256) k_uni_acc_faces(UniView v, NuView nv, Dev
       r = l + 1;
     }
   } else {
-    j = int(g / v.nx);
+    j = int(g / v.nx);  // local face row: between local rows j - 1 and j
     i = int(g % v.nx);
-    boundary = j == 0 || j == v.ny;
-    side = j == 0 ? 2 : 0;
-    edge = size_t(j == 0 ? 0 : v.ny - 1) * v.nx + i;
+    const int gf = v.gy0 + j;
+    boundary = gf == 0 || gf == v.nyg;
+    side = gf == 0 ? 2 : 0;
+    edge = size_t(gf == 0 ? 0 : v.ny - 1) * v.nx + i;
     if (!boundary) {
-      l = size_t(j - 1) * v.nx + i;
-      r = l + v.nx;
+      l = cidx(v, i, j - 1);
+      r = cidx(v, i, j);
     }
   }
   double* qp = xf ? qx + g : qy + g;
@@ -316,10 +332,11 @@ __global__ void __launch_bounds__(256) k_uni_acc_cells(UniView v, NuView nv, con
     s[0] -= zdiv(dt * ((qe - qw) + (qn - qs)), v.R);
     s[3] = 0.5 * (qw + qe);
     s[6] = 0.5 * (qs + qn);
+    const int gj = v.gy0 + j;
     if (!manual) {
       for (int f = 0; f < v.ninflow; ++f) {
         if (!c->on[f]) continue;
-        if (i >= v.rect[4 * f] && j >= v.rect[4 * f + 1] && i <= v.rect[4 * f + 2] && j <= v.rect[4 * f + 3])
+        if (i >= v.rect[4 * f] && gj >= v.rect[4 * f + 1] && i <= v.rect[4 * f + 2] && gj <= v.rect[4 * f + 3])
           s[0] += ddiv(c->per_cell[f] * 1, v.R * v.R);
       }
     }
@@ -327,10 +344,10 @@ __global__ void __launch_bounds__(256) k_uni_acc_cells(UniView v, NuView nv, con
     u[9 * k + 3] = s[3];
     u[9 * k + 6] = s[6];
   }
-  if (!manual) reduce_leaf(nv, red, *c, s, v.R, leaf_key(0, i, j), valid);
+  if (!manual) reduce_leaf(nv, red, *c, s, v.R, leaf_key(0, i, v.gy0 + j), valid);
 }
 
-__global__ void k_uni_reduce_init(NuView nv, int nx, const DevClock* clk, DevRed* red,
+__global__ void k_uni_reduce_init(NuView nv, int nx, int gy0, const DevClock* clk, DevRed* red,
                                   const double* __restrict__ u) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool valid = k < nv.n;
@@ -338,7 +355,7 @@ __global__ void k_uni_reduce_init(NuView nv, int nx, const DevClock* clk, DevRed
   int i = 0, j = 0;
   if (valid) {
     ld9(u, k, s);
-    j = int(k / nx);
+    j = gy0 + int(k / nx);
     i = int(k % nx);
   }
   DevClock c = clk[0];
@@ -405,7 +422,7 @@ __global__ void k_uni_ij(int nx, long long n, int32_t* li, int32_t* lj) {
 __global__ void k_uni_inflow_add(UniView v, const double* __restrict__ per_cell, double* u) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= (long long)v.nx * v.ny) return;
-  const int j = int(k / v.nx), i = int(k % v.nx);
+  const int j = v.gy0 + int(k / v.nx), i = int(k % v.nx);
   double h = u[9 * k];
   for (int f = 0; f < v.ninflow; ++f) {
     if (per_cell[f] == 0.0) continue;
@@ -421,6 +438,10 @@ UniView uview(const Sim& s) {
   UniView v{};
   v.nx = s.nx;
   v.ny = s.ny;
+  v.gy0 = s.gy0;
+  v.nyg = s.nyg ? s.nyg : s.ny;
+  v.hs = s.ghost_s;
+  v.hn = s.ghost_n;
   v.scheme = s.scheme;
   v.ninflow = s.ninflow;
   v.libm = s.libm;
@@ -516,51 +537,68 @@ void uniform_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem) {
   s.nseg = int64_t(s.nx + 1) * s.ny + int64_t(s.nx) * (s.ny + 1);
 }
 
-void un_launch_step(Sim& s, bool manual, double mdt, int* err) {
+// The device phases of a uniform-raster step (the op sequence of nu_step_ops;
+// exchanges and reductions of a sharded band are the shard layer's).
+void un_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
   cudaStream_t st = stream();
   const UniView v = uview(s);
   const NuView nv = s.view();
   const dim3 grid((s.nx + TX - 1) / TX, (s.ny + TY - 1) / TY);
-  if (!manual) launch_decide(s);  // the step decision, once (step_common.cuh)
-  if (s.scheme == FM_ACC) {
-    const long long nf = s.nseg;
-    kt_begin(KF_ACC_FACES);
-    k_uni_acc_faces<<<nblk(nf, 256), 256, 0, st>>>(v, nv, s.clk.p, s.red.p, s.hydro.p, s.u.p, s.aqx.p,
-                                                    s.aqy.p, manual, mdt);
-    FM_LAUNCHED();
-    kt_end();
-    kt_begin(KF_ACC_LEAVES);
-    k_uni_acc_cells<<<nblk(s.n, 256), 256, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, s.aqx.p, s.aqy.p,
-                                                     manual, mdt);
-    FM_LAUNCHED();
-    kt_end();
-  } else if (s.scheme == FM_FV1) {
-    launch_head_friction(s, s.us.p, s.u.p, manual, mdt);
-    kt_begin(KF_UNI_STAGE1);
-    if (s.p2)
-      k_uni_stage<1, true><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
-    else
-      k_uni_stage<1, false><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, 1, manual, mdt, err);
-    FM_LAUNCHED();
-    kt_end();
-  } else {
-    launch_head_friction(s, s.u.p, s.u.p, manual, mdt);
-    kt_begin(KF_UNI_STAGE1);
-    if (s.p2)
-      k_uni_stage<1, true><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
-    else
-      k_uni_stage<1, false><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, 0, manual, mdt, err);
-    FM_LAUNCHED();
-    kt_end();
-    kt_begin(KF_UNI_STAGE2);
-    if (s.p2)
-      k_uni_stage<2, true><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
-    else
-      k_uni_stage<2, false><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
-    FM_LAUNCHED();
-    kt_end();
+  const bool fv1 = s.scheme == FM_FV1;
+  switch (op) {
+    case OP_ACC: {
+      if (!manual) launch_decide(s);  // the step decision, once (step_common.cuh)
+      const long long nf = int64_t(s.nx + 1) * s.ny + int64_t(s.nx) * (s.ny + 1);
+      kt_begin(KF_ACC_FACES);
+      k_uni_acc_faces<<<nblk(nf, 256), 256, 0, st>>>(v, nv, s.clk.p, s.red.p, s.hydro.p, s.u.p, s.aqx.p,
+                                                      s.aqy.p, manual, mdt);
+      FM_LAUNCHED();
+      kt_end();
+      kt_begin(KF_ACC_LEAVES);
+      k_uni_acc_cells<<<nblk(s.n, 256), 256, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, s.aqx.p, s.aqy.p,
+                                                       manual, mdt);
+      FM_LAUNCHED();
+      kt_end();
+      break;
+    }
+    case OP_HEAD:
+      if (!manual) launch_decide(s);
+      launch_head_friction(s, fv1 ? s.us.p : s.u.p, s.u.p, manual, mdt);
+      break;
+    case OP_STAGE1:
+      kt_begin(KF_UNI_STAGE1);
+      if (s.p2)
+        k_uni_stage<1, true><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, fv1 ? 1 : 0, manual, mdt, err);
+      else
+        k_uni_stage<1, false><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, fv1 ? 1 : 0, manual, mdt, err);
+      FM_LAUNCHED();
+      kt_end();
+      break;
+    case OP_STAGE2:
+      kt_begin(KF_UNI_STAGE2);
+      if (s.p2)
+        k_uni_stage<2, true><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+      else
+        k_uni_stage<2, false><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+      FM_LAUNCHED();
+      kt_end();
+      break;
+    case OP_COMMIT:
+      launch_commit(s);
+      break;
+    default:
+      break;
   }
-  if (!manual) launch_commit(s);
+}
+
+void un_launch_step(Sim& s, bool manual, double mdt, int* err) {
+  for (int op : nu_step_ops(s, manual)) {
+    if (op == OP_EXCH_U || op == OP_EXCH_US || op == OP_REDUCE) {
+      if (s.shard) shard_op(s, op);
+    } else {
+      un_step_op(s, op, manual, mdt, err);
+    }
+  }
 }
 
 void un_launch_inflow_add(Sim& s, const double* per_cell_dev) {
@@ -569,7 +607,7 @@ void un_launch_inflow_add(Sim& s, const double* per_cell_dev) {
 }
 
 void un_launch_reduce_init(Sim& s) {
-  k_uni_reduce_init<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.nx, s.clk.p, s.red.p, s.u.p);
+  k_uni_reduce_init<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.nx, s.gy0, s.clk.p, s.red.p, s.u.p);
   FM_LAUNCHED();
 }
 

@@ -8,6 +8,7 @@ two gloo ranks (world_size 2), exactly the messages the NCCL path sends.
 GPU: a local group of R shards on one device stepped by fm_group_run ends in
 the same state bits as the unsharded sim (DG2, FV1, ACC; rain and point
 sources; R = 2, 3)."""
+import dataclasses
 import os
 import socket
 
@@ -206,15 +207,45 @@ def test_local_group_matches_unsharded_bit_exact(gpu, name, nranks):
 
 
 @pytest.mark.gpu
-def test_shard_rejects_adaptive_and_uniform(gpu):
+def test_shard_rejects_adaptive(gpu):
     from paper_2107_02750_b200.abi import FmError
     comm = gpu.comm_local(2)
-    sc = S.config2(8)  # HWFV1
+    sc = S.config2(8)  # HWFV1: re-grids every step, replicas only
     with pytest.raises(FmError):
         gpu.shard_sim(sc, None, comm, 0)
-    sc = S.config4(64, uniform=True)
-    with pytest.raises(FmError):
-        gpu.shard_sim(sc, None, comm, 0)
+
+
+UNIFORM_CASES = {
+    "c4_uniform_dg2_rain_s32": (lambda: S.config4(32, uniform=True), 20),
+    "c0_uniform_dg2_s4": (lambda: dataclasses.replace(S.config0(4), grid_mode="uniform"), 25),
+    "c1_uniform_acc_s8": (lambda: dataclasses.replace(S.config1(8), grid_mode="uniform"), 30),
+    "c2_uniform_fv1_s8": (lambda: dataclasses.replace(S.config2(8, adaptive=False),
+                                                      grid_mode="uniform"), 30),
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("name", list(UNIFORM_CASES))
+def test_uniform_bands_match_unsharded_bit_exact(gpu, name, nranks):
+    """Row-band shards of the uniform raster (one ghost row each side)."""
+    mk, steps = UNIFORM_CASES[name]
+    sc = mk()
+    ref = gpu.sim(sc, None)
+    ck_a, ra = ref.run(steps, gauge_interval=10.0)
+    comm = gpu.comm_local(nranks)
+    shards = [gpu.shard_sim(sc, None, comm, r) for r in range(nranks)]
+    info = [s.shard_info() for s in shards]
+    assert sum(x["owned"] for x in info) == ref.num_cells
+    ck_b, rb = gpu.group_run(shards, steps, gauge_interval=10.0)
+    assert (ra.steps, ra.dt_min, ra.dt_max, ck_a.now) == (rb.steps, rb.dt_min, rb.dt_max, ck_b.now)
+    a = ref.download()
+    parts = [s.download() for s in shards]  # j-major bands in rank order
+    for k in range(5):
+        assert np.array_equal(a[k], np.concatenate([p[k] for p in parts]))
+    # rasters: the bands stack (row 0 north: the last band first)
+    full = ref.raster(0)
+    assert np.array_equal(full, np.concatenate([s.raster(0) for s in shards[::-1]]))
 
 
 @pytest.mark.gpu
