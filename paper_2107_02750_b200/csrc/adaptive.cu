@@ -526,9 +526,9 @@ void adaptive_adapt(Sim& s, double t) {
   }
   refresh_topology(s);
   s.fv1_in_star = false;
-  if (s.graph) {
-    cudaGraphExecDestroy(s.graph);
-    s.graph = nullptr;
+  for (auto& g : s.gexec) {
+    if (g) cudaGraphExecDestroy(g);
+    g = nullptr;
   }
   FM_CUDA(cudaStreamSynchronize(st));
   s.element_log.emplace_back(t, s.n);

@@ -139,6 +139,13 @@ std::vector<int64_t> reference_order(const Grid& g, std::vector<int8_t>* l = nul
 
 double elapsed_ms(cudaEvent_t a, cudaEvent_t b);
 
+// Launch helper for the step chain (a plain launch + error check).
+template <typename... KArgs, typename... Args>
+void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  k<<<grid, block, 0, st>>>(static_cast<KArgs>(args)...);
+  FM_CUDA(cudaGetLastError());
+}
+
 // Optional per-launch timing for fm_sim_profile: when on, every kernel launch
 // of a step is bracketed by CUDA events on the library stream.
 enum KernelFamily {
@@ -153,6 +160,7 @@ enum KernelFamily {
   KF_UNI_STAGE2,  // uniform raster: stage 2
   KF_SEG1,        // segment states, stage 1
   KF_SEG2,        // segment states, stage 2
+  KF_DECIDE,      // the one-thread step decision
   KF_COUNT
 };
 const char* kernel_family_name(int f);

@@ -140,10 +140,9 @@ struct Sim {
   int adapt_every = 1;
   int64_t since_adapt = 0;
   std::vector<std::pair<double, int64_t>> element_log;
-  // CUDA graph of a batch of steps
-  cudaGraphExec_t graph = nullptr;
-  int graph_steps = 0;
-  int64_t graph_kernels = 0;
+  // CUDA graphs of 32, 8 and 1 device-loop steps (sim_run)
+  cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};
+  int64_t gkern[3] = {0, 0, 0};
   std::unique_ptr<Shard> shard;  // set for a sharded (multi-rank) static sim
   // device order -> reference (level, j, i) order, cached per leaf set (order.cu)
   DBuf<int32_t> ref_perm;

@@ -548,6 +548,8 @@ inline unsigned nblk(long long n, int t) { return unsigned((n + t - 1) / t); }
 
 }  // namespace
 
+void launch_decide(Sim& s);
+
 // ---- launch helpers used by sim.cu --------------------------------------------
 // A step is a fixed sequence of operations (StepOp): device phases plus, for a
 // sharded sim, the halo exchanges of the state a phase is about to gather and
@@ -584,18 +586,15 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
   auto seg = [&](int fam, const double* in) {
     kt_begin(fam);
     if (s.p2)
-      k_seg<true><<<nblk(ns, 256), 256, 0, st>>>(v, clk, in, s.segst.p, manual, err);
+      launch_k(k_seg<true>, nblk(ns, 256), 256, st, v, (const DevClock*)clk, in, s.segst.p, (int)manual, err);
     else
-      k_seg<false><<<nblk(ns, 256), 256, 0, st>>>(v, clk, in, s.segst.p, manual, err);
+      launch_k(k_seg<false>, nblk(ns, 256), 256, st, v, (const DevClock*)clk, in, s.segst.p, (int)manual, err);
     FM_LAUNCHED();
     kt_end();
   };
   switch (op) {
     case OP_ACC:
-      if (!manual) {
-        k_decide<<<1, 1, 0, st>>>(v, clk, red, s.hydro.p);
-        FM_LAUNCHED();
-      }
+      if (!manual) launch_decide(s);
       kt_begin(KF_ACC_FACES);
       k_acc_faces<<<nblk(ns, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.u.p, s.accq.p, manual, mdt);
       FM_LAUNCHED();
@@ -606,14 +605,11 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       kt_end();
       break;
     case OP_HEAD:
-      if (!manual) {
-        k_decide<<<1, 1, 0, st>>>(v, clk, red, s.hydro.p);
-        FM_LAUNCHED();
-      }
+      if (!manual) launch_decide(s);
       // FV1 keeps its state in U* between steps; the head moves it to U with friction
       kt_begin(KF_HEAD);
-      k_head_friction<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, fv1 ? s.us.p : s.u.p, s.u.p,
-                                                    manual, mdt);
+      launch_k(k_head_friction, nblk(n, 256), 256, st, v, clk, red, (const Hydro*)s.hydro.p,
+                 (const double*)(fv1 ? s.us.p : s.u.p), s.u.p, (int)manual, mdt);
       FM_LAUNCHED();
       kt_end();
       break;
@@ -622,9 +618,9 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       kt_begin(KF_STAGE1);
       const int last1 = fv1 ? 1 : 0;
       if (s.p2)
-        k_stage<1, true><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, last1, manual, mdt, err);
+        launch_k(k_stage<1, true>, nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, st, v, (const DevClock*)clk, red, (const double*)s.u.p, (const double*)nullptr, s.us.p, last1, (int)manual, mdt, err);
       else
-        k_stage<1, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.u.p, nullptr, s.us.p, last1, manual, mdt, err);
+        launch_k(k_stage<1, false>, nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, st, v, (const DevClock*)clk, red, (const double*)s.u.p, (const double*)nullptr, s.us.p, last1, (int)manual, mdt, err);
       FM_LAUNCHED();
       kt_end();
       break;
@@ -633,15 +629,15 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       seg(KF_SEG2, s.us.p);
       kt_begin(KF_STAGE2);
       if (s.p2)
-        k_stage<2, true><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+        launch_k(k_stage<2, true>, nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
       else
-        k_stage<2, false><<<nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, 0, st>>>(v, clk, red, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+        launch_k(k_stage<2, false>, nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
       FM_LAUNCHED();
       kt_end();
       break;
     case OP_COMMIT:
       kt_begin(KF_COMMIT);
-      k_commit<<<1, 1, 0, st>>>(clk);
+      launch_k(k_commit, 1, 1, st, clk);
       FM_LAUNCHED();
       kt_end();
       break;
@@ -661,8 +657,10 @@ void nu_launch_step(Sim& s, bool manual, double mdt, int* err) {
 }
 
 void launch_decide(Sim& s) {
-  k_decide<<<1, 1, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.hydro.p);
+  kt_begin(KF_DECIDE);
+  launch_k(k_decide, 1, 1, stream(), s.view(), s.clk.p, s.red.p, (const Hydro*)s.hydro.p);
   FM_LAUNCHED();
+  kt_end();
 }
 
 void launch_head_friction(Sim& s, const double* src, double* dst, bool manual, double mdt) {

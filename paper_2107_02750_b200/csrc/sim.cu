@@ -111,7 +111,8 @@ __global__ void k_finite(long long n, const int8_t* __restrict__ lvl, const int3
 
 Sim::~Sim() {
   if (shard && shard->comm) comm_forget(shard->comm, this);
-  if (graph) cudaGraphExecDestroy(graph);
+  for (auto& g : gexec)
+    if (g) cudaGraphExecDestroy(g);
   if (ad) adaptive_destroy(ad);
 }
 
@@ -589,24 +590,30 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
       }
     }
   } else {
-    constexpr int kBatch = 32;
-    const int64_t before = launches();
-    if (!s.graph) {
-      cudaGraph_t gr;
-      FM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      for (int k = 0; k < kBatch; ++k) launch_step(s, false, 0.0, err.p);
-      FM_CUDA(cudaStreamEndCapture(st, &gr));
-      FM_CUDA(cudaGraphInstantiate(&s.graph, gr, 0));
-      cudaGraphDestroy(gr);
-      s.graph_steps = kBatch;
-      s.graph_kernels = launches() - before;  // kernels per replay
-    }
+    // graphs of 32, 8 and 1 steps, captured on first use; the step count is
+    // covered greedily so no graph replays surplus (no-op) steps
+    static constexpr int kSizes[3] = {32, 8, 1};
+    auto graph_of = [&](int q) {
+      if (!s.gexec[q]) {
+        const int64_t before = launches();
+        cudaGraph_t gr;
+        FM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        for (int k = 0; k < kSizes[q]; ++k) launch_step(s, false, 0.0, err.p);
+        FM_CUDA(cudaStreamEndCapture(st, &gr));
+        FM_CUDA(cudaGraphInstantiate(&s.gexec[q], gr, 0));
+        cudaGraphDestroy(gr);
+        s.gkern[q] = launches() - before;  // kernels per replay
+      }
+      return s.gexec[q];
+    };
     int64_t done = 0;
     while (done < max_steps) {
-      FM_CUDA(cudaGraphLaunch(s.graph, st));
-      count_graph_launches(s.graph_kernels);
-      done += s.graph_steps;
-      if (done < max_steps) {
+      const int64_t rem = max_steps - done;
+      const int q = rem >= kSizes[0] ? 0 : rem >= kSizes[1] ? 1 : 2;
+      FM_CUDA(cudaGraphLaunch(graph_of(q), st));
+      count_graph_launches(s.gkern[q]);
+      done += kSizes[q];
+      if (q == 0 && done < max_steps) {
         DevClock c;
         s.clk.download(&c, 1);
         FM_CUDA(cudaStreamSynchronize(st));
