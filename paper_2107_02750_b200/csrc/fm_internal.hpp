@@ -152,7 +152,7 @@ enum KernelFamily {
   KF_HEAD = 0,    // step head + friction (DG2/FV1)
   KF_STAGE1,      // RK stage 1 (FV1: the whole update)
   KF_STAGE2,      // RK stage 2 + fused epilogue
-  KF_COMMIT,      // clock commit
+  KF_COMMIT,      // (unused: the clock needs no commit kernel)
   KF_ACC_FACES,   // ACC face discharges + step head
   KF_ACC_LEAVES,  // ACC leaf update + fused epilogue
   KF_UNI_HEAD,    // uniform raster: head + friction

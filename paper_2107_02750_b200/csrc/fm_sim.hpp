@@ -12,8 +12,9 @@ constexpr int kMaxInflows = 8;
 constexpr int kMaxHydroSamples = 4096;
 
 // Device copy of the EventClock (sim_common.hpp:31-45) plus the per-step
-// control block written by the step-head kernel.  clk[0] is the state at the
-// start of a step, clk[1] the state of the step in flight.
+// control block written by the step-decision kernel.  clk[1] is the published
+// state: k_decide reads it as the step-start state and replaces it with the
+// step in flight, which is the next step's start state.  clk[0] is unused.
 struct DevClock {
   double end_time, out_int, gauge_int, now;
   long long next_out, next_gauge;
@@ -70,7 +71,7 @@ struct NuView {
 };
 
 // Operations of one step (nu_step_ops in nu_flow.cu).
-enum StepOp { OP_HEAD, OP_EXCH_U, OP_STAGE1, OP_EXCH_US, OP_STAGE2, OP_ACC, OP_REDUCE, OP_COMMIT };
+enum StepOp { OP_HEAD, OP_EXCH_U, OP_STAGE1, OP_EXCH_US, OP_STAGE2, OP_ACC, OP_REDUCE };
 
 struct Comm;  // shard.cu: the transport between the ranks of a sharded sim
 

@@ -509,25 +509,21 @@ __global__ void k_reduce_init(NuView v, const DevClock* clk, DevRed* red, const 
     key = leaf_key(l, v.li[k], v.lj[k]);
     load9(u, k, s);
   }
-  DevClock c = clk[0];
+  DevClock c = clk[1];
   reduce_leaf(v, red, c, s, sz, key, valid);
 }
 
 // Close the last step of a run: the non-finite guard and event counters of
 // decide_step without starting a new step.
 __global__ void k_close(DevClock* clk, DevRed* red, const Hydro* hy, NuView v) {
-  DevClock c0 = clk[0];
+  DevClock c0 = clk[1];
   c0.max_steps = c0.steps;  // forbid a new step
   DevClock c;
   decide_step(c0, red[c0.steps & 1], hy, v.scheme, v.courant, v.g, v.hdry, v.ninflow, c);
-  c.max_steps = clk[0].max_steps;
-  clk[0] = c;
+  c.max_steps = clk[1].max_steps;
+  clk[1] = c;
 }
 
-__global__ void k_commit(DevClock* clk) {
-  // end of step: the in-flight state becomes the step-start state
-  clk[0] = clk[1];
-}
 
 // apply_inflows for the host API path.
 __global__ void k_inflow_add(NuView v, const double* per_cell, double* u) {
@@ -554,10 +550,11 @@ void launch_decide(Sim& s);
 // A step is a fixed sequence of operations (StepOp): device phases plus, for a
 // sharded sim, the halo exchanges of the state a phase is about to gather and
 // the cross-rank reduction of the next-step CFL / non-finite slot.
-//   DG2: HEAD  X(U)  STAGE1  X(U*)  STAGE2  REDUCE  COMMIT
-//   FV1: HEAD  X(U)  STAGE1  REDUCE  COMMIT
-//   ACC: X(U)  ACC  REDUCE  COMMIT
-// (manual host-API steps have no REDUCE / COMMIT).
+//   DG2: HEAD  X(U)  STAGE1  X(U*)  STAGE2  REDUCE
+//   FV1: HEAD  X(U)  STAGE1  REDUCE
+//   ACC: X(U)  ACC  REDUCE
+// (manual host-API steps have no REDUCE).  HEAD and ACC start with the
+// one-thread step decision (k_decide).
 std::vector<int> nu_step_ops(const Sim& s, bool manual) {
   std::vector<int> ops;
   if (s.scheme == FM_ACC) {
@@ -567,10 +564,7 @@ std::vector<int> nu_step_ops(const Sim& s, bool manual) {
   } else {
     ops = {OP_HEAD, OP_EXCH_U, OP_STAGE1, OP_EXCH_US, OP_STAGE2};
   }
-  if (!manual) {
-    ops.push_back(OP_REDUCE);
-    ops.push_back(OP_COMMIT);
-  }
+  if (!manual) ops.push_back(OP_REDUCE);
   return ops;
 }
 
@@ -635,12 +629,6 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       FM_LAUNCHED();
       kt_end();
       break;
-    case OP_COMMIT:
-      kt_begin(KF_COMMIT);
-      launch_k(k_commit, 1, 1, st, clk);
-      FM_LAUNCHED();
-      kt_end();
-      break;
     default:
       break;
   }
@@ -671,12 +659,6 @@ void launch_head_friction(Sim& s, const double* src, double* dst, bool manual, d
   kt_end();
 }
 
-void launch_commit(Sim& s) {
-  kt_begin(KF_COMMIT);
-  k_commit<<<1, 1, 0, stream()>>>(s.clk.p);
-  FM_LAUNCHED();
-  kt_end();
-}
 
 void nu_launch_reduce_init(Sim& s) {
   k_reduce_init<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.u.p);

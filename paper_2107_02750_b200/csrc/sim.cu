@@ -397,6 +397,12 @@ DevClock fresh_clock(const fm_clock* c, int64_t max_steps, int stop) {
   return d;
 }
 
+// The device clock: clk[1] is the published state (the step-start state of
+// the next step once a step has been decided).
+void read_clock(Sim& s, DevClock& c) {
+  FM_CUDA(cudaMemcpyAsync(&c, s.clk.p + 1, sizeof(DevClock), cudaMemcpyDeviceToHost, stream()));
+}
+
 void key_xy(const Sim& s, unsigned long long key, double* bx, double* by) {
   const int l = int(key >> 58), j = int((key >> 29) & ((1u << 29) - 1)), i = int(key & ((1u << 29) - 1));
   if (s.uniform) {
@@ -413,8 +419,8 @@ void key_xy(const Sim& s, unsigned long long key, double* bx, double* by) {
 double sim_compute_dt(Sim& s) {
   if (fv1_staged(s)) fv1_to_u(s);
   init_red(s);
-  DevClock c{};
-  s.clk.upload(&c, 1);  // steps = 0 -> slot 0
+  DevClock pair0[2] = {};
+  s.clk.upload(pair0, 2);  // steps = 0 -> slot 0
   launch_reduce_init(s);
   DevRed r[2];
   s.red.download(r, 2);
@@ -567,7 +573,7 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
     for (int64_t k = 0; k < max_steps; ++k) {
       launch_step(s, false, 0.0, err.p);
       DevClock c;
-      s.clk.download(&c, 1);
+      read_clock(s, c);
       FM_CUDA(cudaStreamSynchronize(st));
       if (!c.active || !c.had_step) break;
       s.since_adapt += 1;
@@ -615,7 +621,7 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
       done += kSizes[q];
       if (q == 0 && done < max_steps) {
         DevClock c;
-        s.clk.download(&c, 1);
+        read_clock(s, c);
         FM_CUDA(cudaStreamSynchronize(st));
         if (!c.active) break;
       }
@@ -624,7 +630,7 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
   FM_CUDA(cudaEventRecord(e1, st));
   nu_launch_close(s);
   DevClock c;
-  s.clk.download(&c, 1);
+  read_clock(s, c);
   int herr = 0;
   err.download(&herr, 1);
   FM_CUDA(cudaStreamSynchronize(st));
@@ -695,7 +701,7 @@ void group_run(const std::vector<Sim*>& sims, fm_clock* ck, int64_t max_steps, i
       }
     }
     DevClock c;
-    sims[0]->clk.download(&c, 1);
+    read_clock(*sims[0], c);
     FM_CUDA(cudaStreamSynchronize(st));
     if (!c.active) break;
   }
@@ -709,7 +715,7 @@ void group_run(const std::vector<Sim*>& sims, fm_clock* ck, int64_t max_steps, i
     herr |= h;
   }
   DevClock c;
-  sims[0]->clk.download(&c, 1);
+  read_clock(*sims[0], c);
   FM_CUDA(cudaStreamSynchronize(st));
   for (Sim* s : sims) s->last_run_ms = elapsed_ms(e0, e1);
   cudaEventDestroy(e0);

@@ -167,7 +167,7 @@ __device__ bool decide_step(const DevClock& c0, const DevRed& r, const Hydro* hy
 // accumulates into.  The step's kernels then only read clk[1].
 __device__ __forceinline__ void decide_publish(const NuView& v, DevClock* clk, DevRed* red,
                                                const Hydro* hy) {
-  const DevClock c0 = clk[0];
+  const DevClock c0 = clk[1];  // the last published state
   const int p = int(c0.steps & 1);
   DevClock c;
   const bool g = decide_step(c0, red[p], hy, v.scheme, v.courant, v.g, v.hdry, v.ninflow, c);

@@ -27,7 +27,6 @@ namespace fmh {
 
 void launch_head_friction(Sim& s, const double* src, double* dst, bool manual, double mdt);
 void launch_decide(Sim& s);
-void launch_commit(Sim& s);
 void project_planes_rowmajor(const fm_raster* r, DBuf<double>& out);
 
 namespace {
@@ -358,7 +357,7 @@ __global__ void k_uni_reduce_init(NuView nv, int nx, int gy0, const DevClock* cl
     j = gy0 + int(k / nx);
     i = int(k % nx);
   }
-  DevClock c = clk[0];
+  DevClock c = clk[1];
   reduce_leaf(nv, red, c, s, nv.R, leaf_key(0, i, j), valid);
 }
 
@@ -582,9 +581,6 @@ void un_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
         k_uni_stage<2, false><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
       FM_LAUNCHED();
       kt_end();
-      break;
-    case OP_COMMIT:
-      launch_commit(s);
       break;
     default:
       break;
