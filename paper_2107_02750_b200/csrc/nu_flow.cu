@@ -2,39 +2,30 @@
 //
 // Replaces NonUniformSim::step_rk / step_acc / compute_dt / apply_inflows /
 // finite_state (solver_nonuniform.cpp:306-487) and the drive-loop body
-// (run.cpp:80-111).  One thread per leaf, leaves in Morton order:
+// (run.cpp:80-111).  Leaves in Morton order; per DG2 step:
 //
-//   k_head_friction  step head: next dt from the previous step's reduction
-//                    (compute_dt :427-449 + EventClock::clip), clock advance,
-//                    then Manning friction (sim_common.cpp:30-46) in place.
-//   k_stage<1>       segment HLL + side-effective states + L operator + Euler
-//                    update + positivity for every leaf, gathering its
-//                    neighbours (segment_states :91-115, side_effective
-//                    :117-178, assemble :180-274, positivity :276-304).
-//   k_stage<2>       the same on U*, RK2 average, then (fused epilogue) the
+//   k_decide         the step decision (compute_dt :427-449 + EventClock::clip
+//                    from the previous step's reduction), one thread.
+//   k_head_friction  Manning friction (sim_common.cpp:30-46) in place.
+//   k_seg            one thread per interior segment: segment_states
+//                    (:91-115), the HLL flux of every face solved once.
+//   k_stage<1>       one thread per leaf: side-effective states from the
+//                    segment states, assemble, L operator, Euler update,
+//                    positivity (:117-304).
+//   k_seg, k_stage<2>  the same on U*, RK2 average, then (fused epilogue) the
 //                    inflow sources, the non-finite guard and the CFL
 //                    reduction for the next step.
 //   k_acc_faces / k_acc_leaves   ACC (step_acc :350-418).
 //
-// There is no segment scratch for DG2/FV1: each leaf evaluates the HLL flux
-// of every sub-face on its own sides.  A face shared by two leaves is
-// evaluated by both, from identical inputs in identical order, so both see
-// the same bits; in exchange no 48 B/segment state round-trips through HBM
-// and a whole RK stage is one launch.  All sums are gathers in the
-// reference's order (sides N,E,S,W; sub-faces south-to-north / west-to-east),
-// never floating-point atomics, so results do not depend on scheduling.
+// All sums are gathers in the reference's order (sides N,E,S,W; sub-faces
+// south-to-north / west-to-east), never floating-point atomics, so results
+// do not depend on scheduling.
 #include "fm_device.cuh"
 #include "fm_sim.hpp"
 #include "step_common.cuh"
 
 // minimum resident CTAs per SM (register caps; tuned on B200 with
 // scripts/ab_profile.py)
-#ifndef FM_STAGE1_MINB
-#define FM_STAGE1_MINB 8
-#endif
-#ifndef FM_STAGE2_MINB
-#define FM_STAGE2_MINB 8
-#endif
 #ifndef FM_SEG_MINB
 #define FM_SEG_MINB 1
 #endif
@@ -158,44 +149,24 @@ __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClo
 // STAGE 1: out = positivity(U + dt L(U))               -> U*  (FV1: the full step)
 // STAGE 2: out = positivity(((U* + dt L(U*)) + U) / 2) -> U (in place)
 //
-// Four threads per leaf, one per side (N, E, S, W): each evaluates its side's
-// limit (limit_at, solver_nonuniform.cpp:52-66), the HLL flux of each
-// sub-face on that side (segment_states :91-115), the side-effective starred
-// state (side_effective :117-178) and the side's flux sum with the pressure
-// correction (assemble :190-226).  The four sides' results meet in shared
-// memory; the four Gauss-point physical fluxes of the L operator are split
-// over the four lanes; then every lane forms the full update (cheap) and
-// stores a third of the leaf's 9 coefficients, so a warp writes 8 leaves'
-// 576 contiguous bytes.
-constexpr int kLeavesPerBlock = 32;
-
+// One thread per leaf takes its four sides in turn (E, W, then N, S): the
+// side's face limit (limit_at, solver_nonuniform.cpp:52-66), the
+// side-effective starred state from the side's segment states
+// (side_effective :117-178), the side's flux sum with the pressure correction
+// (assemble :190-226); then the Gauss-point physical fluxes, the L operator,
+// the update and positivity.  (A four-threads-per-leaf layout with the sides
+// meeting in shared memory measured 1.6x slower on B200: the per-lane
+// redundant update and the exchange cost more than the parallel sides gain.)
 struct SideOut {
   double h, qx, qy, zd, fm, fn, ft;
 };
 
-template <int STAGE, bool P2>
-__global__ void __launch_bounds__(4 * kLeavesPerBlock, STAGE == 2 ? FM_STAGE2_MINB : FM_STAGE1_MINB) k_stage(
-    NuView v, const DevClock* __restrict__ clk, DevRed* red, const double* __restrict__ in,
-    const double* uold, double* out, int last, int manual, double mdt, int* err) {
-  __shared__ SideOut so[kLeavesPerBlock][4];
-  __shared__ double pf[kLeavesPerBlock][4][3];
-  const int sd = threadIdx.x & 3;
-  const int lq = threadIdx.x >> 2;
-  const long long k = blockIdx.x * (long long)kLeavesPerBlock + lq;
-  const DevClock* c = clk + 1;
-  if (!manual && !c->active) return;
-  const double dt = manual ? mdt : c->dt;
-  const bool valid = k < v.n;
-  const long long kk = valid ? k : v.n - 1;  // keep the quad's loads in bounds
-  const int l = v.lvl[kk], i = v.li[kk], j = v.lj[kk];
-  const double sz = lsize(v, l);
-  const double inv = v.linv[l];
-  const double cx = P2 ? 0.0 : lcen(v.x0, v, l, i), cy = P2 ? 0.0 : lcen(v.y0, v, l, j);
-  double s[9];
-  load9(in, kk, s);
-  const P3 zc = load3(v.z, kk);
-  const int kind = (v.sk[kk] >> (2 * sd)) & 3;
-  // issue the dependent gathers early: segment ids -> segment states
+template <bool P2>
+__device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9], const P3& zc,
+                                             long long kk, int sd, int kind, double cx, double cy,
+                                             double sz, int* err) {
+  const bool xn = sd == 1 || sd == 3;
+  const bool mine_left = sd == 0 || sd == 1;
   const int nseg = kind == 0 ? 0 : kind == 3 ? 2 : 1;
   double sg[2][6];
 #pragma unroll
@@ -206,96 +177,111 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock, STAGE == 2 ? FM_STAGE2_MI
       for (int e = 0; e < 6; ++e) sg[t][e] = q[e];
     }
   }
-  double u0[9];  // stage 2: the step-start state, loaded late (fewer live registers)
-#ifdef FM_U0_EARLY
-  if (STAGE == 2) load9(uold, kk, u0);
-#endif
-  const bool xn = sd == 1 || sd == 3;
-  const bool mine_left = sd == 0 || sd == 1;
-  {
-    // ---- this lane's side -------------------------------------------------
-    const double ox = sd == 1 ? 0.5 : sd == 3 ? -0.5 : 0.0;
-    const double oy = sd == 0 ? 0.5 : sd == 2 ? -0.5 : 0.0;
-    const double fx = P2 ? 0.0 : cx + (sd == 1 ? sz / 2 : sd == 3 ? -sz / 2 : 0.0);
-    const double fy = P2 ? 0.0 : cy + (sd == 0 ? sz / 2 : sd == 2 ? -sz / 2 : 0.0);
-    const Pt me = P2 ? limit_rel(s, zc, ox, oy, v.hdry) : limit(s, zc, cx, cy, sz, fx, fy, v.hdry);
-    // the side's segments (segment_states, solver_nonuniform.cpp:91-115,
-    // computed once per segment by k_seg); the weight len/sz is exactly 1/2
-    // for two finer neighbours and 1 otherwise (sizes are R * 2^k).
-    const double w = kind == 3 ? 0.5 : 1.0;
-    double zstar;
-    if (kind == 0) {
-      zstar = me.z;
-    } else if (nseg == 1) {
-      zstar = sg[0][3];
-    } else if (v.zpair) {
-      zstar = smax(me.z, v.zpair[4 * kk + sd]);
-    } else {
-      double acc = 0.0;
-      acc += w * sg[0][3];
-      acc += w * sg[1][3];
-      zstar = acc;
-    }
-    SideOut o;
-    const double h = smax(0.0, me.eta - zstar);
-    o.h = h;
-    o.qx = h * me.u;
-    o.qy = h * me.v;
-    o.zd = zstar - smax(0.0, zstar - me.eta);
-    Flx acc{0.0, 0.0, 0.0};
-    if (kind == 0) {
-      const double qn = xn ? o.qx : o.qy, qt = xn ? o.qy : o.qx;
-      const double qg = v.bc[sd] == FM_REFLECTIVE ? -qn : qn;
-      const Flx f = mine_left ? hll(h, qn, qt, h, qg, qt, v.g, v.hdry, err)
-                              : hll(h, qg, qt, h, qn, qt, v.g, v.hdry, err);
-      acc.m += f.m;
-      acc.n += f.n;
-      acc.t += f.t;
-    } else {
+  const double ox = sd == 1 ? 0.5 : sd == 3 ? -0.5 : 0.0;
+  const double oy = sd == 0 ? 0.5 : sd == 2 ? -0.5 : 0.0;
+  const double fx = P2 ? 0.0 : cx + (sd == 1 ? sz / 2 : sd == 3 ? -sz / 2 : 0.0);
+  const double fy = P2 ? 0.0 : cy + (sd == 0 ? sz / 2 : sd == 2 ? -sz / 2 : 0.0);
+  const Pt me = P2 ? limit_rel(s, zc, ox, oy, v.hdry) : limit(s, zc, cx, cy, sz, fx, fy, v.hdry);
+  const double w = kind == 3 ? 0.5 : 1.0;
+  double zstar;
+  if (kind == 0) {
+    zstar = me.z;
+  } else if (nseg == 1) {
+    zstar = sg[0][3];
+  } else if (v.zpair) {
+    zstar = smax(me.z, v.zpair[4 * kk + sd]);
+  } else {
+    double acc = 0.0;
+    acc += w * sg[0][3];
+    acc += w * sg[1][3];
+    zstar = acc;
+  }
+  SideOut o;
+  const double h = smax(0.0, me.eta - zstar);
+  o.h = h;
+  o.qx = h * me.u;
+  o.qy = h * me.v;
+  o.zd = zstar - smax(0.0, zstar - me.eta);
+  Flx acc{0.0, 0.0, 0.0};
+  if (kind == 0) {
+    const double qn = xn ? o.qx : o.qy, qt = xn ? o.qy : o.qx;
+    const double qg = v.bc[sd] == FM_REFLECTIVE ? -qn : qn;
+    const Flx f = mine_left ? hll(h, qn, qt, h, qg, qt, v.g, v.hdry, err)
+                            : hll(h, qg, qt, h, qn, qt, v.g, v.hdry, err);
+    acc.m += f.m;
+    acc.n += f.n;
+    acc.t += f.t;
+  } else {
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        if (t < nseg) {
-          const double hme = mine_left ? sg[t][4] : sg[t][5];
-          const double corr = 0.5 * v.g * (h * h - hme * hme);
-          acc.m += w * sg[t][0];
-          acc.n += w * (sg[t][1] + corr);
-          acc.t += w * sg[t][2];
-        }
+    for (int t = 0; t < 2; ++t) {
+      if (t < nseg) {
+        const double hme = mine_left ? sg[t][4] : sg[t][5];
+        const double corr = 0.5 * v.g * (h * h - hme * hme);
+        acc.m += w * sg[t][0];
+        acc.n += w * (sg[t][1] + corr);
+        acc.t += w * sg[t][2];
       }
     }
-    o.fm = acc.m;
-    o.fn = acc.n;
-    o.ft = acc.t;
-    so[lq][sd] = o;
   }
-  __syncwarp();
-  const SideOut en = so[lq][0], ee = so[lq][1], es = so[lq][2], ew = so[lq][3];
+  o.fm = acc.m;
+  o.fn = acc.n;
+  o.ft = acc.t;
+  return o;
+}
+
+// 64-thread CTAs, >= 8 resident per SM (a 128-register cap): tuned by A/B on
+// B200 (scripts/ab_profile.py)
+#ifndef FM_STAGE_THREADS
+#define FM_STAGE_THREADS 64
+#endif
+#ifndef FM_STAGE_MINB
+#define FM_STAGE_MINB 8
+#endif
+
+template <int STAGE, bool P2>
+__global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
+    NuView v, const DevClock* __restrict__ clk, DevRed* red, const double* __restrict__ in,
+    const double* uold, double* out, int last, int manual, double mdt, int* err) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const DevClock* c = clk + 1;
+  if (!manual && !c->active) return;
+  const double dt = manual ? mdt : c->dt;
+  const bool valid = k < v.n;
+  const long long kk = valid ? k : v.n - 1;
+  const int l = v.lvl[kk], i = v.li[kk], j = v.lj[kk];
+  const double sz = lsize(v, l);
+  const double inv = v.linv[l];
+  const double cx = P2 ? 0.0 : lcen(v.x0, v, l, i), cy = P2 ? 0.0 : lcen(v.y0, v, l, j);
+  double s[9];
+  load9(in, kk, s);
+  const P3 zc = load3(v.z, kk);
+  const int code = v.sk[kk];
+  const bool dg2 = v.scheme == FM_DG2;
+  // x direction: E and W sides, then the Gauss-point fluxes along x
+  const SideOut ee = side_eval<P2>(v, s, zc, kk, 1, (code >> 2) & 3, cx, cy, sz, err);
+  const SideOut ew = side_eval<P2>(v, s, zc, kk, 3, (code >> 6) & 3, cx, cy, sz, err);
   const DirMod X{0.5 * (ee.h + ew.h),   (ee.h - ew.h) * kHalfInvS3,   0.5 * (ee.qx + ew.qx),
                  (ee.qx - ew.qx) * kHalfInvS3, 0.5 * (ee.qy + ew.qy), (ee.qy - ew.qy) * kHalfInvS3,
                  (ee.zd - ew.zd) * kHalfInvS3};
+  double xp[3] = {0, 0, 0}, xm[3] = {0, 0, 0};
+  if (dg2) {
+    phys_x(X.h0 + X.h1, X.qx0 + X.qx1, X.qy0 + X.qy1, v.g, v.hdry, xp[0], xp[1], xp[2]);
+    phys_x(X.h0 - X.h1, X.qx0 - X.qx1, X.qy0 - X.qy1, v.g, v.hdry, xm[0], xm[1], xm[2]);
+  }
+  const Flx fe{ee.fm, ee.fn, ee.ft}, fw{ew.fm, ew.fn, ew.ft};
+  // y direction
+  const SideOut en = side_eval<P2>(v, s, zc, kk, 0, code & 3, cx, cy, sz, err);
+  const SideOut es = side_eval<P2>(v, s, zc, kk, 2, (code >> 4) & 3, cx, cy, sz, err);
   const DirMod Y{0.5 * (en.h + es.h),   (en.h - es.h) * kHalfInvS3,   0.5 * (en.qx + es.qx),
                  (en.qx - es.qx) * kHalfInvS3, 0.5 * (en.qy + es.qy), (en.qy - es.qy) * kHalfInvS3,
                  (en.zd - es.zd) * kHalfInvS3};
-  const bool dg2 = v.scheme == FM_DG2;
+  double yp[3] = {0, 0, 0}, ym[3] = {0, 0, 0};
   if (dg2) {
-    // the four Gauss-point physical fluxes (solver_nonuniform.cpp:245-266), one per lane
-    double a, b, cc;
-    if (sd == 0)
-      phys_x(X.h0 + X.h1, X.qx0 + X.qx1, X.qy0 + X.qy1, v.g, v.hdry, a, b, cc);
-    else if (sd == 1)
-      phys_x(X.h0 - X.h1, X.qx0 - X.qx1, X.qy0 - X.qy1, v.g, v.hdry, a, b, cc);
-    else if (sd == 2)
-      phys_y(Y.h0 + Y.h1, Y.qx0 + Y.qx1, Y.qy0 + Y.qy1, v.g, v.hdry, a, b, cc);
-    else
-      phys_y(Y.h0 - Y.h1, Y.qx0 - Y.qx1, Y.qy0 - Y.qy1, v.g, v.hdry, a, b, cc);
-    pf[lq][sd][0] = a;
-    pf[lq][sd][1] = b;
-    pf[lq][sd][2] = cc;
-    __syncwarp();
+    phys_y(Y.h0 + Y.h1, Y.qx0 + Y.qx1, Y.qy0 + Y.qy1, v.g, v.hdry, yp[0], yp[1], yp[2]);
+    phys_y(Y.h0 - Y.h1, Y.qx0 - Y.qx1, Y.qy0 - Y.qy1, v.g, v.hdry, ym[0], ym[1], ym[2]);
   }
+  const Flx fn{en.fm, en.fn, en.ft}, fs{es.fm, es.fn, es.ft};
   // L operator (solver_nonuniform.cpp:228-271)
-  const Flx fn{en.fm, en.fn, en.ft}, fe{ee.fm, ee.fn, ee.ft}, fs{es.fm, es.fn, es.ft},
-      fw{ew.fm, ew.fn, ew.ft};
   double Lr[9];
   Lr[0] = div_sz<P2>(-((fe.m - fw.m) + (fn.m - fs.m)), sz, inv);
   Lr[3] = div_sz<P2>(-((fe.n - fw.n) + (fn.t - fs.t)), sz, inv) -
@@ -304,10 +290,6 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock, STAGE == 2 ? FM_STAGE2_MI
           div_sz<P2>(v.g * Y.h0 * (2.0 * kS3 * Y.z1), sz, inv);
   if (dg2) {
     const double kk3 = P2 ? kS3 * inv : kS3 / sz;
-    const double* xp = pf[lq][0];
-    const double* xm = pf[lq][1];
-    const double* yp = pf[lq][2];
-    const double* ym = pf[lq][3];
     Lr[1] = -kk3 * (fe.m + fw.m - xp[0] - xm[0]);
     Lr[4] = -kk3 * (fe.n + fw.n - xp[1] - xm[1]) - div_sz<P2>(v.g * X.h1 * (2.0 * kS3 * X.z1), sz, inv);
     Lr[7] = -kk3 * (fe.t + fw.t - xp[2] - xm[2]);
@@ -322,9 +304,8 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock, STAGE == 2 ? FM_STAGE2_MI
 #pragma unroll
     for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
   } else {
-#ifndef FM_U0_EARLY
+    double u0[9];
     load9(uold, kk, u0);
-#endif
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
       double a = s[q];
@@ -336,62 +317,20 @@ __global__ void __launch_bounds__(4 * kLeavesPerBlock, STAGE == 2 ? FM_STAGE2_MI
   }
   positivity(res, v.hdry);
   const bool epi = last && !manual;
-  if (!epi) {
-    if (valid) {
-      double* o = out + 9 * kk;
-      // lane sd stores components sd, sd + 4, sd + 8 (coalesced over the warp)
-      o[sd] = res[sd];
-      o[sd + 4] = res[sd + 4];
-      if (sd == 0) o[8] = res[8];
-    }
-    return;
-  }
-  // ---- fused epilogue: inflows, finite guard, next-step CFL ------------------
-  // Lanes store and check their own components; h.c0 (which the inflows
-  // modify) and the CFL of all 32 leaves are then handled by warp 0 alone, so
-  // the divisions and the reduction run once per leaf instead of on 4 lanes.
-  __shared__ double ep[kLeavesPerBlock][4];
-  if (valid) {
-    double* o = out + 9 * kk;
-    if (sd) o[sd] = res[sd];
-    o[sd + 4] = res[sd + 4];
-    if (sd == 0) o[8] = res[8];
-    const bool fin = (sd == 0 || isfinite(res[sd])) && isfinite(res[sd + 4]) &&
-                     (sd != 0 || isfinite(res[8]));
-    if (!fin) atomicMin(&red[c->steps & 1].badkey, leaf_key(l, i, j));
-  }
-  if (sd == 0) {
-    ep[lq][0] = res[0];
-    ep[lq][1] = res[3];
-    ep[lq][2] = res[6];
-    ep[lq][3] = sz;
-  }
-  __syncthreads();
-  if (threadIdx.x >= 32) return;
-  const int e = threadIdx.x;
-  const long long ke = blockIdx.x * (long long)kLeavesPerBlock + e;
-  double dtc = INFINITY;
-  if (ke < v.n) {
-    double h = ep[e][0];
-    const double sze = ep[e][3];
+  if (epi && valid) {
     // apply_inflows (solver_nonuniform.cpp:451-465), inflow order
     for (int f = 0; f < v.ninflow; ++f) {
       if (!c->on[f]) continue;
-      const int cnt = v.infc[f * v.n + ke];
-      if (cnt) h += ddiv(c->per_cell[f] * cnt, sze * sze);
-    }
-    out[9 * ke] = h;
-    if (!isfinite(h)) atomicMin(&red[c->steps & 1].badkey, leaf_key(v.lvl[ke], v.li[ke], v.lj[ke]));
-    // compute_dt (solver_nonuniform.cpp:427-449) candidate of this leaf
-    if (h > v.hdry) {
-      const double cw = sqrt(v.g * h);
-      const double sx = fabs(zdiv(ep[e][1], h)) + cw;
-      const double sy = fabs(zdiv(ep[e][2], h)) + cw;
-      dtc = ddiv(sze, smax(sx, sy));
+      const int cnt = v.infc[f * v.n + kk];
+      if (cnt) res[0] += ddiv(c->per_cell[f] * cnt, sz * sz);
     }
   }
-  for (int o = 16; o; o >>= 1) dtc = smin(dtc, __shfl_xor_sync(0xffffffffu, dtc, o));
-  if (e == 0 && dtc < INFINITY) atomicMin(&red[c->steps & 1].dtmin, dbits(dtc));
+  if (valid) {
+    double* o = out + 9 * kk;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) o[q] = res[q];
+  }
+  if (epi) reduce_leaf(v, red, *c, res, sz, leaf_key(l, i, j), valid);
 }
 
 // ---- ACC ------------------------------------------------------------------
@@ -612,9 +551,9 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       kt_begin(KF_STAGE1);
       const int last1 = fv1 ? 1 : 0;
       if (s.p2)
-        launch_k(k_stage<1, true>, nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, st, v, (const DevClock*)clk, red, (const double*)s.u.p, (const double*)nullptr, s.us.p, last1, (int)manual, mdt, err);
+        launch_k(k_stage<1, true>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.u.p, (const double*)nullptr, s.us.p, last1, (int)manual, mdt, err);
       else
-        launch_k(k_stage<1, false>, nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, st, v, (const DevClock*)clk, red, (const double*)s.u.p, (const double*)nullptr, s.us.p, last1, (int)manual, mdt, err);
+        launch_k(k_stage<1, false>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.u.p, (const double*)nullptr, s.us.p, last1, (int)manual, mdt, err);
       FM_LAUNCHED();
       kt_end();
       break;
@@ -623,9 +562,9 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       seg(KF_SEG2, s.us.p);
       kt_begin(KF_STAGE2);
       if (s.p2)
-        launch_k(k_stage<2, true>, nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
+        launch_k(k_stage<2, true>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
       else
-        launch_k(k_stage<2, false>, nblk(n, kLeavesPerBlock), 4 * kLeavesPerBlock, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
+        launch_k(k_stage<2, false>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
       FM_LAUNCHED();
       kt_end();
       break;
