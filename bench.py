@@ -300,20 +300,30 @@ def run_ours(args, ws, rank, local):
     barrier(ws)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    ph = {}
     g2 = lib.grid(sc_p.dem, sc_p.L, sc_p.eps)
+    ph["upload_mra"] = time.perf_counter()
     s2 = lib.shard_sim(sc_p, g2, comm, rank) if comm is not None else lib.sim(sc_p, g2)
+    ph["sim_create"] = time.perf_counter()
     ck2, r2 = s2.run(args.warmup, gauge_interval=10.0)
     s2.snapshot()
     ck0 = (ck2.end_time, ck2.output_interval, ck2.gauge_interval, ck2.now, ck2.next_output,
            ck2.next_gauge)
+    ph["warmup"] = time.perf_counter()
     done = 0
     while done < args.steps:
         n = min(args.chunk, args.steps - done)
         s2.restore()
         _, r2 = s2.run(n, clock=c_clock(*ck0))
         done += r2.steps
+    ph["steps"] = time.perf_counter()
     out = s2.download(out=outs)
+    ph["download"] = time.perf_counter()
     e2e_s = time.perf_counter() - t0
+    prev, phases = t0, {}
+    for k, v in ph.items():
+        phases[k] = round(1000.0 * (v - prev), 2)
+        prev = v
     e2e_s = allreduce_max(e2e_s, ws)
     h2d = sc.dem.values.nbytes + sc.manning_raster.values.nbytes
     d2h = sum(a.nbytes for a in out)
@@ -355,7 +365,7 @@ def run_ours(args, ws, rank, local):
                 "bytes": mra_bytes, "achieved_gbs": mra_bytes / (mra_ms / 1000.0) / 1e9,
                 "frac": mra_bytes / (mra_ms / 1000.0) / 1e9 / hbm},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
-                "d2h_bytes_per_step": d2h / e2e_steps, "seconds": e2e_s,
+                "d2h_bytes_per_step": d2h / e2e_steps, "seconds": e2e_s, "phases_ms": phases,
                 "what": "host DEM -> fm_mra_static -> fm_sim_create(_shard) -> W+K steps -> host state"},
         "uniform": uni,
         "gpu_launches": int(launches),
