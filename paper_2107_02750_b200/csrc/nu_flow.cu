@@ -27,7 +27,7 @@
 // minimum resident CTAs per SM (register caps; tuned on B200 with
 // scripts/ab_profile.py)
 #ifndef FM_SEG_MINB
-#define FM_SEG_MINB 1
+#define FM_SEG_MINB 4  // 64 registers: 4 CTAs of 256 threads per SM
 #endif
 
 using namespace fmd;
@@ -110,8 +110,10 @@ __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClo
     // centre lies on the face, at the finer (or either) leaf's centre along it
     const double ta = la < lb ? (((xn ? jb : ib) & 1) ? 0.25 : -0.25) : 0.0;
     const double tb = lb < la ? (((xn ? ja : ia) & 1) ? 0.25 : -0.25) : 0.0;
-    A = xn ? limit_rel(sa, za, 0.5, ta, v.hdry) : limit_rel(sa, za, ta, 0.5, v.hdry);
-    B = xn ? limit_rel(sb, zb, -0.5, tb, v.hdry) : limit_rel(sb, zb, tb, -0.5, v.hdry);
+    // one evaluation path for the x- and y-normal segments that interleave in
+    // a warp: select the offsets, not the call
+    A = limit_rel(sa, za, xn ? 0.5 : ta, xn ? ta : 0.5, v.hdry);
+    B = limit_rel(sb, zb, xn ? -0.5 : tb, xn ? tb : -0.5, v.hdry);
   } else {
     const double sza = lsize(v, la), szb = lsize(v, lb);
     const double cxa = lcen(v.x0, v, la, ia), cya = lcen(v.y0, v, la, ja);
