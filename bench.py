@@ -342,6 +342,9 @@ def run_ours(args, ws, rank, local):
     cpu = None
     if ws == 1 and not args.no_cpu:
         cpu, _, _ = cpu_rate(args.cpu_steps, 2)
+    configs = None
+    if ws == 1 and not args.no_configs:
+        configs = config_legs(lib, args, with_cpu=not args.no_cpu)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -368,6 +371,7 @@ def run_ours(args, ws, rank, local):
                 "d2h_bytes_per_step": d2h / e2e_steps, "seconds": e2e_s, "phases_ms": phases,
                 "what": "host DEM -> fm_mra_static -> fm_sim_create(_shard) -> W+K steps -> host state"},
         "uniform": uni,
+        "configs": configs,
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
@@ -417,6 +421,53 @@ def uniform_leg(lib, args, ws, rank, comm, hbm):
             "kernels_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in prof.items()}}
 
 
+CONFIG_LEGS = [
+    # (name, scenario factory, static grid?, GPU steps, CPU steps)
+    ("c0_static_dg2", lambda: S.config0(1), True, 100, 20),
+    ("c1_static_acc", lambda: S.config1(1), True, 400, 40),
+    ("c2_static_fv1", lambda: S.config2(1, adaptive=False), True, 400, 40),
+    ("c2_adaptive_hwfv1", lambda: S.config2(1), False, 100, 5),
+    ("c3_adaptive_mwdg2", lambda: S.config3(1), False, 50, 3),
+]
+
+
+def _leg(be, sc, static, warm, steps, device_time):
+    g = be.grid(sc.dem, sc.L, sc.eps) if static else None
+    s = be.sim(sc, g)
+    ck, _ = s.run(warm, gauge_interval=10.0)
+    t0 = time.perf_counter()
+    ck, r = s.run(steps, clock=ck)
+    wall = time.perf_counter() - t0
+    ms = s.last_run_ms() if device_time else 1000.0 * wall
+    if static:
+        cells = float(s.num_cells) * r.steps
+    else:  # adaptive: the leaf count of every step (element_log, one entry per adapt)
+        _, counts = s.element_log()
+        cells = float(np.sum(counts[-r.steps:])) if len(counts) else float(s.num_cells) * r.steps
+    return {"leaves": int(s.num_cells), "steps": int(r.steps), "ms_per_step": ms / max(r.steps, 1),
+            "value": cells / (ms / 1000.0)}
+
+
+def config_legs(lib, args, with_cpu):
+    """Every BASELINE config on one GPU (full size), and the reference on the
+    host cores on a bounded number of steps of the same run."""
+    out = {}
+    ref = None
+    if with_cpu:
+        ref, kind = reference_backend()
+        if ref.has("set_threads"):
+            ref.fn["set_threads"](os.cpu_count() or 1)
+    for name, mk, static, gsteps, csteps in CONFIG_LEGS:
+        sc = mk()
+        d = {"gpu": _leg(lib, sc, static, 3, gsteps, True)}
+        if ref is not None:
+            d["cpu_reference"] = _leg(ref, sc, static, 1, csteps, False)
+            d["cpu_reference"]["threads"] = os.cpu_count() or 1
+            d["speedup"] = d["gpu"]["value"] / d["cpu_reference"]["value"]
+        out[name] = d
+    return out
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -431,6 +482,8 @@ def main():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--uniform-steps", type=int, default=32,
                    help="timed steps of the uniform-raster comparator (0: skip)")
+    p.add_argument("--no-configs", action="store_true",
+                   help="skip the per-config table (configs 0-3 on GPU and CPU)")
     p.add_argument("--force-shard", action="store_true",
                    help="N=1: run the sharded (NCCL) code path with a single rank")
     args = p.parse_args()
