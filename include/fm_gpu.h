@@ -242,6 +242,14 @@ int fm_sim_profile(fm_sim* s, int64_t steps, double* ms, int64_t* launches, int3
                    int32_t* n);
 const char* fm_sim_kernel_name(fm_sim* s, int32_t family);
 
+/* extent_metrics (metrics.cpp:51-73): a cell is inundated iff depth >=
+ * wet_threshold, nodata cells of either raster are skipped.  counts =
+ * {hits, misses, false_alarms}, rates = {hit_rate, false_alarm, csi}.  Either
+ * raster may be device resident (e.g. from fm_sim_raster(..., out_on_device=1)).
+ * Mismatched geometries: FM_ERR_IO (ParseError). */
+int fm_extent_metrics(const fm_raster* test, const fm_raster* ref, double wet_threshold,
+                      int64_t* counts, double* rates);
+
 /* ---- multi-GPU: Morton-range shards of a static non-uniform sim ----------
  * (the reference is single-process.)  Rank r of R owns the
  * contiguous range [floor(n r / R), floor(n (r+1) / R)) of the Morton-ordered

@@ -367,6 +367,33 @@ int orc_sim_topology(orc_sim* s, int32_t* lv, int32_t* ii, int32_t* jj, int32_t*
     }
   });
 }
+// extent_metrics (metrics.cpp:51-73)
+int orc_extent_metrics(const fm_raster* test, const fm_raster* ref, double wet, int64_t* counts,
+                       double* rates) {
+  return guard([&] {
+    if (test->ncols != ref->ncols || test->nrows != ref->nrows || test->xll != ref->xll ||
+        test->yll != ref->yll || test->cellsize != ref->cellsize)
+      throw Fail(E_IO, "extent_metrics: raster geometries do not match");
+    long long h = 0, m = 0, f = 0;
+    const size_t n = size_t(ref->ncols) * ref->nrows;
+    for (size_t k = 0; k < n; ++k) {
+      const double a = test->values[k], b = ref->values[k];
+      if (a == test->nodata || b == ref->nodata) continue;
+      const bool wt = a >= wet, wr = b >= wet;
+      if (wt && wr)
+        ++h;
+      else if (!wt && wr)
+        ++m;
+      else if (wt && !wr)
+        ++f;
+    }
+    counts[0] = h, counts[1] = m, counts[2] = f;
+    rates[0] = (h + m) > 0 ? double(h) / double(h + m) : 1.0;
+    rates[1] = (h + f) > 0 ? double(f) / double(h + f) : 0.0;
+    rates[2] = (h + m + f) > 0 ? double(h) / double(h + m + f) : 1.0;
+  });
+}
+
 int orc_sim_upload(orc_sim* s, const double* u9) {
   return guard([&] {
     auto& u = s->un() ? s->un()->u : s->nu()->u;

@@ -25,6 +25,7 @@
 #include "../include/fm_gpu.h"
 #include "floodmra/detail_tree.hpp"
 #include "floodmra/errors.hpp"
+#include "floodmra/metrics.hpp"
 #include "floodmra/hll.hpp"
 #include "floodmra/raster.hpp"
 #include "floodmra/sim_common.hpp"
@@ -372,6 +373,15 @@ int ref_sim_sample_gauges(ref_sim* s, int32_t n, const double* x, const double* 
       const fm::GaugeValue v = s->visit([&](auto& sim) { return sim.sample_gauge(x[k], y[k]); });
       out4[4 * k] = v.h, out4[4 * k + 1] = v.eta, out4[4 * k + 2] = v.u, out4[4 * k + 3] = v.v;
     }
+  });
+}
+
+int ref_extent_metrics(const fm_raster* test, const fm_raster* ref, double wet, int64_t* counts,
+                       double* rates) {
+  return guard([&] {
+    const fm::ExtentMetrics m = fm::extent_metrics(to_raster(test), to_raster(ref), wet);
+    counts[0] = m.hits, counts[1] = m.misses, counts[2] = m.false_alarms;
+    rates[0] = m.hit_rate, rates[1] = m.false_alarm, rates[2] = m.csi;
   });
 }
 

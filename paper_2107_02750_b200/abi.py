@@ -142,6 +142,7 @@ OPTIONAL = {
                              PI64, PI64]),
     "sim_topology": (C.c_int, [P, PI32, PI32, PI32, PI32, PI32]),
     "grid_import": (C.c_int, [I32, I32, I32, D, D, D, I64, PI32, PI32, PI32, PD, PP]),
+    "extent_metrics": (C.c_int, [C.POINTER(c_raster), C.POINTER(c_raster), D, C.POINTER(C.c_int64), PD]),
 }
 
 
@@ -204,6 +205,17 @@ class Backend:
         g = Grid.__new__(Grid)
         g.be, g.h, g.eps, g._keep = self, h, 0.0, []
         return g
+
+    def extent_metrics(self, test, ref, wet_threshold: float):
+        """extent_metrics (metrics.cpp:51-73): ({hits, misses, false_alarms},
+        {hit_rate, false_alarm, csi})."""
+        keep: list = []
+        a, b = make_raster(test, keep), make_raster(ref, keep)
+        cnt = np.zeros(3, np.int64)
+        rates = np.zeros(3, np.float64)
+        self.call("extent_metrics", C.byref(a), C.byref(b), float(wet_threshold),
+                  cnt.ctypes.data_as(C.POINTER(C.c_int64)), dptr(rates))
+        return cnt, rates
 
     # ---- sharding (SURVEY §8e) ----
     def comm_local(self, nranks: int) -> "Comm":

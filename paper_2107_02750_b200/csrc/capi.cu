@@ -427,6 +427,13 @@ int fm_sim_topology(fm_sim* s, int32_t* level, int32_t* i, int32_t* j, int32_t* 
     FM_CUDA(cudaStreamSynchronize(stream()));
   });
 }
+int fm_extent_metrics(const fm_raster* test, const fm_raster* ref, double wet_threshold, int64_t* counts,
+                      double* rates) {
+  return guard([&] {
+    require_device();
+    extent_metrics(test, ref, wet_threshold, counts, rates);
+  });
+}
 int fm_sim_snapshot(fm_sim* s) {
   return guard([&] { sim_snapshot(*s->s); });
 }

@@ -178,6 +178,8 @@ void sim_raster_shape(const Sim& s, int32_t* nc, int32_t* nr, double* xll, doubl
                       double* nodata);
 void sim_raster(Sim& s, int which, double* out, bool on_device);
 void sim_sample_gauges(Sim& s, int n, const double* x, const double* y, double* out4);
+void extent_metrics(const fm_raster* test, const fm_raster* ref, double wet, int64_t* counts,
+                    double* rates);
 void sim_restore(Sim& s);
 
 // step operations (nu_flow.cu) and the shard layer (shard.cu)

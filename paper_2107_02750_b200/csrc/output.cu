@@ -11,6 +11,8 @@
 //   k_raster_uni   field_raster (solver_uniform.cpp:501-516): c0 per cell.
 //   k_gauges       NonUniformSim::sample_gauge (solver_nonuniform.cpp:489-506)
 //                  / UniformSim::sample_gauge (solver_uniform.cpp:480-498).
+//   k_extent       extent_metrics (metrics.cpp:51-73): hit / miss / false-alarm
+//                  counts of two depth rasters, warp-reduced, one atomic each.
 //
 // The reference probes a hash map per fine cell (QuadGrid::find_containing,
 // quadgrid.cpp:61-68) on one host thread: 67M probes for config 4.
@@ -131,6 +133,30 @@ __global__ void k_gauges(NuView v, GaugeGeom gg, const unsigned long long* __res
   out4[4 * g + 3] = vel(h, qy, v.hdry);
 }
 
+__global__ void k_extent(long long n, const double* __restrict__ test, const double* __restrict__ ref,
+                         double nd_test, double nd_ref, double wet, unsigned long long* __restrict__ cnt) {
+  unsigned long long h = 0, m = 0, f = 0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const double a = test[k], b = ref[k];
+    if (a == nd_test || b == nd_ref) continue;
+    const bool wt = a >= wet, wr = b >= wet;
+    h += wt && wr;
+    m += !wt && wr;
+    f += wt && !wr;
+  }
+  for (int o = 16; o; o >>= 1) {
+    h += __shfl_xor_sync(0xffffffffu, h, o);
+    m += __shfl_xor_sync(0xffffffffu, m, o);
+    f += __shfl_xor_sync(0xffffffffu, f, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (h) atomicAdd(&cnt[0], h);
+    if (m) atomicAdd(&cnt[1], m);
+    if (f) atomicAdd(&cnt[2], f);
+  }
+}
+
 void leaf_starts(Sim& s, DBuf<unsigned long long>& start) {
   start.alloc(size_t(s.n));
   k_leaf_start<<<nblk(s.n, 256), 256, 0, stream()>>>(s.n, s.L, s.M, s.lvl.p, s.li.p, s.lj.p,
@@ -192,6 +218,43 @@ void sim_sample_gauges(Sim& s, int n, const double* x, const double* y, double* 
   FM_LAUNCHED();
   dout.download(out4, 4 * size_t(n));
   FM_CUDA(cudaStreamSynchronize(stream()));
+}
+
+// extent_metrics (metrics.cpp:51-73) of two rasters, host or device resident.
+void extent_metrics(const fm_raster* test, const fm_raster* ref, double wet, int64_t* counts,
+                    double* rates) {
+  if (!test || !ref) throw Error(FM_ERR_CONFIG, "extent_metrics: null raster");
+  if (test->ncols != ref->ncols || test->nrows != ref->nrows || test->xll != ref->xll ||
+      test->yll != ref->yll || test->cellsize != ref->cellsize)
+    throw Error(FM_ERR_IO, "extent_metrics: raster geometries do not match");
+  const long long n = (long long)ref->ncols * ref->nrows;
+  cudaStream_t st = stream();
+  DBuf<double> ta, tb;
+  const double* a = test->values;
+  const double* b = ref->values;
+  if (!test->on_device) {
+    ta.upload(test->values, n);
+    a = ta.p;
+  }
+  if (!ref->on_device) {
+    tb.upload(ref->values, n);
+    b = tb.p;
+  }
+  DBuf<unsigned long long> c(3);
+  c.zero();
+  k_extent<<<148 * 8, 256, 0, st>>>(n, a, b, test->nodata, ref->nodata, wet, c.p);
+  FM_LAUNCHED();
+  unsigned long long h[3];
+  c.download(h, 3);
+  FM_CUDA(cudaStreamSynchronize(st));
+  const long long hits = (long long)h[0], misses = (long long)h[1], fa = (long long)h[2];
+  if (counts) counts[0] = hits, counts[1] = misses, counts[2] = fa;
+  if (rates) {
+    rates[0] = (hits + misses) > 0 ? double(hits) / double(hits + misses) : 1.0;
+    rates[1] = (hits + fa) > 0 ? double(fa) / double(hits + fa) : 0.0;
+    const long long denom = hits + misses + fa;
+    rates[2] = denom > 0 ? double(hits) / double(denom) : 1.0;
+  }
 }
 
 }  // namespace fmh

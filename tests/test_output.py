@@ -115,3 +115,39 @@ def test_gpu_raster_full_size_c4(gpu):
     c0, cx, cy = u[k, 0:3]
     if cx == 0 and cy == 0:
         assert (blk == c0).all()
+
+
+def _rasters(seed, n=(37, 53), nodata_frac=0.05):
+    rng = np.random.default_rng(seed)
+    a = rng.exponential(0.05, n)
+    b = a + rng.normal(0, 0.02, n)
+    a[rng.random(n) < nodata_frac] = -9999.0
+    b[rng.random(n) < nodata_frac] = -9999.0
+    return S.Raster(a, cellsize=2.0), S.Raster(b, cellsize=2.0)
+
+
+@pytest.mark.parametrize("wet", [0.0, 0.01, 0.05, 1e9])
+def test_extent_metrics_oracle_matches_reference(orc, ref, wet):
+    t, r = _rasters(3)
+    ca, ra = orc.extent_metrics(t, r, wet)
+    cb, rb = ref.extent_metrics(t, r, wet)
+    assert np.array_equal(ca, cb) and np.array_equal(ra, rb)
+
+
+def test_extent_metrics_geometry_mismatch(orc, ref):
+    from paper_2107_02750_b200.abi import FmError
+    t, r = _rasters(4)
+    r2 = S.Raster(r.values, cellsize=1.0)
+    for be in (orc, ref):
+        with pytest.raises(FmError) as e:
+            be.extent_metrics(t, r2, 0.01)
+        assert e.value.code == 3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("wet", [0.0, 0.01, 0.05, 1e9])
+def test_extent_metrics_gpu_matches_oracle(gpu, orc, wet):
+    t, r = _rasters(5, n=(1031, 517))
+    ca, ra = gpu.extent_metrics(t, r, wet)
+    cb, rb = orc.extent_metrics(t, r, wet)
+    assert np.array_equal(ca, cb) and np.array_equal(ra, rb)
