@@ -88,6 +88,12 @@ struct Shard {
   std::vector<int64_t> hoff, hcnt;        // per peer: slice of the halo (local n + hoff)
   DBuf<int32_t> send_idx;                 // local indices of the owned leaves sent
   DBuf<double> send_buf;                  // 9 doubles per sent leaf
+  // NCCL: the exchange runs on a side stream (fork/join through events, also
+  // under graph capture) while the segments that need no halo are computed
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool pending = false;
+  ~Shard();
 };
 
 struct Sim {
@@ -106,6 +112,7 @@ struct Sim {
   // the element size with exact reciprocal multiplies (bit-identical).
   bool p2 = false;
   int64_t n = 0, nseg = 0;
+  int64_t nseg_inner = 0;  // shards: leading local segments with both leaves owned
   // leaves (device Morton order) and state
   DBuf<int8_t> lvl;
   DBuf<int32_t> li, lj;
@@ -193,6 +200,7 @@ inline void step_op(Sim& s, int op, bool manual, double mdt, int* err) {
     nu_step_op(s, op, manual, mdt, err);
 }
 void shard_op(Sim& s, int op);  // exchange / reduce for a sharded sim (NCCL)
+void shard_finish(Sim& s);      // join an exchange started by shard_op
 struct ShardPlan {
   int64_t first = 0, count = 0;
   std::vector<int64_t> segs;              // global ids of the local segments, ascending

@@ -91,10 +91,10 @@ __global__ void __launch_bounds__(256) k_head_friction(NuView v, DevClock* clk, 
 template <bool P2>
 __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClock* __restrict__ clk,
                                              const double* __restrict__ in, double* __restrict__ out,
-                                             int manual, int* err) {
-  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+                                             int manual, int* err, long long q0, long long q1) {
+  const long long q = q0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (!manual && !clk[1].active) return;
-  if (q >= v.nseg) return;
+  if (q >= q1) return;
   const int a = v.seg_l[q], b = v.seg_r[q];  // W/S and E/N leaf
   const int la = v.lvl[a], lb = v.lvl[b];
   const int ia = v.li[a], ja = v.lj[a], ib = v.li[b], jb = v.lj[b];
@@ -518,17 +518,30 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
   const long long n = s.n;
   const long long ns = std::max<long long>(s.nseg, 1);
   const bool fv1 = s.scheme == FM_FV1;
+  // Segment states over [q0, q1).  A sharded sim orders its segments with
+  // the ones that touch only owned leaves first: those run while the halo
+  // exchange is in flight on the shard's side stream, the rest after it.
+  auto seg_range = [&](const double* in, long long q0, long long q1) {
+    if (q1 <= q0) return;
+    if (s.p2)
+      launch_k(k_seg<true>, nblk(q1 - q0, 256), 256, st, v, (const DevClock*)clk, in, s.segst.p, (int)manual,
+               err, q0, q1);
+    else
+      launch_k(k_seg<false>, nblk(q1 - q0, 256), 256, st, v, (const DevClock*)clk, in, s.segst.p,
+               (int)manual, err, q0, q1);
+    FM_LAUNCHED();
+  };
   auto seg = [&](int fam, const double* in) {
     kt_begin(fam);
-    if (s.p2)
-      launch_k(k_seg<true>, nblk(ns, 256), 256, st, v, (const DevClock*)clk, in, s.segst.p, (int)manual, err);
-    else
-      launch_k(k_seg<false>, nblk(ns, 256), 256, st, v, (const DevClock*)clk, in, s.segst.p, (int)manual, err);
-    FM_LAUNCHED();
+    const long long inner = s.shard ? std::min<long long>(s.nseg_inner, ns) : ns;
+    seg_range(in, 0, inner);
+    if (s.shard) shard_finish(s);  // the halo has landed
+    seg_range(in, inner, ns);
     kt_end();
   };
   switch (op) {
     case OP_ACC:
+      if (s.shard) shard_finish(s);
       if (!manual) launch_decide(s);
       kt_begin(KF_ACC_FACES);
       k_acc_faces<<<nblk(ns, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.u.p, s.accq.p, manual, mdt);

@@ -219,6 +219,14 @@ std::vector<T> gather(const std::vector<T>& src, const std::vector<int64_t>& ids
 
 }  // namespace
 
+// One eager exchange + reduction right after construction: NCCL sets up its
+// peer connections on first use, outside any graph capture.
+static void shard_warmup(Sim& s) {
+  shard_op(s, OP_EXCH_U);
+  shard_op(s, OP_REDUCE);  // joins the exchange first
+  FM_CUDA(cudaStreamSynchronize(stream()));
+}
+
 // The uniform raster shards into row bands: rank r owns the global rows
 // [floor(ny r / R), floor(ny (r+1) / R)) (a contiguous range of the raster's
 // own j-major cell order), stored first, then one ghost row south and one
@@ -328,6 +336,7 @@ static Sim* uniform_shard(const fm_sim_desc* d, const fm_raster* dem, Comm* comm
   if (comm->kind == COMM_LOCAL) comm->members[rank] = &s;
   G.reset();
   FM_CUDA(cudaStreamSynchronize(st));
+  if (comm->kind == COMM_NCCL) shard_warmup(s);
   return S.release();
 }
 
@@ -394,10 +403,27 @@ Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* gr
     if (it == p.halo.end() || *it != g) return -1;
     return int32_t(p.count + (it - p.halo.begin()));
   };
+  // local segment order: the segments whose two leaves are both owned first
+  // (computed while the halo exchange is in flight), then those touching the
+  // halo; global order within each class
+  std::vector<int32_t> pos(p.segs.size());
+  std::vector<int64_t> segs_ord;
+  segs_ord.reserve(p.segs.size());
+  auto owned_leaf = [&](int64_t g) { return g >= p.first && g < p.first + p.count; };
+  for (int pass = 0; pass < 2; ++pass)
+    for (size_t k = 0; k < p.segs.size(); ++k) {
+      const bool inner = owned_leaf(seg_l[p.segs[k]]) && owned_leaf(seg_r[p.segs[k]]);
+      if (inner == (pass == 0)) {
+        pos[k] = int32_t(segs_ord.size());
+        segs_ord.push_back(p.segs[k]);
+      }
+      if (pass == 0 && k + 1 == p.segs.size()) s.nseg_inner = int64_t(segs_ord.size());
+    }
+  if (p.segs.empty()) s.nseg_inner = 0;
   auto seg2l = [&](int64_t q) -> int32_t {
     const auto it = std::lower_bound(p.segs.begin(), p.segs.end(), q);
     if (it == p.segs.end() || *it != q) throw Error(FM_ERR_STRUCTURE, "shard: segment outside the shard");
-    return int32_t(it - p.segs.begin());
+    return pos[size_t(it - p.segs.begin())];
   };
   s.n = p.count;
   s.nseg = int64_t(p.segs.size());
@@ -424,10 +450,10 @@ Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* gr
     s.sid.upload(sidl.data(), sidl.size());
   }
   {
-    std::vector<int32_t> sl(p.segs.size()), sr(p.segs.size());
-    for (size_t k = 0; k < p.segs.size(); ++k) {
-      sl[k] = g2l(seg_l[p.segs[k]]);
-      sr[k] = g2l(seg_r[p.segs[k]]);
+    std::vector<int32_t> sl(segs_ord.size()), sr(segs_ord.size());
+    for (size_t k = 0; k < segs_ord.size(); ++k) {
+      sl[k] = g2l(seg_l[segs_ord[k]]);
+      sr[k] = g2l(seg_r[segs_ord[k]]);
       if (sl[k] < 0 || sr[k] < 0) throw Error(FM_ERR_STRUCTURE, "shard: segment leaf outside the shard");
     }
     if (sl.empty()) sl.push_back(0), sr.push_back(0);  // no segments: a dummy entry
@@ -476,6 +502,7 @@ Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* gr
   if (comm->kind == COMM_LOCAL) comm->members[rank] = &s;
   G.reset();
   FM_CUDA(cudaStreamSynchronize(st));
+  if (comm->kind == COMM_NCCL) shard_warmup(s);
   return S.release();
 }
 
@@ -517,6 +544,19 @@ void shard_local_reduce(const std::vector<Sim*>& sims) {
   FM_CUDA(cudaStreamSynchronize(stream()));
 }
 
+Shard::~Shard() {
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (side) cudaStreamDestroy(side);
+}
+
+void shard_finish(Sim& s) {
+  Shard& sh = *s.shard;
+  if (!sh.pending) return;
+  FM_CUDA(cudaStreamWaitEvent(stream(), sh.ev_join, 0));
+  sh.pending = false;
+}
+
 void shard_op(Sim& s, int op) {
   Shard& sh = *s.shard;
   if (!sh.comm) throw Error(FM_ERR_CONFIG, "shard: the communicator was destroyed");
@@ -524,6 +564,7 @@ void shard_op(Sim& s, int op) {
     throw Error(FM_ERR_CONFIG, "shard: a local-group shard steps only through fm_group_run");
   const NcclApi& api = nccl();
   cudaStream_t st = stream();
+  shard_finish(s);
   if (op == OP_REDUCE) {
     // both parity slots: the other slot is already identical on every rank
     nccl_check(api.AllReduce(s.red.p, s.red.p, 2 * sizeof(DevRed) / 8, ncclUint64, ncclMin,
@@ -532,22 +573,34 @@ void shard_op(Sim& s, int op) {
   }
   double* arr = op == OP_EXCH_U ? s.u.p : s.us.p;
   shard_pack(s, arr);
+  // fork: the exchange runs on the side stream, the main stream goes on with
+  // the segments that need no halo; shard_finish joins
+  if (!sh.side) {
+    FM_CUDA(cudaStreamCreateWithFlags(&sh.side, cudaStreamNonBlocking));
+    FM_CUDA(cudaEventCreateWithFlags(&sh.ev_fork, cudaEventDisableTiming));
+    FM_CUDA(cudaEventCreateWithFlags(&sh.ev_join, cudaEventDisableTiming));
+  }
+  FM_CUDA(cudaEventRecord(sh.ev_fork, st));
+  FM_CUDA(cudaStreamWaitEvent(sh.side, sh.ev_fork, 0));
   nccl_check(api.GroupStart(), "ncclGroupStart");
   for (size_t k = 0; k < sh.peers.size(); ++k) {
     if (sh.scnt[k])
       nccl_check(api.Send(sh.send_buf.p + 9 * sh.soff[k], size_t(9 * sh.scnt[k]), ncclFloat64,
-                          sh.peers[k], sh.comm->nc, st), "ncclSend");
+                          sh.peers[k], sh.comm->nc, sh.side), "ncclSend");
     if (sh.hcnt[k])
       nccl_check(api.Recv(arr + 9 * (s.n + sh.hoff[k]), size_t(9 * sh.hcnt[k]), ncclFloat64,
-                          sh.peers[k], sh.comm->nc, st), "ncclRecv");
+                          sh.peers[k], sh.comm->nc, sh.side), "ncclRecv");
   }
   nccl_check(api.GroupEnd(), "ncclGroupEnd");
+  FM_CUDA(cudaEventRecord(sh.ev_join, sh.side));
+  sh.pending = true;
 }
 
 // Host-API reductions of a sharded sim across its NCCL ranks (a local-group
 // shard answers for itself).
 void shard_allreduce_u64_min(Sim& s, unsigned long long* dev, int count) {
   if (!s.shard || !s.shard->comm || s.shard->comm->kind != COMM_NCCL) return;
+  shard_finish(s);
   nccl_check(nccl().AllReduce(dev, dev, size_t(count), ncclUint64, ncclMin, s.shard->comm->nc, stream()),
              "ncclAllReduce");
 }

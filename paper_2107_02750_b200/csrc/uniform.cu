@@ -544,6 +544,7 @@ void un_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
   const NuView nv = s.view();
   const dim3 grid((s.nx + TX - 1) / TX, (s.ny + TY - 1) / TY);
   const bool fv1 = s.scheme == FM_FV1;
+  if (s.shard && (op == OP_ACC || op == OP_STAGE1 || op == OP_STAGE2)) shard_finish(s);
   switch (op) {
     case OP_ACC: {
       if (!manual) launch_decide(s);  // the step decision, once (step_common.cuh)
