@@ -26,6 +26,10 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+#include <type_traits>
+
 #include <algorithm>
 #include <cstring>
 #include <numeric>
@@ -209,13 +213,6 @@ __global__ void k_red_combine(DevRed* const* reds, int n) {
   for (int r = 0; r < n; ++r) reinterpret_cast<unsigned long long*>(reds[r])[f] = m;
 }
 
-template <typename T>
-std::vector<T> gather(const std::vector<T>& src, const std::vector<int64_t>& ids, int width) {
-  std::vector<T> out(ids.size() * size_t(width));
-  for (size_t k = 0; k < ids.size(); ++k)
-    std::memcpy(&out[k * width], &src[size_t(ids[k]) * width], sizeof(T) * width);
-  return out;
-}
 
 }  // namespace
 
@@ -240,17 +237,6 @@ static Sim* uniform_shard(const fm_sim_desc* d, const fm_raster* dem, Comm* comm
   if (nyg < R) throw Error(FM_ERR_CONFIG, "shard: fewer raster rows than ranks");
   const int g0 = int(shard_first(nyg, R, rank)), g1 = int(shard_first(nyg, R, rank + 1));
   const int nyo = g1 - g0, hs = g0 > 0 ? 1 : 0, hn = g1 < nyg ? 1 : 0;
-  std::vector<int64_t> rows;  // storage row -> global row
-  for (int j = g0; j < g1; ++j) rows.push_back(j);
-  if (hs) rows.push_back(g0 - 1);
-  if (hn) rows.push_back(g1);
-  std::vector<int64_t> cells;
-  cells.reserve(rows.size() * size_t(nx));
-  for (int64_t j : rows)
-    for (int i = 0; i < nx; ++i) cells.push_back(j * nx + i);
-  const std::vector<double> u = G->u.to_host(), z = G->z.to_host(), nman = G->nman.to_host();
-  const std::vector<int32_t> li = G->li.to_host(), lj = G->lj.to_host();
-
   auto S = std::make_unique<Sim>();
   Sim& s = *S;
   s.solver = G->solver;
@@ -280,25 +266,37 @@ static Sim* uniform_shard(const fm_sim_desc* d, const fm_raster* dem, Comm* comm
   s.region = G->region;
   s.rect = G->rect;
   s.manning = G->manning;
-  {
-    Hydro h;
-    G->hydro.download(&h, 1);
-    FM_CUDA(cudaStreamSynchronize(st));
-    s.hydro.upload(&h, 1);
-  }
+  s.hydro.alloc(1);
+  FM_CUDA(cudaMemcpyAsync(s.hydro.p, G->hydro.p, sizeof(Hydro), cudaMemcpyDeviceToDevice, st));
   s.clk.alloc(2);
   s.red.alloc(2);
   s.n = int64_t(nx) * nyo;
   s.nseg = int64_t(nx + 1) * nyo + int64_t(nx) * (nyo + 1);
-  const size_t nt = cells.size();
-  std::vector<int64_t> owned(cells.begin(), cells.begin() + s.n);
-  s.u.upload(gather(u, cells, 9).data(), 9 * nt);
+  // owned rows first, then the ghost rows: contiguous row copies on the device
+  const size_t nt = size_t(nyo + hs + hn) * nx;
+  auto rows = [&](auto& dst, const auto& src, int width) {
+    using T = std::remove_pointer_t<decltype(src.p)>;
+    dst.alloc(nt * width);
+    const size_t rw = size_t(nx) * width * sizeof(T);
+    FM_CUDA(cudaMemcpyAsync(dst.p, src.p + size_t(g0) * nx * width, rw * nyo, cudaMemcpyDeviceToDevice, st));
+    if (hs)
+      FM_CUDA(cudaMemcpyAsync(dst.p + size_t(nyo) * nx * width, src.p + size_t(g0 - 1) * nx * width, rw,
+                              cudaMemcpyDeviceToDevice, st));
+    if (hn)
+      FM_CUDA(cudaMemcpyAsync(dst.p + size_t(nyo + hs) * nx * width, src.p + size_t(g1) * nx * width, rw,
+                              cudaMemcpyDeviceToDevice, st));
+  };
+  rows(s.u, G->u, 9);
   s.us.alloc(9 * nt);
   FM_CUDA(cudaMemcpyAsync(s.us.p, s.u.p, 9 * nt * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  s.z.upload(gather(z, cells, 3).data(), 3 * nt);
-  s.nman.upload(gather(nman, cells, 1).data(), nt);
-  s.li.upload(gather(li, owned, 1).data(), owned.size());
-  s.lj.upload(gather(lj, owned, 1).data(), owned.size());
+  rows(s.z, G->z, 3);
+  rows(s.nman, G->nman, 1);
+  s.li.alloc(s.n);
+  s.lj.alloc(s.n);
+  FM_CUDA(cudaMemcpyAsync(s.li.p, G->li.p + size_t(g0) * nx, size_t(s.n) * sizeof(int32_t),
+                          cudaMemcpyDeviceToDevice, st));
+  FM_CUDA(cudaMemcpyAsync(s.lj.p, G->lj.p + size_t(g0) * nx, size_t(s.n) * sizeof(int32_t),
+                          cudaMemcpyDeviceToDevice, st));
   if (s.scheme == FM_ACC) {
     s.aqx.alloc(size_t(nx + 1) * nyo);
     s.aqy.alloc(size_t(nx) * (nyo + 1));
@@ -340,6 +338,115 @@ static Sim* uniform_shard(const fm_sim_desc* d, const fm_raster* dem, Comm* comm
   return S.release();
 }
 
+// ---- device-side shard construction ---------------------------------------
+// The plan of shard_plan, built with flags + stream compactions over the
+// global topology already on the device (no host round trip of the grid).
+namespace {
+
+constexpr int kMaxRanks = 64;
+struct Owners {
+  long long firsts[kMaxRanks + 1];
+  int nranks;
+};
+__device__ __forceinline__ int owner_d(const Owners& o, long long g) {
+  int r = 0;
+  while (r + 1 < o.nranks && g >= o.firsts[r + 1]) ++r;
+  return r;
+}
+
+// per segment: inner (both leaves owned), boundary (one owned); per boundary
+// segment its remote leaf joins the halo and its owned leaf the peer's send list
+__global__ void k_seg_class(long long nseg, const int32_t* __restrict__ sl, const int32_t* __restrict__ sr,
+                            Owners o, int rank, long long first, long long count, uint8_t* inner,
+                            uint8_t* bound, uint8_t* halo_mark, uint8_t* send_mark) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= nseg) return;
+  const long long a = sl[q], b = sr[q];
+  const bool ma = a >= first && a < first + count, mb = b >= first && b < first + count;
+  inner[q] = ma && mb;
+  bound[q] = ma != mb;
+  if (ma != mb) {
+    const long long rem = ma ? b : a, own = ma ? a : b;
+    halo_mark[rem] = 1;
+    send_mark[(long long)owner_d(o, rem) * count + (own - first)] = 1;
+  }
+}
+
+__global__ void k_fill_i32(long long n, int32_t v, int32_t* out) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k < n) out[k] = v;
+}
+
+// dense global -> local maps
+__global__ void k_leaf_map(long long first, long long count, const int32_t* __restrict__ halo,
+                           long long nhalo, int32_t* map) {
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r < count)
+    map[first + r] = int32_t(r);
+  else if (r < count + nhalo)
+    map[halo[r - count]] = int32_t(r);
+}
+__global__ void k_seg_map(const int32_t* __restrict__ ids, long long n, long long base, int32_t* map) {
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r < n) map[ids[r]] = int32_t(base + r);
+}
+
+// local rows: owned [first, first + count) then the halo
+template <typename T>
+__global__ void k_gather_local(long long ntot, int width, long long first, long long count,
+                               const int32_t* __restrict__ halo, const T* __restrict__ src, T* __restrict__ dst) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= ntot * width) return;
+  const long long r = t / width, e = t % width;
+  const long long g = r < count ? first + r : halo[r - count];
+  dst[t] = src[g * width + e];
+}
+
+__global__ void k_remap_owned(long long first, long long count, const int32_t* __restrict__ nb,
+                              const int32_t* __restrict__ sid, const int32_t* __restrict__ lmap,
+                              const int32_t* __restrict__ smap, int32_t* nbl, int32_t* sidl) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= 8 * count) return;
+  const int32_t gn = nb[8 * first + t], gs = sid[8 * first + t];
+  nbl[t] = gn < 0 ? -1 : lmap[gn];
+  sidl[t] = gs < 0 ? -1 : smap[gs];
+}
+
+__global__ void k_local_segs(long long nloc, long long ninner, const int32_t* __restrict__ inner_ids,
+                             const int32_t* __restrict__ bound_ids, const int32_t* __restrict__ sl,
+                             const int32_t* __restrict__ sr, const int32_t* __restrict__ lmap, int32_t* osl,
+                             int32_t* osr) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= nloc) return;
+  const long long g = k < ninner ? inner_ids[k] : bound_ids[k - ninner];
+  osl[k] = lmap[sl[g]];
+  osr[k] = lmap[sr[g]];
+}
+
+__global__ void k_halo_owner(long long nhalo, const int32_t* __restrict__ halo, Owners o, int32_t* out) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k < nhalo) out[k] = owner_d(o, halo[k]);
+}
+
+// indices i in [0, n) with flag[i] != 0, ascending; returns the count
+int64_t select_flagged(const uint8_t* flags, int64_t n, DBuf<int32_t>& out) {
+  cudaStream_t st = stream();
+  out.alloc(std::max<int64_t>(n, 1));
+  DBuf<int> cnt(1);
+  cub::CountingInputIterator<int32_t> it(0);
+  size_t tmp = 0;
+  FM_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, it, flags, out.p, cnt.p, int(n), st));
+  DBuf<unsigned char> t(std::max<size_t>(tmp, 1));
+  FM_CUDA(cub::DeviceSelect::Flagged(t.p, tmp, it, flags, out.p, cnt.p, int(n), st));
+  FM_LAUNCHED();
+  int c = 0;
+  cnt.download(&c, 1);
+  FM_CUDA(cudaStreamSynchronize(st));
+  return c;
+}
+
+}  // namespace
+
 Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* grid, Comm* comm, int rank) {
   if (!comm) throw Error(FM_ERR_CONFIG, "shard: null communicator");
   if (rank < 0 || rank >= comm->nranks) throw Error(FM_ERR_CONFIG, "shard: rank out of range");
@@ -348,18 +455,41 @@ Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* gr
   if (d->solver == FM_MWDG2 || d->solver == FM_HWFV1)
     throw Error(FM_ERR_CONFIG, "shard: adaptive sims re-grid every step and run as replicas");
   if (!grid) return uniform_shard(d, dem, comm, rank);
+  if (comm->nranks > kMaxRanks) throw Error(FM_ERR_CONFIG, "shard: more than 64 ranks");
   cudaStream_t st = stream();
   std::unique_ptr<Sim> G(sim_create(d, dem, grid));
   const int64_t n = G->n, nseg = G->nseg;
-  // global state and topology on the host
-  const std::vector<int8_t> lvl = G->lvl.to_host();
-  const std::vector<int32_t> li = G->li.to_host(), lj = G->lj.to_host();
-  const std::vector<double> z = G->z.to_host(), nman = G->nman.to_host(), u = G->u.to_host();
-  const std::vector<int32_t> nb = G->nb.to_host(), sid = G->sid.to_host();
-  const std::vector<uint8_t> sk = G->sk.to_host();
-  const std::vector<int32_t> seg_l = G->seg_l.to_host(), seg_r = G->seg_r.to_host();
-  const std::vector<int32_t> infc = G->infc.to_host();
-  ShardPlan p = shard_plan(n, nseg, seg_l.data(), seg_r.data(), comm->nranks, rank);
+  const int R = comm->nranks;
+  if (n < R) throw Error(FM_ERR_CONFIG, "shard plan: fewer leaves than ranks");
+  Owners own{};
+  own.nranks = R;
+  for (int r = 0; r <= R; ++r) own.firsts[r] = shard_first(n, R, r);
+  const int64_t first = own.firsts[rank], count = own.firsts[rank + 1] - first;
+
+  // classify segments; mark the halo and the send lists
+  DBuf<uint8_t> inner_f(std::max<int64_t>(nseg, 1)), bound_f(std::max<int64_t>(nseg, 1));
+  DBuf<uint8_t> halo_f(n), send_f(size_t(R) * count);
+  halo_f.zero();
+  send_f.zero();
+  k_seg_class<<<nblk(nseg, 256), 256, 0, st>>>(nseg, G->seg_l.p, G->seg_r.p, own, rank, first, count,
+                                               inner_f.p, bound_f.p, halo_f.p, send_f.p);
+  FM_LAUNCHED();
+  DBuf<int32_t> inner_ids, bound_ids, halo, owner;
+  const int64_t ninner = select_flagged(inner_f.p, nseg, inner_ids);
+  const int64_t nbound = select_flagged(bound_f.p, nseg, bound_ids);
+  const int64_t nhalo = select_flagged(halo_f.p, n, halo);
+  std::vector<DBuf<int32_t>> sends(R);
+  std::vector<int64_t> nsend(R, 0);
+  for (int r = 0; r < R; ++r)
+    if (r != rank) nsend[r] = select_flagged(send_f.p + size_t(r) * count, count, sends[r]);
+  std::vector<int32_t> hown(static_cast<size_t>(nhalo));
+  if (nhalo) {
+    owner.alloc(nhalo);
+    k_halo_owner<<<nblk(nhalo, 256), 256, 0, st>>>(nhalo, halo.p, own, owner.p);
+    FM_LAUNCHED();
+    owner.download(hown.data(), size_t(nhalo));
+    FM_CUDA(cudaStreamSynchronize(st));
+  }
 
   auto S = std::make_unique<Sim>();
   Sim& s = *S;
@@ -384,88 +514,65 @@ Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* gr
   s.region = G->region;
   s.rect = G->rect;
   s.manning = G->manning;
-  {
-    Hydro h;
-    G->hydro.download(&h, 1);
-    FM_CUDA(cudaStreamSynchronize(st));
-    s.hydro.upload(&h, 1);
-  }
+  s.hydro.alloc(1);
+  FM_CUDA(cudaMemcpyAsync(s.hydro.p, G->hydro.p, sizeof(Hydro), cudaMemcpyDeviceToDevice, st));
   s.clk.alloc(2);
   s.red.alloc(2);
 
-  // local leaves: owned, then the halo
-  std::vector<int64_t> loc(size_t(p.count) + p.halo.size());
-  std::iota(loc.begin(), loc.begin() + p.count, p.first);
-  std::copy(p.halo.begin(), p.halo.end(), loc.begin() + p.count);
-  auto g2l = [&](int64_t g) -> int32_t {
-    if (g >= p.first && g < p.first + p.count) return int32_t(g - p.first);
-    const auto it = std::lower_bound(p.halo.begin(), p.halo.end(), g);
-    if (it == p.halo.end() || *it != g) return -1;
-    return int32_t(p.count + (it - p.halo.begin()));
+  // maps and local arrays
+  DBuf<int32_t> lmap(n), smap(std::max<int64_t>(nseg, 1));
+  k_fill_i32<<<nblk(n, 256), 256, 0, st>>>(n, -1, lmap.p);
+  FM_LAUNCHED();
+  k_fill_i32<<<nblk(std::max<int64_t>(nseg, 1), 256), 256, 0, st>>>(std::max<int64_t>(nseg, 1), -1, smap.p);
+  FM_LAUNCHED();
+  const int64_t ntot = count + nhalo;
+  k_leaf_map<<<nblk(ntot, 256), 256, 0, st>>>(first, count, halo.p, nhalo, lmap.p);
+  FM_LAUNCHED();
+  if (ninner) {
+    k_seg_map<<<nblk(ninner, 256), 256, 0, st>>>(inner_ids.p, ninner, 0, smap.p);
+    FM_LAUNCHED();
+  }
+  if (nbound) {
+    k_seg_map<<<nblk(nbound, 256), 256, 0, st>>>(bound_ids.p, nbound, ninner, smap.p);
+    FM_LAUNCHED();
+  }
+  s.n = count;
+  s.nseg = ninner + nbound;
+  s.nseg_inner = ninner;
+  auto gather = [&](auto& dst, const auto& src, int width) {
+    using T = std::remove_pointer_t<decltype(src.p)>;
+    dst.alloc(size_t(ntot) * width);
+    k_gather_local<T><<<nblk(ntot * width, 256), 256, 0, st>>>(ntot, width, first, count, halo.p, src.p,
+                                                                 dst.p);
+    FM_LAUNCHED();
   };
-  // local segment order: the segments whose two leaves are both owned first
-  // (computed while the halo exchange is in flight), then those touching the
-  // halo; global order within each class
-  std::vector<int32_t> pos(p.segs.size());
-  std::vector<int64_t> segs_ord;
-  segs_ord.reserve(p.segs.size());
-  auto owned_leaf = [&](int64_t g) { return g >= p.first && g < p.first + p.count; };
-  for (int pass = 0; pass < 2; ++pass)
-    for (size_t k = 0; k < p.segs.size(); ++k) {
-      const bool inner = owned_leaf(seg_l[p.segs[k]]) && owned_leaf(seg_r[p.segs[k]]);
-      if (inner == (pass == 0)) {
-        pos[k] = int32_t(segs_ord.size());
-        segs_ord.push_back(p.segs[k]);
-      }
-      if (pass == 0 && k + 1 == p.segs.size()) s.nseg_inner = int64_t(segs_ord.size());
-    }
-  if (p.segs.empty()) s.nseg_inner = 0;
-  auto seg2l = [&](int64_t q) -> int32_t {
-    const auto it = std::lower_bound(p.segs.begin(), p.segs.end(), q);
-    if (it == p.segs.end() || *it != q) throw Error(FM_ERR_STRUCTURE, "shard: segment outside the shard");
-    return pos[size_t(it - p.segs.begin())];
-  };
-  s.n = p.count;
-  s.nseg = int64_t(p.segs.size());
-  const size_t nt = loc.size();
-  std::vector<int64_t> owned(loc.begin(), loc.begin() + p.count);
-  s.lvl.upload(gather(lvl, loc, 1).data(), nt);
-  s.li.upload(gather(li, loc, 1).data(), nt);
-  s.lj.upload(gather(lj, loc, 1).data(), nt);
-  s.z.upload(gather(z, loc, 3).data(), 3 * nt);
-  s.nman.upload(gather(nman, loc, 1).data(), nt);
-  s.u.upload(gather(u, loc, 9).data(), 9 * nt);
-  s.us.alloc(9 * nt);
-  FM_CUDA(cudaMemcpyAsync(s.us.p, s.u.p, 9 * nt * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  s.sk.upload(gather(sk, owned, 1).data(), owned.size());
-  {
-    std::vector<int32_t> nbl(8 * owned.size()), sidl(8 * owned.size());
-    for (size_t k = 0; k < owned.size(); ++k)
-      for (int e = 0; e < 8; ++e) {
-        const int32_t gn = nb[8 * owned[k] + e], gs = sid[8 * owned[k] + e];
-        nbl[8 * k + e] = gn < 0 ? -1 : g2l(gn);
-        sidl[8 * k + e] = gs < 0 ? -1 : seg2l(gs);
-      }
-    s.nb.upload(nbl.data(), nbl.size());
-    s.sid.upload(sidl.data(), sidl.size());
+  gather(s.lvl, G->lvl, 1);
+  gather(s.li, G->li, 1);
+  gather(s.lj, G->lj, 1);
+  gather(s.z, G->z, 3);
+  gather(s.nman, G->nman, 1);
+  gather(s.u, G->u, 9);
+  s.us.alloc(9 * size_t(ntot));
+  FM_CUDA(cudaMemcpyAsync(s.us.p, s.u.p, 9 * size_t(ntot) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  s.sk.alloc(count);
+  FM_CUDA(cudaMemcpyAsync(s.sk.p, G->sk.p + first, size_t(count), cudaMemcpyDeviceToDevice, st));
+  s.nb.alloc(8 * count);
+  s.sid.alloc(8 * count);
+  k_remap_owned<<<nblk(8 * count, 256), 256, 0, st>>>(first, count, G->nb.p, G->sid.p, lmap.p, smap.p, s.nb.p,
+                                                      s.sid.p);
+  FM_LAUNCHED();
+  s.seg_l.alloc(std::max<int64_t>(s.nseg, 1));
+  s.seg_r.alloc(std::max<int64_t>(s.nseg, 1));
+  if (s.nseg) {
+    k_local_segs<<<nblk(s.nseg, 256), 256, 0, st>>>(s.nseg, ninner, inner_ids.p, bound_ids.p, G->seg_l.p,
+                                                    G->seg_r.p, lmap.p, s.seg_l.p, s.seg_r.p);
+    FM_LAUNCHED();
   }
-  {
-    std::vector<int32_t> sl(segs_ord.size()), sr(segs_ord.size());
-    for (size_t k = 0; k < segs_ord.size(); ++k) {
-      sl[k] = g2l(seg_l[segs_ord[k]]);
-      sr[k] = g2l(seg_r[segs_ord[k]]);
-      if (sl[k] < 0 || sr[k] < 0) throw Error(FM_ERR_STRUCTURE, "shard: segment leaf outside the shard");
-    }
-    if (sl.empty()) sl.push_back(0), sr.push_back(0);  // no segments: a dummy entry
-    s.seg_l.upload(sl.data(), sl.size());
-    s.seg_r.upload(sr.data(), sr.size());
-  }
-  {
-    std::vector<int32_t> ic(std::max<int64_t>(1, int64_t(s.ninflow) * s.n), 0);
-    for (int f = 0; f < s.ninflow; ++f)
-      for (int64_t k = 0; k < s.n; ++k) ic[size_t(f) * s.n + k] = infc[size_t(f) * n + owned[k]];
-    s.infc.upload(ic.data(), ic.size());
-  }
+  s.infc.alloc(std::max<int64_t>(1, int64_t(s.ninflow) * count));
+  if (s.ninflow == 0) s.infc.zero();
+  for (int f = 0; f < s.ninflow; ++f)
+    FM_CUDA(cudaMemcpyAsync(s.infc.p + size_t(f) * count, G->infc.p + size_t(f) * n + first,
+                            size_t(count) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
   if (s.scheme == FM_ACC) {
     s.accq.alloc(std::max<int64_t>(s.nseg, 1));
     s.accq.zero();
@@ -475,33 +582,37 @@ Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* gr
     s.segst.alloc(6 * size_t(std::max<int64_t>(s.nseg, 1)));
   }
 
-  // exchange plan
+  // exchange plan: peers ascending; halo slices grouped by owner (ascending)
   auto sh = std::make_unique<Shard>();
   sh->comm = comm;
   sh->rank = rank;
-  sh->nranks = comm->nranks;
-  sh->first = p.first;
+  sh->nranks = R;
+  sh->first = first;
   sh->n_global = n;
-  sh->n_halo = int64_t(p.halo.size());
-  std::vector<int32_t> sidx;
-  for (int r = 0; r < comm->nranks; ++r) {
-    const int64_t h0 = std::lower_bound(p.halo_owner.begin(), p.halo_owner.end(), r) - p.halo_owner.begin();
-    const int64_t h1 = std::upper_bound(p.halo_owner.begin(), p.halo_owner.end(), r) - p.halo_owner.begin();
-    if (r == rank || (p.send[r].empty() && h1 == h0)) continue;
+  sh->n_halo = nhalo;
+  int64_t total_send = 0;
+  for (int r = 0; r < R; ++r) total_send += nsend[r];
+  sh->send_idx.alloc(std::max<int64_t>(total_send, 1));
+  int64_t at = 0;
+  for (int r = 0; r < R; ++r) {
+    const int64_t h0 = std::lower_bound(hown.begin(), hown.end(), r) - hown.begin();
+    const int64_t h1 = std::upper_bound(hown.begin(), hown.end(), r) - hown.begin();
+    if (r == rank || (nsend[r] == 0 && h1 == h0)) continue;
     sh->peers.push_back(r);
-    sh->soff.push_back(int64_t(sidx.size()));
-    sh->scnt.push_back(int64_t(p.send[r].size()));
-    for (int64_t g : p.send[r]) sidx.push_back(int32_t(g - p.first));
+    sh->soff.push_back(at);
+    sh->scnt.push_back(nsend[r]);
+    if (nsend[r])
+      FM_CUDA(cudaMemcpyAsync(sh->send_idx.p + at, sends[r].p, size_t(nsend[r]) * sizeof(int32_t),
+                              cudaMemcpyDeviceToDevice, st));
+    at += nsend[r];
     sh->hoff.push_back(h0);
     sh->hcnt.push_back(h1 - h0);
   }
-  if (sidx.empty()) sidx.push_back(0);  // keep the buffers non-empty (no peers)
-  sh->send_idx.upload(sidx.data(), sidx.size());
-  sh->send_buf.alloc(9 * std::max<size_t>(sidx.size(), 1));
+  sh->send_buf.alloc(9 * size_t(std::max<int64_t>(total_send, 1)));
   s.shard = std::move(sh);
   if (comm->kind == COMM_LOCAL) comm->members[rank] = &s;
-  G.reset();
   FM_CUDA(cudaStreamSynchronize(st));
+  G.reset();
   if (comm->kind == COMM_NCCL) shard_warmup(s);
   return S.release();
 }
