@@ -265,3 +265,24 @@ def test_nccl_single_rank_shard_runs_the_graph_path(gpu):
     for x, y in zip(ref.download(), sh.download()):
         assert np.array_equal(x, y)
     assert sh.compute_dt() == ref.compute_dt()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks", [2, 3, 5])
+def test_device_plan_matches_host_plan(gpu, nranks):
+    """The shards built on the device (segment classification + stream
+    compaction) hold exactly the plan of the host function the CPU tests
+    check: owned range, halo size and the local segment count."""
+    sc = S.config4(16)
+    g = gpu.grid(sc.dem, sc.L, sc.eps)
+    glob = gpu.sim(sc, g)
+    lv, i, j, sl, sr = glob.topology()
+    n = glob.num_cells
+    comm = gpu.comm_local(nranks)
+    for r in range(nranks):
+        p = gpu.shard_plan(n, sl, sr, nranks, r)
+        sh = gpu.shard_sim(sc, g, comm, r)
+        info = sh.shard_info()
+        assert (info["first"], info["owned"], info["halo"]) == (p["first"], p["count"], len(p["halo"]))
+        assert sh.num_segments == p["nseg_local"]
+        del sh
