@@ -4,7 +4,7 @@
 // Layout: cell (i, j) at j*nx + i (the reference's own order), 9 flow
 // coefficients + 3 topography coefficients per cell (AoS).
 //
-// k_uni_stage<STAGE>: one CTA per 32 x 8 tile.  Phase 1: every cell revises
+// k_uni_stage<STAGE>: one CTA per 32 x TY tile.  Phase 1: every cell revises
 // its four faces (revise_faces :73-137) into shared memory, and the tile's
 // one-cell halo revises only the face it shares with the tile.  Phase 2:
 // each interior and boundary face's HLL flux (fluxes :139-185) is evaluated
@@ -31,7 +31,15 @@ void project_planes_rowmajor(const fm_raster* r, DBuf<double>& out);
 
 namespace {
 
-constexpr int TX = 32, TY = 8;
+// 32 x 4 tiles, >= 8 resident per SM (a 64-register cap): tuned by A/B on
+// B200 (scripts/ab_uniform.py); 32 x 8 tiles at 110 registers ran 25 % slower
+#ifndef FM_UNI_TY
+#define FM_UNI_TY 4
+#endif
+#ifndef FM_UNI_MINB
+#define FM_UNI_MINB 8
+#endif
+constexpr int TX = 32, TY = FM_UNI_TY;
 
 // A raster band: rows [gy0, gy0 + ny) of the global ny_g rows are owned and
 // stored first (row-major); the ghost rows of a sharded band (the rows just
@@ -89,7 +97,7 @@ __device__ __forceinline__ void ld9(const double* a, size_t c, double s[9]) {
 }
 
 template <int STAGE, bool P2>
-__global__ void __launch_bounds__(TX* TY) k_uni_stage(UniView v, NuView nv, const DevClock* __restrict__ clk,
+__global__ void __launch_bounds__(TX* TY, FM_UNI_MINB) k_uni_stage(UniView v, NuView nv, const DevClock* __restrict__ clk,
                                                        DevRed* red, const double* __restrict__ in,
                                                        const double* uold, double* out, int last,
                                                        int manual, double mdt, int* err) {
