@@ -26,9 +26,13 @@ class FmError(RuntimeError):
 
 
 class BlowUpError(FmError):
-    def __init__(self, code: int, msg: str, t: float):
+    """BlowUpError{t} (errors.hpp:34-37); `result` is the run's fm_run_result
+    (steps done, bad_x / bad_y of the first non-finite leaf)."""
+
+    def __init__(self, code: int, msg: str, t: float, result=None):
         super().__init__(code, msg)
         self.t = t
+        self.result = result
 
 
 class c_raster(C.Structure):
@@ -175,7 +179,7 @@ class Backend:
         if status != FM_OK:
             msg = self.fn["last_error"]().decode(errors="replace")
             if status == 4 and result is not None:
-                raise BlowUpError(status, msg, result.blow_up_time)
+                raise BlowUpError(status, msg, result.blow_up_time, result)
             raise FmError(status, msg)
 
     def call(self, name, *args):

@@ -187,3 +187,22 @@ def test_inline_division_is_ieee(gpu):
         for seed in (1, 2, 3, 4):
             gpu.call("selftest", which, 25_000_000, seed, ctypes.byref(fails))
             assert fails.value == 0, (which, seed)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mk", [lambda: S.config0(4), lambda: S.config0(2)], ids=["c0_s4", "c0_s2"])
+def test_blow_up_reproduced_bit_exact(gpu, orc, mk):
+    """The reference's DG2 has no slope limiter and the dam break diverges
+    (DESIGN.md §8).  Lockstep to the end: the GPU blows up at the same step,
+    the same time and the same first non-finite leaf as the oracle."""
+    from paper_2107_02750_b200.abi import BlowUpError
+    sc = mk()
+    out = []
+    for be in (gpu, orc):
+        g = be.grid(sc.dem, sc.L, sc.eps)
+        s = be.sim(sc, g, libm=1)
+        with pytest.raises(BlowUpError) as e:
+            s.run(3000, gauge_interval=10.0)
+        r = e.value.result
+        out.append((r.steps, r.blow_up_time, r.bad_x, r.bad_y))
+    assert out[0] == out[1]

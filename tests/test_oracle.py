@@ -254,3 +254,20 @@ def test_sim_matches_reference_live(orc, ref, name):
         s.run(25, gauge_interval=10.0)
         out.append(s.download()[3])
     assert np.array_equal(out[0], out[1])
+
+
+def test_blow_up_matches_reference(orc, ref):
+    """The reference's own divergence on the dam break: the
+    oracle blows up at the same step, time and first non-finite leaf."""
+    from paper_2107_02750_b200.abi import BlowUpError
+    sc = S.config0(4)
+    out = []
+    for be in (orc, ref):
+        g = be.grid(sc.dem, sc.L, sc.eps)
+        s = be.sim(sc, g)
+        with pytest.raises(BlowUpError) as e:
+            s.run(3000, gauge_interval=10.0)
+        r = e.value.result
+        out.append((r.steps, r.blow_up_time, r.bad_x, r.bad_y))
+    assert out[0] == out[1]
+    assert out[0][0] < 3000
