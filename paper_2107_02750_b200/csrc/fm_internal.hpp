@@ -139,6 +139,22 @@ std::vector<int64_t> reference_order(const Grid& g, std::vector<int8_t>* l = nul
 
 double elapsed_ms(cudaEvent_t a, cudaEvent_t b);
 
+// A pair of timing events, destroyed on every exit path.
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  EventPair() {
+    FM_CUDA(cudaEventCreate(&a));
+    FM_CUDA(cudaEventCreate(&b));
+  }
+  EventPair(const EventPair&) = delete;
+  EventPair& operator=(const EventPair&) = delete;
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  double ms() const { return elapsed_ms(a, b); }
+};
+
 // Launch helper for the step chain (a plain launch + error check).
 template <typename... KArgs, typename... Args>
 void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {

@@ -527,9 +527,8 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
       if (lev_in > 0) roots[k].alloc(3 * g.nodes(lev_in));
     }
   }
-  cudaEvent_t e0, e1;
-  FM_CUDA(cudaEventCreate(&e0));
-  FM_CUDA(cudaEventCreate(&e1));
+  EventPair ev;
+  cudaEvent_t e0 = ev.a, e1 = ev.b;
   FM_CUDA(cudaEventRecord(e0, st));
 
   k_vertex_max<<<148 * 8, 256, 0, st>>>(vdev, nv, dem->nodata, scal.p);
@@ -582,8 +581,6 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
   if (hs.err) throw Error(FM_ERR_DOMAIN, "project_vertices: non-finite vertex value");
   g.field_norm = hs.norm;
   if (ms) *ms = elapsed_ms(e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
 }
 
 // Final flags (closure + optional 2:1 grading) and subtree leaf counts, one
@@ -708,9 +705,8 @@ Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind)
     g->off[l].alloc(g->nodes(l));
   }
   cudaStream_t st = stream();
-  cudaEvent_t e0, e1;
-  FM_CUDA(cudaEventCreate(&e0));
-  FM_CUDA(cudaEventCreate(&e1));
+  EventPair ev;
+  cudaEvent_t e0 = ev.a, e1 = ev.b;
   FM_CUDA(cudaEventRecord(e0, st));
   grade_count_levels(*g, graded);
   build_leaves(*g);
@@ -719,8 +715,6 @@ Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind)
   g->mra_ms = enc_ms + elapsed_ms(e0, e1);
   const double Nf = double(g->nodes(L)), Nint = double(uint64_t(g->M) * g->N) * ((std::pow(4.0, L) - 1) / 3);
   g->mra_bytes = 24.0 * Nf + 73.0 * Nint + 36.0 * double(g->nleaves);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   return g.release();
 }
 

@@ -564,9 +564,8 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
   DBuf<int>& err = s.errflag;
   err.alloc(1);
   err.zero();
-  cudaEvent_t e0, e1;
-  FM_CUDA(cudaEventCreate(&e0));
-  FM_CUDA(cudaEventCreate(&e1));
+  EventPair ev;
+  cudaEvent_t e0 = ev.a, e1 = ev.b;
   FM_CUDA(cudaEventRecord(e0, st));
   if (s.adaptive) {
     // adapt between steps on the host-driven path (device kernels, host sequencing)
@@ -635,8 +634,6 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
   err.download(&herr, 1);
   FM_CUDA(cudaStreamSynchronize(st));
   s.last_run_ms = elapsed_ms(e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   if (herr) throw Error(FM_ERR_DOMAIN, "hll_flux: negative depth");
   ck->now = c.now;
   ck->next_output = c.next_out;
@@ -684,9 +681,8 @@ void group_run(const std::vector<Sim*>& sims, fm_clock* ck, int64_t max_steps, i
     s->errflag.zero();
   }
   shard_local_reduce(sims);
-  cudaEvent_t e0, e1;
-  FM_CUDA(cudaEventCreate(&e0));
-  FM_CUDA(cudaEventCreate(&e1));
+  EventPair ev;
+  cudaEvent_t e0 = ev.a, e1 = ev.b;
   FM_CUDA(cudaEventRecord(e0, st));
   const std::vector<int> ops = nu_step_ops(*sims[0], false);
   for (int64_t k = 0; k < max_steps; ++k) {
@@ -718,8 +714,6 @@ void group_run(const std::vector<Sim*>& sims, fm_clock* ck, int64_t max_steps, i
   read_clock(*sims[0], c);
   FM_CUDA(cudaStreamSynchronize(st));
   for (Sim* s : sims) s->last_run_ms = elapsed_ms(e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   if (herr) throw Error(FM_ERR_DOMAIN, "hll_flux: negative depth");
   ck->now = c.now;
   ck->next_output = c.next_out;
