@@ -140,6 +140,12 @@ int64_t fm_launch_count(void);
  * bit mismatches. */
 int fm_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* failures);
 
+/* The libm building blocks as the device evaluates them, for tests:
+ * fn 0 = pow(x, 7/3) (FM_LIBM_NATIVE: correctly rounded in double-double),
+ * 1 = cbrt(x) (native), 2 = CUDA's pow(x, 7.0/3.0), 3 = pow(x, 7/3) with the
+ * portable cube root. */
+int fm_eval_libm(int32_t fn, int64_t n, const double* x, double* out);
+
 /* ---- static MRA --------------------------------------------------------- */
 /* generate_static_grid(dem, eps, L, graded, kind)  — detail_tree.hpp:55-56,
  * detail_tree.cpp:172-178.  Pipeline: project_raster (field.cpp:106-117) ->

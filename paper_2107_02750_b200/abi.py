@@ -147,6 +147,7 @@ OPTIONAL = {
     "sim_topology": (C.c_int, [P, PI32, PI32, PI32, PI32, PI32]),
     "grid_import": (C.c_int, [I32, I32, I32, D, D, D, I64, PI32, PI32, PI32, PD, PP]),
     "extent_metrics": (C.c_int, [C.POINTER(c_raster), C.POINTER(c_raster), D, C.POINTER(C.c_int64), PD]),
+    "eval_libm": (C.c_int, [I32, I64, PD, PD]),
 }
 
 

@@ -108,6 +108,14 @@ __global__ void k_selftest_div(int which, int64_t n, uint64_t seed, unsigned lon
   const double ref = a / b;
   if (__double_as_longlong(q) != __double_as_longlong(ref)) atomicAdd(fails, 1ull);
 }
+
+__global__ void k_eval_libm(int fn, int64_t n, const double* __restrict__ x, double* __restrict__ out) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= n) return;
+  const double v = x[k];
+  out[k] = fn == 0 ? fmd::pow73_m(v, FM_LIBM_NATIVE) : fn == 1 ? fmd::cbrt_m(v, FM_LIBM_NATIVE)
+         : fn == 2 ? pow(v, 7.0 / 3.0) : fmd::pow73_m(v, FM_LIBM_PORTABLE);
+}
 }  // namespace
 
 struct fm_grid {
@@ -432,6 +440,18 @@ int fm_extent_metrics(const fm_raster* test, const fm_raster* ref, double wet_th
   return guard([&] {
     require_device();
     extent_metrics(test, ref, wet_threshold, counts, rates);
+  });
+}
+int fm_eval_libm(int32_t fn, int64_t n, const double* x, double* out) {
+  return guard([&] {
+    require_device();
+    if (fn < 0 || fn > 3) throw Error(FM_ERR_CONFIG, "eval_libm: unknown function");
+    DBuf<double> dx, dy(std::max<int64_t>(n, 1));
+    dx.upload(x, n);
+    k_eval_libm<<<unsigned((n + 255) / 256), 256, 0, stream()>>>(fn, n, dx.p, dy.p);
+    FM_LAUNCHED();
+    dy.download(out, n);
+    FM_CUDA(cudaStreamSynchronize(stream()));
   });
 }
 int fm_sim_snapshot(fm_sim* s) {

@@ -78,7 +78,10 @@ def main():
     ref = Backend(REF_SO, "ref_")
     ref.fn["set_threads"](os.cpu_count() or 1)
     report = {}
+    only = sys.argv[2].split(",") if len(sys.argv) > 2 else None
     for name, mk, static, steps in CASES:
+        if only and name not in only:
+            continue
         sc = mk()
         gi, ga, ge, gnear = run(gpu, sc, static, steps)
         ri, ra, re_, _ = run(ref, sc, static, steps)
