@@ -73,35 +73,6 @@ __global__ void k_mark_leaves(long long n, int M, const int8_t* __restrict__ lvl
   for (int q = 0; q < 9; ++q) o[q] = u[9 * k + q];
 }
 
-template <int KIND>
-__global__ void k_encode_up(uint64_t nodes, uint8_t* __restrict__ kn, const uint8_t* __restrict__ kn1,
-                            double* __restrict__ sc, const double* __restrict__ sc1,
-                            double* __restrict__ det) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= nodes || kn[n] != 0) return;
-  const uint32_t k4 = *reinterpret_cast<const uint32_t*>(kn1 + 4 * n);
-  if ((k4 & 0xffu) == 0 || (k4 & 0xff00u) == 0 || (k4 & 0xff0000u) == 0 || (k4 & 0xff000000u) == 0) return;
-  // encode_flow (wavelets.cpp:102-120): h, qx, qy independently
-#pragma unroll
-  for (int f = 0; f < 3; ++f) {
-    P3 kids[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const double* s = sc1 + 9 * (4 * n + c) + 3 * f;
-      kids[c] = P3{s[0], s[1], s[2]};
-    }
-    P3 p;
-    double d[9];
-    encode_k<KIND>(kids, p, d);
-    sc[9 * n + 3 * f] = p.c0;
-    sc[9 * n + 3 * f + 1] = p.cx;
-    sc[9 * n + 3 * f + 2] = p.cy;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) det[27 * n + 9 * f + q] = d[q];
-  }
-  kn[n] = 2;
-}
-
 __global__ void k_norms(long long n, const double* __restrict__ u, unsigned long long* out) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   double a = 0.0, b = 0.0, c = 0.0;
@@ -122,113 +93,6 @@ __global__ void k_norms(long long n, const double* __restrict__ u, unsigned long
   }
 }
 
-// solver_adaptive.cpp:59-73 without the closure
-__global__ void k_flag(uint64_t nodes, const uint8_t* __restrict__ zsig, const uint8_t* __restrict__ kn,
-                       const double* __restrict__ det, const unsigned long long* __restrict__ norms,
-                       double eps, uint8_t* __restrict__ flag) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= nodes) return;
-  uint8_t f = zsig[n];
-  if (!f && kn[n] == 2) {
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      double d[9];
-#pragma unroll
-      for (int r = 0; r < 9; ++r) d[r] = det[27 * n + 9 * q + r];
-      if (dhat(d, bitsd(norms[q])) >= eps) f = 1;
-    }
-  }
-  flag[n] = f;
-}
-
-// ancestor_closure, one level: parent |= any child (detail_tree.cpp:56-64)
-__global__ void k_closure(uint64_t nodes, uint8_t* __restrict__ flag, const uint8_t* __restrict__ flag1) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= nodes) return;
-  if (*reinterpret_cast<const uint32_t*>(flag1 + 4 * n)) flag[n] = 1;
-}
-
-// buffer_ring, one level: dilate to the same-level 8-neighbourhood (:75-94)
-__global__ void k_ring(uint64_t nodes, int l, int M, int N, const uint8_t* __restrict__ flag,
-                       uint8_t* __restrict__ out) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= nodes) return;
-  uint8_t f = flag[n];
-  if (!f) {
-    int i, j;
-    node_ij(l, n, M, i, j);
-    const int w = M << l, h = N << l;
-    for (int dj = -1; dj <= 1 && !f; ++dj)
-      for (int di = -1; di <= 1; ++di) {
-        const int ni = i + di, nj = j + dj;
-        if (ni < 0 || nj < 0 || ni >= w || nj >= h) continue;
-        if (flag[node_index(l, ni, nj, M)]) {
-          f = 1;
-          break;
-        }
-      }
-  }
-  out[n] = f;
-}
-
-// transfer (solver_adaptive.cpp:96-134), one level of the new tree.
-template <int KIND>
-__global__ void k_transfer(uint64_t nodes, int l, int L, const uint8_t* __restrict__ flp,
-                           const uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
-                           const uint8_t* __restrict__ kn, const uint8_t* __restrict__ kn1,
-                           const double* __restrict__ sc, const double* __restrict__ sc1,
-                           const double* __restrict__ det, const double* __restrict__ vin,
-                           double* __restrict__ vout, const int32_t* __restrict__ off,
-                           const int32_t* __restrict__ off1, double* __restrict__ u) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= nodes) return;
-  if (l > 0 && !flp[n >> 2]) return;  // not in the new tree
-  double v[9];
-  const double* src = l == 0 ? sc + 9 * n : vin + 9 * n;
-#pragma unroll
-  for (int q = 0; q < 9; ++q) v[q] = src[q];
-  if (!fl[n]) {  // a level-0 leaf (deeper leaves are written by their parent)
-    if (l == 0) {
-      double* o = u + 9 * off[n];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) o[q] = v[q];  // sc[0] = old leaf value when it was one
-    }
-    return;
-  }
-  const bool internal = kn[n] == 2;
-  double kids[4][9];
-#pragma unroll
-  for (int f = 0; f < 3; ++f) {
-    double d[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) d[q] = internal ? det[27 * n + 9 * f + q] : 0.0;
-    P3 out[4];
-    decode_k<KIND>(P3{v[3 * f], v[3 * f + 1], v[3 * f + 2]}, d, out);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      kids[c][3 * f] = out[c].c0;
-      kids[c][3 * f + 1] = out[c].cx;
-      kids[c][3 * f + 2] = out[c].cy;
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const uint64_t ch = 4 * n + c;
-    const bool leaf = l + 1 == L || !fl1[ch];
-    if (leaf) {
-      const int32_t at = l + 1 < L ? off1[ch] : off[n] + c;
-      double* o = u + 9 * at;
-      const bool old = kn1[ch] == 1;  // surviving leaf keeps its bits (:114-116)
-#pragma unroll
-      for (int q = 0; q < 9; ++q) o[q] = old ? sc1[9 * ch + q] : kids[c][q];
-    } else {
-      double* o = vout + 9 * ch;
-#pragma unroll
-      for (int q = 0; q < 9; ++q) o[q] = kids[c][q];
-    }
-  }
-}
-
 // Piecewise-constant representation after an adapt (solver_adaptive.cpp:157-164)
 __global__ void k_zero_slopes(long long n, double* __restrict__ z, double* __restrict__ u) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -237,35 +101,6 @@ __global__ void k_zero_slopes(long long n, double* __restrict__ z, double* __res
   u[9 * k + 1] = u[9 * k + 2] = 0.0;
   u[9 * k + 4] = u[9 * k + 5] = 0.0;
   u[9 * k + 7] = u[9 * k + 8] = 0.0;
-}
-
-// region_topo (solver_nonuniform.cpp:80-89) for every flagged node: the
-// encode of its four children, each a leaf's z or a deeper region.
-template <int KIND>
-__global__ void k_zpyr(uint64_t nodes, int l, int L, const uint8_t* __restrict__ flp,
-                       const uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
-                       const double* __restrict__ zp1, double* __restrict__ zp,
-                       const int32_t* __restrict__ off, const int32_t* __restrict__ off1,
-                       const double* __restrict__ z) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= nodes) return;
-  if ((l > 0 && !flp[n >> 2]) || !fl[n]) return;
-  P3 kids[4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const uint64_t ch = 4 * n + c;
-    const bool leaf = l + 1 == L || !fl1[ch];
-    const double* s;
-    if (leaf)
-      s = z + 3 * (l + 1 < L ? off1[ch] : off[n] + c);
-    else
-      s = zp1 + 3 * ch;
-    kids[c] = P3{s[0], s[1], s[2]};
-  }
-  const P3 p = encode_parent_k<KIND>(kids);
-  zp[3 * n] = p.c0;
-  zp[3 * n + 1] = p.cx;
-  zp[3 * n + 2] = p.cy;
 }
 
 struct ZpTab {
@@ -309,6 +144,274 @@ __global__ void k_leaf_ij(long long n, int L, int M, int8_t* lvl, int32_t* li, i
   lj[k] = j;
 }
 
+// ---- level-fused passes ---------------------------------------------------
+// The re-grid walks the pyramid level by level; the coarse levels are tiny
+// (level l of one root block has 4^l nodes) and a launch per level makes the
+// adapt launch-bound.  A pass therefore runs each large level as its own
+// launch and all the small levels (<= kSmallNodes nodes) in ONE single-CTA
+// launch that walks them in the pass's order with a __syncthreads between
+// levels; per-level-independent passes run every level in one launch.  The
+// per-node bodies are the kernels' previous bodies, unchanged.
+constexpr uint64_t kSmallNodes = 1024;
+constexpr int kMaxLv = 16;
+
+struct LvTab {
+  int L, M, N;
+  uint8_t* known[kMaxLv + 1];
+  double* sc[kMaxLv + 1];
+  double* fdet[kMaxLv];
+  const uint8_t* zsig[kMaxLv];
+  uint8_t* flag[kMaxLv];
+  uint8_t* tmp[kMaxLv];
+  double* fs[kMaxLv];
+  double* zp[kMaxLv];
+  const int32_t* off[kMaxLv];
+  const unsigned long long* norms;
+  double eps;
+  double* unew;
+  const double* z;
+  __host__ __device__ uint64_t nodes(int l) const { return uint64_t(M) * N << (2 * l); }
+};
+
+template <int KIND>
+struct EncodeUpBody {
+  __device__ static void node(int l, uint64_t n, const LvTab& t) {
+    uint8_t* kn = t.known[l];
+    if (kn[n] != 0) return;
+    const uint32_t k4 = *reinterpret_cast<const uint32_t*>(t.known[l + 1] + 4 * n);
+    if ((k4 & 0xffu) == 0 || (k4 & 0xff00u) == 0 || (k4 & 0xff0000u) == 0 || (k4 & 0xff000000u) == 0) return;
+    const double* sc1 = t.sc[l + 1];
+    // encode_flow (wavelets.cpp:102-120): h, qx, qy independently
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      P3 kids[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double* s = sc1 + 9 * (4 * n + c) + 3 * f;
+        kids[c] = P3{s[0], s[1], s[2]};
+      }
+      P3 p;
+      double d[9];
+      encode_k<KIND>(kids, p, d);
+      t.sc[l][9 * n + 3 * f] = p.c0;
+      t.sc[l][9 * n + 3 * f + 1] = p.cx;
+      t.sc[l][9 * n + 3 * f + 2] = p.cy;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) t.fdet[l][27 * n + 9 * f + q] = d[q];
+    }
+    kn[n] = 2;
+  }
+};
+
+// solver_adaptive.cpp:59-73 without the closure
+struct FlagBody {
+  __device__ static void node(int l, uint64_t n, const LvTab& t) {
+    uint8_t f = t.zsig[l][n];
+    if (!f && t.known[l][n] == 2) {
+      const double* det = t.fdet[l];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        double d[9];
+#pragma unroll
+        for (int r = 0; r < 9; ++r) d[r] = det[27 * n + 9 * q + r];
+        if (dhat(d, bitsd(t.norms[q])) >= t.eps) f = 1;
+      }
+    }
+    t.flag[l][n] = f;
+  }
+};
+
+// ancestor_closure: parent level l |= any child at l + 1 (detail_tree.cpp:56-64)
+struct ClosureBody {
+  __device__ static void node(int l, uint64_t n, const LvTab& t) {
+    if (*reinterpret_cast<const uint32_t*>(t.flag[l + 1] + 4 * n)) t.flag[l][n] = 1;
+  }
+};
+
+// buffer_ring, one level: dilate to the same-level 8-neighbourhood (:75-94)
+struct RingBody {
+  __device__ static void node(int l, uint64_t n, const LvTab& t) {
+    const uint8_t* flag = t.flag[l];
+    uint8_t f = flag[n];
+    if (!f) {
+      int i, j;
+      node_ij(l, n, t.M, i, j);
+      const int w = t.M << l, h = t.N << l;
+      for (int dj = -1; dj <= 1 && !f; ++dj)
+        for (int di = -1; di <= 1; ++di) {
+          const int ni = i + di, nj = j + dj;
+          if (ni < 0 || nj < 0 || ni >= w || nj >= h) continue;
+          if (flag[node_index(l, ni, nj, t.M)]) {
+            f = 1;
+            break;
+          }
+        }
+    }
+    t.tmp[l][n] = f;
+  }
+};
+
+// transfer (solver_adaptive.cpp:96-134), one level of the new tree.
+template <int KIND>
+struct TransferBody {
+  __device__ static void node(int l, uint64_t n, const LvTab& t) {
+    const int L = t.L;
+    if (l > 0 && !t.flag[l - 1][n >> 2]) return;  // not in the new tree
+    double v[9];
+    const double* src = l == 0 ? t.sc[0] + 9 * n : t.fs[l] + 9 * n;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) v[q] = src[q];
+    if (!t.flag[l][n]) {  // a level-0 leaf (deeper leaves are written by their parent)
+      if (l == 0) {
+        double* o = t.unew + 9 * t.off[0][n];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) o[q] = v[q];  // sc[0] = old leaf value when it was one
+      }
+      return;
+    }
+    const bool internal = t.known[l][n] == 2;
+    double kids[4][9];
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      double d[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) d[q] = internal ? t.fdet[l][27 * n + 9 * f + q] : 0.0;
+      P3 out[4];
+      decode_k<KIND>(P3{v[3 * f], v[3 * f + 1], v[3 * f + 2]}, d, out);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        kids[c][3 * f] = out[c].c0;
+        kids[c][3 * f + 1] = out[c].cx;
+        kids[c][3 * f + 2] = out[c].cy;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint64_t ch = 4 * n + c;
+      const bool leaf = l + 1 == L || !t.flag[l + 1][ch];
+      if (leaf) {
+        const int32_t at = l + 1 < L ? t.off[l + 1][ch] : t.off[l][n] + c;
+        double* o = t.unew + 9 * at;
+        const bool old = t.known[l + 1][ch] == 1;  // surviving leaf keeps its bits (:114-116)
+#pragma unroll
+        for (int q = 0; q < 9; ++q) o[q] = old ? t.sc[l + 1][9 * ch + q] : kids[c][q];
+      } else {
+        double* o = t.fs[l + 1] + 9 * ch;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) o[q] = kids[c][q];
+      }
+    }
+  }
+};
+
+// region_topo (solver_nonuniform.cpp:80-89) for every flagged node
+template <int KIND>
+struct ZpyrBody {
+  __device__ static void node(int l, uint64_t n, const LvTab& t) {
+    const int L = t.L;
+    if ((l > 0 && !t.flag[l - 1][n >> 2]) || !t.flag[l][n]) return;
+    P3 kids[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint64_t ch = 4 * n + c;
+      const bool leaf = l + 1 == L || !t.flag[l + 1][ch];
+      const double* s;
+      if (leaf)
+        s = t.z + 3 * (l + 1 < L ? t.off[l + 1][ch] : t.off[l][n] + c);
+      else
+        s = t.zp[l + 1] + 3 * ch;
+      kids[c] = P3{s[0], s[1], s[2]};
+    }
+    const P3 p = encode_parent_k<KIND>(kids);
+    t.zp[l][3 * n] = p.c0;
+    t.zp[l][3 * n + 1] = p.cx;
+    t.zp[l][3 * n + 2] = p.cy;
+  }
+};
+
+template <class Body>
+__global__ void k_level(LvTab t, int l) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n < t.nodes(l)) Body::node(l, n, t);
+}
+// the small levels from `first` to `last` (either direction), one CTA
+template <class Body>
+__global__ void __launch_bounds__(1024) k_levels_small(LvTab t, int first, int last) {
+  const int step = last >= first ? 1 : -1;
+  for (int l = first;; l += step) {
+    const uint64_t nodes = t.nodes(l);
+    for (uint64_t n = threadIdx.x; n < nodes; n += blockDim.x) Body::node(l, n, t);
+    __syncthreads();
+    if (l == last) break;
+  }
+}
+// every level at once (per-level independent bodies): blockIdx.y = level
+template <class Body>
+__global__ void k_levels_flat(LvTab t, int l0) {
+  const int l = l0 + blockIdx.y;
+  const uint64_t nodes = t.nodes(l);
+  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < nodes;
+       n += uint64_t(gridDim.x) * blockDim.x)
+    Body::node(l, n, t);
+}
+
+// Run Body over levels lo..hi in the given order: big levels one launch each,
+// the small ones (all at the coarse end) in one launch.
+template <class Body>
+void run_levels(const LvTab& t, int lo, int hi, bool fine_to_coarse) {
+  if (hi < lo) return;
+  cudaStream_t st = stream();
+  int ls = -1;  // the finest small level
+  for (int l = lo; l <= hi; ++l)
+    if (t.nodes(l) <= kSmallNodes) ls = l;
+  auto big = [&](int l) {
+    k_level<Body><<<nblk(t.nodes(l), 256), 256, 0, st>>>(t, l);
+    FM_LAUNCHED();
+  };
+  auto small = [&](int a, int b) {
+    k_levels_small<Body><<<1, 1024, 0, st>>>(t, a, b);
+    FM_LAUNCHED();
+  };
+  if (fine_to_coarse) {
+    for (int l = hi; l > ls && l >= lo; --l) big(l);
+    if (ls >= lo) small(ls, lo);
+  } else {
+    if (ls >= lo) small(lo, ls);
+    for (int l = std::max(ls + 1, lo); l <= hi; ++l) big(l);
+  }
+}
+template <class Body>
+void run_levels_flat(const LvTab& t, int lo, int hi) {
+  if (hi < lo) return;
+  const unsigned bx = unsigned(std::min<uint64_t>(nblk(t.nodes(hi), 256), 148 * 8));
+  k_levels_flat<Body><<<dim3(bx, hi - lo + 1), 256, 0, stream()>>>(t, lo);
+  FM_LAUNCHED();
+}
+
+LvTab lv_tab(Sim& s, Grid& g, AdaptState& a) {
+  LvTab t{};
+  t.L = g.L;
+  t.M = g.M;
+  t.N = g.N;
+  for (int l = 0; l <= g.L; ++l) {
+    t.known[l] = a.known[l].p;
+    t.sc[l] = a.sc[l].p;
+  }
+  for (int l = 0; l < g.L; ++l) {
+    t.fdet[l] = a.fdet[l].p;
+    t.zsig[l] = a.zsig[l].p;
+    t.flag[l] = g.flag[l].p;
+    t.tmp[l] = a.tmp[l].p;
+    t.fs[l] = a.fs[l].p;
+    t.zp[l] = a.zp[l].p;
+    t.off[l] = g.off.size() > size_t(l) ? g.off[l].p : nullptr;
+  }
+  t.norms = a.norms.p;
+  t.eps = a.eps;
+  t.z = s.z.p;
+  return t;
+}
+
 void copy_leaves_from_grid(Sim& s, const Grid& g) {
   cudaStream_t st = stream();
   s.n = g.nleaves;
@@ -333,21 +436,11 @@ void refresh_topology(Sim& s) {
   build_topology(s, g);
   // z encode-up over the new leaves, then the partner values
   const int L = s.L;
-  for (int l = L - 1; l >= 0; --l) {
-    const uint64_t nodes = g.nodes(l);
-    const bool last = l + 1 == L;
-    if (a.kind == 0)
-      k_zpyr<0><<<nblk(nodes, 256), 256, 0, st>>>(nodes, l, L, l ? g.flag[l - 1].p : nullptr, g.flag[l].p,
-                                                  last ? nullptr : g.flag[l + 1].p,
-                                                  last ? nullptr : a.zp[l + 1].p, a.zp[l].p, g.off[l].p,
-                                                  last ? nullptr : g.off[l + 1].p, s.z.p);
-    else
-      k_zpyr<1><<<nblk(nodes, 256), 256, 0, st>>>(nodes, l, L, l ? g.flag[l - 1].p : nullptr, g.flag[l].p,
-                                                  last ? nullptr : g.flag[l + 1].p,
-                                                  last ? nullptr : a.zp[l + 1].p, a.zp[l].p, g.off[l].p,
-                                                  last ? nullptr : g.off[l + 1].p, s.z.p);
-    FM_LAUNCHED();
-  }
+  LvTab tab = lv_tab(s, g, a);
+  if (a.kind == 0)
+    run_levels<ZpyrBody<0>>(tab, 0, L - 1, true);
+  else
+    run_levels<ZpyrBody<1>>(tab, 0, L - 1, true);
   ZpTab t{};
   for (int l = 0; l < L; ++l) t.zp[l] = a.zp[l].p;
   s.zpair.alloc(4 * s.n);
@@ -445,14 +538,19 @@ void adaptive_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem) {
   adaptive_adapt(s, 0.0);
 }
 
+struct ZeroKnownBody {
+  __device__ static void node(int l, uint64_t n, const LvTab& t) { t.known[l][n] = 0; }
+};
+
 void adaptive_adapt(Sim& s, double t) {
   s.ref_perm_ok = false;  // the leaf set changes
   cudaStream_t st = stream();
   Grid& g = *s.grid;
   AdaptState& a = *s.ad;
   const int L = g.L;
+  LvTab tab = lv_tab(s, g, a);
   // encode_up
-  for (int l = 0; l <= L; ++l) a.known[l].zero();
+  run_levels_flat<ZeroKnownBody>(tab, 0, L);
   PtrTab pt{};
   for (int l = 0; l <= L; ++l) {
     pt.known[l] = a.known[l].p;
@@ -460,63 +558,34 @@ void adaptive_adapt(Sim& s, double t) {
   }
   k_mark_leaves<<<nblk(s.n, 256), 256, 0, st>>>(s.n, s.M, s.lvl.p, s.li.p, s.lj.p, s.u.p, pt);
   FM_LAUNCHED();
-  for (int l = L - 1; l >= 0; --l) {
-    const uint64_t nodes = g.nodes(l);
-    if (a.kind == 0)
-      k_encode_up<0><<<nblk(nodes, 256), 256, 0, st>>>(nodes, a.known[l].p, a.known[l + 1].p, a.sc[l].p,
-                                                        a.sc[l + 1].p, a.fdet[l].p);
-    else
-      k_encode_up<1><<<nblk(nodes, 256), 256, 0, st>>>(nodes, a.known[l].p, a.known[l + 1].p, a.sc[l].p,
-                                                        a.sc[l + 1].p, a.fdet[l].p);
-    FM_LAUNCHED();
-  }
+  if (a.kind == 0)
+    run_levels<EncodeUpBody<0>>(tab, 0, L - 1, true);
+  else
+    run_levels<EncodeUpBody<1>>(tab, 0, L - 1, true);
   // norms over the current leaves
   a.norms.zero();
   k_norms<<<nblk(s.n, 256), 256, 0, st>>>(s.n, s.u.p, a.norms.p);
   FM_LAUNCHED();
   // flag + closure
-  for (int l = 0; l < L; ++l) {
-    k_flag<<<nblk(g.nodes(l), 256), 256, 0, st>>>(g.nodes(l), a.zsig[l].p, a.known[l].p, a.fdet[l].p,
-                                                   a.norms.p, a.eps, g.flag[l].p);
-    FM_LAUNCHED();
-  }
-  for (int l = L - 1; l >= 1; --l) {
-    k_closure<<<nblk(g.nodes(l - 1), 256), 256, 0, st>>>(g.nodes(l - 1), g.flag[l - 1].p, g.flag[l].p);
-    FM_LAUNCHED();
-  }
+  run_levels_flat<FlagBody>(tab, 0, L - 1);
+  run_levels<ClosureBody>(tab, 0, L - 2, true);
   // buffer_ring + closure
-  for (int l = 0; l < L; ++l) {
-    k_ring<<<nblk(g.nodes(l), 256), 256, 0, st>>>(g.nodes(l), l, g.M, g.N, g.flag[l].p, a.tmp[l].p);
-    FM_LAUNCHED();
-    std::swap(g.flag[l], a.tmp[l]);
-  }
-  for (int l = L - 1; l >= 1; --l) {
-    k_closure<<<nblk(g.nodes(l - 1), 256), 256, 0, st>>>(g.nodes(l - 1), g.flag[l - 1].p, g.flag[l].p);
-    FM_LAUNCHED();
-  }
+  run_levels_flat<RingBody>(tab, 0, L - 1);
+  for (int l = 0; l < L; ++l) std::swap(g.flag[l], a.tmp[l]);
+  tab = lv_tab(s, g, a);
+  run_levels<ClosureBody>(tab, 0, L - 2, true);
   // grade + counts + leaves + exact topography (assemble_grid)
   grade_count_levels(g, true);
   build_leaves(g);
   // transfer the flow onto the new leaves
   const int64_t n_new = g.nleaves;
   DBuf<double> u_new(9 * n_new);
-  for (int l = 0; l < L; ++l) {
-    const uint64_t nodes = g.nodes(l);
-    const bool last = l + 1 == L;
-    auto launch = [&](auto kind_tag) {
-      constexpr int K = decltype(kind_tag)::value;
-      k_transfer<K><<<nblk(nodes, 256), 256, 0, st>>>(
-          nodes, l, L, l ? g.flag[l - 1].p : nullptr, g.flag[l].p, last ? nullptr : g.flag[l + 1].p,
-          a.known[l].p, a.known[l + 1].p, a.sc[l].p, a.sc[l + 1].p, a.fdet[l].p,
-          l ? a.fs[l].p : nullptr, last ? nullptr : a.fs[l + 1].p, g.off[l].p,
-          last ? nullptr : g.off[l + 1].p, u_new.p);
-    };
-    if (a.kind == 0)
-      launch(std::integral_constant<int, 0>{});
-    else
-      launch(std::integral_constant<int, 1>{});
-    FM_LAUNCHED();
-  }
+  tab = lv_tab(s, g, a);
+  tab.unew = u_new.p;
+  if (a.kind == 0)
+    run_levels<TransferBody<0>>(tab, 0, L - 1, false);
+  else
+    run_levels<TransferBody<1>>(tab, 0, L - 1, false);
   s.u = std::move(u_new);
   s.us.alloc(9 * n_new);
   copy_leaves_from_grid(s, g);
