@@ -152,7 +152,13 @@ __global__ void k_leaf_ij(long long n, int L, int M, int8_t* lvl, int32_t* li, i
 // launch that walks them in the pass's order with a __syncthreads between
 // levels; per-level-independent passes run every level in one launch.  The
 // per-node bodies are the kernels' previous bodies, unchanged.
-constexpr uint64_t kSmallNodes = 1024;
+#ifndef FM_SMALL_NODES
+#define FM_SMALL_NODES 256
+#endif
+constexpr uint64_t kSmallNodes = FM_SMALL_NODES;
+#ifndef FM_SMALL_THREADS
+#define FM_SMALL_THREADS 256
+#endif
 constexpr int kMaxLv = 16;
 
 struct LvTab {
@@ -336,7 +342,7 @@ __global__ void k_level(LvTab t, int l) {
 }
 // the small levels from `first` to `last` (either direction), one CTA
 template <class Body>
-__global__ void __launch_bounds__(1024) k_levels_small(LvTab t, int first, int last) {
+__global__ void __launch_bounds__(FM_SMALL_THREADS) k_levels_small(LvTab t, int first, int last) {
   const int step = last >= first ? 1 : -1;
   for (int l = first;; l += step) {
     const uint64_t nodes = t.nodes(l);
@@ -369,7 +375,7 @@ void run_levels(const LvTab& t, int lo, int hi, bool fine_to_coarse) {
     FM_LAUNCHED();
   };
   auto small = [&](int a, int b) {
-    k_levels_small<Body><<<1, 1024, 0, st>>>(t, a, b);
+    k_levels_small<Body><<<1, FM_SMALL_THREADS, 0, st>>>(t, a, b);
     FM_LAUNCHED();
   };
   if (fine_to_coarse) {
