@@ -221,10 +221,12 @@ def run_ours(args, ws, rank, local):
     n_leaves, n_seg = sim.num_cells, sim.num_segments
     n_global = sim.shard_info()["n_global"] if comm is not None else n_leaves
     ck, r = sim.run(args.warmup, gauge_interval=10.0)
-    # The reference DG2 scheme diverges under this forcing after ~130 steps (thin
-    # rain films on 10 m building walls; DESIGN.md §"Config 4 dynamics"), so the
-    # K timed steps run in chunks that each restart from the post-warm-up state
-    # (device-side snapshot, restored outside the timed region).
+    # The reference DG2 scheme (no slope limiter) is unstable under this forcing:
+    # the CFL step of the still 0.14 mm film after the first dry step is 8.9 s,
+    # its update overshoots at the building walls and dt then collapses
+    # (profiles/c4_dynamics_r1.txt).  So the K timed steps run in
+    # chunks that each restart from the post-warm-up state (device-side
+    # snapshot, restored outside the timed region): every leaf is wet there.
     sim.snapshot()
     ck0 = (ck.end_time, ck.output_interval, ck.gauge_interval, ck.now, ck.next_output,
            ck.next_gauge)
