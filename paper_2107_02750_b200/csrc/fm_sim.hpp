@@ -65,6 +65,7 @@ struct NuView {
   // ACC
   const int32_t* seg_l;
   const int32_t* seg_r;
+  const uint8_t* seg_geo;  // per segment: x-normal + limit-point offsets (k_seg_geo)
   const int32_t* sid;   // 8 per leaf: segment ids of the sub-faces per side
   const double* segst;  // 6 per segment: HLL flux (m n t), z*, h*L, h*R
   long long nseg;
@@ -118,7 +119,7 @@ struct Sim {
   DBuf<int32_t> li, lj;
   DBuf<double> u, us, z, nman, zpair;
   DBuf<int32_t> nb, sid, seg_l, seg_r;
-  DBuf<uint8_t> sk;
+  DBuf<uint8_t> sk, seg_geo;
   DBuf<double> segst;       // DG2/FV1 segment states (6 per segment)
   DBuf<double> accq, accqb;  // ACC: per segment, per leaf-side (4 per leaf)
   DBuf<double> aqx, aqy;     // uniform ACC faces
@@ -226,6 +227,7 @@ void group_run(const std::vector<Sim*>& sims, fm_clock* clk, int64_t max_steps, 
                fm_run_result* out);
 // topology (topo.cu)
 void build_topology(Sim& s, const Grid& g);
+void build_seg_geo(Sim& s);  // after seg_l / seg_r and the leaf keys are final
 void resolve_inflows(Sim& s, const Grid& g);
 void resolve_manning(Sim& s);
 int64_t scan_exclusive(const int32_t* in, int32_t* out, int64_t n);

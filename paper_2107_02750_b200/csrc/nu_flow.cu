@@ -96,25 +96,31 @@ __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClo
   if (!manual && !clk[1].active) return;
   if (q >= q1) return;
   const int a = v.seg_l[q], b = v.seg_r[q];  // W/S and E/N leaf
-  const int la = v.lvl[a], lb = v.lvl[b];
-  const int ia = v.li[a], ja = v.lj[a], ib = v.li[b], jb = v.lj[b];
-  // x-normal iff b starts where a ends along x (fine-cell units)
-  const bool xn = (ib << (v.L - lb)) == ((ia + 1) << (v.L - la));
   double sa[9], sb[9];
   load9(in, a, sa);
   load9(in, b, sb);
   const P3 za = load3(v.z, a), zb = load3(v.z, b);
   Pt A, B;
+  bool xn;
   if (P2) {
     // enumerate_faces geometry (quadgrid.cpp:222-245) as exact offsets: the
-    // centre lies on the face, at the finer (or either) leaf's centre along it
-    const double ta = la < lb ? (((xn ? jb : ib) & 1) ? 0.25 : -0.25) : 0.0;
-    const double tb = lb < la ? (((xn ? ja : ia) & 1) ? 0.25 : -0.25) : 0.0;
+    // centre lies on the face, at the finer (or either) leaf's centre along
+    // it.  Static per segment, precomputed (k_seg_geo): no gathers of the
+    // leaves' keys on this kernel's critical path.
+    const int gc = v.seg_geo[q];
+    xn = gc & 1;
+    const int ca = (gc >> 1) & 3, cb = (gc >> 3) & 3;
+    const double ta = ca == 0 ? 0.0 : ca == 2 ? 0.25 : -0.25;
+    const double tb = cb == 0 ? 0.0 : cb == 2 ? 0.25 : -0.25;
     // one evaluation path for the x- and y-normal segments that interleave in
     // a warp: select the offsets, not the call
     A = limit_rel(sa, za, xn ? 0.5 : ta, xn ? ta : 0.5, v.hdry);
     B = limit_rel(sb, zb, xn ? -0.5 : tb, xn ? tb : -0.5, v.hdry);
   } else {
+    const int la = v.lvl[a], lb = v.lvl[b];
+    const int ia = v.li[a], ja = v.lj[a], ib = v.li[b], jb = v.lj[b];
+    // x-normal iff b starts where a ends along x (fine-cell units)
+    xn = (ib << (v.L - lb)) == ((ia + 1) << (v.L - la));
     const double sza = lsize(v, la), szb = lsize(v, lb);
     const double cxa = lcen(v.x0, v, la, ia), cya = lcen(v.y0, v, la, ja);
     const double cxb = lcen(v.x0, v, lb, ib), cyb = lcen(v.y0, v, lb, jb);

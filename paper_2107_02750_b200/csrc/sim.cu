@@ -148,6 +148,7 @@ NuView Sim::view() const {
   v.infc = infc.p;
   v.seg_l = seg_l.p;
   v.seg_r = seg_r.p;
+  v.seg_geo = seg_geo.p;
   v.sid = sid.p;
   v.segst = segst.p;
   v.nseg = nseg;

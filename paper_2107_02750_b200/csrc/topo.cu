@@ -143,6 +143,26 @@ __global__ void k_segments(long long n, const int32_t* __restrict__ li,
   }
 }
 
+// Static per-segment geometry for the segment kernel (k_seg, P2 geometry):
+// bit 0 x-normal; bits 1-2 / 3-4 the tangential offset code of the W/S and
+// E/N leaf's limit point (0: centre of its face, 1: -1/4, 2: +1/4 of its
+// size).  The segment centre (enumerate_faces, quadgrid.cpp:222-245) lies at
+// the finer leaf's face centre, i.e. a quarter off the coarser leaf's.
+__global__ void k_seg_geo(long long nseg, int L, const int32_t* __restrict__ seg_l,
+                          const int32_t* __restrict__ seg_r, const int8_t* __restrict__ lvl,
+                          const int32_t* __restrict__ li, const int32_t* __restrict__ lj,
+                          uint8_t* __restrict__ geo) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= nseg) return;
+  const int a = seg_l[q], b = seg_r[q];
+  const int la = lvl[a], lb = lvl[b];
+  const int ia = li[a], ja = lj[a], ib = li[b], jb = lj[b];
+  const bool xn = (ib << (L - lb)) == ((ia + 1) << (L - la));
+  const int ta = la < lb ? ((((xn ? jb : ib) & 1) ? 2 : 1)) : 0;
+  const int tb = lb < la ? ((((xn ? ja : ia) & 1) ? 2 : 1)) : 0;
+  geo[q] = uint8_t((xn ? 1 : 0) | (ta << 1) | (tb << 3));
+}
+
 // --- scan -----------------------------------------------------------------
 __global__ void k_block_sums(const int32_t* __restrict__ in, long long n,
                              long long* __restrict__ sums) {
@@ -269,6 +289,15 @@ int64_t scan_exclusive(const int32_t* in, int32_t* out, int64_t n) {
   return tot;
 }
 
+void build_seg_geo(Sim& s) {
+  s.seg_geo.alloc(std::max<int64_t>(s.nseg, 1));
+  if (s.nseg) {
+    k_seg_geo<<<nblk(s.nseg, 256), 256, 0, stream()>>>(s.nseg, s.L, s.seg_l.p, s.seg_r.p, s.lvl.p, s.li.p,
+                                                      s.lj.p, s.seg_geo.p);
+    FM_LAUNCHED();
+  }
+}
+
 void build_topology(Sim& s, const Grid& g) {
   cudaStream_t st = stream();
   const long long n = s.n;
@@ -292,6 +321,7 @@ void build_topology(Sim& s, const Grid& g) {
     k_segments<<<nblk(n, 256), 256, 0, st>>>(n, s.li.p, s.lj.p, s.nb.p, s.sk.p, base.p, s.sid.p,
                                               s.seg_l.p, s.seg_r.p);
     FM_LAUNCHED();
+    build_seg_geo(s);
     if (s.scheme != FM_ACC) s.segst.alloc(6 * size_t(std::max<int64_t>(s.nseg, 1)));
   }
 }
