@@ -144,13 +144,10 @@ __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClo
   const double unA = xn ? A.u : A.v, utA = xn ? A.v : A.u;
   const double unB = xn ? B.u : B.v, utB = xn ? B.v : B.u;
   const Flx f = hll_inl(hl, hl * unA, hl * utA, hr, hr * unB, hr * utB, v.g, v.hdry, err);
-  double* o = out + 6 * q;
-  o[0] = f.m;
-  o[1] = f.n;
-  o[2] = f.t;
-  o[3] = zs;
-  o[4] = hl;
-  o[5] = hr;
+  double2* o = reinterpret_cast<double2*>(out + 6 * q);  // 16 B aligned
+  o[0] = make_double2(f.m, f.n);
+  o[1] = make_double2(f.t, zs);
+  o[2] = make_double2(hl, hr);
 }
 
 // ---- one RK stage over all leaves ---------------------------------------
@@ -180,9 +177,14 @@ __device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9],
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
     if (t < nseg) {
-      const double* q = v.segst + 6 * (long long)v.sid[8 * kk + 2 * sd + t];
+      // 48 B state, 16 B aligned: three 16 B loads
+      const double2* q = reinterpret_cast<const double2*>(v.segst + 6 * (long long)v.sid[8 * kk + 2 * sd + t]);
 #pragma unroll
-      for (int e = 0; e < 6; ++e) sg[t][e] = q[e];
+      for (int e = 0; e < 3; ++e) {
+        const double2 w2 = q[e];
+        sg[t][2 * e] = w2.x;
+        sg[t][2 * e + 1] = w2.y;
+      }
     }
   }
   const double ox = sd == 1 ? 0.5 : sd == 3 ? -0.5 : 0.0;
