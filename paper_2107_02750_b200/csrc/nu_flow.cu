@@ -97,9 +97,9 @@ __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClo
   if (q >= q1) return;
   const int a = v.seg_l[q], b = v.seg_r[q];  // W/S and E/N leaf
   double sa[9], sb[9];
-  load9(in, a, sa);
-  load9(in, b, sb);
-  const P3 za = load3(v.z, a), zb = load3(v.z, b);
+  load9v(in, a, sa);
+  load9v(in, b, sb);
+  const P3 za = load3v(v.z, a), zb = load3v(v.z, b);
   Pt A, B;
   bool xn;
   if (P2) {
@@ -263,8 +263,8 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   const double inv = v.linv[l];
   const double cx = P2 ? 0.0 : lcen(v.x0, v, l, i), cy = P2 ? 0.0 : lcen(v.y0, v, l, j);
   double s[9];
-  load9(in, kk, s);
-  const P3 zc = load3(v.z, kk);
+  load9v(in, kk, s);
+  const P3 zc = load3v(v.z, kk);
   const int code = v.sk[kk];
   const bool dg2 = v.scheme == FM_DG2;
   // x direction: E and W sides, then the Gauss-point fluxes along x
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
     for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
   } else {
     double u0[9];
-    load9(uold, kk, u0);
+    load9v(uold, kk, u0);
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
       double a = s[q];
@@ -335,11 +335,7 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
       if (cnt) res[0] += ddiv(c->per_cell[f] * cnt, sz * sz);
     }
   }
-  if (valid) {
-    double* o = out + 9 * kk;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) o[q] = res[q];
-  }
+  if (valid) store9v(out, kk, res);
   if (epi) reduce_leaf(v, red, *c, res, sz, leaf_key(l, i, j), valid);
 }
 
