@@ -136,6 +136,8 @@ int64_t fm_launch_count(void);
 /* Device self-checks of the arithmetic building blocks against IEEE:
  * which = 0: the inlined division vs `/` on n seeded random operand pairs;
  * which = 1: the constant-divisor division of project4 (a / (4 sqrt3)) vs `/`;
+ * which = 2: the shared-divisor division of zdiv2 (nvcc's fast-path sequence
+ *            with the reciprocal computed once) vs `a == 0 ? a : a / b`;
  * spanning the fast-path exponent window and its edges.  *failures counts
  * bit mismatches. */
 int fm_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* failures);

@@ -103,6 +103,12 @@ __global__ void k_selftest_div(int which, int64_t n, uint64_t seed, unsigned lon
     if (__double_as_longlong(q1) != __double_as_longlong(r1)) atomicAdd(fails, 1ull);
     return;
   }
+  if (which == 2) {  // the shared-divisor path of zdiv2 (fmd::zquot_ieee)
+    const double q2 = fmd::div_fast_ok(b) ? fmd::zquot_ieee(a, b, fmd::recip_ieee(b)) : fmd::zdiv(a, b);
+    const double r2 = a == 0.0 ? a : a / b;
+    if (__double_as_longlong(q2) != __double_as_longlong(r2)) atomicAdd(fails, 1ull);
+    return;
+  }
   // the inline division kernel builds use with -DFM_INLINE_DIV (fmd::quot)
   const double q = (fmd::div_fast_ok(a) && fmd::div_fast_ok(b)) ? fmd::quot(a, b, fmd::recip(b)) : a / b;
   const double ref = a / b;
@@ -154,7 +160,7 @@ int64_t fm_launch_count(void) { return launches(); }
 int fm_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* failures) {
   return guard([&] {
     require_device();
-    if (which != 0 && which != 1) throw Error(FM_ERR_CONFIG, "unknown self-test");
+    if (which < 0 || which > 2) throw Error(FM_ERR_CONFIG, "unknown self-test");
     DBuf<unsigned long long> f(1);
     f.zero();
     k_selftest_div<<<unsigned((n + 255) / 256), 256, 0, stream()>>>(which, n, seed, f.p);

@@ -249,8 +249,10 @@ __device__ __forceinline__ void reduce_leaf(const NuView& v, DevRed* red, const 
       }
     } else if (h > v.hdry) {
       const double cw = sqrt(v.g * h);
-      const double sx = fabs(zdiv(s[3], h)) + cw;
-      const double sy = fabs(zdiv(s[6], h)) + cw;
+      double ux, uy;
+      zdiv2(s[3], s[6], h, ux, uy);
+      const double sx = fabs(ux) + cw;
+      const double sy = fabs(uy) + cw;
       dtc = ddiv(sz, smax(sx, sy));
     }
     bool fin = true;

@@ -180,10 +180,11 @@ def test_inline_division_is_ieee(gpu):
     """fmd::quot (reciprocal-refinement division: -DFM_INLINE_DIV builds, and
     the constant-divisor division of project4 in every build) returns exactly
     IEEE a / b on 10^8 random operand pairs, and a / (4 sqrt3) on 10^8
-    random numerators."""
+    random numerators; the shared-divisor division of zdiv2 (every build)
+    returns exactly IEEE a / b on 10^8 pairs."""
     import ctypes
     fails = ctypes.c_int64(-1)
-    for which in (0, 1):
+    for which in (0, 1, 2):
         for seed in (1, 2, 3, 4):
             gpu.call("selftest", which, 25_000_000, seed, ctypes.byref(fails))
             assert fails.value == 0, (which, seed)
