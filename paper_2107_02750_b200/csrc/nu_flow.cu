@@ -267,6 +267,10 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   const P3 zc = load3v(v.z, kk);
   const int code = v.sk[kk];
   const bool dg2 = v.scheme == FM_DG2;
+  const bool epi = last && !manual;
+  // the first inflow's count for this leaf, loaded early: its latency
+  // otherwise sits at the end of the leaf's critical path
+  const int cnt0 = (epi && v.ninflow > 0) ? v.infc[kk] : 0;
   // x direction: E and W sides, then the Gauss-point fluxes along x
   const SideOut ee = side_eval<P2>(v, s, zc, kk, 1, (code >> 2) & 3, cx, cy, sz, err);
   const SideOut ew = side_eval<P2>(v, s, zc, kk, 3, (code >> 6) & 3, cx, cy, sz, err);
@@ -326,13 +330,16 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
     }
   }
   positivity(res, v.hdry);
-  const bool epi = last && !manual;
   if (epi && valid) {
-    // apply_inflows (solver_nonuniform.cpp:451-465), inflow order
+    // apply_inflows (solver_nonuniform.cpp:451-465), inflow order.  P2: the
+    // leaf area is a power of two, so / (sz sz) is exactly * (inv inv)
     for (int f = 0; f < v.ninflow; ++f) {
       if (!c->on[f]) continue;
-      const int cnt = v.infc[f * v.n + kk];
-      if (cnt) res[0] += ddiv(c->per_cell[f] * cnt, sz * sz);
+      const int cnt = f == 0 ? cnt0 : v.infc[f * v.n + kk];
+      if (cnt) {
+        const double num = c->per_cell[f] * cnt;
+        res[0] += P2 ? num * (inv * inv) : ddiv(num, sz * sz);
+      }
     }
   }
   if (valid) store9v(out, kk, res);
