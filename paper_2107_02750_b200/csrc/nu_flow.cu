@@ -166,10 +166,13 @@ struct SideOut {
   double h, qx, qy, zd, fm, fn, ft;
 };
 
+#ifndef FM_SID_ROW
+#define FM_SID_ROW 1
+#endif
 template <bool P2>
 __device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9], const P3& zc,
                                              long long kk, int sd, int kind, double cx, double cy,
-                                             double sz, int* err) {
+                                             double sz, int* err, int2 ids) {
   const bool xn = sd == 1 || sd == 3;
   const bool mine_left = sd == 0 || sd == 1;
   const int nseg = kind == 0 ? 0 : kind == 3 ? 2 : 1;
@@ -178,7 +181,12 @@ __device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9],
   for (int t = 0; t < 2; ++t) {
     if (t < nseg) {
       // 48 B state, 16 B aligned: three 16 B loads
-      const double2* q = reinterpret_cast<const double2*>(v.segst + 6 * (long long)v.sid[8 * kk + 2 * sd + t]);
+#if FM_SID_ROW
+      const int id = t == 0 ? ids.x : ids.y;
+#else
+      const int id = v.sid[8 * kk + 2 * sd + t];
+#endif
+      const double2* q = reinterpret_cast<const double2*>(v.segst + 6 * (long long)id);
 #pragma unroll
       for (int e = 0; e < 3; ++e) {
         const double2 w2 = q[e];
@@ -271,9 +279,17 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   // the first inflow's count for this leaf, loaded early: its latency
   // otherwise sits at the end of the leaf's critical path
   const int cnt0 = (epi && v.ninflow > 0) ? v.infc[kk] : 0;
+  // the leaf's segment ids, 2 per side (N E S W), as two 16 B loads
+#if FM_SID_ROW
+  const int4* srow = reinterpret_cast<const int4*>(v.sid + 8 * kk);
+  const int4 s03 = srow[0], s47 = srow[1];
+  const int2 idn{s03.x, s03.y}, ide{s03.z, s03.w}, ids_{s47.x, s47.y}, idw{s47.z, s47.w};
+#else
+  const int2 idn{0, 0}, ide{0, 0}, ids_{0, 0}, idw{0, 0};
+#endif
   // x direction: E and W sides, then the Gauss-point fluxes along x
-  const SideOut ee = side_eval<P2>(v, s, zc, kk, 1, (code >> 2) & 3, cx, cy, sz, err);
-  const SideOut ew = side_eval<P2>(v, s, zc, kk, 3, (code >> 6) & 3, cx, cy, sz, err);
+  const SideOut ee = side_eval<P2>(v, s, zc, kk, 1, (code >> 2) & 3, cx, cy, sz, err, ide);
+  const SideOut ew = side_eval<P2>(v, s, zc, kk, 3, (code >> 6) & 3, cx, cy, sz, err, idw);
   const DirMod X{0.5 * (ee.h + ew.h),   (ee.h - ew.h) * kHalfInvS3,   0.5 * (ee.qx + ew.qx),
                  (ee.qx - ew.qx) * kHalfInvS3, 0.5 * (ee.qy + ew.qy), (ee.qy - ew.qy) * kHalfInvS3,
                  (ee.zd - ew.zd) * kHalfInvS3};
@@ -284,8 +300,8 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   }
   const Flx fe{ee.fm, ee.fn, ee.ft}, fw{ew.fm, ew.fn, ew.ft};
   // y direction
-  const SideOut en = side_eval<P2>(v, s, zc, kk, 0, code & 3, cx, cy, sz, err);
-  const SideOut es = side_eval<P2>(v, s, zc, kk, 2, (code >> 4) & 3, cx, cy, sz, err);
+  const SideOut en = side_eval<P2>(v, s, zc, kk, 0, code & 3, cx, cy, sz, err, idn);
+  const SideOut es = side_eval<P2>(v, s, zc, kk, 2, (code >> 4) & 3, cx, cy, sz, err, ids_);
   const DirMod Y{0.5 * (en.h + es.h),   (en.h - es.h) * kHalfInvS3,   0.5 * (en.qx + es.qx),
                  (en.qx - es.qx) * kHalfInvS3, 0.5 * (en.qy + es.qy), (en.qy - es.qy) * kHalfInvS3,
                  (en.zd - es.zd) * kHalfInvS3};
