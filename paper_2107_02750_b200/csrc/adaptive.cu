@@ -1,25 +1,29 @@
 // Dynamically adaptive MWDG2 / HWFV1 entirely on the device
 // (AdaptiveSim, solver_adaptive.cpp).
 //
-// Every adapt (solver_adaptive.cpp:136-171) runs as level-by-level kernels
-// over dense block-Morton pyramids, with no host round trip for data:
-//   encode_up    (:16-57)   k_mark_leaves + k_encode_up per level
+// Every adapt (solver_adaptive.cpp:136-171) runs on the device over dense
+// block-Morton pyramids, with no host round trip for data.  The per-level
+// passes run each large level as one launch and all levels of <= 256 nodes in
+// one single-CTA launch (run_levels); level-independent passes run every level
+// in one launch (run_levels_flat):
+//   encode_up    (:16-57)   k_mark_leaves + EncodeUpBody per level
 //   norms        (:139-144) k_norms (exact max reductions)
-//   flag         (:59-73)   k_flag per level (static topography significance
+//   flag         (:59-73)   FlagBody (static topography significance
 //                           precomputed once: max(a,b) >= eps <=> a >= eps || b >= eps)
-//   closure      (detail_tree.cpp:56-64) k_closure per level
-//   buffer_ring  (:75-94)   k_ring per level, then closure again
+//   closure      (detail_tree.cpp:56-64) ClosureBody per level
+//   buffer_ring  (:75-94)   RingBody, then closure again
 //   grade_flags  (detail_tree.cpp:97-113) + leaf counts: grade_count_levels
 //   assemble_grid(detail_tree.cpp:132-164): build_leaves (topography decode)
-//   transfer     (:96-134)  k_transfer per level: flow decode top-down with
-//                           stored or zero details; unchanged leaves keep
-//                           their coefficients bit-for-bit (the encode_up
-//                           copy of the old leaf IS the old value)
+//   transfer     (:96-134)  k_transfer_leaves: one thread per new leaf walks
+//                           its ancestor chain, decoding with stored or zero
+//                           details; unchanged leaves keep their coefficients
+//                           bit-for-bit (the encode_up copy of the old leaf IS
+//                           the old value)
 //   remap + rebuild_topology (:173-202, solver_nonuniform.cpp:521-527):
 //                           resolve_manning, resolve_inflows, build_topology,
 //                           and the encode_pairing partner z* of two-segment
 //                           sides (region_topo, solver_nonuniform.cpp:80-89)
-//                           from a z encode-up pyramid (k_zpyr, k_zpair).
+//                           from a z encode-up pyramid (ZpyrBody, k_zpair).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -257,58 +261,51 @@ struct RingBody {
   }
 };
 
-// transfer (solver_adaptive.cpp:96-134), one level of the new tree.
+// transfer as a walk per NEW leaf (one launch instead of one per level):
+// from the level-0 scaling down the leaf's ancestor chain, decoding at each
+// ancestor only the child on the path, with the stored flow details where the
+// ancestor was internal (kInternal) and zero details otherwise — the
+// reference's own DFS order (transfer, solver_adaptive.cpp:96-134).  A leaf that was
+// an old leaf keeps its bits (:114-116).  Each child's decode is decode_k's
+// arithmetic for that child, so this equals a level-by-level decode.
 template <int KIND>
-struct TransferBody {
-  __device__ static void node(int l, uint64_t n, const LvTab& t) {
-    const int L = t.L;
-    if (l > 0 && !t.flag[l - 1][n >> 2]) return;  // not in the new tree
-    double v[9];
-    const double* src = l == 0 ? t.sc[0] + 9 * n : t.fs[l] + 9 * n;
+__global__ void __launch_bounds__(256) k_transfer_leaves(LvTab t, long long n, const int8_t* __restrict__ lvl,
+                                                         const int32_t* __restrict__ li,
+                                                         const int32_t* __restrict__ lj) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int l = lvl[k];
+  const uint64_t nl = node_index(l, li[k], lj[k], t.M);
+  double v[9];
+  if (l > 0 && t.known[l][nl] == 1) {
+    const double* o = t.sc[l] + 9 * nl;
 #pragma unroll
-    for (int q = 0; q < 9; ++q) v[q] = src[q];
-    if (!t.flag[l][n]) {  // a level-0 leaf (deeper leaves are written by their parent)
-      if (l == 0) {
-        double* o = t.unew + 9 * t.off[0][n];
+    for (int q = 0; q < 9; ++q) v[q] = o[q];
+  } else {
+    const double* o = t.sc[0] + 9 * (nl >> (2 * l));
 #pragma unroll
-        for (int q = 0; q < 9; ++q) o[q] = v[q];  // sc[0] = old leaf value when it was one
-      }
-      return;
-    }
-    const bool internal = t.known[l][n] == 2;
-    double kids[4][9];
+    for (int q = 0; q < 9; ++q) v[q] = o[q];
+    for (int m = 0; m < l; ++m) {
+      const uint64_t a = nl >> (2 * (l - m));
+      const int c = int(nl >> (2 * (l - m - 1))) & 3;
+      const bool internal = t.known[m][a] == 2;
+      const double* dd = t.fdet[m] + 27 * a;
 #pragma unroll
-    for (int f = 0; f < 3; ++f) {
-      double d[9];
+      for (int f = 0; f < 3; ++f) {
+        double d[9];
 #pragma unroll
-      for (int q = 0; q < 9; ++q) d[q] = internal ? t.fdet[l][27 * n + 9 * f + q] : 0.0;
-      P3 out[4];
-      decode_k<KIND>(P3{v[3 * f], v[3 * f + 1], v[3 * f + 2]}, d, out);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        kids[c][3 * f] = out[c].c0;
-        kids[c][3 * f + 1] = out[c].cx;
-        kids[c][3 * f + 2] = out[c].cy;
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint64_t ch = 4 * n + c;
-      const bool leaf = l + 1 == L || !t.flag[l + 1][ch];
-      if (leaf) {
-        const int32_t at = l + 1 < L ? t.off[l + 1][ch] : t.off[l][n] + c;
-        double* o = t.unew + 9 * at;
-        const bool old = t.known[l + 1][ch] == 1;  // surviving leaf keeps its bits (:114-116)
-#pragma unroll
-        for (int q = 0; q < 9; ++q) o[q] = old ? t.sc[l + 1][9 * ch + q] : kids[c][q];
-      } else {
-        double* o = t.fs[l + 1] + 9 * ch;
-#pragma unroll
-        for (int q = 0; q < 9; ++q) o[q] = kids[c][q];
+        for (int q = 0; q < 9; ++q) d[q] = internal ? dd[9 * f + q] : 0.0;
+        const P3 o3 = decode_child_k<KIND>(P3{v[3 * f], v[3 * f + 1], v[3 * f + 2]}, d, c);
+        v[3 * f] = o3.c0;
+        v[3 * f + 1] = o3.cx;
+        v[3 * f + 2] = o3.cy;
       }
     }
   }
-};
+  double* o = t.unew + 9 * k;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) o[q] = v[q];
+}
 
 // region_topo (solver_nonuniform.cpp:80-89) for every flagged node
 template <int KIND>
@@ -588,10 +585,13 @@ void adaptive_adapt(Sim& s, double t) {
   DBuf<double> u_new(9 * n_new);
   tab = lv_tab(s, g, a);
   tab.unew = u_new.p;
-  if (a.kind == 0)
-    run_levels<TransferBody<0>>(tab, 0, L - 1, false);
-  else
-    run_levels<TransferBody<1>>(tab, 0, L - 1, false);
+  if (n_new) {
+    if (a.kind == 0)
+      k_transfer_leaves<0><<<nblk(n_new, 256), 256, 0, st>>>(tab, n_new, g.lf_l.p, g.lf_i.p, g.lf_j.p);
+    else
+      k_transfer_leaves<1><<<nblk(n_new, 256), 256, 0, st>>>(tab, n_new, g.lf_l.p, g.lf_i.p, g.lf_j.p);
+    FM_LAUNCHED();
+  }
   s.u = std::move(u_new);
   s.us.alloc(9 * n_new);
   copy_leaves_from_grid(s, g);
