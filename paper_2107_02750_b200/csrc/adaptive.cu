@@ -47,7 +47,6 @@ struct AdaptState {
   std::vector<DBuf<uint8_t>> known;  // [L+1] 0 unknown, 1 leaf, 2 internal
   std::vector<DBuf<double>> sc;      // [L+1] flow scaling, 9 per node
   std::vector<DBuf<double>> fdet;    // [L] flow details, 27 per node
-  std::vector<DBuf<double>> fs;      // [L] top-down flow scratch, 9 per node
   std::vector<DBuf<double>> zp;      // [L] z encode-up pyramid, 3 per node
   std::vector<DBuf<uint8_t>> tmp;    // [L] ring scratch
   DBuf<unsigned long long> norms;    // 3
@@ -173,7 +172,6 @@ struct LvTab {
   const uint8_t* zsig[kMaxLv];
   uint8_t* flag[kMaxLv];
   uint8_t* tmp[kMaxLv];
-  double* fs[kMaxLv];
   double* zp[kMaxLv];
   const int32_t* off[kMaxLv];
   const unsigned long long* norms;
@@ -405,7 +403,6 @@ LvTab lv_tab(Sim& s, Grid& g, AdaptState& a) {
     t.zsig[l] = a.zsig[l].p;
     t.flag[l] = g.flag[l].p;
     t.tmp[l] = a.tmp[l].p;
-    t.fs[l] = a.fs[l].p;
     t.zp[l] = a.zp[l].p;
     t.off[l] = g.off.size() > size_t(l) ? g.off[l].p : nullptr;
   }
@@ -482,7 +479,6 @@ void adaptive_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem) {
   a.known.resize(L + 1);
   a.sc.resize(L + 1);
   a.fdet.resize(L);
-  a.fs.resize(L);
   a.zp.resize(L);
   a.tmp.resize(L);
   for (int l = 0; l <= L; ++l) {
@@ -493,7 +489,6 @@ void adaptive_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem) {
       a.zsig[l].alloc(nodes);
       FM_CUDA(cudaMemcpyAsync(a.zsig[l].p, g.flag[l].p, nodes, cudaMemcpyDeviceToDevice, st));
       a.fdet[l].alloc(27 * nodes);
-      a.fs[l].alloc(9 * nodes);
       a.zp[l].alloc(3 * nodes);
       a.tmp[l].alloc(nodes);
     }

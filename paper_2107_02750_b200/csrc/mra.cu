@@ -247,11 +247,9 @@ __global__ void k_copy_fine(VertexView vv, const Scalars* __restrict__ s, double
 // edge-adjacent to P's child block, and G(l+1) is final before level l is
 // visited in both formulations.  (Verified against the oracle on random trees
 // in tests/test_mra_gpu.py.)
-__global__ void k_grade_count(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
-                              int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1, int l,
-                              int L, int M, int N, uint64_t nodes, int graded) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= nodes) return;
+__device__ __forceinline__ void grade_count_node(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
+                                                 int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1,
+                                                 int l, int L, int M, int N, uint64_t n, int graded) {
   int g = fl[n];
   int c = 1;
   if (l + 1 < L) {
@@ -282,6 +280,34 @@ __global__ void k_grade_count(uint8_t* __restrict__ fl, const uint8_t* __restric
   }
   fl[n] = uint8_t(g);
   cnt[n] = c;
+}
+__global__ void k_grade_count(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
+                              int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1, int l,
+                              int L, int M, int N, uint64_t nodes, int graded) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n < nodes) grade_count_node(fl, fl1, cnt, cnt1, l, L, M, N, n, graded);
+}
+
+// The small levels (<= kSmallLevelNodes nodes, all at the coarse end) of the
+// per-level passes in ONE single-CTA launch, walking the levels in the pass's
+// order with a barrier between levels: at the coarse end a launch per level
+// costs more than the level's work.
+constexpr uint64_t kSmallLevelNodes = 256;
+struct LevelPtrs {
+  uint8_t* fl[kMaxL];
+  int32_t* cnt[kMaxL];
+  int32_t* off[kMaxL];
+  double* zs[kMaxL];  // zs[0] = the level-0 scaling
+  const double* det[kMaxL];
+};
+__global__ void __launch_bounds__(256) k_grade_count_small(LevelPtrs p, int lhi, int L, int M, int N, int graded) {
+  for (int l = lhi; l >= 0; --l) {
+    const uint64_t nodes = uint64_t(M) * N << (2 * l);
+    for (uint64_t n = threadIdx.x; n < nodes; n += blockDim.x)
+      grade_count_node(p.fl[l], l + 1 < L ? p.fl[l + 1] : nullptr, p.cnt[l], l + 1 < L ? p.cnt[l + 1] : nullptr, l,
+                       L, M, N, n, graded);
+    __syncthreads();
+  }
 }
 
 // Exclusive scan of the level-0 counts (M*N nodes) in one CTA.
@@ -333,14 +359,12 @@ __device__ __forceinline__ void emit_leaf(const LeafOut& o, int l, uint64_t node
 // node decodes its stored details into its four children; children that are
 // leaves are emitted at their final index, the others pass their plane and
 // offset down through the level-(l+1) scratch.
-__global__ void k_topdown(const uint8_t* __restrict__ flp, const uint8_t* __restrict__ fl,
-                          const uint8_t* __restrict__ fl1, const int32_t* __restrict__ cnt1,
-                          const int32_t* __restrict__ off, int32_t* __restrict__ off1,
-                          const double* __restrict__ zin, double* __restrict__ zout,
-                          const double* __restrict__ det, int l, int L, int M, int kind,
-                          uint64_t nodes, LeafOut out) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= nodes) return;
+__device__ __forceinline__ void topdown_node(const uint8_t* __restrict__ flp, const uint8_t* __restrict__ fl,
+                                             const uint8_t* __restrict__ fl1, const int32_t* __restrict__ cnt1,
+                                             const int32_t* __restrict__ off, int32_t* __restrict__ off1,
+                                             const double* __restrict__ zin, double* __restrict__ zout,
+                                             const double* __restrict__ det, int l, int L, int M, int kind,
+                                             uint64_t n, const LeafOut& out) {
   if (l > 0 && !flp[n >> 2]) return;
   const P3 z{zin[3 * n], zin[3 * n + 1], zin[3 * n + 2]};
   const int32_t o = off[n];
@@ -371,6 +395,27 @@ __global__ void k_topdown(const uint8_t* __restrict__ flp, const uint8_t* __rest
       off1[c] = run;
       run += cnt1[c];
     }
+  }
+}
+__global__ void k_topdown(const uint8_t* __restrict__ flp, const uint8_t* __restrict__ fl,
+                          const uint8_t* __restrict__ fl1, const int32_t* __restrict__ cnt1,
+                          const int32_t* __restrict__ off, int32_t* __restrict__ off1,
+                          const double* __restrict__ zin, double* __restrict__ zout,
+                          const double* __restrict__ det, int l, int L, int M, int kind,
+                          uint64_t nodes, LeafOut out) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n < nodes) topdown_node(flp, fl, fl1, cnt1, off, off1, zin, zout, det, l, L, M, kind, n, out);
+}
+__global__ void __launch_bounds__(256) k_topdown_small(LevelPtrs p, int lhi, int L, int M, int N, int kind,
+                                                       LeafOut out) {
+  for (int l = 0; l <= lhi; ++l) {
+    const uint64_t nodes = uint64_t(M) * N << (2 * l);
+    const bool last = l + 1 == L;
+    for (uint64_t n = threadIdx.x; n < nodes; n += blockDim.x)
+      topdown_node(l ? p.fl[l - 1] : nullptr, p.fl[l], last ? nullptr : p.fl[l + 1],
+                   last ? nullptr : p.cnt[l + 1], p.off[l], last ? nullptr : p.off[l + 1], p.zs[l],
+                   last ? nullptr : p.zs[l + 1], p.det[l], l, L, M, kind, n, out);
+    __syncthreads();
   }
 }
 
@@ -455,7 +500,23 @@ int64_t build_leaves(Grid& g) {
   // decoded-plane scratch per level (levels 1..L-1)
   std::vector<DBuf<double>> zs(L);
   for (int l = 1; l < L; ++l) zs[l].alloc(3 * g.nodes(l));
-  for (int l = 0; l < L; ++l) {
+  // the small coarse levels in one single-CTA launch, then a launch per level
+  int ls = -1;
+  for (int l = 0; l < L; ++l)
+    if (g.nodes(l) <= kSmallLevelNodes) ls = l;
+  if (ls >= 0) {
+    LevelPtrs p{};
+    for (int l = 0; l < L; ++l) {
+      p.fl[l] = g.flag[l].p;
+      p.cnt[l] = g.cnt[l].p;
+      p.off[l] = g.off[l].p;
+      p.zs[l] = l ? zs[l].p : g.coarse.p;
+      p.det[l] = g.det[l].p;
+    }
+    k_topdown_small<<<1, 256, 0, st>>>(p, ls, L, g.M, g.N, g.kind, out);
+    FM_LAUNCHED();
+  }
+  for (int l = ls + 1; l < L; ++l) {
     const uint64_t nodes = g.nodes(l);
     const bool last = l + 1 == L;
     k_topdown<<<blocks_for(nodes, 256), 256, 0, st>>>(
@@ -590,11 +651,23 @@ void grade_count_levels(Grid& g, bool graded) {
   const int L = g.L;
   g.cnt.resize(L);
   for (int l = 0; l < L; ++l) g.cnt[l].alloc(g.nodes(l));
-  for (int l = L - 1; l >= 0; --l) {
+  int ls = -1;  // the finest small level
+  for (int l = 0; l < L; ++l)
+    if (g.nodes(l) <= kSmallLevelNodes) ls = l;
+  for (int l = L - 1; l > ls; --l) {
     const uint64_t nodes = g.nodes(l);
     k_grade_count<<<blocks_for(nodes, 256), 256, 0, st>>>(
         g.flag[l].p, l + 1 < L ? g.flag[l + 1].p : nullptr, g.cnt[l].p,
         l + 1 < L ? g.cnt[l + 1].p : nullptr, l, L, g.M, g.N, nodes, graded ? 1 : 0);
+    FM_LAUNCHED();
+  }
+  if (ls >= 0) {
+    LevelPtrs p{};
+    for (int l = 0; l < L; ++l) {
+      p.fl[l] = g.flag[l].p;
+      p.cnt[l] = g.cnt[l].p;
+    }
+    k_grade_count_small<<<1, 256, 0, st>>>(p, ls, L, g.M, g.N, graded ? 1 : 0);
     FM_LAUNCHED();
   }
 }
