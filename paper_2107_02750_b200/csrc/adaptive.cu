@@ -89,10 +89,21 @@ __global__ void k_norms(long long n, const double* __restrict__ u, unsigned long
     b = smax(b, __shfl_xor_sync(0xffffffffu, b, o));
     c = smax(c, __shfl_xor_sync(0xffffffffu, c, o));
   }
+  // then across the block's warps as the same max over bit patterns the
+  // atomics take (|c0| >= 0 orders as its bits), so one atomic per block and
+  // field: per-warp atomics on three addresses serialised ~9k atomics per adapt
+  __shared__ unsigned long long sm[3][32];
+  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   if ((threadIdx.x & 31) == 0) {
-    atomicMax(out, dbits(a));
-    atomicMax(out + 1, dbits(b));
-    atomicMax(out + 2, dbits(c));
+    sm[0][w] = dbits(a);
+    sm[1][w] = dbits(b);
+    sm[2][w] = dbits(c);
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    unsigned long long m = 0;
+    for (int q = 0; q < nw; ++q) m = m > sm[threadIdx.x][q] ? m : sm[threadIdx.x][q];
+    atomicMax(out + threadIdx.x, m);
   }
 }
 
