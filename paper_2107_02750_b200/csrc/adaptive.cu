@@ -196,19 +196,28 @@ template <int KIND>
 struct EncodeUpBody {
   __device__ static void node(int l, uint64_t n, const LvTab& t) {
     uint8_t* kn = t.known[l];
-    if (kn[n] != 0) return;
+    // both flags in one round trip
+    const uint8_t kself = kn[n];
     const uint32_t k4 = *reinterpret_cast<const uint32_t*>(t.known[l + 1] + 4 * n);
+    if (kself != 0) return;
     if ((k4 & 0xffu) == 0 || (k4 & 0xff00u) == 0 || (k4 & 0xff0000u) == 0 || (k4 & 0xff000000u) == 0) return;
-    const double* sc1 = t.sc[l + 1];
+    // the four children's rows are 36 contiguous, 16 B aligned doubles: load
+    // them all before any store (the stores below could alias them for the
+    // compiler, which would otherwise serialise a round trip per field)
+    double ch[36];
+    const double2* src = reinterpret_cast<const double2*>(t.sc[l + 1] + 36 * n);
+#pragma unroll
+    for (int q = 0; q < 18; ++q) {
+      const double2 w = src[q];
+      ch[2 * q] = w.x;
+      ch[2 * q + 1] = w.y;
+    }
     // encode_flow (wavelets.cpp:102-120): h, qx, qy independently
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
       P3 kids[4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const double* s = sc1 + 9 * (4 * n + c) + 3 * f;
-        kids[c] = P3{s[0], s[1], s[2]};
-      }
+      for (int c = 0; c < 4; ++c) kids[c] = P3{ch[9 * c + 3 * f], ch[9 * c + 3 * f + 1], ch[9 * c + 3 * f + 2]};
       P3 p;
       double d[9];
       encode_k<KIND>(kids, p, d);
