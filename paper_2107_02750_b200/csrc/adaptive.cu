@@ -587,11 +587,12 @@ void adaptive_adapt(Sim& s, double t) {
   // flag + closure
   run_levels_flat<FlagBody>(tab, 0, L - 1);
   run_levels<ClosureBody>(tab, 0, L - 2, true);
-  // buffer_ring + closure
+  // buffer_ring; its ancestor closure is subsumed by the grading pass: the
+  // gather form of grade_flags sets G(l) = F(l) | any child G(l+1) | ring,
+  // bottom-up, so G(closure(F)) = G(F) level by level (the closure's child
+  // term is contained in G's)
   run_levels_flat<RingBody>(tab, 0, L - 1);
   for (int l = 0; l < L; ++l) std::swap(g.flag[l], a.tmp[l]);
-  tab = lv_tab(s, g, a);
-  run_levels<ClosureBody>(tab, 0, L - 2, true);
   // grade + counts + leaves + exact topography (assemble_grid)
   grade_count_levels(g, true);
   build_leaves(g);

@@ -209,6 +209,43 @@ def test_grading_random_trees(orc):
         assert np.array_equal(f, g2)  # idempotent
 
 
+def gather_grade(flat, L, M, N):
+    """The gather form of grading the device runs (mra.cu k_grade_count),
+    applied WITHOUT a prior ancestor closure, bottom-up: G(l) = F(l) | any
+    child G(l+1) | any G(l+1) among the 8 ring nodes around the child block."""
+    levels, at = [], 0
+    for l in range(L):
+        n = (N << l) * (M << l)
+        levels.append(flat[at:at + n].reshape(N << l, M << l).copy())
+        at += n
+    for l in range(L - 2, -1, -1):
+        fine = levels[l + 1]
+        h, w = fine.shape
+        pad = np.zeros((h + 2, w + 2), np.uint8)
+        pad[1:-1, 1:-1] = fine
+        G = levels[l].copy()
+        for j in range(N << l):
+            for i in range(M << l):
+                cj, ci = 2 * j + 1, 2 * i + 1  # the child block in padded coordinates
+                kids = pad[cj:cj + 2, ci:ci + 2].any()
+                ring = (pad[cj:cj + 2, ci - 1].any() or pad[cj:cj + 2, ci + 2].any()
+                        or pad[cj - 1, ci:ci + 2].any() or pad[cj + 2, ci:ci + 2].any())
+                G[j, i] |= bool(kids or ring)
+        levels[l] = G
+    return np.concatenate([x.ravel() for x in levels])
+
+
+def test_closure_subsumed_by_gather_grading(orc):
+    """adaptive.cu skips buffer_ring's ancestor closure before grading:
+    grading in gather form on the UNCLOSED flags equals the reference's
+    closure + grade_flags (the oracle, pinned to the reference)."""
+    for L, M, N in [(4, 2, 1), (5, 1, 1), (4, 3, 2)]:
+        for flat in random_flag_trees(301 + L, 40, L=L, M=M, N=N):
+            a = flat.copy()
+            orc.call("grade_flags", L, M, N, 1, u8p(a))
+            assert np.array_equal(gather_grade(flat, L, M, N), a)
+
+
 def test_grid_properties(orc):  # test_mra.cpp:61-211
     flat = S.Raster(np.full((17, 17), 4.0))
     g = orc.grid(flat, 2, 1e-3)
