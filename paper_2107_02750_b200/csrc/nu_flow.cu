@@ -26,6 +26,11 @@
 
 // minimum resident CTAs per SM (register caps; tuned on B200 with
 // scripts/ab_profile.py)
+// 1: the segment and stage kernels have no early exit on inactive steps (A/B
+// on B200: 0.799 -> 0.792 ms/step; the row loads issue ahead of the clock load)
+#ifndef FM_NO_EXIT
+#define FM_NO_EXIT 1
+#endif
 #ifndef FM_SEG_MINB
 #define FM_SEG_MINB 4  // 64 registers: 4 CTAs of 256 threads per SM
 #endif
@@ -93,9 +98,15 @@ __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClo
                                              const double* __restrict__ in, double* __restrict__ out,
                                              int manual, int* err, long long q0, long long q1) {
   const long long q = q0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (!manual && !clk[1].active) return;
   if (q >= q1) return;
-  const int a = v.seg_l[q], b = v.seg_r[q];  // W/S and E/N leaf
+  const int a = v.seg_l[q], b = v.seg_r[q];  // W/S and E/N leaf (loaded before the active check)
+#if FM_NO_EXIT
+  const bool act = manual || clk[1].active;
+  if (!act) err = nullptr;
+#else
+  if (!manual && !clk[1].active) return;
+  const bool act = true;
+#endif
   double sa[9], sb[9];
   load9v(in, a, sa);
   load9v(in, b, sb);
@@ -144,6 +155,7 @@ __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClo
   const double unA = xn ? A.u : A.v, utA = xn ? A.v : A.u;
   const double unB = xn ? B.u : B.v, utB = xn ? B.v : B.u;
   const Flx f = hll_inl(hl, hl * unA, hl * utA, hr, hr * unB, hr * utB, v.g, v.hdry, err);
+  if (!act) return;
   double2* o = reinterpret_cast<double2*>(out + 6 * q);  // 16 B aligned
   o[0] = make_double2(f.m, f.n);
   o[1] = make_double2(f.t, zs);
@@ -261,24 +273,16 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
     NuView v, const DevClock* __restrict__ clk, DevRed* red, const double* __restrict__ in,
     const double* uold, double* out, int last, int manual, double mdt, int* err) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const DevClock* c = clk + 1;
-  if (!manual && !c->active) return;
-  const double dt = manual ? mdt : c->dt;
   const bool valid = k < v.n;
   const long long kk = valid ? k : v.n - 1;
+  // the leaf's rows are loaded before the step-active check: they do not
+  // depend on it, and the check's clock load would otherwise put a second
+  // round trip in front of the first gathers
   const int l = v.lvl[kk], i = v.li[kk], j = v.lj[kk];
-  const double sz = lsize(v, l);
-  const double inv = v.linv[l];
-  const double cx = P2 ? 0.0 : lcen(v.x0, v, l, i), cy = P2 ? 0.0 : lcen(v.y0, v, l, j);
   double s[9];
   load9v(in, kk, s);
   const P3 zc = load3v(v.z, kk);
   const int code = v.sk[kk];
-  const bool dg2 = v.scheme == FM_DG2;
-  const bool epi = last && !manual;
-  // the first inflow's count for this leaf, loaded early: its latency
-  // otherwise sits at the end of the leaf's critical path
-  const int cnt0 = (epi && v.ninflow > 0) ? v.infc[kk] : 0;
   // the leaf's segment ids, 2 per side (N E S W), as two 16 B loads
 #if FM_SID_ROW
   const int4* srow = reinterpret_cast<const int4*>(v.sid + 8 * kk);
@@ -287,6 +291,26 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
 #else
   const int2 idn{0, 0}, ide{0, 0}, ids_{0, 0}, idw{0, 0};
 #endif
+  const DevClock* c = clk + 1;
+#if FM_NO_EXIT
+  // no early exit: an inactive step (rare: the tail of a graph batch after an
+  // event) computes on a stale dt with every side effect predicated off, so
+  // the compiler keeps all the row loads ahead of the clock load
+  const bool act = manual || c->active;
+  if (!act) err = nullptr;
+#else
+  if (!manual && !c->active) return;
+  const bool act = true;
+#endif
+  const double dt = manual ? mdt : c->dt;
+  const double sz = lsize(v, l);
+  const double inv = v.linv[l];
+  const double cx = P2 ? 0.0 : lcen(v.x0, v, l, i), cy = P2 ? 0.0 : lcen(v.y0, v, l, j);
+  const bool dg2 = v.scheme == FM_DG2;
+  const bool epi = last && !manual;
+  // the first inflow's count for this leaf, loaded early: its latency
+  // otherwise sits at the end of the leaf's critical path
+  const int cnt0 = (epi && v.ninflow > 0) ? v.infc[kk] : 0;
   // x direction: E and W sides, then the Gauss-point fluxes along x
   const SideOut ee = side_eval<P2>(v, s, zc, kk, 1, (code >> 2) & 3, cx, cy, sz, err, ide);
   const SideOut ew = side_eval<P2>(v, s, zc, kk, 3, (code >> 6) & 3, cx, cy, sz, err, idw);
@@ -358,8 +382,8 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
       }
     }
   }
-  if (valid) store9v(out, kk, res);
-  if (epi) reduce_leaf(v, red, *c, res, sz, leaf_key(l, i, j), valid);
+  if (valid && act) store9v(out, kk, res);
+  if (epi && act) reduce_leaf(v, red, *c, res, sz, leaf_key(l, i, j), valid);
 }
 
 // ---- one RK stage, two lanes per leaf ---------------------------------------
