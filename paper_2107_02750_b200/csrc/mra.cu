@@ -2,7 +2,7 @@
 //
 // Replaces generate_static_grid (detail_tree.cpp:172-178) and its stages:
 //   project_raster      field.cpp:64-117     -> fused into k_encode_tiles
-//   build_detail_tree   detail_tree.cpp:10-54 -> k_field_norm + k_encode_tiles
+//   build_detail_tree   detail_tree.cpp:10-54 -> k_dem_stats (+ k_field_norm_fix) + k_encode_tiles
 //   flag_significant    detail_tree.cpp:66-74 -> sig flags in k_encode_tiles
 //   ancestor_closure +  detail_tree.cpp:56-64,
 //   grade_flags                      :97-113 -> k_grade_count (one gather pass per level)
@@ -41,11 +41,13 @@ __device__ __forceinline__ double from_ordered(unsigned long long u) {
   return bitsd((u >> 63) ? (u & 0x7fffffffffffffffull) : ~u);
 }
 
+constexpr int kNodataSeen = 1, kBig = 2;
+
 struct Scalars {
   unsigned long long vmax_ord;  // ordered max over non-nodata vertices
   unsigned long long norm_bits; // max |c0| (non-negative)
   int err;                      // 1: non-finite vertex
-  int pad;
+  int flags;                    // kNodataSeen | kBig (k_dem_stats)
   double wall;
   double norm;
 };
@@ -94,11 +96,63 @@ __global__ void k_wall(Scalars* s) {
   double z = from_ordered(s->vmax_ord);
   if (!isfinite(z)) z = 0.0;
   s->wall = z + 100.0;
+  // k_dem_stats' norm left out the cells with a nodata vertex: redo it
+  if (s->flags & kNodataSeen) s->norm_bits = 0;
+}
+
+// One pass over the elements for the static MRA: the nodata-wall maximum
+// (field.cpp:48-54), the non-finite check, and field_norm
+// (detail_tree.cpp:22-23).  Each element checks its SW vertex (plus the north
+// row and east column at the raster's edges), so every vertex is checked once;
+// the norm is taken over the raw vertex values, which is field_norm exactly
+// when the DEM has no nodata vertex (otherwise k_wall resets it and
+// k_field_norm_fix recomputes it with the wall).  kBig marks a vertex above
+// 1e300 in magnitude: the encode then keeps its zero filter taps.
+__global__ void k_dem_stats(VertexView vv, Scalars* s) {
+  double m = -INFINITY, nm = 0.0;
+  int bad = 0, fl = 0;
+  auto chk = [&](double x) {
+    if (x != vv.nodata) {
+      m = smax(m, x);
+      if (!isfinite(x)) bad = 1;
+      if (fabs(x) > 1e300) fl |= kBig;
+    } else {
+      fl |= kNodataSeen;
+    }
+  };
+  // element rows over CTAs, columns over threads (coalesced, no index division)
+  for (int j = blockIdx.x; j < vv.m; j += gridDim.x) {
+    const int rs = vv.nrows - 1 - j, rn = rs - 1;
+    const double* vn = vv.v + size_t(rn) * vv.ncols;
+    const double* vs = vv.v + size_t(rs) * vv.ncols;
+    for (int i = threadIdx.x; i < vv.n; i += blockDim.x) {
+      const double nw = vn[i], ne = vn[i + 1], sw = vs[i], se = vs[i + 1];
+      chk(sw);
+      if (i == vv.n - 1) chk(se);
+      if (rn == 0) {
+        chk(nw);
+        if (i == vv.n - 1) chk(ne);
+      }
+      nm = smax(nm, fabs(0.25 * (ne + nw + se + sw)));  // project4's c0 (field.cpp:15)
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    m = smax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    nm = smax(nm, __shfl_xor_sync(0xffffffffu, nm, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    fl |= __shfl_xor_sync(0xffffffffu, fl, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&s->vmax_ord, ordered_bits(m));
+    if (nm > 0.0) atomicMax(&s->norm_bits, dbits(nm));
+    if (bad) atomicOr(&s->err, 1);
+    if (fl) atomicOr(&s->flags, fl);
+  }
 }
 
 // detail_tree.cpp:22-23 — field_norm = max |c0| over the fine elements.
-__global__ void k_field_norm(VertexView vv, const Scalars* __restrict__ sin, Scalars* s) {
-  vv.wall = sin->wall;
+__device__ __forceinline__ void k_field_norm_body(VertexView vv, Scalars* s) {
+  vv.wall = s->wall;
   const size_t total = size_t(vv.n) * vv.m;
   double m = 0.0;
   for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < total;
@@ -109,6 +163,12 @@ __global__ void k_field_norm(VertexView vv, const Scalars* __restrict__ sin, Sca
   }
   for (int o = 16; o; o >>= 1) m = smax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(&s->norm_bits, dbits(m));
+}
+
+// field_norm again, with the wall, only when the DEM has nodata vertices (see k_dem_stats)
+__global__ void k_field_norm_fix(VertexView vv, Scalars* s) {
+  if (!(s->flags & kNodataSeen)) return;
+  k_field_norm_body(vv, s);
 }
 
 __global__ void k_norm_final(Scalars* s) { s->norm = bitsd(s->norm_bits); }
@@ -146,8 +206,14 @@ __device__ __forceinline__ void store_details(const double* __restrict__ sdet, d
   for (int e = tid; e < total / 2; e += nthr) dst[e] = src[e];
 }
 
+#ifndef FM_ENC_MINB
+#define FM_ENC_MINB 5  // 51 registers (A/B on B200: MRA 2.31 -> 1.69 ms)
+#endif
+#ifndef FM_ENC_T
+#define FM_ENC_T 5  // levels per encode pass (4^(T-1) threads per CTA)
+#endif
 template <bool FROM_VERTICES>
-__global__ void __launch_bounds__(256) k_encode_tiles(EncParams p) {
+__global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) {
   extern __shared__ double smem[];
   const int nthr = blockDim.x;
   P3* sbuf = reinterpret_cast<P3*>(smem);
@@ -155,6 +221,8 @@ __global__ void __launch_bounds__(256) k_encode_tiles(EncParams p) {
   const int tid = threadIdx.x;
   const uint64_t tile = blockIdx.x;
   const double norm = p.scal->norm;
+  // every input finite (a non-finite vertex fails the build) and bounded
+  const bool skip0 = !(p.scal->flags & kBig);
   // a register copy: writing into the by-value parameter struct would make
   // every thread spill the whole 344-byte EncParams to local memory
   VertexView vv = p.vv;
@@ -179,7 +247,7 @@ __global__ void __launch_bounds__(256) k_encode_tiles(EncParams p) {
   }
   P3 par_s;
   double d[9];
-  encode(kids, p.kind, par_s, d);
+  encode_b(kids, p.kind, skip0, par_s, d);
 #pragma unroll
   for (int n = 0; n < 9; ++n) sdet[9 * tid + n] = d[n];
   p.flag[lev][par] = dhat(d, norm) >= p.eps ? 1 : 0;
@@ -204,7 +272,7 @@ __global__ void __launch_bounds__(256) k_encode_tiles(EncParams p) {
     if (have) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) kids[k] = sbuf[4 * tid + k];
-      encode(kids, p.kind, mine, d);
+      encode_b(kids, p.kind, skip0, mine, d);
       p.flag[lev][node0 + tid] = dhat(d, norm) >= p.eps ? 1 : 0;
     }
     __syncthreads();  // sbuf reads and the previous sdet stores are done
@@ -576,7 +644,7 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
   // tile-root scaling buffers of the multi-pass encode
   std::vector<int> passes;
   for (int lev_in = L; lev_in > 0;) {
-    const int T = std::min(5, lev_in);
+    const int T = std::min(FM_ENC_T, lev_in);
     passes.push_back(T);
     lev_in -= T;
   }
@@ -592,12 +660,12 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
   cudaEvent_t e0 = ev.a, e1 = ev.b;
   FM_CUDA(cudaEventRecord(e0, st));
 
-  k_vertex_max<<<148 * 8, 256, 0, st>>>(vdev, nv, dem->nodata, scal.p);
+  VertexView vv{vdev, dem->ncols, dem->nrows, n, m, dem->nodata, 0.0};
+  k_dem_stats<<<148 * 8, 256, 0, st>>>(vv, scal.p);
   FM_LAUNCHED();
   k_wall<<<1, 1, 0, st>>>(scal.p);
   FM_LAUNCHED();
-  VertexView vv{vdev, dem->ncols, dem->nrows, n, m, dem->nodata, 0.0};
-  k_field_norm<<<148 * 8, 256, 0, st>>>(vv, scal.p, scal.p);
+  k_field_norm_fix<<<148 * 8, 256, 0, st>>>(vv, scal.p);
   FM_LAUNCHED();
   k_norm_final<<<1, 1, 0, st>>>(scal.p);
   FM_LAUNCHED();

@@ -75,7 +75,38 @@ def test_nodata_walls(gpu, orc):
     v = rng.uniform(0, 3, (65, 65))
     v[10:14, 20:30] = -9999.0
     dem = S.Raster(v, cellsize=1.0)
-    assert same_grid(gpu.grid(dem, 6, 1e-3), orc.grid(dem, 6, 1e-3))
+    g, o = gpu.grid(dem, 6, 1e-3), orc.grid(dem, 6, 1e-3)
+    assert same_grid(g, o)
+    # the norm is recomputed with the wall when the DEM has nodata (k_field_norm_fix)
+    assert g.info() == o.info()
+    for l in range(6):
+        assert np.array_equal(g.dhat(l), o.dhat(l)), l
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_details_bit_exact_all_levels(gpu, orc, kind):
+    # normalised details of every node: the encode's zero-tap elision (inputs
+    # finite and bounded) gives the same bits as the full filter bank
+    sc = S.config1(2)
+    g, o = gpu.grid(sc.dem, sc.L, sc.eps, True, kind), orc.grid(sc.dem, sc.L, sc.eps, True, kind)
+    assert g.info() == o.info()
+    for l in range(sc.L):
+        assert np.array_equal(g.dhat(l), o.dhat(l)), l
+        assert np.array_equal(g.flags(l), o.flags(l)), l
+
+
+@pytest.mark.parametrize("scale", [1e306, 1.7e308])
+def test_huge_elevations_keep_full_filter_bank(gpu, orc, scale):
+    # |z| > 1e300: the encode keeps its zero taps (kBig); at 1.7e308 the planes
+    # overflow (norm = inf, NaN details) the same way as the reference's
+    rng = np.random.default_rng(5)
+    v = rng.uniform(-1.0, 1.0, (33, 33)) * scale
+    v[0, 0] = 0.0
+    dem = S.Raster(v, cellsize=1.0)
+    g, o = gpu.grid(dem, 5, 1e-3), orc.grid(dem, 5, 1e-3)
+    assert all(np.array_equal(x, y, equal_nan=x.dtype.kind == "f") for x, y in zip(g.leaves(), o.leaves()))
+    for l in range(5):
+        assert np.array_equal(g.dhat(l), o.dhat(l), equal_nan=True), l
 
 
 def test_grading_random_trees_match_oracle(gpu, orc):
