@@ -6,7 +6,8 @@
 // scattering 200 MB of state on the host cost ~0.4 s per download for
 // config 4; here the leaf keys (level << 58 | j << 29 | i, the reference's
 // own leaf_key layout) are radix-sorted on the device once per leaf set, and
-// every transfer is a device gather/scatter plus one contiguous copy.
+// every transfer is a device gather/scatter plus one contiguous copy (into
+// page-locked host memory the gather writes the host rows directly).
 #include <cub/device/device_radix_sort.cuh>
 
 #include "fm_device.cuh"
@@ -61,6 +62,20 @@ __global__ void k_widen(int64_t n, const int32_t* __restrict__ perm, const int8_
   if (r < n) out[r] = lvl[perm[r]];
 }
 
+// The device view of a page-locked host buffer (cudaHostAlloc / registered,
+// mapped under unified addressing), or nullptr for pageable memory.  A gather
+// into such a buffer writes the host rows straight over PCIe: no staging
+// buffer to allocate and no separate copy.
+template <typename T>
+T* mapped_host(T* host) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? static_cast<T*>(a.devicePointer) : nullptr;
+}
+
 }  // namespace
 
 const int32_t* sim_ref_perm(Sim& s) {
@@ -90,6 +105,12 @@ void gather_rows(const int32_t* perm, int64_t n, int width, const double* src, d
     FM_CUDA(cudaMemcpyAsync(host_dst, src, size_t(n) * width * sizeof(double), cudaMemcpyDeviceToHost, st));
     return;
   }
+  if (double* d = mapped_host(host_dst)) {
+    k_gather<double><<<nblk(n * width, 256), 256, 0, st>>>(n, width, perm, src, d);
+    FM_LAUNCHED();
+    FM_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
   DBuf<double> tmp(std::max<int64_t>(n * width, 1));
   k_gather<double><<<nblk(n * width, 256), 256, 0, st>>>(n, width, perm, src, tmp.p);
   FM_LAUNCHED();
@@ -103,6 +124,12 @@ void gather_i32(const int32_t* perm, int64_t n, const int32_t* src, int32_t* hos
     FM_CUDA(cudaMemcpyAsync(host_dst, src, size_t(n) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     return;
   }
+  if (int32_t* d = mapped_host(host_dst)) {
+    k_gather<int32_t><<<nblk(n, 256), 256, 0, st>>>(n, 1, perm, src, d);
+    FM_LAUNCHED();
+    FM_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
   DBuf<int32_t> tmp(std::max<int64_t>(n, 1));
   k_gather<int32_t><<<nblk(n, 256), 256, 0, st>>>(n, 1, perm, src, tmp.p);
   FM_LAUNCHED();
@@ -112,6 +139,12 @@ void gather_i32(const int32_t* perm, int64_t n, const int32_t* src, int32_t* hos
 
 void gather_levels(const int32_t* perm, int64_t n, const int8_t* lvl, int32_t* host_dst) {
   cudaStream_t st = stream();
+  if (int32_t* d = perm ? mapped_host(host_dst) : nullptr) {
+    k_widen<<<nblk(n, 256), 256, 0, st>>>(n, perm, lvl, d);
+    FM_LAUNCHED();
+    FM_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
   DBuf<int32_t> tmp(std::max<int64_t>(n, 1));
   if (perm) {
     k_widen<<<nblk(n, 256), 256, 0, st>>>(n, perm, lvl, tmp.p);

@@ -229,3 +229,20 @@ def test_native_pow73_matches_glibc(gpu):
         out[fn] = np.mean(y != ref)
     assert out[0] < 0.08, out
     assert out[0] < out[2] / 3, out
+
+
+def test_download_into_page_locked_buffers(gpu):
+    # page-locked destinations take the direct gather (no staging copy): the
+    # same arrays as a download into pageable memory
+    import torch
+
+    sc = S.config0(4)
+    s = make(gpu, sc, PORTABLE)
+    s.run(5, gauge_interval=10.0)
+    n = s.num_cells
+    shapes = [((n,), torch.int32)] * 3 + [((n, 9), torch.float64), ((n, 3), torch.float64)]
+    pinned = [torch.zeros(sh, dtype=dt, pin_memory=True) for sh, dt in shapes]
+    got = s.download(out=[t.numpy() for t in pinned])
+    ref = s.download()
+    for x, y in zip(got, ref):
+        assert np.array_equal(x, y)
