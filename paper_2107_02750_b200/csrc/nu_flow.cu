@@ -386,251 +386,6 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   if (epi && act) reduce_leaf(v, red, *c, res, sz, leaf_key(l, i, j), valid);
 }
 
-// ---- one RK stage, two lanes per leaf ---------------------------------------
-// The same stage as k_stage with each leaf on an adjacent lane pair: the even
-// lane takes the x direction (E then W), the odd lane the y direction (N then
-// S), each in its own face-normal frame (n, t), so both lanes run one code
-// path.  In that frame phys_y(h, qx, qy) is phys_x(h, qy, qx) with its last two
-// outputs swapped, and the y direction's slopes (Lr 2, 5, 8) are the x
-// direction's (1, 7, 4) with n and t exchanged.  The lanes meet three times by
-// shuffle: the flux differences both means need, the two h slopes positivity
-// needs, and the finished coefficients for the row store.  Every sum keeps the
-// reference's operands (a + b == b + a bitwise), so the result is the same
-// bits as k_stage's.
-template <bool P2, bool FIRST>
-__device__ __forceinline__ SideOut side_eval_lane(const NuView& v, const double s[9], const P3& zc,
-                                                  long long kk, bool xn, int sd, int kind, int bcs,
-                                                  double cx, double cy, double sz, int* err,
-                                                  int2 ids) {
-  // FIRST: the E (x lane) or N (y lane) side, where this leaf is the left state
-  const int nseg = kind == 0 ? 0 : kind == 3 ? 2 : 1;
-  double sg[2][6];
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    if (t < nseg) {
-      const int id = t == 0 ? ids.x : ids.y;
-      const double2* q = reinterpret_cast<const double2*>(v.segst + 6 * (long long)id);
-#pragma unroll
-      for (int e = 0; e < 3; ++e) {
-        const double2 w2 = q[e];
-        sg[t][2 * e] = w2.x;
-        sg[t][2 * e + 1] = w2.y;
-      }
-    }
-  }
-  const double off = FIRST ? 0.5 : -0.5;
-  const double ox = xn ? off : 0.0, oy = xn ? 0.0 : off;
-  const double hs = FIRST ? sz / 2 : -sz / 2;
-  const double fx = P2 ? 0.0 : cx + (xn ? hs : 0.0);
-  const double fy = P2 ? 0.0 : cy + (xn ? 0.0 : hs);
-  const Pt me = P2 ? limit_rel(s, zc, ox, oy, v.hdry) : limit(s, zc, cx, cy, sz, fx, fy, v.hdry);
-  const double w = kind == 3 ? 0.5 : 1.0;
-  double zstar;
-  if (kind == 0) {
-    zstar = me.z;
-  } else if (nseg == 1) {
-    zstar = sg[0][3];
-  } else if (v.zpair) {
-    zstar = smax(me.z, v.zpair[4 * kk + sd]);
-  } else {
-    double acc = 0.0;
-    acc += w * sg[0][3];
-    acc += w * sg[1][3];
-    zstar = acc;
-  }
-  SideOut o;
-  const double h = smax(0.0, me.eta - zstar);
-  o.h = h;
-  o.qx = h * me.u;
-  o.qy = h * me.v;
-  o.zd = zstar - smax(0.0, zstar - me.eta);
-  Flx acc{0.0, 0.0, 0.0};
-  if (kind == 0) {
-    const double qn = xn ? o.qx : o.qy, qt = xn ? o.qy : o.qx;
-    const double qg = bcs == FM_REFLECTIVE ? -qn : qn;
-    const Flx f = FIRST ? hll(h, qn, qt, h, qg, qt, v.g, v.hdry, err)
-                        : hll(h, qg, qt, h, qn, qt, v.g, v.hdry, err);
-    acc.m += f.m;
-    acc.n += f.n;
-    acc.t += f.t;
-  } else {
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      if (t < nseg) {
-        const double hme = FIRST ? sg[t][4] : sg[t][5];
-        const double corr = 0.5 * v.g * (h * h - hme * hme);
-        acc.m += w * sg[t][0];
-        acc.n += w * (sg[t][1] + corr);
-        acc.t += w * sg[t][2];
-      }
-    }
-  }
-  o.fm = acc.m;
-  o.fn = acc.n;
-  o.ft = acc.t;
-  return o;
-}
-
-__device__ __forceinline__ double pair_swap(double x) { return __shfl_xor_sync(0xffffffffu, x, 1); }
-
-#ifndef FM_STAGE_PAIR
-#define FM_STAGE_PAIR 0
-#endif
-#ifndef FM_PAIR_THREADS
-#define FM_PAIR_THREADS 128
-#endif
-#ifndef FM_PAIR_MINB
-#define FM_PAIR_MINB 6
-#endif
-
-template <int STAGE, bool P2>
-__global__ void __launch_bounds__(FM_PAIR_THREADS, FM_PAIR_MINB) k_stage_pair(
-    NuView v, const DevClock* __restrict__ clk, DevRed* red, const double* __restrict__ in,
-    const double* uold, double* out, int last, int manual, double mdt, int* err) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long k = t >> 1;
-  const bool py = t & 1;  // false: x direction (E, W); true: y direction (N, S)
-  const bool xn = !py;
-  const DevClock* c = clk + 1;
-  if (!manual && !c->active) return;
-  const double dt = manual ? mdt : c->dt;
-  const bool valid = k < v.n;
-  const long long kk = valid ? k : v.n - 1;
-  const int l = v.lvl[kk], i = v.li[kk], j = v.lj[kk];
-  const double sz = lsize(v, l);
-  const double inv = v.linv[l];
-  const double cx = P2 ? 0.0 : lcen(v.x0, v, l, i), cy = P2 ? 0.0 : lcen(v.y0, v, l, j);
-  double s[9];
-  load9v(in, kk, s);
-  const P3 zc = load3v(v.z, kk);
-  const int code = v.sk[kk];
-  const bool dg2 = v.scheme == FM_DG2;
-  const bool epi = last && !manual;
-  const int cnt0 = (epi && v.ninflow > 0) ? v.infc[kk] : 0;
-  // this lane's sides: x lane E (1) then W (3); y lane N (0) then S (2).  Segment
-  // ids per side (N E S W) at 8 kk + 2 sd: one 8 B load each.
-  const int sda = py ? 0 : 1, sdb = sda + 2;
-  const int2* srow = reinterpret_cast<const int2*>(v.sid + 8 * kk);
-  const int2 ida = srow[sda], idb = srow[sdb];
-  const int bca = py ? v.bc[0] : v.bc[1], bcb = py ? v.bc[2] : v.bc[3];
-  const SideOut a = side_eval_lane<P2, true>(v, s, zc, kk, xn, sda, (code >> (2 * sda)) & 3, bca, cx,
-                                             cy, sz, err, ida);
-  const SideOut b = side_eval_lane<P2, false>(v, s, zc, kk, xn, sdb, (code >> (2 * sdb)) & 3, bcb, cx,
-                                              cy, sz, err, idb);
-  // the direction's modal state in the face frame (normal n, tangential t)
-  const double an = xn ? a.qx : a.qy, at = xn ? a.qy : a.qx;
-  const double bn = xn ? b.qx : b.qy, bt = xn ? b.qy : b.qx;
-  const double D_h0 = 0.5 * (a.h + b.h), D_h1 = (a.h - b.h) * kHalfInvS3;
-  const double D_n0 = 0.5 * (an + bn), D_n1 = (an - bn) * kHalfInvS3;
-  const double D_t0 = 0.5 * (at + bt), D_t1 = (at - bt) * kHalfInvS3;
-  const double D_z1 = (a.zd - b.zd) * kHalfInvS3;
-  // exchange 1: the mass-flux and tangential-flux differences
-  const double dm = a.fm - b.fm, dn = a.fn - b.fn, dtn = a.ft - b.ft;
-  const double dm_o = pair_swap(dm), dt_o = pair_swap(dtn);
-  // L operator (solver_nonuniform.cpp:228-271), this lane's coefficients:
-  // h mean (both lanes), its momentum mean (qx: x lane, qy: y lane), its slopes
-  const double dmx = py ? dm_o : dm, dmy = py ? dm : dm_o;
-  const double L0 = div_sz<P2>(-(dmx + dmy), sz, inv);
-  const double m1 = py ? dt_o : dn, m2 = py ? dn : dt_o;  // x: (fe.n-fw.n)+(fn.t-fs.t); y: (fe.t-fw.t)+(fn.n-fs.n)
-  const double Lq = div_sz<P2>(-(m1 + m2), sz, inv) - div_sz<P2>(v.g * D_h0 * (2.0 * kS3 * D_z1), sz, inv);
-  double Lm = 0.0, Ln = 0.0, Lt = 0.0;
-  if (dg2) {
-    double pm, pn, pt, qm, qn, qt;
-    phys_x(D_h0 + D_h1, D_n0 + D_n1, D_t0 + D_t1, v.g, v.hdry, pm, pn, pt);
-    phys_x(D_h0 - D_h1, D_n0 - D_n1, D_t0 - D_t1, v.g, v.hdry, qm, qn, qt);
-    const double kk3 = P2 ? kS3 * inv : kS3 / sz;
-    Lm = -kk3 * (a.fm + b.fm - pm - qm);
-    Ln = -kk3 * (a.fn + b.fn - pn - qn) - div_sz<P2>(v.g * D_h1 * (2.0 * kS3 * D_z1), sz, inv);
-    Lt = -kk3 * (a.ft + b.ft - pt - qt);
-  }
-  // this lane's coefficient indices: h mean 0; momentum mean 3 | 6; slopes
-  // h 1 | 2, normal momentum 4 | 8, tangential momentum 7 | 5
-  const double s0 = s[0], sq = py ? s[6] : s[3], sm = py ? s[2] : s[1];
-  const double sn = py ? s[8] : s[4], st = py ? s[5] : s[7];
-  double r0, rq, rm, rn, rt;
-  if (STAGE == 1) {
-    r0 = s0 + L0 * dt;
-    rq = sq + Lq * dt;
-    rm = sm + Lm * dt;
-    rn = sn + Ln * dt;
-    rt = st + Lt * dt;
-  } else {
-    const double* u0 = uold + 9 * kk;
-    const double o0 = u0[0], oq = u0[py ? 6 : 3], om = u0[py ? 2 : 1];
-    const double on = u0[py ? 8 : 4], ot = u0[py ? 5 : 7];
-    auto avg = [dt](double x, double L, double o) {
-      double r = x;
-      r += L * dt;
-      r += o;
-      r *= 0.5;
-      return r;
-    };
-    r0 = avg(s0, L0, o0);
-    rq = avg(sq, Lq, oq);
-    rm = avg(sm, Lm, om);
-    rn = avg(sn, Ln, on);
-    rt = avg(st, Lt, ot);
-  }
-  // positivity (solver_nonuniform.cpp:276-304); exchange 2: the other h slope
-  const double rm_o = pair_swap(rm);
-  if (!(r0 > 0.0)) {
-    r0 = smax(r0, 0.0);
-    rq = rm = rn = rt = 0.0;
-  } else if (r0 <= v.hdry) {
-    rq = rm = rn = rt = 0.0;
-  } else {
-    const double f1 = py ? rm_o : rm, f2 = py ? rm : rm_o;
-    const double span = kS3 * (fabs(f1) + fabs(f2));
-    if (r0 - span < 0.0) {
-      const double th = ddiv(r0, span);
-      rm *= th;
-      rn *= th;
-      rt *= th;
-    }
-  }
-  if (epi && valid) {
-    for (int f = 0; f < v.ninflow; ++f) {
-      if (!c->on[f]) continue;
-      const int cnt = f == 0 ? cnt0 : v.infc[f * v.n + kk];
-      if (cnt) {
-        const double num = c->per_cell[f] * cnt;
-        r0 += P2 ? num * (inv * inv) : ddiv(num, sz * sz);
-      }
-    }
-  }
-  // exchange 3: the other lane's four coefficients
-  const double xq = pair_swap(rq), xm = pair_swap(rm), xn_ = pair_swap(rn), xt = pair_swap(rt);
-  double res[9];
-  res[0] = r0;
-  res[1] = py ? xm : rm;
-  res[2] = py ? rm : xm;
-  res[3] = py ? xq : rq;
-  res[4] = py ? xn_ : rn;
-  res[5] = py ? rt : xt;
-  res[6] = py ? rq : xq;
-  res[7] = py ? xt : rt;
-  res[8] = py ? rn : xn_;
-  if (valid) {
-    // the row's 16 B part split between the lanes (x: vectors 0-1, y: 2-3 and
-    // the single double), both parities by one instruction sequence
-    const bool odd = kk & 1;
-    double* p = out + 9 * kk;
-    double2* pv = reinterpret_cast<double2*>(p + (odd ? 1 : 0));
-    double w[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) w[e] = odd ? res[e + 1] : res[e];
-    if (!py) {
-      pv[0] = make_double2(w[0], w[1]);
-      pv[1] = make_double2(w[2], w[3]);
-    } else {
-      pv[2] = make_double2(w[4], w[5]);
-      pv[3] = make_double2(w[6], w[7]);
-      p[odd ? 0 : 8] = odd ? res[0] : res[8];
-    }
-  }
-  if (epi) reduce_leaf(v, red, *c, res, sz, leaf_key(l, i, j), valid && !py);
-}
-
 // ---- ACC ------------------------------------------------------------------
 // Per interior segment (solver_nonuniform.cpp:354-371).  Also the step head.
 __global__ void __launch_bounds__(256) k_acc_faces(NuView v, DevClock* clk, DevRed* red,
@@ -861,11 +616,7 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       seg(KF_SEG1, s.u.p);
       kt_begin(KF_STAGE1);
       const int last1 = fv1 ? 1 : 0;
-      if (FM_STAGE_PAIR && s.p2)
-        launch_k(k_stage_pair<1, true>, nblk(2 * n, FM_PAIR_THREADS), FM_PAIR_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.u.p, (const double*)nullptr, s.us.p, last1, (int)manual, mdt, err);
-      else if (FM_STAGE_PAIR)
-        launch_k(k_stage_pair<1, false>, nblk(2 * n, FM_PAIR_THREADS), FM_PAIR_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.u.p, (const double*)nullptr, s.us.p, last1, (int)manual, mdt, err);
-      else if (s.p2)
+      if (s.p2)
         launch_k(k_stage<1, true>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.u.p, (const double*)nullptr, s.us.p, last1, (int)manual, mdt, err);
       else
         launch_k(k_stage<1, false>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.u.p, (const double*)nullptr, s.us.p, last1, (int)manual, mdt, err);
@@ -876,11 +627,7 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
     case OP_STAGE2:
       seg(KF_SEG2, s.us.p);
       kt_begin(KF_STAGE2);
-      if (FM_STAGE_PAIR && s.p2)
-        launch_k(k_stage_pair<2, true>, nblk(2 * n, FM_PAIR_THREADS), FM_PAIR_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
-      else if (FM_STAGE_PAIR)
-        launch_k(k_stage_pair<2, false>, nblk(2 * n, FM_PAIR_THREADS), FM_PAIR_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
-      else if (s.p2)
+      if (s.p2)
         launch_k(k_stage<2, true>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
       else
         launch_k(k_stage<2, false>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
