@@ -233,15 +233,38 @@ __global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) 
   const uint64_t par0 = tile << (2 * (p.T - 1));
   const uint64_t par = par0 + uint64_t(tid);
   P3 kids[4];
+  if constexpr (FROM_VERTICES) {
+    // the four children (2I + dx, 2J + dy) share a 3 x 3 vertex block: nine
+    // loads instead of sixteen.  Edge replication (VertexView::plane) clamps
+    // the element column / row; a clamped second child reuses the first's.
+    int I, J;
+    node_ij(p.lev_in - 1, par, p.M, I, J);
+    const int ia = min(2 * I, vv.n - 1), ib = min(2 * I + 1, vv.n - 1);
+    const int ja = min(2 * J, vv.m - 1), jb = min(2 * J + 1, vv.m - 1);
+    const int rsa = vv.nrows - 1 - ja, rsb = vv.nrows - 1 - jb;
+    const int rows[3] = {rsa, rsa - 1, rsb - 1};  // south to north
+    const int cols[3] = {ia, ia + 1, ib + 1};      // west to east
+    double V[3][3];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const uint64_t c = 4 * par + k;
-    if constexpr (FROM_VERTICES) {
-      int i, j;
-      node_ij(p.lev_in, c, p.M, i, j);
-      kids[k] = vv.plane(i, j);
-    } else {
-      const double* s = p.sc_in + 3 * c;
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) V[r][c] = vv.at(rows[r], cols[c]);
+    const bool xs = ib != ia, ys = jb != ja;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool sx = (k & 1) && xs, sy = (k >> 1) && ys;  // shifted one column / row
+      double q[2][2];  // [south, north][west, east]
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+          q[a][b] = sy ? (sx ? V[1 + a][1 + b] : V[1 + a][b]) : (sx ? V[a][1 + b] : V[a][b]);
+      kids[k] = project4(q[1][0], q[1][1], q[0][0], q[0][1]);  // nw ne sw se
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double* s = p.sc_in + 3 * (4 * par + k);
       kids[k] = P3{s[0], s[1], s[2]};
     }
   }
