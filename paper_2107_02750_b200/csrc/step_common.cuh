@@ -260,15 +260,26 @@ __device__ __forceinline__ void reduce_leaf(const NuView& v, DevRed* red, const 
     for (int q = 0; q < 9; ++q) fin = fin && isfinite(s[q]);
     if (!fin) bad = key;
   }
-  for (int o = 16; o; o >>= 1) {
-    dtc = smin(dtc, __shfl_xor_sync(0xffffffffu, dtc, o));
-    hm = smax(hm, __shfl_xor_sync(0xffffffffu, hm, o));
-    const unsigned long long b2 = __shfl_xor_sync(0xffffffffu, bad, o);
-    bad = b2 < bad ? b2 : bad;
+  // warp minimum of the CFL candidates: they are >= 0 (or NaN), where the
+  // order of the bit patterns is the numeric order, so two 32-bit REDUX
+  // minima (high word, then the low word among the lanes holding that high
+  // word) give the exact minimum; a NaN candidate never wins
+  const unsigned long long db = dbits(dtc);
+  const unsigned hi = __reduce_min_sync(0xffffffffu, unsigned(db >> 32));
+  const unsigned lo = __reduce_min_sync(0xffffffffu, unsigned(db >> 32) == hi ? unsigned(db) : 0xffffffffu);
+  const unsigned long long dmin = (static_cast<unsigned long long>(hi) << 32) | lo;
+  if (v.scheme == FM_ACC) {  // grid-uniform: the depth maximum only for ACC
+    for (int o = 16; o; o >>= 1) hm = smax(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+  }
+  if (__any_sync(0xffffffffu, bad != ~0ull)) {  // the non-finite guard, rarely taken
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long b2 = __shfl_xor_sync(0xffffffffu, bad, o);
+      bad = b2 < bad ? b2 : bad;
+    }
   }
   if ((threadIdx.x & 31) == 0) {
     DevRed& r = red[(c.steps) & 1];
-    if (dtc < INFINITY) atomicMin(&r.dtmin, dbits(dtc));
+    if (dmin < dbits(INFINITY)) atomicMin(&r.dtmin, dmin);
     if (hm > 0.0) atomicMin(&r.hmaxc, ~dbits(hm));
     if (bad != ~0ull) atomicMin(&r.badkey, bad);
   }

@@ -246,3 +246,26 @@ def test_download_into_page_locked_buffers(gpu):
     ref = s.download()
     for x, y in zip(got, ref):
         assert np.array_equal(x, y)
+
+
+def test_compute_dt_ignores_nan_candidates(gpu, orc):
+    # compute_dt (solver_nonuniform.cpp:439-448) folds candidates with
+    # std::min, so a leaf whose CFL candidate is NaN never sets dt; the device
+    # warp minimum must drop such a lane too, wherever it sits in its warp
+    sc = S.config0(4)
+    a, b = make(gpu, sc, PORTABLE), make(orc, sc, PORTABLE)
+    a.run(20, gauge_interval=10.0)
+    b.run(20, gauge_interval=10.0)
+    u = b.download()[3]
+    wet = np.flatnonzero(u[:, 0] > 1e-3)
+    assert len(wet) > 64
+    # qx.c0 = NaN on every wet leaf but three: those leaves stay wet and
+    # their candidates are NaN, so lane 0 of the warp holding the minimum is
+    # almost surely one of them
+    keep = wet[[len(wet) // 5, len(wet) // 2, (4 * len(wet)) // 5]]
+    nan = np.setdiff1d(wet, keep)
+    u[nan, 3] = np.nan
+    a.upload(u)
+    b.upload(u)
+    da, db = a.compute_dt(), b.compute_dt()
+    assert np.isfinite(db) and da == db
