@@ -178,13 +178,22 @@ struct SideOut {
   double h, qx, qy, zd, fm, fn, ft;
 };
 
+// 1: the stage kernels keep the leaf's own row (9 + 3 doubles) in a per-thread
+// shared-memory slot and reload it where it is used (each side's face limit,
+// the update) instead of holding it in registers across the kernel: no spills
+// at 102 registers, 10 CTAs per SM (A/B on B200: 0.796 -> 0.775 ms/step,
+// bit-identical)
+#ifndef FM_STAGE_SROW
+#define FM_STAGE_SROW 1
+#endif
 #ifndef FM_SID_ROW
 #define FM_SID_ROW 1
 #endif
 template <bool P2>
 __device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9], const P3& zc,
                                              long long kk, int sd, int kind, double cx, double cy,
-                                             double sz, int* err, int2 ids) {
+                                             double sz, int* err, int2 ids,
+                                             const volatile double* lrow) {
   const bool xn = sd == 1 || sd == 3;
   const bool mine_left = sd == 0 || sd == 1;
   const int nseg = kind == 0 ? 0 : kind == 3 ? 2 : 1;
@@ -211,7 +220,16 @@ __device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9],
   const double oy = sd == 0 ? 0.5 : sd == 2 ? -0.5 : 0.0;
   const double fx = P2 ? 0.0 : cx + (sd == 1 ? sz / 2 : sd == 3 ? -sz / 2 : 0.0);
   const double fy = P2 ? 0.0 : cy + (sd == 0 ? sz / 2 : sd == 2 ? -sz / 2 : 0.0);
+#if FM_STAGE_SROW
+  // the leaf's row from its shared-memory copy, read where it is used
+  double sl[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) sl[q] = lrow[q];
+  const P3 zl{lrow[9], lrow[10], lrow[11]};
+  const Pt me = P2 ? limit_rel(sl, zl, ox, oy, v.hdry) : limit(sl, zl, cx, cy, sz, fx, fy, v.hdry);
+#else
   const Pt me = P2 ? limit_rel(s, zc, ox, oy, v.hdry) : limit(s, zc, cx, cy, sz, fx, fy, v.hdry);
+#endif
   const double w = kind == 3 ? 0.5 : 1.0;
   double zstar;
   if (kind == 0) {
@@ -259,13 +277,14 @@ __device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9],
   return o;
 }
 
-// 64-thread CTAs, >= 8 resident per SM (a 128-register cap): tuned by A/B on
-// B200 (scripts/ab_profile.py)
+// 64-thread CTAs, >= 10 resident per SM (a 102-register cap, with the row in
+// shared memory; 8 / 9 / 11 / 12 and 128-thread CTAs measured slower): tuned
+// by A/B on B200 (scripts/ab_profile.py)
 #ifndef FM_STAGE_THREADS
 #define FM_STAGE_THREADS 64
 #endif
 #ifndef FM_STAGE_MINB
-#define FM_STAGE_MINB 8
+#define FM_STAGE_MINB 10
 #endif
 
 template <int STAGE, bool P2>
@@ -283,6 +302,17 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   load9v(in, kk, s);
   const P3 zc = load3v(v.z, kk);
   const int code = v.sk[kk];
+#if FM_STAGE_SROW
+  __shared__ double srow_all[FM_STAGE_THREADS * 13];  // 13-double stride: conflict-free
+  volatile double* lrow = srow_all + 13 * threadIdx.x;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) lrow[q] = s[q];
+  lrow[9] = zc.c0;
+  lrow[10] = zc.cx;
+  lrow[11] = zc.cy;
+#else
+  const volatile double* lrow = nullptr;
+#endif
   // the leaf's segment ids, 2 per side (N E S W), as two 16 B loads
 #if FM_SID_ROW
   const int4* srow = reinterpret_cast<const int4*>(v.sid + 8 * kk);
@@ -312,8 +342,8 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   // otherwise sits at the end of the leaf's critical path
   const int cnt0 = (epi && v.ninflow > 0) ? v.infc[kk] : 0;
   // x direction: E and W sides, then the Gauss-point fluxes along x
-  const SideOut ee = side_eval<P2>(v, s, zc, kk, 1, (code >> 2) & 3, cx, cy, sz, err, ide);
-  const SideOut ew = side_eval<P2>(v, s, zc, kk, 3, (code >> 6) & 3, cx, cy, sz, err, idw);
+  const SideOut ee = side_eval<P2>(v, s, zc, kk, 1, (code >> 2) & 3, cx, cy, sz, err, ide, lrow);
+  const SideOut ew = side_eval<P2>(v, s, zc, kk, 3, (code >> 6) & 3, cx, cy, sz, err, idw, lrow);
   const DirMod X{0.5 * (ee.h + ew.h),   (ee.h - ew.h) * kHalfInvS3,   0.5 * (ee.qx + ew.qx),
                  (ee.qx - ew.qx) * kHalfInvS3, 0.5 * (ee.qy + ew.qy), (ee.qy - ew.qy) * kHalfInvS3,
                  (ee.zd - ew.zd) * kHalfInvS3};
@@ -324,8 +354,8 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   }
   const Flx fe{ee.fm, ee.fn, ee.ft}, fw{ew.fm, ew.fn, ew.ft};
   // y direction
-  const SideOut en = side_eval<P2>(v, s, zc, kk, 0, code & 3, cx, cy, sz, err, idn);
-  const SideOut es = side_eval<P2>(v, s, zc, kk, 2, (code >> 4) & 3, cx, cy, sz, err, ids_);
+  const SideOut en = side_eval<P2>(v, s, zc, kk, 0, code & 3, cx, cy, sz, err, idn, lrow);
+  const SideOut es = side_eval<P2>(v, s, zc, kk, 2, (code >> 4) & 3, cx, cy, sz, err, ids_, lrow);
   const DirMod Y{0.5 * (en.h + es.h),   (en.h - es.h) * kHalfInvS3,   0.5 * (en.qx + es.qx),
                  (en.qx - es.qx) * kHalfInvS3, 0.5 * (en.qy + es.qy), (en.qy - es.qy) * kHalfInvS3,
                  (en.zd - es.zd) * kHalfInvS3};
@@ -354,6 +384,10 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
     Lr[1] = Lr[2] = Lr[4] = Lr[5] = Lr[7] = Lr[8] = 0.0;
   }
   double res[9];
+#if FM_STAGE_SROW
+#pragma unroll
+  for (int q = 0; q < 9; ++q) s[q] = lrow[q];
+#endif
   if (STAGE == 1) {
 #pragma unroll
     for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
