@@ -176,6 +176,11 @@ void sim_snapshot(Sim& s);
 void sim_sync_u(Sim& s);  // FV1: move the staged post-step state back into u
 // reference-order transfers (order.cu); perm == nullptr means identity
 const int32_t* sim_ref_perm(Sim& s);
+// Lends device scratch to the gathers below for the scope's lifetime.
+struct StageScope {
+  StageScope(void* p, size_t bytes);
+  ~StageScope();
+};
 void gather_rows(const int32_t* perm, int64_t n, int width, const double* src, double* host_dst);
 void gather_i32(const int32_t* perm, int64_t n, const int32_t* src, int32_t* host_dst);
 void gather_levels(const int32_t* perm, int64_t n, const int8_t* lvl, int32_t* host_dst);

@@ -76,7 +76,23 @@ T* mapped_host(T* host) {
   return a.type == cudaMemoryTypeHost ? static_cast<T*>(a.devicePointer) : nullptr;
 }
 
+// Device scratch a caller lends to the gathers (the sim's idle U* buffer),
+// so a download to pageable memory needs no allocation.
+struct Stage {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+thread_local Stage g_stage;
+
+template <typename T>
+T* staging(size_t count) {
+  return g_stage.p && count * sizeof(T) <= g_stage.bytes ? static_cast<T*>(g_stage.p) : nullptr;
+}
+
 }  // namespace
+
+StageScope::StageScope(void* p, size_t bytes) { g_stage = Stage{p, bytes}; }
+StageScope::~StageScope() { g_stage = Stage{}; }
 
 const int32_t* sim_ref_perm(Sim& s) {
   if (s.uniform) return nullptr;  // j * nx + i is already the reference order
@@ -111,10 +127,15 @@ void gather_rows(const int32_t* perm, int64_t n, int width, const double* src, d
     FM_CUDA(cudaStreamSynchronize(st));
     return;
   }
-  DBuf<double> tmp(std::max<int64_t>(n * width, 1));
-  k_gather<double><<<nblk(n * width, 256), 256, 0, st>>>(n, width, perm, src, tmp.p);
+  DBuf<double> tmp;
+  double* buf = staging<double>(size_t(n) * width);
+  if (!buf) {
+    tmp.alloc(std::max<int64_t>(n * width, 1));
+    buf = tmp.p;
+  }
+  k_gather<double><<<nblk(n * width, 256), 256, 0, st>>>(n, width, perm, src, buf);
   FM_LAUNCHED();
-  FM_CUDA(cudaMemcpyAsync(host_dst, tmp.p, size_t(n) * width * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FM_CUDA(cudaMemcpyAsync(host_dst, buf, size_t(n) * width * sizeof(double), cudaMemcpyDeviceToHost, st));
   FM_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -130,10 +151,15 @@ void gather_i32(const int32_t* perm, int64_t n, const int32_t* src, int32_t* hos
     FM_CUDA(cudaStreamSynchronize(st));
     return;
   }
-  DBuf<int32_t> tmp(std::max<int64_t>(n, 1));
-  k_gather<int32_t><<<nblk(n, 256), 256, 0, st>>>(n, 1, perm, src, tmp.p);
+  DBuf<int32_t> tmp;
+  int32_t* buf = staging<int32_t>(size_t(n));
+  if (!buf) {
+    tmp.alloc(std::max<int64_t>(n, 1));
+    buf = tmp.p;
+  }
+  k_gather<int32_t><<<nblk(n, 256), 256, 0, st>>>(n, 1, perm, src, buf);
   FM_LAUNCHED();
-  FM_CUDA(cudaMemcpyAsync(host_dst, tmp.p, size_t(n) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  FM_CUDA(cudaMemcpyAsync(host_dst, buf, size_t(n) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   FM_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -145,14 +171,19 @@ void gather_levels(const int32_t* perm, int64_t n, const int8_t* lvl, int32_t* h
     FM_CUDA(cudaStreamSynchronize(st));
     return;
   }
-  DBuf<int32_t> tmp(std::max<int64_t>(n, 1));
+  DBuf<int32_t> tmp;
+  int32_t* buf = staging<int32_t>(size_t(n));
+  if (!buf) {
+    tmp.alloc(std::max<int64_t>(n, 1));
+    buf = tmp.p;
+  }
   if (perm) {
-    k_widen<<<nblk(n, 256), 256, 0, st>>>(n, perm, lvl, tmp.p);
+    k_widen<<<nblk(n, 256), 256, 0, st>>>(n, perm, lvl, buf);
     FM_LAUNCHED();
   } else {
-    tmp.zero();
+    FM_CUDA(cudaMemsetAsync(buf, 0, size_t(n) * sizeof(int32_t), st));
   }
-  FM_CUDA(cudaMemcpyAsync(host_dst, tmp.p, size_t(n) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  FM_CUDA(cudaMemcpyAsync(host_dst, buf, size_t(n) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   FM_CUDA(cudaStreamSynchronize(st));
 }
 

@@ -530,6 +530,8 @@ void sim_sync_u(Sim& s) {
 void sim_download(Sim& s, int32_t* lo, int32_t* io, int32_t* jo, double* u9, double* z3) {
   if (fv1_staged(s)) fv1_to_u(s);
   const int32_t* perm = sim_ref_perm(s);
+  // U* is idle between steps (FV1's staged state was just moved back to U)
+  StageScope lend(s.us.p, s.us.n * sizeof(double));
   if (lo) gather_levels(perm, s.n, s.lvl.p, lo);
   if (io) gather_i32(perm, s.n, s.li.p, io);
   if (jo) gather_i32(perm, s.n, s.lj.p, jo);
