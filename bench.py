@@ -459,14 +459,16 @@ def config_legs(lib, args, with_cpu):
         ref, kind = reference_backend()
         if ref.has("set_threads"):
             ref.fn["set_threads"](os.cpu_count() or 1)
+    # every GPU leg first: the small configs are launch-bound, and a host that
+    # has just run the 16-thread reference launches graphs measurably slower
     for name, mk, static, gsteps, csteps in CONFIG_LEGS:
-        sc = mk()
-        d = {"gpu": _leg(lib, sc, static, 3, gsteps, True)}
-        if ref is not None:
-            d["cpu_reference"] = _leg(ref, sc, static, 1, csteps, False)
+        out[name] = {"gpu": _leg(lib, mk(), static, 3, gsteps, True)}
+    if ref is not None:
+        for name, mk, static, gsteps, csteps in CONFIG_LEGS:
+            d = out[name]
+            d["cpu_reference"] = _leg(ref, mk(), static, 1, csteps, False)
             d["cpu_reference"]["threads"] = os.cpu_count() or 1
             d["speedup"] = d["gpu"]["value"] / d["cpu_reference"]["value"]
-        out[name] = d
     return out
 
 
