@@ -279,7 +279,9 @@ def run_ours(args, ws, rank, local):
     import dataclasses
 
     def pinned(a, dtype=np.float64):
-        t = torch.empty(a.shape if hasattr(a, "shape") else a, dtype=getattr(torch, np.dtype(dtype).name),
+        # zero-filled: the host pages are touched when the buffer is made,
+        # not by the first transfer into it
+        t = torch.zeros(a.shape if hasattr(a, "shape") else a, dtype=getattr(torch, np.dtype(dtype).name),
                         pin_memory=True)
         arr = t.numpy()
         if hasattr(a, "shape"):

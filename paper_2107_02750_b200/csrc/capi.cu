@@ -144,6 +144,7 @@ int fm_init(int32_t device) {
     require_device();
     FM_CUDA(cudaSetDevice(device));
     upload_banks();
+    order_preload();
   });
 }
 
@@ -303,6 +304,10 @@ int fm_sim_create(const fm_sim_desc* d, const fm_raster* dem, const fm_grid* gri
     require_device();
     auto h = std::make_unique<fm_sim>();
     h->s.reset(sim_create(d, dem, grid ? grid->g.get() : nullptr));
+    // the reference-order permutation of a static leaf set, built with the
+    // sim (scratch allocations and a sort) rather than inside the first
+    // download; adaptive sims rebuild it after a re-grid on demand
+    if (!h->s->adaptive) sim_ref_perm(*h->s);
     *out = h.release();
   });
 }

@@ -176,6 +176,7 @@ void sim_snapshot(Sim& s);
 void sim_sync_u(Sim& s);  // FV1: move the staged post-step state back into u
 // reference-order transfers (order.cu); perm == nullptr means identity
 const int32_t* sim_ref_perm(Sim& s);
+void order_preload();
 // Lends device scratch to the gathers below for the scope's lifetime.
 struct StageScope {
   StageScope(void* p, size_t bytes);

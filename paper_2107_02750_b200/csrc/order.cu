@@ -94,6 +94,34 @@ T* staging(size_t count) {
 StageScope::StageScope(void* p, size_t bytes) { g_stage = Stage{p, bytes}; }
 StageScope::~StageScope() { g_stage = Stage{}; }
 
+// Runs every kernel of this file once on two elements, so their module is
+// loaded at fm_init and not (lazily, with a variable cost measured up to
+// 0.1-0.3 s on B200 boxes) inside the first download or sim setup.
+void order_preload() {
+  cudaStream_t st = stream();
+  const int64_t n = 2;
+  DBuf<int8_t> lvl(n);
+  DBuf<int32_t> li(n), lj(n), idx(n), perm(n), i32(n);
+  DBuf<unsigned long long> k0(n), k1(n);
+  DBuf<double> a(3 * n), b(3 * n);
+  lvl.zero();
+  li.zero();
+  lj.zero();
+  k_keys<<<1, 32, 0, st>>>(n, lvl.p, li.p, lj.p, k0.p, idx.p);
+  size_t tmp_bytes = 0;
+  FM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0.p, k1.p, idx.p, perm.p, int(n), 0, 62, st));
+  DBuf<unsigned char> tmp(std::max<size_t>(tmp_bytes, 1));
+  FM_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, k0.p, k1.p, idx.p, perm.p, int(n), 0, 62, st));
+  a.zero();
+  k_gather<double><<<1, 32, 0, st>>>(n, 3, perm.p, a.p, b.p);
+  k_scatter<double><<<1, 32, 0, st>>>(n, 3, perm.p, a.p, b.p);
+  k_gather<int32_t><<<1, 32, 0, st>>>(n, 1, perm.p, li.p, i32.p);
+  k_widen<<<1, 32, 0, st>>>(n, perm.p, lvl.p, i32.p);
+  k_gather_col<<<1, 32, 0, st>>>(n, 3, 0, perm.p, a.p, b.p);
+  FM_CUDA(cudaGetLastError());
+  FM_CUDA(cudaStreamSynchronize(st));
+}
+
 const int32_t* sim_ref_perm(Sim& s) {
   if (s.uniform) return nullptr;  // j * nx + i is already the reference order
   if (s.ref_perm_ok && s.ref_perm.n == size_t(s.n)) return s.ref_perm.p;
