@@ -143,41 +143,70 @@ def reference_backend():
     return Backend(ORC_SO, "orc_"), "port"
 
 
-def cpu_rate(steps: int, warmup: int, scale: int = 4):
-    """The reference CPU path on a bounded sample: config 4's generator at
-    (8192/scale)^2 cells, L = 13 - log2(scale), warm-up then `steps` timed DG2
-    steps with all host threads (run.cpp:79-113 times the step loop only)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_rate(steps: int, warmup: int, scale: int = 1, serial_steps: int = 2):
+    """The reference CPU path on the SAME workload as the GPU line (config 4,
+    8192^2, L = 13, static non-uniform DG2): the unmodified
+    reference library builds the grid and the sim once (setup untimed), runs
+    `warmup` steps, then times `steps` DG2 steps with every host thread and
+    `serial_steps` more with one thread (run.cpp:79-113 times the step loop
+    only).  The sample is bounded by the step count, not by the grid."""
     be, kind = reference_backend()
     cores = os.cpu_count() or 1
-    if be.has("set_threads"):
+    threaded = be.has("set_threads")
+    if threaded:
         be.fn["set_threads"](cores)
     else:
         cores = 1
     sc = S.config4(scale)
+    t_setup = time.perf_counter()
     g = be.grid(sc.dem, sc.L, sc.eps)
     s = be.sim(sc, g)
+    setup_s = time.perf_counter() - t_setup
     ck, _ = s.run(warmup, gauge_interval=10.0)
     t0 = time.perf_counter()
     ck, r = s.run(steps, clock=ck)
     dt = time.perf_counter() - t0
     n = s.num_cells
-    return {"value": n * r.steps / dt, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"config-4 generator at {8192 // scale}^2 cells (L={sc.L}, {n} leaves), "
-                      f"{r.steps} timed DG2 steps after {warmup} warm-up, {cores} threads, "
-                      f"{dt:.2f} s"}, r.steps, dt
+    out = {"value": n * r.steps / dt, "unit": UNIT, "cores": cores, "kind": kind,
+           "cpu_model": cpu_model(), "nproc": os.cpu_count() or 1,
+           "workload": "c4_static_nonuniform_dg2", "leaves": int(n),
+           "setup_s": round(setup_s, 2),
+           "sample": f"config 4 full size ({8192 // scale}^2 cells, L={sc.L}, {n} leaves): "
+                     f"{r.steps} timed DG2 steps after {warmup} warm-up, {cores} threads, "
+                     f"{dt:.2f} s; grid + sim setup {setup_s:.1f} s untimed"}
+    if threaded and serial_steps > 0:
+        be.fn["set_threads"](1)
+        t1 = time.perf_counter()
+        ck, r1 = s.run(serial_steps, clock=ck)
+        d1 = time.perf_counter() - t1
+        be.fn["set_threads"](cores)
+        out["threads1"] = {"value": n * r1.steps / d1, "steps": int(r1.steps), "seconds": round(d1, 2)}
+    return out, r.steps, dt
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
         return
     steps = max(1, min(args.steps, args.cpu_steps_cap))
-    cb, n_done, secs = cpu_rate(steps, max(1, min(args.warmup, 3)))
+    cb, n_done, secs = cpu_rate(steps, args.warmup, serial_steps=0)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": n_done, "warmup": args.warmup,
             "ms_per_step": 1000.0 * secs / max(n_done, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c4_static_nonuniform_dg2 (bounded CPU sample)",
-                       "sample": cb["sample"]},
+            "config": {"workload": "c4_static_nonuniform_dg2", "cells": "8192^2", "L": 13, "eps": 1e-3,
+                       "leaves": cb["leaves"], "same_config": True,
+                       "sample": cb["sample"],
+                       "steps_note": f"K={args.steps} requested, {n_done} timed (cap --cpu-steps-cap)"},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -264,14 +293,24 @@ def run_ours(args, ws, rank, local):
     achieved = bytes_launch / (avg_ms / 1000.0) / 1e9
     step_ms = sum(v[0] for v in prof.values()) / max(args.profile_steps, 1)
     step_bytes = 424.0 * n_leaves + 16.0 * n_seg
-    traffic = None
+    # dram__bytes_read.sum + dram__bytes_write.sum per launch of k_stage<2>
+    # cannot be counted inside this (un-profiled) run: it is read from the
+    # committed ncu capture of the same build, named in traffic_source
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("k_stage<2>")
+            tj = json.load(open(tpath))
+            traffic = tj.get("k_stage<2>")
+            traffic_src = tj.get("source", "profiles/ncu_traffic.json")
         except Exception:
             traffic = None
-    del sim, grid, dem_d
+    del sim
+    solvers = None
+    if ws == 1 and args.solver_steps > 0:
+        solvers = {name: static_solver_leg(lib, sc, grid, name, cour, bpl, bps, args, hbm)
+                   for name, cour, bpl, bps in (("acc", 0.7, 48.0, 24.0), ("fv1", 0.5, 64.0, 8.0))}
+    del grid, dem_d
 
     # ---- e2e leg: public API from host buffers, wall clock ----
     # inputs (DEM, Manning raster) and outputs (final state) in pinned host
@@ -345,7 +384,7 @@ def run_ours(args, ws, rank, local):
         return
     cpu = None
     if ws == 1 and not args.no_cpu:
-        cpu, _, _ = cpu_rate(args.cpu_steps, 2)
+        cpu, _, _ = cpu_rate(args.cpu_steps, args.warmup)
     configs = None
     if ws == 1 and not args.no_configs:
         configs = config_legs(lib, args, with_cpu=not args.no_cpu)
@@ -362,25 +401,72 @@ def run_ours(args, ws, rank, local):
                    "solver": "static non-uniform DG2 RK2, rain 50 mm/h, Manning street raster"},
         "roofline": {"bound": "hbm", "kernel": "k_stage<2>", "achieved": achieved, "peak": hbm,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "bytes_per_launch": bytes_launch,
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "bytes_per_launch": bytes_launch,
+                     "bytes_formula": "248*N_l + 8*N_s (SURVEY §8 d4, DG2 stage 2)",
                      "avg_launch_ms": avg_ms,
                      "step": {"bytes": step_bytes, "ms": step_ms,
                               "achieved": step_bytes / (step_ms / 1000.0) / 1e9,
                               "frac": step_bytes / (step_ms / 1000.0) / 1e9 / hbm},
                      "kernels_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in prof.items()}},
         "mra": {"coeffs_per_s": 12.0 * n_int / (mra_ms / 1000.0), "ms": mra_ms,
-                "bytes": mra_bytes, "achieved_gbs": mra_bytes / (mra_ms / 1000.0) / 1e9,
+                "bytes": mra_bytes,
+                "bytes_formula": "8*(n+1)^2 + 73*N_int + 36*N_l (SURVEY §8 d4, projection fused)", "achieved_gbs": mra_bytes / (mra_ms / 1000.0) / 1e9,
                 "frac": mra_bytes / (mra_ms / 1000.0) / 1e9 / hbm},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
                 "d2h_bytes_per_step": d2h / e2e_steps, "seconds": e2e_s, "phases_ms": phases,
                 "what": "host DEM -> fm_mra_static -> fm_sim_create(_shard) -> W+K steps -> host state"},
         "uniform": uni,
+        "solvers": solvers,
         "configs": configs,
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
+
+
+def static_solver_leg(lib, sc, grid, solver, courant, b_leaf, b_seg, args, hbm):
+    """Config 4's static grid (the same 2.3 M leaves) under the ACC or FV1
+    update: SURVEY §8 d4 bytes per step, b_leaf*N_l + b_seg*N_s (ACC 48/24,
+    FV1 64/8), against the CUDA-event step time and per-kernel launch times."""
+    import dataclasses
+
+    import torch
+    sc2 = dataclasses.replace(sc, solver=solver, courant=courant)
+    sim = lib.sim(sc2, grid)
+    n, ns = sim.num_cells, sim.num_segments
+    ck, _ = sim.run(args.warmup, gauge_interval=10.0)
+    sim.snapshot()
+    ck0 = (ck.end_time, ck.output_interval, ck.gauge_interval, ck.now, ck.next_output, ck.next_gauge)
+    ms, done = 0.0, 0
+    while done < args.solver_steps:
+        k = min(args.chunk, args.solver_steps - done)
+        sim.restore()
+        torch.cuda.synchronize()
+        _, r = sim.run(k, clock=c_clock(*ck0))
+        torch.cuda.synchronize()
+        if r.steps != k:
+            raise SystemExit(f"{solver}: only {r.steps} of {k} steps ran")
+        ms += sim.last_run_ms()
+        done += k
+    sim.restore()
+    prof = sim.profile(args.profile_steps)
+    step_bytes = b_leaf * n + b_seg * ns
+    per = {k: v[0] / max(args.profile_steps, 1) for k, v in prof.items()}
+    top = max(per, key=per.get)
+    prof_step = sum(per.values())
+    ms_step = ms / args.solver_steps
+    del sim
+    return {"workload": f"c4_static_nonuniform_{solver}", "leaves": int(n), "segments": int(ns),
+            "steps": args.solver_steps, "ms_per_step": ms_step, "value": n / (ms_step / 1000.0),
+            "unit": UNIT,
+            "roofline": {"bound": "hbm", "bytes_per_step": step_bytes,
+                         "bytes_formula": f"{b_leaf:g}*N_l + {b_seg:g}*N_s (SURVEY §8 d4)",
+                         "achieved": step_bytes / (ms_step / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": step_bytes / (ms_step / 1000.0) / 1e9 / hbm,
+                         "profiled_step_ms": prof_step, "top_kernel": top},
+            "kernels_ms_per_step": per}
 
 
 def uniform_leg(lib, args, ws, rank, comm, hbm):
@@ -483,7 +569,9 @@ def main():
     p.add_argument("--scale", type=int, default=1, help="shrink config 4 (tests only)")
     p.add_argument("--profile-steps", type=int, default=10)
     p.add_argument("--chunk", type=int, default=16, help="timed steps between state restores")
-    p.add_argument("--cpu-steps", type=int, default=40)
+    p.add_argument("--cpu-steps", type=int, default=20)
+    p.add_argument("--solver-steps", type=int, default=64,
+                   help="timed steps of the config-4 ACC and FV1 legs (0: skip)")
     p.add_argument("--cpu-steps-cap", type=int, default=20)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--uniform-steps", type=int, default=32,

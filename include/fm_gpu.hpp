@@ -169,7 +169,9 @@ class Sim {
   // semantics of EventClock (sim_common.cpp:48-82).  Throws BlowUpError(t).
   fm_run_result run(fm_clock& clk, int64_t max_steps, bool stop_at_events = true) {
     fm_run_result r{};
-    check(fm_sim_run(s_, &clk, max_steps, stop_at_events ? 1 : 0, &r), r.blow_up_time);
+    // the status first: r.blow_up_time is only filled by the call
+    const int st = fm_sim_run(s_, &clk, max_steps, stop_at_events ? 1 : 0, &r);
+    check(st, r.blow_up_time);
     return r;
   }
   int64_t cells() const { return fm_sim_num_cells(s_); }

@@ -151,6 +151,20 @@ OPTIONAL = {
 }
 
 
+
+def _check_array(a, dtype, shape, writable=False):
+    """Raise ValueError unless `a` is a C-contiguous ndarray of `dtype` and
+    `shape` (the C ABI writes/reads exactly that many elements through a raw
+    pointer)."""
+    if not isinstance(a, np.ndarray):
+        raise ValueError(f"expected a numpy array, got {type(a).__name__}")
+    if a.dtype != dtype or a.shape != tuple(shape) or not a.flags.c_contiguous:
+        raise ValueError(f"expected a C-contiguous {np.dtype(dtype).name} array of shape {tuple(shape)}, "
+                         f"got {a.dtype.name} {a.shape} (c_contiguous={a.flags.c_contiguous})")
+    if writable and not a.flags.writeable:
+        raise ValueError("output array is read-only")
+
+
 def dptr(a: np.ndarray):
     return a.ctypes.data_as(PD)
 
@@ -468,13 +482,17 @@ class Sim:
             z = np.zeros((n, 3), np.float64)
         else:
             lv, i, j, u, z = out
-            assert len(lv) == n and u.shape == (n, 9) and z.shape == (n, 3)
+            for a, dt, sh in ((lv, np.int32, (n,)), (i, np.int32, (n,)), (j, np.int32, (n,)),
+                              (u, np.float64, (n, 9)), (z, np.float64, (n, 3))):
+                _check_array(a, dt, sh, writable=True)
         self.be.call("sim_download", self.h, lv.ctypes.data_as(PI32), i.ctypes.data_as(PI32),
                      j.ctypes.data_as(PI32), dptr(u), dptr(z))
         return lv, i, j, u, z
 
     def upload(self, u9: np.ndarray):
         u9 = np.ascontiguousarray(u9, np.float64)
+        if u9.shape != (self.num_cells, 9):
+            raise ValueError(f"upload: u9 must have shape ({self.num_cells}, 9), got {u9.shape}")
         self.be.call("sim_upload", self.h, dptr(u9))
 
     def shard_info(self) -> dict:

@@ -562,6 +562,7 @@ struct ZeroKnownBody {
 
 void adaptive_adapt(Sim& s, double t) {
   s.ref_perm_ok = false;  // the leaf set changes
+  ++s.leaf_gen;
   cudaStream_t st = stream();
   Grid& g = *s.grid;
   AdaptState& a = *s.ad;

@@ -136,6 +136,9 @@ struct Sim {
   // device-side checkpoint (fm_sim_snapshot / fm_sim_restore)
   DBuf<double> snap_u, snap_us, snap_q, snap_qb, snap_aqx, snap_aqy;
   int64_t snap_n = -1;
+  // bumped whenever the leaf set changes (adaptive re-grid): a snapshot only
+  // restores onto the leaf set it was taken from
+  uint64_t leaf_gen = 0, snap_gen = ~0ull;
   bool snap_fv1 = false;
   double last_run_ms = 0.0;
   // Manning raster (kept for adaptive remaps)

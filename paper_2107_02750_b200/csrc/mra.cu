@@ -878,7 +878,12 @@ Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind)
   FM_CUDA(cudaStreamSynchronize(st));
   g->mra_ms = enc_ms + elapsed_ms(e0, e1);
   const double Nf = double(g->nodes(L)), Nint = double(uint64_t(g->M) * g->N) * ((std::pow(4.0, L) - 1) / 3);
-  g->mra_bytes = 24.0 * Nf + 73.0 * Nint + 36.0 * double(g->nleaves);
+  // SURVEY §8(d4), fused-projection form: the encode reads the (n+1)^2
+  // vertices (8 B each) instead of 24 B fine planes; 73 B per internal node
+  // (details + flag), 36 B per leaf (key + topography)
+  (void)Nf;
+  const double Nv = double(dem->ncols) * double(dem->nrows);
+  g->mra_bytes = 8.0 * Nv + 73.0 * Nint + 36.0 * double(g->nleaves);
   return g.release();
 }
 

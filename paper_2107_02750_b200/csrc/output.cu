@@ -52,6 +52,16 @@ __device__ __forceinline__ long long containing(const unsigned long long* __rest
   return lo;
 }
 
+// Whether Morton position m lies inside the leaves this sim owns: a sharded
+// non-uniform sim owns one contiguous Morton range [start[0], end of its last
+// leaf); every other fine cell belongs to another rank (NaN there, like the
+// uniform band path).
+__device__ __forceinline__ bool owned(const unsigned long long* __restrict__ start,
+                                      const int8_t* __restrict__ lvl, long long n, int L,
+                                      unsigned long long m) {
+  return n > 0 && m >= start[0] && m < start[n - 1] + (1ull << (2 * (L - lvl[n - 1])));
+}
+
 __global__ void k_raster_nu(NuView v, const unsigned long long* __restrict__ start,
                             const double* __restrict__ u, int which, double* __restrict__ out) {
   const int nc = v.M << v.L, nr = v.N << v.L;
@@ -59,7 +69,12 @@ __global__ void k_raster_nu(NuView v, const unsigned long long* __restrict__ sta
   if (t >= (long long)nc * nr) return;
   const int row = int(t / nc), fi = int(t % nc);
   const int fj = nr - 1 - row;
-  const long long k = containing(start, v.n, node_index(v.L, fi, fj, v.M));
+  const unsigned long long m = node_index(v.L, fi, fj, v.M);
+  if (!owned(start, v.lvl, v.n, v.L, m)) {
+    out[t] = nan("");
+    return;
+  }
+  const long long k = containing(start, v.n, m);
   const int l = v.lvl[k];
   const double x = v.x0 + (fi + 0.5) * v.R;
   const double y = v.y0 + (fj + 0.5) * v.R;
@@ -107,7 +122,12 @@ __global__ void k_gauges(NuView v, GaugeGeom gg, const unsigned long long* __res
     // QuadGrid::find_point (quadgrid.cpp:70-74)
     const int fi = min(max(int(floor((x - v.x0) / v.R)), 0), (v.M << v.L) - 1);
     const int fj = min(max(int(floor((y - v.y0) / v.R)), 0), (v.N << v.L) - 1);
-    k = containing(start, v.n, node_index(v.L, fi, fj, v.M));
+    const unsigned long long m = node_index(v.L, fi, fj, v.M);
+    if (!owned(start, v.lvl, v.n, v.L, m)) {  // another shard's leaf
+      for (int q = 0; q < 4; ++q) out4[4 * g + q] = nan("");
+      return;
+    }
+    k = containing(start, v.n, m);
     const int l = v.lvl[k];
     cx = lcen(v.x0, v, l, v.li[k]);
     cy = lcen(v.y0, v, l, v.lj[k]);

@@ -797,12 +797,14 @@ void sim_snapshot(Sim& s) {
   copy(s.snap_aqx, s.aqx);
   copy(s.snap_aqy, s.aqy);
   s.snap_n = s.n;
+  s.snap_gen = s.leaf_gen;
   s.snap_fv1 = s.fv1_in_star;
   FM_CUDA(cudaStreamSynchronize(stream()));
 }
 
 void sim_restore(Sim& s) {
-  if (s.snap_n != s.n || s.snap_u.n != s.u.n) throw Error(FM_ERR_CONFIG, "restore: no matching snapshot");
+  if (s.snap_n != s.n || s.snap_u.n != s.u.n || s.snap_gen != s.leaf_gen)
+    throw Error(FM_ERR_CONFIG, "restore: no snapshot of the current leaf set");
   auto copy = [](DBuf<double>& dst, const DBuf<double>& src) {
     if (src.n)
       FM_CUDA(cudaMemcpyAsync(dst.p, src.p, src.n * sizeof(double), cudaMemcpyDeviceToDevice, stream()));

@@ -92,14 +92,21 @@ def grids():
             np.savez_compressed(os.path.join(OUT, f"grid_{name}_k{kind}.npz"), **d)
 
 
+# Step counts: the horizon at which the fixture's final state is stored.  The
+# DG2 horizons sit inside the reference's own stable window: a run of the
+# oracle with a *different* correctly-rounded cube root (portable libm, a far
+# larger perturbation than CUDA's cbrt, which agrees with glibc on 99.4 % of
+# arguments) first leaves the 1e-9 / 1e-10 tolerance at step 23 (c0, c3),
+# 10 (c4_nu) and 13 (c4_uni) (scripts/golden_horizons.py); FV1/ACC/HWFV1 never
+# do.  The GPU parity tests assert isclose_flow at exactly these horizons.
 SIMS = {
-    "c0_dg2_s8": (S.config0(8), 40),
+    "c0_dg2_s8": (S.config0(8), 15),
     "c1_acc_s16": (S.config1(16), 60),
     "c2_fv1_s16": (S.config2(16, adaptive=False), 60),
     "c2_hwfv1_s16": (S.config2(16), 30),
-    "c3_mwdg2_s32": (S.config3(32), 20),
-    "c4_nu_s64": (S.config4(64), 20),
-    "c4_uni_s64": (S.config4(64, uniform=True), 20),
+    "c3_mwdg2_s32": (S.config3(32), 15),
+    "c4_nu_s64": (S.config4(64), 6),
+    "c4_uni_s64": (S.config4(64, uniform=True), 8),
 }
 
 
@@ -125,7 +132,11 @@ def sims():
 
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    point_kernels()
-    grids()
-    sims()
+    what = sys.argv[1:] or ["points", "grids", "sims"]
+    if "points" in what:
+        point_kernels()
+    if "grids" in what:
+        grids()
+    if "sims" in what:
+        sims()
     print("golden fixtures written to", OUT)

@@ -81,19 +81,21 @@ def test_native_against_reference_golden(gpu, path):
         pytest.skip("uniform raster: see test_uniform_gpu.py")
     s = make(gpu, sc)
     assert np.array_equal(s.download()[3], d["u0"])
+    # the fixture's horizon lies inside the reference's stable window
+    # (scripts/make_golden.py): the production libm must match there
     steps = int(d["run_steps"])
-    if sc.solver == "dg2":
-        steps = 3  # the reference amplifies a 1-ulp cbrt change past 1e-9 within tens of steps
     ck, r = s.run(steps, gauge_interval=10.0)
     lv, i, j, u, z = s.download()
-    assert np.array_equal(lv, d["level"]) and np.array_equal(z, d["z"])
-    if steps == int(d["run_steps"]):
-        assert r.steps == int(d["steps_done"])
-        assert isclose_flow(u, d["u"]).all()
-        assert ck.now == pytest.approx(float(d["now"]), rel=1e-12)
+    assert np.array_equal(lv, d["level"]) and np.array_equal(i, d["i"]) and np.array_equal(j, d["j"])
+    assert np.array_equal(z, d["z"])
+    assert r.steps == int(d["steps_done"]) == steps
+    ok = isclose_flow(u, d["u"])
+    assert ok.all(), f"{int((~ok).sum())} coefficients outside 1e-9 rel / 1e-10 abs after {steps} steps"
+    assert ck.now == pytest.approx(float(d["now"]), rel=1e-12)
 
 
-@pytest.mark.parametrize("name,steps", [("c0_dg2_full", 3), ("c1_acc", 300), ("c2_fv1", 200)])
+@pytest.mark.parametrize("name,steps", [("c0_dg2_full", 40), ("c0_dg2", 10), ("c1_acc", 300),
+                                        ("c2_fv1", 200), ("c4_nu_dg2", 15)])
 def test_native_libm_within_tolerance(gpu, orc, name, steps):
     sc = STATIC[name][0]()
     a, b = make(gpu, sc), make(orc, sc)
