@@ -194,6 +194,11 @@ int fm_sim_create(const fm_sim_desc* desc, const fm_raster* dem, const fm_grid* 
                   fm_sim** out);
 int fm_sim_destroy(fm_sim* s);
 int64_t fm_sim_num_cells(const fm_sim* s);
+/* The sim's QuadGrid geometry (quadgrid.hpp:54-60): finest level L, coarse
+ * blocks M x N, finest element size Rfine and the domain origin (x0, y0).
+ * Uniform sims report L = 0 with M x N the raster's cells. */
+int fm_sim_geometry(const fm_sim* s, int32_t* L, int32_t* M, int32_t* N, double* Rfine, double* x0,
+                    double* y0);
 int64_t fm_sim_num_segments(const fm_sim* s);
 /* Sim::compute_dt (solver_nonuniform.cpp:427-449, solver_uniform.cpp:424-442). */
 int fm_sim_compute_dt(fm_sim* s, double* dt);

@@ -384,6 +384,18 @@ int fm_sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const fm_gri
     *out = h.release();
   });
 }
+int fm_sim_geometry(const fm_sim* s, int32_t* L, int32_t* M, int32_t* N, double* Rfine, double* x0,
+                    double* y0) {
+  return guard([&] {
+    const Sim& m = *s->s;
+    if (L) *L = m.uniform ? 0 : m.L;
+    if (M) *M = m.uniform ? m.nx : m.M;
+    if (N) *N = m.uniform ? (m.nyg ? m.nyg : m.ny) : m.N;
+    if (Rfine) *Rfine = m.R;
+    if (x0) *x0 = m.x0;
+    if (y0) *y0 = m.y0;
+  });
+}
 int fm_sim_shard_info(const fm_sim* s, int32_t* rank, int32_t* nranks, int64_t* first, int64_t* owned,
                       int64_t* halo, int64_t* n_global) {
   return guard([&] {

@@ -297,3 +297,60 @@ def spike(n: int = 16, height: float = 1.0) -> Raster:
     v = np.zeros((n + 1, n + 1))
     v[(n + 1) // 2, (n + 1) // 2] = height
     return Raster(v, cellsize=1.0)
+
+
+def _write_asc(path: str, r: "Raster"):
+    # ESRI ASCII grid as the reference reads and writes it (raster.cpp:22-96):
+    # 17 significant digits, row 0 north
+    v = np.asarray(r.values, dtype=np.float64)
+    with open(path, "w") as f:
+        f.write(f"ncols {v.shape[1]}\nnrows {v.shape[0]}\nxllcorner {r.xll!r}\nyllcorner {r.yll!r}\n"
+                f"cellsize {r.cellsize!r}\nNODATA_value {r.nodata!r}\n")
+        np.savetxt(f, v, fmt="%.17g")
+
+
+def emit_config(sc: "Scenario", out_dir: str, end_time: float, output_interval: float = 0.0,
+                gauge_interval: float = 0.0, gauges=(), threads: int = 1) -> str:
+    """Write `sc` as the reference's own scenario files (config.cpp:93-245
+    `key = value` config, ASCII rasters, `t,Q` hydrograph CSVs) under
+    `out_dir`; returns the config path.  The reference's run_scenario and the
+    GPU drop-in both read exactly these files."""
+    import os
+    os.makedirs(out_dir, exist_ok=True)
+    _write_asc(os.path.join(out_dir, "dem.asc"), sc.dem)
+    names = {"dg2": "dg2", "fv1": "fv1", "acc": "acc", "mwdg2": "mwdg2", "hwfv1": "hwfv1"}
+    lines = ["dem_path = dem.asc", f"solver = {names[sc.solver]}", f"grid_mode = {sc.grid_mode}",
+             f"epsilon = {sc.eps!r}", f"max_level = {sc.L}", f"end_time = {end_time!r}",
+             f"manning = {sc.manning!r}", f"g = {sc.g!r}", f"h_dry = {sc.h_dry!r}",
+             f"adapt_every = {sc.adapt_every}", f"threads = {threads}"]
+    if output_interval > 0:
+        lines.append(f"output_interval = {output_interval!r}")
+    if gauge_interval > 0:
+        lines.append(f"gauge_interval = {gauge_interval!r}")
+    if sc.courant > 0:
+        lines.append(f"courant = {sc.courant!r}")
+    for key, b in zip(("boundary_n", "boundary_e", "boundary_s", "boundary_w"), sc.bc):
+        lines.append(f"{key} = {'open' if b else 'reflective'}")
+    if sc.manning_raster is not None:
+        _write_asc(os.path.join(out_dir, "manning.asc"), sc.manning_raster)
+        lines.append("manning_raster = manning.asc")
+    if sc.initial_depth_raster is not None:
+        _write_asc(os.path.join(out_dir, "h0.asc"), sc.initial_depth_raster)
+        lines.append("initial_depth_raster = h0.asc")
+    if sc.initial_surface is not None:
+        lines.append(f"initial_surface = {sc.initial_surface!r}")
+    if sc.initial_depth:
+        lines.append(f"initial_depth = {sc.initial_depth!r}")
+    for k, f in enumerate(sc.inflows):
+        p = f"hyd{k}.csv"
+        with open(os.path.join(out_dir, p), "w") as h:
+            h.write("t,Q\n")
+            for t, q in zip(f.t, f.q):
+                h.write(f"{t!r},{q!r}\n")
+        lines.append(f"inflow = {p} @ {f.i0} {f.j0} {f.i1} {f.j1}")
+    for x, y in gauges:
+        lines.append(f"gauge = {x!r} {y!r}")
+    path = os.path.join(out_dir, "scenario.cfg")
+    with open(path, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    return path
