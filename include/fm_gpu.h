@@ -143,9 +143,10 @@ int64_t fm_launch_count(void);
 int fm_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* failures);
 
 /* The libm building blocks as the device evaluates them, for tests:
- * fn 0 = pow(x, 7/3) (FM_LIBM_NATIVE: correctly rounded in double-double),
- * 1 = cbrt(x) (native), 2 = CUDA's pow(x, 7.0/3.0), 3 = pow(x, 7/3) with the
- * portable cube root. */
+ * fn 0 = pow(x, 7/3) (FM_LIBM_NATIVE: correctly rounded in double-double,
+ * fp32 correction terms), 1 = cbrt(x) (native), 2 = CUDA's pow(x, 7.0/3.0),
+ * 3 = pow(x, 7/3) with the portable cube root, 4 = the all-fp64
+ * double-double evaluation (the check for fn 0). */
 int fm_eval_libm(int32_t fn, int64_t n, const double* x, double* out);
 
 /* ---- static MRA --------------------------------------------------------- */

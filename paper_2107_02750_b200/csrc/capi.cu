@@ -120,7 +120,7 @@ __global__ void k_eval_libm(int fn, int64_t n, const double* __restrict__ x, dou
   if (k >= n) return;
   const double v = x[k];
   out[k] = fn == 0 ? fmd::pow73_m(v, FM_LIBM_NATIVE) : fn == 1 ? fmd::cbrt_m(v, FM_LIBM_NATIVE)
-         : fn == 2 ? pow(v, 7.0 / 3.0) : fmd::pow73_m(v, FM_LIBM_PORTABLE);
+         : fn == 2 ? pow(v, 7.0 / 3.0) : fn == 3 ? fmd::pow73_m(v, FM_LIBM_PORTABLE) : fmd::pow73_cr(v);
 }
 }  // namespace
 
@@ -468,7 +468,7 @@ int fm_extent_metrics(const fm_raster* test, const fm_raster* ref, double wet_th
 int fm_eval_libm(int32_t fn, int64_t n, const double* x, double* out) {
   return guard([&] {
     require_device();
-    if (fn < 0 || fn > 3) throw Error(FM_ERR_CONFIG, "eval_libm: unknown function");
+    if (fn < 0 || fn > 4) throw Error(FM_ERR_CONFIG, "eval_libm: unknown function");
     DBuf<double> dx, dy(std::max<int64_t>(n, 1));
     dx.upload(x, n);
     k_eval_libm<<<unsigned((n + 255) / 256), 256, 0, stream()>>>(fn, n, dx.p, dy.p);

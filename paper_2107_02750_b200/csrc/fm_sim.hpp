@@ -133,6 +133,13 @@ struct Sim {
   DBuf<DevRed> red;          // [2]
   DBuf<int> errflag;         // device error bits (negative depth into HLL)
   bool fv1_in_star = false;
+  // ACC's compact state while the device loop runs (nu_flow.cu): h (owned +
+  // halo), qx, qy (owned), z.c0 (owned + halo) and the minimum key of a leaf
+  // with a non-finite slope; acc_soa: the compact arrays hold the state and
+  // the c0 columns of U are stale (the slopes in U never change under ACC)
+  DBuf<double> ch, cqx, cqy, czc;
+  DBuf<unsigned long long> cbad;
+  bool acc_soa = false;
   // device-side checkpoint (fm_sim_snapshot / fm_sim_restore)
   DBuf<double> snap_u, snap_us, snap_q, snap_qb, snap_aqx, snap_aqy;
   int64_t snap_n = -1;
@@ -227,8 +234,9 @@ void comm_unique_id(uint8_t* out);
 void comm_destroy(Comm* c);
 void comm_forget(Comm* c, Sim* s);
 Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* grid, Comm* comm, int rank);
-void shard_pack(Sim& s, const double* arr);
-void shard_local_recv(Sim& s, double* arr);
+double* exch_array(Sim& s, int op, int* w);
+void shard_pack(Sim& s, const double* arr, int w);
+void shard_local_recv(Sim& s, double* arr, int w);
 void shard_local_reduce(const std::vector<Sim*>& sims);
 void shard_allreduce_u64_min(Sim& s, unsigned long long* dev, int count);
 double shard_allreduce_sum(Sim& s, double v);

@@ -429,9 +429,19 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
 }
 
 // ---- ACC ------------------------------------------------------------------
+// ACC's state is h.c0, qx.c0, qy.c0 (the slopes are zero and never change,
+// solver_nonuniform.cpp:600-607), so while the device loop runs it lives in
+// three compact arrays (SoA) instead of the 72 B rows: the face kernel's
+// leaf gathers (h, z.c0, n, level: 25 B per leaf, ~60 MB at config 4) stay
+// L2-resident, and the leaf kernel writes 24 B per leaf instead of three
+// partial sectors of a row.  acc_to_soa / acc_to_aos (sim.cu) convert at the
+// API boundary.  The arithmetic is the reference's, operand for operand.
+
 // Per interior segment (solver_nonuniform.cpp:354-371).  Also the step head.
+template <bool P2>
 __global__ void __launch_bounds__(256) k_acc_faces(NuView v, DevClock* clk, DevRed* red,
-                                                  const Hydro* hy, const double* __restrict__ u,
+                                                  const Hydro* hy, const double* __restrict__ ch,
+                                                  const double* __restrict__ czc,
                                                   double* __restrict__ q, int manual, double mdt) {
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int go;
@@ -439,99 +449,202 @@ __global__ void __launch_bounds__(256) k_acc_faces(NuView v, DevClock* clk, DevR
   step_head(v, clk, red, hy, manual, mdt, go, dt);
   if (!go || s >= v.nseg) return;
   const int l = v.seg_l[s], r = v.seg_r[s];
-  const double zl = v.z[3 * l], zr = v.z[3 * r];
-  const double el = u[9 * l] + zl, er = u[9 * r] + zr;
+  const double zl = czc[l], zr = czc[r];
+  const double el = ch[l] + zl, er = ch[r] + zr;
   const double hf = smax(el, er) - smax(zl, zr);
   double Q = q[s];
   if (hf <= v.hdry) {
     q[s] = 0.0;
     return;
   }
-  const double dist = 0.5 * (lsize(v, v.lvl[l]) + lsize(v, v.lvl[r]));
+  const int al = v.lvl[l], ar = v.lvl[r];
+  const double dist = 0.5 * (lsize(v, al) + lsize(v, ar));
   const double nf = 0.5 * (v.nman[l] + v.nman[r]);
-  Q = ddiv(Q - ddiv(v.g * hf * dt * (er - el), dist),
-           1.0 + zdiv(v.g * dt * nf * nf * fabs(Q), pow73_m(hf, v.libm)));
+  // P2, equal levels: dist is the (power-of-two) leaf size and / dist is
+  // exactly * 1/size
+  const double grad = (P2 && al == ar) ? (v.g * hf * dt * (er - el)) * v.linv[al]
+                                       : ddiv(v.g * hf * dt * (er - el), dist);
+  Q = ddiv(Q - grad, 1.0 + zdiv(v.g * dt * nf * nf * fabs(Q), pow73_m(hf, v.libm)));
   q[s] = Q;
+}
+
+// The next step's ACC reductions (compute_dt :429-437, finite_state :479-487)
+// of a block: the minimum wet leaf size, the maximum wet depth and the minimum
+// key of a leaf with a non-finite coefficient, warp then block reduced, one
+// atomic per block and field (one per warp put ~150 k same-address atomics
+// in every step's tail).
+template <int NT>
+__device__ __forceinline__ void reduce_acc(DevRed* red, const DevClock& c, double h, double sz,
+                                           double hdry, unsigned long long bad, bool valid) {
+  double dtc = INFINITY, hm = 0.0;
+  if (valid && h > hdry) {
+    hm = h;
+    dtc = sz;
+  }
+  unsigned long long db = dbits(dtc);
+  const unsigned hi = __reduce_min_sync(0xffffffffu, unsigned(db >> 32));
+  const unsigned lo = __reduce_min_sync(0xffffffffu, unsigned(db >> 32) == hi ? unsigned(db) : 0xffffffffu);
+  db = (static_cast<unsigned long long>(hi) << 32) | lo;
+  for (int o = 16; o; o >>= 1) hm = smax(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+  if (__any_sync(0xffffffffu, bad != ~0ull)) {
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long b2 = __shfl_xor_sync(0xffffffffu, bad, o);
+      bad = b2 < bad ? b2 : bad;
+    }
+  }
+  constexpr int W = NT / 32;
+  __shared__ unsigned long long s_d[W], s_b[W];
+  __shared__ double s_h[W];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_d[w] = db;
+    s_h[w] = hm;
+    s_b[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 1; k < W; ++k) {
+      db = s_d[k] < db ? s_d[k] : db;
+      hm = smax(hm, s_h[k]);
+      bad = s_b[k] < bad ? s_b[k] : bad;
+    }
+    DevRed& r = red[(c.steps) & 1];
+    if (db < dbits(INFINITY)) atomicMin(&r.dtmin, db);
+    if (hm > 0.0) atomicMin(&r.hmaxc, ~dbits(hm));
+    if (bad != ~0ull) atomicMin(&r.badkey, bad);
+  }
 }
 
 // Per leaf: boundary discharges (:372-386), volume update and diagnostic
 // discharges (:387-417), then the fused inflow / finite / CFL epilogue.
-__global__ void __launch_bounds__(256) k_acc_leaves(NuView v, const DevClock* __restrict__ clk,
-                                                   DevRed* red, double* __restrict__ u,
-                                                   const double* __restrict__ q,
-                                                   double* __restrict__ qb, int manual, double mdt) {
+// A side's sub-face length needs no neighbour lookup: on a graded grid it is
+// the leaf's size, or half of it when the side has two (finer) neighbours
+// (kind 3) -- the same IEEE value as min(size_l, size_r).
+constexpr int kAccLeafThreads = 256;
+template <bool P2>
+__global__ void __launch_bounds__(kAccLeafThreads) k_acc_leaves(
+    NuView v, const DevClock* __restrict__ clk, DevRed* red, double* __restrict__ ch,
+    double* __restrict__ cqx, double* __restrict__ cqy, const double* __restrict__ q,
+    double* __restrict__ qb, const unsigned long long* __restrict__ slope_bad, int manual, double mdt) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const DevClock* c = clk + 1;
   if (!manual && !c->active) return;
   const double dt = manual ? mdt : c->dt;
   const bool valid = k < v.n;
-  double s[9];
-  double sz = 0.0;
-  unsigned long long key = 0;
+  double h = 0.0, sz = 0.0;
+  unsigned long long bad = ~0ull;
   if (valid) {
     const int l = v.lvl[k];
     sz = lsize(v, l);
-    key = leaf_key(l, v.li[k], v.lj[k]);
-    load9(u, k, s);
+    const double inv = v.linv[l];  // P2: 1 / sz exactly
+    h = ch[k];
     const uint8_t code = v.sk[k];
+    const int4* srow = reinterpret_cast<const int4*>(v.sid + 8 * k);
+    const int4 s03 = srow[0], s47 = srow[1];
+    const int ids[8] = {s03.x, s03.y, s03.z, s03.w, s47.x, s47.y, s47.z, s47.w};
     const double area = sz * sz;
     double net = 0.0, sx = 0.0, sy = 0.0;
 #pragma unroll
     for (int sd = 0; sd < 4; ++sd) {
       const int kind = (code >> (2 * sd)) & 3;
       const double sign = (sd == 1 || sd == 0) ? -1.0 : 1.0;
-      const int nseg = kind == 0 ? 1 : kind == 3 ? 2 : 1;
-      for (int t = 0; t < nseg; ++t) {
-        double Q, len;
-        if (kind == 0) {
-          double b = qb[4 * k + sd];
-          if (v.bc[sd] == FM_REFLECTIVE) {
+      if (kind == 0) {
+        double b = qb[4 * k + sd];
+        if (v.bc[sd] == FM_REFLECTIVE) {
+          b = 0.0;
+        } else {
+          const double hf = h;
+          if (hf <= v.hdry) {
             b = 0.0;
           } else {
-            const double hf = s[0];
-            if (hf <= v.hdry) {
-              b = 0.0;
-            } else {
-              const double nf = v.nman[k];
-              b = zdiv(b, 1.0 + zdiv(v.g * dt * nf * nf * fabs(b), pow73_m(hf, v.libm)));
-            }
+            const double nf = v.nman[k];
+            b = zdiv(b, 1.0 + zdiv(v.g * dt * nf * nf * fabs(b), pow73_m(hf, v.libm)));
           }
-          qb[4 * k + sd] = b;
-          Q = b;
-          len = sz;
-        } else {
-          const int id = v.sid[8 * k + 2 * sd + t];
-          Q = q[id];
-          const int oth = v.nb[8 * k + 2 * sd + t];
-          const double osz = lsize(v, v.lvl[oth]);
-          len = kind == 1 ? smin(osz, sz) : smin(sz, osz);
         }
-        net += sign * Q * len;
+        qb[4 * k + sd] = b;
+        net += sign * b * sz;
         if (sd == 1 || sd == 3)
-          sx += Q * len;
+          sx += b * sz;
         else
-          sy += Q * len;
+          sy += b * sz;
+      } else {
+        const double len = kind == 3 ? 0.5 * sz : sz;
+        const int nseg = kind == 3 ? 2 : 1;
+        for (int t = 0; t < nseg; ++t) {
+          const double Q = q[ids[2 * sd + t]];
+          net += sign * Q * len;
+          if (sd == 1 || sd == 3)
+            sx += Q * len;
+          else
+            sy += Q * len;
+        }
       }
     }
-    s[0] += zdiv(dt * net, area);
-    s[3] = zdiv(0.5 * sx, sz);
-    s[6] = zdiv(0.5 * sy, sz);
+    // P2: the leaf size and area are powers of two, so the divisions are
+    // exact reciprocal multiplies (bit-identical)
+    h += P2 ? (dt * net) * (inv * inv) : zdiv(dt * net, area);
+    const double qx = div_sz<P2>(0.5 * sx, sz, inv);
+    const double qy = div_sz<P2>(0.5 * sy, sz, inv);
     if (!manual) {
       for (int f = 0; f < v.ninflow; ++f) {
         if (!c->on[f]) continue;
         const int cnt = v.infc[f * v.n + k];
-        if (cnt) s[0] += ddiv(c->per_cell[f] * cnt, area);
+        if (cnt) {
+          const double num = c->per_cell[f] * cnt;
+          h += P2 ? num * (inv * inv) : ddiv(num, area);
+        }
       }
     }
-    u[9 * k] = s[0];
-    u[9 * k + 3] = s[3];
-    u[9 * k + 6] = s[6];
+    ch[k] = h;
+    cqx[k] = qx;
+    cqy[k] = qy;
+    if (!(isfinite(h) && isfinite(qx) && isfinite(qy))) bad = leaf_key(l, v.li[k], v.lj[k]);
   }
-  if (!manual) reduce_leaf(v, red, *c, s, sz, key, valid);
+  if (!manual) {
+    // the slopes never change under ACC: their non-finite key (if any) was
+    // found when the state entered the compact layout
+    if (k == 0 && *slope_bad != ~0ull) bad = min(bad, *slope_bad);
+    reduce_acc<kAccLeafThreads>(red, *c, h, sz, v.hdry, bad, valid);
+  }
+}
+
+// Layout changes of the ACC state.  To SoA: h, qx, qy from the rows, z.c0 of
+// every local leaf (owned + halo) and the minimum key of a leaf with a
+// non-finite slope.  To the rows: c0 of h, qx, qy (the slopes are untouched).
+__global__ void k_acc_to_soa(long long n, long long ntot, const int8_t* __restrict__ lvl,
+                             const int32_t* __restrict__ li, const int32_t* __restrict__ lj,
+                             const double* __restrict__ u, const double* __restrict__ z,
+                             double* __restrict__ ch, double* __restrict__ cqx, double* __restrict__ cqy,
+                             double* __restrict__ czc, unsigned long long* __restrict__ slope_bad) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= ntot) return;
+  czc[k] = z[3 * k];
+  ch[k] = u[9 * k];
+  if (k >= n) return;
+  cqx[k] = u[9 * k + 3];
+  cqy[k] = u[9 * k + 6];
+  const double* r = u + 9 * k;
+  if (!(isfinite(r[1]) && isfinite(r[2]) && isfinite(r[4]) && isfinite(r[5]) && isfinite(r[7]) &&
+        isfinite(r[8])))
+    atomicMin(slope_bad, leaf_key(lvl[k], li[k], lj[k]));
+}
+
+__global__ void k_acc_to_aos(long long n, const double* __restrict__ ch, const double* __restrict__ cqx,
+                             const double* __restrict__ cqy, double* __restrict__ u) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  u[9 * k] = ch[k];
+  u[9 * k + 3] = cqx[k];
+  u[9 * k + 6] = cqy[k];
 }
 
 // Initial reduction (before the first step of a run) into slot steps&1.
-__global__ void k_reduce_init(NuView v, const DevClock* clk, DevRed* red, const double* __restrict__ u) {
+// ACC in the compact layout: c0 of h, qx, qy from the compact arrays (the
+// slopes in U are current: ACC never changes them).
+__global__ void k_reduce_init(NuView v, const DevClock* clk, DevRed* red, const double* __restrict__ u,
+                              const double* __restrict__ ch, const double* __restrict__ cqx,
+                              const double* __restrict__ cqy) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool valid = k < v.n;
   double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -542,6 +655,11 @@ __global__ void k_reduce_init(NuView v, const DevClock* clk, DevRed* red, const 
     sz = lsize(v, l);
     key = leaf_key(l, v.li[k], v.lj[k]);
     load9(u, k, s);
+    if (ch) {
+      s[0] = ch[k];
+      s[3] = cqx[k];
+      s[6] = cqy[k];
+    }
   }
   DevClock c = clk[1];
   reduce_leaf(v, red, c, s, sz, key, valid);
@@ -637,11 +755,13 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       if (s.shard) shard_finish(s);
       if (!manual) launch_decide(s);
       kt_begin(KF_ACC_FACES);
-      k_acc_faces<<<nblk(ns, 256), 256, 0, st>>>(v, clk, red, s.hydro.p, s.u.p, s.accq.p, manual, mdt);
+      (s.p2 ? k_acc_faces<true> : k_acc_faces<false>)<<<nblk(ns, 256), 256, 0, st>>>(
+          v, clk, red, s.hydro.p, s.ch.p, s.czc.p, s.accq.p, manual, mdt);
       FM_LAUNCHED();
       kt_end();
       kt_begin(KF_ACC_LEAVES);
-      k_acc_leaves<<<nblk(n, 256), 256, 0, st>>>(v, clk, red, s.u.p, s.accq.p, s.accqb.p, manual, mdt);
+      (s.p2 ? k_acc_leaves<true> : k_acc_leaves<false>)<<<nblk(n, kAccLeafThreads), kAccLeafThreads, 0, st>>>(
+          v, clk, red, s.ch.p, s.cqx.p, s.cqy.p, s.accq.p, s.accqb.p, s.cbad.p, manual, mdt);
       FM_LAUNCHED();
       kt_end();
       break;
@@ -708,12 +828,31 @@ void launch_head_friction(Sim& s, const double* src, double* dst, bool manual, d
 
 
 void nu_launch_reduce_init(Sim& s) {
-  k_reduce_init<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.u.p);
+  const bool c = s.acc_soa;
+  k_reduce_init<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.u.p, c ? s.ch.p : nullptr,
+                                                       c ? s.cqx.p : nullptr, c ? s.cqy.p : nullptr);
   FM_LAUNCHED();
 }
 
 void nu_launch_close(Sim& s) {
   k_close<<<1, 1, 0, stream()>>>(s.clk.p, s.red.p, s.hydro.p, s.view());
+  FM_LAUNCHED();
+}
+
+void nu_launch_acc_to_soa(Sim& s, long long ntot) {
+  s.ch.alloc(size_t(ntot));
+  s.czc.alloc(size_t(ntot));
+  s.cqx.alloc(size_t(s.n));
+  s.cqy.alloc(size_t(s.n));
+  s.cbad.alloc(1);
+  s.cbad.fill_bytes(0xff);
+  k_acc_to_soa<<<nblk(ntot, 256), 256, 0, stream()>>>(s.n, ntot, s.lvl.p, s.li.p, s.lj.p, s.u.p, s.z.p, s.ch.p,
+                                                       s.cqx.p, s.cqy.p, s.czc.p, s.cbad.p);
+  FM_LAUNCHED();
+}
+
+void nu_launch_acc_to_aos(Sim& s) {
+  k_acc_to_aos<<<nblk(s.n, 256), 256, 0, stream()>>>(s.n, s.ch.p, s.cqx.p, s.cqy.p, s.u.p);
   FM_LAUNCHED();
 }
 

@@ -196,12 +196,12 @@ namespace {
 
 inline unsigned nblk(uint64_t n, int t) { return unsigned((n + t - 1) / t); }
 
-__global__ void k_pack(const double* __restrict__ u, const int32_t* __restrict__ idx, long long m,
+__global__ void k_pack(const double* __restrict__ u, int w, const int32_t* __restrict__ idx, long long m,
                        double* __restrict__ buf) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= 9 * m) return;
-  const long long k = t / 9, q = t % 9;
-  buf[t] = u[9 * (long long)idx[k] + q];
+  if (t >= w * m) return;
+  const long long k = t / w, q = t % w;
+  buf[t] = u[w * (long long)idx[k] + q];
 }
 
 // Local group: min-combine the reduction slots of every shard into all of them.
@@ -620,16 +620,28 @@ Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* gr
 
 // ---- step operations ---------------------------------------------------------
 
-void shard_pack(Sim& s, const double* arr) {
+// The array a halo exchange moves and its width in doubles per leaf: the
+// 72 B rows of U (or U*), or ACC's compact depth (8 B per halo leaf, SURVEY
+// §8 e3) while the ACC state is in its compact layout.
+double* exch_array(Sim& s, int op, int* w) {
+  if (op == OP_EXCH_U && s.acc_soa) {
+    *w = 1;
+    return s.ch.p;
+  }
+  *w = 9;
+  return op == OP_EXCH_U ? s.u.p : s.us.p;
+}
+
+void shard_pack(Sim& s, const double* arr, int w) {
   Shard& sh = *s.shard;
   const long long m = (long long)(sh.soff.empty() ? 0 : sh.soff.back() + sh.scnt.back());
   if (m == 0) return;
-  k_pack<<<nblk(9 * m, 256), 256, 0, stream()>>>(arr, sh.send_idx.p, m, sh.send_buf.p);
+  k_pack<<<nblk(w * m, 256), 256, 0, stream()>>>(arr, w, sh.send_idx.p, m, sh.send_buf.p);
   FM_LAUNCHED();
 }
 
 // Local group: copy every peer's packed slice for this shard into its halo.
-void shard_local_recv(Sim& s, double* arr) {
+void shard_local_recv(Sim& s, double* arr, int w) {
   Shard& sh = *s.shard;
   Comm& c = *sh.comm;
   for (size_t k = 0; k < sh.peers.size(); ++k) {
@@ -641,8 +653,8 @@ void shard_local_recv(Sim& s, double* arr) {
     const size_t j = size_t(it - ps.peers.begin());
     if (ps.scnt[j] != sh.hcnt[k]) throw Error(FM_ERR_STRUCTURE, "local group: halo size mismatch");
     if (sh.hcnt[k])
-      FM_CUDA(cudaMemcpyAsync(arr + 9 * (s.n + sh.hoff[k]), ps.send_buf.p + 9 * ps.soff[j],
-                              9 * sh.hcnt[k] * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+      FM_CUDA(cudaMemcpyAsync(arr + w * (s.n + sh.hoff[k]), ps.send_buf.p + w * ps.soff[j],
+                              w * sh.hcnt[k] * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
   }
 }
 
@@ -683,8 +695,9 @@ void shard_op(Sim& s, int op) {
                              sh.comm->nc, st), "ncclAllReduce");
     return;
   }
-  double* arr = op == OP_EXCH_U ? s.u.p : s.us.p;
-  shard_pack(s, arr);
+  int w = 9;
+  double* arr = exch_array(s, op, &w);
+  shard_pack(s, arr, w);
   // fork: the exchange runs on the side stream, the main stream goes on with
   // the segments that need no halo; shard_finish joins
   if (!sh.side) {
@@ -697,10 +710,10 @@ void shard_op(Sim& s, int op) {
   nccl_check(api.GroupStart(), "ncclGroupStart");
   for (size_t k = 0; k < sh.peers.size(); ++k) {
     if (sh.scnt[k])
-      nccl_check(api.Send(sh.send_buf.p + 9 * sh.soff[k], size_t(9 * sh.scnt[k]), ncclFloat64,
+      nccl_check(api.Send(sh.send_buf.p + w * sh.soff[k], size_t(w * sh.scnt[k]), ncclFloat64,
                           sh.peers[k], sh.comm->nc, sh.side), "ncclSend");
     if (sh.hcnt[k])
-      nccl_check(api.Recv(arr + 9 * (s.n + sh.hoff[k]), size_t(9 * sh.hcnt[k]), ncclFloat64,
+      nccl_check(api.Recv(arr + w * (s.n + sh.hoff[k]), size_t(w * sh.hcnt[k]), ncclFloat64,
                           sh.peers[k], sh.comm->nc, sh.side), "ncclRecv");
   }
   nccl_check(api.GroupEnd(), "ncclGroupEnd");

@@ -17,6 +17,8 @@ void nu_launch_step(Sim& s, bool manual, double mdt, int* err);
 void nu_launch_reduce_init(Sim& s);
 void nu_launch_close(Sim& s);
 void nu_launch_inflow_add(Sim& s, const double* per_cell_dev);
+void nu_launch_acc_to_soa(Sim& s, long long ntot);
+void nu_launch_acc_to_aos(Sim& s);
 // uniform.cu
 void un_launch_step(Sim& s, bool manual, double mdt, int* err);
 void un_launch_reduce_init(Sim& s);
@@ -354,6 +356,32 @@ void fv1_to_star(Sim& s) {
 }
 bool fv1_staged(const Sim& s) { return s.scheme == FM_FV1; }
 
+// ACC on a non-uniform grid keeps h, qx, qy in compact arrays between the API
+// calls that read or write U (nu_flow.cu, k_acc_*).
+bool acc_compact(const Sim& s) { return s.scheme == FM_ACC && !s.uniform && !s.adaptive; }
+void acc_to_soa(Sim& s) {
+  if (acc_compact(s) && !s.acc_soa) {
+    nu_launch_acc_to_soa(s, s.n + (s.shard ? s.shard->n_halo : 0));
+    s.acc_soa = true;
+  }
+}
+void acc_to_u(Sim& s) {
+  if (s.acc_soa) {
+    nu_launch_acc_to_aos(s);
+    s.acc_soa = false;
+  }
+}
+// Every U consumer first brings the state back into U (FV1: from U*, ACC:
+// from the compact arrays); every stepping entry point moves it out again.
+void state_to_u(Sim& s) {
+  if (fv1_staged(s)) fv1_to_u(s);
+  acc_to_u(s);
+}
+void state_to_step(Sim& s) {
+  if (fv1_staged(s)) fv1_to_star(s);
+  acc_to_soa(s);
+}
+
 void init_red(Sim& s) {
   DevRed r[2];
   for (auto& x : r) {
@@ -418,7 +446,7 @@ void key_xy(const Sim& s, unsigned long long key, double* bx, double* by) {
 }  // namespace
 
 double sim_compute_dt(Sim& s) {
-  if (fv1_staged(s)) fv1_to_u(s);
+  state_to_u(s);
   init_red(s);
   DevClock pair0[2] = {};
   s.clk.upload(pair0, 2);  // steps = 0 -> slot 0
@@ -442,7 +470,7 @@ double sim_compute_dt(Sim& s) {
 void sim_step(Sim& s, double dt) {
   DBuf<int> err(1);
   err.zero();
-  if (fv1_staged(s)) fv1_to_star(s);
+  state_to_step(s);
   launch_step(s, true, dt, err.p);
   int h = 0;
   err.download(&h, 1);
@@ -464,7 +492,7 @@ static double hydro_host(const std::vector<double>& t, const std::vector<double>
 }
 
 double sim_apply_inflows(Sim& s, double t, double dt) {
-  if (fv1_staged(s)) fv1_to_u(s);
+  state_to_u(s);
   double added = 0.0;
   double per[kMaxInflows] = {0};
   for (int f = 0; f < s.ninflow; ++f) {
@@ -487,7 +515,7 @@ double sim_apply_inflows(Sim& s, double t, double dt) {
 double sim_volume(Sim& s) {
   // Kahan in reference order (solver_nonuniform.cpp:467-477) over h.c0 and
   // the leaf levels, gathered into reference order on the device
-  if (fv1_staged(s)) fv1_to_u(s);
+  state_to_u(s);
   const int32_t* perm = sim_ref_perm(s);
   std::vector<double> h(s.n);
   std::vector<int32_t> l(s.n, 0);
@@ -507,7 +535,7 @@ double sim_volume(Sim& s) {
 }
 
 bool sim_finite(Sim& s, double* bx, double* by) {
-  if (fv1_staged(s)) fv1_to_u(s);
+  state_to_u(s);
   DBuf<unsigned long long> bad(1);
   bad.fill_bytes(0xff);
   k_finite<<<nblk(s.n, 256), 256, 0, stream()>>>(s.n, s.uniform ? nullptr : s.lvl.p, s.li.p, s.lj.p, s.u.p, bad.p);
@@ -522,13 +550,13 @@ bool sim_finite(Sim& s, double* bx, double* by) {
 }
 
 void sim_sync_u(Sim& s) {
-  if (fv1_staged(s)) fv1_to_u(s);
+  state_to_u(s);
 }
 
 // Reference order: (level, j, i) for leaves (quadgrid.cpp:94-98), j*nx+i for
 // rasters; permuted on the device (order.cu).
 void sim_download(Sim& s, int32_t* lo, int32_t* io, int32_t* jo, double* u9, double* z3) {
-  if (fv1_staged(s)) fv1_to_u(s);
+  state_to_u(s);
   const int32_t* perm = sim_ref_perm(s);
   // U* is idle between steps (FV1's staged state was just moved back to U)
   StageScope lend(s.us.p, s.us.n * sizeof(double));
@@ -541,13 +569,13 @@ void sim_download(Sim& s, int32_t* lo, int32_t* io, int32_t* jo, double* u9, dou
 }
 
 void sim_upload(Sim& s, const double* u9) {
-  if (fv1_staged(s)) fv1_to_u(s);
+  state_to_u(s);
   scatter_rows(sim_ref_perm(s), s.n, 9, u9, s.u.p);
 }
 
 void sim_adapt(Sim& s, double t) {
   if (!s.adaptive) throw Error(FM_ERR_CONFIG, "adapt: not an adaptive simulation");
-  if (fv1_staged(s)) fv1_to_u(s);
+  state_to_u(s);
   adaptive_adapt(s, t);
   s.since_adapt = 0;
 }
@@ -558,7 +586,7 @@ void sim_adapt(Sim& s, double t) {
 // of the last batch are no-ops and the host syncs once per batch.
 void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run_result* out) {
   cudaStream_t st = stream();
-  if (fv1_staged(s)) fv1_to_star(s);
+  state_to_step(s);
   DevClock c0 = fresh_clock(ck, max_steps, stop_at_events);
   DevClock pair[2] = {c0, c0};
   s.clk.upload(pair, 2);
@@ -580,9 +608,9 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
       if (!c.active || !c.had_step) break;
       s.since_adapt += 1;
       if (s.since_adapt >= s.adapt_every && !(c.now >= c.end_time)) {
-        if (fv1_staged(s)) fv1_to_u(s);
+        state_to_u(s);
         adaptive_adapt(s, c.now);
-        if (fv1_staged(s)) fv1_to_star(s);
+        state_to_step(s);
         s.since_adapt = 0;
         // the adapt changed the leaf set: refresh the step's reductions
         DevRed r[2];
@@ -672,7 +700,7 @@ void group_run(const std::vector<Sim*>& sims, fm_clock* ck, int64_t max_steps, i
       throw Error(FM_ERR_CONFIG, "group: shards must be given in rank order and share a communicator");
   const DevClock c0 = fresh_clock(ck, max_steps, stop_at_events);
   for (Sim* s : sims) {
-    if (fv1_staged(*s)) fv1_to_star(*s);
+    state_to_step(*s);
     DevClock pair[2] = {c0, c0};
     s->clk.upload(pair, 2);
     init_red(*s);
@@ -691,8 +719,16 @@ void group_run(const std::vector<Sim*>& sims, fm_clock* ck, int64_t max_steps, i
   for (int64_t k = 0; k < max_steps; ++k) {
     for (int op : ops) {
       if (op == OP_EXCH_U || op == OP_EXCH_US) {
-        for (Sim* s : sims) shard_pack(*s, op == OP_EXCH_U ? s->u.p : s->us.p);
-        for (Sim* s : sims) shard_local_recv(*s, op == OP_EXCH_U ? s->u.p : s->us.p);
+        for (Sim* s : sims) {
+          int w = 9;
+          const double* a = exch_array(*s, op, &w);
+          shard_pack(*s, a, w);
+        }
+        for (Sim* s : sims) {
+          int w = 9;
+          double* a = exch_array(*s, op, &w);
+          shard_local_recv(*s, a, w);
+        }
       } else if (op == OP_REDUCE) {
         shard_local_reduce(sims);
       } else {
@@ -742,7 +778,7 @@ namespace fmh {
 // Per-kernel timing of `steps` device-loop steps launched without a graph.
 void sim_profile(Sim& s, int64_t steps, double* ms, int64_t* counts, int cap, int* nfam) {
   cudaStream_t st = stream();
-  if (fv1_staged(s)) fv1_to_star(s);
+  state_to_step(s);
   fm_clock ck{1e12, 0.0, 10.0, 0.0, 1, 1};
   DevClock c0 = fresh_clock(&ck, steps, 0);
   DevClock pair[2] = {c0, c0};
@@ -785,6 +821,7 @@ void sim_profile(Sim& s, int64_t steps, double* ms, int64_t* counts, int cap, in
 namespace fmh {
 
 void sim_snapshot(Sim& s) {
+  acc_to_u(s);  // the snapshot holds U (ACC's compact state folded back)
   auto copy = [](DBuf<double>& dst, const DBuf<double>& src) {
     dst.alloc(src.n);
     if (src.n)
@@ -816,6 +853,7 @@ void sim_restore(Sim& s) {
   copy(s.aqx, s.snap_aqx);
   copy(s.aqy, s.snap_aqy);
   s.fv1_in_star = s.snap_fv1;
+  s.acc_soa = false;  // U is the state again
   FM_CUDA(cudaStreamSynchronize(stream()));
 }
 

@@ -22,7 +22,10 @@ from paper_2107_02750_b200.abi import Backend
 from paper_2107_02750_b200 import scenarios as S
 be = Backend(LIB, "fm_")
 be.call("init", 0)
+import dataclasses
 sc = S.config4(SCALE)
+if SOLVER != "dg2":
+    sc = dataclasses.replace(sc, solver=SOLVER, courant={"fv1": 0.5, "acc": 0.7}[SOLVER])
 g = be.grid(sc.dem, sc.L, sc.eps)
 s = be.sim(sc, g)
 s.run(5, gauge_interval=1e9)
@@ -42,12 +45,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scale", type=int, default=1)
     ap.add_argument("--steps", type=int, default=16)
+    ap.add_argument("--solver", default="dg2", choices=["dg2", "fv1", "acc"])
     ap.add_argument("libs", nargs="+")
     a = ap.parse_args()
     hashes = set()
     for lib in a.libs:
         code = (CHILD.replace("ROOT", repr(ROOT)).replace("LIB", repr(os.path.abspath(lib)))
-                .replace("SCALE", str(a.scale)).replace("STEPS", str(a.steps)))
+                .replace("SCALE", str(a.scale)).replace("STEPS", str(a.steps))
+                .replace("SOLVER", repr(a.solver)))
         out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
         if out.returncode:
             print(os.path.basename(lib), "FAILED", out.stderr[-2000:])
