@@ -438,34 +438,67 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
 // API boundary.  The arithmetic is the reference's, operand for operand.
 
 // Per interior segment (solver_nonuniform.cpp:354-371).  Also the step head.
+// FM_ACC_SPT segments per thread (strided by the block size, so every load
+// stays coalesced): the independent gather chains (segment ids -> leaf
+// depth / level / Manning) of several segments are in flight together.
+#ifndef FM_ACC_SPT
+#define FM_ACC_SPT 2
+#endif
 template <bool P2>
 __global__ void __launch_bounds__(256) k_acc_faces(NuView v, DevClock* clk, DevRed* red,
                                                   const Hydro* hy, const double* __restrict__ ch,
                                                   const double* __restrict__ czc,
                                                   double* __restrict__ q, int manual, double mdt) {
-  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  constexpr int S = FM_ACC_SPT;
+  const long long s0 = blockIdx.x * (long long)(S * blockDim.x) + threadIdx.x;
   int go;
   double dt;
   step_head(v, clk, red, hy, manual, mdt, go, dt);
-  if (!go || s >= v.nseg) return;
-  const int l = v.seg_l[s], r = v.seg_r[s];
-  const double zl = czc[l], zr = czc[r];
-  const double el = ch[l] + zl, er = ch[r] + zr;
-  const double hf = smax(el, er) - smax(zl, zr);
-  double Q = q[s];
-  if (hf <= v.hdry) {
-    q[s] = 0.0;
-    return;
+  if (!go) return;
+  int l[S], r[S];
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    const long long sj = s0 + j * (long long)blockDim.x;
+    const long long sc = sj < v.nseg ? sj : v.nseg - 1;
+    l[j] = v.seg_l[sc];
+    r[j] = v.seg_r[sc];
   }
-  const int al = v.lvl[l], ar = v.lvl[r];
-  const double dist = 0.5 * (lsize(v, al) + lsize(v, ar));
-  const double nf = 0.5 * (v.nman[l] + v.nman[r]);
-  // P2, equal levels: dist is the (power-of-two) leaf size and / dist is
-  // exactly * 1/size
-  const double grad = (P2 && al == ar) ? (v.g * hf * dt * (er - el)) * v.linv[al]
-                                       : ddiv(v.g * hf * dt * (er - el), dist);
-  Q = ddiv(Q - grad, 1.0 + zdiv(v.g * dt * nf * nf * fabs(Q), pow73_m(hf, v.libm)));
-  q[s] = Q;
+  double zl[S], zr[S], hl[S], hr[S], Qo[S], nl[S], nr[S];
+  int al[S], ar[S];
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    const long long sj = s0 + j * (long long)blockDim.x;
+    const long long sc = sj < v.nseg ? sj : v.nseg - 1;
+    zl[j] = czc[l[j]];
+    zr[j] = czc[r[j]];
+    hl[j] = ch[l[j]];
+    hr[j] = ch[r[j]];
+    Qo[j] = q[sc];
+    al[j] = v.lvl[l[j]];
+    ar[j] = v.lvl[r[j]];
+    nl[j] = v.nman[l[j]];
+    nr[j] = v.nman[r[j]];
+  }
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    const long long sj = s0 + j * (long long)blockDim.x;
+    if (sj >= v.nseg) break;
+    const double el = hl[j] + zl[j], er = hr[j] + zr[j];
+    const double hf = smax(el, er) - smax(zl[j], zr[j]);
+    double Q = Qo[j];
+    if (hf <= v.hdry) {
+      q[sj] = 0.0;
+      continue;
+    }
+    const double dist = 0.5 * (lsize(v, al[j]) + lsize(v, ar[j]));
+    const double nf = 0.5 * (nl[j] + nr[j]);
+    // P2, equal levels: dist is the (power-of-two) leaf size and / dist is
+    // exactly * 1/size
+    const double grad = (P2 && al[j] == ar[j]) ? (v.g * hf * dt * (er - el)) * v.linv[al[j]]
+                                               : ddiv(v.g * hf * dt * (er - el), dist);
+    Q = ddiv(Q - grad, 1.0 + zdiv(v.g * dt * nf * nf * fabs(Q), pow73_m(hf, v.libm)));
+    q[sj] = Q;
+  }
 }
 
 // The next step's ACC reductions (compute_dt :429-437, finite_state :479-487)
@@ -755,7 +788,7 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       if (s.shard) shard_finish(s);
       if (!manual) launch_decide(s);
       kt_begin(KF_ACC_FACES);
-      (s.p2 ? k_acc_faces<true> : k_acc_faces<false>)<<<nblk(ns, 256), 256, 0, st>>>(
+      (s.p2 ? k_acc_faces<true> : k_acc_faces<false>)<<<nblk(ns, 256 * FM_ACC_SPT), 256, 0, st>>>(
           v, clk, red, s.hydro.p, s.ch.p, s.czc.p, s.accq.p, manual, mdt);
       FM_LAUNCHED();
       kt_end();
