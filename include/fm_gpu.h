@@ -238,6 +238,12 @@ int fm_sim_sample_gauges(fm_sim* s, int32_t n, const double* x, const double* y,
  * since the snapshot (adaptive re-gridding). */
 int fm_sim_snapshot(fm_sim* s);
 int fm_sim_restore(fm_sim* s);
+/* UniformSim's ACC face discharges acc_qx ((nx+1) x ny, row-major j*(nx+1)+i)
+ * and acc_qy (nx x (ny+1)) (solver_uniform.hpp:53-54), read into get_x/get_y
+ * and/or overwritten from set_x/set_y (any pointer may be NULL); the tests of
+ * test_solver_uniform.cpp:303-326 set and read them directly.  Uniform ACC
+ * sims only (FM_ERR_CONFIG otherwise). */
+int fm_sim_acc_faces(fm_sim* s, double* get_x, double* get_y, const double* set_x, const double* set_y);
 /* AdaptiveSim::element_log (solver_adaptive.hpp:23): number of entries, and copy. */
 int64_t fm_sim_element_log(fm_sim* s, double* t, int64_t* count, int64_t cap);
 /* The drive<Sim> loop body (run.cpp:80-111) resident on the device:
@@ -278,6 +284,12 @@ int fm_comm_create_nccl(int32_t nranks, int32_t rank, const uint8_t id[128], fm_
 /* Local group: all ranks as shards in this process on this device, stepped
  * together by fm_group_run (single-GPU check of the partition logic). */
 int fm_comm_create_local(int32_t nranks, fm_comm** out);
+/* A host transport: one process per rank (any devices, one GPU included),
+ * halo slices and reduction slots staged through the POSIX shared-memory
+ * segment `name` ("/..."; every rank passes the same name, rank 0 unlinks it
+ * on destroy) with a process-shared barrier.  Steps are not graph-captured
+ * on this transport.  Collective: every rank must call it. */
+int fm_comm_create_host(int32_t nranks, int32_t rank, const char* name, fm_comm** out);
 int fm_comm_destroy(fm_comm* c);
 /* make_nonuniform_sim (solver_nonuniform.cpp:558-636) restricted to this
  * rank's shard.  fm_sim_run / step / compute_dt / finite / volume on an NCCL

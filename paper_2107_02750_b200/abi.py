@@ -123,6 +123,8 @@ OPTIONAL = {
     "sim_restore": (C.c_int, [P]),
     "sim_kernel_name": (C.c_char_p, [P, I32]),
     "sim_acc_q": (C.c_int, [P, PD, PD]),
+    "sim_acc_faces": (C.c_int, [P, PD, PD, PD, PD]),
+    "sim_geometry": (C.c_int, [P, PI32, PI32, PI32, PD, PD, PD]),
     "set_threads": (None, [I32]),
     "hw_threads": (I32, []),
     "generate_static_grid": (C.c_int, [C.POINTER(c_raster), I32, D, I32, I32, PI64]),
@@ -138,6 +140,7 @@ OPTIONAL = {
     "comm_unique_id": (C.c_int, [C.c_char_p]),
     "comm_create_nccl": (C.c_int, [I32, I32, C.c_char_p, PP]),
     "comm_create_local": (C.c_int, [I32, PP]),
+    "comm_create_host": (C.c_int, [I32, I32, C.c_char_p, PP]),
     "comm_destroy": (C.c_int, [P]),
     "sim_create_shard": (C.c_int, [C.POINTER(c_desc), C.POINTER(c_raster), P, P, I32, PP]),
     "sim_shard_info": (C.c_int, [P, PI32, PI32, PI64, PI64, PI64, PI64]),
@@ -250,6 +253,12 @@ class Backend:
     def comm_nccl(self, nranks: int, rank: int, uid: bytes) -> "Comm":
         h = P()
         self.call("comm_create_nccl", int(nranks), int(rank), C.c_char_p(bytes(uid)), C.byref(h))
+        return Comm(self, h, nranks, rank)
+
+    def comm_host(self, nranks: int, rank: int, name: str) -> "Comm":
+        """fm_comm_create_host: one process per rank over a shared-memory segment."""
+        h = P()
+        self.call("comm_create_host", int(nranks), int(rank), name.encode(), C.byref(h))
         return Comm(self, h, nranks, rank)
 
     def shard_sim(self, scenario, grid, comm: "Comm", rank: int, libm: int = 0):
@@ -494,6 +503,27 @@ class Sim:
         if u9.shape != (self.num_cells, 9):
             raise ValueError(f"upload: u9 must have shape ({self.num_cells}, 9), got {u9.shape}")
         self.be.call("sim_upload", self.h, dptr(u9))
+
+    def acc_faces(self, set_x=None, set_y=None):
+        """UniformSim acc_qx / acc_qy (solver_uniform.hpp:53-54): optionally
+        overwrite them, then return copies ((nx+1) x ny and nx x (ny+1))."""
+        g = self.geometry()
+        nx, ny = g["M"], g["N"]
+        gx = np.zeros((ny, nx + 1))
+        gy = np.zeros((ny + 1, nx))
+        sx = None if set_x is None else np.ascontiguousarray(set_x, np.float64).reshape(ny, nx + 1)
+        sy = None if set_y is None else np.ascontiguousarray(set_y, np.float64).reshape(ny + 1, nx)
+        px = None if sx is None else dptr(sx)
+        py = None if sy is None else dptr(sy)
+        self.be.call("sim_acc_faces", self.h, dptr(gx), dptr(gy), px, py)
+        return gx, gy
+
+    def geometry(self) -> dict:
+        L, M, N = I32(), I32(), I32()
+        R, x0, y0 = D(), D(), D()
+        self.be.call("sim_geometry", self.h, C.byref(L), C.byref(M), C.byref(N), C.byref(R),
+                     C.byref(x0), C.byref(y0))
+        return dict(L=L.value, M=M.value, N=N.value, R=R.value, x0=x0.value, y0=y0.value)
 
     def shard_info(self) -> dict:
         r, nr = I32(), I32()

@@ -364,6 +364,13 @@ int fm_comm_create_nccl(int32_t nranks, int32_t rank, const uint8_t id[128], fm_
     *out = h.release();
   });
 }
+int fm_comm_create_host(int32_t nranks, int32_t rank, const char* name, fm_comm** out) {
+  return guard([&] {
+    auto h = std::make_unique<fm_comm>();
+    h->c = comm_create_host(nranks, rank, name);
+    *out = h.release();
+  });
+}
 int fm_comm_create_local(int32_t nranks, fm_comm** out) {
   return guard([&] {
     auto h = std::make_unique<fm_comm>();
@@ -382,6 +389,18 @@ int fm_sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const fm_gri
     auto h = std::make_unique<fm_sim>();
     h->s.reset(sim_create_shard(d, dem, grid ? grid->g.get() : nullptr, comm->c, rank));
     *out = h.release();
+  });
+}
+int fm_sim_acc_faces(fm_sim* s, double* gx, double* gy, const double* sx, const double* sy) {
+  return guard([&] {
+    Sim& m = *s->s;
+    if (!m.uniform || m.scheme != FM_ACC || m.shard)
+      throw Error(FM_ERR_CONFIG, "acc_faces: an unsharded uniform ACC simulation only");
+    if (sx) m.aqx.upload(sx, m.aqx.n);
+    if (sy) m.aqy.upload(sy, m.aqy.n);
+    if (gx) m.aqx.download(gx, m.aqx.n);
+    if (gy) m.aqy.download(gy, m.aqy.n);
+    FM_CUDA(cudaStreamSynchronize(stream()));
   });
 }
 int fm_sim_geometry(const fm_sim* s, int32_t* L, int32_t* M, int32_t* N, double* Rfine, double* x0,

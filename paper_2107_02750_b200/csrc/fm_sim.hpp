@@ -230,6 +230,8 @@ ShardPlan shard_plan(int64_t n, int64_t nseg, const int32_t* seg_l, const int32_
                      int rank);
 Comm* comm_create_local(int nranks);
 Comm* comm_create_nccl(int nranks, int rank, const uint8_t* id);
+Comm* comm_create_host(int nranks, int rank, const char* name);
+bool shard_eager(const Sim& s);  // the step cannot be graph-captured (host transport)
 void comm_unique_id(uint8_t* out);
 void comm_destroy(Comm* c);
 void comm_forget(Comm* c, Sim* s);

@@ -19,12 +19,26 @@
 // sim's CUDA graph.
 //
 // Transports: NCCL (one process per GPU; libnccl is loaded at run time, the
-// copy already in the process when there is one, e.g. torch's), or a local
+// copy already in the process when there is one, e.g. torch's), a local
 // group (all ranks as shards of one process on one device, driven phase by
 // phase by fm_group_run) — the single-GPU harness that checks the partition,
-// halo and reduction logic bit-for-bit against the unsharded sim.
+// halo and reduction logic bit-for-bit against the unsharded sim — or a host
+// transport (one process per rank, any devices, the halo slices and the
+// reduction slots staged through a POSIX shared-memory segment with a
+// process-shared barrier): the library's own pack / halo-slot / reduction
+// code across real process boundaries, on however many GPUs there are,
+// including one (no kernel ever waits on another rank; only host threads do).
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <nccl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <chrono>
+#include <string>
 
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
@@ -92,14 +106,110 @@ static void nccl_check(ncclResult_t r, const char* what) {
     throw Error(FM_ERR_CUDA, std::string("[nccl] ") + what + ": " + nccl().ErrorString(r));
 }
 
-enum CommKind { COMM_LOCAL = 0, COMM_NCCL = 1 };
+enum CommKind { COMM_LOCAL = 0, COMM_NCCL = 1, COMM_HOST = 2 };
+
+// Host transport: one shared-memory segment per partition.  Layout: the
+// barrier header, the reduction area (nranks x 8 u64), then nranks x nranks
+// slots (src, dst) of slot_bytes each for the halo slices.
+struct ShmHeader {
+  std::atomic<int> count;
+  std::atomic<int> gen;
+  int nranks;
+  int pad;
+};
+constexpr size_t kShmReduce = 64;  // bytes per rank in the reduction area
+constexpr size_t kShmBytes = size_t(256) << 20;
 
 struct Comm {
   int kind = COMM_LOCAL;
   int nranks = 1, rank = 0;
   ncclComm_t nc = nullptr;
   std::vector<Sim*> members;  // local group: the shard sim of each rank (or null)
+  // host transport
+  std::string shm_name;
+  void* shm = nullptr;
+  size_t slot_bytes = 0;
+  std::vector<double> stage;  // host staging of the packed send buffer
+  ShmHeader* hdr() const { return static_cast<ShmHeader*>(shm); }
+  unsigned char* reduce_area() const { return static_cast<unsigned char*>(shm) + 64; }
+  unsigned char* slot(int src, int dst) const {
+    return reduce_area() + kShmReduce * size_t(nranks) + (size_t(src) * nranks + dst) * slot_bytes;
+  }
 };
+
+// Sense-counting barrier of the ranks' host threads over the segment.  A rank
+// that waits longer than two minutes gives up (a peer died).
+static void shm_barrier(Comm& c) {
+  ShmHeader* h = c.hdr();
+  const int g = h->gen.load(std::memory_order_acquire);
+  if (h->count.fetch_add(1, std::memory_order_acq_rel) == c.nranks - 1) {
+    h->count.store(0, std::memory_order_relaxed);
+    h->gen.fetch_add(1, std::memory_order_acq_rel);
+    return;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  int spins = 0;
+  while (h->gen.load(std::memory_order_acquire) == g) {
+    if (++spins > 1000) {
+      sched_yield();
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+        throw Error(FM_ERR_OTHER, "host transport: a peer rank did not reach the barrier");
+    }
+  }
+}
+
+Comm* comm_create_host(int nranks, int rank, const char* name) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(FM_ERR_CONFIG, "comm: bad rank / size");
+  if (!name || name[0] != '/') throw Error(FM_ERR_CONFIG, "host comm: the name must start with '/'");
+  auto c = std::make_unique<Comm>();
+  c->kind = COMM_HOST;
+  c->nranks = nranks;
+  c->rank = rank;
+  c->shm_name = name;
+  const int fd = shm_open(name, O_CREAT | O_RDWR, 0600);
+  if (fd < 0) throw Error(FM_ERR_IO, std::string("host comm: shm_open failed for ") + name);
+  if (ftruncate(fd, off_t(kShmBytes)) != 0) {
+    close(fd);
+    throw Error(FM_ERR_IO, "host comm: ftruncate failed");
+  }
+  void* p = mmap(nullptr, kShmBytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) throw Error(FM_ERR_IO, "host comm: mmap failed");
+  c->shm = p;
+  c->slot_bytes = ((kShmBytes - 64 - kShmReduce * nranks) / (size_t(nranks) * nranks)) & ~size_t(63);
+  shm_barrier(*c);  // every rank has the segment mapped (a fresh one is zero-filled)
+  return c.release();
+}
+
+static void host_allreduce_u64_min(Comm& c, unsigned long long* dev, int count) {
+  if (count > int(kShmReduce / 8)) throw Error(FM_ERR_OTHER, "host comm: reduction too wide");
+  unsigned long long v[8];
+  FM_CUDA(cudaMemcpyAsync(v, dev, count * 8, cudaMemcpyDeviceToHost, stream()));
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  std::memcpy(c.reduce_area() + kShmReduce * c.rank, v, count * 8);
+  shm_barrier(c);
+  for (int r = 0; r < c.nranks; ++r) {
+    unsigned long long w[8];
+    std::memcpy(w, c.reduce_area() + kShmReduce * r, count * 8);
+    for (int q = 0; q < count; ++q) v[q] = std::min(v[q], w[q]);
+  }
+  shm_barrier(c);  // the area may be reused
+  FM_CUDA(cudaMemcpyAsync(dev, v, count * 8, cudaMemcpyHostToDevice, stream()));
+  FM_CUDA(cudaStreamSynchronize(stream()));
+}
+
+static double host_allreduce_sum(Comm& c, double x) {
+  std::memcpy(c.reduce_area() + kShmReduce * c.rank, &x, 8);
+  shm_barrier(c);
+  double sum = 0.0;  // rank order: the same bits on every rank
+  for (int r = 0; r < c.nranks; ++r) {
+    double w;
+    std::memcpy(&w, c.reduce_area() + kShmReduce * r, 8);
+    sum += w;
+  }
+  shm_barrier(c);
+  return sum;
+}
 
 Comm* comm_create_local(int nranks) {
   if (nranks < 1) throw Error(FM_ERR_CONFIG, "comm: nranks must be >= 1");
@@ -132,6 +242,10 @@ Comm* comm_create_nccl(int nranks, int rank, const uint8_t* id) {
 void comm_destroy(Comm* c) {
   if (!c) return;
   if (c->kind == COMM_NCCL && c->nc) nccl().CommDestroy(c->nc);
+  if (c->kind == COMM_HOST && c->shm) {
+    munmap(c->shm, kShmBytes);
+    if (c->rank == 0) shm_unlink(c->shm_name.c_str());
+  }
   for (Sim* s : c->members)
     if (s && s->shard) s->shard->comm = nullptr;
   delete c;
@@ -450,8 +564,8 @@ int64_t select_flagged(const uint8_t* flags, int64_t n, DBuf<int32_t>& out) {
 Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* grid, Comm* comm, int rank) {
   if (!comm) throw Error(FM_ERR_CONFIG, "shard: null communicator");
   if (rank < 0 || rank >= comm->nranks) throw Error(FM_ERR_CONFIG, "shard: rank out of range");
-  if (comm->kind == COMM_NCCL && rank != comm->rank)
-    throw Error(FM_ERR_CONFIG, "shard: rank differs from the NCCL communicator's");
+  if ((comm->kind == COMM_NCCL || comm->kind == COMM_HOST) && rank != comm->rank)
+    throw Error(FM_ERR_CONFIG, "shard: rank differs from the communicator's");
   if (d->solver == FM_MWDG2 || d->solver == FM_HWFV1)
     throw Error(FM_ERR_CONFIG, "shard: adaptive sims re-grid every step and run as replicas");
   if (!grid) return uniform_shard(d, dem, comm, rank);
@@ -681,9 +795,45 @@ void shard_finish(Sim& s) {
   sh.pending = false;
 }
 
+// A host-transport exchange: pack, stage the slices through the segment,
+// land the peers' slices in the halo slots.
+static void host_exchange(Sim& s, double* arr, int w) {
+  Shard& sh = *s.shard;
+  Comm& c = *sh.comm;
+  shard_pack(s, arr, w);
+  const long long m = (long long)(sh.soff.empty() ? 0 : sh.soff.back() + sh.scnt.back());
+  c.stage.resize(size_t(std::max<long long>(m, 1)) * w);
+  if (m) FM_CUDA(cudaMemcpyAsync(c.stage.data(), sh.send_buf.p, size_t(m) * w * 8, cudaMemcpyDeviceToHost, stream()));
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  for (size_t k = 0; k < sh.peers.size(); ++k) {
+    const size_t bytes = size_t(sh.scnt[k]) * w * 8;
+    if (bytes > c.slot_bytes) throw Error(FM_ERR_OTHER, "host comm: halo slice larger than a slot");
+    if (bytes) std::memcpy(c.slot(sh.rank, sh.peers[k]), c.stage.data() + size_t(w) * sh.soff[k], bytes);
+  }
+  shm_barrier(c);
+  for (size_t k = 0; k < sh.peers.size(); ++k)
+    if (sh.hcnt[k])
+      FM_CUDA(cudaMemcpyAsync(arr + size_t(w) * (s.n + sh.hoff[k]), c.slot(sh.peers[k], sh.rank),
+                              size_t(sh.hcnt[k]) * w * 8, cudaMemcpyHostToDevice, stream()));
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  shm_barrier(c);  // the slots may be reused
+}
+
+bool shard_eager(const Sim& s) { return s.shard && s.shard->comm && s.shard->comm->kind == COMM_HOST; }
+
 void shard_op(Sim& s, int op) {
   Shard& sh = *s.shard;
   if (!sh.comm) throw Error(FM_ERR_CONFIG, "shard: the communicator was destroyed");
+  if (sh.comm->kind == COMM_HOST) {
+    if (op == OP_REDUCE) {
+      host_allreduce_u64_min(*sh.comm, reinterpret_cast<unsigned long long*>(s.red.p), 8);
+    } else {
+      int w = 9;
+      double* arr = exch_array(s, op, &w);
+      host_exchange(s, arr, w);
+    }
+    return;
+  }
   if (sh.comm->kind != COMM_NCCL)
     throw Error(FM_ERR_CONFIG, "shard: a local-group shard steps only through fm_group_run");
   const NcclApi& api = nccl();
@@ -724,12 +874,17 @@ void shard_op(Sim& s, int op) {
 // Host-API reductions of a sharded sim across its NCCL ranks (a local-group
 // shard answers for itself).
 void shard_allreduce_u64_min(Sim& s, unsigned long long* dev, int count) {
+  if (s.shard && s.shard->comm && s.shard->comm->kind == COMM_HOST) {
+    host_allreduce_u64_min(*s.shard->comm, dev, count);
+    return;
+  }
   if (!s.shard || !s.shard->comm || s.shard->comm->kind != COMM_NCCL) return;
   shard_finish(s);
   nccl_check(nccl().AllReduce(dev, dev, size_t(count), ncclUint64, ncclMin, s.shard->comm->nc, stream()),
              "ncclAllReduce");
 }
 double shard_allreduce_sum(Sim& s, double v) {
+  if (s.shard && s.shard->comm && s.shard->comm->kind == COMM_HOST) return host_allreduce_sum(*s.shard->comm, v);
   if (!s.shard || !s.shard->comm || s.shard->comm->kind != COMM_NCCL) return v;
   DBuf<double> d;
   d.upload(&v, 1);

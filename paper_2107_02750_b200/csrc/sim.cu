@@ -625,6 +625,19 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
         launch_reduce_init(s);
       }
     }
+  } else if (shard_eager(s)) {
+    // host transport: every exchange and reduction waits on the host, so the
+    // steps are launched one by one (the per-step decision on the device
+    // still turns surplus steps into no-ops)
+    for (int64_t k = 0; k < max_steps; ++k) {
+      launch_step(s, false, 0.0, err.p);
+      if ((k & 31) == 31 && k + 1 < max_steps) {
+        DevClock c;
+        read_clock(s, c);
+        FM_CUDA(cudaStreamSynchronize(st));
+        if (!c.active) break;
+      }
+    }
   } else {
     // graphs of 32, 8 and 1 steps, captured on first use; the step count is
     // covered greedily so no graph replays surplus (no-op) steps

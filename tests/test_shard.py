@@ -286,3 +286,105 @@ def test_device_plan_matches_host_plan(gpu, nranks):
         assert (info["first"], info["owned"], info["halo"]) == (p["first"], p["count"], len(p["halo"]))
         assert sh.num_segments == p["nseg_local"]
         del sh
+
+
+# ------------------------------------------- host transport, real processes
+
+HOST_CASES = {
+    "c0_dg2_s4": (lambda: S.config0(4), 30, True),
+    "c1_acc_s8": (lambda: S.config1(8), 30, True),
+    "c2_fv1_s8": (lambda: S.config2(8, adaptive=False), 30, True),
+    "c4_uniform_dg2_s32": (lambda: S.config4(32, uniform=True), 20, False),
+}
+
+
+def _host_rank(name, nranks, rank, shm, out_q):
+    """One rank in its own process: the library's shard code (pack, halo
+    slots, reduction) over the host transport; reports its owned state."""
+    try:
+        from paper_2107_02750_b200 import api
+        lib = api.lib()
+        mk, steps, static = HOST_CASES[name]
+        sc = mk()
+        comm = lib.comm_host(nranks, rank, shm)
+        g = lib.grid(sc.dem, sc.L, sc.eps) if static else None
+        sh = lib.shard_sim(sc, g, comm, rank)
+        ck, r = sh.run(steps, gauge_interval=10.0)
+        dt = sh.compute_dt()
+        vol = sh.volume()
+        ok, _, _ = sh.finite_state()
+        out_q.put((rank, (r.steps, r.dt_min, r.dt_max, ck.now, dt, vol, ok), sh.download()))
+        del sh
+    except Exception as e:  # surfaced by the parent
+        out_q.put((rank, repr(e), None))
+
+
+def _handshake(nranks, rank, shm, out_q):
+    lib = cpu_lib()
+    c = lib.comm_host(nranks, rank, shm)  # returns only once every rank has mapped the segment
+    out_q.put(rank)
+    del c
+
+
+def test_host_comm_handshake_across_processes():
+    """CPU: the host transport's segment and barrier across real processes
+    (no device needed to create and join it)."""
+    import multiprocessing as mp
+    import uuid
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    shm = f"/fm_test_{uuid.uuid4().hex[:12]}"
+    procs = [ctx.Process(target=_handshake, args=(3, r, shm, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == [0, 1, 2]
+    assert not os.path.exists("/dev/shm" + shm)  # rank 0 unlinked it
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("name", list(HOST_CASES))
+def test_host_transport_processes_match_unsharded_bit_exact(gpu, name, nranks):
+    """nranks processes, one shard each, exchanging halos and reduction slots
+    through fm_comm_create_host (shared memory), end in the unsharded sim's
+    state bits; the host-API collectives (compute_dt, finite_state) agree and
+    volume() is the rank-order sum of the shards' audits."""
+    import multiprocessing as mp
+    import uuid
+    mk, steps, static = HOST_CASES[name]
+    sc = mk()
+    g = gpu.grid(sc.dem, sc.L, sc.eps) if static else None
+    ref = gpu.sim(sc, g)
+    ck_a, ra = ref.run(steps, gauge_interval=10.0)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    shm = f"/fm_test_{uuid.uuid4().hex[:12]}"
+    procs = [ctx.Process(target=_host_rank, args=(name, nranks, r, shm, q)) for r in range(nranks)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=600) for _ in procs), key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=120)
+    for rank, stats, _ in res:
+        assert not isinstance(stats, str), f"rank {rank}: {stats}"
+    for p in procs:
+        assert p.exitcode == 0
+    for rank, stats, _ in res:
+        steps_b, dtmin, dtmax, now, dt, vol, ok = stats
+        assert (ra.steps, ra.dt_min, ra.dt_max, ck_a.now) == (steps_b, dtmin, dtmax, now)
+        assert dt == ref.compute_dt() and ok
+        assert vol == pytest.approx(ref.volume(), rel=1e-12)
+    parts = [r[2] for r in res]
+    a = ref.download()
+    if static:
+        lv, i, j, u, z = (np.concatenate([p[k] for p in parts]) for k in range(5))
+        order = np.lexsort((i, j, lv))
+        b = (lv[order], i[order], j[order], u[order], z[order])
+    else:  # row bands in rank order
+        b = tuple(np.concatenate([p[k] for p in parts]) for k in range(5))
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
