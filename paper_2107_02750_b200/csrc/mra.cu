@@ -50,6 +50,8 @@ struct Scalars {
   int flags;                    // kNodataSeen | kBig (k_dem_stats)
   double wall;
   double norm;
+  int redo;                     // the speculative encode met a nodata / non-finite / huge vertex
+  int pad;
 };
 
 // field.cpp:48-54 (nodata wall) — max over the non-nodata vertex samples.
@@ -179,7 +181,8 @@ struct EncParams {
   double* sc_out;            // tile-root scaling (3 per node) at level lev_in - T
   double* det[kMaxL];        // per level, 9 per node
   uint8_t* flag[kMaxL];      // per level, significance
-  const Scalars* scal;
+  double* dmx[kMaxL];        // SPEC: per level, max |d| (the numerator of d_hat)
+  Scalars* scal;
   double eps;
   int lev_in, T, M, kind;
 };
@@ -212,7 +215,22 @@ __device__ __forceinline__ void store_details(const double* __restrict__ sdet, d
 #ifndef FM_ENC_T
 #define FM_ENC_T 5  // levels per encode pass (4^(T-1) threads per CTA)
 #endif
-template <bool FROM_VERTICES>
+__device__ __forceinline__ double max_abs9(const double d[9]) {
+  double m = 0.0;
+#pragma unroll
+  for (int n = 0; n < 9; ++n) m = smax(m, fabs(d[n]));
+  return m;
+}
+// SPEC (speculative single DEM read): the DEM statistics are not known yet,
+// so the encode assumes what holds for every DEM without nodata, non-finite
+// or |z| > 1e300 vertices -- no wall, zero taps dropped -- and checks that
+// assumption on every vertex it reads (redo if it fails: the caller reruns
+// the exact two-pass path).  It takes field_norm (max |c0| over the fine
+// planes, detail_tree.cpp:22-23) from the planes it projects, and writes
+// max |d| per node instead of the flag; k_sig_from_dmx forms
+// d_hat = max|d| / max(1, norm) >= eps once the norm is complete, the same
+// operations as dhat() (wavelets.cpp:137-149).
+template <bool FROM_VERTICES, bool SPEC>
 __global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) {
   extern __shared__ double smem[];
   const int nthr = blockDim.x;
@@ -220,13 +238,15 @@ __global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) 
   double* sdet = smem + 3 * nthr;  // 9 per first-level parent
   const int tid = threadIdx.x;
   const uint64_t tile = blockIdx.x;
-  const double norm = p.scal->norm;
+  const double norm = SPEC ? 0.0 : p.scal->norm;
   // every input finite (a non-finite vertex fails the build) and bounded
-  const bool skip0 = !(p.scal->flags & kBig);
+  const bool skip0 = SPEC || !(p.scal->flags & kBig);
   // a register copy: writing into the by-value parameter struct would make
   // every thread spill the whole 344-byte EncParams to local memory
   VertexView vv = p.vv;
-  if constexpr (FROM_VERTICES) vv.wall = p.scal->wall;
+  if constexpr (FROM_VERTICES && !SPEC) vv.wall = p.scal->wall;
+  // SPEC: a nodata vertex reads as NaN, which the vertex check turns into a redo
+  if constexpr (FROM_VERTICES && SPEC) vv.wall = __longlong_as_double(0x7ff8000000000000ll);
 
   // first level: parent (lev_in - 1), local index tid
   int lev = p.lev_in - 1;
@@ -249,6 +269,14 @@ __global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) 
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int c = 0; c < 3; ++c) V[r][c] = vv.at(rows[r], cols[c]);
+    if constexpr (SPEC) {
+      bool bad = false;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) bad |= (V[r][c] == vv.nodata) | !(fabs(V[r][c]) <= 1e300);
+      if (bad) atomicOr(&p.scal->redo, 1);
+    }
     const bool xs = ib != ia, ys = jb != ja;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -268,12 +296,28 @@ __global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) 
       kids[k] = P3{s[0], s[1], s[2]};
     }
   }
+  if constexpr (SPEC && FROM_VERTICES) {
+    // field_norm over this tile's fine planes: block maximum, one atomic
+    double nm = smax(smax(fabs(kids[0].c0), fabs(kids[1].c0)), smax(fabs(kids[2].c0), fabs(kids[3].c0)));
+    for (int o = 16; o; o >>= 1) nm = smax(nm, __shfl_xor_sync(0xffffffffu, nm, o));
+    double* red = smem;  // free until the first sbuf / sdet write below
+    if ((tid & 31) == 0) red[tid >> 5] = nm;
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < (nthr >> 5); ++w) nm = smax(nm, red[w]);
+      if (nm > 0.0) atomicMax(&p.scal->norm_bits, dbits(nm));
+    }
+    __syncthreads();
+  }
   P3 par_s;
   double d[9];
   encode_b(kids, p.kind, skip0, par_s, d);
 #pragma unroll
   for (int n = 0; n < 9; ++n) sdet[9 * tid + n] = d[n];
-  p.flag[lev][par] = dhat(d, norm) >= p.eps ? 1 : 0;
+  if constexpr (SPEC)
+    p.dmx[lev][par] = max_abs9(d);
+  else
+    p.flag[lev][par] = dhat(d, norm) >= p.eps ? 1 : 0;
   if (p.T == 1) {
     double* o = p.sc_out + 3 * par;
     o[0] = par_s.c0;
@@ -296,7 +340,10 @@ __global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) 
 #pragma unroll
       for (int k = 0; k < 4; ++k) kids[k] = sbuf[4 * tid + k];
       encode_b(kids, p.kind, skip0, mine, d);
-      p.flag[lev][node0 + tid] = dhat(d, norm) >= p.eps ? 1 : 0;
+      if constexpr (SPEC)
+        p.dmx[lev][node0 + tid] = max_abs9(d);
+      else
+        p.flag[lev][node0 + tid] = dhat(d, norm) >= p.eps ? 1 : 0;
     }
     __syncthreads();  // sbuf reads and the previous sdet stores are done
     if (have) {
@@ -313,6 +360,22 @@ __global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) 
     o[1] = sbuf[0].cx;
     o[2] = sbuf[0].cy;
   }
+}
+
+// flag_significant (detail_tree.cpp:66-74) from the speculative encode's
+// max |d|: d_hat = max|d| / max(1, norm) >= eps, every level in one launch.
+struct DmxLevels {
+  const double* dmx[kMaxL];
+  uint8_t* flag[kMaxL];
+};
+__global__ void k_sig_from_dmx(DmxLevels t, int M, int N, const Scalars* __restrict__ s, double eps) {
+  const int l = blockIdx.y;
+  const uint64_t nodes = uint64_t(M) * N << (2 * l);
+  const double norm = bitsd(s->norm_bits);
+  const double den = smax(1.0, norm);
+  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < nodes;
+       n += uint64_t(gridDim.x) * blockDim.x)
+    t.flag[l][n] = t.dmx[l][n] / den >= eps ? 1 : 0;
 }
 
 // L = 0: the fine field is the coarse field.
@@ -681,22 +744,9 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
   }
   EventPair ev;
   cudaEvent_t e0 = ev.a, e1 = ev.b;
-  FM_CUDA(cudaEventRecord(e0, st));
-
   VertexView vv{vdev, dem->ncols, dem->nrows, n, m, dem->nodata, 0.0};
-  k_dem_stats<<<148 * 8, 256, 0, st>>>(vv, scal.p);
-  FM_LAUNCHED();
-  k_wall<<<1, 1, 0, st>>>(scal.p);
-  FM_LAUNCHED();
-  k_field_norm_fix<<<148 * 8, 256, 0, st>>>(vv, scal.p);
-  FM_LAUNCHED();
-  k_norm_final<<<1, 1, 0, st>>>(scal.p);
-  FM_LAUNCHED();
-  if (L == 0) {
-    k_copy_fine<<<blocks_for(g.nodes(0), 256), 256, 0, st>>>(vv, scal.p, g.coarse.p, g.M, g.nodes(0));
-    FM_LAUNCHED();
-  } else {
-    // encode L levels in passes of up to 5 levels (4^5 = 1024 inputs per CTA)
+  // the encode passes of up to 5 levels (4^5 = 1024 inputs per CTA)
+  auto encode_passes = [&](bool spec, std::vector<DBuf<double>>* dmx) {
     int lev_in = L;
     for (size_t k = 0; k < passes.size(); ++k) {
       const int T = passes[k];
@@ -708,6 +758,7 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
       for (int l = 0; l < L; ++l) {
         p.det[l] = g.det[l].p;
         p.flag[l] = g.flag[l].p;
+        p.dmx[l] = dmx ? (*dmx)[l].p : nullptr;
       }
       p.scal = scal.p;
       p.eps = eps;
@@ -718,21 +769,71 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
       const uint64_t tiles = g.nodes(lev_out);
       const int threads = 1 << (2 * (T - 1));
       const size_t smem = (sizeof(P3) + 9 * sizeof(double)) * threads;
-      if (k == 0)
-        k_encode_tiles<true><<<unsigned(tiles), threads, smem, st>>>(p);
+      if (spec)
+        (k == 0 ? k_encode_tiles<true, true> : k_encode_tiles<false, true>)<<<unsigned(tiles), threads, smem, st>>>(p);
       else
-        k_encode_tiles<false><<<unsigned(tiles), threads, smem, st>>>(p);
+        (k == 0 ? k_encode_tiles<true, false> : k_encode_tiles<false, false>)<<<unsigned(tiles), threads, smem, st>>>(p);
       FM_LAUNCHED();
       lev_in = lev_out;
     }
-  }
-  FM_CUDA(cudaEventRecord(e1, st));
+  };
+  // the exact two-pass path: DEM statistics (nodata wall, non-finite check,
+  // field_norm), then the encode with the flags
+  auto two_pass = [&]() {
+    scal.zero();
+    k_dem_stats<<<148 * 8, 256, 0, st>>>(vv, scal.p);
+    FM_LAUNCHED();
+    k_wall<<<1, 1, 0, st>>>(scal.p);
+    FM_LAUNCHED();
+    k_field_norm_fix<<<148 * 8, 256, 0, st>>>(vv, scal.p);
+    FM_LAUNCHED();
+    k_norm_final<<<1, 1, 0, st>>>(scal.p);
+    FM_LAUNCHED();
+    if (L == 0) {
+      k_copy_fine<<<blocks_for(g.nodes(0), 256), 256, 0, st>>>(vv, scal.p, g.coarse.p, g.M, g.nodes(0));
+      FM_LAUNCHED();
+    } else {
+      encode_passes(false, nullptr);
+    }
+  };
   Scalars hs{};
-  scal.download(&hs, 1);
-  FM_CUDA(cudaStreamSynchronize(st));
+  double t_ms = 0.0;
+  bool done = false;
+  if (L > 0) {
+    // one DEM read: the speculative encode (max |d| per node, the norm from
+    // the projected planes), then the flags from max |d| and the norm
+    std::vector<DBuf<double>> dmx(L);
+    for (int l = 0; l < L; ++l) dmx[l].alloc(g.nodes(l));
+    FM_CUDA(cudaEventRecord(e0, st));
+    encode_passes(true, &dmx);
+    DmxLevels t{};
+    for (int l = 0; l < L; ++l) {
+      t.dmx[l] = dmx[l].p;
+      t.flag[l] = g.flag[l].p;
+    }
+    const unsigned bx = unsigned(std::min<uint64_t>(blocks_for(g.nodes(L - 1), 256), 148 * 8));
+    k_sig_from_dmx<<<dim3(bx, L), 256, 0, st>>>(t, g.M, g.N, scal.p, eps);
+    FM_LAUNCHED();
+    FM_CUDA(cudaEventRecord(e1, st));
+    scal.download(&hs, 1);
+    FM_CUDA(cudaStreamSynchronize(st));
+    t_ms = elapsed_ms(e0, e1);
+    if (!hs.redo) {
+      std::memcpy(&hs.norm, &hs.norm_bits, 8);
+      done = true;
+    }
+  }
+  if (!done) {  // nodata, non-finite or huge vertices (or L = 0): the exact two-pass path
+    FM_CUDA(cudaEventRecord(e0, st));
+    two_pass();
+    FM_CUDA(cudaEventRecord(e1, st));
+    scal.download(&hs, 1);
+    FM_CUDA(cudaStreamSynchronize(st));
+    t_ms += elapsed_ms(e0, e1);
+  }
   if (hs.err) throw Error(FM_ERR_DOMAIN, "project_vertices: non-finite vertex value");
   g.field_norm = hs.norm;
-  if (ms) *ms = elapsed_ms(e0, e1);
+  if (ms) *ms = t_ms;
 }
 
 // Final flags (closure + optional 2:1 grading) and subtree leaf counts, one
