@@ -140,6 +140,11 @@ struct Sim {
   DBuf<double> ch, cqx, cqy, czc;
   DBuf<unsigned long long> cbad;
   bool acc_soa = false;
+  // FV1's compact state (nu_flow.cu): rows of 3 (h, qx, qy means) for U
+  // (owned + halo) and U*; fv1c: the state is there (between steps in cs3),
+  // the slopes in U are +0 exactly (checked when the state moves in)
+  DBuf<double> cu3, cs3;
+  bool fv1c = false;
   // device-side checkpoint (fm_sim_snapshot / fm_sim_restore)
   DBuf<double> snap_u, snap_us, snap_q, snap_qb, snap_aqx, snap_aqy;
   int64_t snap_n = -1;
@@ -162,6 +167,7 @@ struct Sim {
   // CUDA graphs of 32, 8 and 1 device-loop steps (sim_run)
   cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};
   int64_t gkern[3] = {0, 0, 0};
+  int g_layout = 0;  // the state layout the graphs were captured with
   std::unique_ptr<Shard> shard;  // set for a sharded (multi-rank) static sim
   // device order -> reference (level, j, i) order, cached per leaf set (order.cu)
   DBuf<int32_t> ref_perm;

@@ -49,6 +49,7 @@ __global__ void k_decide(NuView v, DevClock* clk, DevRed* red, const Hydro* hy) 
 // ---- step head: clock + friction (DG2/FV1) ------------------------------
 // src == dst for DG2; FV1 keeps its post-step state in U* (see k_stage) and
 // the head moves it back into U while applying friction.
+template <int W>
 __global__ void __launch_bounds__(256) k_head_friction(NuView v, DevClock* clk, DevRed* red,
                                                       const Hydro* hy, const double* src,
                                                       double* dst, int manual, double mdt) {
@@ -80,11 +81,19 @@ __global__ void __launch_bounds__(256) k_head_friction(NuView v, DevClock* clk, 
     return;
   }
   double s[9];
-  load9(src, k, s);
+  if constexpr (W == 9) {
+    load9(src, k, s);
+  } else {
+    load_row<W>(src, k, s);
+  }
   friction(s, v.nman[k], v.g, v.hdry, dt, v.libm);
-  double* o = dst + 9 * k;
+  if constexpr (W == 9) {
+    double* o = dst + 9 * k;
 #pragma unroll
-  for (int q = 0; q < 9; ++q) o[q] = s[q];
+    for (int q = 0; q < 9; ++q) o[q] = s[q];
+  } else {
+    store_row<W>(dst, k, s);
+  }
 }
 
 // ---- segment states ------------------------------------------------------
@@ -93,7 +102,7 @@ __global__ void __launch_bounds__(256) k_head_friction(NuView v, DevClock* clk, 
 // depths and the HLL flux, stored as {m, n, t, z*, h*L, h*R}.  Every segment
 // runs the same code path (one HLL), unlike a per-leaf-side formulation where
 // lanes of a warp face 0, 1 or 2 sub-faces and every face is solved twice.
-template <bool P2>
+template <bool P2, int W>
 __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClock* __restrict__ clk,
                                              const double* __restrict__ in, double* __restrict__ out,
                                              int manual, int* err, long long q0, long long q1) {
@@ -108,8 +117,8 @@ __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClo
   const bool act = true;
 #endif
   double sa[9], sb[9];
-  load9v(in, a, sa);
-  load9v(in, b, sb);
+  load_row<W>(in, a, sa);
+  load_row<W>(in, b, sb);
   const P3 za = load3v(v.z, a), zb = load3v(v.z, b);
   Pt A, B;
   bool xn;
@@ -287,7 +296,7 @@ __device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9],
 #define FM_STAGE_MINB 10
 #endif
 
-template <int STAGE, bool P2>
+template <int STAGE, bool P2, int W = 9>
 __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
     NuView v, const DevClock* __restrict__ clk, DevRed* red, const double* __restrict__ in,
     const double* uold, double* out, int last, int manual, double mdt, int* err) {
@@ -299,7 +308,7 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   // round trip in front of the first gathers
   const int l = v.lvl[kk], i = v.li[kk], j = v.lj[kk];
   double s[9];
-  load9v(in, kk, s);
+  load_row<W>(in, kk, s);
   const P3 zc = load3v(v.z, kk);
   const int code = v.sk[kk];
 #if FM_STAGE_SROW
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
     for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
   } else {
     double u0[9];
-    load9v(uold, kk, u0);
+    load_row<W>(uold, kk, u0);
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
       double a = s[q];
@@ -424,7 +433,7 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
       }
     }
   }
-  if (valid && act) store9v(out, kk, res);
+  if (valid && act) store_row<W>(out, kk, res);
   if (epi && act) reduce_leaf(v, red, *c, res, sz, leaf_key(l, i, j), valid);
 }
 
@@ -677,7 +686,7 @@ __global__ void k_acc_to_aos(long long n, const double* __restrict__ ch, const d
 // slopes in U are current: ACC never changes them).
 __global__ void k_reduce_init(NuView v, const DevClock* clk, DevRed* red, const double* __restrict__ u,
                               const double* __restrict__ ch, const double* __restrict__ cqx,
-                              const double* __restrict__ cqy) {
+                              const double* __restrict__ cqy, int cst) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool valid = k < v.n;
   double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -689,9 +698,9 @@ __global__ void k_reduce_init(NuView v, const DevClock* clk, DevRed* red, const 
     key = leaf_key(l, v.li[k], v.lj[k]);
     load9(u, k, s);
     if (ch) {
-      s[0] = ch[k];
-      s[3] = cqx[k];
-      s[6] = cqy[k];
+      s[0] = ch[cst * k];
+      s[3] = cqx[cst * k];
+      s[6] = cqy[cst * k];
     }
   }
   DevClock c = clk[1];
@@ -765,14 +774,13 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
   // Segment states over [q0, q1).  A sharded sim orders its segments with
   // the ones that touch only owned leaves first: those run while the halo
   // exchange is in flight on the shard's side stream, the rest after it.
+  // FV1 in the compact layout (s.fv1c): rows of 3 (h, qx, qy means) in
+  // s.cu3 (U) and s.cs3 (U*) instead of the 72 B rows of U and U*
+  const bool c3 = s.fv1c;
   auto seg_range = [&](const double* in, long long q0, long long q1) {
     if (q1 <= q0) return;
-    if (s.p2)
-      launch_k(k_seg<true>, nblk(q1 - q0, 256), 256, st, v, (const DevClock*)clk, in, s.segst.p, (int)manual,
-               err, q0, q1);
-    else
-      launch_k(k_seg<false>, nblk(q1 - q0, 256), 256, st, v, (const DevClock*)clk, in, s.segst.p,
-               (int)manual, err, q0, q1);
+    auto kern = s.p2 ? (c3 ? k_seg<true, 3> : k_seg<true, 9>) : (c3 ? k_seg<false, 3> : k_seg<false, 9>);
+    launch_k(kern, nblk(q1 - q0, 256), 256, st, v, (const DevClock*)clk, in, s.segst.p, (int)manual, err, q0, q1);
     FM_LAUNCHED();
   };
   auto seg = [&](int fam, const double* in) {
@@ -802,19 +810,25 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       if (!manual) launch_decide(s);
       // FV1 keeps its state in U* between steps; the head moves it to U with friction
       kt_begin(KF_HEAD);
-      launch_k(k_head_friction, nblk(n, 256), 256, st, v, clk, red, (const Hydro*)s.hydro.p,
+      if (c3)
+        launch_k(k_head_friction<3>, nblk(n, 256), 256, st, v, clk, red, (const Hydro*)s.hydro.p,
+                 (const double*)s.cs3.p, s.cu3.p, (int)manual, mdt);
+      else
+        launch_k(k_head_friction<9>, nblk(n, 256), 256, st, v, clk, red, (const Hydro*)s.hydro.p,
                  (const double*)(fv1 ? s.us.p : s.u.p), s.u.p, (int)manual, mdt);
       FM_LAUNCHED();
       kt_end();
       break;
     case OP_STAGE1: {
-      seg(KF_SEG1, s.u.p);
+      const double* in = c3 ? s.cu3.p : s.u.p;
+      double* out = c3 ? s.cs3.p : s.us.p;
+      seg(KF_SEG1, in);
       kt_begin(KF_STAGE1);
       const int last1 = fv1 ? 1 : 0;
-      if (s.p2)
-        launch_k(k_stage<1, true>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.u.p, (const double*)nullptr, s.us.p, last1, (int)manual, mdt, err);
-      else
-        launch_k(k_stage<1, false>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.u.p, (const double*)nullptr, s.us.p, last1, (int)manual, mdt, err);
+      auto kern = s.p2 ? (c3 ? k_stage<1, true, 3> : k_stage<1, true, 9>)
+                       : (c3 ? k_stage<1, false, 3> : k_stage<1, false, 9>);
+      launch_k(kern, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, in,
+               (const double*)nullptr, out, last1, (int)manual, mdt, err);
       FM_LAUNCHED();
       kt_end();
       break;
@@ -823,9 +837,9 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       seg(KF_SEG2, s.us.p);
       kt_begin(KF_STAGE2);
       if (s.p2)
-        launch_k(k_stage<2, true>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
+        launch_k(k_stage<2, true, 9>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
       else
-        launch_k(k_stage<2, false>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
+        launch_k(k_stage<2, false, 9>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
       FM_LAUNCHED();
       kt_end();
       break;
@@ -853,17 +867,22 @@ void launch_decide(Sim& s) {
 
 void launch_head_friction(Sim& s, const double* src, double* dst, bool manual, double mdt) {
   kt_begin(s.uniform ? KF_UNI_HEAD : KF_HEAD);
-  k_head_friction<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.hydro.p, src,
-                                                         dst, manual, mdt);
+  k_head_friction<9><<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.hydro.p, src,
+                                                            dst, manual, mdt);
   FM_LAUNCHED();
   kt_end();
 }
 
 
 void nu_launch_reduce_init(Sim& s) {
-  const bool c = s.acc_soa;
-  k_reduce_init<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.u.p, c ? s.ch.p : nullptr,
-                                                       c ? s.cqx.p : nullptr, c ? s.cqy.p : nullptr);
+  // the compact layouts hold the means (ACC: three arrays; FV1: rows of 3 in U*)
+  const double* ch = s.acc_soa ? s.ch.p : s.fv1c ? s.cs3.p : nullptr;
+  const double* cqx = s.acc_soa ? s.cqx.p : s.fv1c ? s.cs3.p + 1 : nullptr;
+  const double* cqy = s.acc_soa ? s.cqy.p : s.fv1c ? s.cs3.p + 2 : nullptr;
+  // FV1 on 72 B rows between steps keeps its state in U* (fv1_in_star)
+  const double* st = s.fv1_in_star ? s.us.p : s.u.p;
+  k_reduce_init<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.clk.p, s.red.p, st, ch, cqx, cqy,
+                                                       s.fv1c ? 3 : 1);
   FM_LAUNCHED();
 }
 
@@ -886,6 +905,48 @@ void nu_launch_acc_to_soa(Sim& s, long long ntot) {
 
 void nu_launch_acc_to_aos(Sim& s) {
   k_acc_to_aos<<<nblk(s.n, 256), 256, 0, stream()>>>(s.n, s.ch.p, s.cqx.p, s.cqy.p, s.u.p);
+  FM_LAUNCHED();
+}
+
+namespace {
+// FV1 into the compact layout: the means of U's rows into U* compact (the
+// next step's head moves them to U compact with friction); `nz` counts owned
+// leaves with a slope that is not +0 exactly (then the compact path is off)
+__global__ void k_fv1_to_c(long long n, const double* __restrict__ u, double* __restrict__ cs3,
+                           unsigned long long* __restrict__ nz) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double* r = u + 9 * k;
+  store3v(cs3, k, r[0], r[3], r[6]);
+  const unsigned long long o = dbits(r[1]) | dbits(r[2]) | dbits(r[4]) | dbits(r[5]) | dbits(r[7]) | dbits(r[8]);
+  if (o) atomicAdd(nz, 1ull);
+}
+__global__ void k_c3_to_u(long long n, const double* __restrict__ cs3, double* __restrict__ u) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const P3 p = load3v(cs3, k);
+  u[9 * k] = p.c0;
+  u[9 * k + 3] = p.cx;
+  u[9 * k + 6] = p.cy;
+}
+}  // namespace
+
+// Returns whether the compact FV1 layout is in use (every slope +0).
+bool nu_fv1_to_compact(Sim& s, long long ntot) {
+  s.cu3.alloc(size_t(3 * ntot));
+  s.cs3.alloc(size_t(3 * s.n));
+  DBuf<unsigned long long> nz(1);
+  nz.zero();
+  k_fv1_to_c<<<nblk(s.n, 256), 256, 0, stream()>>>(s.n, s.u.p, s.cs3.p, nz.p);
+  FM_LAUNCHED();
+  unsigned long long h = 0;
+  nz.download(&h, 1);
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  return h == 0;
+}
+
+void nu_c3_to_u(Sim& s) {
+  k_c3_to_u<<<nblk(s.n, 256), 256, 0, stream()>>>(s.n, s.cs3.p, s.u.p);
   FM_LAUNCHED();
 }
 

@@ -742,6 +742,10 @@ double* exch_array(Sim& s, int op, int* w) {
     *w = 1;
     return s.ch.p;
   }
+  if (op == OP_EXCH_U && s.fv1c) {  // FV1 compact: the head's output rows of 3
+    *w = 3;
+    return s.cu3.p;
+  }
   *w = 9;
   return op == OP_EXCH_U ? s.u.p : s.us.p;
 }

@@ -18,6 +18,8 @@ void nu_launch_reduce_init(Sim& s);
 void nu_launch_close(Sim& s);
 void nu_launch_inflow_add(Sim& s, const double* per_cell_dev);
 void nu_launch_acc_to_soa(Sim& s, long long ntot);
+bool nu_fv1_to_compact(Sim& s, long long ntot);
+void nu_c3_to_u(Sim& s);
 void nu_launch_acc_to_aos(Sim& s);
 // uniform.cu
 void un_launch_step(Sim& s, bool manual, double mdt, int* err);
@@ -373,11 +375,34 @@ void acc_to_u(Sim& s) {
 }
 // Every U consumer first brings the state back into U (FV1: from U*, ACC:
 // from the compact arrays); every stepping entry point moves it out again.
+// FV1 on a non-uniform grid runs on compact rows of 3 between the API calls
+// that touch U, as long as every slope is +0 (FV1 never makes one non-zero;
+// only an upload could): otherwise it stays on the 72 B rows.
+#ifndef FM_FV1_COMPACT
+#define FM_FV1_COMPACT 1
+#endif
+bool fv1_compact_ok(const Sim& s) { return FM_FV1_COMPACT && s.scheme == FM_FV1 && !s.uniform && !s.adaptive; }
+void fv1c_to_u(Sim& s) {
+  if (s.fv1c) {
+    nu_c3_to_u(s);
+    s.fv1c = false;
+    s.fv1_in_star = false;
+  }
+}
 void state_to_u(Sim& s) {
+  fv1c_to_u(s);
   if (fv1_staged(s)) fv1_to_u(s);
   acc_to_u(s);
 }
 void state_to_step(Sim& s) {
+  if (fv1_compact_ok(s) && !s.fv1c) {
+    if (fv1_staged(s)) fv1_to_u(s);
+    if (nu_fv1_to_compact(s, s.n + (s.shard ? s.shard->n_halo : 0))) {
+      s.fv1c = true;
+      return;
+    }
+  }
+  if (s.fv1c) return;
   if (fv1_staged(s)) fv1_to_star(s);
   acc_to_soa(s);
 }
@@ -476,7 +501,7 @@ void sim_step(Sim& s, double dt) {
   err.download(&h, 1);
   FM_CUDA(cudaStreamSynchronize(stream()));
   if (h) throw Error(FM_ERR_DOMAIN, "hll_flux: negative depth");
-  if (fv1_staged(s)) s.fv1_in_star = true;
+  if (fv1_staged(s) && !s.fv1c) s.fv1_in_star = true;
   if (s.adaptive) s.since_adapt += 1;
 }
 
@@ -642,6 +667,15 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
     // graphs of 32, 8 and 1 steps, captured on first use; the step count is
     // covered greedily so no graph replays surplus (no-op) steps
     static constexpr int kSizes[3] = {32, 8, 1};
+    // graphs bake the state layout in (FV1: compact rows or the 72 B rows)
+    const int layout = s.fv1c ? 1 : 0;
+    if (layout != s.g_layout) {
+      for (auto& gx : s.gexec) {
+        if (gx) cudaGraphExecDestroy(gx);
+        gx = nullptr;
+      }
+      s.g_layout = layout;
+    }
     auto graph_of = [&](int q) {
       if (!s.gexec[q]) {
         const int64_t before = launches();
@@ -834,7 +868,8 @@ void sim_profile(Sim& s, int64_t steps, double* ms, int64_t* counts, int cap, in
 namespace fmh {
 
 void sim_snapshot(Sim& s) {
-  acc_to_u(s);  // the snapshot holds U (ACC's compact state folded back)
+  acc_to_u(s);  // the snapshot holds U (the compact states folded back)
+  fv1c_to_u(s);
   auto copy = [](DBuf<double>& dst, const DBuf<double>& src) {
     dst.alloc(src.n);
     if (src.n)
@@ -867,6 +902,7 @@ void sim_restore(Sim& s) {
   copy(s.aqy, s.snap_aqy);
   s.fv1_in_star = s.snap_fv1;
   s.acc_soa = false;  // U is the state again
+  s.fv1c = false;
   FM_CUDA(cudaStreamSynchronize(stream()));
 }
 

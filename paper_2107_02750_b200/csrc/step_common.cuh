@@ -104,6 +104,33 @@ __device__ __forceinline__ P3 load3v(const double* __restrict__ a, long long k) 
   return odd ? P3{x, t.x, t.y} : P3{t.x, t.y, x};
 }
 
+__device__ __forceinline__ void store3v(double* __restrict__ a, long long k, double x0, double x1, double x2) {
+  const bool odd = k & 1;
+  double* p = a + 3 * k;
+  *reinterpret_cast<double2*>(p + (odd ? 1 : 0)) = odd ? make_double2(x1, x2) : make_double2(x0, x1);
+  p[odd ? 0 : 2] = odd ? x0 : x2;
+}
+// A flow row of width W: the 72 B rows of U (W = 9), or FV1's compact rows
+// (W = 3: h, qx, qy means; the slopes are +0 exactly and read as +0)
+template <int W>
+__device__ __forceinline__ void load_row(const double* __restrict__ a, long long k, double s[9]) {
+  if constexpr (W == 9) {
+    load9v(a, k, s);
+  } else {
+    const P3 p = load3v(a, k);
+    s[0] = p.c0, s[1] = 0.0, s[2] = 0.0;
+    s[3] = p.cx, s[4] = 0.0, s[5] = 0.0;
+    s[6] = p.cy, s[7] = 0.0, s[8] = 0.0;
+  }
+}
+template <int W>
+__device__ __forceinline__ void store_row(double* __restrict__ a, long long k, const double s[9]) {
+  if constexpr (W == 9)
+    store9v(a, k, s);
+  else
+    store3v(a, k, s[0], s[3], s[6]);
+}
+
 __device__ __forceinline__ unsigned long long leaf_key(int l, int i, int j) {
   return (static_cast<unsigned long long>(l) << 58) | (static_cast<unsigned long long>(j) << 29) |
          static_cast<unsigned long long>(i);

@@ -612,7 +612,9 @@ void un_launch_inflow_add(Sim& s, const double* per_cell_dev) {
 }
 
 void un_launch_reduce_init(Sim& s) {
-  k_uni_reduce_init<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.nx, s.gy0, s.clk.p, s.red.p, s.u.p);
+  // FV1 between steps keeps its state in U* (fv1_in_star): reduce over that
+  const double* st = s.fv1_in_star ? s.us.p : s.u.p;
+  k_uni_reduce_init<<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.nx, s.gy0, s.clk.p, s.red.p, st);
   FM_LAUNCHED();
 }
 

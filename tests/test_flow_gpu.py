@@ -280,3 +280,24 @@ def test_compute_dt_ignores_nan_candidates(gpu, orc):
     b.upload(u)
     da, db = a.compute_dt(), b.compute_dt()
     assert np.isfinite(db) and da == db
+
+
+@pytest.mark.parametrize("solver,uniform", [("fv1", False), ("fv1", True), ("acc", False), ("acc", True),
+                                            ("dg2", False), ("dg2", True)])
+def test_second_run_resumes_from_the_current_state(gpu, orc, solver, uniform):
+    """A second fm_sim_run with a fresh clock takes its first dt from the
+    state the first run left (compute_dt, solver_nonuniform.cpp:427-449),
+    wherever the device keeps it between steps (FV1: U* or the compact rows;
+    ACC: the compact arrays).  Portable libm: bit-exact vs the oracle."""
+    import dataclasses
+    sc = dataclasses.replace(S.config4(8, uniform=uniform), solver=solver,
+                             courant={"fv1": 0.5, "acc": 0.7, "dg2": 0.33}[solver])
+    out = []
+    for be in (gpu, orc):
+        g = None if uniform else be.grid(sc.dem, sc.L, sc.eps)
+        s = be.sim(sc, g, libm=PORTABLE)
+        s.run(5, gauge_interval=10.0)
+        ck, r = s.run(6, gauge_interval=10.0)
+        out.append((ck.now, r.dt_min, r.dt_max, s.download()[3]))
+    assert out[0][:3] == out[1][:3]
+    assert np.array_equal(out[0][3], out[1][3])
