@@ -435,10 +435,10 @@ LvTab lv_tab(Sim& s, Grid& g, AdaptState& a) {
 void copy_leaves_from_grid(Sim& s, const Grid& g) {
   cudaStream_t st = stream();
   s.n = g.nleaves;
-  s.lvl.alloc(s.n);
-  s.li.alloc(s.n);
-  s.lj.alloc(s.n);
-  s.z.alloc(3 * s.n);
+  s.lvl.ensure(s.n);
+  s.li.ensure(s.n);
+  s.lj.ensure(s.n);
+  s.z.ensure(3 * s.n);
   FM_CUDA(cudaMemcpyAsync(s.lvl.p, g.lf_l.p, s.n, cudaMemcpyDeviceToDevice, st));
   FM_CUDA(cudaMemcpyAsync(s.li.p, g.lf_i.p, 4 * s.n, cudaMemcpyDeviceToDevice, st));
   FM_CUDA(cudaMemcpyAsync(s.lj.p, g.lf_j.p, 4 * s.n, cudaMemcpyDeviceToDevice, st));
@@ -450,7 +450,7 @@ void refresh_topology(Sim& s) {
   cudaStream_t st = stream();
   Grid& g = *s.grid;
   AdaptState& a = *s.ad;
-  s.nman.alloc(s.n);
+  s.nman.ensure(s.n);
   resolve_manning(s);
   resolve_inflows(s, g);
   build_topology(s, g);
@@ -463,7 +463,7 @@ void refresh_topology(Sim& s) {
     run_levels<ZpyrBody<1>>(tab, 0, L - 1, true);
   ZpTab t{};
   for (int l = 0; l < L; ++l) t.zp[l] = a.zp[l].p;
-  s.zpair.alloc(4 * s.n);
+  s.zpair.ensure(4 * s.n);
   k_zpair<<<nblk(s.n, 256), 256, 0, st>>>(s.n, s.M, s.lvl.p, s.li.p, s.lj.p, s.sk.p, t, s.zpair.p);
   FM_LAUNCHED();
 }
@@ -598,10 +598,12 @@ void adaptive_adapt(Sim& s, double t) {
   grade_count_levels(g, true);
   build_leaves(g);
   // transfer the flow onto the new leaves
+  // the new state goes into the U* scratch, which then becomes U (no
+  // allocation per adapt: the buffers only grow)
   const int64_t n_new = g.nleaves;
-  DBuf<double> u_new(9 * n_new);
+  s.us.ensure(9 * n_new);
   tab = lv_tab(s, g, a);
-  tab.unew = u_new.p;
+  tab.unew = s.us.p;
   if (n_new) {
     if (a.kind == 0)
       k_transfer_leaves<0><<<nblk(n_new, 256), 256, 0, st>>>(tab, n_new, g.lf_l.p, g.lf_i.p, g.lf_j.p);
@@ -609,8 +611,8 @@ void adaptive_adapt(Sim& s, double t) {
       k_transfer_leaves<1><<<nblk(n_new, 256), 256, 0, st>>>(tab, n_new, g.lf_l.p, g.lf_i.p, g.lf_j.p);
     FM_LAUNCHED();
   }
-  s.u = std::move(u_new);
-  s.us.alloc(9 * n_new);
+  std::swap(s.u, s.us);
+  s.us.ensure(9 * n_new);
   copy_leaves_from_grid(s, g);
   if (s.scheme != FM_DG2) {
     k_zero_slopes<<<nblk(s.n, 256), 256, 0, st>>>(s.n, s.z.p, s.u.p);
@@ -622,8 +624,7 @@ void adaptive_adapt(Sim& s, double t) {
     if (g) cudaGraphExecDestroy(g);
     g = nullptr;
   }
-  FM_CUDA(cudaStreamSynchronize(st));
-  s.element_log.emplace_back(t, s.n);
+  s.element_log.emplace_back(t, s.n);  // s.n is known on the host: no sync here
 }
 
 }  // namespace fmh

@@ -34,29 +34,45 @@ template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  size_t cap = 0;  // elements allocated (>= n)
   DBuf() = default;
   explicit DBuf(size_t count) { alloc(count); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) {
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), cap(o.cap) {
     o.p = nullptr;
     o.n = 0;
+    o.cap = 0;
   }
   DBuf& operator=(DBuf&& o) noexcept {
     if (this != &o) {
       release();
       p = o.p;
       n = o.n;
+      cap = o.cap;
       o.p = nullptr;
       o.n = 0;
+      o.cap = 0;
     }
     return *this;
   }
   ~DBuf() { release(); }
+  // Logical size `count`, keeping the allocation when it holds count
+  // elements (re-gridded sims: no free / malloc per adapt); grows by 1/4.
+  void ensure(size_t count) {
+    if (p && count <= cap) {
+      n = count;
+      return;
+    }
+    const size_t c = count + count / 4;
+    alloc(c);
+    n = count;
+  }
   void alloc(size_t count) {
     if (count == n && p) return;
     release();
     n = count;
+    cap = count;
 #ifdef FM_PLAIN_MALLOC
     if (count) {
       FM_CUDA(cudaStreamSynchronize(stream()));
@@ -77,6 +93,7 @@ struct DBuf {
 #endif
     p = nullptr;
     n = 0;
+    cap = 0;
   }
   void zero() {
     if (n) FM_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), stream()));
@@ -117,6 +134,7 @@ struct Grid {
   DBuf<int8_t> lf_l;
   DBuf<int32_t> lf_i, lf_j;
   DBuf<double> lf_z;  // 3 per leaf
+  std::vector<DBuf<double>> zs;  // build_leaves' decoded-plane scratch per level
   double mra_ms = 0, mra_bytes = 0;
   uint64_t nodes(int l) const { return uint64_t(M) * N << (2 * l); }
 };

@@ -631,10 +631,10 @@ int64_t build_leaves(Grid& g) {
     g.nleaves = tot;
   }
   if (g.nleaves > INT32_MAX) throw Error(FM_ERR_STRUCTURE, "leaf count exceeds int32");
-  g.lf_l.alloc(g.nleaves);
-  g.lf_i.alloc(g.nleaves);
-  g.lf_j.alloc(g.nleaves);
-  g.lf_z.alloc(3 * g.nleaves);
+  g.lf_l.ensure(g.nleaves);
+  g.lf_i.ensure(g.nleaves);
+  g.lf_j.ensure(g.nleaves);
+  g.lf_z.ensure(3 * g.nleaves);
   LeafOut out{g.lf_l.p, g.lf_i.p, g.lf_j.p, g.lf_z.p};
   if (L == 0) {
     // copy coarse planes out as leaves (node order == Morton order at level 0)
@@ -652,7 +652,8 @@ int64_t build_leaves(Grid& g) {
     return g.nleaves;
   }
   // decoded-plane scratch per level (levels 1..L-1)
-  std::vector<DBuf<double>> zs(L);
+  std::vector<DBuf<double>>& zs = g.zs;  // kept across builds (adaptive re-grids)
+  zs.resize(L);
   for (int l = 1; l < L; ++l) zs[l].alloc(3 * g.nodes(l));
   // the small coarse levels in one single-CTA launch, then a launch per level
   int ls = -1;

@@ -407,6 +407,12 @@ void state_to_step(Sim& s) {
   acc_to_soa(s);
 }
 
+__global__ void k_red_reset(DevRed* red, int p) {
+  red[p].dtmin = 0x7ff0000000000000ull;  // +inf
+  red[p].hmaxc = ~0ull;
+  red[p].badkey = ~0ull;
+}
+
 void init_red(Sim& s) {
   DevRed r[2];
   for (auto& x : r) {
@@ -638,15 +644,9 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
         state_to_step(s);
         s.since_adapt = 0;
         // the adapt changed the leaf set: refresh the step's reductions
-        DevRed r[2];
-        s.red.download(r, 2);
-        FM_CUDA(cudaStreamSynchronize(st));
-        const int p = int(c.steps & 1);
-        double inf = std::numeric_limits<double>::infinity();
-        std::memcpy(&r[p].dtmin, &inf, 8);
-        r[p].hmaxc = ~0ull;
-        r[p].badkey = ~0ull;
-        s.red.upload(r, 2);
+        // (reset the slot on the device, no host round trip)
+        k_red_reset<<<1, 1, 0, st>>>(s.red.p, int(c.steps & 1));
+        FM_LAUNCHED();
         launch_reduce_init(s);
       }
     }

@@ -271,26 +271,35 @@ inline unsigned nblk(long long n, int t) { return unsigned((n + t - 1) / t); }
 
 }  // namespace
 
-int64_t scan_exclusive(const int32_t* in, int32_t* out, int64_t n) {
+// Exclusive scan; the total lands in *total_dev (device), no host sync.
+void scan_exclusive_async(const int32_t* in, int32_t* out, int64_t n, long long* total_dev) {
   cudaStream_t st = stream();
   const int T = 1024;
   const long long nb = (n + T - 1) / T;
-  DBuf<long long> sums(std::max<long long>(nb, 1)), total(1);
-  if (n == 0) return 0;
+  if (n == 0) {
+    FM_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(long long), st));
+    return;
+  }
+  DBuf<long long> sums(std::max<long long>(nb, 1));
   k_block_sums<<<unsigned(nb), T, 0, st>>>(in, n, sums.p);
   FM_LAUNCHED();
-  k_scan_sums<<<1, 1024, 0, st>>>(sums.p, nb, total.p);
+  k_scan_sums<<<1, 1024, 0, st>>>(sums.p, nb, total_dev);
   FM_LAUNCHED();
   k_scan_apply<<<unsigned(nb), T, 0, st>>>(in, out, n, sums.p);
   FM_LAUNCHED();
+}
+
+int64_t scan_exclusive(const int32_t* in, int32_t* out, int64_t n) {
+  DBuf<long long> total(1);
+  scan_exclusive_async(in, out, n, total.p);
   long long tot = 0;
   total.download(&tot, 1);
-  FM_CUDA(cudaStreamSynchronize(st));
+  FM_CUDA(cudaStreamSynchronize(stream()));
   return tot;
 }
 
 void build_seg_geo(Sim& s) {
-  s.seg_geo.alloc(std::max<int64_t>(s.nseg, 1));
+  s.seg_geo.ensure(std::max<int64_t>(s.nseg, 1));
   if (s.nseg) {
     k_seg_geo<<<nblk(s.nseg, 256), 256, 0, stream()>>>(s.nseg, s.L, s.seg_l.p, s.seg_r.p, s.lvl.p, s.li.p,
                                                       s.lj.p, s.seg_geo.p);
@@ -301,35 +310,38 @@ void build_seg_geo(Sim& s) {
 void build_topology(Sim& s, const Grid& g) {
   cudaStream_t st = stream();
   const long long n = s.n;
-  s.nb.alloc(8 * n);
-  s.sk.alloc(n);
+  s.nb.ensure(8 * n);
+  s.sk.ensure(n);
   DBuf<int32_t> owned(n), base(n);
-  DBuf<int> err(1);
-  err.zero();
+  // [0]: segment total (scan), [1]: the ungraded-grid error flag; one sync for both
+  DBuf<long long> tot2(2);
+  tot2.zero();
   const TopoIn t = topo_in(g);
-  k_topo<<<nblk(n, 256), 256, 0, st>>>(t, n, s.lvl.p, s.li.p, s.lj.p, s.nb.p, s.sk.p, owned.p, err.p);
+  k_topo<<<nblk(n, 256), 256, 0, st>>>(t, n, s.lvl.p, s.li.p, s.lj.p, s.nb.p, s.sk.p, owned.p,
+                                        reinterpret_cast<int*>(tot2.p + 1));
   FM_LAUNCHED();
-  s.nseg = scan_exclusive(owned.p, base.p, n);
-  int herr = 0;
-  err.download(&herr, 1);
+  scan_exclusive_async(owned.p, base.p, n, tot2.p);
+  long long h2[2] = {0, 0};
+  tot2.download(h2, 2);
   FM_CUDA(cudaStreamSynchronize(st));
-  if (herr) throw Error(FM_ERR_STRUCTURE, "non-uniform solvers require a graded (2:1) grid");
+  s.nseg = h2[0];
+  if (h2[1]) throw Error(FM_ERR_STRUCTURE, "non-uniform solvers require a graded (2:1) grid");
   {
-    s.sid.alloc(8 * n);
-    s.seg_l.alloc(std::max<int64_t>(s.nseg, 1));
-    s.seg_r.alloc(std::max<int64_t>(s.nseg, 1));
+    s.sid.ensure(8 * n);
+    s.seg_l.ensure(std::max<int64_t>(s.nseg, 1));
+    s.seg_r.ensure(std::max<int64_t>(s.nseg, 1));
     k_segments<<<nblk(n, 256), 256, 0, st>>>(n, s.li.p, s.lj.p, s.nb.p, s.sk.p, base.p, s.sid.p,
                                               s.seg_l.p, s.seg_r.p);
     FM_LAUNCHED();
     build_seg_geo(s);
-    if (s.scheme != FM_ACC) s.segst.alloc(6 * size_t(std::max<int64_t>(s.nseg, 1)));
+    if (s.scheme != FM_ACC) s.segst.ensure(6 * size_t(std::max<int64_t>(s.nseg, 1)));
   }
 }
 
 void resolve_inflows(Sim& s, const Grid& g) {
   (void)g;
   cudaStream_t st = stream();
-  s.infc.alloc(std::max<int64_t>(1, int64_t(s.ninflow) * s.n));
+  s.infc.ensure(std::max<int64_t>(1, int64_t(s.ninflow) * s.n));
   if (s.ninflow == 0) s.infc.zero();
   for (int f = 0; f < s.ninflow; ++f) {
     const int* r = &s.rect[4 * f];
