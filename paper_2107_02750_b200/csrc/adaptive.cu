@@ -6,11 +6,11 @@
 // passes run each large level as one launch and all levels of <= 256 nodes in
 // one single-CTA launch (run_levels); level-independent passes run every level
 // in one launch (run_levels_flat):
-//   encode_up    (:16-57)   k_mark_leaves + EncodeUpBody per level
 //   norms        (:139-144) k_norms (exact max reductions)
-//   flag         (:59-73)   FlagBody (static topography significance
+//   encode_up    (:16-57)   k_mark_leaves + EncodeFlagBody per level, which
+//   flag         (:59-73)   also flags the node (static topography significance
 //                           precomputed once: max(a,b) >= eps <=> a >= eps || b >= eps)
-//   closure      (detail_tree.cpp:56-64) ClosureBody per level
+//   closure      (detail_tree.cpp:56-64) and closes it over its children
 //   buffer_ring  (:75-94)   RingBody, then closure again
 //   grade_flags  (detail_tree.cpp:97-113) + leaf counts: grade_count_levels
 //   assemble_grid(detail_tree.cpp:132-164): build_leaves (topography decode)
@@ -25,6 +25,8 @@
 //                           sides (region_topo, solver_nonuniform.cpp:80-89)
 //                           from a z encode-up pyramid (ZpyrBody, k_zpair).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -48,8 +50,18 @@ struct AdaptState {
   std::vector<DBuf<double>> sc;      // [L+1] flow scaling, 9 per node
   std::vector<DBuf<double>> fdet;    // [L] flow details, 27 per node
   std::vector<DBuf<double>> zp;      // [L] z encode-up pyramid, 3 per node
-  std::vector<DBuf<uint8_t>> tmp;    // [L] ring scratch
+  std::vector<DBuf<uint8_t>> tmp;    // [L] flags before the ring dilation
   DBuf<unsigned long long> norms;    // 3
+  // the device-sized prefix of every adapt (encode up to the leaf list) as
+  // one CUDA graph: dn[0] = current leaf count (set before each replay),
+  // dn[1] = the new leaf count (read back after it)
+  DBuf<long long> dn;
+  cudaGraphExec_t prefix = nullptr;
+  std::vector<const void*> prefix_key;  // the buffers the graph was captured on
+  int64_t prefix_kernels = 0;
+  ~AdaptState() {
+    if (prefix) cudaGraphExecDestroy(prefix);
+  }
 };
 
 void adaptive_destroy(AdaptState* a) { delete a; }
@@ -63,26 +75,31 @@ struct PtrTab {
   double* sc[16];
 };
 
-__global__ void k_mark_leaves(long long n, int M, const int8_t* __restrict__ lvl,
-                              const int32_t* __restrict__ li, const int32_t* __restrict__ lj,
-                              const double* __restrict__ u, PtrTab t) {
-  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int l = lvl[k];
-  const uint64_t node = node_index(l, li[k], lj[k], M);
-  t.known[l][node] = 1;
-  double* o = t.sc[l] + 9 * node;
+// the leaf count from the device (graph replays): grid-stride
+__global__ void k_mark_leaves_dn(const long long* __restrict__ dn, int M, const int8_t* __restrict__ lvl,
+                                 const int32_t* __restrict__ li, const int32_t* __restrict__ lj,
+                                 const double* __restrict__ u, PtrTab t) {
+  const long long n = dn[0];
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int l = lvl[k];
+    const uint64_t node = node_index(l, li[k], lj[k], M);
+    t.known[l][node] = 1;
+    double* o = t.sc[l] + 9 * node;
 #pragma unroll
-  for (int q = 0; q < 9; ++q) o[q] = u[9 * k + q];
+    for (int q = 0; q < 9; ++q) o[q] = u[9 * k + q];
+  }
 }
 
-__global__ void k_norms(long long n, const double* __restrict__ u, unsigned long long* out) {
-  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__global__ void k_norms(const long long* __restrict__ dn, const double* __restrict__ u,
+                        unsigned long long* out) {
+  const long long n = dn[0];
   double a = 0.0, b = 0.0, c = 0.0;
-  if (k < n) {
-    a = fabs(u[9 * k]);
-    b = fabs(u[9 * k + 3]);
-    c = fabs(u[9 * k + 6]);
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    a = smax(a, fabs(u[9 * k]));
+    b = smax(b, fabs(u[9 * k + 3]));
+    c = smax(c, fabs(u[9 * k + 6]));
   }
   for (int o = 16; o; o >>= 1) {
     a = smax(a, __shfl_xor_sync(0xffffffffu, a, o));
@@ -231,9 +248,17 @@ struct EncodeUpBody {
   }
 };
 
-// solver_adaptive.cpp:59-73 without the closure
-struct FlagBody {
+// encode_up + flag + ancestor_closure in ONE fine-to-coarse sweep
+// (solver_adaptive.cpp:16-73, detail_tree.cpp:56-64): at level l a node whose
+// four children are known is encoded (EncodeUpBody); its flag is the static
+// topography significance, or a flow detail of the node just encoded with
+// d_hat >= eps (the norms are taken over the current leaves first), or --
+// the closure -- any flagged child at l + 1, whose flags are final because
+// the sweep visited level l + 1 before.  Equal to the three passes in turn.
+template <int KIND>
+struct EncodeFlagBody {
   __device__ static void node(int l, uint64_t n, const LvTab& t) {
+    EncodeUpBody<KIND>::node(l, n, t);
     uint8_t f = t.zsig[l][n];
     if (!f && t.known[l][n] == 2) {
       const double* det = t.fdet[l];
@@ -245,21 +270,16 @@ struct FlagBody {
         if (dhat(d, bitsd(t.norms[q])) >= t.eps) f = 1;
       }
     }
-    t.flag[l][n] = f;
+    if (!f && l + 1 < t.L && *reinterpret_cast<const uint32_t*>(t.tmp[l + 1] + 4 * n)) f = 1;
+    t.tmp[l][n] = f;
   }
 };
 
-// ancestor_closure: parent level l |= any child at l + 1 (detail_tree.cpp:56-64)
-struct ClosureBody {
-  __device__ static void node(int l, uint64_t n, const LvTab& t) {
-    if (*reinterpret_cast<const uint32_t*>(t.flag[l + 1] + 4 * n)) t.flag[l][n] = 1;
-  }
-};
-
-// buffer_ring, one level: dilate to the same-level 8-neighbourhood (:75-94)
+// buffer_ring, one level: dilate to the same-level 8-neighbourhood (:75-94),
+// from the closed flags (tmp) into the grid's flags
 struct RingBody {
   __device__ static void node(int l, uint64_t n, const LvTab& t) {
-    const uint8_t* flag = t.flag[l];
+    const uint8_t* flag = t.tmp[l];
     uint8_t f = flag[n];
     if (!f) {
       int i, j;
@@ -275,7 +295,7 @@ struct RingBody {
           }
         }
     }
-    t.tmp[l][n] = f;
+    t.flag[l][n] = f;
   }
 };
 
@@ -514,6 +534,7 @@ void adaptive_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem) {
     }
   }
   a.norms.alloc(3);
+  a.dn.alloc(2);
   // the initial uniform level-L grid (make_uniform_quadgrid) with nug0.topo =
   // the projected fine planes (not a decode)
   for (int l = 0; l < L; ++l) {
@@ -560,43 +581,127 @@ struct ZeroKnownBody {
   __device__ static void node(int l, uint64_t n, const LvTab& t) { t.known[l][n] = 0; }
 };
 
-void adaptive_adapt(Sim& s, double t) {
-  s.ref_perm_ok = false;  // the leaf set changes
-  ++s.leaf_gen;
+// FM_ADAPT_PROFILE=1: per-phase device time of every adapt on stderr (CUDA
+// events between the phases; diagnostics only)
+namespace {
+struct PhaseClock {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char*> name;
+  explicit PhaseClock(cudaStream_t st) : st_(st) {
+    const char* e = std::getenv("FM_ADAPT_PROFILE");
+    on = e && e[0] == '1';
+    mark("start");
+  }
+  void mark(const char* n) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st_);
+    ev.push_back(e);
+    name.push_back(n);
+  }
+  ~PhaseClock() {
+    if (!on) return;
+    cudaEventSynchronize(ev.back());
+    for (size_t k = 1; k < ev.size(); ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[k - 1], ev[k]);
+      std::fprintf(stderr, "%s=%.1f ", name[k], 1000.0 * ms);
+    }
+    float tot = 0.f;
+    cudaEventElapsedTime(&tot, ev.front(), ev.back());
+    std::fprintf(stderr, "| adapt %.1f us\n", 1000.0 * tot);
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+
+ private:
+  cudaStream_t st_;
+};
+}  // namespace
+
+namespace {
+__global__ void k_set_dn(long long* dn, long long n) { dn[0] = n; }
+
+// The device-sized part of an adapt, in the reference's order: encode_up +
+// flag + closure (one sweep), buffer_ring, grade_flags + leaf counts, and
+// leaves_from_flags + assemble_grid (build_leaves_device).  The current leaf
+// count is read from dn[0], the new one written to dn[1]; every buffer is of
+// fixed size (the dense pyramids; leaf arrays of capacity M N 4^L), so the
+// launches are captured once in a CUDA graph and replayed every adapt.
+void launch_prefix(Sim& s, Grid& g, AdaptState& a, const LvTab& tab) {
   cudaStream_t st = stream();
-  Grid& g = *s.grid;
-  AdaptState& a = *s.ad;
   const int L = g.L;
-  LvTab tab = lv_tab(s, g, a);
-  // encode_up
   run_levels_flat<ZeroKnownBody>(tab, 0, L);
   PtrTab pt{};
   for (int l = 0; l <= L; ++l) {
     pt.known[l] = a.known[l].p;
     pt.sc[l] = a.sc[l].p;
   }
-  k_mark_leaves<<<nblk(s.n, 256), 256, 0, st>>>(s.n, s.M, s.lvl.p, s.li.p, s.lj.p, s.u.p, pt);
+  k_mark_leaves_dn<<<148 * 4, 256, 0, st>>>(a.dn.p, s.M, s.lvl.p, s.li.p, s.lj.p, s.u.p, pt);
   FM_LAUNCHED();
+  // norms over the current leaves (solver_adaptive.cpp:139-144)
+  FM_CUDA(cudaMemsetAsync(a.norms.p, 0, 3 * sizeof(unsigned long long), st));
+  k_norms<<<148 * 4, 256, 0, st>>>(a.dn.p, s.u.p, a.norms.p);
+  FM_LAUNCHED();
+  // encode_up + flag + closure, one sweep (into tmp)
   if (a.kind == 0)
-    run_levels<EncodeUpBody<0>>(tab, 0, L - 1, true);
+    run_levels<EncodeFlagBody<0>>(tab, 0, L - 1, true);
   else
-    run_levels<EncodeUpBody<1>>(tab, 0, L - 1, true);
-  // norms over the current leaves
-  a.norms.zero();
-  k_norms<<<nblk(s.n, 256), 256, 0, st>>>(s.n, s.u.p, a.norms.p);
-  FM_LAUNCHED();
-  // flag + closure
-  run_levels_flat<FlagBody>(tab, 0, L - 1);
-  run_levels<ClosureBody>(tab, 0, L - 2, true);
-  // buffer_ring; its ancestor closure is subsumed by the grading pass: the
-  // gather form of grade_flags sets G(l) = F(l) | any child G(l+1) | ring,
-  // bottom-up, so G(closure(F)) = G(F) level by level (the closure's child
-  // term is contained in G's)
+    run_levels<EncodeFlagBody<1>>(tab, 0, L - 1, true);
+  // buffer_ring (tmp -> the grid's flags); its ancestor closure is subsumed
+  // by the grading pass: the gather form of grade_flags sets
+  // G(l) = F(l) | any child G(l+1) | ring, bottom-up, so G(closure(F)) = G(F)
+  // level by level (the closure's child term is contained in G's)
   run_levels_flat<RingBody>(tab, 0, L - 1);
-  for (int l = 0; l < L; ++l) std::swap(g.flag[l], a.tmp[l]);
   // grade + counts + leaves + exact topography (assemble_grid)
   grade_count_levels(g, true);
-  build_leaves(g);
+  build_leaves_device(g, a.dn.p + 1);
+}
+
+void adapt_prefix(Sim& s, Grid& g, AdaptState& a, const LvTab& tab) {
+  cudaStream_t st = stream();
+  k_set_dn<<<1, 1, 0, st>>>(a.dn.p, s.n);
+  FM_LAUNCHED();
+  const std::vector<const void*> key = {s.u.p, s.lvl.p, s.li.p, s.lj.p, g.lf_l.p, g.lf_i.p, g.lf_j.p, g.lf_z.p};
+  if (!a.prefix || key != a.prefix_key) {
+    if (a.prefix) cudaGraphExecDestroy(a.prefix);
+    a.prefix = nullptr;
+    const int64_t before = launches();
+    cudaGraph_t gr;
+    FM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    launch_prefix(s, g, a, tab);
+    FM_CUDA(cudaStreamEndCapture(st, &gr));
+    FM_CUDA(cudaGraphInstantiate(&a.prefix, gr, 0));
+    cudaGraphDestroy(gr);
+    a.prefix_key = key;
+    a.prefix_kernels = launches() - before;
+  }
+  FM_CUDA(cudaGraphLaunch(a.prefix, st));
+  count_graph_launches(a.prefix_kernels);
+}
+}  // namespace
+
+void adaptive_adapt(Sim& s, double t) {
+  s.ref_perm_ok = false;  // the leaf set changes
+  ++s.leaf_gen;
+  cudaStream_t st = stream();
+  PhaseClock pc(st);
+  Grid& g = *s.grid;
+  AdaptState& a = *s.ad;
+  const int L = g.L;
+  LvTab tab = lv_tab(s, g, a);
+  // everything up to the new leaf list, one graph replay (adapt_prefix),
+  // then the new leaf count: the adapt's one host round trip before the
+  // topology's
+  adapt_prefix(s, g, a, tab);
+  long long n_dev = 0;
+  FM_CUDA(cudaMemcpyAsync(&n_dev, a.dn.p + 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  FM_CUDA(cudaStreamSynchronize(st));
+  g.nleaves = n_dev;
+  g.lf_l.n = g.lf_i.n = g.lf_j.n = size_t(n_dev);
+  g.lf_z.n = 3 * size_t(n_dev);
+  pc.mark("prefix");
   // transfer the flow onto the new leaves
   // the new state goes into the U* scratch, which then becomes U (no
   // allocation per adapt: the buffers only grow)
@@ -611,14 +716,18 @@ void adaptive_adapt(Sim& s, double t) {
       k_transfer_leaves<1><<<nblk(n_new, 256), 256, 0, st>>>(tab, n_new, g.lf_l.p, g.lf_i.p, g.lf_j.p);
     FM_LAUNCHED();
   }
-  std::swap(s.u, s.us);
-  s.us.ensure(9 * n_new);
+  pc.mark("transfer");
+  // U keeps its allocation (the prefix graph reads it): copy the new state in
+  s.u.ensure(9 * n_new);
+  FM_CUDA(cudaMemcpyAsync(s.u.p, s.us.p, 9 * size_t(n_new) * sizeof(double), cudaMemcpyDeviceToDevice, st));
   copy_leaves_from_grid(s, g);
   if (s.scheme != FM_DG2) {
     k_zero_slopes<<<nblk(s.n, 256), 256, 0, st>>>(s.n, s.z.p, s.u.p);
     FM_LAUNCHED();
   }
+  pc.mark("copy");
   refresh_topology(s);
+  pc.mark("topology");
   s.fv1_in_star = false;
   for (auto& g : s.gexec) {
     if (g) cudaGraphExecDestroy(g);

@@ -150,6 +150,7 @@ void grade_count_levels(Grid& g, bool graded);
 // (already in g.flag) compute counts, offsets, then decode topography details
 // top-down into the leaf arrays.  Returns the leaf count.
 int64_t build_leaves(Grid& g);
+void build_leaves_device(Grid& g, long long* total);
 // Permutation device-order -> reference (level, j, i) order, computed on the host.
 std::vector<int64_t> reference_order(const Grid& g, std::vector<int8_t>* l = nullptr,
                                      std::vector<int32_t>* i = nullptr,

@@ -684,6 +684,44 @@ int64_t build_leaves(Grid& g) {
   return g.nleaves;
 }
 
+// build_leaves without a host round trip (the adaptive re-grid's graph):
+// level-0 offsets, then the top-down decode into leaf arrays that hold every
+// possible leaf (capacity M N 4^L); the leaf count lands in *total.  cnt /
+// off / zs must already be allocated (a previous build_leaves).
+void build_leaves_device(Grid& g, long long* total) {
+  cudaStream_t st = stream();
+  const int L = g.L;
+  k_level0_offsets<<<1, 1024, 0, st>>>(g.cnt[0].p, g.off[0].p, int64_t(g.nodes(0)), total);
+  FM_LAUNCHED();
+  LeafOut out{g.lf_l.p, g.lf_i.p, g.lf_j.p, g.lf_z.p};
+  std::vector<DBuf<double>>& zs = g.zs;
+  int ls = -1;
+  for (int l = 0; l < L; ++l)
+    if (g.nodes(l) <= kSmallLevelNodes) ls = l;
+  if (ls >= 0) {
+    LevelPtrs p{};
+    for (int l = 0; l < L; ++l) {
+      p.fl[l] = g.flag[l].p;
+      p.cnt[l] = g.cnt[l].p;
+      p.off[l] = g.off[l].p;
+      p.zs[l] = l ? zs[l].p : g.coarse.p;
+      p.det[l] = g.det[l].p;
+    }
+    k_topdown_small<<<1, 256, 0, st>>>(p, ls, L, g.M, g.N, g.kind, out);
+    FM_LAUNCHED();
+  }
+  for (int l = ls + 1; l < L; ++l) {
+    const uint64_t nodes = g.nodes(l);
+    const bool last = l + 1 == L;
+    k_topdown<<<blocks_for(nodes, 256), 256, 0, st>>>(
+        l ? g.flag[l - 1].p : nullptr, g.flag[l].p, last ? nullptr : g.flag[l + 1].p,
+        last ? nullptr : g.cnt[l + 1].p, g.off[l].p, last ? nullptr : g.off[l + 1].p,
+        l ? zs[l].p : g.coarse.p, last ? nullptr : zs[l + 1].p, g.det[l].p, l, L, g.M, g.kind,
+        nodes, out);
+    FM_LAUNCHED();
+  }
+}
+
 // Projection + multi-level encode (detail_tree.cpp:10-54 with the fused
 // field.cpp:64-117): fills g.det, g.flag (= significance, detail_tree.cpp:66-72,
 // before closure), g.coarse and g.field_norm.  All buffers are allocated
