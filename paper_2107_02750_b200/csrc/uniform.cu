@@ -31,13 +31,14 @@ void project_planes_rowmajor(const fm_raster* r, DBuf<double>& out);
 
 namespace {
 
-// 32 x 4 tiles, >= 8 resident per SM (a 64-register cap): tuned by A/B on
+// 32 x 4 tiles, >= 7 resident per SM (a 72-register cap; 8: 20.31, 7: 19.49,
+// 6: 20.26, 5: 20.99 ms/step in the round-2 A/B): tuned by A/B on
 // B200 (scripts/ab_uniform.py); 32 x 8 tiles at 110 registers ran 25 % slower
 #ifndef FM_UNI_TY
 #define FM_UNI_TY 4
 #endif
 #ifndef FM_UNI_MINB
-#define FM_UNI_MINB 8
+#define FM_UNI_MINB 7
 #endif
 constexpr int TX = 32, TY = FM_UNI_TY;
 
