@@ -237,6 +237,13 @@ int fm_sim_sample_gauges(fm_sim* s, int32_t n, const double* x, const double* y,
  * its restore, without host traffic; restore fails if the leaf set changed
  * since the snapshot (adaptive re-gridding). */
 int fm_sim_snapshot(fm_sim* s);
+/* Binary checkpoint / restart (the reference has none): the leaf
+ * keys and topography in the reference order, the flow state, and ACC's
+ * face discharges.  Resume requires the same scenario and leaf set (keys
+ * and topography bit for bit; FM_ERR_CONFIG otherwise); the EventClock
+ * stays with the caller.  I/O errors: FM_ERR_IO. */
+int fm_sim_checkpoint(fm_sim* s, const char* path);
+int fm_sim_resume(fm_sim* s, const char* path);
 int fm_sim_restore(fm_sim* s);
 /* UniformSim's ACC face discharges acc_qx ((nx+1) x ny, row-major j*(nx+1)+i)
  * and acc_qy (nx x (ny+1)) (solver_uniform.hpp:53-54), read into get_x/get_y
@@ -267,6 +274,12 @@ const char* fm_sim_kernel_name(fm_sim* s, int32_t family);
  * {hits, misses, false_alarms}, rates = {hit_rate, false_alarm, csi}.  Either
  * raster may be device resident (e.g. from fm_sim_raster(..., out_on_device=1)).
  * Mismatched geometries: FM_ERR_IO (ParseError). */
+/* rmse (metrics.cpp:32-46) of two gauge series (t strictly increasing): the
+ * test series linearly interpolated at the reference's sample times inside
+ * the overlap, the reference's summation order.  Host-side: gauge series are
+ * hundreds of samples.  Empty or non-overlapping series: FM_ERR_IO. */
+int fm_rmse(const double* test_t, const double* test_v, int64_t n_test, const double* ref_t,
+            const double* ref_v, int64_t n_ref, double* out);
 int fm_extent_metrics(const fm_raster* test, const fm_raster* ref, double wet_threshold,
                       int64_t* counts, double* rates);
 

@@ -22,8 +22,10 @@
 #include "fm_gpu.hpp"
 
 #include "src/run.cpp"  // the reference's run.cpp, verbatim, from -I$(REF_ROOT)
+#include "floodmra/metrics.hpp"
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -49,8 +51,23 @@ RunResult run_scenario_gpu(const ScenarioConfig& cfg) {
 }  // namespace floodmra
 
 int main(int argc, char** argv) {
+  if (argc == 5 && std::strcmp(argv[1], "compare") == 0) {
+    // the reference's own post-processing (metrics.cpp:100-143) of two run
+    // directories: rmse of every gauge (h, eta, speed) and the extent
+    // metrics of every depth raster
+    try {
+      const floodmra::CompareReport r = floodmra::compare_runs(argv[2], argv[3], std::atof(argv[4]));
+      for (const auto& row : r.rows)
+        std::printf("%s %s %s %.17g %d\n", row.kind.c_str(), row.id.c_str(), row.metric.c_str(), row.value,
+                    row.absent ? 1 : 0);
+    } catch (const std::exception& e) {
+      std::fprintf(stderr, "compare error: %s\n", e.what());
+      return 3;
+    }
+    return 0;
+  }
   if (argc != 4 || (std::strcmp(argv[1], "ref") && std::strcmp(argv[1], "gpu"))) {
-    std::fprintf(stderr, "usage: %s ref|gpu CONFIG OUTPUT_DIR\n", argv[0]);
+    std::fprintf(stderr, "usage: %s ref|gpu CONFIG OUTPUT_DIR | compare TEST_DIR REF_DIR WET\n", argv[0]);
     return 2;
   }
   try {

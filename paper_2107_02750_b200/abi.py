@@ -124,6 +124,8 @@ OPTIONAL = {
     "sim_kernel_name": (C.c_char_p, [P, I32]),
     "sim_acc_q": (C.c_int, [P, PD, PD]),
     "sim_acc_faces": (C.c_int, [P, PD, PD, PD, PD]),
+    "sim_checkpoint": (C.c_int, [P, C.c_char_p]),
+    "sim_resume": (C.c_int, [P, C.c_char_p]),
     "sim_geometry": (C.c_int, [P, PI32, PI32, PI32, PD, PD, PD]),
     "set_threads": (None, [I32]),
     "hw_threads": (I32, []),
@@ -517,6 +519,14 @@ class Sim:
         py = None if sy is None else dptr(sy)
         self.be.call("sim_acc_faces", self.h, dptr(gx), dptr(gy), px, py)
         return gx, gy
+
+    def checkpoint(self, path: str):
+        """fm_sim_checkpoint: leaf keys, flow state, topography, ACC discharges."""
+        self.be.call("sim_checkpoint", self.h, str(path).encode())
+
+    def resume(self, path: str):
+        """fm_sim_resume onto the same scenario and leaf set."""
+        self.be.call("sim_resume", self.h, str(path).encode())
 
     def geometry(self) -> dict:
         L, M, N = I32(), I32(), I32()

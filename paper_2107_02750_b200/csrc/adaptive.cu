@@ -683,6 +683,7 @@ void adapt_prefix(Sim& s, Grid& g, AdaptState& a, const LvTab& tab) {
 }  // namespace
 
 void adaptive_adapt(Sim& s, double t) {
+  FM_RANGE("adapt");
   s.ref_perm_ok = false;  // the leaf set changes
   ++s.leaf_gen;
   cudaStream_t st = stream();

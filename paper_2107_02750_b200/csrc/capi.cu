@@ -1,5 +1,7 @@
 // The C ABI of include/fm_gpu.h.  Every entry point converts C++ exceptions
 // into status codes + a thread-local message; no exception crosses the ABI.
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -477,6 +479,34 @@ int fm_sim_topology(fm_sim* s, int32_t* level, int32_t* i, int32_t* j, int32_t* 
     FM_CUDA(cudaStreamSynchronize(stream()));
   });
 }
+int fm_rmse(const double* tt, const double* tv, int64_t nt, const double* rt, const double* rv, int64_t nr,
+            double* out) {
+  return guard([&] {
+    if (nt <= 0 || nr <= 0 || !tt || !tv || !rt || !rv || !out) throw Error(FM_ERR_IO, "rmse: empty series");
+    // interpolate (metrics.cpp:20-28)
+    auto interp = [&](double t) {
+      const double* hi = std::upper_bound(tt, tt + nt, t);
+      if (hi == tt) return tv[0];
+      if (hi == tt + nt) return tv[nt - 1];
+      const int64_t k = hi - tt;
+      const double t0 = tt[k - 1], t1 = tt[k];
+      const double w = (t - t0) / (t1 - t0);
+      return tv[k - 1] + w * (tv[k] - tv[k - 1]);
+    };
+    const double lo = std::max(tt[0], rt[0]);
+    const double hi = std::min(tt[nt - 1], rt[nr - 1]);
+    double sum = 0.0;
+    long long n = 0;
+    for (int64_t k = 0; k < nr; ++k) {
+      if (rt[k] < lo || rt[k] > hi) continue;
+      const double d = interp(rt[k]) - rv[k];
+      sum += d * d;
+      ++n;
+    }
+    if (n == 0) throw Error(FM_ERR_IO, "rmse: series do not overlap in time");
+    *out = std::sqrt(sum / double(n));
+  });
+}
 int fm_extent_metrics(const fm_raster* test, const fm_raster* ref, double wet_threshold, int64_t* counts,
                       double* rates) {
   return guard([&] {
@@ -495,6 +525,12 @@ int fm_eval_libm(int32_t fn, int64_t n, const double* x, double* out) {
     dy.download(out, n);
     FM_CUDA(cudaStreamSynchronize(stream()));
   });
+}
+int fm_sim_checkpoint(fm_sim* s, const char* path) {
+  return guard([&] { sim_checkpoint(*s->s, path); });
+}
+int fm_sim_resume(fm_sim* s, const char* path) {
+  return guard([&] { sim_resume(*s->s, path); });
 }
 int fm_sim_snapshot(fm_sim* s) {
   return guard([&] { sim_snapshot(*s->s); });

@@ -11,7 +11,17 @@
 
 #include "../../include/fm_gpu.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace fmh {
+
+struct NvtxRange {
+  explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 struct Error : std::runtime_error {
   int code;
@@ -21,6 +31,9 @@ struct Error : std::runtime_error {
 void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 #define FM_CUDA(x) ::fmh::cuda_check((x), #x, __FILE__, __LINE__)
 #define FM_LAUNCHED() ::fmh::count_launch(__FILE__, __LINE__)
+// NVTX ranges around the library's phases (no-ops unless a profiler such as
+// Nsight Systems attaches; header-only NVTX v3 from the CUDA toolkit)
+#define FM_RANGE(name) ::fmh::NvtxRange fm_nvtx_range_(name)
 void count_launch(const char* file, int line);
 int64_t launches();
 void count_graph_launches(int64_t n);  // kernels replayed by a graph launch

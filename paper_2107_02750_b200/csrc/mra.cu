@@ -609,6 +609,7 @@ inline unsigned blocks_for(uint64_t n, int t) { return unsigned((n + t - 1) / t)
 }  // namespace
 
 int64_t build_leaves(Grid& g) {
+  FM_RANGE("build_leaves");
   cudaStream_t st = stream();
   const int L = g.L;
   g.cnt.resize(L);
@@ -727,6 +728,7 @@ void build_leaves_device(Grid& g, long long* total) {
 // before closure), g.coarse and g.field_norm.  All buffers are allocated
 // before the first kernel so `ms` (CUDA events) times kernels only.
 void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, double* ms) {
+  FM_RANGE("mra_encode");
   if (!dem || !dem->values) throw Error(FM_ERR_CONFIG, "null DEM raster");
   if (dem->ncols < 2 || dem->nrows < 2)
     throw Error(FM_ERR_CONFIG, "DEM must have at least 2x2 samples to define elements");
@@ -997,6 +999,7 @@ Grid* grid_from_leaves(int L, int M, int N, double R, double x0, double y0, int6
 }
 
 Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind) {
+  FM_RANGE("fm_mra_static");
   auto g = std::make_unique<Grid>();
   g->graded = graded;
   double enc_ms = 0.0;

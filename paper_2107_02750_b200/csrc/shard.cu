@@ -826,6 +826,7 @@ static void host_exchange(Sim& s, double* arr, int w) {
 bool shard_eager(const Sim& s) { return s.shard && s.shard->comm && s.shard->comm->kind == COMM_HOST; }
 
 void shard_op(Sim& s, int op) {
+  FM_RANGE(op == OP_REDUCE ? "shard_reduce" : "shard_exchange");
   Shard& sh = *s.shard;
   if (!sh.comm) throw Error(FM_ERR_CONFIG, "shard: the communicator was destroyed");
   if (sh.comm->kind == COMM_HOST) {

@@ -2,6 +2,8 @@
 // solver_nonuniform.cpp:558-636), the drive<Sim> member functions
 // (run.cpp:35-141) and the device-resident step loop captured in a CUDA graph.
 #include <algorithm>
+#include <cstdio>
+#include <memory>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -324,6 +326,7 @@ void ic_finish(Sim& s) {
 }
 
 Sim* sim_create(const fm_sim_desc* d, const fm_raster* dem, const Grid* grid) {
+  FM_RANGE("fm_sim_create");
   if (!d || !dem) throw Error(FM_ERR_CONFIG, "null descriptor or DEM");
   upload_banks();
   auto s = std::make_unique<Sim>();
@@ -477,6 +480,7 @@ void key_xy(const Sim& s, unsigned long long key, double* bx, double* by) {
 }  // namespace
 
 double sim_compute_dt(Sim& s) {
+  FM_RANGE("fm_sim_compute_dt");
   state_to_u(s);
   init_red(s);
   DevClock pair0[2] = {};
@@ -499,6 +503,7 @@ double sim_compute_dt(Sim& s) {
 }
 
 void sim_step(Sim& s, double dt) {
+  FM_RANGE("fm_sim_step");
   DBuf<int> err(1);
   err.zero();
   state_to_step(s);
@@ -587,6 +592,7 @@ void sim_sync_u(Sim& s) {
 // Reference order: (level, j, i) for leaves (quadgrid.cpp:94-98), j*nx+i for
 // rasters; permuted on the device (order.cu).
 void sim_download(Sim& s, int32_t* lo, int32_t* io, int32_t* jo, double* u9, double* z3) {
+  FM_RANGE("fm_sim_download");
   state_to_u(s);
   const int32_t* perm = sim_ref_perm(s);
   // U* is idle between steps (FV1's staged state was just moved back to U)
@@ -600,6 +606,7 @@ void sim_download(Sim& s, int32_t* lo, int32_t* io, int32_t* jo, double* u9, dou
 }
 
 void sim_upload(Sim& s, const double* u9) {
+  FM_RANGE("fm_sim_upload");
   state_to_u(s);
   scatter_rows(sim_ref_perm(s), s.n, 9, u9, s.u.p);
 }
@@ -616,6 +623,7 @@ void sim_adapt(Sim& s, double t) {
 // whether to run (end time, step budget, events, blow-up), so surplus steps
 // of the last batch are no-ops and the host syncs once per batch.
 void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run_result* out) {
+  FM_RANGE("fm_sim_run");
   cudaStream_t st = stream();
   state_to_step(s);
   DevClock c0 = fresh_clock(ck, max_steps, stop_at_events);
@@ -866,6 +874,116 @@ void sim_profile(Sim& s, int64_t steps, double* ms, int64_t* counts, int cap, in
 }  // namespace fmh
 
 namespace fmh {
+
+// ---- binary checkpoint ("a binary state dump: leaf keys + 9
+// doubles + 3 topo doubles"), the restart path the reference lacks -------
+namespace {
+struct CkptHeader {
+  char magic[8];  // "FMCKPT1"
+  int32_t solver, scheme, uniform, L, M, N, nx, ny;
+  double R, x0, y0;
+  int64_t n, nseg, n_accq, n_accqb, n_aqx, n_aqy;
+};
+void write_all(FILE* f, const void* p, size_t bytes) {
+  if (bytes && std::fwrite(p, 1, bytes, f) != bytes) throw Error(FM_ERR_IO, "checkpoint: write failed");
+}
+void read_all(FILE* f, void* p, size_t bytes) {
+  if (bytes && std::fread(p, 1, bytes, f) != bytes) throw Error(FM_ERR_IO, "checkpoint: truncated file");
+}
+template <typename T>
+std::vector<T> dev_to_host(const DBuf<T>& b, size_t n) {
+  std::vector<T> v(n);
+  if (n) FM_CUDA(cudaMemcpyAsync(v.data(), b.p, n * sizeof(T), cudaMemcpyDeviceToHost, stream()));
+  return v;
+}
+}  // namespace
+
+// The leaf keys (level, i, j in the reference order), the flow state (9 per
+// leaf) and topography (3 per leaf), and ACC's face discharges (device
+// order, with the leaf set they belong to).
+void sim_checkpoint(Sim& s, const char* path) {
+  if (s.shard) throw Error(FM_ERR_CONFIG, "checkpoint: a shard checkpoints through its own rank");
+  state_to_u(s);
+  const int64_t n = s.n;
+  std::vector<int32_t> l(n), i(n), j(n);
+  std::vector<double> u(9 * size_t(n)), z(3 * size_t(n));
+  sim_download(s, l.data(), i.data(), j.data(), u.data(), z.data());
+  CkptHeader h{};
+  std::memcpy(h.magic, "FMCKPT1", 8);
+  h.solver = s.solver, h.scheme = s.scheme, h.uniform = s.uniform ? 1 : 0;
+  h.L = s.L, h.M = s.M, h.N = s.N, h.nx = s.nx, h.ny = s.ny;
+  h.R = s.R, h.x0 = s.x0, h.y0 = s.y0;
+  h.n = n, h.nseg = s.nseg;
+  const bool acc = s.scheme == FM_ACC;
+  h.n_accq = acc && !s.uniform ? int64_t(s.accq.n) : 0;
+  h.n_accqb = acc && !s.uniform ? int64_t(s.accqb.n) : 0;
+  h.n_aqx = acc && s.uniform ? int64_t(s.aqx.n) : 0;
+  h.n_aqy = acc && s.uniform ? int64_t(s.aqy.n) : 0;
+  const auto q = dev_to_host(s.accq, size_t(h.n_accq)), qb = dev_to_host(s.accqb, size_t(h.n_accqb));
+  const auto ax = dev_to_host(s.aqx, size_t(h.n_aqx)), ay = dev_to_host(s.aqy, size_t(h.n_aqy));
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  FILE* f = std::fopen(path, "wb");
+  if (!f) throw Error(FM_ERR_IO, std::string("checkpoint: cannot open ") + path);
+  try {
+    write_all(f, &h, sizeof(h));
+    write_all(f, l.data(), 4 * size_t(n));
+    write_all(f, i.data(), 4 * size_t(n));
+    write_all(f, j.data(), 4 * size_t(n));
+    write_all(f, u.data(), 8 * u.size());
+    write_all(f, z.data(), 8 * z.size());
+    write_all(f, q.data(), 8 * q.size());
+    write_all(f, qb.data(), 8 * qb.size());
+    write_all(f, ax.data(), 8 * ax.size());
+    write_all(f, ay.data(), 8 * ay.size());
+  } catch (...) {
+    std::fclose(f);
+    throw;
+  }
+  if (std::fclose(f) != 0) throw Error(FM_ERR_IO, "checkpoint: close failed");
+}
+
+// Restores a checkpoint onto a sim of the same scenario and leaf set (the
+// keys and topography must match bit for bit; otherwise FM_ERR_CONFIG).
+void sim_resume(Sim& s, const char* path) {
+  if (s.shard) throw Error(FM_ERR_CONFIG, "resume: a shard resumes through its own rank");
+  FILE* f = std::fopen(path, "rb");
+  if (!f) throw Error(FM_ERR_IO, std::string("resume: cannot open ") + path);
+  std::unique_ptr<FILE, int (*)(FILE*)> guard(f, std::fclose);
+  CkptHeader h{};
+  read_all(f, &h, sizeof(h));
+  if (std::memcmp(h.magic, "FMCKPT1", 8) != 0) throw Error(FM_ERR_IO, "resume: not a floodmra-b200 checkpoint");
+  if (h.solver != s.solver || h.uniform != (s.uniform ? 1 : 0) || h.L != s.L || h.M != s.M || h.N != s.N ||
+      h.nx != s.nx || h.ny != s.ny || h.R != s.R || h.x0 != s.x0 || h.y0 != s.y0 || h.n != s.n)
+    throw Error(FM_ERR_CONFIG, "resume: the checkpoint belongs to another scenario or leaf set");
+  const int64_t n = h.n;
+  std::vector<int32_t> l(n), i(n), j(n), l0(n), i0(n), j0(n);
+  std::vector<double> u(9 * size_t(n)), z(3 * size_t(n)), z0(3 * size_t(n));
+  read_all(f, l.data(), 4 * size_t(n));
+  read_all(f, i.data(), 4 * size_t(n));
+  read_all(f, j.data(), 4 * size_t(n));
+  read_all(f, u.data(), 8 * u.size());
+  read_all(f, z.data(), 8 * z.size());
+  std::vector<double> q(size_t(h.n_accq)), qb(size_t(h.n_accqb)), ax(size_t(h.n_aqx)), ay(size_t(h.n_aqy));
+  read_all(f, q.data(), 8 * q.size());
+  read_all(f, qb.data(), 8 * qb.size());
+  read_all(f, ax.data(), 8 * ax.size());
+  read_all(f, ay.data(), 8 * ay.size());
+  state_to_u(s);
+  sim_download(s, l0.data(), i0.data(), j0.data(), nullptr, z0.data());
+  if (l != l0 || i != i0 || j != j0 || std::memcmp(z.data(), z0.data(), 8 * z.size()) != 0)
+    throw Error(FM_ERR_CONFIG, "resume: the leaf set or topography differs from the checkpoint's");
+  if (size_t(h.n_accq) != (s.scheme == FM_ACC && !s.uniform ? s.accq.n : 0) ||
+      size_t(h.n_accqb) != (s.scheme == FM_ACC && !s.uniform ? s.accqb.n : 0) ||
+      size_t(h.n_aqx) != (s.scheme == FM_ACC && s.uniform ? s.aqx.n : 0) ||
+      size_t(h.n_aqy) != (s.scheme == FM_ACC && s.uniform ? s.aqy.n : 0))
+    throw Error(FM_ERR_CONFIG, "resume: ACC discharge arrays differ in size");
+  sim_upload(s, u.data());
+  if (!q.empty()) FM_CUDA(cudaMemcpyAsync(s.accq.p, q.data(), 8 * q.size(), cudaMemcpyHostToDevice, stream()));
+  if (!qb.empty()) FM_CUDA(cudaMemcpyAsync(s.accqb.p, qb.data(), 8 * qb.size(), cudaMemcpyHostToDevice, stream()));
+  if (!ax.empty()) FM_CUDA(cudaMemcpyAsync(s.aqx.p, ax.data(), 8 * ax.size(), cudaMemcpyHostToDevice, stream()));
+  if (!ay.empty()) FM_CUDA(cudaMemcpyAsync(s.aqy.p, ay.data(), 8 * ay.size(), cudaMemcpyHostToDevice, stream()));
+  FM_CUDA(cudaStreamSynchronize(stream()));
+}
 
 void sim_snapshot(Sim& s) {
   acc_to_u(s);  // the snapshot holds U (the compact states folded back)

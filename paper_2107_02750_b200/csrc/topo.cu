@@ -308,6 +308,7 @@ void build_seg_geo(Sim& s) {
 }
 
 void build_topology(Sim& s, const Grid& g) {
+  FM_RANGE("build_topology");
   cudaStream_t st = stream();
   const long long n = s.n;
   s.nb.ensure(8 * n);

@@ -55,3 +55,46 @@ def test_library_loads_and_fails_loudly_without_gpu():
 def test_sass_is_sm100a():
     out = subprocess.run(["cuobjdump", "--list-elf", GPU_SO], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
+
+
+def test_rmse_restates_metrics_cpp():
+    """fm_rmse (host side of the library) against a plain restatement of
+    metrics.cpp:20-46 in the same operation order: bit-exact."""
+    import bisect
+    import numpy as np
+    lib = ctypes.CDLL(GPU_SO)
+    P = ctypes.POINTER(ctypes.c_double)
+    lib.fm_rmse.argtypes = [P, P, ctypes.c_int64, P, P, ctypes.c_int64, P]
+    rng = np.random.default_rng(2)
+    tt = np.cumsum(rng.uniform(0.5, 3.0, 200))
+    tv = rng.normal(size=200)
+    rt = np.cumsum(rng.uniform(0.2, 2.0, 300)) + 5.0
+    rv = rng.normal(size=300)
+
+    def interp(t):
+        hi = bisect.bisect_right(list(tt), t)
+        if hi == 0:
+            return tv[0]
+        if hi == len(tt):
+            return tv[-1]
+        t0, t1 = tt[hi - 1], tt[hi]
+        w = (t - t0) / (t1 - t0)
+        return tv[hi - 1] + w * (tv[hi] - tv[hi - 1])
+
+    lo, hi = max(tt[0], rt[0]), min(tt[-1], rt[-1])
+    s, n = 0.0, 0
+    for t, v in zip(rt, rv):
+        if t < lo or t > hi:
+            continue
+        d = interp(t) - v
+        s += d * d
+        n += 1
+    want = float(np.sqrt(s / n))
+    out = ctypes.c_double()
+    c = [np.ascontiguousarray(a) for a in (tt, tv, rt, rv)]
+    st = lib.fm_rmse(*(a.ctypes.data_as(P) for a in c[:2]), len(tt), *(a.ctypes.data_as(P) for a in c[2:]),
+                     len(rt), ctypes.byref(out))
+    assert st == 0 and out.value == want
+    st = lib.fm_rmse(c[0].ctypes.data_as(P), c[1].ctypes.data_as(P), 0, c[2].ctypes.data_as(P),
+                     c[3].ctypes.data_as(P), len(rt), ctypes.byref(out))
+    assert st == 3  # empty series: ParseError class

@@ -118,6 +118,13 @@ def test_reference_arm_runs_on_cpu(tmp_path):
     files = os.listdir(tmp_path / "out")
     for f in ("stats.txt", "elements.csv", "gauge_0.csv", "depth_0000.asc", "grid_0000.nug"):
         assert f in files
+    # the reference's compare_runs of a directory with itself
+    rc = subprocess.run([EXE, "compare", str(tmp_path / "out"), str(tmp_path / "out"), "0.01"],
+                        capture_output=True, text=True, timeout=300)
+    assert rc.returncode == 0, rc.stderr
+    rows = [ln.split() for ln in rc.stdout.splitlines()]
+    assert any(r[0] == "rmse" for r in rows) and any(r[0] == "extent" for r in rows)
+    assert all(float(r[3]) == (0.0 if r[0] == "rmse" or r[2] == "F" else 1.0) for r in rows)
 
 
 def test_gpu_arm_fails_loudly_without_a_device(tmp_path):
@@ -146,6 +153,21 @@ def test_drive_gpu_matches_reference_drive(tmp_path, name):
     assert ra.returncode == 0, ra.stderr
     s = compare_dirs(str(tmp_path / "gpu"), str(tmp_path / "ref"))
     assert int(s["steps"]) > 0
+    # the reference's own compare_runs (metrics.cpp:100-143) on the two run
+    # directories: gauge RMSEs ~0, identical inundation extents
+    rc = subprocess.run([EXE, "compare", str(tmp_path / "gpu"), str(tmp_path / "ref"), "0.01"],
+                        capture_output=True, text=True, timeout=300)
+    assert rc.returncode == 0, rc.stderr
+    rows = [ln.split() for ln in rc.stdout.splitlines() if ln.strip()]
+    assert rows and all(r[-1] == "0" for r in rows)  # nothing absent
+    for kind, _, metric, value, _ in rows:
+        v = float(value)
+        if kind == "rmse":
+            assert v <= 1e-9 or np.isnan(v), rows
+        elif metric in ("H", "C"):
+            assert v == 1.0, rows
+        else:
+            assert v == 0.0, rows
     if name.startswith(("c0", "c1", "c2", "c3", "c4_static")):
         assert int(s["leaf_count"]) > 0  # sim_leaf_count overloads reached (run.cpp:24-33)
 

@@ -301,3 +301,50 @@ def test_second_run_resumes_from_the_current_state(gpu, orc, solver, uniform):
         out.append((ck.now, r.dt_min, r.dt_max, s.download()[3]))
     assert out[0][:3] == out[1][:3]
     assert np.array_equal(out[0][3], out[1][3])
+
+
+@pytest.mark.parametrize("name", ["c0_dg2", "c1_acc", "c2_fv1", "uni_acc", "uni_dg2"])
+def test_checkpoint_resume_continues_bit_exact(gpu, tmp_path, name):
+    """fm_sim_checkpoint / fm_sim_resume (the binary restart path of SURVEY
+    §5): N steps, checkpoint, M steps == a fresh sim resumed from the
+    checkpoint then M steps, bit for bit (the clock is the caller's)."""
+    import dataclasses
+    from paper_2107_02750_b200.abi import c_clock
+    sc = {"c0_dg2": lambda: S.config0(4), "c1_acc": lambda: S.config1(8),
+          "c2_fv1": lambda: S.config2(8, adaptive=False),
+          "uni_acc": lambda: dataclasses.replace(S.config4(64, uniform=True), solver="acc", courant=0.7),
+          "uni_dg2": lambda: S.config4(64, uniform=True)}[name]()
+    a = make(gpu, sc)
+    ck, _ = a.run(12, gauge_interval=10.0)
+    path = tmp_path / "state.fmck"
+    a.checkpoint(path)
+    ck2 = c_clock(ck.end_time, ck.output_interval, ck.gauge_interval, ck.now, ck.next_output, ck.next_gauge)
+    a.run(10, clock=ck)
+    b = make(gpu, sc)
+    b.resume(path)
+    b.run(10, clock=ck2)
+    for x, y in zip(a.download(), b.download()):
+        assert np.array_equal(x, y)
+
+
+def test_resume_rejects_another_scenario_or_leaf_set(gpu, tmp_path):
+    from paper_2107_02750_b200.abi import FmError
+    sc = S.config0(4)
+    a = make(gpu, sc)
+    a.run(5, gauge_interval=10.0)
+    p = tmp_path / "a.fmck"
+    a.checkpoint(p)
+    with pytest.raises(FmError) as e:  # another solver
+        make(gpu, S.config1(8)).resume(p)
+    assert e.value.code == 2
+    raw = bytearray(p.read_bytes())
+    hdr = 8 + 4 * 8 + 3 * 8 + 6 * 8  # CkptHeader
+    raw[hdr] ^= 1  # the first leaf's level
+    q = tmp_path / "b.fmck"
+    q.write_bytes(bytes(raw))
+    with pytest.raises(FmError) as e:  # another leaf set
+        make(gpu, sc).resume(q)
+    assert e.value.code == 2
+    with pytest.raises(FmError) as e:
+        make(gpu, sc).resume(tmp_path / "missing.fmck")
+    assert e.value.code == 3
