@@ -534,8 +534,25 @@ def _leg(be, sc, static, warm, steps, device_time):
     else:  # adaptive: the leaf count of every step (element_log, one entry per adapt)
         _, counts = s.element_log()
         cells = float(np.sum(counts[-r.steps:])) if len(counts) else float(s.num_cells) * r.steps
-    return {"leaves": int(s.num_cells), "steps": int(r.steps), "ms_per_step": ms / max(r.steps, 1),
-            "value": cells / (ms / 1000.0)}
+    out = {"leaves": int(s.num_cells), "steps": int(r.steps), "ms_per_step": ms / max(r.steps, 1),
+           "value": cells / (ms / 1000.0)}
+    if device_time and not static and be.has("sim_adapt_stats"):
+        # SURVEY §8 d4 per adapted step: the adapt (MW: 72 N_l + 360 N_enc +
+        # N_int + 108 N_l' + 32 N_s'; HW: 24 / 120 / 36 for 72 / 360 / 108)
+        # plus the flow step (MWDG2: DG2 424 N_l + 16 N_s; HWFV1: FV1 64 N_l + 8 N_s)
+        st = s.adapt_stats()
+        nl, ns, ne, ni = float(s.num_cells), float(s.num_segments), st["n_encoded"], st["n_internal"]
+        mw = sc.solver == "mwdg2"
+        a, b, c = (72.0, 360.0, 108.0) if mw else (24.0, 120.0, 36.0)
+        adapt_b = a * nl + b * ne + ni + c * nl + 32.0 * ns
+        step_b = (424.0 * nl + 16.0 * ns) if mw else (64.0 * nl + 8.0 * ns)
+        sec = out["ms_per_step"] / 1000.0
+        hbm, _ = peaks()
+        out["roofline"] = {"bound": "hbm", "adapt_bytes": adapt_b, "step_bytes": step_b,
+                           "n_encoded": int(ne), "n_internal": int(ni),
+                           "achieved": (adapt_b + step_b) / sec / 1e9,
+                           "frac": (adapt_b + step_b) / sec / 1e9 / hbm}
+    return out
 
 
 def config_legs(lib, args, with_cpu):

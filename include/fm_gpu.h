@@ -237,6 +237,10 @@ int fm_sim_sample_gauges(fm_sim* s, int32_t n, const double* x, const double* y,
  * its restore, without host traffic; restore fails if the leaf set changed
  * since the snapshot (adaptive re-gridding). */
 int fm_sim_snapshot(fm_sim* s);
+/* The last adapt's sizes (adaptive sims): parents encoded by encode_up
+ * (solver_adaptive.cpp:16-57) and the pyramid's internal nodes, for the
+ * SURVEY §8 d4 adapt byte count. */
+int fm_sim_adapt_stats(fm_sim* s, int64_t* n_encoded, int64_t* n_internal);
 /* Binary checkpoint / restart (the reference has none): the leaf
  * keys and topography in the reference order, the flow state, and ACC's
  * face discharges.  Resume requires the same scenario and leaf set (keys

@@ -125,6 +125,7 @@ OPTIONAL = {
     "sim_acc_q": (C.c_int, [P, PD, PD]),
     "sim_acc_faces": (C.c_int, [P, PD, PD, PD, PD]),
     "sim_checkpoint": (C.c_int, [P, C.c_char_p]),
+    "sim_adapt_stats": (C.c_int, [P, PI64, PI64]),
     "sim_resume": (C.c_int, [P, C.c_char_p]),
     "sim_geometry": (C.c_int, [P, PI32, PI32, PI32, PD, PD, PD]),
     "set_threads": (None, [I32]),
@@ -519,6 +520,12 @@ class Sim:
         py = None if sy is None else dptr(sy)
         self.be.call("sim_acc_faces", self.h, dptr(gx), dptr(gy), px, py)
         return gx, gy
+
+    def adapt_stats(self) -> dict:
+        """The last adapt's encoded parents and the pyramid's internal nodes."""
+        a, b = I64(), I64()
+        self.be.call("sim_adapt_stats", self.h, C.byref(a), C.byref(b))
+        return dict(n_encoded=a.value, n_internal=b.value)
 
     def checkpoint(self, path: str):
         """fm_sim_checkpoint: leaf keys, flow state, topography, ACC discharges."""

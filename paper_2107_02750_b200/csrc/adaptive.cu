@@ -682,6 +682,42 @@ void adapt_prefix(Sim& s, Grid& g, AdaptState& a, const LvTab& tab) {
 }
 }  // namespace
 
+namespace {
+__global__ void k_count_encoded(LvTab t, int l0, unsigned long long* out) {
+  const int l = l0 + blockIdx.y;
+  const uint64_t nodes = t.nodes(l);
+  unsigned long long c = 0;
+  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < nodes;
+       n += uint64_t(gridDim.x) * blockDim.x)
+    c += t.known[l][n] == 2;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+}  // namespace
+
+// The last adapt's sizes for SURVEY §8 d4's adapt bytes: parents encoded in
+// encode_up (N_enc) and the internal nodes of the pyramid (N_int).
+void adaptive_stats(Sim& s, int64_t* n_enc, int64_t* n_int) {
+  if (!s.adaptive || !s.ad) throw Error(FM_ERR_CONFIG, "adapt_stats: not an adaptive simulation");
+  Grid& g = *s.grid;
+  AdaptState& a = *s.ad;
+  LvTab tab = lv_tab(s, g, a);
+  DBuf<unsigned long long> c(1);
+  c.zero();
+  const unsigned bx = unsigned(std::min<uint64_t>(nblk(g.nodes(g.L - 1), 256), 148 * 8));
+  k_count_encoded<<<dim3(bx, g.L), 256, 0, stream()>>>(tab, 0, c.p);
+  FM_LAUNCHED();
+  unsigned long long h = 0;
+  c.download(&h, 1);
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  if (n_enc) *n_enc = int64_t(h);
+  if (n_int) {
+    int64_t ni = 0;
+    for (int l = 0; l < g.L; ++l) ni += int64_t(g.nodes(l));
+    *n_int = ni;
+  }
+}
+
 void adaptive_adapt(Sim& s, double t) {
   FM_RANGE("adapt");
   s.ref_perm_ok = false;  // the leaf set changes

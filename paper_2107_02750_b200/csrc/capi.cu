@@ -526,6 +526,9 @@ int fm_eval_libm(int32_t fn, int64_t n, const double* x, double* out) {
     FM_CUDA(cudaStreamSynchronize(stream()));
   });
 }
+int fm_sim_adapt_stats(fm_sim* s, int64_t* n_encoded, int64_t* n_internal) {
+  return guard([&] { adaptive_stats(*s->s, n_encoded, n_internal); });
+}
 int fm_sim_checkpoint(fm_sim* s, const char* path) {
   return guard([&] { sim_checkpoint(*s->s, path); });
 }

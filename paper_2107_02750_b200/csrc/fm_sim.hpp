@@ -189,6 +189,7 @@ void sim_upload(Sim& s, const double* u9);
 void sim_run(Sim& s, fm_clock* clk, int64_t max_steps, int stop_at_events, fm_run_result* out);
 void sim_profile(Sim& s, int64_t steps, double* ms, int64_t* counts, int cap, int* nfam);
 void sim_snapshot(Sim& s);
+void adaptive_stats(Sim& s, int64_t* n_enc, int64_t* n_int);
 void sim_checkpoint(Sim& s, const char* path);
 void sim_resume(Sim& s, const char* path);
 void sim_sync_u(Sim& s);  // FV1: move the staged post-step state back into u
