@@ -205,7 +205,8 @@ struct LvTab {
   const unsigned long long* norms;
   double eps;
   double* unew;
-  const double* z;
+  const double* z;  // leaf topography (3 per leaf, device order)
+  int zero_slopes;  // HWFV1: the leaves' z planes are taken with zero slopes
   __host__ __device__ uint64_t nodes(int l) const { return uint64_t(M) * N << (2 * l); }
 };
 
@@ -361,7 +362,8 @@ struct ZpyrBody {
         s = t.z + 3 * (l + 1 < L ? t.off[l + 1][ch] : t.off[l][n] + c);
       else
         s = t.zp[l + 1] + 3 * ch;
-      kids[c] = P3{s[0], s[1], s[2]};
+      // FV1 leaves carry zero topography slopes (k_zero_slopes, +0 exactly)
+      kids[c] = (leaf && t.zero_slopes) ? P3{s[0], 0.0, 0.0} : P3{s[0], s[1], s[2]};
     }
     const P3 p = encode_parent_k<KIND>(kids);
     t.zp[l][3 * n] = p.c0;
@@ -474,13 +476,9 @@ void refresh_topology(Sim& s) {
   resolve_manning(s);
   resolve_inflows(s, g);
   build_topology(s, g);
-  // z encode-up over the new leaves, then the partner values
+  // the partner values from the z encode-up pyramid (built in the adapt's
+  // prefix graph, right after the leaf list)
   const int L = s.L;
-  LvTab tab = lv_tab(s, g, a);
-  if (a.kind == 0)
-    run_levels<ZpyrBody<0>>(tab, 0, L - 1, true);
-  else
-    run_levels<ZpyrBody<1>>(tab, 0, L - 1, true);
   ZpTab t{};
   for (int l = 0; l < L; ++l) t.zp[l] = a.zp[l].p;
   s.zpair.ensure(4 * s.n);
@@ -657,6 +655,16 @@ void launch_prefix(Sim& s, Grid& g, AdaptState& a, const LvTab& tab) {
   // grade + counts + leaves + exact topography (assemble_grid)
   grade_count_levels(g, true);
   build_leaves_device(g, a.dn.p + 1);
+  // region_topo (solver_nonuniform.cpp:80-89) of every flagged node over the
+  // new leaves' topography (the grid's leaf planes; HWFV1 takes them with
+  // zero slopes, as the sim's own copy will hold them)
+  LvTab zt = tab;
+  zt.z = g.lf_z.p;
+  zt.zero_slopes = s.scheme != FM_DG2 ? 1 : 0;
+  if (a.kind == 0)
+    run_levels<ZpyrBody<0>>(zt, 0, L - 1, true);
+  else
+    run_levels<ZpyrBody<1>>(zt, 0, L - 1, true);
 }
 
 void adapt_prefix(Sim& s, Grid& g, AdaptState& a, const LvTab& tab) {
