@@ -124,15 +124,6 @@ __global__ void k_norms(const long long* __restrict__ dn, const double* __restri
   }
 }
 
-// Piecewise-constant representation after an adapt (solver_adaptive.cpp:157-164)
-__global__ void k_zero_slopes(long long n, double* __restrict__ z, double* __restrict__ u) {
-  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  z[3 * k + 1] = z[3 * k + 2] = 0.0;
-  u[9 * k + 1] = u[9 * k + 2] = 0.0;
-  u[9 * k + 4] = u[9 * k + 5] = 0.0;
-  u[9 * k + 7] = u[9 * k + 8] = 0.0;
-}
 
 struct ZpTab {
   const double* zp[16];
@@ -192,6 +183,14 @@ constexpr uint64_t kSmallNodes = FM_SMALL_NODES;
 #endif
 constexpr int kMaxLv = 16;
 
+struct Install {
+  int8_t* lvl;
+  int32_t* li;
+  int32_t* lj;
+  double* z;
+  const double* gz;  // the grid's leaf topography
+};
+
 struct LvTab {
   int L, M, N;
   uint8_t* known[kMaxLv + 1];
@@ -207,6 +206,8 @@ struct LvTab {
   double* unew;
   const double* z;  // leaf topography (3 per leaf, device order)
   int zero_slopes;  // HWFV1: the leaves' z planes are taken with zero slopes
+  int do_install;   // k_transfer_leaves also installs the leaf set (inst)
+  Install inst;
   __host__ __device__ uint64_t nodes(int l) const { return uint64_t(M) * N << (2 * l); }
 };
 
@@ -342,6 +343,20 @@ __global__ void __launch_bounds__(256) k_transfer_leaves(LvTab t, long long n, c
     }
   }
   double* o = t.unew + 9 * k;
+  if (t.do_install) {
+    // the sim takes the new leaf set in the same pass (copy_leaves_from_grid)
+    // and, for FV1, the piecewise-constant representation
+    // (solver_adaptive.cpp:157-164: slopes of U and z zeroed)
+    const double* zg = t.inst.gz + 3 * k;
+    double* zo = t.inst.z + 3 * k;
+    t.inst.lvl[k] = int8_t(l);
+    t.inst.li[k] = li[k];
+    t.inst.lj[k] = lj[k];
+    zo[0] = zg[0];
+    zo[1] = t.zero_slopes ? 0.0 : zg[1];
+    zo[2] = t.zero_slopes ? 0.0 : zg[2];
+    if (t.zero_slopes) v[1] = v[2] = v[4] = v[5] = v[7] = v[8] = 0.0;
+  }
 #pragma unroll
   for (int q = 0; q < 9; ++q) o[q] = v[q];
 }
@@ -362,7 +377,7 @@ struct ZpyrBody {
         s = t.z + 3 * (l + 1 < L ? t.off[l + 1][ch] : t.off[l][n] + c);
       else
         s = t.zp[l + 1] + 3 * ch;
-      // FV1 leaves carry zero topography slopes (k_zero_slopes, +0 exactly)
+      // FV1 leaves carry zero topography slopes (set by the transfer, +0 exactly)
       kids[c] = (leaf && t.zero_slopes) ? P3{s[0], 0.0, 0.0} : P3{s[0], s[1], s[2]};
     }
     const P3 p = encode_parent_k<KIND>(kids);
@@ -452,19 +467,6 @@ LvTab lv_tab(Sim& s, Grid& g, AdaptState& a) {
   t.eps = a.eps;
   t.z = s.z.p;
   return t;
-}
-
-void copy_leaves_from_grid(Sim& s, const Grid& g) {
-  cudaStream_t st = stream();
-  s.n = g.nleaves;
-  s.lvl.ensure(s.n);
-  s.li.ensure(s.n);
-  s.lj.ensure(s.n);
-  s.z.ensure(3 * s.n);
-  FM_CUDA(cudaMemcpyAsync(s.lvl.p, g.lf_l.p, s.n, cudaMemcpyDeviceToDevice, st));
-  FM_CUDA(cudaMemcpyAsync(s.li.p, g.lf_i.p, 4 * s.n, cudaMemcpyDeviceToDevice, st));
-  FM_CUDA(cudaMemcpyAsync(s.lj.p, g.lf_j.p, 4 * s.n, cudaMemcpyDeviceToDevice, st));
-  FM_CUDA(cudaMemcpyAsync(s.z.p, g.lf_z.p, 24 * s.n, cudaMemcpyDeviceToDevice, st));
 }
 
 // remap_after_adapt + rebuild_topology + encode_pairing partners
@@ -734,7 +736,6 @@ void adaptive_adapt(Sim& s, double t) {
   PhaseClock pc(st);
   Grid& g = *s.grid;
   AdaptState& a = *s.ad;
-  const int L = g.L;
   LvTab tab = lv_tab(s, g, a);
   // everything up to the new leaf list, one graph replay (adapt_prefix),
   // then the new leaf count: the adapt's one host round trip before the
@@ -747,13 +748,22 @@ void adaptive_adapt(Sim& s, double t) {
   g.lf_l.n = g.lf_i.n = g.lf_j.n = size_t(n_dev);
   g.lf_z.n = 3 * size_t(n_dev);
   pc.mark("prefix");
-  // transfer the flow onto the new leaves
-  // the new state goes into the U* scratch, which then becomes U (no
-  // allocation per adapt: the buffers only grow)
+  // transfer the flow onto the new leaves, straight into U (the old leaves'
+  // rows are in the encode-up pyramid since the prefix), and install the
+  // new leaf set into the sim in the same pass; buffers only grow
   const int64_t n_new = g.nleaves;
+  s.u.ensure(9 * n_new);
   s.us.ensure(9 * n_new);
+  s.n = n_new;
+  s.lvl.ensure(s.n);
+  s.li.ensure(s.n);
+  s.lj.ensure(s.n);
+  s.z.ensure(3 * s.n);
   tab = lv_tab(s, g, a);
-  tab.unew = s.us.p;
+  tab.unew = s.u.p;
+  tab.do_install = 1;
+  tab.inst = Install{s.lvl.p, s.li.p, s.lj.p, s.z.p, g.lf_z.p};
+  tab.zero_slopes = s.scheme != FM_DG2 ? 1 : 0;
   if (n_new) {
     if (a.kind == 0)
       k_transfer_leaves<0><<<nblk(n_new, 256), 256, 0, st>>>(tab, n_new, g.lf_l.p, g.lf_i.p, g.lf_j.p);
@@ -762,15 +772,6 @@ void adaptive_adapt(Sim& s, double t) {
     FM_LAUNCHED();
   }
   pc.mark("transfer");
-  // U keeps its allocation (the prefix graph reads it): copy the new state in
-  s.u.ensure(9 * n_new);
-  FM_CUDA(cudaMemcpyAsync(s.u.p, s.us.p, 9 * size_t(n_new) * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  copy_leaves_from_grid(s, g);
-  if (s.scheme != FM_DG2) {
-    k_zero_slopes<<<nblk(s.n, 256), 256, 0, st>>>(s.n, s.z.p, s.u.p);
-    FM_LAUNCHED();
-  }
-  pc.mark("copy");
   refresh_topology(s);
   pc.mark("topology");
   s.fv1_in_star = false;
