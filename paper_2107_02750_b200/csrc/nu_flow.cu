@@ -459,7 +459,15 @@ __global__ void __launch_bounds__(256) k_acc_faces(NuView v, DevClock* clk, DevR
                                                   const double* __restrict__ czc,
                                                   double* __restrict__ q, int manual, double mdt) {
   constexpr int S = FM_ACC_SPT;
-  const long long s0 = blockIdx.x * (long long)(S * blockDim.x) + threadIdx.x;
+  // blocks in reverse order (FM_ACC_REV): the leaf kernel that follows walks
+  // the leaves forward, so the discharges written last -- the low segments,
+  // owned by the low leaves -- are the first it gathers, still in L2; and this
+  // kernel gathers the depths the previous leaf kernel wrote last first
+#ifndef FM_ACC_REV
+#define FM_ACC_REV 1
+#endif
+  const long long blk = FM_ACC_REV ? (long long)gridDim.x - 1 - blockIdx.x : (long long)blockIdx.x;
+  const long long s0 = blk * (long long)(S * blockDim.x) + threadIdx.x;
   int go;
   double dt;
   step_head(v, clk, red, hy, manual, mdt, go, dt);

@@ -38,6 +38,7 @@
 
 #include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <string>
 
 #include <cub/device/device_select.cuh>
@@ -118,7 +119,13 @@ struct ShmHeader {
   int pad;
 };
 constexpr size_t kShmReduce = 64;  // bytes per rank in the reduction area
-constexpr size_t kShmBytes = size_t(256) << 20;
+// segment size: 32 MB by default (a container's /dev/shm is often 64 MB), or
+// $FM_HOST_COMM_MB; each (src, dst) slot gets 1 / nranks^2 of it
+static size_t shm_bytes() {
+  const char* e = std::getenv("FM_HOST_COMM_MB");
+  const long mb = e ? std::atol(e) : 32;
+  return size_t(mb > 0 ? mb : 32) << 20;
+}
 
 struct Comm {
   int kind = COMM_LOCAL;
@@ -128,6 +135,7 @@ struct Comm {
   // host transport
   std::string shm_name;
   void* shm = nullptr;
+  size_t shm_size = 0;
   size_t slot_bytes = 0;
   std::vector<double> stage;  // host staging of the packed send buffer
   ShmHeader* hdr() const { return static_cast<ShmHeader*>(shm); }
@@ -168,15 +176,17 @@ Comm* comm_create_host(int nranks, int rank, const char* name) {
   c->shm_name = name;
   const int fd = shm_open(name, O_CREAT | O_RDWR, 0600);
   if (fd < 0) throw Error(FM_ERR_IO, std::string("host comm: shm_open failed for ") + name);
-  if (ftruncate(fd, off_t(kShmBytes)) != 0) {
+  const size_t bytes = shm_bytes();
+  if (ftruncate(fd, off_t(bytes)) != 0) {
     close(fd);
     throw Error(FM_ERR_IO, "host comm: ftruncate failed");
   }
-  void* p = mmap(nullptr, kShmBytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
   close(fd);
   if (p == MAP_FAILED) throw Error(FM_ERR_IO, "host comm: mmap failed");
   c->shm = p;
-  c->slot_bytes = ((kShmBytes - 64 - kShmReduce * nranks) / (size_t(nranks) * nranks)) & ~size_t(63);
+  c->shm_size = bytes;
+  c->slot_bytes = ((bytes - 64 - kShmReduce * nranks) / (size_t(nranks) * nranks)) & ~size_t(63);
   shm_barrier(*c);  // every rank has the segment mapped (a fresh one is zero-filled)
   return c.release();
 }
@@ -243,7 +253,7 @@ void comm_destroy(Comm* c) {
   if (!c) return;
   if (c->kind == COMM_NCCL && c->nc) nccl().CommDestroy(c->nc);
   if (c->kind == COMM_HOST && c->shm) {
-    munmap(c->shm, kShmBytes);
+    munmap(c->shm, c->shm_size);
     if (c->rank == 0) shm_unlink(c->shm_name.c_str());
   }
   for (Sim* s : c->members)
@@ -811,7 +821,8 @@ static void host_exchange(Sim& s, double* arr, int w) {
   FM_CUDA(cudaStreamSynchronize(stream()));
   for (size_t k = 0; k < sh.peers.size(); ++k) {
     const size_t bytes = size_t(sh.scnt[k]) * w * 8;
-    if (bytes > c.slot_bytes) throw Error(FM_ERR_OTHER, "host comm: halo slice larger than a slot");
+    if (bytes > c.slot_bytes)
+      throw Error(FM_ERR_OTHER, "host comm: halo slice larger than a slot (raise $FM_HOST_COMM_MB)");
     if (bytes) std::memcpy(c.slot(sh.rank, sh.peers[k]), c.stage.data() + size_t(w) * sh.soff[k], bytes);
   }
   shm_barrier(c);
