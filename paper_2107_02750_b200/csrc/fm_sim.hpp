@@ -155,6 +155,7 @@ struct Sim {
   double last_run_ms = 0.0;
   // Manning raster (kept for adaptive remaps)
   DBuf<double> mr;
+  const double* mr_ext = nullptr;  // the caller's raster, read in place during creation only
   int mr_ncols = 0, mr_nrows = 0;
   double mr_xll = 0, mr_yll = 0, mr_cs = 1, manning = 0;
   bool has_mr = false;

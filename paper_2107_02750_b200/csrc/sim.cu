@@ -193,7 +193,28 @@ void common_params(Sim& s, const fm_sim_desc* d) {
     s.mr_xll = m->xll;
     s.mr_yll = m->yll;
     s.mr_cs = m->cellsize;
-    if (m->on_device) {
+    // A static non-uniform sim samples the raster once per leaf at creation
+    // (solver_nonuniform.cpp:575-584) and never again: a raster already
+    // reachable from the device -- device memory, or page-locked host memory
+    // through its mapped pointer (zero-copy: ~2 leaf lookups per cell row
+    // cross PCIe instead of the whole raster) -- is read in place.  Adaptive
+    // sims re-sample it at every adapt and uniform sims read every cell, so
+    // they keep a device copy.
+    const bool once = !s.uniform && !s.adaptive;
+    const double* dp = nullptr;
+    if (once && m->on_device) {
+      dp = m->values;
+    } else if (once) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, m->values) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+          at.devicePointer)
+        dp = static_cast<const double*>(at.devicePointer);
+      else
+        cudaGetLastError();  // pageable memory: not an error
+    }
+    if (dp) {
+      s.mr_ext = dp;
+    } else if (m->on_device) {
       s.mr.alloc(size_t(m->ncols) * m->nrows);
       FM_CUDA(cudaMemcpyAsync(s.mr.p, m->values, s.mr.n * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
     } else {
@@ -330,17 +351,18 @@ Sim* sim_create(const fm_sim_desc* d, const fm_raster* dem, const Grid* grid) {
   if (!d || !dem) throw Error(FM_ERR_CONFIG, "null descriptor or DEM");
   upload_banks();
   auto s = std::make_unique<Sim>();
+  s->adaptive = d->solver == FM_MWDG2 || d->solver == FM_HWFV1;
+  s->uniform = !s->adaptive && !grid;
   common_params(*s, d);
-  if (d->solver == FM_MWDG2 || d->solver == FM_HWFV1) {
-    s->adaptive = true;
+  if (s->adaptive) {
     adaptive_init(*s, d, dem);
   } else if (grid) {
     nonuniform_init(*s, d, dem, *grid);
   } else {
-    s->uniform = true;
     uniform_init(*s, d, dem);
   }
   FM_CUDA(cudaStreamSynchronize(stream()));
+  s->mr_ext = nullptr;  // the caller's raster: not referenced after creation
   return s.release();
 }
 

@@ -354,7 +354,7 @@ void resolve_inflows(Sim& s, const Grid& g) {
 
 void resolve_manning(Sim& s) {
   k_manning<<<nblk(s.n, 256), 256, 0, stream()>>>(
-      s.n, s.L, s.R, s.x0, s.y0, s.lvl.p, s.li.p, s.lj.p, s.has_mr ? s.mr.p : nullptr, s.mr_ncols,
+      s.n, s.L, s.R, s.x0, s.y0, s.lvl.p, s.li.p, s.lj.p, s.has_mr ? (s.mr_ext ? s.mr_ext : s.mr.p) : nullptr, s.mr_ncols,
       s.mr_nrows, s.mr_xll, s.mr_yll, s.mr_cs, s.manning, s.nman.p);
   FM_LAUNCHED();
 }

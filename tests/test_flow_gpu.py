@@ -348,3 +348,23 @@ def test_resume_rejects_another_scenario_or_leaf_set(gpu, tmp_path):
     with pytest.raises(FmError) as e:
         make(gpu, sc).resume(tmp_path / "missing.fmck")
     assert e.value.code == 3
+
+
+def test_manning_raster_read_in_place_when_pinned(gpu):
+    """A static sim samples its Manning raster once at creation; from
+    page-locked host memory it reads it in place (zero-copy) instead of
+    uploading it.  Same trajectory bits as from pageable memory."""
+    import dataclasses
+
+    import torch
+    sc = S.config4(16)
+    g = gpu.grid(sc.dem, sc.L, sc.eps)
+    a = gpu.sim(sc, g)
+    t = torch.zeros(sc.manning_raster.values.shape, dtype=torch.float64, pin_memory=True)
+    t.numpy()[...] = sc.manning_raster.values
+    scp = dataclasses.replace(sc, manning_raster=dataclasses.replace(sc.manning_raster, values=t.numpy()))
+    b = gpu.sim(scp, g)
+    del t  # the sim keeps no reference to the caller's raster
+    a.run(12, gauge_interval=10.0)
+    b.run(12, gauge_interval=10.0)
+    assert np.array_equal(a.download()[3], b.download()[3])
