@@ -478,6 +478,7 @@ void refresh_topology(Sim& s) {
   resolve_manning(s);
   resolve_inflows(s, g);
   build_topology(s, g);
+  build_seg_z(s);
   // the partner values from the z encode-up pyramid (built in the adapt's
   // prefix graph, right after the leaf list)
   const int L = s.L;

@@ -66,6 +66,7 @@ struct NuView {
   const int32_t* seg_l;
   const int32_t* seg_r;
   const uint8_t* seg_geo;  // per segment: x-normal + limit-point offsets (k_seg_geo)
+  const double2* segz;     // P2: per segment, both leaves' z at its centre (k_seg_z)
   const int32_t* sid;   // 8 per leaf: segment ids of the sub-faces per side
   const double* segst;  // 6 per segment: HLL flux (m n t), z*, h*L, h*R
   long long nseg;
@@ -120,6 +121,7 @@ struct Sim {
   DBuf<double> u, us, z, nman, zpair;
   DBuf<int32_t> nb, sid, seg_l, seg_r;
   DBuf<uint8_t> sk, seg_geo;
+  DBuf<double> segz;        // P2: 2 per segment (static topography limits)
   DBuf<double> segst;       // DG2/FV1 segment states (6 per segment)
   DBuf<double> accq, accqb;  // ACC: per segment, per leaf-side (4 per leaf)
   DBuf<double> aqx, aqy;     // uniform ACC faces
@@ -257,6 +259,7 @@ void group_run(const std::vector<Sim*>& sims, fm_clock* clk, int64_t max_steps, 
 // topology (topo.cu)
 void build_topology(Sim& s, const Grid& g);
 void build_seg_geo(Sim& s);  // after seg_l / seg_r and the leaf keys are final
+void build_seg_z(Sim& s);    // after build_seg_geo and the final topography z
 void resolve_inflows(Sim& s, const Grid& g);
 void resolve_manning(Sim& s);
 int64_t scan_exclusive(const int32_t* in, int32_t* out, int64_t n);

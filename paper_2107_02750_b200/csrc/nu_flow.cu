@@ -119,7 +119,10 @@ __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClo
   double sa[9], sb[9];
   load_row<W>(in, a, sa);
   load_row<W>(in, b, sb);
-  const P3 za = load3v(v.z, a), zb = load3v(v.z, b);
+  // P2: the static topography limits at the segment centre (k_seg_z) in one
+  // 16 B load instead of both leaves' z rows and two plane evaluations
+  const double2 zz = P2 ? v.segz[q] : make_double2(0.0, 0.0);
+  const P3 za = P2 ? P3{0.0, 0.0, 0.0} : load3v(v.z, a), zb = P2 ? P3{0.0, 0.0, 0.0} : load3v(v.z, b);
   Pt A, B;
   bool xn;
   if (P2) {
@@ -134,8 +137,8 @@ __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClo
     const double tb = cb == 0 ? 0.0 : cb == 2 ? 0.25 : -0.25;
     // one evaluation path for the x- and y-normal segments that interleave in
     // a warp: select the offsets, not the call
-    A = limit_rel(sa, za, xn ? 0.5 : ta, xn ? ta : 0.5, v.hdry);
-    B = limit_rel(sb, zb, xn ? -0.5 : tb, xn ? tb : -0.5, v.hdry);
+    A = limit_rel_z(sa, zz.x, xn ? 0.5 : ta, xn ? ta : 0.5, v.hdry);
+    B = limit_rel_z(sb, zz.y, xn ? -0.5 : tb, xn ? tb : -0.5, v.hdry);
   } else {
     const int la = v.lvl[a], lb = v.lvl[b];
     const int ia = v.li[a], ja = v.lj[a], ib = v.li[b], jb = v.lj[b];

@@ -693,6 +693,7 @@ Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* gr
     FM_LAUNCHED();
   }
   build_seg_geo(s);
+  build_seg_z(s);
   s.infc.alloc(std::max<int64_t>(1, int64_t(s.ninflow) * count));
   if (s.ninflow == 0) s.infc.zero();
   for (int f = 0; f < s.ninflow; ++f)

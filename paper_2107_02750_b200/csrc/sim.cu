@@ -155,6 +155,7 @@ NuView Sim::view() const {
   v.seg_l = seg_l.p;
   v.seg_r = seg_r.p;
   v.seg_geo = seg_geo.p;
+  v.segz = reinterpret_cast<const double2*>(segz.p);
   v.sid = sid.p;
   v.segst = segst.p;
   v.nseg = nseg;
@@ -320,6 +321,7 @@ static void nonuniform_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem, 
   }
   k_ic_finish<<<nblk(n, 256), 256, 0, st>>>(n, s.scheme != FM_DG2, s.hdry, s.z.p, s.u.p);
   FM_LAUNCHED();
+  build_seg_z(s);  // the topography is final now (FV1 / ACC: z slopes zeroed)
   for (int f = 0; f < s.ninflow; ++f) {
     const int* r = &s.rect[4 * f];
     if (r[0] < 0 || r[1] < 0 || r[2] >= (s.M << s.L) || r[3] >= (s.N << s.L))

@@ -42,6 +42,17 @@ __device__ __forceinline__ Pt limit(const double s[9], const P3& zc, double cx, 
 __device__ __forceinline__ double eval_rel(double c0, double cx, double cy, double rx, double ry) {
   return c0 + cx * 2.0 * kS3 * rx + cy * 2.0 * kS3 * ry;
 }
+// limit_rel with the topography's value at the point already known (static)
+__device__ __forceinline__ Pt limit_rel_z(const double s[9], double z, double rx, double ry, double hdry) {
+  Pt p;
+  p.h = smax(0.0, eval_rel(s[0], s[1], s[2], rx, ry));
+  p.qx = eval_rel(s[3], s[4], s[5], rx, ry);
+  p.qy = eval_rel(s[6], s[7], s[8], rx, ry);
+  p.z = z;
+  p.eta = p.h + p.z;
+  vel2(p.h, p.qx, p.qy, hdry, p.u, p.v);
+  return p;
+}
 __device__ __forceinline__ Pt limit_rel(const double s[9], const P3& zc, double rx, double ry,
                                         double hdry) {
   Pt p;

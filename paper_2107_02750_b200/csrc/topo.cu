@@ -16,6 +16,7 @@
 // enumerate_faces (quadgrid.cpp:206-208).
 #include "fm_device.cuh"
 #include "fm_sim.hpp"
+#include "step_common.cuh"
 
 using namespace fmd;
 
@@ -163,6 +164,26 @@ __global__ void k_seg_geo(long long nseg, int L, const int32_t* __restrict__ seg
   geo[q] = uint8_t((xn ? 1 : 0) | (ta << 1) | (tb << 3));
 }
 
+// Static topography limits of every segment (P2 geometry): z of each leaf's
+// plane at the segment centre, evaluated exactly as k_seg's limit_rel would
+// (limit_at, solver_nonuniform.cpp:52-66): the topography never changes on a
+// static grid, so k_seg reads these 16 B instead of both leaves' z rows.
+__global__ void k_seg_z(long long nseg, const int32_t* __restrict__ seg_l, const int32_t* __restrict__ seg_r,
+                        const uint8_t* __restrict__ geo, const double* __restrict__ z, double2* __restrict__ out) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= nseg) return;
+  const int a = seg_l[q], b = seg_r[q];
+  const int gc = geo[q];
+  const bool xn = gc & 1;
+  const int ca = (gc >> 1) & 3, cb = (gc >> 3) & 3;
+  const double ta = ca == 0 ? 0.0 : ca == 2 ? 0.25 : -0.25;
+  const double tb = cb == 0 ? 0.0 : cb == 2 ? 0.25 : -0.25;
+  const double* za = z + 3 * (long long)a;
+  const double* zb = z + 3 * (long long)b;
+  out[q] = make_double2(eval_rel(za[0], za[1], za[2], xn ? 0.5 : ta, xn ? ta : 0.5),
+                        eval_rel(zb[0], zb[1], zb[2], xn ? -0.5 : tb, xn ? tb : -0.5));
+}
+
 // --- scan -----------------------------------------------------------------
 __global__ void k_block_sums(const int32_t* __restrict__ in, long long n,
                              long long* __restrict__ sums) {
@@ -303,6 +324,16 @@ void build_seg_geo(Sim& s) {
   if (s.nseg) {
     k_seg_geo<<<nblk(s.nseg, 256), 256, 0, stream()>>>(s.nseg, s.L, s.seg_l.p, s.seg_r.p, s.lvl.p, s.li.p,
                                                       s.lj.p, s.seg_geo.p);
+    FM_LAUNCHED();
+  }
+}
+
+// after the topography is final (initial conditions zero FV1/ACC's z slopes)
+void build_seg_z(Sim& s) {
+  if (s.nseg && s.p2) {
+    s.segz.ensure(2 * size_t(s.nseg));
+    k_seg_z<<<nblk(s.nseg, 256), 256, 0, stream()>>>(s.nseg, s.seg_l.p, s.seg_r.p, s.seg_geo.p, s.z.p,
+                                                    reinterpret_cast<double2*>(s.segz.p));
     FM_LAUNCHED();
   }
 }
