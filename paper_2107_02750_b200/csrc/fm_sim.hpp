@@ -67,6 +67,7 @@ struct NuView {
   const int32_t* seg_r;
   const uint8_t* seg_geo;  // per segment: x-normal + limit-point offsets (k_seg_geo)
   const double2* segz;     // P2: per segment, both leaves' z at its centre (k_seg_z)
+  const double* zside;     // P2: per leaf, z at its four side midpoints N E S W (k_seg_z)
   const int32_t* sid;   // 8 per leaf: segment ids of the sub-faces per side
   const double* segst;  // 6 per segment: HLL flux (m n t), z*, h*L, h*R
   long long nseg;
@@ -122,6 +123,7 @@ struct Sim {
   DBuf<int32_t> nb, sid, seg_l, seg_r;
   DBuf<uint8_t> sk, seg_geo;
   DBuf<double> segz;        // P2: 2 per segment (static topography limits)
+  DBuf<double> zside;       // P2: 4 per leaf (static topography side limits)
   DBuf<double> segst;       // DG2/FV1 segment states (6 per segment)
   DBuf<double> accq, accqb;  // ACC: per segment, per leaf-side (4 per leaf)
   DBuf<double> aqx, aqy;     // uniform ACC faces

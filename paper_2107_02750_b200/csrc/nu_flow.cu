@@ -237,10 +237,12 @@ __device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9],
   double sl[9];
 #pragma unroll
   for (int q = 0; q < 9; ++q) sl[q] = lrow[q];
+  // P2: the leaf's static topography limit on this side (k_seg_z's zside,
+  // in lrow[9 + sd]) instead of its z plane evaluated here
   const P3 zl{lrow[9], lrow[10], lrow[11]};
-  const Pt me = P2 ? limit_rel(sl, zl, ox, oy, v.hdry) : limit(sl, zl, cx, cy, sz, fx, fy, v.hdry);
+  const Pt me = P2 ? limit_rel_z(sl, lrow[9 + sd], ox, oy, v.hdry) : limit(sl, zl, cx, cy, sz, fx, fy, v.hdry);
 #else
-  const Pt me = P2 ? limit_rel(s, zc, ox, oy, v.hdry) : limit(s, zc, cx, cy, sz, fx, fy, v.hdry);
+  const Pt me = P2 ? limit_rel_z(s, v.zside[4 * kk + sd], ox, oy, v.hdry) : limit(s, zc, cx, cy, sz, fx, fy, v.hdry);
 #endif
   const double w = kind == 3 ? 0.5 : 1.0;
   double zstar;
@@ -312,16 +314,33 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   const int l = v.lvl[kk], i = v.li[kk], j = v.lj[kk];
   double s[9];
   load_row<W>(in, kk, s);
-  const P3 zc = load3v(v.z, kk);
+  // P2: the four static side limits of the topography (N E S W, k_seg_z);
+  // otherwise the z plane
+  P3 zc{0.0, 0.0, 0.0};
+  double2 zs01 = make_double2(0.0, 0.0), zs23 = make_double2(0.0, 0.0);
+  if (P2) {
+    const double2* zp = reinterpret_cast<const double2*>(v.zside + 4 * kk);
+    zs01 = zp[0];
+    zs23 = zp[1];
+  } else {
+    zc = load3v(v.z, kk);
+  }
   const int code = v.sk[kk];
 #if FM_STAGE_SROW
   __shared__ double srow_all[FM_STAGE_THREADS * 13];  // 13-double stride: conflict-free
   volatile double* lrow = srow_all + 13 * threadIdx.x;
 #pragma unroll
   for (int q = 0; q < 9; ++q) lrow[q] = s[q];
-  lrow[9] = zc.c0;
-  lrow[10] = zc.cx;
-  lrow[11] = zc.cy;
+  if (P2) {
+    lrow[9] = zs01.x;
+    lrow[10] = zs01.y;
+    lrow[11] = zs23.x;
+    lrow[12] = zs23.y;
+  } else {
+    lrow[9] = zc.c0;
+    lrow[10] = zc.cx;
+    lrow[11] = zc.cy;
+  }
 #else
   const volatile double* lrow = nullptr;
 #endif

@@ -156,6 +156,7 @@ NuView Sim::view() const {
   v.seg_r = seg_r.p;
   v.seg_geo = seg_geo.p;
   v.segz = reinterpret_cast<const double2*>(segz.p);
+  v.zside = zside.p;
   v.sid = sid.p;
   v.segst = segst.p;
   v.nseg = nseg;

@@ -184,6 +184,18 @@ __global__ void k_seg_z(long long nseg, const int32_t* __restrict__ seg_l, const
                         eval_rel(zb[0], zb[1], zb[2], xn ? -0.5 : tb, xn ? tb : -0.5));
 }
 
+// ... and of every leaf side: z of the leaf's plane at its side midpoints
+// (N E S W), as k_stage's side evaluation (limit_rel at (0, 1/2), (1/2, 0),
+// (0, -1/2), (-1/2, 0)) would compute it.
+__global__ void k_side_z(long long n, const double* __restrict__ z, double* __restrict__ out) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double* p = z + 3 * k;
+  double2* o = reinterpret_cast<double2*>(out + 4 * k);
+  o[0] = make_double2(eval_rel(p[0], p[1], p[2], 0.0, 0.5), eval_rel(p[0], p[1], p[2], 0.5, 0.0));
+  o[1] = make_double2(eval_rel(p[0], p[1], p[2], 0.0, -0.5), eval_rel(p[0], p[1], p[2], -0.5, 0.0));
+}
+
 // --- scan -----------------------------------------------------------------
 __global__ void k_block_sums(const int32_t* __restrict__ in, long long n,
                              long long* __restrict__ sums) {
@@ -330,6 +342,11 @@ void build_seg_geo(Sim& s) {
 
 // after the topography is final (initial conditions zero FV1/ACC's z slopes)
 void build_seg_z(Sim& s) {
+  if (s.p2 && s.n) {
+    s.zside.ensure(4 * size_t(s.n));
+    k_side_z<<<nblk(s.n, 256), 256, 0, stream()>>>(s.n, s.z.p, s.zside.p);
+    FM_LAUNCHED();
+  }
   if (s.nseg && s.p2) {
     s.segz.ensure(2 * size_t(s.nseg));
     k_seg_z<<<nblk(s.nseg, 256), 256, 0, stream()>>>(s.nseg, s.seg_l.p, s.seg_r.p, s.seg_geo.p, s.z.p,
