@@ -96,6 +96,54 @@ __global__ void __launch_bounds__(256) k_head_friction(NuView v, DevClock* clk, 
   }
 }
 
+// The DG2 head in place with FM_HEAD_LPT leaves per thread (strided by the
+// block size, so the loads stay coalesced), every row's three values and
+// Manning n loaded before the friction chains (A/B on B200, config 4: the
+// former head 0.062 ms; this kernel 0.053 / 0.055 / 0.056 ms at 1 / 2 / 4
+// leaves per thread).
+#ifndef FM_HEAD_LPT
+#define FM_HEAD_LPT 1
+#endif
+__global__ void __launch_bounds__(256) k_head_fric_ip(NuView v, DevClock* clk, DevRed* red, const Hydro* hy,
+                                                     double* __restrict__ u, int manual, double mdt) {
+  constexpr int P = FM_HEAD_LPT;
+  const long long k0 = blockIdx.x * (long long)(P * blockDim.x) + threadIdx.x;
+  int go;
+  double dt;
+  step_head(v, clk, red, hy, manual, mdt, go, dt);
+  if (!go) return;
+  double h[P], a[P], b[P], nm[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const long long k = k0 + j * (long long)blockDim.x;
+    const long long kc = k < v.n ? k : v.n - 1;
+    h[j] = u[9 * kc];
+    a[j] = u[9 * kc + 3];
+    b[j] = u[9 * kc + 6];
+    nm[j] = v.nman[kc];
+  }
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const long long k = k0 + j * (long long)blockDim.x;
+    if (k >= v.n) continue;
+    double* o = u + 9 * k;
+    if (h[j] <= v.hdry) {
+#pragma unroll
+      for (int q = 3; q < 9; ++q) o[q] = 0.0;
+      continue;
+    }
+    double s[9];
+    s[0] = h[j];
+    s[3] = a[j];
+    s[6] = b[j];
+    friction(s, nm[j], v.g, v.hdry, dt, v.libm);
+    if (s[3] != a[j] || s[6] != b[j]) {  // bit-level: friction changed them
+      o[3] = s[3];
+      o[6] = s[6];
+    }
+  }
+}
+
 // ---- segment states ------------------------------------------------------
 // One thread per interior segment (segment_states, solver_nonuniform.cpp:91-115):
 // both leaves' limits at the segment centre, z* = max(zL, zR), the starred
@@ -843,9 +891,12 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       if (c3)
         launch_k(k_head_friction<3>, nblk(n, 256), 256, st, v, clk, red, (const Hydro*)s.hydro.p,
                  (const double*)s.cs3.p, s.cu3.p, (int)manual, mdt);
+      else if (!fv1)  // DG2: in place
+        launch_k(k_head_fric_ip, nblk(n, 256 * FM_HEAD_LPT), 256, st, v, clk, red, (const Hydro*)s.hydro.p, s.u.p,
+                 (int)manual, mdt);
       else
         launch_k(k_head_friction<9>, nblk(n, 256), 256, st, v, clk, red, (const Hydro*)s.hydro.p,
-                 (const double*)(fv1 ? s.us.p : s.u.p), s.u.p, (int)manual, mdt);
+                 (const double*)s.us.p, s.u.p, (int)manual, mdt);
       FM_LAUNCHED();
       kt_end();
       break;
