@@ -948,8 +948,12 @@ void launch_decide(Sim& s) {
 
 void launch_head_friction(Sim& s, const double* src, double* dst, bool manual, double mdt) {
   kt_begin(s.uniform ? KF_UNI_HEAD : KF_HEAD);
-  k_head_friction<9><<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.hydro.p, src,
-                                                            dst, manual, mdt);
+  if (src == dst)  // DG2: in place
+    k_head_fric_ip<<<nblk(s.n, 256 * FM_HEAD_LPT), 256, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.hydro.p, dst,
+                                                                       manual, mdt);
+  else
+    k_head_friction<9><<<nblk(s.n, 256), 256, 0, stream()>>>(s.view(), s.clk.p, s.red.p, s.hydro.p, src,
+                                                              dst, manual, mdt);
   FM_LAUNCHED();
   kt_end();
 }
