@@ -11,7 +11,7 @@
 //   flag         (:59-73)   also flags the node (static topography significance
 //                           precomputed once: max(a,b) >= eps <=> a >= eps || b >= eps)
 //   closure      (detail_tree.cpp:56-64) and closes it over its children
-//   buffer_ring  (:75-94)   RingBody, then closure again
+//   buffer_ring  (:75-94)   inside grade_count_levels (ring = tmp)
 //   grade_flags  (detail_tree.cpp:97-113) + leaf counts: grade_count_levels
 //   assemble_grid(detail_tree.cpp:132-164): build_leaves (topography decode)
 //   transfer     (:96-134)  k_transfer_leaves: one thread per new leaf walks
@@ -279,28 +279,6 @@ struct EncodeFlagBody {
 
 // buffer_ring, one level: dilate to the same-level 8-neighbourhood (:75-94),
 // from the closed flags (tmp) into the grid's flags
-struct RingBody {
-  __device__ static void node(int l, uint64_t n, const LvTab& t) {
-    const uint8_t* flag = t.tmp[l];
-    uint8_t f = flag[n];
-    if (!f) {
-      int i, j;
-      node_ij(l, n, t.M, i, j);
-      const int w = t.M << l, h = t.N << l;
-      for (int dj = -1; dj <= 1 && !f; ++dj)
-        for (int di = -1; di <= 1; ++di) {
-          const int ni = i + di, nj = j + dj;
-          if (ni < 0 || nj < 0 || ni >= w || nj >= h) continue;
-          if (flag[node_index(l, ni, nj, t.M)]) {
-            f = 1;
-            break;
-          }
-        }
-    }
-    t.flag[l][n] = f;
-  }
-};
-
 // transfer as a walk per NEW leaf (one launch instead of one per level):
 // from the level-0 scaling down the leaf's ancestor chain, decoding at each
 // ancestor only the child on the path, with the stored flow details where the
@@ -650,13 +628,16 @@ void launch_prefix(Sim& s, Grid& g, AdaptState& a, const LvTab& tab) {
     run_levels<EncodeFlagBody<0>>(tab, 0, L - 1, true);
   else
     run_levels<EncodeFlagBody<1>>(tab, 0, L - 1, true);
-  // buffer_ring (tmp -> the grid's flags); its ancestor closure is subsumed
-  // by the grading pass: the gather form of grade_flags sets
-  // G(l) = F(l) | any child G(l+1) | ring, bottom-up, so G(closure(F)) = G(F)
-  // level by level (the closure's child term is contained in G's)
-  run_levels_flat<RingBody>(tab, 0, L - 1);
+  // buffer_ring (tmp -> the grid's flags) is taken inside the grading pass
+  // (each node's own flag = the ring dilation of tmp at its level); its
+  // ancestor closure is subsumed by grading: the gather form of grade_flags
+  // sets G(l) = F(l) | any child G(l+1) | ring, bottom-up, so
+  // G(closure(F)) = G(F) level by level (the closure's child term is
+  // contained in G's)
+  std::vector<const uint8_t*> ring(L);
+  for (int l = 0; l < L; ++l) ring[l] = a.tmp[l].p;
   // grade + counts + leaves + exact topography (assemble_grid)
-  grade_count_levels(g, true);
+  grade_count_levels(g, true, &ring);
   build_leaves_device(g, a.dn.p + 1);
   // region_topo (solver_nonuniform.cpp:80-89) of every flagged node over the
   // new leaves' topography (the grid's leaf planes; HWFV1 takes them with

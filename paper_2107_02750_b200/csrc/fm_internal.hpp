@@ -158,7 +158,9 @@ Grid* grid_from_leaves(int L, int M, int N, double R, double x0, double y0, int6
                        const int32_t* li, const int32_t* lj, const double* topo3);
 // The stages of mra_static, reused by the adaptive solver.
 void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, double* ms);
-void grade_count_levels(Grid& g, bool graded);
+// ring (optional, per level): take each node's own flag as the same-level
+// 8-neighbour dilation of ring[l] (buffer_ring) instead of g.flag[l]
+void grade_count_levels(Grid& g, bool graded, const std::vector<const uint8_t*>* ring = nullptr);
 // Shared by the static and the adaptive pipelines: from final per-level flags
 // (already in g.flag) compute counts, offsets, then decode topography details
 // top-down into the leaf arrays.  Returns the leaf count.

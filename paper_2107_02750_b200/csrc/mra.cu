@@ -401,10 +401,29 @@ __global__ void k_copy_fine(VertexView vv, const Scalars* __restrict__ s, double
 // edge-adjacent to P's child block, and G(l+1) is final before level l is
 // visited in both formulations.  (Verified against the oracle on random trees
 // in tests/test_mra_gpu.py.)
+// ring (adaptive re-grid): the node's own flag is buffer_ring's dilation
+// (solver_adaptive.cpp:75-94) of the closed flags `ring` of its level, taken
+// here rather than in a separate pass: any flagged node in the same-level
+// 8-neighbourhood (or itself)
+__device__ __forceinline__ int ring_flag(const uint8_t* __restrict__ ring, int l, int M, int N, uint64_t n) {
+  if (ring[n]) return 1;
+  int i, j;
+  node_ij(l, n, M, i, j);
+  const int w = M << l, h = N << l;
+  for (int dj = -1; dj <= 1; ++dj)
+    for (int di = -1; di <= 1; ++di) {
+      const int ni = i + di, nj = j + dj;
+      if (ni < 0 || nj < 0 || ni >= w || nj >= h) continue;
+      if (ring[node_index(l, ni, nj, M)]) return 1;
+    }
+  return 0;
+}
+
 __device__ __forceinline__ void grade_count_node(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
                                                  int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1,
-                                                 int l, int L, int M, int N, uint64_t n, int graded) {
-  int g = fl[n];
+                                                 int l, int L, int M, int N, uint64_t n, int graded,
+                                                 const uint8_t* __restrict__ ring = nullptr) {
+  int g = ring ? ring_flag(ring, l, M, N, n) : fl[n];
   int c = 1;
   if (l + 1 < L) {
     const uint32_t kids = *reinterpret_cast<const uint32_t*>(fl1 + 4 * n);
@@ -437,9 +456,10 @@ __device__ __forceinline__ void grade_count_node(uint8_t* __restrict__ fl, const
 }
 __global__ void k_grade_count(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
                               int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1, int l,
-                              int L, int M, int N, uint64_t nodes, int graded) {
+                              int L, int M, int N, uint64_t nodes, int graded,
+                              const uint8_t* __restrict__ ring = nullptr) {
   const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n < nodes) grade_count_node(fl, fl1, cnt, cnt1, l, L, M, N, n, graded);
+  if (n < nodes) grade_count_node(fl, fl1, cnt, cnt1, l, L, M, N, n, graded, ring);
 }
 
 // The small levels (<= kSmallLevelNodes nodes, all at the coarse end) of the
@@ -447,6 +467,9 @@ __global__ void k_grade_count(uint8_t* __restrict__ fl, const uint8_t* __restric
 // order with a barrier between levels: at the coarse end a launch per level
 // costs more than the level's work.
 constexpr uint64_t kSmallLevelNodes = 256;
+struct RingPtrs {
+  const uint8_t* ring[kMaxL];  // per level, or all null
+};
 struct LevelPtrs {
   uint8_t* fl[kMaxL];
   int32_t* cnt[kMaxL];
@@ -454,12 +477,13 @@ struct LevelPtrs {
   double* zs[kMaxL];  // zs[0] = the level-0 scaling
   const double* det[kMaxL];
 };
-__global__ void __launch_bounds__(256) k_grade_count_small(LevelPtrs p, int lhi, int L, int M, int N, int graded) {
+__global__ void __launch_bounds__(256) k_grade_count_small(LevelPtrs p, int lhi, int L, int M, int N, int graded,
+                                                           RingPtrs r) {
   for (int l = lhi; l >= 0; --l) {
     const uint64_t nodes = uint64_t(M) * N << (2 * l);
     for (uint64_t n = threadIdx.x; n < nodes; n += blockDim.x)
       grade_count_node(p.fl[l], l + 1 < L ? p.fl[l + 1] : nullptr, p.cnt[l], l + 1 < L ? p.cnt[l + 1] : nullptr, l,
-                       L, M, N, n, graded);
+                       L, M, N, n, graded, r.ring[l]);
     __syncthreads();
   }
 }
@@ -879,7 +903,7 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
 
 // Final flags (closure + optional 2:1 grading) and subtree leaf counts, one
 // gather pass per level fine -> coarse (k_grade_count).
-void grade_count_levels(Grid& g, bool graded) {
+void grade_count_levels(Grid& g, bool graded, const std::vector<const uint8_t*>* ring) {
   cudaStream_t st = stream();
   const int L = g.L;
   g.cnt.resize(L);
@@ -891,16 +915,19 @@ void grade_count_levels(Grid& g, bool graded) {
     const uint64_t nodes = g.nodes(l);
     k_grade_count<<<blocks_for(nodes, 256), 256, 0, st>>>(
         g.flag[l].p, l + 1 < L ? g.flag[l + 1].p : nullptr, g.cnt[l].p,
-        l + 1 < L ? g.cnt[l + 1].p : nullptr, l, L, g.M, g.N, nodes, graded ? 1 : 0);
+        l + 1 < L ? g.cnt[l + 1].p : nullptr, l, L, g.M, g.N, nodes, graded ? 1 : 0,
+        ring ? (*ring)[l] : nullptr);
     FM_LAUNCHED();
   }
   if (ls >= 0) {
     LevelPtrs p{};
+    RingPtrs r{};
     for (int l = 0; l < L; ++l) {
       p.fl[l] = g.flag[l].p;
       p.cnt[l] = g.cnt[l].p;
+      r.ring[l] = ring ? (*ring)[l] : nullptr;
     }
-    k_grade_count_small<<<1, 256, 0, st>>>(p, ls, L, g.M, g.N, graded ? 1 : 0);
+    k_grade_count_small<<<1, 256, 0, st>>>(p, ls, L, g.M, g.N, graded ? 1 : 0, r);
     FM_LAUNCHED();
   }
 }
