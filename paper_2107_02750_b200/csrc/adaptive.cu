@@ -33,6 +33,7 @@
 
 #include "fm_device.cuh"
 #include "fm_sim.hpp"
+#include "levels.cuh"
 
 using namespace fmd;
 
@@ -211,68 +212,57 @@ struct LvTab {
   __host__ __device__ uint64_t nodes(int l) const { return uint64_t(M) * N << (2 * l); }
 };
 
-template <int KIND>
-struct EncodeUpBody {
-  __device__ static void node(int l, uint64_t n, const LvTab& t) {
-    uint8_t* kn = t.known[l];
-    // both flags in one round trip
-    const uint8_t kself = kn[n];
-    const uint32_t k4 = *reinterpret_cast<const uint32_t*>(t.known[l + 1] + 4 * n);
-    if (kself != 0) return;
-    if ((k4 & 0xffu) == 0 || (k4 & 0xff00u) == 0 || (k4 & 0xff0000u) == 0 || (k4 & 0xff000000u) == 0) return;
-    // the four children's rows are 36 contiguous, 16 B aligned doubles: load
-    // them all before any store (the stores below could alias them for the
-    // compiler, which would otherwise serialise a round trip per field)
-    double ch[36];
-    const double2* src = reinterpret_cast<const double2*>(t.sc[l + 1] + 36 * n);
-#pragma unroll
-    for (int q = 0; q < 18; ++q) {
-      const double2 w = src[q];
-      ch[2 * q] = w.x;
-      ch[2 * q + 1] = w.y;
-    }
-    // encode_flow (wavelets.cpp:102-120): h, qx, qy independently
-#pragma unroll
-    for (int f = 0; f < 3; ++f) {
-      P3 kids[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) kids[c] = P3{ch[9 * c + 3 * f], ch[9 * c + 3 * f + 1], ch[9 * c + 3 * f + 2]};
-      P3 p;
-      double d[9];
-      encode_k<KIND>(kids, p, d);
-      t.sc[l][9 * n + 3 * f] = p.c0;
-      t.sc[l][9 * n + 3 * f + 1] = p.cx;
-      t.sc[l][9 * n + 3 * f + 2] = p.cy;
-#pragma unroll
-      for (int q = 0; q < 9; ++q) t.fdet[l][27 * n + 9 * f + q] = d[q];
-    }
-    kn[n] = 2;
-  }
-};
-
 // encode_up + flag + ancestor_closure in ONE fine-to-coarse sweep
-// (solver_adaptive.cpp:16-73, detail_tree.cpp:56-64): at level l a node whose
-// four children are known is encoded (EncodeUpBody); its flag is the static
-// topography significance, or a flow detail of the node just encoded with
-// d_hat >= eps (the norms are taken over the current leaves first), or --
-// the closure -- any flagged child at l + 1, whose flags are final because
-// the sweep visited level l + 1 before.  Equal to the three passes in turn.
+// (solver_adaptive.cpp:16-73, detail_tree.cpp:56-64): at level l a node that
+// is not a current leaf and whose four children are known is encoded
+// (encode_flow, wavelets.cpp:102-120); its flag is the static topography
+// significance, or a flow detail of the node just encoded with d_hat >= eps
+// (the norms are taken over the current leaves first), or -- the closure --
+// any flagged child at l + 1, whose flags are final because the sweep
+// visited level l + 1 before.  Equal to the three passes in turn.  Every
+// load a node needs (its flags, the children's flags and rows) issues before
+// the first store, and d_hat is taken from the details in registers: the
+// sweep is a chain of levels, so each node's latency is on the critical path.
 template <int KIND>
 struct EncodeFlagBody {
   __device__ static void node(int l, uint64_t n, const LvTab& t) {
-    EncodeUpBody<KIND>::node(l, n, t);
-    uint8_t f = t.zsig[l][n];
-    if (!f && t.known[l][n] == 2) {
-      const double* det = t.fdet[l];
+    uint8_t* kn = t.known[l];
+    const uint8_t kself = kn[n];
+    const uint32_t k4 = *reinterpret_cast<const uint32_t*>(t.known[l + 1] + 4 * n);
+    const uint8_t zs = t.zsig[l][n];
+    const uint32_t ct = l + 1 < t.L ? *reinterpret_cast<const uint32_t*>(t.tmp[l + 1] + 4 * n) : 0u;
+    uint8_t f = zs;  // (a non-zero significance value is kept as is)
+    bool sig = false;
+    const bool enc = kself == 0 && (k4 & 0xffu) && (k4 & 0xff00u) && (k4 & 0xff0000u) && (k4 & 0xff000000u);
+    if (enc) {
+      // the four children's rows are 36 contiguous, 16 B aligned doubles:
+      // load them all before any store (the stores below could alias them)
+      double ch[36];
+      const double2* src = reinterpret_cast<const double2*>(t.sc[l + 1] + 36 * n);
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        double d[9];
-#pragma unroll
-        for (int r = 0; r < 9; ++r) d[r] = det[27 * n + 9 * q + r];
-        if (dhat(d, bitsd(t.norms[q])) >= t.eps) f = 1;
+      for (int q = 0; q < 18; ++q) {
+        const double2 w = src[q];
+        ch[2 * q] = w.x;
+        ch[2 * q + 1] = w.y;
       }
+#pragma unroll
+      for (int fi = 0; fi < 3; ++fi) {
+        P3 kids[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) kids[c] = P3{ch[9 * c + 3 * fi], ch[9 * c + 3 * fi + 1], ch[9 * c + 3 * fi + 2]};
+        P3 p;
+        double d[9];
+        encode_k<KIND>(kids, p, d);
+        t.sc[l][9 * n + 3 * fi] = p.c0;
+        t.sc[l][9 * n + 3 * fi + 1] = p.cx;
+        t.sc[l][9 * n + 3 * fi + 2] = p.cy;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) t.fdet[l][27 * n + 9 * fi + q] = d[q];
+        if (dhat(d, bitsd(t.norms[fi])) >= t.eps) sig = true;
+      }
+      kn[n] = 2;
     }
-    if (!f && l + 1 < t.L && *reinterpret_cast<const uint32_t*>(t.tmp[l + 1] + 4 * n)) f = 1;
+    if (!f && (sig || ct)) f = 1;
     t.tmp[l][n] = f;
   }
 };
@@ -391,8 +381,30 @@ __global__ void k_levels_flat(LvTab t, int l0) {
     Body::node(l, n, t);
 }
 
-// Run Body over levels lo..hi in the given order: big levels one launch each,
-// the small ones (all at the coarse end) in one launch.
+// The middle levels of a vertical pass (each node reads only its children or
+// its parent) as subtrees: CTA b owns the level-r node b and walks its
+// subtree's levels r..rt in the pass's order with a block barrier between
+// levels — the level-(l+1) results it reads were written by its own threads,
+// so no launch boundary (and its ~µs gap) is needed per level.  rt: the
+// finest level with at most kTreeThreads nodes per subtree.
+#ifndef FM_TREE_THREADS
+#define FM_TREE_THREADS 64
+#endif
+constexpr int kTreeThreads = FM_TREE_THREADS;
+template <class Body>
+__global__ void __launch_bounds__(kTreeThreads) k_levels_tree(LvTab t, int r, int rt, int fine_to_coarse) {
+  const uint64_t b = blockIdx.x;
+  for (int q = 0; q <= rt - r; ++q) {
+    const int l = fine_to_coarse ? rt - q : r + q;
+    const uint64_t per = uint64_t(1) << (2 * (l - r));
+    for (uint64_t j = threadIdx.x; j < per; j += blockDim.x) Body::node(l, b * per + j, t);
+    __syncthreads();
+  }
+}
+
+// Run Body over levels lo..hi in the given order: the small coarse levels
+// (<= kSmallNodes nodes) in one single-CTA launch, the middle levels as
+// subtrees in one launch (k_levels_tree), the fine levels one launch each.
 template <class Body>
 void run_levels(const LvTab& t, int lo, int hi, bool fine_to_coarse) {
   if (hi < lo) return;
@@ -400,6 +412,11 @@ void run_levels(const LvTab& t, int lo, int hi, bool fine_to_coarse) {
   int ls = -1;  // the finest small level
   for (int l = lo; l <= hi; ++l)
     if (t.nodes(l) <= kSmallNodes) ls = l;
+  const int r = std::max(ls + 1, lo);  // subtree roots
+  int rt = r - 1;                      // the finest subtree level
+  for (int l = r; l <= hi; ++l)
+    if ((uint64_t(1) << (2 * (l - r))) <= uint64_t(kTreeThreads)) rt = l;
+  if (rt == r) rt = r - 1;  // one level: a plain launch
   auto big = [&](int l) {
     k_level<Body><<<nblk(t.nodes(l), 256), 256, 0, st>>>(t, l);
     FM_LAUNCHED();
@@ -408,12 +425,20 @@ void run_levels(const LvTab& t, int lo, int hi, bool fine_to_coarse) {
     k_levels_small<Body><<<1, FM_SMALL_THREADS, 0, st>>>(t, a, b);
     FM_LAUNCHED();
   };
+  auto tree = [&]() {
+    if (rt < r) return;
+    k_levels_tree<Body><<<unsigned(t.nodes(r)), kTreeThreads, 0, st>>>(t, r, rt, fine_to_coarse ? 1 : 0);
+    FM_LAUNCHED();
+  };
+  const int fb = std::max(rt + 1, r);  // the first per-level launch
   if (fine_to_coarse) {
-    for (int l = hi; l > ls && l >= lo; --l) big(l);
+    for (int l = hi; l >= fb; --l) big(l);
+    tree();
     if (ls >= lo) small(ls, lo);
   } else {
     if (ls >= lo) small(lo, ls);
-    for (int l = std::max(ls + 1, lo); l <= hi; ++l) big(l);
+    tree();
+    for (int l = fb; l <= hi; ++l) big(l);
   }
 }
 template <class Body>

@@ -23,6 +23,7 @@
 #include <numeric>
 
 #include "fm_device.cuh"
+#include "levels.cuh"
 #include "fm_internal.hpp"
 
 using namespace fmd;
@@ -392,68 +393,6 @@ __global__ void k_copy_fine(VertexView vv, const Scalars* __restrict__ s, double
   coarse[3 * k + 2] = q.cy;
 }
 
-// Final flags and subtree leaf counts, one level per launch, fine -> coarse.
-// G(l) = sig(l) | any G(l+1) child | (graded) any G(l+1) node edge-adjacent to
-// the 2x2 child block.  This single gather equals the reference's closure +
-// sequential grading sweep (detail_tree.cpp:56-64, 97-113): a level-(l+1)
-// flagged node flags the parents of its four edge neighbours, i.e. the
-// parent P gets flagged iff a flagged level-(l+1) node is a child of P or
-// edge-adjacent to P's child block, and G(l+1) is final before level l is
-// visited in both formulations.  (Verified against the oracle on random trees
-// in tests/test_mra_gpu.py.)
-// ring (adaptive re-grid): the node's own flag is buffer_ring's dilation
-// (solver_adaptive.cpp:75-94) of the closed flags `ring` of its level, taken
-// here rather than in a separate pass: any flagged node in the same-level
-// 8-neighbourhood (or itself)
-__device__ __forceinline__ int ring_flag(const uint8_t* __restrict__ ring, int l, int M, int N, uint64_t n) {
-  if (ring[n]) return 1;
-  int i, j;
-  node_ij(l, n, M, i, j);
-  const int w = M << l, h = N << l;
-  for (int dj = -1; dj <= 1; ++dj)
-    for (int di = -1; di <= 1; ++di) {
-      const int ni = i + di, nj = j + dj;
-      if (ni < 0 || nj < 0 || ni >= w || nj >= h) continue;
-      if (ring[node_index(l, ni, nj, M)]) return 1;
-    }
-  return 0;
-}
-
-__device__ __forceinline__ void grade_count_node(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
-                                                 int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1,
-                                                 int l, int L, int M, int N, uint64_t n, int graded,
-                                                 const uint8_t* __restrict__ ring = nullptr) {
-  int g = ring ? ring_flag(ring, l, M, N, n) : fl[n];
-  int c = 1;
-  if (l + 1 < L) {
-    const uint32_t kids = *reinterpret_cast<const uint32_t*>(fl1 + 4 * n);
-    if (kids) g = 1;
-    if (graded && !g) {
-      int i, j;
-      node_ij(l, n, M, i, j);
-      const int w = M << (l + 1), h = N << (l + 1);
-      const int ci = 2 * i, cj = 2 * j;
-      const int ri[8] = {ci - 1, ci - 1, ci + 2, ci + 2, ci, ci + 1, ci, ci + 1};
-      const int rj[8] = {cj, cj + 1, cj, cj + 1, cj - 1, cj - 1, cj + 2, cj + 2};
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if (ri[q] < 0 || rj[q] < 0 || ri[q] >= w || rj[q] >= h) continue;
-        if (fl1[node_index(l + 1, ri[q], rj[q], M)]) {
-          g = 1;
-          break;
-        }
-      }
-    }
-    if (g) {
-      const int4 cc = *reinterpret_cast<const int4*>(cnt1 + 4 * n);
-      c = cc.x + cc.y + cc.z + cc.w;
-    }
-  } else if (g) {
-    c = 4;
-  }
-  fl[n] = uint8_t(g);
-  cnt[n] = c;
-}
 __global__ void k_grade_count(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
                               int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1, int l,
                               int L, int M, int N, uint64_t nodes, int graded,
@@ -514,67 +453,6 @@ __global__ void k_level0_offsets(const int32_t* __restrict__ cnt, int32_t* __res
   if (threadIdx.x == 0) *total = base;
 }
 
-struct LeafOut {
-  int8_t* l;
-  int32_t* i;
-  int32_t* j;
-  double* z;
-};
-
-__device__ __forceinline__ void emit_leaf(const LeafOut& o, int l, uint64_t node, int M, int32_t at,
-                                          const P3& z) {
-  int i, j;
-  node_ij(l, node, M, i, j);
-  o.l[at] = int8_t(l);
-  o.i[at] = i;
-  o.j[at] = j;
-  o.z[3 * at] = z.c0;
-  o.z[3 * at + 1] = z.cx;
-  o.z[3 * at + 2] = z.cy;
-}
-
-// Top-down decode of one level (detail_tree.cpp:132-164): an active flagged
-// node decodes its stored details into its four children; children that are
-// leaves are emitted at their final index, the others pass their plane and
-// offset down through the level-(l+1) scratch.
-__device__ __forceinline__ void topdown_node(const uint8_t* __restrict__ flp, const uint8_t* __restrict__ fl,
-                                             const uint8_t* __restrict__ fl1, const int32_t* __restrict__ cnt1,
-                                             const int32_t* __restrict__ off, int32_t* __restrict__ off1,
-                                             const double* __restrict__ zin, double* __restrict__ zout,
-                                             const double* __restrict__ det, int l, int L, int M, int kind,
-                                             uint64_t n, const LeafOut& out) {
-  if (l > 0 && !flp[n >> 2]) return;
-  const P3 z{zin[3 * n], zin[3 * n + 1], zin[3 * n + 2]};
-  const int32_t o = off[n];
-  if (!fl[n]) {
-    if (l == 0) emit_leaf(out, 0, n, M, o, z);
-    return;
-  }
-  double d[9];
-#pragma unroll
-  for (int q = 0; q < 9; ++q) d[q] = det[9 * n + q];
-  P3 kids[4];
-  decode(z, d, kind, kids);
-  int32_t run = o;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const uint64_t c = 4 * n + k;
-    if (l + 1 == L) {
-      emit_leaf(out, L, c, M, run, kids[k]);
-      run += 1;
-    } else if (!fl1[c]) {
-      emit_leaf(out, l + 1, c, M, run, kids[k]);
-      off1[c] = run;
-      run += 1;
-    } else {
-      zout[3 * c] = kids[k].c0;
-      zout[3 * c + 1] = kids[k].cx;
-      zout[3 * c + 2] = kids[k].cy;
-      off1[c] = run;
-      run += cnt1[c];
-    }
-  }
-}
 __global__ void k_topdown(const uint8_t* __restrict__ flp, const uint8_t* __restrict__ fl,
                           const uint8_t* __restrict__ fl1, const int32_t* __restrict__ cnt1,
                           const int32_t* __restrict__ off, int32_t* __restrict__ off1,
@@ -632,6 +510,70 @@ inline unsigned blocks_for(uint64_t n, int t) { return unsigned((n + t - 1) / t)
 
 }  // namespace
 
+namespace {
+// The middle levels of the top-down decode as subtrees (adaptive.cu's
+// k_levels_tree): CTA b owns level-r node b and decodes its subtree down to
+// level rt, a block barrier between levels instead of a launch per level.
+constexpr int kTreeThreads = 64;
+__global__ void __launch_bounds__(kTreeThreads) k_topdown_tree(LevelPtrs p, int r, int rt, int L, int M, int kind,
+                                                               LeafOut out) {
+  const uint64_t b = blockIdx.x;
+  for (int l = r; l <= rt; ++l) {
+    const uint64_t per = uint64_t(1) << (2 * (l - r));
+    const bool last = l + 1 == L;
+    for (uint64_t j = threadIdx.x; j < per; j += blockDim.x)
+      topdown_node(l ? p.fl[l - 1] : nullptr, p.fl[l], last ? nullptr : p.fl[l + 1],
+                   last ? nullptr : p.cnt[l + 1], p.off[l], last ? nullptr : p.off[l + 1], p.zs[l],
+                   last ? nullptr : p.zs[l + 1], p.det[l], l, L, M, kind, b * per + j, out);
+    __syncthreads();
+  }
+}
+}  // namespace
+
+// assemble_grid's top-down decode (levels 0..L-1, offsets of level 0 done):
+// the small coarse levels in one single-CTA launch, the middle levels as
+// subtrees in one launch, then a launch per fine level.
+void launch_topdown(Grid& g, const LeafOut& out) {
+  cudaStream_t st = stream();
+  const int L = g.L;
+  std::vector<DBuf<double>>& zs = g.zs;
+  LevelPtrs p{};
+  for (int l = 0; l < L; ++l) {
+    p.fl[l] = g.flag[l].p;
+    p.cnt[l] = g.cnt[l].p;
+    p.off[l] = g.off[l].p;
+    p.zs[l] = l ? zs[l].p : g.coarse.p;
+    p.det[l] = g.det[l].p;
+  }
+  int ls = -1;
+  for (int l = 0; l < L; ++l)
+    if (g.nodes(l) <= kSmallLevelNodes) ls = l;
+  if (ls >= 0) {
+    k_topdown_small<<<1, 256, 0, st>>>(p, ls, L, g.M, g.N, g.kind, out);
+    FM_LAUNCHED();
+  }
+  const int r = ls + 1;
+  int rt = r - 1;
+  for (int l = r; l < L; ++l)
+    if ((uint64_t(1) << (2 * (l - r))) <= uint64_t(kTreeThreads)) rt = l;
+  if (rt > r && r < L) {
+    k_topdown_tree<<<unsigned(g.nodes(r)), kTreeThreads, 0, st>>>(p, r, rt, L, g.M, g.kind, out);
+    FM_LAUNCHED();
+  } else {
+    rt = r - 1;
+  }
+  for (int l = rt + 1; l < L; ++l) {
+    const uint64_t nodes = g.nodes(l);
+    const bool last = l + 1 == L;
+    k_topdown<<<blocks_for(nodes, 256), 256, 0, st>>>(
+        l ? g.flag[l - 1].p : nullptr, g.flag[l].p, last ? nullptr : g.flag[l + 1].p,
+        last ? nullptr : g.cnt[l + 1].p, g.off[l].p, last ? nullptr : g.off[l + 1].p,
+        l ? zs[l].p : g.coarse.p, last ? nullptr : zs[l + 1].p, g.det[l].p, l, L, g.M, g.kind,
+        nodes, out);
+    FM_LAUNCHED();
+  }
+}
+
 int64_t build_leaves(Grid& g) {
   FM_RANGE("build_leaves");
   cudaStream_t st = stream();
@@ -680,32 +622,7 @@ int64_t build_leaves(Grid& g) {
   std::vector<DBuf<double>>& zs = g.zs;  // kept across builds (adaptive re-grids)
   zs.resize(L);
   for (int l = 1; l < L; ++l) zs[l].alloc(3 * g.nodes(l));
-  // the small coarse levels in one single-CTA launch, then a launch per level
-  int ls = -1;
-  for (int l = 0; l < L; ++l)
-    if (g.nodes(l) <= kSmallLevelNodes) ls = l;
-  if (ls >= 0) {
-    LevelPtrs p{};
-    for (int l = 0; l < L; ++l) {
-      p.fl[l] = g.flag[l].p;
-      p.cnt[l] = g.cnt[l].p;
-      p.off[l] = g.off[l].p;
-      p.zs[l] = l ? zs[l].p : g.coarse.p;
-      p.det[l] = g.det[l].p;
-    }
-    k_topdown_small<<<1, 256, 0, st>>>(p, ls, L, g.M, g.N, g.kind, out);
-    FM_LAUNCHED();
-  }
-  for (int l = ls + 1; l < L; ++l) {
-    const uint64_t nodes = g.nodes(l);
-    const bool last = l + 1 == L;
-    k_topdown<<<blocks_for(nodes, 256), 256, 0, st>>>(
-        l ? g.flag[l - 1].p : nullptr, g.flag[l].p, last ? nullptr : g.flag[l + 1].p,
-        last ? nullptr : g.cnt[l + 1].p, g.off[l].p, last ? nullptr : g.off[l + 1].p,
-        l ? zs[l].p : g.coarse.p, last ? nullptr : zs[l + 1].p, g.det[l].p, l, L, g.M, g.kind,
-        nodes, out);
-    FM_LAUNCHED();
-  }
+  launch_topdown(g, out);
   return g.nleaves;
 }
 
@@ -718,33 +635,7 @@ void build_leaves_device(Grid& g, long long* total) {
   const int L = g.L;
   k_level0_offsets<<<1, 1024, 0, st>>>(g.cnt[0].p, g.off[0].p, int64_t(g.nodes(0)), total);
   FM_LAUNCHED();
-  LeafOut out{g.lf_l.p, g.lf_i.p, g.lf_j.p, g.lf_z.p};
-  std::vector<DBuf<double>>& zs = g.zs;
-  int ls = -1;
-  for (int l = 0; l < L; ++l)
-    if (g.nodes(l) <= kSmallLevelNodes) ls = l;
-  if (ls >= 0) {
-    LevelPtrs p{};
-    for (int l = 0; l < L; ++l) {
-      p.fl[l] = g.flag[l].p;
-      p.cnt[l] = g.cnt[l].p;
-      p.off[l] = g.off[l].p;
-      p.zs[l] = l ? zs[l].p : g.coarse.p;
-      p.det[l] = g.det[l].p;
-    }
-    k_topdown_small<<<1, 256, 0, st>>>(p, ls, L, g.M, g.N, g.kind, out);
-    FM_LAUNCHED();
-  }
-  for (int l = ls + 1; l < L; ++l) {
-    const uint64_t nodes = g.nodes(l);
-    const bool last = l + 1 == L;
-    k_topdown<<<blocks_for(nodes, 256), 256, 0, st>>>(
-        l ? g.flag[l - 1].p : nullptr, g.flag[l].p, last ? nullptr : g.flag[l + 1].p,
-        last ? nullptr : g.cnt[l + 1].p, g.off[l].p, last ? nullptr : g.off[l + 1].p,
-        l ? zs[l].p : g.coarse.p, last ? nullptr : zs[l + 1].p, g.det[l].p, l, L, g.M, g.kind,
-        nodes, out);
-    FM_LAUNCHED();
-  }
+  launch_topdown(g, LeafOut{g.lf_l.p, g.lf_i.p, g.lf_j.p, g.lf_z.p});
 }
 
 // Projection + multi-level encode (detail_tree.cpp:10-54 with the fused
