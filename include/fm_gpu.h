@@ -139,8 +139,17 @@ int64_t fm_launch_count(void);
  * which = 2: the shared-divisor division of zdiv2 (nvcc's fast-path sequence
  *            with the reciprocal computed once) vs `a == 0 ? a : a / b`;
  * spanning the fast-path exponent window and its edges.  *failures counts
- * bit mismatches. */
+ * bit mismatches.  which = 3 (FM_GUARD=1 only): one deliberate write past a
+ * buffer's end, *failures = the overruns fm_debug_guard_report then finds
+ * (the checker's positive control; n and seed unused). */
 int fm_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* failures);
+/* Out-of-bounds write check (this pool refuses compute-sanitizer): with
+ * FM_GUARD=1 in the environment when the library loads, every device
+ * allocation carries 256 B guard bands of a known pattern on both sides,
+ * verified on the device when the buffer is freed and, here, for every live
+ * buffer.  *checked: band checks so far; *overruns: bands found modified.
+ * Both 0 when FM_GUARD is off. */
+int fm_debug_guard_report(int64_t* checked, int64_t* overruns);
 
 /* The libm building blocks as the device evaluates them, for tests:
  * fn 0 = pow(x, 7/3) (FM_LIBM_NATIVE: correctly rounded in double-double,

@@ -134,6 +134,7 @@ OPTIONAL = {
     "grade_flags": (C.c_int, [I32, I32, I32, I32, PU8]),
     "pcbrt": (D, [D]),
     "selftest": (C.c_int, [I32, I64, C.c_uint64, PI64]),
+    "debug_guard_report": (C.c_int, [PI64, PI64]),
     "hll": (None, [D, D, D, D, D, D, D, D, PD]),
     "friction": (None, [D, PD, PD, D, D, D, D]),
     "encode": (None, [PD, I32, PD, PD]),

@@ -95,6 +95,10 @@ __device__ __forceinline__ double rand_operand(uint64_t r, uint64_t r2) {
   return __longlong_as_double(static_cast<long long>((sign << 63) | (e << 52) | mant));
 }
 
+// FM_GUARD's positive control: one write just past a buffer's end (into its
+// guard band, which exists only under FM_GUARD=1)
+__global__ void k_write_past_end(double* p, int64_t n) { p[n] = 1.0; }
+
 __global__ void k_selftest_div(int which, int64_t n, uint64_t seed, unsigned long long* fails) {
   const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (k >= n) return;
@@ -160,10 +164,29 @@ int fm_synchronize(void) {
 
 int64_t fm_launch_count(void) { return launches(); }
 
+int fm_debug_guard_report(int64_t* checked, int64_t* overruns) {
+  return guard([&] { guard_report(checked, overruns); });
+}
+
 int fm_selftest(int32_t which, int64_t n, uint64_t seed, int64_t* failures) {
   return guard([&] {
     require_device();
-    if (which < 0 || which > 2) throw Error(FM_ERR_CONFIG, "unknown self-test");
+    if (which < 0 || which > 3) throw Error(FM_ERR_CONFIG, "unknown self-test");
+    if (which == 3) {
+      // the guard checker finds a deliberate overrun (FM_GUARD=1 only: the
+      // write lands in the buffer's guard band); *failures = overruns found
+      if (!guard_enabled()) throw Error(FM_ERR_CONFIG, "self-test 3 needs FM_GUARD=1 when the library loads");
+      int64_t c0 = 0, o0 = 0, c1 = 0, o1 = 0;
+      guard_report(&c0, &o0);
+      {
+        DBuf<double> b(4);
+        k_write_past_end<<<1, 1, 0, stream()>>>(b.p, 4);
+        FM_LAUNCHED();
+      }
+      guard_report(&c1, &o1);
+      *failures = o1 - o0;
+      return;
+    }
     DBuf<unsigned long long> f(1);
     f.zero();
     k_selftest_div<<<unsigned((n + 255) / 256), 256, 0, stream()>>>(which, n, seed, f.p);

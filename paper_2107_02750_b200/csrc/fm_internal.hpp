@@ -42,6 +42,16 @@ cudaStream_t stream();
 void set_stream(cudaStream_t s);
 void upload_banks();  // fills fmd::c_bank once per device
 
+// Device allocation (stream-ordered pool; FM_PLAIN_MALLOC: cudaMalloc).
+// FM_GUARD=1 in the environment: every allocation carries guard bands of a
+// known byte pattern before and after it, checked on the device when it is
+// freed and for every live allocation by fm_debug_guard_report: an
+// out-of-bounds write past either end of a buffer is counted (runtime.cu).
+void* dev_alloc(size_t bytes);
+void dev_free(void* p, size_t bytes);
+void guard_report(int64_t* checked, int64_t* overruns);
+bool guard_enabled();
+
 // Owning device buffer.
 template <typename T>
 struct DBuf {
@@ -86,24 +96,10 @@ struct DBuf {
     release();
     n = count;
     cap = count;
-#ifdef FM_PLAIN_MALLOC
-    if (count) {
-      FM_CUDA(cudaStreamSynchronize(stream()));
-      FM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
-    }
-#else
-    if (count) FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream()));
-#endif
+    if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T)));
   }
   void release() {
-#ifdef FM_PLAIN_MALLOC
-    if (p) {
-      cudaStreamSynchronize(stream());
-      cudaFree(p);
-    }
-#else
-    if (p) cudaFreeAsync(p, stream());
-#endif
+    if (p) dev_free(p, cap * sizeof(T));
     p = nullptr;
     n = 0;
     cap = 0;

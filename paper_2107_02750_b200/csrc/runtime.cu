@@ -2,7 +2,10 @@
 // launch counter and the constant-memory filter banks.
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 
 #include "fm_device.cuh"
 #include "fm_internal.hpp"
@@ -87,6 +90,116 @@ void kt_end() {
   FM_CUDA(cudaEventCreate(&e));
   FM_CUDA(cudaEventRecord(e, stream()));
   t.b.push_back(e);
+}
+
+// ---- device allocations and the FM_GUARD checker --------------------------
+namespace {
+constexpr size_t kGuard = 256;  // bytes of pattern before and after (keeps 256 B alignment)
+constexpr unsigned char kGuardByte = 0xA5;
+bool guard_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("FM_GUARD");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+struct GuardReg {
+  std::mutex mu;
+  std::unordered_map<void*, size_t> live;  // user pointer -> user bytes
+  unsigned long long* bad = nullptr;       // device: overrun count
+  int64_t checked = 0;
+};
+GuardReg& guard_reg() {
+  static GuardReg* r = new GuardReg();  // never destroyed (frees may run at exit)
+  return *r;
+}
+__global__ void k_guard_check(const unsigned char* base, size_t bytes, unsigned long long* bad) {
+  // the band before (base .. base + kGuard) and after (base + kGuard + bytes ..);
+  // one count per damaged buffer
+  int hit = 0;
+  for (size_t q = threadIdx.x; q < 2 * kGuard; q += blockDim.x) {
+    const size_t at = q < kGuard ? q : kGuard + bytes + (q - kGuard);
+    hit |= base[at] != kGuardByte;
+  }
+  if (__syncthreads_or(hit) && threadIdx.x == 0) atomicAdd(bad, 1ull);
+}
+void guard_check_async(void* user, size_t bytes) {
+  GuardReg& r = guard_reg();
+  k_guard_check<<<1, 128, 0, stream()>>>(static_cast<unsigned char*>(user) - kGuard, bytes, r.bad);
+  r.checked += 1;
+}
+void* raw_alloc(size_t bytes) {
+  void* p = nullptr;
+#ifdef FM_PLAIN_MALLOC
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  FM_CUDA(cudaMalloc(&p, bytes));
+#else
+  FM_CUDA(cudaMallocAsync(&p, bytes, stream()));
+#endif
+  return p;
+}
+void raw_free(void* p) {
+#ifdef FM_PLAIN_MALLOC
+  cudaStreamSynchronize(stream());
+  cudaFree(p);
+#else
+  cudaFreeAsync(p, stream());
+#endif
+}
+}  // namespace
+
+void* dev_alloc(size_t bytes) {
+  if (!guard_on()) return raw_alloc(bytes);
+  GuardReg& r = guard_reg();
+  std::lock_guard<std::mutex> lk(r.mu);
+  if (!r.bad) {
+    FM_CUDA(cudaMalloc(&r.bad, sizeof(unsigned long long)));
+    FM_CUDA(cudaMemset(r.bad, 0, sizeof(unsigned long long)));
+  }
+  unsigned char* base = static_cast<unsigned char*>(raw_alloc(bytes + 2 * kGuard));
+  FM_CUDA(cudaMemsetAsync(base, kGuardByte, kGuard, stream()));
+  FM_CUDA(cudaMemsetAsync(base + kGuard + bytes, kGuardByte, kGuard, stream()));
+  r.live[base + kGuard] = bytes;
+  return base + kGuard;
+}
+
+void dev_free(void* p, size_t bytes) {
+  if (!p) return;
+  if (!guard_on()) {
+    raw_free(p);
+    return;
+  }
+  GuardReg& r = guard_reg();
+  std::lock_guard<std::mutex> lk(r.mu);
+  auto it = r.live.find(p);
+  if (it != r.live.end()) {
+    bytes = it->second;
+    r.live.erase(it);
+  }
+  guard_check_async(p, bytes);
+  raw_free(static_cast<unsigned char*>(p) - kGuard);
+}
+
+bool guard_enabled() { return guard_on(); }
+
+// Checks every live allocation's bands and reports the totals (checks done
+// so far, overruns found); no-op counts when FM_GUARD is off.
+void guard_report(int64_t* checked, int64_t* overruns) {
+  int64_t c = 0, o = 0;
+  if (guard_on()) {
+    GuardReg& r = guard_reg();
+    std::lock_guard<std::mutex> lk(r.mu);
+    for (const auto& kv : r.live) guard_check_async(kv.first, kv.second);
+    unsigned long long h = 0;
+    if (r.bad) {
+      FM_CUDA(cudaMemcpyAsync(&h, r.bad, sizeof(h), cudaMemcpyDeviceToHost, stream()));
+      FM_CUDA(cudaStreamSynchronize(stream()));
+    }
+    c = r.checked;
+    o = int64_t(h);
+  }
+  if (checked) *checked = c;
+  if (overruns) *overruns = o;
 }
 
 // The filter banks are compile-time constants (fmd::tap); nothing to upload.

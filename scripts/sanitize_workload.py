@@ -29,7 +29,16 @@ for sc, steps in static:
     s.download()
     s.volume()
     s.finite_state()
+def guard_line():
+    import ctypes as C
+    if os.environ.get("FM_GUARD") == "1":
+        c, o = C.c_int64(0), C.c_int64(0)
+        lib.call("debug_guard_report", C.byref(c), C.byref(o))
+        print(f"FM_GUARD checked={c.value} overruns={o.value}")
+
+
 if small:
+    guard_line()
     print("sanitize workload ok (small)")
     sys.exit(0)
 for sc, steps in ((S.config2(16), 4), (S.config3(32), 3)):
@@ -42,4 +51,5 @@ for solver in ("dg2", "fv1", "acc"):
     s = lib.sim(sc, None)
     s.run(3, gauge_interval=10.0)
     s.download()
+guard_line()
 print("sanitize workload ok")

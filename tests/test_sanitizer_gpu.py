@@ -40,3 +40,36 @@ def test_compute_sanitizer_clean(tool):
     assert out.returncode == 0, f"{tool} reported errors (rc {out.returncode}):\n{log[-4000:]}"
     assert "sanitize workload ok" in log
     assert "ERROR SUMMARY: 0 errors" in log or "RACECHECK SUMMARY: 0 hazards" in log, log[-2000:]
+
+
+def _run_guarded(args, timeout=900):
+    env = dict(os.environ, FM_GUARD="1")
+    return subprocess.run([sys.executable, *args], capture_output=True, text=True, timeout=timeout, cwd=ROOT,
+                          env=env)
+
+
+@pytest.mark.gpu
+def test_guard_bands_catch_a_deliberate_overrun():
+    """The FM_GUARD checker's positive control: fm_selftest(3) writes one
+    double past a 4-double buffer (into its guard band) and must see it."""
+    code = ("import sys, ctypes as C; sys.path.insert(0, %r);"
+            "from paper_2107_02750_b200 import api; lib = api.lib(); f = C.c_int64(-1);"
+            "lib.call('selftest', 3, 0, 0, C.byref(f)); print('OVERRUNS', f.value)" % ROOT)
+    out = _run_guarded(["-c", code], timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "OVERRUNS 1" in out.stdout, out.stdout + out.stderr[-1000:]
+
+
+@pytest.mark.gpu
+def test_guard_bands_clean_over_every_kernel_family():
+    """Out-of-bounds writes (either end of any device buffer) over the whole
+    sanitize workload: static MRA (MW, HW), DG2 / FV1 / ACC device loops and
+    host-API steps, adaptive HWFV1 / MWDG2 re-grids, the uniform raster
+    solvers, rasters, gauges, downloads."""
+    out = _run_guarded([WORKLOAD])
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = [x for x in out.stdout.splitlines() if x.startswith("FM_GUARD")]
+    assert line, out.stdout[-2000:]
+    kv = dict(t.split("=") for t in line[-1].split()[1:])
+    assert int(kv["checked"]) > 100
+    assert int(kv["overruns"]) == 0, line[-1]
