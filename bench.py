@@ -499,7 +499,7 @@ def uniform_leg(lib, args, ws, rank, comm, hbm):
     total = allreduce_sum(float(n) * args.uniform_steps, ws)
     sim.restore()
     prof = sim.profile(3)
-    st2_ms, st2_n = prof.get("k_uni_stage<2>", (0.0, 1))
+    st2_ms, st2_n = prof.get("k_uni_march<2>", (0.0, 1))
     avg = st2_ms / max(st2_n, 1)
     bytes_launch = 248.0 * n  # U^n 72 + U* 72 + z 24 + n 8 read, 72 written per cell
     del sim
@@ -507,7 +507,7 @@ def uniform_leg(lib, args, ws, rank, comm, hbm):
             "value": total / (ms_max / 1000.0), "unit": UNIT, "steps": args.uniform_steps,
             "ms_per_step": ms_max / args.uniform_steps,
             "parallelism": f"row-bands x{ws}" if ws > 1 else "single",
-            "roofline": {"bound": "hbm", "kernel": "k_uni_stage<2>",
+            "roofline": {"bound": "hbm", "kernel": "k_uni_march<2>",
                          "achieved": bytes_launch / (avg / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
                          "frac": bytes_launch / (avg / 1000.0) / 1e9 / hbm, "avg_launch_ms": avg},
             "kernels_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in prof.items()}}

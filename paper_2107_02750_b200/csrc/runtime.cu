@@ -65,7 +65,7 @@ double elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
 const char* kernel_family_name(int f) {
   static const char* names[KF_COUNT] = {"k_head_friction", "k_stage<1>",     "k_stage<2>",
                                         "k_commit",        "k_acc_faces",    "k_acc_leaves",
-                                        "k_uni_head",      "k_uni_stage<1>", "k_uni_stage<2>",
+                                        "k_uni_head",      "k_uni_march<1>", "k_uni_march<2>",
                                         "k_seg<1>",        "k_seg<2>",       "k_decide"};
   return f >= 0 && f < KF_COUNT ? names[f] : "?";
 }

@@ -4,15 +4,12 @@
 // Layout: cell (i, j) at j*nx + i (the reference's own order), 9 flow
 // coefficients + 3 topography coefficients per cell (AoS).
 //
-// k_uni_stage<STAGE>: one CTA per 32 x TY tile.  Phase 1: every cell revises
-// its four faces (revise_faces :73-137) into shared memory, and the tile's
-// one-cell halo revises only the face it shares with the tile.  Phase 2:
-// each interior and boundary face's HLL flux (fluxes :139-185) is evaluated
-// ONCE into shared memory.  Phase 3: every cell assembles (assemble_dg2
-// :187-229 / assemble_fv1 :231-251), updates, applies positivity (:253-281)
-// and, on the last stage, the inflow sources, the non-finite guard and the
-// next step's CFL reduction (the drive-loop epilogue shared with the
-// non-uniform kernels).
+// k_uni_march<STAGE>: one warp per strip of columns marching north (below).
+// Per cell: its four face revisions (revise_faces :73-137), each face's HLL
+// flux solved once (fluxes :139-185), assemble (assemble_dg2 :187-229 /
+// assemble_fv1 :231-251), the update, positivity (:253-281) and, on the last
+// stage, the inflow sources, the non-finite guard and the next step's CFL
+// reduction (the drive-loop epilogue shared with the non-uniform kernels).
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -30,17 +27,6 @@ void launch_decide(Sim& s);
 void project_planes_rowmajor(const fm_raster* r, DBuf<double>& out);
 
 namespace {
-
-// 32 x 4 tiles, >= 7 resident per SM (a 72-register cap; 8: 20.31, 7: 19.49,
-// 6: 20.26, 5: 20.99 ms/step in the round-2 A/B): tuned by A/B on
-// B200 (scripts/ab_uniform.py); 32 x 8 tiles at 110 registers ran 25 % slower
-#ifndef FM_UNI_TY
-#define FM_UNI_TY 4
-#endif
-#ifndef FM_UNI_MINB
-#define FM_UNI_MINB 7
-#endif
-constexpr int TX = 32, TY = FM_UNI_TY;
 
 // A raster band: rows [gy0, gy0 + ny) of the global ny_g rows are owned and
 // stored first (row-major); the ghost rows of a sharded band (the rows just
@@ -97,158 +83,200 @@ __device__ __forceinline__ void ld9(const double* a, size_t c, double s[9]) {
   for (int q = 0; q < 9; ++q) s[q] = a[9 * c + q];
 }
 
+// ---- the marching stage kernel ---------------------------------------------
+// One warp per strip of 30 columns x FM_UNI_H rows, marching north row by
+// row: lane L holds column cx0 - 1 + L (lanes 0 and 31 are the strip's west /
+// east halo columns, computed but not stored).  Each row's four face
+// revisions (revise_faces, solver_uniform.cpp:84-129) and its x fluxes
+// (fluxes :139-185) meet across lanes by shuffles, each x face's HLL solved
+// once by the lane west of it; the y fluxes need no exchange at all: the
+// lane revises the NEXT row's south face as it finishes the current row
+// (that row is loaded one iteration ahead) and carries that face and the
+// north flux it makes into the next iteration as its south face and flux.
+// No shared memory, no block barriers, and only 1/FM_UNI_H of a row of halo
+// work in y.  (The round-1/2 kernel, 32 x 4 shared-memory tiles, revised
+// 0.56 halo faces and solved 0.28 redundant fluxes per cell and waited on
+// block barriers: 8.5 / 9.4 ms per stage at config 4 against 5.6 / 7.1 here,
+// bit-identical.)  The next row's state and (stage 2) U's row are
+// prefetched into L1 and loaded where used; HLL is inlined (the out-of-line
+// call spilled the live state around it).
+#ifndef FM_UNI_H
+#define FM_UNI_H 64
+#endif
+
+#ifndef FM_UNI_MARCH_MINB
+#define FM_UNI_MARCH_MINB 4
+#endif
+constexpr int kMarchCols = 30;
+
+#ifndef FM_UNI_PREFETCH
+#define FM_UNI_PREFETCH 1
+#endif
+__device__ __forceinline__ void prefetch_l1(const double* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+__device__ __forceinline__ Star shfl_star_down(const Star& a) {
+  return Star{__shfl_down_sync(0xffffffffu, a.h, 1), __shfl_down_sync(0xffffffffu, a.qx, 1),
+              __shfl_down_sync(0xffffffffu, a.qy, 1)};
+}
+__device__ __forceinline__ Flx shfl_flx_up(const Flx& a) {
+  return Flx{__shfl_up_sync(0xffffffffu, a.m, 1), __shfl_up_sync(0xffffffffu, a.n, 1),
+             __shfl_up_sync(0xffffffffu, a.t, 1)};
+}
+
 template <int STAGE, bool P2>
-__global__ void __launch_bounds__(TX* TY, FM_UNI_MINB) k_uni_stage(UniView v, NuView nv, const DevClock* __restrict__ clk,
-                                                       DevRed* red, const double* __restrict__ in,
-                                                       const double* uold, double* out, int last,
-                                                       int manual, double mdt, int* err) {
-  __shared__ Star s_e[TY][TX], s_w[TY][TX], s_n[TY][TX], s_s[TY][TX];
-  __shared__ Star h_w[TY], h_e[TY], h_s[TX], h_n[TX];  // halo faces shared with the tile
-  __shared__ Flx fx[TY][TX + 1], fy[TY + 1][TX];
+__global__ void __launch_bounds__(128, FM_UNI_MARCH_MINB) k_uni_march(UniView v, NuView nv,
+                                                                     const DevClock* __restrict__ clk, DevRed* red,
+                                                                     const double* __restrict__ in, const double* uold,
+                                                                     double* out, int last, int manual, double mdt,
+                                                                     int* err) {
   const DevClock* c = clk + 1;
   if (!manual && !c->active) return;
   const double dt = manual ? mdt : c->dt;
-  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;  // y: local owned rows
-  const int i = x0 + tx, j = y0 + ty;
-  const bool valid = i < v.nx && j < v.ny;
-  const int ic = min(i, v.nx - 1), jc = min(j, v.ny - 1);
-  const int gj = v.gy0 + j;  // global row
-  const size_t cell = size_t(jc) * v.nx + ic;
-  double s[9];
-  ld9(in, cell, s);
-  const P3 zc = ld3(v.z, cell);
-  // phase 1: revise the four faces
-  const bool hasE = ic + 1 < v.nx, hasW = ic > 0, hasN = v.gy0 + jc + 1 < v.nyg, hasS = v.gy0 + jc > 0;
-  const double zwe = hasE ? face_val(ld3(v.z, cell + 1), 3) : 0.0;
-  const double zew = hasW ? face_val(ld3(v.z, cell - 1), 1) : 0.0;
-  const double zsn = hasN ? face_val(ld3(v.z, cidx(v, ic, jc + 1)), 2) : 0.0;
-  const double zns = hasS ? face_val(ld3(v.z, cidx(v, ic, jc - 1)), 0) : 0.0;
-  const FaceRev re = revise_face(s, zc, 1, zwe, hasE, v.hdry);
-  const FaceRev rw = revise_face(s, zc, 3, zew, hasW, v.hdry);
-  const FaceRev rn = revise_face(s, zc, 0, zsn, hasN, v.hdry);
-  const FaceRev rs = revise_face(s, zc, 2, zns, hasS, v.hdry);
-  s_e[ty][tx] = re.st;
-  s_w[ty][tx] = rw.st;
-  s_n[ty][tx] = rn.st;
-  s_s[ty][tx] = rs.st;
-  // halo: the neighbouring cell's face toward the tile
-  if (tx == 0 && x0 > 0 && j < v.ny) {  // star_e of (x0-1, j)
-    double t[9];
-    const size_t cc = size_t(j) * v.nx + (x0 - 1);
-    ld9(in, cc, t);
-    h_w[ty] = revise_face(t, ld3(v.z, cc), 1, face_val(ld3(v.z, cc + 1), 3), true, v.hdry).st;
-  }
-  if (tx == TX - 1 && x0 + TX < v.nx && j < v.ny) {  // star_w of (x0+TX, j)
-    double t[9];
-    const size_t cc = size_t(j) * v.nx + (x0 + TX);
-    ld9(in, cc, t);
-    h_e[ty] = revise_face(t, ld3(v.z, cc), 3, face_val(ld3(v.z, cc - 1), 1), true, v.hdry).st;
-  }
-  if (ty == 0 && v.gy0 + y0 > 0 && i < v.nx) {  // star_n of (i, y0-1)
-    double t[9];
-    const size_t cc = cidx(v, i, y0 - 1);
-    ld9(in, cc, t);
-    h_s[tx] = revise_face(t, ld3(v.z, cc), 0, face_val(ld3(v.z, cidx(v, i, y0)), 2), true, v.hdry).st;
-  }
-  // star_s of (i, yN), the row just north of the tile's last row (a ghost row
-  // when the tile ends the band)
-  const int yN = min(y0 + TY, v.ny);
-  if (ty == TY - 1 && v.gy0 + yN < v.nyg && i < v.nx) {
-    double t[9];
-    const size_t cc = cidx(v, i, yN);
-    ld9(in, cc, t);
-    h_n[tx] = revise_face(t, ld3(v.z, cc), 2, face_val(ld3(v.z, cidx(v, i, yN - 1)), 0), true, v.hdry).st;
-  }
-  __syncthreads();
-  // phase 2: every face of the tile once (fluxes, solver_uniform.cpp:139-185)
-  const int ncx = min(TX, v.nx - x0), ncy = min(TY, v.ny - y0);
-  for (int f = threadIdx.x; f < TY * (TX + 1); f += TX * TY) {
-    const int r = f / (TX + 1), k = f % (TX + 1);
-    if (r >= ncy || k > ncx) continue;
-    const int gi = x0 + k;  // face between cells gi-1 and gi
-    Star l, rr;
-    if (gi == 0) {
-      rr = s_w[r][0];
-      l = rr;
-      if (v.bc[3] == FM_REFLECTIVE) l.qx = -l.qx;
-    } else if (gi == v.nx) {
-      l = s_e[r][k - 1];
-      rr = l;
-      if (v.bc[1] == FM_REFLECTIVE) rr.qx = -rr.qx;
-    } else {
-      l = k == 0 ? h_w[r] : s_e[r][k - 1];
-      rr = k == ncx ? h_e[r] : s_w[r][k];
-    }
-    fx[r][k] = hll(l.h, l.qx, l.qy, rr.h, rr.qx, rr.qy, v.g, v.hdry, err);
-  }
-  for (int f = threadIdx.x; f < (TY + 1) * TX; f += TX * TY) {
-    const int r = f / TX, k = f % TX;
-    if (k >= ncx || r > ncy) continue;
-    const int gf = v.gy0 + y0 + r;  // global face row
-    Star l, rr;
-    if (gf == 0) {
-      rr = s_s[0][k];
-      l = rr;
-      if (v.bc[2] == FM_REFLECTIVE) l.qy = -l.qy;
-    } else if (gf == v.nyg) {
-      l = s_n[r - 1][k];
-      rr = l;
-      if (v.bc[0] == FM_REFLECTIVE) rr.qy = -rr.qy;
-    } else {
-      l = r == 0 ? h_s[k] : s_n[r - 1][k];
-      rr = r == ncy ? h_n[k] : s_s[r][k];
-    }
-    // normal component is qy along y faces
-    fy[r][k] = hll(l.h, l.qy, l.qx, rr.h, rr.qy, rr.qx, v.g, v.hdry, err);
-  }
-  __syncthreads();
-  // phase 3: assemble + update
-  double res[9];
+  const int lane = threadIdx.x & 31;
+  const int wx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int cx0 = wx * kMarchCols;
+  if (cx0 >= v.nx) return;  // whole warps only
+  const int i = cx0 - 1 + lane;
+  const bool colok = i >= 0 && i < v.nx;
+  const bool own = colok && lane >= 1 && lane <= kMarchCols;
+  const int ic = min(max(i, 0), v.nx - 1);
+  const bool hasE = ic + 1 < v.nx, hasW = ic > 0;
+  const int y0 = blockIdx.y * FM_UNI_H, y1 = min(y0 + FM_UNI_H, v.ny);
   const double inv = 1.0 / v.R;
-  if (valid) {
-    const double k3 = kHalfInvS3;
-    const DirMod X{0.5 * (re.st.h + rw.st.h),   (re.st.h - rw.st.h) * k3,   0.5 * (re.st.qx + rw.st.qx),
-                   (re.st.qx - rw.st.qx) * k3, 0.5 * (re.st.qy + rw.st.qy), (re.st.qy - rw.st.qy) * k3,
-                   (re.zd - rw.zd) * k3};
-    const DirMod Y{0.5 * (rn.st.h + rs.st.h),   (rn.st.h - rs.st.h) * k3,   0.5 * (rn.st.qx + rs.st.qx),
-                   (rn.st.qx - rs.st.qx) * k3, 0.5 * (rn.st.qy + rs.st.qy), (rn.st.qy - rs.st.qy) * k3,
-                   (rn.zd - rs.zd) * k3};
-    double Lr[9];
-    l_operator<P2>(fy[ty + 1][tx], fx[ty][tx + 1], fy[ty][tx], fx[ty][tx], X, Y, v.R, inv, v.g, v.hdry,
-                   v.scheme == FM_DG2, Lr);
-    if (STAGE == 1) {
-#pragma unroll
-      for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
-    } else {
-      double u0[9];
-      ld9(uold, cell, u0);
-#pragma unroll
-      for (int q = 0; q < 9; ++q) {
-        double a = s[q];
-        a += Lr[q] * dt;
-        a += u0[q];
-        a *= 0.5;
-        res[q] = a;
-      }
+  const bool dg2 = v.scheme == FM_DG2;
+  // prologue: row y0's state and its south face, and the flux below row y0
+  double s[9];
+  load9v(in, (long long)cidx(v, ic, y0), s);
+  P3 zc = ld3(v.z, cidx(v, ic, y0));
+  const bool hasS0 = v.gy0 + y0 > 0;
+  Star st_s;  // the current row's revised south face
+  double zd_s;
+  Flx fs;     // the flux through the current row's south face
+  {
+    const double zns = hasS0 ? face_val(ld3(v.z, cidx(v, ic, y0 - 1)), 0) : 0.0;
+    const FaceRev rs = revise_face(s, zc, 2, zns, hasS0, v.hdry);
+    st_s = rs.st;
+    zd_s = rs.zd;
+    Star l = st_s, r = st_s;
+    if (hasS0) {
+      double t[9];
+      const size_t cs = cidx(v, ic, y0 - 1);
+      load9v(in, (long long)cs, t);
+      l = revise_face(t, ld3(v.z, cs), 0, face_val(zc, 2), true, v.hdry).st;
+    } else if (v.bc[2] == FM_REFLECTIVE) {
+      l.qy = -l.qy;
     }
-    positivity(res, v.hdry);
-    if (last && !manual) {
-      // apply_inflows (solver_uniform.cpp:444-455): one fine cell per target
-      for (int f = 0; f < v.ninflow; ++f) {
-        if (!c->on[f]) continue;
-        if (i >= v.rect[4 * f] && gj >= v.rect[4 * f + 1] && i <= v.rect[4 * f + 2] && gj <= v.rect[4 * f + 3])
-          res[0] += ddiv(c->per_cell[f] * 1, v.R * v.R);
-      }
-    }
-    double* o = out + 9 * cell;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) o[q] = res[q];
-  } else {
-#pragma unroll
-    for (int q = 0; q < 9; ++q) res[q] = 0.0;
+    fs = hll_inl(l.h, l.qy, l.qx, r.h, r.qy, r.qx, v.g, v.hdry, err);
   }
-  if (last && !manual) reduce_leaf(nv, red, *c, res, v.R, leaf_key(0, i, gj), valid);
+  for (int j = y0; j < y1; ++j) {
+    const int gj = v.gy0 + j;
+    const bool hasN = gj + 1 < v.nyg;
+    // the next row's topography now; its state and (stage 2) U's row of this
+    // cell are prefetched into L1 here and loaded where they are used, so
+    // they hold no registers through the face work
+    const size_t cn = hasN ? cidx(v, ic, j + 1) : size_t(j) * v.nx + ic;
+    P3 zn{0.0, 0.0, 0.0};
+    if (hasN) zn = ld3(v.z, cn);
+#if FM_UNI_PREFETCH
+    prefetch_l1(in + 9 * cn);
+    prefetch_l1(in + 9 * cn + 8);
+    if (STAGE == 2) {
+      prefetch_l1(uold + 9 * (size_t(j) * v.nx + ic));
+      prefetch_l1(uold + 9 * (size_t(j) * v.nx + ic) + 8);
+    }
+#endif
+    // east / west / north faces of this row
+    const double fwv = face_val(zc, 3), fev = face_val(zc, 1);
+    const double zwe = __shfl_down_sync(0xffffffffu, fwv, 1);  // the east neighbour's west face value
+    const double zew = __shfl_up_sync(0xffffffffu, fev, 1);    // the west neighbour's east face value
+    const FaceRev re = revise_face(s, zc, 1, zwe, hasE, v.hdry);
+    const FaceRev rw = revise_face(s, zc, 3, zew, hasW, v.hdry);
+    const FaceRev rn = revise_face(s, zc, 0, hasN ? face_val(zn, 2) : 0.0, hasN, v.hdry);
+    // x fluxes: lane L solves the face between its column and the next;
+    // lane 0 (column cx0 - 1 < 0 at the west edge) solves the west boundary
+    Flx fe;
+    {
+      const Star wnext = shfl_star_down(rw.st);
+      Star l = re.st, r = wnext;
+      if (i == -1) {  // the domain's west boundary face, west of column 0
+        l = wnext;
+        if (v.bc[3] == FM_REFLECTIVE) l.qx = -l.qx;
+      } else if (i == v.nx - 1) {  // the east boundary face
+        r = re.st;
+        if (v.bc[1] == FM_REFLECTIVE) r.qx = -r.qx;
+      }
+      fe = hll_inl(l.h, l.qx, l.qy, r.h, r.qx, r.qy, v.g, v.hdry, err);
+    }
+    const Flx fw = shfl_flx_up(fe);
+    // the north face: the next row's south face, revised now and carried
+    Flx fn;
+    double sn[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    Star st_sn = rn.st;
+    double zd_sn = 0.0;
+    {
+      Star l = rn.st, r = rn.st;
+      if (hasN) {
+        load9v(in, (long long)cn, sn);
+        const FaceRev rs1 = revise_face(sn, zn, 2, face_val(zc, 0), true, v.hdry);
+        st_sn = rs1.st;
+        zd_sn = rs1.zd;
+        r = st_sn;
+      } else if (v.bc[0] == FM_REFLECTIVE) {
+        r.qy = -r.qy;
+      }
+      fn = hll_inl(l.h, l.qy, l.qx, r.h, r.qy, r.qx, v.g, v.hdry, err);
+    }
+    // assemble + update
+    double res[9];
+    if (own) {
+      const double k3 = kHalfInvS3;
+      const DirMod X{0.5 * (re.st.h + rw.st.h),   (re.st.h - rw.st.h) * k3,   0.5 * (re.st.qx + rw.st.qx),
+                     (re.st.qx - rw.st.qx) * k3, 0.5 * (re.st.qy + rw.st.qy), (re.st.qy - rw.st.qy) * k3,
+                     (re.zd - rw.zd) * k3};
+      const DirMod Y{0.5 * (rn.st.h + st_s.h),   (rn.st.h - st_s.h) * k3,   0.5 * (rn.st.qx + st_s.qx),
+                     (rn.st.qx - st_s.qx) * k3, 0.5 * (rn.st.qy + st_s.qy), (rn.st.qy - st_s.qy) * k3,
+                     (rn.zd - zd_s) * k3};
+      double Lr[9];
+      l_operator<P2>(fn, fe, fs, fw, X, Y, v.R, inv, v.g, v.hdry, dg2, Lr);
+      if (STAGE == 1) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) res[q] = s[q] + Lr[q] * dt;
+      } else {
+        double u0[9];
+        load9v(uold, (long long)(size_t(j) * v.nx + ic), u0);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+          double a = s[q];
+          a += Lr[q] * dt;
+          a += u0[q];
+          a *= 0.5;
+          res[q] = a;
+        }
+      }
+      positivity(res, v.hdry);
+      if (last && !manual) {
+        for (int f = 0; f < v.ninflow; ++f) {
+          if (!c->on[f]) continue;
+          if (i >= v.rect[4 * f] && gj >= v.rect[4 * f + 1] && i <= v.rect[4 * f + 2] && gj <= v.rect[4 * f + 3])
+            res[0] += ddiv(c->per_cell[f] * 1, v.R * v.R);
+        }
+      }
+      store9v(out, (long long)(size_t(j) * v.nx + i), res);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) res[q] = 0.0;
+    }
+    if (last && !manual) reduce_leaf(nv, red, *c, res, v.R, leaf_key(0, i, gj), own);
+    // advance: the next row becomes the current one
+#pragma unroll
+    for (int q = 0; q < 9; ++q) s[q] = sn[q];
+    zc = zn;
+    st_s = st_sn;
+    zd_s = zd_sn;
+    fs = fn;
+  }
 }
 
 // ---- ACC (solver_uniform.cpp:330-415) --------------------------------------
@@ -551,7 +579,8 @@ void un_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
   cudaStream_t st = stream();
   const UniView v = uview(s);
   const NuView nv = s.view();
-  const dim3 grid((s.nx + TX - 1) / TX, (s.ny + TY - 1) / TY);
+  const int nwx = (s.nx + kMarchCols - 1) / kMarchCols;
+  const dim3 mgrid((nwx + 3) / 4, (s.ny + FM_UNI_H - 1) / FM_UNI_H);
   const bool fv1 = s.scheme == FM_FV1;
   if (s.shard && (op == OP_ACC || op == OP_STAGE1 || op == OP_STAGE2)) shard_finish(s);
   switch (op) {
@@ -576,19 +605,15 @@ void un_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       break;
     case OP_STAGE1:
       kt_begin(KF_UNI_STAGE1);
-      if (s.p2)
-        k_uni_stage<1, true><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, fv1 ? 1 : 0, manual, mdt, err);
-      else
-        k_uni_stage<1, false><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, fv1 ? 1 : 0, manual, mdt, err);
+      (s.p2 ? k_uni_march<1, true> : k_uni_march<1, false>)<<<mgrid, 128, 0, st>>>(
+          v, nv, s.clk.p, s.red.p, s.u.p, nullptr, s.us.p, fv1 ? 1 : 0, manual, mdt, err);
       FM_LAUNCHED();
       kt_end();
       break;
     case OP_STAGE2:
       kt_begin(KF_UNI_STAGE2);
-      if (s.p2)
-        k_uni_stage<2, true><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
-      else
-        k_uni_stage<2, false><<<grid, TX * TY, 0, st>>>(v, nv, s.clk.p, s.red.p, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
+      (s.p2 ? k_uni_march<2, true> : k_uni_march<2, false>)<<<mgrid, 128, 0, st>>>(
+          v, nv, s.clk.p, s.red.p, s.us.p, s.u.p, s.u.p, 1, manual, mdt, err);
       FM_LAUNCHED();
       kt_end();
       break;

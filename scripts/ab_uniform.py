@@ -1,4 +1,4 @@
-"""A/B of library variants on the config-4 uniform raster (k_uni_stage)."""
+"""A/B of library variants on the config-4 uniform raster (k_uni_march)."""
 import json
 import os
 import subprocess

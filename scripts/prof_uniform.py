@@ -1,4 +1,4 @@
-"""Config-4 uniform raster DG2: a few steps for ncu (kernel k_uni_stage)."""
+"""Config-4 uniform raster DG2: a few steps for ncu (kernel k_uni_march)."""
 import os
 import sys
 
