@@ -96,6 +96,12 @@ struct Shard {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool pending = false;
+  // the stage split (DG2 stage 1): the owned leaves some peer needs (each
+  // once, ascending) and the rest; stage 1 runs the first list, starts the
+  // U* exchange (NCCL) and runs the rest while it is in flight
+  DBuf<int32_t> stage_first, stage_rest;
+  int64_t n_first = 0, n_rest = 0;
+  bool us_started = false;  // this step's U* exchange was started inside stage 1
   ~Shard();
 };
 
@@ -232,6 +238,7 @@ inline void step_op(Sim& s, int op, bool manual, double mdt, int* err) {
 }
 void shard_op(Sim& s, int op);  // exchange / reduce for a sharded sim (NCCL)
 void shard_finish(Sim& s);      // join an exchange started by shard_op
+void shard_stage_lists(Sim& s);  // the stage split's leaf lists (after send_idx)
 struct ShardPlan {
   int64_t first = 0, count = 0;
   std::vector<int64_t> segs;              // global ids of the local segments, ascending
@@ -246,6 +253,7 @@ Comm* comm_create_local(int nranks);
 Comm* comm_create_nccl(int nranks, int rank, const uint8_t* id);
 Comm* comm_create_host(int nranks, int rank, const char* name);
 bool shard_eager(const Sim& s);  // the step cannot be graph-captured (host transport)
+bool shard_nccl(const Sim& s);   // a shard on an NCCL communicator
 void comm_unique_id(uint8_t* out);
 void comm_destroy(Comm* c);
 void comm_forget(Comm* c, Sim* s);

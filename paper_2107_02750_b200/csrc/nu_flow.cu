@@ -349,13 +349,15 @@ __device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9],
 #define FM_STAGE_MINB 10
 #endif
 
-template <int STAGE, bool P2, int W = 9>
+// LIST: the leaves are list[0..cnt) (a shard's stage split) instead of 0..n-1
+template <int STAGE, bool P2, int W = 9, bool LIST = false>
 __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
     NuView v, const DevClock* __restrict__ clk, DevRed* red, const double* __restrict__ in,
-    const double* uold, double* out, int last, int manual, double mdt, int* err) {
-  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool valid = k < v.n;
-  const long long kk = valid ? k : v.n - 1;
+    const double* uold, double* out, int last, int manual, double mdt, int* err,
+    const int32_t* __restrict__ list, long long cnt) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool valid = LIST ? t < cnt : t < v.n;
+  const long long kk = LIST ? (long long)list[valid ? t : cnt - 1] : (valid ? t : v.n - 1);
   // the leaf's rows are loaded before the step-active check: they do not
   // depend on it, and the check's clock load would otherwise put a second
   // round trip in front of the first gathers
@@ -906,10 +908,34 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       seg(KF_SEG1, in);
       kt_begin(KF_STAGE1);
       const int last1 = fv1 ? 1 : 0;
+      if (s.shard && !fv1) {
+        // the stage split: the leaves a peer needs first, then (NCCL) their
+        // U* exchange starts on the side stream while the rest run
+        Shard& sh = *s.shard;
+        auto lk = s.p2 ? k_stage<1, true, 9, true> : k_stage<1, false, 9, true>;
+        if (sh.n_first) {
+          launch_k(lk, nblk(sh.n_first, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, in,
+                   (const double*)nullptr, out, last1, (int)manual, mdt, err, (const int32_t*)sh.stage_first.p,
+                   (long long)sh.n_first);
+          FM_LAUNCHED();
+        }
+        if (shard_nccl(s)) {
+          shard_op(s, OP_EXCH_US);
+          sh.us_started = true;
+        }
+        if (sh.n_rest) {
+          launch_k(lk, nblk(sh.n_rest, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, in,
+                   (const double*)nullptr, out, last1, (int)manual, mdt, err, (const int32_t*)sh.stage_rest.p,
+                   (long long)sh.n_rest);
+          FM_LAUNCHED();
+        }
+        kt_end();
+        break;
+      }
       auto kern = s.p2 ? (c3 ? k_stage<1, true, 3> : k_stage<1, true, 9>)
                        : (c3 ? k_stage<1, false, 3> : k_stage<1, false, 9>);
       launch_k(kern, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, in,
-               (const double*)nullptr, out, last1, (int)manual, mdt, err);
+               (const double*)nullptr, out, last1, (int)manual, mdt, err, (const int32_t*)nullptr, 0ll);
       FM_LAUNCHED();
       kt_end();
       break;
@@ -918,9 +944,9 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       seg(KF_SEG2, s.us.p);
       kt_begin(KF_STAGE2);
       if (s.p2)
-        launch_k(k_stage<2, true, 9>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
+        launch_k(k_stage<2, true, 9>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err, (const int32_t*)nullptr, 0ll);
       else
-        launch_k(k_stage<2, false, 9>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err);
+        launch_k(k_stage<2, false, 9>, nblk(n, FM_STAGE_THREADS), FM_STAGE_THREADS, st, v, (const DevClock*)clk, red, (const double*)s.us.p, (const double*)s.u.p, s.u.p, 1, (int)manual, mdt, err, (const int32_t*)nullptr, 0ll);
       FM_LAUNCHED();
       kt_end();
       break;
@@ -931,6 +957,10 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
 
 void nu_launch_step(Sim& s, bool manual, double mdt, int* err) {
   for (int op : nu_step_ops(s, manual)) {
+    if (op == OP_EXCH_US && s.shard && s.shard->us_started) {
+      s.shard->us_started = false;  // already in flight (the stage split)
+      continue;
+    }
     if (op == OP_EXCH_U || op == OP_EXCH_US || op == OP_REDUCE) {
       if (s.shard) shard_op(s, op);
     } else {

@@ -736,6 +736,7 @@ Sim* sim_create_shard(const fm_sim_desc* d, const fm_raster* dem, const Grid* gr
   }
   sh->send_buf.alloc(9 * size_t(std::max<int64_t>(total_send, 1)));
   s.shard = std::move(sh);
+  shard_stage_lists(s);
   if (comm->kind == COMM_LOCAL) comm->members[rank] = &s;
   FM_CUDA(cudaStreamSynchronize(st));
   G.reset();
@@ -834,6 +835,30 @@ static void host_exchange(Sim& s, double* arr, int w) {
   FM_CUDA(cudaStreamSynchronize(stream()));
   shm_barrier(c);  // the slots may be reused
 }
+
+// The stage split's leaf lists from the send plan (once, at creation).
+void shard_stage_lists(Sim& s) {
+  Shard& sh = *s.shard;
+  const int64_t m = sh.soff.empty() ? 0 : sh.soff.back() + sh.scnt.back();
+  std::vector<int32_t> idx(size_t(std::max<int64_t>(m, 0)));
+  if (m) {
+    sh.send_idx.download(idx.data(), size_t(m));
+    FM_CUDA(cudaStreamSynchronize(stream()));
+  }
+  std::vector<uint8_t> sent(size_t(s.n), 0);
+  for (int32_t k : idx)
+    if (k >= 0 && k < s.n) sent[size_t(k)] = 1;
+  std::vector<int32_t> first, rest;
+  for (int64_t k = 0; k < s.n; ++k) (sent[size_t(k)] ? first : rest).push_back(int32_t(k));
+  sh.n_first = int64_t(first.size());
+  sh.n_rest = int64_t(rest.size());
+  if (first.empty()) first.push_back(0);
+  if (rest.empty()) rest.push_back(0);
+  sh.stage_first.upload(first.data(), first.size());
+  sh.stage_rest.upload(rest.data(), rest.size());
+}
+
+bool shard_nccl(const Sim& s) { return s.shard && s.shard->comm && s.shard->comm->kind == COMM_NCCL; }
 
 bool shard_eager(const Sim& s) { return s.shard && s.shard->comm && s.shard->comm->kind == COMM_HOST; }
 

@@ -14,6 +14,15 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+# torch first: the library dlopens the NCCL already in the process (torch's
+# 2.28) and only otherwise the system libnccl.so.2 (2.27); once that one is
+# resident under the soname libnccl.so.2, a later `import torch` resolves its
+# NCCL symbols against it and fails, so test order must not decide which
+try:
+    import torch  # noqa: F401
+except Exception:  # pragma: no cover - torch is optional for the CPU tests
+    pass
+
 ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
 REF_SO = os.path.join(ROOT, "oracle", "_ref", "libfmref.so")
 GPU_SO = os.path.join(ROOT, "paper_2107_02750_b200", "libfm_gpu.so")
