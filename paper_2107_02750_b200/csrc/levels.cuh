@@ -24,15 +24,17 @@ using namespace fmd;
 // (solver_adaptive.cpp:75-94) of the closed flags `ring` of its level, taken
 // here rather than in a separate pass: any flagged node in the same-level
 // 8-neighbourhood (or itself)
-// Every neighbour flag below is loaded up front (predicated on lying inside
-// the domain) and then combined: the grading pass is a chain of levels, and
-// a load-test-branch sequence per neighbour put up to 17 dependent round trips
-// on each node's critical path.  Same results as the early-exit form.
+// The neighbour flags below are loaded together (predicated on lying inside
+// the domain) and then combined, once the node's own flags leave the answer
+// open: the grading pass is a chain of levels, and a load-test-branch
+// sequence per neighbour put up to 17 dependent round trips on a node's
+// critical path.  Same results as the early-exit form.
 __device__ __forceinline__ int ring_flag(const uint8_t* __restrict__ ring, int l, int M, int N, uint64_t n) {
+  if (ring[n]) return 1;
   int i, j;
   node_ij(l, n, M, i, j);
   const int w = M << l, h = N << l;
-  int any = ring[n];
+  int any = 0;
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
     if (q == 4) continue;
@@ -53,7 +55,7 @@ __device__ __forceinline__ void grade_count_node(uint8_t* __restrict__ fl, const
     const uint32_t kids = *reinterpret_cast<const uint32_t*>(fl1 + 4 * n);
     // 2:1 grading: a flagged level-(l+1) node edge-adjacent to the child block
     int nbr = 0;
-    if (graded) {
+    if (graded && !kids && !g) {
       int i, j;
       node_ij(l, n, M, i, j);
       const int w = M << (l + 1), h = N << (l + 1);
@@ -66,10 +68,7 @@ __device__ __forceinline__ void grade_count_node(uint8_t* __restrict__ fl, const
         nbr |= in ? fl1[node_index(l + 1, in ? ri[q] : ci, in ? rj[q] : cj, M)] : 0;
       }
     }
-    if (kids)
-      g = 1;
-    else if (graded && !g && nbr)
-      g = 1;
+    if (kids || nbr) g = 1;
     if (g) {
       const int4 cc = *reinterpret_cast<const int4*>(cnt1 + 4 * n);
       c = cc.x + cc.y + cc.z + cc.w;
