@@ -735,7 +735,17 @@ void adaptive_stats(Sim& s, int64_t* n_enc, int64_t* n_int) {
   }
 }
 
-void adaptive_adapt(Sim& s, double t) {
+void adaptive_adapt_begin(Sim& s) {
+  Grid& g = *s.grid;
+  AdaptState& a = *s.ad;
+  LvTab tab = lv_tab(s, g, a);
+  // everything up to the new leaf list, one graph replay (adapt_prefix); the
+  // new leaf count is read back with the caller's next host sync
+  adapt_prefix(s, g, a, tab);
+  FM_CUDA(cudaMemcpyAsync(&s.slots().n_new, a.dn.p + 1, sizeof(long long), cudaMemcpyDeviceToHost, stream()));
+}
+
+void adaptive_adapt_finish(Sim& s, double t) {
   FM_RANGE("adapt");
   s.ref_perm_ok = false;  // the leaf set changes
   ++s.leaf_gen;
@@ -743,18 +753,10 @@ void adaptive_adapt(Sim& s, double t) {
   PhaseClock pc(st);
   Grid& g = *s.grid;
   AdaptState& a = *s.ad;
-  LvTab tab = lv_tab(s, g, a);
-  // everything up to the new leaf list, one graph replay (adapt_prefix),
-  // then the new leaf count: the adapt's one host round trip before the
-  // topology's
-  adapt_prefix(s, g, a, tab);
-  long long n_dev = 0;
-  FM_CUDA(cudaMemcpyAsync(&n_dev, a.dn.p + 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
-  FM_CUDA(cudaStreamSynchronize(st));
+  const long long n_dev = s.slots().n_new;
   g.nleaves = n_dev;
   g.lf_l.n = g.lf_i.n = g.lf_j.n = size_t(n_dev);
   g.lf_z.n = 3 * size_t(n_dev);
-  pc.mark("prefix");
   // transfer the flow onto the new leaves, straight into U (the old leaves'
   // rows are in the encode-up pyramid since the prefix), and install the
   // new leaf set into the sim in the same pass; buffers only grow
@@ -766,7 +768,7 @@ void adaptive_adapt(Sim& s, double t) {
   s.li.ensure(s.n);
   s.lj.ensure(s.n);
   s.z.ensure(3 * s.n);
-  tab = lv_tab(s, g, a);
+  LvTab tab = lv_tab(s, g, a);
   tab.unew = s.u.p;
   tab.do_install = 1;
   tab.inst = Install{s.lvl.p, s.li.p, s.lj.p, s.z.p, g.lf_z.p};
@@ -782,11 +784,18 @@ void adaptive_adapt(Sim& s, double t) {
   refresh_topology(s);
   pc.mark("topology");
   s.fv1_in_star = false;
-  for (auto& g : s.gexec) {
-    if (g) cudaGraphExecDestroy(g);
-    g = nullptr;
+  for (auto& gx : s.gexec) {
+    if (gx) cudaGraphExecDestroy(gx);
+    gx = nullptr;
   }
   s.element_log.emplace_back(t, s.n);  // s.n is known on the host: no sync here
+}
+
+void adaptive_adapt(Sim& s, double t) {
+  adaptive_adapt_begin(s);
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  s.settle_nseg();
+  adaptive_adapt_finish(s, t);
 }
 
 }  // namespace fmh

@@ -71,6 +71,9 @@ struct NuView {
   const int32_t* sid;   // 8 per leaf: segment ids of the sub-faces per side
   const double* segst;  // 6 per segment: HLL flux (m n t), z*, h*L, h*R
   long long nseg;
+  // adaptive sims: the segment count lives on the device (the host launches
+  // with an upper bound, see build_topology); null for static sims
+  const long long* nseg_dev;
 };
 
 // Operations of one step (nu_step_ops in nu_flow.cu).
@@ -121,6 +124,26 @@ struct Sim {
   // the element size with exact reciprocal multiplies (bit-identical).
   bool p2 = false;
   int64_t n = 0, nseg = 0;
+  // adaptive sims: the re-grid's topology build does not wait for the
+  // segment count; nseg is then an upper bound (4 n) for launch sizes, the
+  // true count is nseg_dev[0] on the device and lands in host->nseg (page-
+  // locked) at the next host sync, when nseg_lazy is cleared
+  DBuf<long long> nseg_dev;
+  bool nseg_lazy = false;
+  // page-locked host slots for readbacks that ride on one sync: the clock,
+  // the new leaf count of an adapt, the segment count
+  struct HostSlots {
+    DevClock clk;
+    long long n_new, nseg;
+  };
+  HostSlots* host = nullptr;
+  HostSlots& slots();
+  void settle_nseg() {  // after a host sync
+    if (nseg_lazy) {
+      nseg = host->nseg;
+      nseg_lazy = false;
+    }
+  }
   int64_t nseg_inner = 0;  // shards: leading local segments with both leaves owned
   // leaves (device Morton order) and state
   DBuf<int8_t> lvl;
@@ -277,6 +300,11 @@ int64_t scan_exclusive(const int32_t* in, int32_t* out, int64_t n);
 // adaptive (adaptive.cu)
 void adaptive_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem);
 void adaptive_adapt(Sim& s, double t);
+// adaptive_adapt in two halves around one host sync: the device-sized prefix
+// (its new leaf count copied to s.slots().n_new), then, after the caller's
+// sync, the transfer and the topology of the new leaf set
+void adaptive_adapt_begin(Sim& s);
+void adaptive_adapt_finish(Sim& s, double t);
 
 // uniform (uniform.cu)
 void uniform_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem);

@@ -211,7 +211,7 @@ __device__ __forceinline__ void store_details(const double* __restrict__ sdet, d
 }
 
 #ifndef FM_ENC_MINB
-#define FM_ENC_MINB 5  // 51 registers (A/B on B200: MRA 2.31 -> 1.69 ms)
+#define FM_ENC_MINB 6  // 40 registers (A/B on B200: MINB 5 -> 6: MRA 1.427 -> 1.402 ms; 4: 1.471)
 #endif
 #ifndef FM_ENC_T
 #define FM_ENC_T 5  // levels per encode pass (4^(T-1) threads per CTA)

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClo
                                              const double* __restrict__ in, double* __restrict__ out,
                                              int manual, int* err, long long q0, long long q1) {
   const long long q = q0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (q >= q1) return;
+  if (q >= q1 || (v.nseg_dev && q >= *v.nseg_dev)) return;  // adaptive: q1 is an upper bound
   const int a = v.seg_l[q], b = v.seg_r[q];  // W/S and E/N leaf (loaded before the active check)
 #if FM_NO_EXIT
   const bool act = manual || clk[1].active;

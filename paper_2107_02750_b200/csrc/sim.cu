@@ -115,7 +115,18 @@ __global__ void k_finite(long long n, const int8_t* __restrict__ lvl, const int3
 
 }  // namespace
 
+Sim::HostSlots& Sim::slots() {
+  if (!host) {
+    void* p = nullptr;
+    FM_CUDA(cudaMallocHost(&p, sizeof(HostSlots)));
+    host = static_cast<HostSlots*>(p);
+    *host = HostSlots{};
+  }
+  return *host;
+}
+
 Sim::~Sim() {
+  if (host) cudaFreeHost(host);
   if (shard && shard->comm) comm_forget(shard->comm, this);
   for (auto& g : gexec)
     if (g) cudaGraphExecDestroy(g);
@@ -160,6 +171,7 @@ NuView Sim::view() const {
   v.sid = sid.p;
   v.segst = segst.p;
   v.nseg = nseg;
+  v.nseg_dev = nseg_lazy ? nseg_dev.p : nullptr;
   return v;
 }
 
@@ -663,17 +675,32 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
   cudaEvent_t e0 = ev.a, e1 = ev.b;
   FM_CUDA(cudaEventRecord(e0, st));
   if (s.adaptive) {
-    // adapt between steps on the host-driven path (device kernels, host sequencing)
+    // adapt between steps on the host-driven path (device kernels, host
+    // sequencing), ONE host sync per step: when an adapt is due, its
+    // device-sized prefix is launched right behind the step, speculatively,
+    // and the step's clock and the prefix's new leaf count come back together.
+    // A prefix whose step turns out inactive (or the last one) is dropped: it
+    // wrote only the grid's own buffers, which the next adapt rebuilds from
+    // the sim's leaves, and the sim's state is untouched.
+    Sim::HostSlots& hs = s.slots();
     for (int64_t k = 0; k < max_steps; ++k) {
       launch_step(s, false, 0.0, err.p);
-      DevClock c;
-      read_clock(s, c);
-      FM_CUDA(cudaStreamSynchronize(st));
-      if (!c.active || !c.had_step) break;
-      s.since_adapt += 1;
-      if (s.since_adapt >= s.adapt_every && !(c.now >= c.end_time)) {
+      const bool due = s.since_adapt + 1 >= s.adapt_every;
+      if (due) {
         state_to_u(s);
-        adaptive_adapt(s, c.now);
+        adaptive_adapt_begin(s);
+      }
+      FM_CUDA(cudaMemcpyAsync(&hs.clk, s.clk.p + 1, sizeof(DevClock), cudaMemcpyDeviceToHost, st));
+      FM_CUDA(cudaStreamSynchronize(st));
+      s.settle_nseg();
+      const DevClock c = hs.clk;
+      if (!c.active || !c.had_step) {
+        if (due) state_to_step(s);
+        break;
+      }
+      s.since_adapt += 1;
+      if (due && !(c.now >= c.end_time)) {
+        adaptive_adapt_finish(s, c.now);
         state_to_step(s);
         s.since_adapt = 0;
         // the adapt changed the leaf set: refresh the step's reductions
@@ -681,6 +708,8 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
         k_red_reset<<<1, 1, 0, st>>>(s.red.p, int(c.steps & 1));
         FM_LAUNCHED();
         launch_reduce_init(s);
+      } else if (due) {
+        state_to_step(s);  // the last step: the speculative prefix is dropped
       }
     }
   } else if (shard_eager(s)) {
@@ -744,6 +773,7 @@ void sim_run(Sim& s, fm_clock* ck, int64_t max_steps, int stop_at_events, fm_run
   int herr = 0;
   err.download(&herr, 1);
   FM_CUDA(cudaStreamSynchronize(st));
+  s.settle_nseg();
   s.last_run_ms = elapsed_ms(e0, e1);
   if (herr) throw Error(FM_ERR_DOMAIN, "hll_flux: negative depth");
   ck->now = c.now;

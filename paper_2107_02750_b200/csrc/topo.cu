@@ -152,9 +152,9 @@ __global__ void k_segments(long long n, const int32_t* __restrict__ li,
 __global__ void k_seg_geo(long long nseg, int L, const int32_t* __restrict__ seg_l,
                           const int32_t* __restrict__ seg_r, const int8_t* __restrict__ lvl,
                           const int32_t* __restrict__ li, const int32_t* __restrict__ lj,
-                          uint8_t* __restrict__ geo) {
+                          uint8_t* __restrict__ geo, const long long* __restrict__ nsd) {
   const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (q >= nseg) return;
+  if (q >= nseg || (nsd && q >= *nsd)) return;
   const int a = seg_l[q], b = seg_r[q];
   const int la = lvl[a], lb = lvl[b];
   const int ia = li[a], ja = lj[a], ib = li[b], jb = lj[b];
@@ -169,9 +169,10 @@ __global__ void k_seg_geo(long long nseg, int L, const int32_t* __restrict__ seg
 // (limit_at, solver_nonuniform.cpp:52-66): the topography never changes on a
 // static grid, so k_seg reads these 16 B instead of both leaves' z rows.
 __global__ void k_seg_z(long long nseg, const int32_t* __restrict__ seg_l, const int32_t* __restrict__ seg_r,
-                        const uint8_t* __restrict__ geo, const double* __restrict__ z, double2* __restrict__ out) {
+                        const uint8_t* __restrict__ geo, const double* __restrict__ z, double2* __restrict__ out,
+                        const long long* __restrict__ nsd) {
   const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (q >= nseg) return;
+  if (q >= nseg || (nsd && q >= *nsd)) return;
   const int a = seg_l[q], b = seg_r[q];
   const int gc = geo[q];
   const bool xn = gc & 1;
@@ -335,7 +336,7 @@ void build_seg_geo(Sim& s) {
   s.seg_geo.ensure(std::max<int64_t>(s.nseg, 1));
   if (s.nseg) {
     k_seg_geo<<<nblk(s.nseg, 256), 256, 0, stream()>>>(s.nseg, s.L, s.seg_l.p, s.seg_r.p, s.lvl.p, s.li.p,
-                                                      s.lj.p, s.seg_geo.p);
+                                                      s.lj.p, s.seg_geo.p, s.nseg_lazy ? s.nseg_dev.p : nullptr);
     FM_LAUNCHED();
   }
 }
@@ -350,7 +351,8 @@ void build_seg_z(Sim& s) {
   if (s.nseg && s.p2) {
     s.segz.ensure(2 * size_t(s.nseg));
     k_seg_z<<<nblk(s.nseg, 256), 256, 0, stream()>>>(s.nseg, s.seg_l.p, s.seg_r.p, s.seg_geo.p, s.z.p,
-                                                    reinterpret_cast<double2*>(s.segz.p));
+                                                    reinterpret_cast<double2*>(s.segz.p),
+                                                    s.nseg_lazy ? s.nseg_dev.p : nullptr);
     FM_LAUNCHED();
   }
 }
@@ -364,17 +366,32 @@ void build_topology(Sim& s, const Grid& g) {
   DBuf<int32_t> owned(n), base(n);
   // [0]: segment total (scan), [1]: the ungraded-grid error flag; one sync for both
   DBuf<long long> tot2(2);
-  tot2.zero();
+  // an adaptive re-grid keeps the total on the device and does not wait for
+  // it: its grid is graded by construction (grade_flags in the adapt's
+  // prefix), and the segment launches take an upper bound (a leaf is the
+  // finer-or-equal side of at most one segment per side: nseg <= 4 n) with
+  // the true count read on the device (NuView::nseg_dev)
+  const bool lazy = s.adaptive;
+  if (lazy) s.nseg_dev.ensure(2);
+  long long* tot = lazy ? s.nseg_dev.p : tot2.p;
+  FM_CUDA(cudaMemsetAsync(tot, 0, 2 * sizeof(long long), st));
   const TopoIn t = topo_in(g);
   k_topo<<<nblk(n, 256), 256, 0, st>>>(t, n, s.lvl.p, s.li.p, s.lj.p, s.nb.p, s.sk.p, owned.p,
-                                        reinterpret_cast<int*>(tot2.p + 1));
+                                        reinterpret_cast<int*>(tot + 1));
   FM_LAUNCHED();
-  scan_exclusive_async(owned.p, base.p, n, tot2.p);
-  long long h2[2] = {0, 0};
-  tot2.download(h2, 2);
-  FM_CUDA(cudaStreamSynchronize(st));
-  s.nseg = h2[0];
-  if (h2[1]) throw Error(FM_ERR_STRUCTURE, "non-uniform solvers require a graded (2:1) grid");
+  scan_exclusive_async(owned.p, base.p, n, tot);
+  if (lazy) {
+    s.nseg = std::max<int64_t>(4 * n, 1);
+    s.nseg_lazy = true;
+    FM_CUDA(cudaMemcpyAsync(&s.slots().nseg, tot, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  } else {
+    long long h2[2] = {0, 0};
+    tot2.download(h2, 2);
+    FM_CUDA(cudaStreamSynchronize(st));
+    s.nseg = h2[0];
+    s.nseg_lazy = false;
+    if (h2[1]) throw Error(FM_ERR_STRUCTURE, "non-uniform solvers require a graded (2:1) grid");
+  }
   {
     s.sid.ensure(8 * n);
     s.seg_l.ensure(std::max<int64_t>(s.nseg, 1));
