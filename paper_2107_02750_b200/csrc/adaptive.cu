@@ -20,10 +20,13 @@
 //                           bit-for-bit (the encode_up copy of the old leaf IS
 //                           the old value)
 //   remap + rebuild_topology (:173-202, solver_nonuniform.cpp:521-527):
-//                           resolve_manning, resolve_inflows, build_topology,
-//                           and the encode_pairing partner z* of two-segment
-//                           sides (region_topo, solver_nonuniform.cpp:80-89)
-//                           from a z encode-up pyramid (ZpyrBody, k_zpair).
+//                           the Manning values and inflow targets of the new
+//                           leaves in the transfer's install, then
+//                           build_topology with the encode_pairing partner z*
+//                           of two-segment sides (region_topo,
+//                           solver_nonuniform.cpp:80-89, from a z encode-up
+//                           pyramid, ZpyrBody) and the segment statics written
+//                           in its segment pass.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -33,6 +36,7 @@
 
 #include "fm_device.cuh"
 #include "fm_sim.hpp"
+#include "leafinfo.cuh"
 #include "levels.cuh"
 
 using namespace fmd;
@@ -126,32 +130,6 @@ __global__ void k_norms(const long long* __restrict__ dn, const double* __restri
 }
 
 
-struct ZpTab {
-  const double* zp[16];
-};
-
-// partner z* for two-segment sides: max(me.z, face_limit(region_topo, opposite))
-// (side_effective, solver_nonuniform.cpp:155-163) — the face_limit part.
-__global__ void k_zpair(long long n, int M, const int8_t* __restrict__ lvl,
-                        const int32_t* __restrict__ li, const int32_t* __restrict__ lj,
-                        const uint8_t* __restrict__ sk, ZpTab t, double* __restrict__ zpair) {
-  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int l = lvl[k], i = li[k], j = lj[k];
-  const uint8_t code = sk[k];
-#pragma unroll
-  for (int sd = 0; sd < 4; ++sd) {
-    double v = 0.0;
-    if (((code >> (2 * sd)) & 3) == 3) {
-      const int ni = i + (sd == 1 ? 1 : sd == 3 ? -1 : 0);
-      const int nj = j + (sd == 0 ? 1 : sd == 2 ? -1 : 0);
-      const double* p = t.zp[l] + 3 * node_index(l, ni, nj, M);
-      v = face_val(P3{p[0], p[1], p[2]}, (sd + 2) & 3);
-    }
-    zpair[4 * k + sd] = v;
-  }
-}
-
 __global__ void k_all_ones(uint64_t n, uint8_t* f) {
   const uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (k < n) f[k] = 1;
@@ -190,6 +168,15 @@ struct Install {
   int32_t* lj;
   double* z;
   const double* gz;  // the grid's leaf topography
+  // the new leaf set's Manning values and inflow target counts, computed as
+  // each leaf is installed (resolve_manning / resolve_inflows fused)
+  double* nman;
+  const double* mr;  // cell-centred raster (null: uniform `manning`)
+  int mr_nc, mr_nr, L, ninflow;
+  double mr_xll, mr_yll, mr_cs, manning, R, x0, y0;
+  int32_t* infc;     // ninflow x n
+  long long n;
+  int rect[4 * kMaxInflows];
 };
 
 struct LvTab {
@@ -324,6 +311,15 @@ __global__ void __launch_bounds__(256) k_transfer_leaves(LvTab t, long long n, c
     zo[1] = t.zero_slopes ? 0.0 : zg[1];
     zo[2] = t.zero_slopes ? 0.0 : zg[2];
     if (t.zero_slopes) v[1] = v[2] = v[4] = v[5] = v[7] = v[8] = 0.0;
+    const Install& in = t.inst;
+    if (in.nman) {
+      const int i = li[k], j = lj[k];
+      in.nman[k] = manning_at(in.L, in.R, in.x0, in.y0, l, i, j, in.mr, in.mr_nc, in.mr_nr, in.mr_xll,
+                              in.mr_yll, in.mr_cs, in.manning);
+      for (int f = 0; f < in.ninflow; ++f)
+        in.infc[f * in.n + k] = inflow_overlap(in.L, l, i, j, in.rect[4 * f], in.rect[4 * f + 1],
+                                               in.rect[4 * f + 2], in.rect[4 * f + 3]);
+    }
   }
 #pragma unroll
   for (int q = 0; q < 9; ++q) o[q] = v[q];
@@ -472,24 +468,16 @@ LvTab lv_tab(Sim& s, Grid& g, AdaptState& a) {
   return t;
 }
 
-// remap_after_adapt + rebuild_topology + encode_pairing partners
+// rebuild_topology + encode_pairing partners (the remap of the Manning values
+// and inflow targets ran in the transfer): one segment pass also writes the
+// segment statics, the side limits and the z* partners from the z encode-up
+// pyramid (built in the adapt's prefix graph, right after the leaf list)
 void refresh_topology(Sim& s) {
-  cudaStream_t st = stream();
   Grid& g = *s.grid;
   AdaptState& a = *s.ad;
-  s.nman.ensure(s.n);
-  resolve_manning(s);
-  resolve_inflows(s, g);
-  build_topology(s, g);
-  build_seg_z(s);
-  // the partner values from the z encode-up pyramid (built in the adapt's
-  // prefix graph, right after the leaf list)
-  const int L = s.L;
-  ZpTab t{};
-  for (int l = 0; l < L; ++l) t.zp[l] = a.zp[l].p;
-  s.zpair.ensure(4 * s.n);
-  k_zpair<<<nblk(s.n, 256), 256, 0, st>>>(s.n, s.M, s.lvl.p, s.li.p, s.lj.p, s.sk.p, t, s.zpair.p);
-  FM_LAUNCHED();
+  const double* zp[16] = {};
+  for (int l = 0; l < s.L && l < 16; ++l) zp[l] = a.zp[l].p;
+  build_topology(s, g, zp);
 }
 
 }  // namespace
@@ -771,7 +759,32 @@ void adaptive_adapt_finish(Sim& s, double t) {
   LvTab tab = lv_tab(s, g, a);
   tab.unew = s.u.p;
   tab.do_install = 1;
-  tab.inst = Install{s.lvl.p, s.li.p, s.lj.p, s.z.p, g.lf_z.p};
+  s.nman.ensure(s.n);
+  s.infc.ensure(std::max<int64_t>(1, int64_t(s.ninflow) * s.n));
+  if (s.ninflow == 0) s.infc.zero();
+  Install in{};
+  in.lvl = s.lvl.p;
+  in.li = s.li.p;
+  in.lj = s.lj.p;
+  in.z = s.z.p;
+  in.gz = g.lf_z.p;
+  in.nman = s.nman.p;
+  in.mr = s.has_mr ? (s.mr_ext ? s.mr_ext : s.mr.p) : nullptr;
+  in.mr_nc = s.mr_ncols;
+  in.mr_nr = s.mr_nrows;
+  in.L = s.L;
+  in.ninflow = s.ninflow;
+  in.mr_xll = s.mr_xll;
+  in.mr_yll = s.mr_yll;
+  in.mr_cs = s.mr_cs;
+  in.manning = s.manning;
+  in.R = s.R;
+  in.x0 = s.x0;
+  in.y0 = s.y0;
+  in.infc = s.infc.p;
+  in.n = s.n;
+  for (int q = 0; q < 4 * s.ninflow && q < 4 * kMaxInflows; ++q) in.rect[q] = s.rect[q];
+  tab.inst = in;
   tab.zero_slopes = s.scheme != FM_DG2 ? 1 : 0;
   if (n_new) {
     if (a.kind == 0)

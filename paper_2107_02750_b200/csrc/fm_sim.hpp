@@ -130,6 +130,8 @@ struct Sim {
   // locked) at the next host sync, when nseg_lazy is cleared
   DBuf<long long> nseg_dev;
   bool nseg_lazy = false;
+  DBuf<int32_t> topo_owned, topo_base;  // adaptive: build_topology's scratch, kept
+  DBuf<long long> topo_sums;
   // page-locked host slots for readbacks that ride on one sync: the clock,
   // the new leaf count of an adapt, the segment count
   struct HostSlots {
@@ -290,7 +292,9 @@ double shard_allreduce_sum(Sim& s, double v);
 void group_run(const std::vector<Sim*>& sims, fm_clock* clk, int64_t max_steps, int stop_at_events,
                fm_run_result* out);
 // topology (topo.cu)
-void build_topology(Sim& s, const Grid& g);
+// zp (adaptive re-grids): the z encode-up pyramid per level; the segment
+// pass then also writes the segment statics, side limits and z* partners
+void build_topology(Sim& s, const Grid& g, const double* const* zp = nullptr);
 void build_seg_geo(Sim& s);  // after seg_l / seg_r and the leaf keys are final
 void build_seg_z(Sim& s);    // after build_seg_geo and the final topography z
 void resolve_inflows(Sim& s, const Grid& g);

@@ -16,6 +16,7 @@
 // enumerate_faces (quadgrid.cpp:206-208).
 #include "fm_device.cuh"
 #include "fm_sim.hpp"
+#include "leafinfo.cuh"
 #include "step_common.cuh"
 
 using namespace fmd;
@@ -107,15 +108,46 @@ __device__ __forceinline__ int owned_before(uint8_t code, int sd) {
   return s;
 }
 
+// The adaptive re-grid's extra per-leaf / per-segment statics, computed in
+// the segment pass (one launch instead of four): the owned segments'
+// geometry byte and (P2) topography limits, the leaf's side topography
+// limits (P2) and its encode_pairing partners z* for two-segment sides
+// (side_effective, solver_nonuniform.cpp:155-163: face_limit of region_topo).
+struct SegExtras {
+  uint8_t* geo;       // null: not fused
+  double2* segz;      // P2 only
+  double* zside;      // P2 only
+  double* zpair;      // 4 per leaf
+  const double* zp[16];  // the z encode-up pyramid per level (3 per node)
+  const double* z;
+  const int8_t* lvl;
+  int L, M;
+};
+
 // Segment ids per leaf side + the owned segments' (left, right) leaves.
 __global__ void k_segments(long long n, const int32_t* __restrict__ li,
                            const int32_t* __restrict__ lj, const int32_t* __restrict__ nb,
                            const uint8_t* __restrict__ sk, const int32_t* __restrict__ base,
                            int32_t* __restrict__ sid, int32_t* __restrict__ seg_l,
-                           int32_t* __restrict__ seg_r) {
+                           int32_t* __restrict__ seg_r, SegExtras ex) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= n) return;
   const uint8_t code = sk[k];
+  const bool fused = ex.geo != nullptr;
+  int lk = 0, ik = 0, jk = 0;
+  if (fused) {
+    lk = ex.lvl[k];
+    ik = li[k];
+    jk = lj[k];
+  }
+  // an owned segment's statics from its two leaves (fused mode)
+  auto statics = [&](int32_t q, int32_t a, int32_t b) {
+    const int la = a == k ? lk : ex.lvl[a], ia = a == k ? ik : li[a], ja = a == k ? jk : lj[a];
+    const int lb = b == k ? lk : ex.lvl[b], ib = b == k ? ik : li[b], jb = b == k ? jk : lj[b];
+    const uint8_t gc = seg_geo_code(ex.L, la, ia, ja, lb, ib, jb);
+    ex.geo[q] = gc;
+    if (ex.segz) ex.segz[q] = seg_z2(gc, ex.z + 3 * (long long)a, ex.z + 3 * (long long)b);
+  };
   for (int sd = 0; sd < 4; ++sd) {
     const int kind = (code >> (2 * sd)) & 3;
     int a = -1, b = -1;
@@ -126,10 +158,12 @@ __global__ void k_segments(long long n, const int32_t* __restrict__ li,
       a = s0;
       seg_l[s0] = mine_left ? int32_t(k) : n0;
       seg_r[s0] = mine_left ? n0 : int32_t(k);
+      if (fused) statics(s0, mine_left ? int32_t(k) : n0, mine_left ? n0 : int32_t(k));
       if (kind == 3) {
         b = s0 + 1;
         seg_l[s0 + 1] = mine_left ? int32_t(k) : n1;
         seg_r[s0 + 1] = mine_left ? n1 : int32_t(k);
+        if (fused) statics(s0 + 1, mine_left ? int32_t(k) : n1, mine_left ? n1 : int32_t(k));
       }
     } else if (kind == 2) {
       const int opp = (sd + 2) & 3;
@@ -141,7 +175,19 @@ __global__ void k_segments(long long n, const int32_t* __restrict__ li,
     }
     sid[8 * k + 2 * sd] = a;
     sid[8 * k + 2 * sd + 1] = b;
+    if (fused) {
+      // k_zpair: the partner z* of a two-segment side
+      double v = 0.0;
+      if (kind == 3) {
+        const int ni = ik + (sd == 1 ? 1 : sd == 3 ? -1 : 0);
+        const int nj = jk + (sd == 0 ? 1 : sd == 2 ? -1 : 0);
+        const double* p = ex.zp[lk] + 3 * node_index(lk, ni, nj, ex.M);
+        v = face_val(P3{p[0], p[1], p[2]}, (sd + 2) & 3);
+      }
+      ex.zpair[4 * k + sd] = v;
+    }
   }
+  if (fused && ex.zside) side_z4(ex.z + 3 * k, ex.zside + 4 * k);
 }
 
 // Static per-segment geometry for the segment kernel (k_seg, P2 geometry):
@@ -156,12 +202,7 @@ __global__ void k_seg_geo(long long nseg, int L, const int32_t* __restrict__ seg
   const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (q >= nseg || (nsd && q >= *nsd)) return;
   const int a = seg_l[q], b = seg_r[q];
-  const int la = lvl[a], lb = lvl[b];
-  const int ia = li[a], ja = lj[a], ib = li[b], jb = lj[b];
-  const bool xn = (ib << (L - lb)) == ((ia + 1) << (L - la));
-  const int ta = la < lb ? ((((xn ? jb : ib) & 1) ? 2 : 1)) : 0;
-  const int tb = lb < la ? ((((xn ? ja : ia) & 1) ? 2 : 1)) : 0;
-  geo[q] = uint8_t((xn ? 1 : 0) | (ta << 1) | (tb << 3));
+  geo[q] = seg_geo_code(L, lvl[a], li[a], lj[a], lvl[b], li[b], lj[b]);
 }
 
 // Static topography limits of every segment (P2 geometry): z of each leaf's
@@ -173,28 +214,15 @@ __global__ void k_seg_z(long long nseg, const int32_t* __restrict__ seg_l, const
                         const long long* __restrict__ nsd) {
   const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (q >= nseg || (nsd && q >= *nsd)) return;
-  const int a = seg_l[q], b = seg_r[q];
-  const int gc = geo[q];
-  const bool xn = gc & 1;
-  const int ca = (gc >> 1) & 3, cb = (gc >> 3) & 3;
-  const double ta = ca == 0 ? 0.0 : ca == 2 ? 0.25 : -0.25;
-  const double tb = cb == 0 ? 0.0 : cb == 2 ? 0.25 : -0.25;
-  const double* za = z + 3 * (long long)a;
-  const double* zb = z + 3 * (long long)b;
-  out[q] = make_double2(eval_rel(za[0], za[1], za[2], xn ? 0.5 : ta, xn ? ta : 0.5),
-                        eval_rel(zb[0], zb[1], zb[2], xn ? -0.5 : tb, xn ? tb : -0.5));
+  out[q] = seg_z2(geo[q], z + 3 * (long long)seg_l[q], z + 3 * (long long)seg_r[q]);
 }
 
 // ... and of every leaf side: z of the leaf's plane at its side midpoints
-// (N E S W), as k_stage's side evaluation (limit_rel at (0, 1/2), (1/2, 0),
-// (0, -1/2), (-1/2, 0)) would compute it.
+// (N E S W), as k_stage's side evaluation would compute it.
 __global__ void k_side_z(long long n, const double* __restrict__ z, double* __restrict__ out) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const double* p = z + 3 * k;
-  double2* o = reinterpret_cast<double2*>(out + 4 * k);
-  o[0] = make_double2(eval_rel(p[0], p[1], p[2], 0.0, 0.5), eval_rel(p[0], p[1], p[2], 0.5, 0.0));
-  o[1] = make_double2(eval_rel(p[0], p[1], p[2], 0.0, -0.5), eval_rel(p[0], p[1], p[2], -0.5, 0.0));
+  side_z4(z + 3 * k, out + 4 * k);
 }
 
 // --- scan -----------------------------------------------------------------
@@ -261,12 +289,7 @@ __global__ void k_inflow_overlap(long long n, int L, const int8_t* __restrict__ 
                                  int j0, int i1, int j1, int32_t* __restrict__ cnt) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const int sh = L - lvl[k];
-  const long long x0 = (long long)li[k] << sh, x1 = x0 + (1ll << sh);
-  const long long y0 = (long long)lj[k] << sh, y1 = y0 + (1ll << sh);
-  const long long wx = max(0ll, min(x1, (long long)i1 + 1) - max(x0, (long long)i0));
-  const long long wy = max(0ll, min(y1, (long long)j1 + 1) - max(y0, (long long)j0));
-  cnt[k] = int32_t(wx * wy);
+  cnt[k] = inflow_overlap(L, lvl[k], li[k], lj[k], i0, j0, i1, j1);
 }
 
 // Manning per leaf from a cell-centred raster (solver_nonuniform.cpp:575-584).
@@ -277,16 +300,7 @@ __global__ void k_manning(long long n, int L, double R, double x0, double y0,
                           double* __restrict__ out) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= n) return;
-  if (!mr) {
-    out[k] = uniform;
-    return;
-  }
-  const int l = lvl[k];
-  const double xc = x0 + (li[k] + 0.5) * R * double(1 << (L - l));
-  const double yc = y0 + (lj[k] + 0.5) * R * double(1 << (L - l));
-  const int col = min(max(int((xc - xll) / cs), 0), nc - 1);
-  const int row = min(max(nr - 1 - int((yc - yll) / cs), 0), nr - 1);
-  out[k] = mr[size_t(row) * nc + col];
+  out[k] = manning_at(L, R, x0, y0, lvl[k], li[k], lj[k], mr, nc, nr, xll, yll, cs, uniform);
 }
 
 TopoIn topo_in(const Grid& g) {
@@ -306,7 +320,8 @@ inline unsigned nblk(long long n, int t) { return unsigned((n + t - 1) / t); }
 }  // namespace
 
 // Exclusive scan; the total lands in *total_dev (device), no host sync.
-void scan_exclusive_async(const int32_t* in, int32_t* out, int64_t n, long long* total_dev) {
+void scan_exclusive_async(const int32_t* in, int32_t* out, int64_t n, long long* total_dev,
+                          DBuf<long long>* scratch = nullptr) {
   cudaStream_t st = stream();
   const int T = 1024;
   const long long nb = (n + T - 1) / T;
@@ -314,7 +329,9 @@ void scan_exclusive_async(const int32_t* in, int32_t* out, int64_t n, long long*
     FM_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(long long), st));
     return;
   }
-  DBuf<long long> sums(std::max<long long>(nb, 1));
+  DBuf<long long> own;
+  DBuf<long long>& sums = scratch ? *scratch : own;
+  sums.ensure(std::max<long long>(nb, 1));
   k_block_sums<<<unsigned(nb), T, 0, st>>>(in, n, sums.p);
   FM_LAUNCHED();
   k_scan_sums<<<1, 1024, 0, st>>>(sums.p, nb, total_dev);
@@ -357,15 +374,21 @@ void build_seg_z(Sim& s) {
   }
 }
 
-void build_topology(Sim& s, const Grid& g) {
+void build_topology(Sim& s, const Grid& g, const double* const* zp) {
   FM_RANGE("build_topology");
   cudaStream_t st = stream();
   const long long n = s.n;
   s.nb.ensure(8 * n);
   s.sk.ensure(n);
-  DBuf<int32_t> owned(n), base(n);
+  // adaptive re-grids keep the scratch (no allocation calls per adapt: the
+  // host enqueues this work right after the adapt's sync, with the GPU idle)
+  DBuf<int32_t> owned_tmp, base_tmp;
+  DBuf<int32_t>& owned = s.adaptive ? s.topo_owned : owned_tmp;
+  DBuf<int32_t>& base = s.adaptive ? s.topo_base : base_tmp;
+  owned.ensure(n);
+  base.ensure(n);
   // [0]: segment total (scan), [1]: the ungraded-grid error flag; one sync for both
-  DBuf<long long> tot2(2);
+  DBuf<long long> tot2(s.adaptive ? 0 : 2);
   // an adaptive re-grid keeps the total on the device and does not wait for
   // it: its grid is graded by construction (grade_flags in the adapt's
   // prefix), and the segment launches take an upper bound (a leaf is the
@@ -379,7 +402,7 @@ void build_topology(Sim& s, const Grid& g) {
   k_topo<<<nblk(n, 256), 256, 0, st>>>(t, n, s.lvl.p, s.li.p, s.lj.p, s.nb.p, s.sk.p, owned.p,
                                         reinterpret_cast<int*>(tot + 1));
   FM_LAUNCHED();
-  scan_exclusive_async(owned.p, base.p, n, tot);
+  scan_exclusive_async(owned.p, base.p, n, tot, s.adaptive ? &s.topo_sums : nullptr);
   if (lazy) {
     s.nseg = std::max<int64_t>(4 * n, 1);
     s.nseg_lazy = true;
@@ -396,10 +419,30 @@ void build_topology(Sim& s, const Grid& g) {
     s.sid.ensure(8 * n);
     s.seg_l.ensure(std::max<int64_t>(s.nseg, 1));
     s.seg_r.ensure(std::max<int64_t>(s.nseg, 1));
+    SegExtras ex{};
+    if (zp) {
+      // the adaptive re-grid: the segment statics, side limits and pairing
+      // partners in this pass (build_seg_geo / build_seg_z / k_zpair fused)
+      s.seg_geo.ensure(std::max<int64_t>(s.nseg, 1));
+      s.zpair.ensure(4 * size_t(n));
+      ex.geo = s.seg_geo.p;
+      if (s.p2) {
+        s.segz.ensure(2 * size_t(std::max<int64_t>(s.nseg, 1)));
+        s.zside.ensure(4 * size_t(n));
+        ex.segz = reinterpret_cast<double2*>(s.segz.p);
+        ex.zside = s.zside.p;
+      }
+      ex.zpair = s.zpair.p;
+      for (int l = 0; l < s.L && l < 16; ++l) ex.zp[l] = zp[l];
+      ex.z = s.z.p;
+      ex.lvl = s.lvl.p;
+      ex.L = s.L;
+      ex.M = s.M;
+    }
     k_segments<<<nblk(n, 256), 256, 0, st>>>(n, s.li.p, s.lj.p, s.nb.p, s.sk.p, base.p, s.sid.p,
-                                              s.seg_l.p, s.seg_r.p);
+                                              s.seg_l.p, s.seg_r.p, ex);
     FM_LAUNCHED();
-    build_seg_geo(s);
+    if (!zp) build_seg_geo(s);
     if (s.scheme != FM_ACC) s.segst.ensure(6 * size_t(std::max<int64_t>(s.nseg, 1)));
   }
 }
