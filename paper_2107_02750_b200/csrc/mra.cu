@@ -514,7 +514,10 @@ namespace {
 // The middle levels of the top-down decode as subtrees (adaptive.cu's
 // k_levels_tree): CTA b owns level-r node b and decodes its subtree down to
 // level rt, a block barrier between levels instead of a launch per level.
-constexpr int kTreeThreads = 64;
+#ifndef FM_TREE_THREADS
+#define FM_TREE_THREADS 64
+#endif
+constexpr int kTreeThreads = FM_TREE_THREADS;
 __global__ void __launch_bounds__(kTreeThreads) k_topdown_tree(LevelPtrs p, int r, int rt, int L, int M, int kind,
                                                                LeafOut out) {
   const uint64_t b = blockIdx.x;
