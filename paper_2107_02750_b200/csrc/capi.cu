@@ -109,10 +109,14 @@ __global__ void k_selftest_div(int which, int64_t n, uint64_t seed, unsigned lon
     if (__double_as_longlong(q1) != __double_as_longlong(r1)) atomicAdd(fails, 1ull);
     return;
   }
-  if (which == 2) {  // the shared-divisor path of zdiv2 (fmd::zquot_ieee)
-    const double q2 = fmd::div_fast_ok(b) ? fmd::zquot_ieee(a, b, fmd::recip_ieee(b)) : fmd::zdiv(a, b);
-    const double r2 = a == 0.0 ? a : a / b;
-    if (__double_as_longlong(q2) != __double_as_longlong(r2)) atomicAdd(fails, 1ull);
+  if (which == 2) {  // the shared-divisor division fmd::zdiv2, both quotients
+    const uint64_t c1 = mix64(b2), c2 = mix64(c1);
+    const double a2 = rand_operand(c1, c2);
+    double q1, q2;
+    fmd::zdiv2(a, a2, b, q1, q2);
+    const double r1 = a == 0.0 ? a : a / b, r2 = a2 == 0.0 ? a2 : a2 / b;
+    if (__double_as_longlong(q1) != __double_as_longlong(r1) || __double_as_longlong(q2) != __double_as_longlong(r2))
+      atomicAdd(fails, 1ull);
     return;
   }
   // the inline division kernel builds use with -DFM_INLINE_DIV (fmd::quot)
