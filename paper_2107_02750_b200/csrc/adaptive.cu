@@ -6,7 +6,7 @@
 // passes run each large level as one launch and all levels of <= 256 nodes in
 // one single-CTA launch (run_levels); level-independent passes run every level
 // in one launch (run_levels_flat):
-//   norms        (:139-144) k_norms (exact max reductions)
+//   norms        (:139-144) in k_mark_leaves_dn (exact max reductions)
 //   encode_up    (:16-57)   k_mark_leaves + EncodeFlagBody per level, which
 //   flag         (:59-73)   also flags the node (static topography significance
 //                           precomputed once: max(a,b) >= eps <=> a >= eps || b >= eps)
@@ -51,7 +51,10 @@ struct AdaptState {
   int kind = 0;
   double eps = 1e-3;
   std::vector<DBuf<uint8_t>> zsig;   // [L] static topography significance
-  std::vector<DBuf<uint8_t>> known;  // [L+1] 0 unknown, 1 leaf, 2 internal
+  // [L+1] 0 unknown, 1 leaf, 2 internal: every level in one allocation
+  // (known_all), so an adapt clears them all with one memset
+  DBuf<uint8_t> known_all;
+  std::vector<uint8_t*> known;
   std::vector<DBuf<double>> sc;      // [L+1] flow scaling, 9 per node
   std::vector<DBuf<double>> fdet;    // [L] flow details, 27 per node
   std::vector<DBuf<double>> zp;      // [L] z encode-up pyramid, 3 per node
@@ -80,40 +83,15 @@ struct PtrTab {
   double* sc[16];
 };
 
-// the leaf count from the device (graph replays): grid-stride
-__global__ void k_mark_leaves_dn(const long long* __restrict__ dn, int M, const int8_t* __restrict__ lvl,
-                                 const int32_t* __restrict__ li, const int32_t* __restrict__ lj,
-                                 const double* __restrict__ u, PtrTab t) {
-  const long long n = dn[0];
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
-       k += (long long)gridDim.x * blockDim.x) {
-    const int l = lvl[k];
-    const uint64_t node = node_index(l, li[k], lj[k], M);
-    t.known[l][node] = 1;
-    double* o = t.sc[l] + 9 * node;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) o[q] = u[9 * k + q];
-  }
-}
-
-__global__ void k_norms(const long long* __restrict__ dn, const double* __restrict__ u,
-                        unsigned long long* out) {
-  const long long n = dn[0];
-  double a = 0.0, b = 0.0, c = 0.0;
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
-       k += (long long)gridDim.x * blockDim.x) {
-    a = smax(a, fabs(u[9 * k]));
-    b = smax(b, fabs(u[9 * k + 3]));
-    c = smax(c, fabs(u[9 * k + 6]));
-  }
+// max over the block of three non-negative values as bit patterns, one
+// atomicMax per field (per-warp atomics on three addresses serialised ~9k
+// atomics per adapt)
+__device__ __forceinline__ void block_max3(double a, double b, double c, unsigned long long* out) {
   for (int o = 16; o; o >>= 1) {
     a = smax(a, __shfl_xor_sync(0xffffffffu, a, o));
     b = smax(b, __shfl_xor_sync(0xffffffffu, b, o));
     c = smax(c, __shfl_xor_sync(0xffffffffu, c, o));
   }
-  // then across the block's warps as the same max over bit patterns the
-  // atomics take (|c0| >= 0 orders as its bits), so one atomic per block and
-  // field: per-warp atomics on three addresses serialised ~9k atomics per adapt
   __shared__ unsigned long long sm[3][32];
   const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   if ((threadIdx.x & 31) == 0) {
@@ -128,6 +106,34 @@ __global__ void k_norms(const long long* __restrict__ dn, const double* __restri
     atomicMax(out + threadIdx.x, m);
   }
 }
+
+// the leaf count from the device (graph replays): grid-stride.  The current
+// leaves into the pyramid (known = 1, their rows as level scaling) and, from
+// the same rows, the norms (solver_adaptive.cpp:139-144): exact maxima over
+// bit patterns, block-reduced, one atomic per block and field.
+__global__ void k_mark_leaves_dn(const long long* __restrict__ dn, int M, const int8_t* __restrict__ lvl,
+                                 const int32_t* __restrict__ li, const int32_t* __restrict__ lj,
+                                 const double* __restrict__ u, PtrTab t, unsigned long long* norms) {
+  const long long n = dn[0];
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int l = lvl[k];
+    const uint64_t node = node_index(l, li[k], lj[k], M);
+    t.known[l][node] = 1;
+    double* o = t.sc[l] + 9 * node;
+    double r[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) r[q] = u[9 * k + q];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) o[q] = r[q];
+    a = smax(a, fabs(r[0]));
+    b = smax(b, fabs(r[3]));
+    c = smax(c, fabs(r[6]));
+  }
+  block_max3(a, b, c, norms);
+}
+
 
 
 __global__ void k_all_ones(uint64_t n, uint8_t* f) {
@@ -451,7 +457,7 @@ LvTab lv_tab(Sim& s, Grid& g, AdaptState& a) {
   t.M = g.M;
   t.N = g.N;
   for (int l = 0; l <= g.L; ++l) {
-    t.known[l] = a.known[l].p;
+    t.known[l] = a.known[l];
     t.sc[l] = a.sc[l].p;
   }
   for (int l = 0; l < g.L; ++l) {
@@ -513,9 +519,14 @@ void adaptive_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem) {
   a.fdet.resize(L);
   a.zp.resize(L);
   a.tmp.resize(L);
+  {
+    std::vector<uint64_t> off(L + 2, 0);  // 16 B aligned levels
+    for (int l = 0; l <= L; ++l) off[l + 1] = (off[l] + (uint64_t(g.M) * g.N << (2 * l)) + 15) & ~uint64_t(15);
+    a.known_all.alloc(off[L + 1]);
+    for (int l = 0; l <= L; ++l) a.known[l] = a.known_all.p + off[l];
+  }
   for (int l = 0; l <= L; ++l) {
     const uint64_t nodes = uint64_t(g.M) * g.N << (2 * l);
-    a.known[l].alloc(nodes);
     a.sc[l].alloc(9 * nodes);
     if (l < L) {
       a.zsig[l].alloc(nodes);
@@ -569,9 +580,6 @@ void adaptive_init(Sim& s, const fm_sim_desc* d, const fm_raster* dem) {
   adaptive_adapt(s, 0.0);
 }
 
-struct ZeroKnownBody {
-  __device__ static void node(int l, uint64_t n, const LvTab& t) { t.known[l][n] = 0; }
-};
 
 // FM_ADAPT_PROFILE=1: per-phase device time of every adapt on stderr (CUDA
 // events between the phases; diagnostics only)
@@ -624,17 +632,16 @@ __global__ void k_set_dn(long long* dn, long long n) { dn[0] = n; }
 void launch_prefix(Sim& s, Grid& g, AdaptState& a, const LvTab& tab) {
   cudaStream_t st = stream();
   const int L = g.L;
-  run_levels_flat<ZeroKnownBody>(tab, 0, L);
+  FM_CUDA(cudaMemsetAsync(a.known_all.p, 0, a.known_all.n, st));
   PtrTab pt{};
   for (int l = 0; l <= L; ++l) {
-    pt.known[l] = a.known[l].p;
+    pt.known[l] = a.known[l];
     pt.sc[l] = a.sc[l].p;
   }
-  k_mark_leaves_dn<<<148 * 4, 256, 0, st>>>(a.dn.p, s.M, s.lvl.p, s.li.p, s.lj.p, s.u.p, pt);
-  FM_LAUNCHED();
-  // norms over the current leaves (solver_adaptive.cpp:139-144)
+  // the current leaves into the pyramid and the norms over them
+  // (solver_adaptive.cpp:139-144)
   FM_CUDA(cudaMemsetAsync(a.norms.p, 0, 3 * sizeof(unsigned long long), st));
-  k_norms<<<148 * 4, 256, 0, st>>>(a.dn.p, s.u.p, a.norms.p);
+  k_mark_leaves_dn<<<148 * 4, 256, 0, st>>>(a.dn.p, s.M, s.lvl.p, s.li.p, s.lj.p, s.u.p, pt, a.norms.p);
   FM_LAUNCHED();
   // encode_up + flag + closure, one sweep (into tmp)
   if (a.kind == 0)
