@@ -224,6 +224,9 @@ struct EncodeFlagBody {
     const uint32_t k4 = *reinterpret_cast<const uint32_t*>(t.known[l + 1] + 4 * n);
     const uint8_t zs = t.zsig[l][n];
     const uint32_t ct = l + 1 < t.L ? *reinterpret_cast<const uint32_t*>(t.tmp[l + 1] + 4 * n) : 0u;
+    // the norms now, not after the stores below (which the compiler cannot
+    // move them past): one round trip fewer on the level's critical path
+    const double nrm[3] = {bitsd(t.norms[0]), bitsd(t.norms[1]), bitsd(t.norms[2])};
     uint8_t f = zs;  // (a non-zero significance value is kept as is)
     bool sig = false;
     const bool enc = kself == 0 && (k4 & 0xffu) && (k4 & 0xff00u) && (k4 & 0xff0000u) && (k4 & 0xff000000u);
@@ -251,7 +254,7 @@ struct EncodeFlagBody {
         t.sc[l][9 * n + 3 * fi + 2] = p.cy;
 #pragma unroll
         for (int q = 0; q < 9; ++q) t.fdet[l][27 * n + 9 * fi + q] = d[q];
-        if (dhat(d, bitsd(t.norms[fi])) >= t.eps) sig = true;
+        if (dhat(d, nrm[fi]) >= t.eps) sig = true;
       }
       kn[n] = 2;
     }
@@ -657,8 +660,7 @@ void launch_prefix(Sim& s, Grid& g, AdaptState& a, const LvTab& tab) {
   std::vector<const uint8_t*> ring(L);
   for (int l = 0; l < L; ++l) ring[l] = a.tmp[l].p;
   // grade + counts + leaves + exact topography (assemble_grid)
-  grade_count_levels(g, true, &ring);
-  build_leaves_device(g, a.dn.p + 1);
+  grade_and_build_leaves_device(g, &ring, a.dn.p + 1);
   // region_topo (solver_nonuniform.cpp:80-89) of every flagged node over the
   // new leaves' topography (the grid's leaf planes; HWFV1 takes them with
   // zero slopes, as the sim's own copy will hold them)

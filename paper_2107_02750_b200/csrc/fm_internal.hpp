@@ -162,6 +162,9 @@ void grade_count_levels(Grid& g, bool graded, const std::vector<const uint8_t*>*
 // top-down into the leaf arrays.  Returns the leaf count.
 int64_t build_leaves(Grid& g);
 void build_leaves_device(Grid& g, long long* total);
+// grade_count_levels(g, true, ring) then build_leaves_device(g, total), the
+// small levels of both in one launch (the adapt's prefix)
+void grade_and_build_leaves_device(Grid& g, const std::vector<const uint8_t*>* ring, long long* total);
 // Permutation device-order -> reference (level, j, i) order, computed on the host.
 std::vector<int64_t> reference_order(const Grid& g, std::vector<int8_t>* l = nullptr,
                                      std::vector<int32_t>* i = nullptr,

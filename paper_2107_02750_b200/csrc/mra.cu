@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kTreeThreads) k_topdown_tree(LevelPtrs p, int 
 // assemble_grid's top-down decode (levels 0..L-1, offsets of level 0 done):
 // the small coarse levels in one single-CTA launch, the middle levels as
 // subtrees in one launch, then a launch per fine level.
-void launch_topdown(Grid& g, const LeafOut& out) {
+void launch_topdown(Grid& g, const LeafOut& out, bool small_done = false) {
   cudaStream_t st = stream();
   const int L = g.L;
   std::vector<DBuf<double>>& zs = g.zs;
@@ -551,7 +551,7 @@ void launch_topdown(Grid& g, const LeafOut& out) {
   int ls = -1;
   for (int l = 0; l < L; ++l)
     if (g.nodes(l) <= kSmallLevelNodes) ls = l;
-  if (ls >= 0) {
+  if (ls >= 0 && !small_done) {
     k_topdown_small<<<1, 256, 0, st>>>(p, ls, L, g.M, g.N, g.kind, out);
     FM_LAUNCHED();
   }
@@ -639,6 +639,70 @@ void build_leaves_device(Grid& g, long long* total) {
   k_level0_offsets<<<1, 1024, 0, st>>>(g.cnt[0].p, g.off[0].p, int64_t(g.nodes(0)), total);
   FM_LAUNCHED();
   launch_topdown(g, LeafOut{g.lf_l.p, g.lf_i.p, g.lf_j.p, g.lf_z.p});
+}
+
+namespace {
+// The adapt's small coarse levels as one single-CTA launch: grading + counts
+// (levels ls..0), the level-0 offsets and new leaf count, then the top-down
+// decode of levels 0..ls -- three launches of one CTA each before, every
+// level a chain of dependent round trips either way.
+__global__ void __launch_bounds__(256) k_small_chain(LevelPtrs p, RingPtrs r, int ls, int L, int M, int N,
+                                                     int graded, int kind, LeafOut out, long long* total) {
+  for (int l = ls; l >= 0; --l) {
+    const uint64_t nodes = uint64_t(M) * N << (2 * l);
+    for (uint64_t n = threadIdx.x; n < nodes; n += blockDim.x)
+      grade_count_node(p.fl[l], l + 1 < L ? p.fl[l + 1] : nullptr, p.cnt[l], l + 1 < L ? p.cnt[l + 1] : nullptr, l,
+                       L, M, N, n, graded, r.ring[l]);
+    __syncthreads();
+  }
+  cta_exclusive_scan(p.cnt[0], p.off[0], int64_t(M) * N, total);
+  __syncthreads();
+  for (int l = 0; l <= ls; ++l) {
+    const uint64_t nodes = uint64_t(M) * N << (2 * l);
+    const bool last = l + 1 == L;
+    for (uint64_t n = threadIdx.x; n < nodes; n += blockDim.x)
+      topdown_node(l ? p.fl[l - 1] : nullptr, p.fl[l], last ? nullptr : p.fl[l + 1],
+                   last ? nullptr : p.cnt[l + 1], p.off[l], last ? nullptr : p.off[l + 1], p.zs[l],
+                   last ? nullptr : p.zs[l + 1], p.det[l], l, L, M, kind, n, out);
+    __syncthreads();
+  }
+}
+}  // namespace
+
+// grade_count_levels (graded, with the ring) + build_leaves_device, the small
+// levels of both in one launch (k_small_chain).
+void grade_and_build_leaves_device(Grid& g, const std::vector<const uint8_t*>* ring, long long* total) {
+  cudaStream_t st = stream();
+  const int L = g.L;
+  int ls = -1;
+  for (int l = 0; l < L; ++l)
+    if (g.nodes(l) <= kSmallLevelNodes) ls = l;
+  if (ls < 0) {
+    grade_count_levels(g, true, ring);
+    build_leaves_device(g, total);
+    return;
+  }
+  for (int l = L - 1; l > ls; --l) {
+    const uint64_t nodes = g.nodes(l);
+    k_grade_count<<<blocks_for(nodes, 256), 256, 0, st>>>(
+        g.flag[l].p, l + 1 < L ? g.flag[l + 1].p : nullptr, g.cnt[l].p, l + 1 < L ? g.cnt[l + 1].p : nullptr, l,
+        L, g.M, g.N, nodes, 1, ring ? (*ring)[l] : nullptr);
+    FM_LAUNCHED();
+  }
+  LevelPtrs p{};
+  RingPtrs r{};
+  for (int l = 0; l < L; ++l) {
+    p.fl[l] = g.flag[l].p;
+    p.cnt[l] = g.cnt[l].p;
+    p.off[l] = g.off[l].p;
+    p.zs[l] = l ? g.zs[l].p : g.coarse.p;
+    p.det[l] = g.det[l].p;
+    r.ring[l] = ring ? (*ring)[l] : nullptr;
+  }
+  const LeafOut out{g.lf_l.p, g.lf_i.p, g.lf_j.p, g.lf_z.p};
+  k_small_chain<<<1, 256, 0, st>>>(p, r, ls, L, g.M, g.N, 1, g.kind, out, total);
+  FM_LAUNCHED();
+  launch_topdown(g, out, true);
 }
 
 // Projection + multi-level encode (detail_tree.cpp:10-54 with the fused
