@@ -79,6 +79,116 @@ __device__ __forceinline__ void grade_count_node(uint8_t* __restrict__ fl, const
   fl[n] = uint8_t(g);
   cnt[n] = c;
 }
+// grade_count_node for the four siblings 4m..4m+3 of level l >= 1 (children
+// of level-(l-1) node m) in one thread: the flags and counts of a sibling
+// quad are contiguous (block-Morton), so its own flags, its children's flags
+// and counts, and the neighbours' flags come as a few 4 / 16 B words from
+// the 3 x 3 level-(l-1) parents around m instead of ~17 byte loads per node,
+// each behind its own index computation.  The same flags and counts as four
+// grade_count_node calls.
+__device__ __forceinline__ void grade_count_quad(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
+                                                 int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1,
+                                                 int l, int L, int M, int N, uint64_t m, int graded,
+                                                 const uint8_t* __restrict__ ring) {
+  int I, J;
+  node_ij(l - 1, m, M, I, J);
+  const int wp = M << (l - 1), hp = N << (l - 1);  // level-(l-1) extent
+  // the 3 x 3 parents' node indices (-1: outside the domain)
+  long long par[3][3];
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int pi = I + dx, pj = J + dy;
+      const bool in = pi >= 0 && pj >= 0 && pi < wp && pj < hp;
+      par[dy + 1][dx + 1] = in ? (long long)node_index(l - 1, pi, pj, M) : -1;
+    }
+  // own flags (or the ring's dilation of its closed flags)
+  int g[4];
+  if (ring) {
+    // the 4 x 4 window of level-l nodes around the quad, bit (4y + x) for
+    // node (2I - 1 + x, 2J - 1 + y), from the parents' sibling words
+    uint32_t w[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        w[a][b] = par[a][b] >= 0 ? *reinterpret_cast<const uint32_t*>(ring + 4 * par[a][b]) : 0u;
+    unsigned win = 0;
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int pa = y == 0 ? 0 : y == 3 ? 2 : 1, pb = x == 0 ? 0 : x == 3 ? 2 : 1;
+        const int cx = (x == 0 || x == 2) ? 1 : 0, cy = (y == 0 || y == 2) ? 1 : 0;
+        const unsigned byte = (w[pa][pb] >> (8 * (cx | (cy << 1)))) & 0xffu;
+        win |= (byte ? 1u : 0u) << (4 * y + x);
+      }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int x = 1 + (c & 1), y = 1 + (c >> 1);  // the node's window position
+      const unsigned nb3 = (0x7u << (x - 1)) * 0x111u << (4 * (y - 1));  // its 3 x 3 block
+      g[c] = (win & nb3) ? 1 : 0;
+    }
+  } else {
+    const uint32_t own = *reinterpret_cast<const uint32_t*>(fl + 4 * m);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) g[c] = int((own >> (8 * c)) & 0xffu);
+  }
+  int cn[4] = {1, 1, 1, 1};
+  if (l + 1 < L) {
+    // the children's flags of the quad's nodes (node c: word c)
+    const uint4 k4 = *reinterpret_cast<const uint4*>(fl1 + 16 * m);
+    const uint32_t kids[4] = {k4.x, k4.y, k4.z, k4.w};
+    bool any_g = false;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      int nbr = 0;
+      if (graded && !kids[c] && !g[c]) {
+        // the level-(l+1) nodes edge-adjacent to node c's child block: the
+        // facing children of its W E S N level-l neighbours, each either a
+        // sibling in this quad or a node of a side parent
+        const int cx = c & 1, cy = c >> 1;
+        auto childw = [&](int nx, int ny) -> uint32_t {  // window coords of a level-l node, 0..3
+          const int pa = ny == 0 ? 0 : ny == 3 ? 2 : 1, pb = nx == 0 ? 0 : nx == 3 ? 2 : 1;
+          const long long p = par[pa][pb];
+          if (p < 0) return 0u;
+          const int cc = (nx == 0 || nx == 2 ? 1 : 0) | ((ny == 0 || ny == 2 ? 1 : 0) << 1);
+          return *reinterpret_cast<const uint32_t*>(fl1 + 4 * (4 * p + cc));
+        };
+        const int x = 1 + cx, y = 1 + cy;
+        const uint32_t W = cx ? kids[c - 1] : childw(x - 1, y);
+        const uint32_t E = cx ? childw(x + 1, y) : kids[c + 1];
+        const uint32_t S = cy ? kids[c - 2] : childw(x, y - 1);
+        const uint32_t Nn = cy ? childw(x, y + 1) : kids[c + 2];
+        // facing children: W's east column (bytes 1, 3), E's west (0, 2),
+        // S's north row (2, 3), N's south row (0, 1)
+        nbr = ((W & 0xff00ff00u) | (E & 0x00ff00ffu) | (S & 0xffff0000u) | (Nn & 0x0000ffffu)) ? 1 : 0;
+      }
+      if (kids[c] || nbr) g[c] = 1;
+      any_g |= g[c] != 0;
+    }
+    if (any_g) {
+      const int4* cc = reinterpret_cast<const int4*>(cnt1 + 16 * m);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (g[c]) {
+          const int4 v = cc[c];
+          cn[c] = v.x + v.y + v.z + v.w;
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (g[c]) cn[c] = 4;
+  }
+  *reinterpret_cast<uint32_t*>(fl + 4 * m) =
+      uint32_t(uint8_t(g[0])) | (uint32_t(uint8_t(g[1])) << 8) | (uint32_t(uint8_t(g[2])) << 16) |
+      (uint32_t(uint8_t(g[3])) << 24);
+  *reinterpret_cast<int4*>(cnt + 4 * m) = make_int4(cn[0], cn[1], cn[2], cn[3]);
+}
+
 struct LeafOut {
   int8_t* l;
   int32_t* i;

@@ -393,6 +393,17 @@ __global__ void k_copy_fine(VertexView vv, const Scalars* __restrict__ s, double
   coarse[3 * k + 2] = q.cy;
 }
 
+#ifndef FM_GRADE_QUAD
+#define FM_GRADE_QUAD 1
+#endif
+// one thread per sibling quad (levels >= 1): grade_count_quad
+__global__ void k_grade_count_quad(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
+                                   int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1, int l, int L,
+                                   int M, int N, uint64_t quads, int graded,
+                                   const uint8_t* __restrict__ ring = nullptr) {
+  const uint64_t m = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (m < quads) grade_count_quad(fl, fl1, cnt, cnt1, l, L, M, N, m, graded, ring);
+}
 __global__ void k_grade_count(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
                               int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1, int l,
                               int L, int M, int N, uint64_t nodes, int graded,
@@ -507,6 +518,25 @@ __global__ void k_parent_level(const double* __restrict__ in, double* __restrict
 }
 
 inline unsigned blocks_for(uint64_t n, int t) { return unsigned((n + t - 1) / t); }
+
+// One level of the grading sweep as its own launch.
+void launch_grade_level(Grid& g, int l, bool graded, const uint8_t* ring) {
+  const int L = g.L;
+  const uint64_t nodes = g.nodes(l);
+  uint8_t* fl = g.flag[l].p;
+  const uint8_t* fl1 = l + 1 < L ? g.flag[l + 1].p : nullptr;
+  int32_t* cnt = g.cnt[l].p;
+  const int32_t* cnt1 = l + 1 < L ? g.cnt[l + 1].p : nullptr;
+  if (FM_GRADE_QUAD && l >= 1) {
+    k_grade_count_quad<<<blocks_for(nodes / 4, 256), 256, 0, stream()>>>(fl, fl1, cnt, cnt1, l, L, g.M, g.N,
+                                                                         nodes / 4, graded ? 1 : 0, ring);
+  } else {
+    k_grade_count<<<blocks_for(nodes, 256), 256, 0, stream()>>>(fl, fl1, cnt, cnt1, l, L, g.M, g.N, nodes,
+                                                               graded ? 1 : 0, ring);
+  }
+  FM_LAUNCHED();
+}
+
 
 }  // namespace
 
@@ -682,13 +712,7 @@ void grade_and_build_leaves_device(Grid& g, const std::vector<const uint8_t*>* r
     build_leaves_device(g, total);
     return;
   }
-  for (int l = L - 1; l > ls; --l) {
-    const uint64_t nodes = g.nodes(l);
-    k_grade_count<<<blocks_for(nodes, 256), 256, 0, st>>>(
-        g.flag[l].p, l + 1 < L ? g.flag[l + 1].p : nullptr, g.cnt[l].p, l + 1 < L ? g.cnt[l + 1].p : nullptr, l,
-        L, g.M, g.N, nodes, 1, ring ? (*ring)[l] : nullptr);
-    FM_LAUNCHED();
-  }
+  for (int l = L - 1; l > ls; --l) launch_grade_level(g, l, true, ring ? (*ring)[l] : nullptr);
   LevelPtrs p{};
   RingPtrs r{};
   for (int l = 0; l < L; ++l) {
@@ -869,14 +893,7 @@ void grade_count_levels(Grid& g, bool graded, const std::vector<const uint8_t*>*
   int ls = -1;  // the finest small level
   for (int l = 0; l < L; ++l)
     if (g.nodes(l) <= kSmallLevelNodes) ls = l;
-  for (int l = L - 1; l > ls; --l) {
-    const uint64_t nodes = g.nodes(l);
-    k_grade_count<<<blocks_for(nodes, 256), 256, 0, st>>>(
-        g.flag[l].p, l + 1 < L ? g.flag[l + 1].p : nullptr, g.cnt[l].p,
-        l + 1 < L ? g.cnt[l + 1].p : nullptr, l, L, g.M, g.N, nodes, graded ? 1 : 0,
-        ring ? (*ring)[l] : nullptr);
-    FM_LAUNCHED();
-  }
+  for (int l = L - 1; l > ls; --l) launch_grade_level(g, l, graded, ring ? (*ring)[l] : nullptr);
   if (ls >= 0) {
     LevelPtrs p{};
     RingPtrs r{};
