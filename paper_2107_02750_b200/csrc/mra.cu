@@ -393,6 +393,9 @@ __global__ void k_copy_fine(VertexView vv, const Scalars* __restrict__ s, double
   coarse[3 * k + 2] = q.cy;
 }
 
+#ifndef FM_TOPDOWN_QUAD
+#define FM_TOPDOWN_QUAD 1
+#endif
 #ifndef FM_GRADE_QUAD
 #define FM_GRADE_QUAD 1
 #endif
@@ -472,6 +475,23 @@ __global__ void k_topdown(const uint8_t* __restrict__ flp, const uint8_t* __rest
                           uint64_t nodes, LeafOut out) {
   const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (n < nodes) topdown_node(flp, fl, fl1, cnt1, off, off1, zin, zout, det, l, L, M, kind, n, out);
+}
+// The same per sibling quad (levels >= 1): at the fine levels most quads
+// have an unflagged parent or no flagged node, and one thread per quad
+// finds that with one byte and one word instead of four threads
+__global__ void k_topdown_quad(const uint8_t* __restrict__ flp, const uint8_t* __restrict__ fl,
+                               const uint8_t* __restrict__ fl1, const int32_t* __restrict__ cnt1,
+                               const int32_t* __restrict__ off, int32_t* __restrict__ off1,
+                               const double* __restrict__ zin, double* __restrict__ zout,
+                               const double* __restrict__ det, int l, int L, int M, int kind, uint64_t quads,
+                               LeafOut out) {
+  const uint64_t m = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (m >= quads || !flp[m]) return;
+  const uint32_t f4 = *reinterpret_cast<const uint32_t*>(fl + 4 * m);
+  if (!f4) return;
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c)
+    if ((f4 >> (8 * c)) & 0xffu) topdown_node(flp, fl, fl1, cnt1, off, off1, zin, zout, det, l, L, M, kind, 4 * m + c, out);
 }
 __global__ void __launch_bounds__(256) k_topdown_small(LevelPtrs p, int lhi, int L, int M, int N, int kind,
                                                        LeafOut out) {
@@ -566,7 +586,10 @@ __global__ void __launch_bounds__(kTreeThreads) k_topdown_tree(LevelPtrs p, int 
 // assemble_grid's top-down decode (levels 0..L-1, offsets of level 0 done):
 // the small coarse levels in one single-CTA launch, the middle levels as
 // subtrees in one launch, then a launch per fine level.
-void launch_topdown(Grid& g, const LeafOut& out, bool small_done = false) {
+// quad: the fine levels one thread per sibling quad (the static MRA, where
+// most fine quads are inactive; the adaptive re-grid's fine levels are
+// mostly active and run one thread per node)
+void launch_topdown(Grid& g, const LeafOut& out, bool small_done = false, bool quad = false) {
   cudaStream_t st = stream();
   const int L = g.L;
   std::vector<DBuf<double>>& zs = g.zs;
@@ -598,11 +621,17 @@ void launch_topdown(Grid& g, const LeafOut& out, bool small_done = false) {
   for (int l = rt + 1; l < L; ++l) {
     const uint64_t nodes = g.nodes(l);
     const bool last = l + 1 == L;
-    k_topdown<<<blocks_for(nodes, 256), 256, 0, st>>>(
-        l ? g.flag[l - 1].p : nullptr, g.flag[l].p, last ? nullptr : g.flag[l + 1].p,
-        last ? nullptr : g.cnt[l + 1].p, g.off[l].p, last ? nullptr : g.off[l + 1].p,
-        l ? zs[l].p : g.coarse.p, last ? nullptr : zs[l + 1].p, g.det[l].p, l, L, g.M, g.kind,
-        nodes, out);
+    if (FM_TOPDOWN_QUAD && quad && l >= 1)
+      k_topdown_quad<<<blocks_for(nodes / 4, 256), 256, 0, st>>>(
+          g.flag[l - 1].p, g.flag[l].p, last ? nullptr : g.flag[l + 1].p, last ? nullptr : g.cnt[l + 1].p,
+          g.off[l].p, last ? nullptr : g.off[l + 1].p, zs[l].p, last ? nullptr : zs[l + 1].p, g.det[l].p, l, L,
+          g.M, g.kind, nodes / 4, out);
+    else
+      k_topdown<<<blocks_for(nodes, 256), 256, 0, st>>>(
+          l ? g.flag[l - 1].p : nullptr, g.flag[l].p, last ? nullptr : g.flag[l + 1].p,
+          last ? nullptr : g.cnt[l + 1].p, g.off[l].p, last ? nullptr : g.off[l + 1].p,
+          l ? zs[l].p : g.coarse.p, last ? nullptr : zs[l + 1].p, g.det[l].p, l, L, g.M, g.kind,
+          nodes, out);
     FM_LAUNCHED();
   }
 }
@@ -655,7 +684,7 @@ int64_t build_leaves(Grid& g) {
   std::vector<DBuf<double>>& zs = g.zs;  // kept across builds (adaptive re-grids)
   zs.resize(L);
   for (int l = 1; l < L; ++l) zs[l].alloc(3 * g.nodes(l));
-  launch_topdown(g, out);
+  launch_topdown(g, out, false, true);
   return g.nleaves;
 }
 
