@@ -87,6 +87,9 @@ struct VertexView {
     const double x = v[size_t(row) * ncols + col];
     return x == nodata ? wall : x;
   }
+  // the value as stored (the speculative encode checks every vertex for
+  // nodata itself and reruns the exact path if it meets one)
+  __device__ __forceinline__ double raw(int row, int col) const { return v[size_t(row) * ncols + col]; }
   // field.cpp:64-91: element (i, j), edge-replicated beyond the raster.
   __device__ __forceinline__ P3 plane(int i, int j) const {
     const int ie = min(i, n - 1), je = min(j, m - 1);
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) 
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) V[r][c] = vv.at(rows[r], cols[c]);
+      for (int c = 0; c < 3; ++c) V[r][c] = SPEC ? vv.raw(rows[r], cols[c]) : vv.at(rows[r], cols[c]);
     if constexpr (SPEC) {
       bool bad = false;
 #pragma unroll
@@ -279,16 +282,25 @@ __global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) 
       if (bad) atomicOr(&p.scal->redo, 1);
     }
     const bool xs = ib != ia, ys = jb != ja;
+    if (xs && ys) {
+      // away from the raster's east / north edge: fixed offsets, no selects
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool sx = (k & 1) && xs, sy = (k >> 1) && ys;  // shifted one column / row
-      double q[2][2];  // [south, north][west, east]
+      for (int k = 0; k < 4; ++k) {
+        const int ox = k & 1, oy = k >> 1;
+        kids[k] = project4(V[oy + 1][ox], V[oy + 1][ox + 1], V[oy][ox], V[oy][ox + 1]);  // nw ne sw se
+      }
+    } else {
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int k = 0; k < 4; ++k) {
+        const bool sx = (k & 1) && xs, sy = (k >> 1) && ys;  // shifted one column / row
+        double q[2][2];  // [south, north][west, east]
 #pragma unroll
-        for (int b = 0; b < 2; ++b)
-          q[a][b] = sy ? (sx ? V[1 + a][1 + b] : V[1 + a][b]) : (sx ? V[a][1 + b] : V[a][b]);
-      kids[k] = project4(q[1][0], q[1][1], q[0][0], q[0][1]);  // nw ne sw se
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+            q[a][b] = sy ? (sx ? V[1 + a][1 + b] : V[1 + a][b]) : (sx ? V[a][1 + b] : V[a][b]);
+        kids[k] = project4(q[1][0], q[1][1], q[0][0], q[0][1]);  // nw ne sw se
+      }
     }
   } else {
 #pragma unroll
