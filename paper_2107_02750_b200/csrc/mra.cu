@@ -213,6 +213,32 @@ __device__ __forceinline__ void store_details(const double* __restrict__ sdet, d
   for (int e = tid; e < total / 2; e += nthr) dst[e] = src[e];
 }
 
+// The same with one bulk (TMA) copy from shared to global memory issued by
+// thread 0 instead of every thread's 16 B load / store loop (when the range
+// is 16 B aligned and a multiple of 16 B; otherwise store_details).  Thread 0
+// must call bulk_read_done before the staging buffer is written again.
+#ifndef FM_ENC_BULK
+#define FM_ENC_BULK 1
+#endif
+__device__ __forceinline__ void store_details_bulk(const double* __restrict__ sdet, double* __restrict__ o,
+                                                   int count, int tid, int nthr) {
+  const unsigned bytes = 72u * unsigned(count);
+  if (!FM_ENC_BULK || (reinterpret_cast<uintptr_t>(o) & 15) || (bytes & 15)) {
+    store_details(sdet, o, count, tid, nthr);
+    return;
+  }
+  if (tid == 0) {
+    const unsigned src = static_cast<unsigned>(__cvta_generic_to_shared(sdet));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(o), "r"(src), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+__device__ __forceinline__ void bulk_read_done(int tid) {
+  if (FM_ENC_BULK && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 #ifndef FM_ENC_MINB
 #define FM_ENC_MINB 6  // 40 registers (A/B on B200: MINB 5 -> 6: MRA 1.427 -> 1.402 ms; 4: 1.471)
 #endif
@@ -340,8 +366,11 @@ __global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) 
     sbuf[tid] = par_s;
   }
   __syncthreads();
-  store_details(sdet, p.det[lev] + 9 * par0, nthr, tid, nthr);
-  if (p.T == 1) return;
+  store_details_bulk(sdet, p.det[lev] + 9 * par0, nthr, tid, nthr);
+  if (p.T == 1) {
+    bulk_read_done(tid);
+    return;
+  }
   int count = nthr;  // nodes at `lev`
   for (int t = 1; t < p.T; ++t) {
     --lev;
@@ -358,6 +387,7 @@ __global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) 
       else
         p.flag[lev][node0 + tid] = dhat(d, norm) >= p.eps ? 1 : 0;
     }
+    bulk_read_done(tid);  // the previous level's bulk copy has read sdet
     __syncthreads();  // sbuf reads and the previous sdet stores are done
     if (have) {
       sbuf[tid] = mine;
@@ -365,8 +395,9 @@ __global__ void __launch_bounds__(256, FM_ENC_MINB) k_encode_tiles(EncParams p) 
       for (int n = 0; n < 9; ++n) sdet[9 * tid + n] = d[n];
     }
     __syncthreads();
-    store_details(sdet, p.det[lev] + 9 * node0, count, tid, nthr);
+    store_details_bulk(sdet, p.det[lev] + 9 * node0, count, tid, nthr);
   }
+  bulk_read_done(tid);
   if (tid == 0) {
     double* o = p.sc_out + 3 * tile;
     o[0] = sbuf[0].c0;
