@@ -90,19 +90,22 @@ __device__ __forceinline__ void grade_count_quad(uint8_t* __restrict__ fl, const
                                                  int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1,
                                                  int l, int L, int M, int N, uint64_t m, int graded,
                                                  const uint8_t* __restrict__ ring) {
-  int I, J;
-  node_ij(l - 1, m, M, I, J);
-  const int wp = M << (l - 1), hp = N << (l - 1);  // level-(l-1) extent
-  // the 3 x 3 parents' node indices (-1: outside the domain)
+  // the 3 x 3 parents' node indices (-1: outside the domain), needed for the
+  // ring and the graded neighbours only
   long long par[3][3];
+  if (ring || (graded && l + 1 < L)) {
+    int I, J;
+    node_ij(l - 1, m, M, I, J);
+    const int wp = M << (l - 1), hp = N << (l - 1);  // level-(l-1) extent
 #pragma unroll
-  for (int dy = -1; dy <= 1; ++dy)
+    for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
-    for (int dx = -1; dx <= 1; ++dx) {
-      const int pi = I + dx, pj = J + dy;
-      const bool in = pi >= 0 && pj >= 0 && pi < wp && pj < hp;
-      par[dy + 1][dx + 1] = in ? (long long)node_index(l - 1, pi, pj, M) : -1;
-    }
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int pi = I + dx, pj = J + dy;
+        const bool in = pi >= 0 && pj >= 0 && pi < wp && pj < hp;
+        par[dy + 1][dx + 1] = in ? (long long)node_index(l - 1, pi, pj, M) : -1;
+      }
+  }
   // own flags (or the ring's dilation of its closed flags)
   int g[4];
   if (ring) {
