@@ -412,14 +412,36 @@ struct DmxLevels {
   const double* dmx[kMaxL];
   uint8_t* flag[kMaxL];
 };
+// The divisor is one value for the whole pass, so its reciprocal is
+// computed once and each quotient is nvcc's fast-path sequence (zdiv2's
+// argument: bit-identical to `/` inside the window, checked by
+// fm_selftest(2)); four nodes per thread as 2 x 16 B loads and one 4 B store.
+__device__ __forceinline__ uint8_t sig_of(double m, double den, double y, bool den_ok, double eps) {
+  const double q = (m == 0.0) ? m : (den_ok && div_fast_ok(m)) ? quot_ieee(m, den, y) : m / den;
+  return q >= eps ? 1 : 0;
+}
 __global__ void k_sig_from_dmx(DmxLevels t, int M, int N, const Scalars* __restrict__ s, double eps) {
   const int l = blockIdx.y;
   const uint64_t nodes = uint64_t(M) * N << (2 * l);
   const double norm = bitsd(s->norm_bits);
   const double den = smax(1.0, norm);
-  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < nodes;
+  const double y = recip_ieee(den);
+  const bool den_ok = div_fast_ok(den);
+  const double* dm = t.dmx[l];
+  uint8_t* fl = t.flag[l];
+  const uint64_t quads = nodes / 4;
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < quads;
+       q += uint64_t(gridDim.x) * blockDim.x) {
+    const double2 a = reinterpret_cast<const double2*>(dm)[2 * q], b = reinterpret_cast<const double2*>(dm)[2 * q + 1];
+    const uint32_t w = uint32_t(sig_of(a.x, den, y, den_ok, eps)) | (uint32_t(sig_of(a.y, den, y, den_ok, eps)) << 8) |
+                       (uint32_t(sig_of(b.x, den, y, den_ok, eps)) << 16) |
+                       (uint32_t(sig_of(b.y, den, y, den_ok, eps)) << 24);
+    reinterpret_cast<uint32_t*>(fl)[q] = w;
+  }
+  // the level's remainder (fewer than four nodes: M N odd at level 0)
+  for (uint64_t n = 4 * quads + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < nodes;
        n += uint64_t(gridDim.x) * blockDim.x)
-    t.flag[l][n] = t.dmx[l][n] / den >= eps ? 1 : 0;
+    fl[n] = sig_of(dm[n], den, y, den_ok, eps);
 }
 
 // L = 0: the fine field is the coarse field.
