@@ -133,6 +133,10 @@ struct Grid {
   int L = 0, M = 1, N = 1, kind = 0;
   double R = 1, x0 = 0, y0 = 0, eps = 0, field_norm = 0;
   bool graded = true;
+  // the topography may hold |z| > 1e300 (or came from a leaf list): its decode
+  // keeps every filter tap (dkind)
+  bool big = true;
+  int dkind() const { return kind | (big ? 0 : 2); }
   int64_t nleaves = 0;
   std::vector<DBuf<double>> det;   // [L] x 9 doubles per node
   std::vector<DBuf<uint8_t>> flag; // [L] final (closed, graded) flags

@@ -670,7 +670,7 @@ void launch_topdown(Grid& g, const LeafOut& out, bool small_done = false, bool q
   for (int l = 0; l < L; ++l)
     if (g.nodes(l) <= kSmallLevelNodes) ls = l;
   if (ls >= 0 && !small_done) {
-    k_topdown_small<<<1, 256, 0, st>>>(p, ls, L, g.M, g.N, g.kind, out);
+    k_topdown_small<<<1, 256, 0, st>>>(p, ls, L, g.M, g.N, g.dkind(), out);
     FM_LAUNCHED();
   }
   const int r = ls + 1;
@@ -678,7 +678,7 @@ void launch_topdown(Grid& g, const LeafOut& out, bool small_done = false, bool q
   for (int l = r; l < L; ++l)
     if ((uint64_t(1) << (2 * (l - r))) <= uint64_t(kTreeThreads)) rt = l;
   if (rt > r && r < L) {
-    k_topdown_tree<<<unsigned(g.nodes(r)), kTreeThreads, 0, st>>>(p, r, rt, L, g.M, g.kind, out);
+    k_topdown_tree<<<unsigned(g.nodes(r)), kTreeThreads, 0, st>>>(p, r, rt, L, g.M, g.dkind(), out);
     FM_LAUNCHED();
   } else {
     rt = r - 1;
@@ -690,12 +690,12 @@ void launch_topdown(Grid& g, const LeafOut& out, bool small_done = false, bool q
       k_topdown_quad<<<blocks_for(nodes / 4, 256), 256, 0, st>>>(
           g.flag[l - 1].p, g.flag[l].p, last ? nullptr : g.flag[l + 1].p, last ? nullptr : g.cnt[l + 1].p,
           g.off[l].p, last ? nullptr : g.off[l + 1].p, zs[l].p, last ? nullptr : zs[l + 1].p, g.det[l].p, l, L,
-          g.M, g.kind, nodes / 4, out);
+          g.M, g.dkind(), nodes / 4, out);
     else
       k_topdown<<<blocks_for(nodes, 256), 256, 0, st>>>(
           l ? g.flag[l - 1].p : nullptr, g.flag[l].p, last ? nullptr : g.flag[l + 1].p,
           last ? nullptr : g.cnt[l + 1].p, g.off[l].p, last ? nullptr : g.off[l + 1].p,
-          l ? zs[l].p : g.coarse.p, last ? nullptr : zs[l + 1].p, g.det[l].p, l, L, g.M, g.kind,
+          l ? zs[l].p : g.coarse.p, last ? nullptr : zs[l + 1].p, g.det[l].p, l, L, g.M, g.dkind(),
           nodes, out);
     FM_LAUNCHED();
   }
@@ -818,7 +818,7 @@ void grade_and_build_leaves_device(Grid& g, const std::vector<const uint8_t*>* r
     r.ring[l] = ring ? (*ring)[l] : nullptr;
   }
   const LeafOut out{g.lf_l.p, g.lf_i.p, g.lf_j.p, g.lf_z.p};
-  k_small_chain<<<1, 256, 0, st>>>(p, r, ls, L, g.M, g.N, 1, g.kind, out, total);
+  k_small_chain<<<1, 256, 0, st>>>(p, r, ls, L, g.M, g.N, 1, g.dkind(), out, total);
   FM_LAUNCHED();
   launch_topdown(g, out, true);
 }
@@ -962,6 +962,7 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
     if (!hs.redo) {
       std::memcpy(&hs.norm, &hs.norm_bits, 8);
       done = true;
+      g.big = false;  // every vertex finite and |z| <= 1e300 (checked by the encode)
     }
   }
   if (!done) {  // nodata, non-finite or huge vertices (or L = 0): the exact two-pass path
@@ -973,6 +974,7 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
     t_ms += elapsed_ms(e0, e1);
   }
   if (hs.err) throw Error(FM_ERR_DOMAIN, "project_vertices: non-finite vertex value");
+  if (!done) g.big = (hs.flags & kBig) != 0;
   g.field_norm = hs.norm;
   if (ms) *ms = t_ms;
 }
