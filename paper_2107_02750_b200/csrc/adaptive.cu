@@ -818,6 +818,10 @@ void adaptive_adapt(Sim& s, double t) {
   FM_CUDA(cudaStreamSynchronize(stream()));
   s.settle_nseg();
   adaptive_adapt_finish(s, t);
+  // an API-level adapt leaves the host's segment count exact (the device
+  // loop settles it at its own syncs instead)
+  FM_CUDA(cudaStreamSynchronize(stream()));
+  s.settle_nseg();
 }
 
 }  // namespace fmh

@@ -44,6 +44,9 @@ def test_adaptive_portable_lockstep_bit_exact(gpu, orc, name):
     assert np.array_equal(na, nb) and np.array_equal(ta, tb)
     for x, y in zip(a.download(), b.download()):
         assert np.array_equal(x, y)
+    # the device loop keeps the segment count on the device between its syncs;
+    # after the run the host's count is exact
+    assert a.num_segments == b.num_segments
 
 
 def test_adaptive_host_api_adapt(gpu, orc):
@@ -62,6 +65,7 @@ def test_adaptive_host_api_adapt(gpu, orc):
         t += dt
         a.adapt(t)
         b.adapt(t)
+        assert a.num_segments == b.num_segments
         for x, y in zip(a.download(), b.download()):
             assert np.array_equal(x, y)
 
