@@ -137,6 +137,11 @@ struct Grid {
   // keeps every filter tap (dkind)
   bool big = true;
   int dkind() const { return kind | (big ? 0 : 2); }
+  // deferred significance (mra_encode's defer_sig): max |d| per node of the
+  // levels > sig_done, d_hat = max|d| / sig_den >= eps taken by the grading
+  std::vector<DBuf<double>> dmx;
+  int sig_done = -1;
+  double sig_den = 1.0;
   int64_t nleaves = 0;
   std::vector<DBuf<double>> det;   // [L] x 9 doubles per node
   std::vector<DBuf<uint8_t>> flag; // [L] final (closed, graded) flags
@@ -157,7 +162,9 @@ Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind)
 Grid* grid_from_leaves(int L, int M, int N, double R, double x0, double y0, int64_t n, const int32_t* lv,
                        const int32_t* li, const int32_t* lj, const double* topo3);
 // The stages of mra_static, reused by the adaptive solver.
-void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, double* ms);
+// defer_sig: leave the significance of the levels with more than 256 nodes
+// to the grading pass, which forms it from the encode's max |d| (g.dmx)
+void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, double* ms, bool defer_sig = false);
 // ring (optional, per level): take each node's own flag as the same-level
 // 8-neighbour dilation of ring[l] (buffer_ring) instead of g.flag[l]
 void grade_count_levels(Grid& g, bool graded, const std::vector<const uint8_t*>* ring = nullptr);

@@ -89,7 +89,8 @@ __device__ __forceinline__ void grade_count_node(uint8_t* __restrict__ fl, const
 __device__ __forceinline__ void grade_count_quad(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
                                                  int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1,
                                                  int l, int L, int M, int N, uint64_t m, int graded,
-                                                 const uint8_t* __restrict__ ring) {
+                                                 const uint8_t* __restrict__ ring,
+                                                 const uint32_t* own_sig = nullptr) {
   // the 3 x 3 parents' node indices (-1: outside the domain), needed for the
   // ring and the graded neighbours only
   long long par[3][3];
@@ -134,7 +135,8 @@ __device__ __forceinline__ void grade_count_quad(uint8_t* __restrict__ fl, const
       g[c] = (win & nb3) ? 1 : 0;
     }
   } else {
-    const uint32_t own = *reinterpret_cast<const uint32_t*>(fl + 4 * m);
+    // own flags: fl's (or, deferred significance, the caller's)
+    const uint32_t own = own_sig ? *own_sig : *reinterpret_cast<const uint32_t*>(fl + 4 * m);
 #pragma unroll
     for (int c = 0; c < 4; ++c) g[c] = int((own >> (8 * c)) & 0xffu);
   }

@@ -465,12 +465,26 @@ __global__ void k_copy_fine(VertexView vv, const Scalars* __restrict__ s, double
 #define FM_GRADE_QUAD 1
 #endif
 // one thread per sibling quad (levels >= 1): grade_count_quad
+// dmx (static MRA, deferred significance): the quad's own flags are
+// max|d| / den >= eps (k_sig_from_dmx's operations) instead of fl's
 __global__ void k_grade_count_quad(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
                                    int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1, int l, int L,
                                    int M, int N, uint64_t quads, int graded,
-                                   const uint8_t* __restrict__ ring = nullptr) {
+                                   const uint8_t* __restrict__ ring = nullptr, const double* __restrict__ dmx = nullptr,
+                                   double den = 1.0, double eps = 0.0) {
   const uint64_t m = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (m < quads) grade_count_quad(fl, fl1, cnt, cnt1, l, L, M, N, m, graded, ring);
+  if (m >= quads) return;
+  if (dmx) {
+    const double y = recip_ieee(den);
+    const bool den_ok = div_fast_ok(den);
+    const double2 a = reinterpret_cast<const double2*>(dmx)[2 * m], b = reinterpret_cast<const double2*>(dmx)[2 * m + 1];
+    const uint32_t own = uint32_t(sig_of(a.x, den, y, den_ok, eps)) | (uint32_t(sig_of(a.y, den, y, den_ok, eps)) << 8) |
+                         (uint32_t(sig_of(b.x, den, y, den_ok, eps)) << 16) |
+                         (uint32_t(sig_of(b.y, den, y, den_ok, eps)) << 24);
+    grade_count_quad(fl, fl1, cnt, cnt1, l, L, M, N, m, graded, nullptr, &own);
+    return;
+  }
+  grade_count_quad(fl, fl1, cnt, cnt1, l, L, M, N, m, graded, ring);
 }
 __global__ void k_grade_count(uint8_t* __restrict__ fl, const uint8_t* __restrict__ fl1,
                               int32_t* __restrict__ cnt, const int32_t* __restrict__ cnt1, int l,
@@ -612,9 +626,12 @@ void launch_grade_level(Grid& g, int l, bool graded, const uint8_t* ring) {
   const uint8_t* fl1 = l + 1 < L ? g.flag[l + 1].p : nullptr;
   int32_t* cnt = g.cnt[l].p;
   const int32_t* cnt1 = l + 1 < L ? g.cnt[l + 1].p : nullptr;
-  if (FM_GRADE_QUAD && l >= 1) {
+  // the level's significance still to form from max |d| (mra_encode's defer_sig)
+  const double* dmx = (!ring && l > g.sig_done && size_t(l) < g.dmx.size()) ? g.dmx[l].p : nullptr;
+  if (dmx || (FM_GRADE_QUAD && l >= 1)) {
     k_grade_count_quad<<<blocks_for(nodes / 4, 256), 256, 0, stream()>>>(fl, fl1, cnt, cnt1, l, L, g.M, g.N,
-                                                                         nodes / 4, graded ? 1 : 0, ring);
+                                                                         nodes / 4, graded ? 1 : 0, ring, dmx,
+                                                                         g.sig_den, g.eps);
   } else {
     k_grade_count<<<blocks_for(nodes, 256), 256, 0, stream()>>>(fl, fl1, cnt, cnt1, l, L, g.M, g.N, nodes,
                                                                graded ? 1 : 0, ring);
@@ -827,7 +844,7 @@ void grade_and_build_leaves_device(Grid& g, const std::vector<const uint8_t*>* r
 // field.cpp:64-117): fills g.det, g.flag (= significance, detail_tree.cpp:66-72,
 // before closure), g.coarse and g.field_norm.  All buffers are allocated
 // before the first kernel so `ms` (CUDA events) times kernels only.
-void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, double* ms) {
+void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, double* ms, bool defer_sig) {
   FM_RANGE("mra_encode");
   if (!dem || !dem->values) throw Error(FM_ERR_CONFIG, "null DEM raster");
   if (dem->ncols < 2 || dem->nrows < 2)
@@ -952,9 +969,20 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
       t.dmx[l] = dmx[l].p;
       t.flag[l] = g.flag[l].p;
     }
-    const unsigned bx = unsigned(std::min<uint64_t>(blocks_for(g.nodes(L - 1), 256), 148 * 8));
-    k_sig_from_dmx<<<dim3(bx, L), 256, 0, st>>>(t, g.M, g.N, scal.p, eps);
-    FM_LAUNCHED();
+    // deferred: only the small levels here (the grading's single-CTA pass
+    // reads flags); the others' significance is formed in the grading
+    int nsig = L;
+    if (defer_sig) {
+      nsig = 0;
+      for (int l = 0; l < L; ++l)
+        if (g.nodes(l) <= kSmallLevelNodes) nsig = l + 1;
+      nsig = std::max(nsig, 1);  // level 0 always here (the quads start at level 1)
+    }
+    if (nsig > 0) {
+      const unsigned bx = unsigned(std::min<uint64_t>(blocks_for(g.nodes(nsig - 1), 256), 148 * 8));
+      k_sig_from_dmx<<<dim3(bx, nsig), 256, 0, st>>>(t, g.M, g.N, scal.p, eps);
+      FM_LAUNCHED();
+    }
     FM_CUDA(cudaEventRecord(e1, st));
     scal.download(&hs, 1);
     FM_CUDA(cudaStreamSynchronize(st));
@@ -963,6 +991,12 @@ void mra_encode(const fm_raster* dem, int L, double eps, int kind, Grid& g, doub
       std::memcpy(&hs.norm, &hs.norm_bits, 8);
       done = true;
       g.big = false;  // every vertex finite and |z| <= 1e300 (checked by the encode)
+      g.sig_done = L - 1;
+      if (nsig < L) {  // the grading forms the rest
+        g.sig_done = nsig - 1;
+        g.sig_den = hs.norm > 1.0 ? hs.norm : 1.0;  // smax(1.0, norm)
+        g.dmx = std::move(dmx);
+      }
     }
   }
   if (!done) {  // nodata, non-finite or huge vertices (or L = 0): the exact two-pass path
@@ -1101,7 +1135,7 @@ Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind)
   auto g = std::make_unique<Grid>();
   g->graded = graded;
   double enc_ms = 0.0;
-  mra_encode(dem, L, eps, kind, *g, &enc_ms);
+  mra_encode(dem, L, eps, kind, *g, &enc_ms, true);
   // pre-size the count/offset pyramids so the timed region holds kernels only
   g->cnt.resize(L);
   g->off.resize(L);
@@ -1114,6 +1148,8 @@ Grid* mra_static(const fm_raster* dem, int L, double eps, bool graded, int kind)
   cudaEvent_t e0 = ev.a, e1 = ev.b;
   FM_CUDA(cudaEventRecord(e0, st));
   grade_count_levels(*g, graded);
+  g->dmx.clear();  // (stream-ordered frees)
+  g->sig_done = L - 1;
   build_leaves(*g);
   FM_CUDA(cudaEventRecord(e1, st));
   FM_CUDA(cudaStreamSynchronize(st));
