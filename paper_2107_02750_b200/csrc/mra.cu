@@ -461,6 +461,9 @@ __global__ void k_copy_fine(VertexView vv, const Scalars* __restrict__ s, double
 #ifndef FM_TOPDOWN_QUAD
 #define FM_TOPDOWN_QUAD 1
 #endif
+#ifndef FM_TOPDOWN_QUAD_LEVELS
+#define FM_TOPDOWN_QUAD_LEVELS 1  // the finest this many levels (A/B at config 4: 1: 0.970, 2: 0.983, all: 0.998, none: 1.010 ms)
+#endif
 #ifndef FM_GRADE_QUAD
 #define FM_GRADE_QUAD 1
 #endif
@@ -703,7 +706,7 @@ void launch_topdown(Grid& g, const LeafOut& out, bool small_done = false, bool q
   for (int l = rt + 1; l < L; ++l) {
     const uint64_t nodes = g.nodes(l);
     const bool last = l + 1 == L;
-    if (FM_TOPDOWN_QUAD && quad && l >= 1)
+    if (FM_TOPDOWN_QUAD && quad && l >= 1 && l >= L - FM_TOPDOWN_QUAD_LEVELS)
       k_topdown_quad<<<blocks_for(nodes / 4, 256), 256, 0, st>>>(
           g.flag[l - 1].p, g.flag[l].p, last ? nullptr : g.flag[l + 1].p, last ? nullptr : g.cnt[l + 1].p,
           g.off[l].p, last ? nullptr : g.off[l + 1].p, zs[l].p, last ? nullptr : zs[l + 1].p, g.det[l].p, l, L,
