@@ -289,10 +289,27 @@ __global__ void __launch_bounds__(256) k_transfer_leaves(LvTab t, long long n, c
     const double* o = t.sc[0] + 9 * (nl >> (2 * l));
 #pragma unroll
     for (int q = 0; q < 9; ++q) v[q] = o[q];
+    // every ancestor's "internal" flag up front (independent loads, one
+    // round trip for the whole chain), and each level's details prefetched
+    // into L1 one level ahead of its decode
+    uint32_t internal_mask = 0;
+#pragma unroll
+    for (int m = 0; m < kMaxLv; ++m)
+      if (m < l && t.known[m][nl >> (2 * (l - m))] == 2) internal_mask |= 1u << m;
+    auto prefetch_det = [&](int m) {
+      if (m < l && ((internal_mask >> m) & 1u)) {
+        const double* dd = t.fdet[m] + 27 * (nl >> (2 * (l - m)));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(dd));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(dd + 13));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(dd + 26));
+      }
+    };
+    prefetch_det(0);
     for (int m = 0; m < l; ++m) {
+      prefetch_det(m + 1);
       const uint64_t a = nl >> (2 * (l - m));
       const int c = int(nl >> (2 * (l - m - 1))) & 3;
-      const bool internal = t.known[m][a] == 2;
+      const bool internal = (internal_mask >> m) & 1u;
       const double* dd = t.fdet[m] + 27 * a;
 #pragma unroll
       for (int f = 0; f < 3; ++f) {
