@@ -296,6 +296,32 @@ int fm_rmse(const double* test_t, const double* test_v, int64_t n_test, const do
 int fm_extent_metrics(const fm_raster* test, const fm_raster* ref, double wet_threshold,
                       int64_t* counts, double* rates);
 
+/* ---- file formats either side of the path -------------
+ * Host-side; the text formats are the reference's, byte for byte, and each
+ * has a binary side format (magic "FMRB1" / "FMNG1", little-endian raw
+ * fields) that the readers recognise by its magic.
+ *
+ * fm_raster_read: read_ascii_grid (raster.cpp:22-79) — six keyword/value
+ * header lines in any order, keywords case-insensitive, then ncols*nrows
+ * whitespace-separated values; the body is parsed by all host threads.  On
+ * success out->values is library-owned host memory (page-locked when a device
+ * is present, so it uploads at the link's rate), out->on_device = 0; free it
+ * with fm_raster_release.  Unopenable file, malformed header or a value count
+ * other than ncols*nrows: FM_ERR_IO (IoError / ParseError). */
+int fm_raster_read(const char* path, fm_raster* out);
+int fm_raster_release(fm_raster* r);
+/* write_ascii_grid (raster.cpp:81-96) when binary == 0 ("%.17g" values, one
+ * raster row per line), else the binary side format.  Host rasters only. */
+int fm_raster_write(const fm_raster* r, const char* path, int32_t binary);
+/* write_nug (quadgrid.cpp:287-302): "nug L M N Rfine x0 y0" then one
+ * "level i j c0 c1x c1y" line per leaf in the reference's leaf order
+ * (binary != 0: the same fields raw). */
+int fm_grid_write(const fm_grid* g, const char* path, int32_t binary);
+/* read_nug (quadgrid.cpp:304-327): records up to the first that does not
+ * parse, then fm_grid_import's construction and checks (StructureError for
+ * leaves that do not tile the domain, ParseError for a malformed header). */
+int fm_grid_read(const char* path, fm_grid** out);
+
 /* ---- multi-GPU: Morton-range shards of a static non-uniform sim ----------
  * (the reference is single-process.)  Rank r of R owns the
  * contiguous range [floor(n r / R), floor(n (r+1) / R)) of the Morton-ordered

@@ -112,6 +112,16 @@ class Grid {
                          topo3.data(), &g));
     return Grid(g);
   }
+  // read_nug (quadgrid.cpp:304-327), or the binary side format by its magic
+  static Grid read(const std::string& path) {
+    fm_grid* g = nullptr;
+    check(fm_grid_read(path.c_str(), &g));
+    return Grid(g);
+  }
+  // write_nug (quadgrid.cpp:287-302), byte for byte; binary: the raw side format
+  void write(const std::string& path, bool binary = false) const {
+    check(fm_grid_write(g_, path.c_str(), binary ? 1 : 0));
+  }
   int64_t size() const { return fm_grid_num_leaves(g_); }
   const fm_grid* get() const { return g_; }
   // leaves in the reference order (level, j, i) and their topography
@@ -129,6 +139,26 @@ class Grid {
   explicit Grid(fm_grid* g) : g_(g) {}
   fm_grid* g_ = nullptr;
 };
+
+// read_ascii_grid (raster.cpp:22-79) into library-owned host memory
+// (page-locked when a device is present); also reads the binary side format.
+class HostRaster {
+ public:
+  explicit HostRaster(const std::string& path) { check(fm_raster_read(path.c_str(), &r_)); }
+  HostRaster(const HostRaster&) = delete;
+  HostRaster& operator=(const HostRaster&) = delete;
+  HostRaster(HostRaster&& o) noexcept : r_(std::exchange(o.r_, fm_raster{})) {}
+  ~HostRaster() { fm_raster_release(&r_); }
+  const fm_raster& get() const { return r_; }
+  double at(int row, int col) const { return r_.values[size_t(row) * size_t(r_.ncols) + size_t(col)]; }
+
+ private:
+  fm_raster r_{};
+};
+// write_ascii_grid (raster.cpp:81-96), byte for byte; binary: the raw side format
+inline void write_raster(const fm_raster& r, const std::string& path, bool binary = false) {
+  check(fm_raster_write(&r, path.c_str(), binary ? 1 : 0));
+}
 
 // ---- member types of the drive<Sim> contract --------------------------------
 #ifdef FM_GPU_WITH_FLOODMRA

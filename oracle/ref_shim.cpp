@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <filesystem>
 #include <fstream>
@@ -192,6 +193,43 @@ int ref_grid_import(int32_t L, int32_t M, int32_t N, double R, double x0, double
       const int idx = g->nug.grid.find(lv[k], ii[k], jj[k]);
       g->nug.topo[idx] = fm::PlanarCoeffs{topo3[3 * k], topo3[3 * k + 1], topo3[3 * k + 2]};
     }
+    *out = g.release();
+  });
+}
+
+// The reference's own file formats (raster.cpp:22-96, quadgrid.cpp:287-327),
+// for the byte-level checks of fm_raster_read / fm_raster_write / fm_grid_write
+// / fm_grid_read (tests/test_io.py).  `binary` must be 0: the binary side
+// formats are the GPU library's own.
+int ref_raster_read(const char* path, fm_raster* out) {
+  return guard([&] {
+    const fm::Raster r = fm::read_ascii_grid(path);
+    double* v = static_cast<double*>(std::malloc(std::max<size_t>(1, r.values.size()) * sizeof(double)));
+    std::memcpy(v, r.values.data(), r.values.size() * sizeof(double));
+    *out = fm_raster{v, r.ncols, r.nrows, r.xll, r.yll, r.cellsize, r.nodata, 0};
+  });
+}
+int ref_raster_release(fm_raster* r) {
+  std::free(const_cast<double*>(r->values));
+  r->values = nullptr;
+  return FM_OK;
+}
+int ref_raster_write(const fm_raster* r, const char* path, int32_t binary) {
+  return guard([&] {
+    if (binary) throw fm::ConfigError("the reference has no binary raster format");
+    fm::write_ascii_grid(to_raster(r), path);
+  });
+}
+int ref_grid_write(const ref_grid* g, const char* path, int32_t binary) {
+  return guard([&] {
+    if (binary) throw fm::ConfigError("the reference has no binary grid format");
+    fm::write_nug(g->nug, path);
+  });
+}
+int ref_grid_read(const char* path, ref_grid** out) {
+  return guard([&] {
+    auto g = std::make_unique<ref_grid>();
+    g->nug = fm::read_nug(path);
     *out = g.release();
   });
 }

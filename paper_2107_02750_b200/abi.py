@@ -9,6 +9,7 @@ __graft_entry__.smoke() and bench.py's CPU legs.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 
 import numpy as np
@@ -155,6 +156,12 @@ OPTIONAL = {
     "grid_import": (C.c_int, [I32, I32, I32, D, D, D, I64, PI32, PI32, PI32, PD, PP]),
     "extent_metrics": (C.c_int, [C.POINTER(c_raster), C.POINTER(c_raster), D, C.POINTER(C.c_int64), PD]),
     "eval_libm": (C.c_int, [I32, I64, PD, PD]),
+    # file formats
+    "raster_read": (C.c_int, [C.c_char_p, C.POINTER(c_raster)]),
+    "raster_release": (C.c_int, [C.POINTER(c_raster)]),
+    "raster_write": (C.c_int, [C.POINTER(c_raster), C.c_char_p, I32]),
+    "grid_write": (C.c_int, [P, C.c_char_p, I32]),
+    "grid_read": (C.c_int, [C.c_char_p, PP]),
 }
 
 
@@ -242,6 +249,33 @@ class Backend:
         self.call("extent_metrics", C.byref(a), C.byref(b), float(wet_threshold),
                   cnt.ctypes.data_as(C.POINTER(C.c_int64)), dptr(rates))
         return cnt, rates
+
+    # ---- file formats ----
+    def read_raster(self, path: str):
+        """read_ascii_grid (raster.cpp:22-79) or the binary side format: a
+        scenarios.Raster copied out of the library's buffer."""
+        from .scenarios import Raster
+        r = c_raster()
+        self.call("raster_read", os.fsencode(path), C.byref(r))
+        try:
+            vals = np.ctypeslib.as_array(r.values, shape=(r.nrows, r.ncols)).copy()
+        finally:
+            self.call("raster_release", C.byref(r))
+        return Raster(vals, r.xll, r.yll, r.cellsize, r.nodata)
+
+    def write_raster(self, raster, path: str, binary: bool = False) -> None:
+        """write_ascii_grid (raster.cpp:81-96), or the binary side format."""
+        keep: list = []
+        r = make_raster(raster, keep)
+        self.call("raster_write", C.byref(r), os.fsencode(path), 1 if binary else 0)
+
+    def read_grid(self, path: str) -> "Grid":
+        """read_nug (quadgrid.cpp:304-327), or the binary side format."""
+        h = P()
+        self.call("grid_read", os.fsencode(path), C.byref(h))
+        g = Grid.__new__(Grid)
+        g.be, g.h, g.eps, g._keep = self, h, 0.0, []
+        return g
 
     # ---- sharding (SURVEY §8e) ----
     def comm_local(self, nranks: int) -> "Comm":
@@ -354,6 +388,10 @@ class Grid:
                      C.byref(x0), C.byref(y0), C.byref(nm))
         return dict(L=L.value, M=M.value, N=N.value, R=R.value, x0=x0.value, y0=y0.value,
                     field_norm=nm.value)
+
+    def write(self, path: str, binary: bool = False) -> None:
+        """write_nug (quadgrid.cpp:287-302), or the binary side format."""
+        self.be.call("grid_write", self.h, os.fsencode(path), 1 if binary else 0)
 
     def leaves(self, order: int = 0):
         n = self.num_leaves

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "fm_device.cuh"
+#include "fm_io.hpp"
 #include "fm_sim.hpp"
 
 using namespace fmh;
@@ -504,6 +505,35 @@ int fm_sim_topology(fm_sim* s, int32_t* level, int32_t* i, int32_t* j, int32_t* 
       if (seg_r) m.seg_r.download(seg_r, m.nseg);
     }
     FM_CUDA(cudaStreamSynchronize(stream()));
+  });
+}
+int fm_raster_read(const char* path, fm_raster* out) {
+  return guard([&] {
+    if (!path || !out) throw Error(FM_ERR_IO, "fm_raster_read: null argument");
+    raster_read(path, out);
+  });
+}
+int fm_raster_release(fm_raster* r) {
+  return guard([&] { raster_release(r); });
+}
+int fm_raster_write(const fm_raster* r, const char* path, int32_t binary) {
+  return guard([&] {
+    if (!path) throw Error(FM_ERR_IO, "fm_raster_write: null path");
+    if (binary) raster_write_bin(r, path);
+    else raster_write_ascii(r, path);
+  });
+}
+int fm_grid_write(const fm_grid* g, const char* path, int32_t binary) {
+  return guard([&] {
+    if (!g || !path) throw Error(FM_ERR_IO, "fm_grid_write: null argument");
+    require_device();
+    grid_write(g, path, binary != 0);
+  });
+}
+int fm_grid_read(const char* path, fm_grid** out) {
+  return guard([&] {
+    if (!path || !out) throw Error(FM_ERR_IO, "fm_grid_read: null argument");
+    grid_read(path, out);
   });
 }
 int fm_rmse(const double* tt, const double* tv, int64_t nt, const double* rt, const double* rv, int64_t nr,
