@@ -249,7 +249,10 @@ struct SideOut {
 #ifndef FM_SID_ROW
 #define FM_SID_ROW 1
 #endif
-template <bool P2>
+#ifndef FM_FV1_CONST
+#define FM_FV1_CONST 1
+#endif
+template <bool P2, int W = 9>
 __device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9], const P3& zc,
                                              long long kk, int sd, int kind, double cx, double cy,
                                              double sz, int* err, int2 ids,
@@ -284,7 +287,12 @@ __device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9],
   // the leaf's row from its shared-memory copy, read where it is used
   double sl[9];
 #pragma unroll
-  for (int q = 0; q < 9; ++q) sl[q] = lrow[q];
+  // W = 3 (compact FV1 rows): the slopes are +0 by construction (load_row),
+  // so they are literals here rather than opaque shared-memory reads
+  // (FM_FV1_CONST 2: the three means stay in registers too, so the four
+  // sides' identical limit values -- their two divisions -- are formed once)
+  for (int q = 0; q < 9; ++q)
+    sl[q] = (FM_FV1_CONST && W == 3 && q % 3 != 0) ? 0.0 : (FM_FV1_CONST == 2 && W == 3) ? s[q] : lrow[q];
   // P2: the leaf's static topography limit on this side (k_seg_z's zside,
   // in lrow[9 + sd]) instead of its z plane evaluated here
   const P3 zl{lrow[9], lrow[10], lrow[11]};
@@ -380,7 +388,8 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   __shared__ double srow_all[FM_STAGE_THREADS * 13];  // 13-double stride: conflict-free
   volatile double* lrow = srow_all + 13 * threadIdx.x;
 #pragma unroll
-  for (int q = 0; q < 9; ++q) lrow[q] = s[q];
+  for (int q = 0; q < 9; ++q)
+    if (!(FM_FV1_CONST && W == 3 && q % 3 != 0)) lrow[q] = s[q];
   if (P2) {
     lrow[9] = zs01.x;
     lrow[10] = zs01.y;
@@ -417,14 +426,14 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   const double sz = lsize(v, l);
   const double inv = v.linv[l];
   const double cx = P2 ? 0.0 : lcen(v.x0, v, l, i), cy = P2 ? 0.0 : lcen(v.y0, v, l, j);
-  const bool dg2 = v.scheme == FM_DG2;
+  const bool dg2 = (FM_FV1_CONST && W == 3) ? false : v.scheme == FM_DG2;
   const bool epi = last && !manual;
   // the first inflow's count for this leaf, loaded early: its latency
   // otherwise sits at the end of the leaf's critical path
   const int cnt0 = (epi && v.ninflow > 0) ? v.infc[kk] : 0;
   // x direction: E and W sides, then the Gauss-point fluxes along x
-  const SideOut ee = side_eval<P2>(v, s, zc, kk, 1, (code >> 2) & 3, cx, cy, sz, err, ide, lrow);
-  const SideOut ew = side_eval<P2>(v, s, zc, kk, 3, (code >> 6) & 3, cx, cy, sz, err, idw, lrow);
+  const SideOut ee = side_eval<P2, W>(v, s, zc, kk, 1, (code >> 2) & 3, cx, cy, sz, err, ide, lrow);
+  const SideOut ew = side_eval<P2, W>(v, s, zc, kk, 3, (code >> 6) & 3, cx, cy, sz, err, idw, lrow);
   const DirMod X{0.5 * (ee.h + ew.h),   (ee.h - ew.h) * kHalfInvS3,   0.5 * (ee.qx + ew.qx),
                  (ee.qx - ew.qx) * kHalfInvS3, 0.5 * (ee.qy + ew.qy), (ee.qy - ew.qy) * kHalfInvS3,
                  (ee.zd - ew.zd) * kHalfInvS3};
@@ -449,8 +458,8 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   const double dxm = fe.m - fw.m, dxn = fe.n - fw.n, dxt = fe.t - fw.t;
   const double srcx = div_sz<P2>(v.g * X.h0 * (2.0 * kS3 * X.z1), sz, inv);
   // y direction
-  const SideOut en = side_eval<P2>(v, s, zc, kk, 0, code & 3, cx, cy, sz, err, idn, lrow);
-  const SideOut es = side_eval<P2>(v, s, zc, kk, 2, (code >> 4) & 3, cx, cy, sz, err, ids_, lrow);
+  const SideOut en = side_eval<P2, W>(v, s, zc, kk, 0, code & 3, cx, cy, sz, err, idn, lrow);
+  const SideOut es = side_eval<P2, W>(v, s, zc, kk, 2, (code >> 4) & 3, cx, cy, sz, err, ids_, lrow);
   const DirMod Y{0.5 * (en.h + es.h),   (en.h - es.h) * kHalfInvS3,   0.5 * (en.qx + es.qx),
                  (en.qx - es.qx) * kHalfInvS3, 0.5 * (en.qy + es.qy), (en.qy - es.qy) * kHalfInvS3,
                  (en.zd - es.zd) * kHalfInvS3};
@@ -475,7 +484,8 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
   double res[9];
 #if FM_STAGE_SROW
 #pragma unroll
-  for (int q = 0; q < 9; ++q) s[q] = lrow[q];
+  for (int q = 0; q < 9; ++q)
+    s[q] = (FM_FV1_CONST && W == 3 && q % 3 != 0) ? 0.0 : (FM_FV1_CONST == 2 && W == 3) ? s[q] : lrow[q];
 #endif
   if (STAGE == 1) {
 #pragma unroll
@@ -643,7 +653,13 @@ __device__ __forceinline__ void reduce_acc(DevRed* red, const DevClock& c, doubl
 // A side's sub-face length needs no neighbour lookup: on a graded grid it is
 // the leaf's size, or half of it when the side has two (finer) neighbours
 // (kind 3) -- the same IEEE value as min(size_l, size_r).
-constexpr int kAccLeafThreads = 256;
+#ifndef FM_ACC_LEAF_THREADS
+#define FM_ACC_LEAF_THREADS 128
+#endif
+#ifndef FM_ACC_HOIST
+#define FM_ACC_HOIST 1
+#endif
+constexpr int kAccLeafThreads = FM_ACC_LEAF_THREADS;
 template <bool P2>
 __global__ void __launch_bounds__(kAccLeafThreads) k_acc_leaves(
     NuView v, const DevClock* __restrict__ clk, DevRed* red, double* __restrict__ ch,
@@ -667,6 +683,13 @@ __global__ void __launch_bounds__(kAccLeafThreads) k_acc_leaves(
     const int ids[8] = {s03.x, s03.y, s03.z, s03.w, s47.x, s47.y, s47.z, s47.w};
     const double area = sz * sz;
     double net = 0.0, sx = 0.0, sy = 0.0;
+#if FM_ACC_HOIST
+    // every side's discharge gathers issued together, ahead of the side
+    // loop's branches (an unused slot holds -1 and loads nothing)
+    double Qs[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) Qs[t] = ids[t] >= 0 ? q[ids[t]] : 0.0;
+#endif
 #pragma unroll
     for (int sd = 0; sd < 4; ++sd) {
       const int kind = (code >> (2 * sd)) & 3;
@@ -694,7 +717,11 @@ __global__ void __launch_bounds__(kAccLeafThreads) k_acc_leaves(
         const double len = kind == 3 ? 0.5 * sz : sz;
         const int nseg = kind == 3 ? 2 : 1;
         for (int t = 0; t < nseg; ++t) {
+#if FM_ACC_HOIST
+          const double Q = t ? Qs[2 * sd + 1] : Qs[2 * sd];
+#else
           const double Q = q[ids[2 * sd + t]];
+#endif
           net += sign * Q * len;
           if (sd == 1 || sd == 3)
             sx += Q * len;
