@@ -356,10 +356,14 @@ __device__ __forceinline__ SideOut side_eval(const NuView& v, const double s[9],
 #ifndef FM_STAGE_MINB
 #define FM_STAGE_MINB 10
 #endif
+// the compact FV1 stage (W = 3) keeps far fewer values live: its own cap
+#ifndef FM_STAGE_MINB3
+#define FM_STAGE_MINB3 FM_STAGE_MINB
+#endif
 
 // LIST: the leaves are list[0..cnt) (a shard's stage split) instead of 0..n-1
 template <int STAGE, bool P2, int W = 9, bool LIST = false>
-__global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
+__global__ void __launch_bounds__(FM_STAGE_THREADS, W == 3 ? FM_STAGE_MINB3 : FM_STAGE_MINB) k_stage(
     NuView v, const DevClock* __restrict__ clk, DevRed* red, const double* __restrict__ in,
     const double* uold, double* out, int last, int manual, double mdt, int* err,
     const int32_t* __restrict__ list, long long cnt) {
@@ -535,8 +539,11 @@ __global__ void __launch_bounds__(FM_STAGE_THREADS, FM_STAGE_MINB) k_stage(
 #ifndef FM_ACC_SPT
 #define FM_ACC_SPT 2
 #endif
+#ifndef FM_ACC_FACE_THREADS
+#define FM_ACC_FACE_THREADS 128
+#endif
 template <bool P2>
-__global__ void __launch_bounds__(256) k_acc_faces(NuView v, DevClock* clk, DevRed* red,
+__global__ void __launch_bounds__(FM_ACC_FACE_THREADS) k_acc_faces(NuView v, DevClock* clk, DevRed* red,
                                                   const Hydro* hy, const double* __restrict__ ch,
                                                   const double* __restrict__ czc,
                                                   double* __restrict__ q, int manual, double mdt) {
@@ -903,7 +910,7 @@ void nu_step_op(Sim& s, int op, bool manual, double mdt, int* err) {
       if (s.shard) shard_finish(s);
       if (!manual) launch_decide(s);
       kt_begin(KF_ACC_FACES);
-      (s.p2 ? k_acc_faces<true> : k_acc_faces<false>)<<<nblk(ns, 256 * FM_ACC_SPT), 256, 0, st>>>(
+      (s.p2 ? k_acc_faces<true> : k_acc_faces<false>)<<<nblk(ns, FM_ACC_FACE_THREADS * FM_ACC_SPT), FM_ACC_FACE_THREADS, 0, st>>>(
           v, clk, red, s.hydro.p, s.ch.p, s.czc.p, s.accq.p, manual, mdt);
       FM_LAUNCHED();
       kt_end();
