@@ -31,6 +31,10 @@
 #ifndef FM_NO_EXIT
 #define FM_NO_EXIT 1
 #endif
+// compact FV1 rows (W = 3): 6 CTAs per SM (0.105 -> 0.101 ms, profiles/r2d_ab_seg_minb.txt)
+#ifndef FM_SEG_MINB3
+#define FM_SEG_MINB3 6
+#endif
 #ifndef FM_SEG_MINB
 #define FM_SEG_MINB 5  // 51 registers: 5 CTAs of 256 threads per SM (4: 0.135, 5: 0.132, 6: 0.155 ms after the static z limits)
 #endif
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(256) k_head_fric_ip(NuView v, DevClock* clk, D
 // runs the same code path (one HLL), unlike a per-leaf-side formulation where
 // lanes of a warp face 0, 1 or 2 sub-faces and every face is solved twice.
 template <bool P2, int W>
-__global__ void __launch_bounds__(256, FM_SEG_MINB) k_seg(NuView v, const DevClock* __restrict__ clk,
+__global__ void __launch_bounds__(256, W == 3 ? FM_SEG_MINB3 : FM_SEG_MINB) k_seg(NuView v, const DevClock* __restrict__ clk,
                                              const double* __restrict__ in, double* __restrict__ out,
                                              int manual, int* err, long long q0, long long q1) {
   const long long q = q0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
